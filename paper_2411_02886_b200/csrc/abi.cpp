@@ -1,0 +1,1145 @@
+// C-ABI host layer (include/tokenselect.h): the paged KV pool with the
+// reference's LIFO frame allocator, the AttentionEngine, and the standalone
+// selection / attention entry points, all launching the sm_100a kernels in
+// decode.cu and aux.cu. Validation happens before any device work and
+// reports the reference's exception type + message (see tokenselect.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/tokenselect.h"
+#include "aux.h"
+#include "decode.h"
+#include "params.h"
+
+using tsb::CacheState;
+using tsb::DecodeParams;
+using tsb::SeqDesc;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+struct ts_error : std::runtime_error {
+  ts_status code;
+  ts_error(ts_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(ts_status c, const std::string& m) { throw ts_error(c, m); }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(TS_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename Fn>
+ts_status guarded(Fn&& fn) {
+  try {
+    fn();
+    return TS_OK;
+  } catch (const ts_error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "allocation failed";
+    return TS_CUDA_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return TS_INVALID_ARGUMENT;
+  }
+}
+
+struct DeviceInfo {
+  int device = -1;
+  int num_sms = 0;
+  int smem_optin = 0;
+};
+
+const DeviceInfo& device_info() {
+  static DeviceInfo info = [] {
+    DeviceInfo d;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      return d;
+    }
+    cudaGetDevice(&d.device);
+    cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, d.device);
+    cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, d.device);
+    return d;
+  }();
+  if (info.device < 0) fail(TS_CUDA_ERROR, "no CUDA device: the tokenselect library has no CPU path");
+  return info;
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Growable device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void* ensure(size_t bytes) {
+    if (bytes <= n) return p;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    ck(cudaMalloc(&p, std::max<size_t>(bytes, 256)), "cudaMalloc");
+    n = std::max<size_t>(bytes, 256);
+    return p;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// Host input -> device (staged); device input passes through.
+template <typename T>
+const T* dev_in(const T* p, size_t count, DevBuf& stage, cudaStream_t st) {
+  if (!p || count == 0) return p;
+  if (is_device_ptr(p)) return p;
+  T* d = static_cast<T*>(stage.ensure(count * sizeof(T)));
+  ck(cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, st), "H2D");
+  return d;
+}
+
+// Per-launch workspaces of the fused kernel + its grid barrier.
+struct Workspace {
+  DevBuf s, keys, m, z, hist, cnt, att, bar;
+  bool bar_init = false;
+  void prepare(int n_ctas, int H, int d, int tpc, int s_in_smem, int n_seq, cudaStream_t st) {
+    if (!s_in_smem) {
+      s.ensure(static_cast<size_t>(n_ctas) * H * tpc * 4);
+      keys.ensure(static_cast<size_t>(n_ctas) * tpc * 4);
+    }
+    m.ensure(static_cast<size_t>(n_ctas) * H * 4);
+    z.ensure(static_cast<size_t>(n_ctas) * H * 4);
+    hist.ensure(static_cast<size_t>(n_seq) * 3 * 2048 * 4);
+    cnt.ensure(static_cast<size_t>(n_ctas) * 2 * 4);
+    att.ensure(static_cast<size_t>(n_ctas) * H * (d + 2) * 4);
+    if (!bar_init) {
+      bar.ensure(64);
+      ck(cudaMemsetAsync(bar.p, 0, 64, st), "memset barrier");
+      bar_init = true;
+    }
+  }
+};
+
+struct Plan {
+  int ctas_per_seq, tpc, s_in_smem;
+  size_t smem;
+  const void* fn;
+  int att_rows;
+};
+
+Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows) {
+  const DeviceInfo& di = device_info();
+  Plan pl{};
+  const tsb::ScanGeom g = tsb::scan_geom(H, H_kv, d);
+  pl.fn = tsb::decode_kernel_ptr(d, H / H_kv, g.fast != 0);
+  if (!pl.fn) pl.fn = tsb::decode_kernel_ptr(0, 0, false);
+  const int base = std::max(max_T, att_rows);
+  int c = (base + 63) / 64;
+  c = std::max(1, std::min(c, std::max(1, di.num_sms / n_seq)));
+  pl.ctas_per_seq = c;
+  pl.tpc = std::max(1, (max_T + c - 1) / c);
+  const int row_bytes = H_kv * d * 2;
+  tsb::SmemLayout L = tsb::smem_layout(H, row_bytes, pl.tpc, 1);
+  if (L.total <= static_cast<size_t>(di.smem_optin)) {
+    pl.s_in_smem = 1;
+  } else {
+    pl.s_in_smem = 0;
+    L = tsb::smem_layout(H, row_bytes, pl.tpc, 0);
+    if (L.total > static_cast<size_t>(di.smem_optin)) fail(TS_INVALID_ARGUMENT, "row too wide for the decode kernel");
+  }
+  pl.smem = L.total;
+  const size_t ring = tsb::smem_layout(H, row_bytes, 1, 0).s - tsb::smem_layout(H, row_bytes, 1, 0).ring;
+  pl.att_rows = static_cast<int>(ring / (2 * static_cast<size_t>(row_bytes)));
+  if (H > 16 * 4) fail(TS_INVALID_ARGUMENT, "num_heads > 64 is not supported by the decode kernel");
+  if (d > 256) fail(TS_INVALID_ARGUMENT, "head_dim > 256 is not supported by the decode kernel");
+  return pl;
+}
+
+void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t st) {
+  const int n_ctas = p.n_seq * pl.ctas_per_seq;
+  ws.prepare(n_ctas, p.H, p.d, pl.tpc, pl.s_in_smem, p.n_seq, st);
+  p.ctas_per_seq = pl.ctas_per_seq;
+  p.tpc = pl.tpc;
+  p.s_in_smem = pl.s_in_smem;
+  p.ws_s = ws.s.as<float>();
+  p.ws_keys = ws.keys.as<uint32_t>();
+  p.ws_m = ws.m.as<float>();
+  p.ws_z = ws.z.as<float>();
+  p.ws_hist = ws.hist.as<uint32_t>();
+  p.ws_cnt = ws.cnt.as<uint32_t>();
+  p.ws_att = ws.att.as<float>();
+  p.bar = ws.bar.as<unsigned int>();
+  p.att_rows_per_cta = pl.att_rows;
+  ck(cudaFuncSetAttribute(pl.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)),
+     "cudaFuncSetAttribute");
+  void* args[] = {&p};
+  ck(cudaLaunchCooperativeKernel(pl.fn, dim3(n_ctas), dim3(tsb::kDecodeThreads), args, pl.smem, st),
+     "decode kernel launch");
+  g_launches.fetch_add(1);
+}
+
+// selattn::Rng::index semantics (rng.hpp:19-26) on std::mt19937_64, so the
+// shuffled free list is the reference's permutation.
+struct RefRng {
+  std::mt19937_64 e;
+  explicit RefRng(uint64_t seed) : e(seed) {}
+  double uniform() { return static_cast<double>(e() >> 11) * 0x1.0p-53; }
+  size_t index(size_t n) { return static_cast<size_t>(uniform() * static_cast<double>(n)) % n; }
+};
+
+}  // namespace
+
+// =================================================================== pool
+struct ts_pool {
+  size_t page_size = 1, H_kv = 0, d = 0, row = 0, total_frames = 0;
+  uint16_t* k_slab = nullptr;
+  uint16_t* v_slab = nullptr;
+  std::vector<uint32_t> free_list;
+  struct Seq {
+    std::vector<uint32_t> frames;
+    size_t len = 0;
+    int32_t* d_pt = nullptr;
+  };
+  std::unordered_map<uint32_t, Seq> seqs;
+  uint32_t next_id = 0;
+  cudaStream_t stream = nullptr;
+  Workspace ws;
+  DevBuf st_a, st_b, st_c, st_d, st_e, st_f;  // staging
+
+  ~ts_pool() {
+    for (auto& kv : seqs)
+      if (kv.second.d_pt) cudaFree(kv.second.d_pt);
+    if (k_slab) cudaFree(k_slab);
+    if (v_slab) cudaFree(v_slab);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  Seq& state(uint32_t id) {
+    auto it = seqs.find(id);
+    if (it == seqs.end()) fail(TS_INVALID_ARGUMENT, "PagedKvPool: unknown or released sequence " + std::to_string(id));
+    return it->second;
+  }
+  const Seq& state(uint32_t id) const { return const_cast<ts_pool*>(this)->state(id); }
+
+  int64_t slab_row(const Seq& s, size_t pos) const {
+    return static_cast<int64_t>(s.frames[pos / page_size]) * static_cast<int64_t>(page_size) +
+           static_cast<int64_t>(pos % page_size);
+  }
+
+  // Allocates frames for t more tokens (kv_pool.cpp:63-76) and uploads the
+  // new page-table entries; returns the slab rows of the new positions.
+  std::vector<int64_t> reserve(Seq& s, size_t t, cudaStream_t st) {
+    const size_t frames_now = (s.len + page_size - 1) / page_size;
+    const size_t frames_after = (s.len + t + page_size - 1) / page_size;
+    const size_t need = frames_after - frames_now;
+    if (need > free_list.size())
+      fail(TS_CAPACITY, "append_kv: pool exhausted (need " + std::to_string(need) + " frames, " +
+                            std::to_string(free_list.size()) + " free)");
+    std::vector<int32_t> fresh;
+    fresh.reserve(need);
+    for (size_t i = 0; i < need; ++i) {
+      s.frames.push_back(free_list.back());
+      fresh.push_back(static_cast<int32_t>(free_list.back()));
+      free_list.pop_back();
+    }
+    if (need) {
+      ck(cudaMemcpyAsync(s.d_pt + frames_now, fresh.data(), need * sizeof(int32_t), cudaMemcpyHostToDevice, st),
+         "page table upload");
+      ck(cudaStreamSynchronize(st), "sync");  // `fresh` is pageable and goes out of scope
+    }
+    std::vector<int64_t> rows(t);
+    for (size_t r = 0; r < t; ++r) rows[r] = slab_row(s, s.len + r);
+    return rows;
+  }
+
+  void append(uint32_t id, const void* k, const void* v, size_t t, bool bf16, size_t* first,
+              size_t* last, cudaStream_t st) {
+    Seq& s = state(id);
+    const size_t f = s.len;
+    if (first) *first = f;
+    if (last) *last = f + t;
+    if (t == 0) return;
+    std::vector<int64_t> rows = reserve(s, t, st);
+    int64_t* d_rows = static_cast<int64_t*>(st_a.ensure(t * sizeof(int64_t)));
+    ck(cudaMemcpyAsync(d_rows, rows.data(), t * sizeof(int64_t), cudaMemcpyHostToDevice, st), "H2D rows");
+    const size_t n = t * row;
+    if (bf16) {
+      const uint16_t* kd = dev_in(static_cast<const uint16_t*>(k), n, st_b, st);
+      const uint16_t* vd = dev_in(static_cast<const uint16_t*>(v), n, st_c, st);
+      ck(tsb::launch_kv_append(k_slab, v_slab, nullptr, nullptr, kd, vd, d_rows, static_cast<int>(t),
+                               static_cast<int>(row), st),
+         "kv_append");
+    } else {
+      const float* kd = dev_in(static_cast<const float*>(k), n, st_b, st);
+      const float* vd = dev_in(static_cast<const float*>(v), n, st_c, st);
+      ck(tsb::launch_kv_append(k_slab, v_slab, kd, vd, nullptr, nullptr, d_rows, static_cast<int>(t),
+                               static_cast<int>(row), st),
+         "kv_append");
+    }
+    g_launches.fetch_add(1);
+    ck(cudaStreamSynchronize(st), "append sync");
+    s.len += t;
+  }
+};
+
+// ================================================================= engine
+struct ts_engine {
+  ts_engine_config cfg{};
+  std::unique_ptr<ts_pool> pool;
+  std::vector<uint32_t> seq_ids;
+  size_t B = 1;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  // per-sequence Selection Cache entries (device)
+  DevBuf cache_state, cached_q, sel, sel_crit;
+  // step IO staging (device) + pinned host mirrors
+  DevBuf d_q, d_k, d_v, d_out;
+  float* h_q = nullptr;
+  float* h_k = nullptr;
+  float* h_v = nullptr;
+  float* h_out = nullptr;
+  CacheState* h_cache = nullptr;
+  Workspace ws;
+  // prefill scratch
+  DevBuf p_qmean, p_sel, p_crit, p_state, p_att, p_natt, p_bad, p_q, p_k, p_v, p_out;
+
+  ~ts_engine() {
+    if (h_q) cudaFreeHost(h_q);
+    if (h_k) cudaFreeHost(h_k);
+    if (h_v) cudaFreeHost(h_v);
+    if (h_out) cudaFreeHost(h_out);
+    if (h_cache) cudaFreeHost(h_cache);
+    if (own_stream) cudaStreamDestroy(own_stream);
+  }
+  size_t W() const { return cfg.num_heads * cfg.head_dim; }
+  size_t KW() const { return cfg.num_kv_heads * cfg.head_dim; }
+  CacheState* cache(size_t b) const { return cache_state.as<CacheState>() + b; }
+  float* cq(size_t b) const { return cached_q.as<float>() + b * W(); }
+  uint32_t* sl(size_t b) const { return sel.as<uint32_t>() + b * std::max<size_t>(cfg.k, 1); }
+  float* sc(size_t b) const { return sel_crit.as<float>() + b * std::max<size_t>(cfg.k, 1); }
+};
+
+namespace {
+
+void validate_cfg(const ts_engine_config& c) {
+  if (c.num_heads == 0 || c.num_kv_heads == 0 || c.head_dim == 0)
+    fail(TS_INVALID_ARGUMENT, "EngineConfig: head counts and head_dim must be >= 1");
+  if (c.num_heads % c.num_kv_heads != 0)
+    fail(TS_INVALID_ARGUMENT, "EngineConfig: num_heads must be a multiple of num_kv_heads");
+  if (c.chunk_size == 0) fail(TS_INVALID_ARGUMENT, "EngineConfig: chunk_size must be >= 1");
+  if (c.block_size == 0) fail(TS_INVALID_ARGUMENT, "EngineConfig: block_size must be >= 1");
+  if (c.selection_method < 0 || c.selection_method > 2) fail(TS_INVALID_ARGUMENT, "select_with: bad method");
+}
+
+void check_method_supported(int m) {
+  if (m == TS_HEAD_VOTE)
+    fail(TS_INVALID_ARGUMENT, "head_vote selection is not implemented on the device path yet");
+}
+
+DecodeParams base_params(const ts_pool* pool, int H, int H_kv, int d, int k, int method, int mode) {
+  DecodeParams p{};
+  p.k_slab = pool ? pool->k_slab : nullptr;
+  p.v_slab = pool ? pool->v_slab : nullptr;
+  p.k_slab_w = pool ? pool->k_slab : nullptr;
+  p.v_slab_w = pool ? pool->v_slab : nullptr;
+  p.page_size = pool ? static_cast<int>(pool->page_size) : 1;
+  p.H = H;
+  p.H_kv = H_kv;
+  p.d = d;
+  p.k = k;
+  p.method = method;
+  p.mode = mode;
+  p.attn_scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
+  return p;
+}
+
+struct GlobalCtx {
+  cudaStream_t stream = nullptr;
+  Workspace ws;
+  DevBuf a, b, c, d, e, f;
+  GlobalCtx() { ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream"); }
+};
+GlobalCtx& gctx() {
+  static GlobalCtx* g = new GlobalCtx();
+  return *g;
+}
+
+// Standalone selection through the fused kernel (score and/or select modes).
+// q: device [H*d] (score mode) ; s_in: device [H*T] (select-from-S mode).
+size_t run_select(const ts_pool* pool, const ts_pool::Seq* seq, int H, int H_kv, int d,
+                  const float* q, const float* s_in, const uint32_t* cand_dev, size_t T, size_t k,
+                  int method, float* s_out_dev, uint32_t* sel_host, double* crit_host, Workspace& ws,
+                  DevBuf& b_sel, DevBuf& b_crit, DevBuf& b_state, cudaStream_t st, bool do_select) {
+  const int mode = (s_in ? tsb::kModeSIn : tsb::kModeScore) | (do_select ? tsb::kModeSelect : 0) |
+                   (s_out_dev ? tsb::kModeSOut : 0);
+  DecodeParams p = base_params(pool, H, H_kv, d, static_cast<int>(k), method, mode);
+  p.n_seq = 1;
+  SeqDesc& sd = p.seqs[0];
+  sd.page_table = seq ? seq->d_pt : nullptr;
+  sd.n_cached = seq ? static_cast<int32_t>(seq->len) : 0;
+  sd.cand_begin = 0;
+  sd.n_cand = static_cast<int32_t>(T);
+  sd.cand = cand_dev;
+  sd.select = 1;
+  sd.q = q;
+  sd.s_in = s_in;
+  sd.s_out = s_out_dev;
+  sd.append_frame = -1;
+  sd.append_page = -1;
+  const size_t kk = std::max<size_t>(std::min(k, T), 1);
+  sd.sel = static_cast<uint32_t*>(b_sel.ensure(kk * 4));
+  sd.sel_crit = static_cast<float*>(b_crit.ensure(kk * 4));
+  sd.cache = static_cast<CacheState*>(b_state.ensure(sizeof(CacheState)));
+  ck(cudaMemsetAsync(sd.cache, 0, sizeof(CacheState), st), "memset");
+  const Plan pl = make_plan(H, H_kv, d, 1, static_cast<int>(T), 1);
+  launch_decode(p, pl, ws, st);
+  if (!do_select) {
+    ck(cudaStreamSynchronize(st), "sync");
+    return 0;
+  }
+  CacheState cs{};
+  ck(cudaMemcpyAsync(&cs, sd.cache, sizeof(CacheState), cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaStreamSynchronize(st), "sync");
+  const size_t n = static_cast<size_t>(cs.n_sel);
+  std::vector<float> crit(n);
+  if (n) {
+    ck(cudaMemcpyAsync(sel_host, sd.sel, n * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaMemcpyAsync(crit.data(), sd.sel_crit, n * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+  }
+  for (size_t i = 0; i < n; ++i) crit_host[i] = static_cast<double>(crit[i]);
+  return n;
+}
+
+// Copy a (host or device) index list to host.
+std::vector<uint32_t> host_copy_u32(const uint32_t* p, size_t n) {
+  std::vector<uint32_t> v(n);
+  if (n == 0) return v;
+  if (is_device_ptr(p)) ck(cudaMemcpy(v.data(), p, n * 4, cudaMemcpyDeviceToHost), "D2H");
+  else std::memcpy(v.data(), p, n * 4);
+  return v;
+}
+
+void copy_out(void* dst, const void* src_dev, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return;
+  ck(cudaMemcpyAsync(dst, src_dev, bytes, is_device_ptr(dst) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st),
+     "copy out");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ts_last_error(void) { return g_err.c_str(); }
+const char* ts_version(void) { return "tokenselect-b200 0.1.0 (sm_100a)"; }
+uint64_t ts_launch_count(void) { return g_launches.load(); }
+
+void ts_engine_config_default(ts_engine_config* c) {
+  c->k = 2048;
+  c->n_local = 512;
+  c->n_init = 128;
+  c->chunk_size = 512;
+  c->theta = 0.9;
+  c->num_heads = 8;
+  c->num_kv_heads = 8;
+  c->head_dim = 64;
+  c->block_size = 64;
+  c->selection_method = TS_HEAD_SOFT_VOTE;
+}
+
+ts_status ts_engine_config_validate(const ts_engine_config* cfg) {
+  return guarded([&] { validate_cfg(*cfg); });
+}
+
+// ------------------------------------------------------------------- pool
+ts_status ts_pool_create(size_t capacity_tokens, size_t page_size, size_t num_kv_heads,
+                         size_t head_dim, ts_pool** out) {
+  return guarded([&] {
+    *out = nullptr;
+    if (page_size == 0) fail(TS_INVALID_ARGUMENT, "PagedKvPool: page_size must be >= 1");
+    if (num_kv_heads * head_dim == 0) fail(TS_INVALID_ARGUMENT, "PagedKvPool: zero row width");
+    device_info();
+    auto p = std::make_unique<ts_pool>();
+    p->page_size = page_size;
+    p->H_kv = num_kv_heads;
+    p->d = head_dim;
+    p->row = num_kv_heads * head_dim;
+    p->total_frames = (capacity_tokens + page_size - 1) / page_size;
+    const size_t elems = std::max<size_t>(p->total_frames * page_size * p->row, 8);
+    ck(cudaMalloc(&p->k_slab, elems * 2), "cudaMalloc K slab");
+    ck(cudaMalloc(&p->v_slab, elems * 2), "cudaMalloc V slab");
+    ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "stream");
+    ck(cudaMemsetAsync(p->k_slab, 0, elems * 2, p->stream), "memset");
+    ck(cudaMemsetAsync(p->v_slab, 0, elems * 2, p->stream), "memset");
+    p->free_list.resize(p->total_frames);
+    // highest frame handed out first (kv_pool.cpp:24-27)
+    for (size_t i = 0; i < p->total_frames; ++i) p->free_list[i] = static_cast<uint32_t>(i);
+    ck(cudaStreamSynchronize(p->stream), "sync");
+    *out = p.release();
+  });
+}
+
+void ts_pool_destroy(ts_pool* pool) { delete pool; }
+
+ts_status ts_pool_create_sequence(ts_pool* pool, uint32_t* seq_id) {
+  return guarded([&] {
+    ts_pool::Seq s;
+    ck(cudaMalloc(&s.d_pt, std::max<size_t>(pool->total_frames, 1) * sizeof(int32_t)), "cudaMalloc page table");
+    const uint32_t id = pool->next_id++;
+    pool->seqs.emplace(id, std::move(s));
+    *seq_id = id;
+  });
+}
+
+ts_status ts_pool_append_kv(ts_pool* pool, uint32_t seq, const float* k, const float* v, size_t t,
+                            size_t* first, size_t* last) {
+  return guarded([&] { pool->append(seq, k, v, t, false, first, last, pool->stream); });
+}
+
+ts_status ts_pool_append_kv_bf16(ts_pool* pool, uint32_t seq, const uint16_t* k, const uint16_t* v,
+                                 size_t t, size_t* first, size_t* last) {
+  return guarded([&] { pool->append(seq, k, v, t, true, first, last, pool->stream); });
+}
+
+ts_status ts_pool_gather(const ts_pool* cpool, uint32_t seq, const uint32_t* idx, size_t n,
+                         float* k_out, float* v_out) {
+  return guarded([&] {
+    ts_pool* pool = const_cast<ts_pool*>(cpool);
+    const ts_pool::Seq& s = pool->state(seq);
+    std::vector<uint32_t> ih = host_copy_u32(idx, n);
+    std::vector<int64_t> rows(n);
+    for (size_t j = 0; j < n; ++j) {
+      if (ih[j] >= s.len)
+        fail(TS_OUT_OF_RANGE, "gather: index " + std::to_string(ih[j]) + " out of range (logical_len " +
+                                  std::to_string(s.len) + ")");
+      rows[j] = pool->slab_row(s, ih[j]);
+    }
+    if (n == 0) return;
+    cudaStream_t st = pool->stream;
+    int64_t* d_rows = static_cast<int64_t*>(pool->st_a.ensure(n * 8));
+    ck(cudaMemcpyAsync(d_rows, rows.data(), n * 8, cudaMemcpyHostToDevice, st), "H2D");
+    const size_t bytes = n * pool->row * 4;
+    float* kd = k_out ? (is_device_ptr(k_out) ? k_out : static_cast<float*>(pool->st_b.ensure(bytes))) : nullptr;
+    float* vd = v_out ? (is_device_ptr(v_out) ? v_out : static_cast<float*>(pool->st_c.ensure(bytes))) : nullptr;
+    ck(tsb::launch_kv_gather(pool->k_slab, pool->v_slab, d_rows, static_cast<int>(n), static_cast<int>(pool->row), kd, vd, st),
+       "gather");
+    g_launches.fetch_add(1);
+    if (k_out && kd != k_out) copy_out(k_out, kd, bytes, st);
+    if (v_out && vd != v_out) copy_out(v_out, vd, bytes, st);
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+ts_status ts_pool_release(ts_pool* pool, uint32_t seq) {
+  return guarded([&] {
+    auto it = pool->seqs.find(seq);
+    if (it == pool->seqs.end())
+      fail(TS_INVALID_ARGUMENT, "release: unknown or already released sequence " + std::to_string(seq));
+    for (uint32_t f : it->second.frames) pool->free_list.push_back(f);
+    if (it->second.d_pt) cudaFree(it->second.d_pt);
+    pool->seqs.erase(it);
+  });
+}
+
+ts_status ts_pool_logical_len(const ts_pool* pool, uint32_t seq, size_t* len) {
+  return guarded([&] { *len = pool->state(seq).len; });
+}
+
+ts_status ts_pool_shuffle_free_frames(ts_pool* pool, uint64_t seed) {
+  return guarded([&] {
+    RefRng rng(seed);
+    for (size_t i = pool->free_list.size(); i > 1; --i) std::swap(pool->free_list[i - 1], pool->free_list[rng.index(i)]);
+  });
+}
+
+ts_status ts_pool_page_table_json(const ts_pool* pool, uint32_t seq, char* buf, size_t cap, size_t* needed) {
+  return guarded([&] {
+    const ts_pool::Seq& s = pool->state(seq);
+    std::string j = "{\"frames\":[";
+    for (size_t i = 0; i < s.frames.size(); ++i) {
+      if (i) j += ",";
+      j += std::to_string(s.frames[i]);
+    }
+    j += "],\"logical_len\":" + std::to_string(s.len) + ",\"seq_id\":" + std::to_string(seq) + "}";
+    if (needed) *needed = j.size() + 1;
+    if (buf && cap) {
+      const size_t n = std::min(cap - 1, j.size());
+      std::memcpy(buf, j.data(), n);
+      buf[n] = 0;
+    }
+  });
+}
+
+size_t ts_pool_total_frames(const ts_pool* p) { return p->total_frames; }
+size_t ts_pool_free_frames(const ts_pool* p) { return p->free_list.size(); }
+size_t ts_pool_page_size(const ts_pool* p) { return p->page_size; }
+size_t ts_pool_num_kv_heads(const ts_pool* p) { return p->H_kv; }
+size_t ts_pool_head_dim(const ts_pool* p) { return p->d; }
+
+ts_status ts_pool_device_views(const ts_pool* pool, uint32_t seq, const void** k_slab, const void** v_slab,
+                               const int32_t** page_table) {
+  return guarded([&] {
+    const ts_pool::Seq& s = pool->state(seq);
+    if (k_slab) *k_slab = pool->k_slab;
+    if (v_slab) *v_slab = pool->v_slab;
+    if (page_table) *page_table = s.d_pt;
+  });
+}
+
+// ----------------------------------------------------------------- select
+ts_status ts_score_paged(const ts_pool* cpool, uint32_t seq, const float* q, size_t num_heads, size_t head_dim,
+                         const uint32_t* candidates, size_t T, size_t block_size, float* s_out) {
+  return guarded([&] {
+    ts_pool* pool = const_cast<ts_pool*>(cpool);
+    if (head_dim != pool->d)
+      fail(TS_INVALID_ARGUMENT, "score_paged: query head_dim " + std::to_string(head_dim) +
+                                    " does not match pool head_dim " + std::to_string(pool->d));
+    if (num_heads == 0 || num_heads % pool->H_kv != 0)
+      fail(TS_INVALID_ARGUMENT, "score_paged: H must be a positive multiple of H_kv");
+    if (block_size == 0) fail(TS_INVALID_ARGUMENT, "score_paged: block_size must be >= 1");
+    const ts_pool::Seq& s = pool->state(seq);
+    std::vector<uint32_t> ch = host_copy_u32(candidates, T);
+    for (size_t j = 0; j < T; ++j)
+      if (ch[j] >= s.len)
+        fail(TS_OUT_OF_RANGE, "key_row: index " + std::to_string(ch[j]) + " out of range (logical_len " +
+                                  std::to_string(s.len) + ")");
+    if (T == 0) return;
+    cudaStream_t st = pool->stream;
+    const float* qd = dev_in(q, num_heads * head_dim, pool->st_a, st);
+    const uint32_t* cd = dev_in(candidates, T, pool->st_b, st);
+    const size_t bytes = num_heads * T * 4;
+    float* sd = is_device_ptr(s_out) ? s_out : static_cast<float*>(pool->st_c.ensure(bytes));
+    DevBuf b1, b2, b3;
+    run_select(pool, &s, static_cast<int>(num_heads), static_cast<int>(pool->H_kv), static_cast<int>(head_dim), qd,
+               nullptr, cd, T, 0, TS_HEAD_SOFT_VOTE, sd, nullptr, nullptr, pool->ws, b1, b2, b3, st, false);
+    if (sd != s_out) {
+      copy_out(s_out, sd, bytes, st);
+      ck(cudaStreamSynchronize(st), "sync");
+    }
+  });
+}
+
+ts_status ts_select(const float* per_head, size_t num_heads, size_t T, const uint32_t* candidate_idx, size_t k,
+                    int method, uint32_t* sel_out, double* crit_out, size_t* n_out) {
+  return guarded([&] {
+    *n_out = 0;
+    if (method < 0 || method > 2) fail(TS_INVALID_ARGUMENT, "select_with: bad method");
+    if (T == 0) return;  // pick(): empty criticality -> empty result
+    if (k == 0) fail(TS_INVALID_ARGUMENT, "topk_indices: k must be >= 1");
+    check_method_supported(method);
+    GlobalCtx& g = gctx();
+    cudaStream_t st = g.stream;
+    const float* sd = dev_in(per_head, num_heads * T, g.a, st);
+    const uint32_t* cd = candidate_idx ? dev_in(candidate_idx, T, g.b, st) : nullptr;
+    *n_out = run_select(nullptr, nullptr, static_cast<int>(num_heads), 1, 1, nullptr, sd, cd, T, k, method, nullptr,
+                        sel_out, crit_out, g.ws, g.c, g.d, g.e, st, true);
+  });
+}
+
+ts_status ts_select_for_chunk(const ts_pool* cpool, uint32_t seq, const float* q_chunk, size_t c, size_t width,
+                              const uint32_t* candidates, size_t T, size_t k, int method, size_t block_size,
+                              uint32_t* sel_out, double* crit_out, size_t* n_out) {
+  return guarded([&] {
+    *n_out = 0;
+    ts_pool* pool = const_cast<ts_pool*>(cpool);
+    if (width == 0 || width % pool->d != 0) fail(TS_INVALID_ARGUMENT, "select_for_chunk: chunk width must be H * d_h");
+    if (c == 0) fail(TS_INVALID_ARGUMENT, "chunk_mean: empty chunk");
+    const size_t H = width / pool->d;
+    if (H % pool->H_kv != 0) fail(TS_INVALID_ARGUMENT, "score_paged: H must be a positive multiple of H_kv");
+    if (block_size == 0) fail(TS_INVALID_ARGUMENT, "score_paged: block_size must be >= 1");
+    if (method < 0 || method > 2) fail(TS_INVALID_ARGUMENT, "select_with: bad method");
+    const ts_pool::Seq& s = pool->state(seq);
+    std::vector<uint32_t> ch = host_copy_u32(candidates, T);
+    for (size_t j = 0; j < T; ++j)
+      if (ch[j] >= s.len)
+        fail(TS_OUT_OF_RANGE, "key_row: index " + std::to_string(ch[j]) + " out of range (logical_len " +
+                                  std::to_string(s.len) + ")");
+    if (T == 0) return;
+    if (k == 0) fail(TS_INVALID_ARGUMENT, "topk_indices: k must be >= 1");
+    check_method_supported(method);
+    cudaStream_t st = pool->stream;
+    const float* qd = dev_in(q_chunk, c * width, pool->st_a, st);
+    float* qm = static_cast<float*>(pool->st_d.ensure(width * 4));
+    ck(tsb::launch_chunk_mean(qd, static_cast<int>(c), static_cast<int>(width), qm, st), "chunk_mean");
+    g_launches.fetch_add(1);
+    const uint32_t* cd = dev_in(candidates, T, pool->st_b, st);
+    DevBuf b1, b2, b3;
+    *n_out = run_select(pool, &s, static_cast<int>(H), static_cast<int>(pool->H_kv), static_cast<int>(pool->d), qm,
+                        nullptr, cd, T, k, method, nullptr, sel_out, crit_out, pool->ws, b1, b2, b3, st, true);
+  });
+}
+
+// -------------------------------------------------------------- attention
+ts_status ts_sparse_attend(const ts_pool* cpool, uint32_t seq, const float* q, const float* k_cur,
+                           const float* v_cur, size_t C, size_t num_heads, const uint32_t* forced_init,
+                           size_t n_init, const uint32_t* selected, size_t n_sel, const uint32_t* forced_local,
+                           size_t n_local, float* out) {
+  return guarded([&] {
+    ts_pool* pool = const_cast<ts_pool*>(cpool);
+    const ts_pool::Seq& s = pool->state(seq);
+    // merged() = merge_dedup (tensor.cpp:159-168)
+    std::vector<uint32_t> merged;
+    for (auto [p, n] : {std::pair{forced_init, n_init}, std::pair{selected, n_sel}, std::pair{forced_local, n_local}}) {
+      std::vector<uint32_t> h = host_copy_u32(p, n);
+      merged.insert(merged.end(), h.begin(), h.end());
+    }
+    std::sort(merged.begin(), merged.end());
+    merged.erase(std::unique(merged.begin(), merged.end()), merged.end());
+    for (uint32_t t : merged)
+      if (t >= s.len)
+        fail(TS_OUT_OF_RANGE, "gather: index " + std::to_string(t) + " out of range (logical_len " +
+                                  std::to_string(s.len) + ")");
+    // sdpa_full shape contract (attention.cpp:56-69) with head_dim = q width / H
+    if (num_heads == 0) fail(TS_INVALID_ARGUMENT, "sdpa_full: q must be [C x (H * d_h)]");
+    const size_t width = num_heads * pool->d;  // callers pass q as [C x H*d_pool]
+    const size_t d = pool->d;
+    const size_t H_kv = pool->H_kv;
+    if (num_heads % H_kv != 0) fail(TS_INVALID_ARGUMENT, "sdpa_full: H must be a multiple of H_kv");
+    if (C == 0) return;
+    cudaStream_t st = pool->stream;
+    const float* qd = dev_in(q, C * width, pool->st_a, st);
+    const float* kd = dev_in(k_cur, C * pool->row, pool->st_b, st);
+    const float* vd = dev_in(v_cur, C * pool->row, pool->st_c, st);
+    const uint32_t* ad = merged.empty() ? nullptr : dev_in(merged.data(), merged.size(), pool->st_e, st);
+    const size_t obytes = C * width * 4;
+    float* od = is_device_ptr(out) ? out : static_cast<float*>(pool->st_f.ensure(obytes));
+    if (C == 1) {
+      DecodeParams p = base_params(pool, static_cast<int>(num_heads), static_cast<int>(H_kv), static_cast<int>(d), 0,
+                                   TS_HEAD_SOFT_VOTE, tsb::kModeAttend);
+      p.n_seq = 1;
+      SeqDesc& sdsc = p.seqs[0];
+      sdsc.page_table = s.d_pt;
+      sdsc.n_cached = static_cast<int32_t>(s.len);
+      sdsc.select = 0;
+      sdsc.q = qd;
+      sdsc.k_new = kd;
+      sdsc.v_new = vd;
+      sdsc.out = od;
+      sdsc.append_frame = -1;
+      sdsc.append_page = -1;
+      sdsc.att_list = ad ? ad : reinterpret_cast<const uint32_t*>(qd);  // non-null => explicit list
+      sdsc.n_att = static_cast<int32_t>(merged.size());
+      const Plan pl = make_plan(static_cast<int>(num_heads), static_cast<int>(H_kv), static_cast<int>(d), 1, 0,
+                                static_cast<int>(merged.size() + 1));
+      launch_decode(p, pl, pool->ws, st);
+    } else {
+      tsb::PrefillAttendParams pa{};
+      pa.q = qd;
+      pa.k_cur = kd;
+      pa.v_cur = vd;
+      pa.k_slab = pool->k_slab;
+      pa.v_slab = pool->v_slab;
+      pa.page_table = s.d_pt;
+      pa.page_size = static_cast<int>(pool->page_size);
+      pa.att = ad;
+      pa.n_att = static_cast<int>(merged.size());
+      pa.n_att_ptr = nullptr;
+      pa.C = static_cast<int>(C);
+      pa.H = static_cast<int>(num_heads);
+      pa.H_kv = static_cast<int>(H_kv);
+      pa.d = static_cast<int>(d);
+      pa.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
+      pa.out = od;
+      ck(tsb::launch_prefill_attend(pa, st), "prefill_attend");
+      g_launches.fetch_add(1);
+    }
+    if (od != out) copy_out(out, od, obytes, st);
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+// ------------------------------------------------------------------ engine
+ts_status ts_engine_create(const ts_engine_config* cfg, size_t capacity_tokens, size_t n_seqs, ts_engine** out) {
+  return guarded([&] {
+    *out = nullptr;
+    validate_cfg(*cfg);
+    check_method_supported(cfg->selection_method);
+    if (n_seqs == 0) fail(TS_INVALID_ARGUMENT, "AttentionEngine: n_seqs must be >= 1");
+    device_info();
+    auto e = std::make_unique<ts_engine>();
+    e->cfg = *cfg;
+    e->B = n_seqs;
+    ts_pool* p = nullptr;
+    // one shared pool, page_size 1 (attention.cpp:219), capacity per sequence
+    ts_status rc = ts_pool_create(capacity_tokens * n_seqs, 1, cfg->num_kv_heads, cfg->head_dim, &p);
+    if (rc != TS_OK) fail(rc, g_err);
+    e->pool.reset(p);
+    for (size_t b = 0; b < n_seqs; ++b) {
+      uint32_t id;
+      rc = ts_pool_create_sequence(p, &id);
+      if (rc != TS_OK) fail(rc, g_err);
+      e->seq_ids.push_back(id);
+    }
+    ck(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking), "stream");
+    e->stream = e->own_stream;
+    const size_t W = e->W(), KW = e->KW(), kk = std::max<size_t>(cfg->k, 1);
+    e->cache_state.ensure(n_seqs * sizeof(CacheState));
+    e->cached_q.ensure(n_seqs * W * 4);
+    e->sel.ensure(n_seqs * kk * 4);
+    e->sel_crit.ensure(n_seqs * kk * 4);
+    e->d_q.ensure(n_seqs * W * 4);
+    e->d_k.ensure(n_seqs * KW * 4);
+    e->d_v.ensure(n_seqs * KW * 4);
+    e->d_out.ensure(n_seqs * W * 4);
+    ck(cudaMallocHost(&e->h_q, n_seqs * W * 4), "pinned");
+    ck(cudaMallocHost(&e->h_k, n_seqs * KW * 4), "pinned");
+    ck(cudaMallocHost(&e->h_v, n_seqs * KW * 4), "pinned");
+    ck(cudaMallocHost(&e->h_out, n_seqs * W * 4), "pinned");
+    ck(cudaMallocHost(&e->h_cache, n_seqs * sizeof(CacheState)), "pinned");
+    std::vector<CacheState> init(n_seqs);
+    for (auto& c : init) {
+      c = CacheState{};
+      c.theta = cfg->theta;  // attention.cpp:222
+      c.last_cos = NAN;
+      c.first_flag = 1;
+      c.last_hit = -1;
+    }
+    ck(cudaMemcpy(e->cache_state.p, init.data(), n_seqs * sizeof(CacheState), cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemset(e->cached_q.p, 0, n_seqs * W * 4), "memset");
+    *out = e.release();
+  });
+}
+
+void ts_engine_destroy(ts_engine* eng) { delete eng; }
+
+ts_status ts_engine_set_stream(ts_engine* eng, void* stream) {
+  return guarded([&] { eng->stream = stream ? static_cast<cudaStream_t>(stream) : eng->own_stream; });
+}
+
+ts_pool* ts_engine_pool(ts_engine* eng) { return eng->pool.get(); }
+uint32_t ts_engine_sequence(const ts_engine* eng, size_t seq) { return eng->seq_ids.at(seq); }
+
+ts_status ts_engine_append(ts_engine* eng, size_t seq, const float* k, const float* v, size_t t) {
+  return guarded([&] {
+    if (seq >= eng->B) fail(TS_INVALID_ARGUMENT, "engine: sequence index out of range");
+    eng->pool->append(eng->seq_ids[seq], k, v, t, false, nullptr, nullptr, eng->stream);
+  });
+}
+
+ts_status ts_engine_append_bf16(ts_engine* eng, size_t seq, const uint16_t* k, const uint16_t* v, size_t t) {
+  return guarded([&] {
+    if (seq >= eng->B) fail(TS_INVALID_ARGUMENT, "engine: sequence index out of range");
+    eng->pool->append(eng->seq_ids[seq], k, v, t, true, nullptr, nullptr, eng->stream);
+  });
+}
+
+namespace {
+
+// One decode step for all sequences (decode_step, attention.cpp:172-200).
+// Inputs are device pointers (already staged). Returns per-sequence append
+// failure flags (capacity), applied after the step as the reference does.
+std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const float* v, float* out) {
+  ts_pool& pool = *e->pool;
+  const ts_engine_config& c = e->cfg;
+  const size_t W = e->W(), KW = e->KW();
+  std::vector<int> cap_fail(e->B, 0);
+  cudaStream_t st = e->stream;
+  for (size_t g0 = 0; g0 < e->B; g0 += tsb::kMaxSeqPerLaunch) {
+    const size_t gn = std::min<size_t>(tsb::kMaxSeqPerLaunch, e->B - g0);
+    DecodeParams p = base_params(&pool, static_cast<int>(c.num_heads), static_cast<int>(c.num_kv_heads),
+                                 static_cast<int>(c.head_dim), static_cast<int>(c.k), c.selection_method,
+                                 tsb::kModeCache | tsb::kModeScore | tsb::kModeSelect | tsb::kModeAttend |
+                                     tsb::kModeAppend);
+    p.n_seq = static_cast<int>(gn);
+    int max_T = 0, max_rows = 0;
+    for (size_t i = 0; i < gn; ++i) {
+      const size_t b = g0 + i;
+      ts_pool::Seq& s = pool.state(e->seq_ids[b]);
+      const size_t N = s.len;
+      SeqDesc& sd = p.seqs[i];
+      sd.page_table = s.d_pt;
+      sd.n_cached = static_cast<int32_t>(N);
+      const bool sel_on = c.k > 0 && N > c.n_init + c.n_local;
+      sd.select = sel_on ? 1 : 0;
+      sd.cand_begin = static_cast<int32_t>(c.n_init);
+      sd.n_cand = sel_on ? static_cast<int32_t>(N - c.n_init - c.n_local) : 0;
+      sd.cand = nullptr;
+      sd.q = q + b * W;
+      sd.k_new = k + b * KW;
+      sd.v_new = v + b * KW;
+      sd.out = out + b * W;
+      sd.init_end = static_cast<int32_t>(std::min(c.n_init, N));
+      sd.local_begin = static_cast<int32_t>(N - std::min(c.n_local, N));
+      sd.att_list = nullptr;
+      sd.cache = e->cache(b);
+      sd.cached_q = e->cq(b);
+      sd.sel = e->sl(b);
+      sd.sel_crit = e->sc(b);
+      // frame for logical position N (page_size 1): LIFO pop, after-the-step failure
+      if (pool.free_list.empty()) {
+        cap_fail[b] = 1;
+        sd.append_frame = -1;
+        sd.append_page = -1;
+      } else {
+        const uint32_t f = pool.free_list.back();
+        pool.free_list.pop_back();
+        s.frames.push_back(f);
+        sd.append_frame = static_cast<int32_t>(f);
+        sd.append_slot = 0;
+        sd.append_page = static_cast<int32_t>(N);
+      }
+      max_T = std::max(max_T, sd.n_cand);
+      max_rows = std::max(max_rows, static_cast<int>(std::min(c.n_init, N) + std::min(c.k, N) + c.n_local + 1));
+    }
+    const Plan pl = make_plan(static_cast<int>(c.num_heads), static_cast<int>(c.num_kv_heads),
+                              static_cast<int>(c.head_dim), static_cast<int>(gn), max_T, max_rows);
+    launch_decode(p, pl, e->ws, st);
+    for (size_t i = 0; i < gn; ++i)
+      if (!cap_fail[g0 + i]) pool.state(e->seq_ids[g0 + i]).len += 1;
+  }
+  return cap_fail;
+}
+
+}  // namespace
+
+ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const float* v, float* out, int* cache_hit,
+                           uint32_t* sel_out, size_t* n_sel) {
+  return guarded([&] {
+    const size_t W = e->W(), KW = e->KW(), B = e->B;
+    cudaStream_t st = e->stream;
+    const bool q_dev = is_device_ptr(q);
+    // zero-query check before any mutation (selection_cache.cpp:18-27)
+    if (!q_dev) {
+      ts_pool& pool = *e->pool;
+      for (size_t b = 0; b < B; ++b) {
+        const size_t N = pool.state(e->seq_ids[b]).len;
+        if (!(e->cfg.k > 0 && N > e->cfg.n_init + e->cfg.n_local)) continue;
+        bool nz = false;
+        for (size_t i = 0; i < W && !nz; ++i) nz = q[b * W + i] != 0.0f;
+        if (!nz) fail(TS_INVALID_ARGUMENT, "lookup_or_select: zero query vector");
+      }
+    }
+    auto stage = [&](const float* src, float* pinned, DevBuf& dbuf, size_t n) -> const float* {
+      if (is_device_ptr(src)) return src;
+      std::memcpy(pinned, src, n * 4);
+      ck(cudaMemcpyAsync(dbuf.p, pinned, n * 4, cudaMemcpyHostToDevice, st), "H2D");
+      return dbuf.as<float>();
+    };
+    const float* qd = stage(q, e->h_q, e->d_q, B * W);
+    const float* kd = stage(k, e->h_k, e->d_k, B * KW);
+    const float* vd = stage(v, e->h_v, e->d_v, B * KW);
+    const bool out_dev = is_device_ptr(out);
+    float* od = out_dev ? out : e->d_out.as<float>();
+    std::vector<int> cap_fail = engine_step(e, qd, kd, vd, od);
+    if (!out_dev) ck(cudaMemcpyAsync(e->h_out, od, B * W * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaMemcpyAsync(e->h_cache, e->cache_state.p, B * sizeof(CacheState), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "decode sync");
+    if (!out_dev) std::memcpy(out, e->h_out, B * W * 4);
+    ts_pool& pool = *e->pool;
+    for (size_t b = 0; b < B; ++b) {
+      const CacheState& cs = e->h_cache[b];
+      if (cs.error) fail(TS_INVALID_ARGUMENT, "lookup_or_select: zero query vector");
+      // the step ran a lookup iff selection was on for the sequence at step start
+      const size_t N_after = pool.state(e->seq_ids[b]).len;
+      const size_t N = N_after - (cap_fail[b] ? 0 : 1);
+      const bool sel_on = e->cfg.k > 0 && N > e->cfg.n_init + e->cfg.n_local;
+      if (cache_hit) cache_hit[b] = sel_on ? cs.last_hit : 0;
+      if (sel_out) {
+        const size_t n = sel_on ? static_cast<size_t>(cs.n_sel) : 0;
+        const size_t kk = std::max<size_t>(e->cfg.k, 1);
+        if (n) ck(cudaMemcpy(sel_out + b * kk, e->sl(b), n * 4, cudaMemcpyDeviceToHost), "D2H sel");
+        if (n_sel) n_sel[b] = n;
+      }
+    }
+    for (size_t b = 0; b < B; ++b)
+      if (cap_fail[b]) fail(TS_CAPACITY, "append_kv: pool exhausted (need 1 frames, 0 free)");
+  });
+}
+
+ts_status ts_engine_decode_async(ts_engine* e, const float* q, const float* k, const float* v, float* out) {
+  return guarded([&] {
+    std::vector<int> cap_fail = engine_step(e, q, k, v, out);
+    for (size_t b = 0; b < e->B; ++b)
+      if (cap_fail[b]) fail(TS_CAPACITY, "append_kv: pool exhausted (need 1 frames, 0 free)");
+  });
+}
+
+ts_status ts_engine_force_miss(ts_engine* e, size_t seq) {
+  return guarded([&] {
+    if (seq >= e->B) fail(TS_INVALID_ARGUMENT, "engine: sequence index out of range");
+    const int one = 1;
+    ck(cudaMemcpyAsync(&e->cache(seq)->first_flag, &one, sizeof(int), cudaMemcpyHostToDevice, e->stream), "H2D");
+    ck(cudaStreamSynchronize(e->stream), "sync");
+  });
+}
+
+ts_status ts_engine_stats(const ts_engine* e, size_t seq, size_t* lookups, size_t* hits, size_t* len, int* last_hit,
+                          double* last_cos) {
+  return guarded([&] {
+    if (seq >= e->B) fail(TS_INVALID_ARGUMENT, "engine: sequence index out of range");
+    CacheState cs{};
+    ck(cudaMemcpyAsync(&cs, e->cache(seq), sizeof(CacheState), cudaMemcpyDeviceToHost, e->stream), "D2H");
+    ck(cudaStreamSynchronize(e->stream), "sync");
+    if (lookups) *lookups = cs.lookups;
+    if (hits) *hits = cs.hits;
+    if (len) *len = e->pool->state(e->seq_ids[seq]).len;
+    if (last_hit) *last_hit = cs.last_hit;
+    if (last_cos) *last_cos = cs.last_cos;
+    if (cs.error) {
+      const int zero = 0;
+      ck(cudaMemcpy(&e->cache(seq)->error, &zero, sizeof(int), cudaMemcpyHostToDevice), "H2D");
+      fail(TS_INVALID_ARGUMENT, "lookup_or_select: zero query vector");
+    }
+  });
+}
+
+ts_status ts_engine_cached_selection(const ts_engine* e, size_t seq, uint32_t* sel_out, double* crit_out,
+                                     size_t* n_out) {
+  return guarded([&] {
+    if (seq >= e->B) fail(TS_INVALID_ARGUMENT, "engine: sequence index out of range");
+    CacheState cs{};
+    ck(cudaMemcpyAsync(&cs, e->cache(seq), sizeof(CacheState), cudaMemcpyDeviceToHost, e->stream), "D2H");
+    ck(cudaStreamSynchronize(e->stream), "sync");
+    const size_t n = static_cast<size_t>(cs.n_sel);
+    *n_out = n;
+    if (!n) return;
+    std::vector<float> crit(n);
+    ck(cudaMemcpy(sel_out, e->sl(seq), n * 4, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(crit.data(), e->sc(seq), n * 4, cudaMemcpyDeviceToHost), "D2H");
+    if (crit_out)
+      for (size_t i = 0; i < n; ++i) crit_out[i] = crit[i];
+  });
+}
+
+ts_status ts_engine_sync(ts_engine* e) {
+  return guarded([&] { ck(cudaStreamSynchronize(e->stream), "sync"); });
+}
+
+ts_status ts_engine_prefill(ts_engine* e, size_t seq, const float* q, const float* k, const float* v, size_t n,
+                            float* out, uint32_t* trace_sel, size_t* trace_counts, size_t max_chunks) {
+  return guarded([&] {
+    if (seq >= e->B) fail(TS_INVALID_ARGUMENT, "engine: sequence index out of range");
+    if (n == 0) fail(TS_INVALID_ARGUMENT, "prefill: empty input");
+    const ts_engine_config& c = e->cfg;
+    ts_pool& pool = *e->pool;
+    const uint32_t sid = e->seq_ids[seq];
+    const size_t W = e->W(), KW = e->KW();
+    const int H = static_cast<int>(c.num_heads), Hkv = static_cast<int>(c.num_kv_heads), d = static_cast<int>(c.head_dim);
+    cudaStream_t st = e->stream;
+    const bool q_dev = is_device_ptr(q), k_dev = is_device_ptr(k), v_dev = is_device_ptr(v), o_dev = is_device_ptr(out);
+    const size_t kk = std::max<size_t>(c.k, 1);
+    size_t trace_off = 0;
+    for (size_t begin = 0, chunk = 0; begin < n; begin += c.chunk_size, ++chunk) {
+      const size_t len = std::min(c.chunk_size, n - begin);
+      const float* qc = q_dev ? q + begin * W : nullptr;
+      const float* kc = k_dev ? k + begin * KW : nullptr;
+      const float* vc = v_dev ? v + begin * KW : nullptr;
+      if (!q_dev) {
+        qc = static_cast<float*>(e->p_q.ensure(len * W * 4));
+        ck(cudaMemcpyAsync(const_cast<float*>(qc), q + begin * W, len * W * 4, cudaMemcpyHostToDevice, st), "H2D");
+      }
+      if (!k_dev) {
+        kc = static_cast<float*>(e->p_k.ensure(len * KW * 4));
+        ck(cudaMemcpyAsync(const_cast<float*>(kc), k + begin * KW, len * KW * 4, cudaMemcpyHostToDevice, st), "H2D");
+      }
+      if (!v_dev) {
+        vc = static_cast<float*>(e->p_v.ensure(len * KW * 4));
+        ck(cudaMemcpyAsync(const_cast<float*>(vc), v + begin * KW, len * KW * 4, cudaMemcpyHostToDevice, st), "H2D");
+      }
+      ts_pool::Seq& s = pool.state(sid);
+      const size_t cached = s.len;
+      uint32_t* psel = static_cast<uint32_t*>(e->p_sel.ensure(kk * 4));
+      CacheState* pstate = static_cast<CacheState*>(e->p_state.ensure(sizeof(CacheState)));
+      ck(cudaMemsetAsync(pstate, 0, sizeof(CacheState), st), "memset");
+      size_t T = 0;
+      if (c.k > 0 && cached > c.n_init + c.n_local) T = cached - c.n_init - c.n_local;
+      if (T > 0) {
+        // select_for_chunk: chunk mean (K9), then the fused score + soft vote + top-k
+        float* qm = static_cast<float*>(e->p_qmean.ensure(W * 4));
+        ck(tsb::launch_chunk_mean(qc, static_cast<int>(len), static_cast<int>(W), qm, st), "chunk_mean");
+        g_launches.fetch_add(1);
+        DecodeParams p = base_params(&pool, H, Hkv, d, static_cast<int>(c.k), c.selection_method,
+                                     tsb::kModeScore | tsb::kModeSelect);
+        p.n_seq = 1;
+        SeqDesc& sd = p.seqs[0];
+        sd.page_table = s.d_pt;
+        sd.n_cached = static_cast<int32_t>(cached);
+        sd.cand_begin = static_cast<int32_t>(c.n_init);
+        sd.n_cand = static_cast<int32_t>(T);
+        sd.select = 1;
+        sd.q = qm;
+        sd.append_frame = -1;
+        sd.append_page = -1;
+        sd.cache = pstate;
+        sd.sel = psel;
+        sd.sel_crit = static_cast<float*>(e->p_crit.ensure(kk * 4));
+        const Plan pl = make_plan(H, Hkv, d, 1, static_cast<int>(T), 1);
+        launch_decode(p, pl, e->ws, st);
+      }
+      // windows (make_windows) -> device merged list
+      const int init_end = static_cast<int>(std::min(c.n_init, cached));
+      const int local_begin = static_cast<int>(cached - std::min(c.n_local, cached));
+      uint32_t* att = static_cast<uint32_t*>(e->p_att.ensure((cached + kk + 1) * 4));
+      int* natt = static_cast<int*>(e->p_natt.ensure(16));
+      unsigned int* bad = static_cast<unsigned int*>(e->p_bad.ensure(16));
+      ck(cudaMemsetAsync(bad, 0, 4, st), "memset");
+      ck(tsb::launch_windows(psel, T > 0 ? &pstate->n_sel : nullptr, 0, static_cast<int>(cached), init_end,
+                             local_begin, att, natt, bad, st),
+         "windows");
+      g_launches.fetch_add(1);
+      float* oc = o_dev ? out + begin * W : static_cast<float*>(e->p_out.ensure(len * W * 4));
+      tsb::PrefillAttendParams pa{};
+      pa.q = qc;
+      pa.k_cur = kc;
+      pa.v_cur = vc;
+      pa.k_slab = pool.k_slab;
+      pa.v_slab = pool.v_slab;
+      pa.page_table = s.d_pt;
+      pa.page_size = static_cast<int>(pool.page_size);
+      pa.att = att;
+      pa.n_att_ptr = natt;
+      pa.C = static_cast<int>(len);
+      pa.H = H;
+      pa.H_kv = Hkv;
+      pa.d = d;
+      pa.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
+      pa.out = oc;
+      ck(tsb::launch_prefill_attend(pa, st), "prefill_attend");
+      g_launches.fetch_add(1);
+      if (!o_dev) ck(cudaMemcpyAsync(out + begin * W, oc, len * W * 4, cudaMemcpyDeviceToHost, st), "D2H");
+      if (trace_counts && chunk < max_chunks) {
+        CacheState cs{};
+        ck(cudaMemcpyAsync(&cs, pstate, sizeof(CacheState), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+        const size_t ns = T > 0 ? static_cast<size_t>(cs.n_sel) : 0;
+        trace_counts[chunk] = ns;
+        if (ns && trace_sel) ck(cudaMemcpy(trace_sel + trace_off, psel, ns * 4, cudaMemcpyDeviceToHost), "D2H");
+        trace_off += ns;
+      }
+      // append the chunk after attending (attention.cpp:167)
+      pool.append(sid, kc, vc, len, false, nullptr, nullptr, st);
+    }
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+}  // extern "C"

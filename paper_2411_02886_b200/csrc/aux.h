@@ -1,0 +1,37 @@
+// Launchers for the auxiliary kernels (aux.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tsb {
+
+struct PrefillAttendParams {
+  const float* q;          // [C][H*d]
+  const float* k_cur;      // [C][H_kv*d]
+  const float* v_cur;
+  const uint16_t* k_slab;  // bf16 bits
+  const uint16_t* v_slab;
+  const int32_t* page_table;
+  int page_size;
+  const uint32_t* att;     // attended cached rows (merged windows)
+  int n_att;
+  const int* n_att_ptr;    // device count (overrides n_att when set)
+  int C, H, H_kv, d;
+  float scale;
+  float* out;              // [C][H*d]
+};
+
+cudaError_t launch_kv_append(uint16_t* k_slab, uint16_t* v_slab, const float* k, const float* v,
+                             const uint16_t* kb, const uint16_t* vb, const int64_t* dst_rows, int t,
+                             int row, cudaStream_t st);
+cudaError_t launch_kv_gather(const uint16_t* k_slab, const uint16_t* v_slab, const int64_t* src_rows,
+                             int n, int row, float* k_out, float* v_out, cudaStream_t st);
+cudaError_t launch_chunk_mean(const float* q, int c, int width, float* out, cudaStream_t st);
+cudaError_t launch_max_index(const uint32_t* idx, int n, unsigned int* out, cudaStream_t st);
+cudaError_t launch_windows(const uint32_t* sel, const int* n_sel_ptr, int n_sel_fixed, int cached,
+                           int init_end, int local_begin, uint32_t* out, int* n_out,
+                           unsigned int* bad, cudaStream_t st);
+cudaError_t launch_prefill_attend(const PrefillAttendParams& p, cudaStream_t st);
+
+}  // namespace tsb

@@ -1,0 +1,861 @@
+// Fused persistent decode-step kernel (sm_100a).
+//
+// One cooperative launch runs the whole TokenSelect decode step of
+// decode_step (reference attention.cpp:172-200) for one or more sequences:
+//
+//   phase 0  K1 append of the current token's K/V row (kv_pool.cpp:55-85)
+//            K2 Selection Cache test, fp64 cosine vs. the cached query
+//               (selection_cache.cpp:16-44, tensor.cpp:92-113)
+//   phase 1  K3 paged dot-product scan S = q.K over the candidates
+//               (selector.cpp:26-68, Alg. 2): K rows streamed by the TMA engine
+//               (cp.async.bulk, evict_first) through an mbarrier ring, GQA
+//               group sharing each row, FFMA2 + shuffle reduce-scatter;
+//               per-CTA head max tracked on the fly, S kept on chip.
+//   phase 2  K4 soft vote (softmax_rows + select_head_soft_vote,
+//               tensor.cpp:31-52, selector.cpp:113-126): per-CTA (m, z),
+//               one grid exchange, crit[j] = sum_h exp(S-M_h)/Z_h
+//   phase 3  K5 radix select (11/11/10-bit digits) with the reference's tie
+//               rule (larger score first, smaller index on ties, output
+//               ascending; tensor.cpp:68-90, selector.cpp:72-85)
+//   phase 4  K7 split-K sparse flash-decoding over init U selected U local U
+//               current (make_windows attention.cpp:35-52, sdpa_full :54-112)
+//   phase 5  K8 log-sum-exp merge of the per-CTA partials.
+//
+// Sequences of a batch are given disjoint CTA groups; phases are separated
+// by grid barriers (all CTAs co-resident: cudaLaunchCooperativeKernel).
+#include <cfloat>
+#include <cmath>
+
+#include "common.cuh"
+#include "decode.h"
+#include "params.h"
+
+namespace tsb {
+
+namespace {
+
+constexpr int kBins = 2048;
+
+struct Smem {
+  uint8_t* ring;
+  float* S;        // [H][tpc] (when on chip)
+  uint32_t* keys;  // [tpc]
+  uint32_t* hist;  // [kBins]
+  int* headmax;    // [H] ordered-int max
+  float* f;        // [H]
+  uint32_t* scratch;  // [64]
+  uint64_t* full;  // [kMaxStages]
+  uint64_t* empty; // [kMaxStages]
+};
+
+__device__ __forceinline__ Smem carve(uint8_t* base, const DecodeParams& p) {
+  SmemLayout L = smem_layout(p.H, p.H_kv * p.d * 2, p.tpc, p.s_in_smem);
+  Smem s;
+  s.ring = base + L.ring;
+  s.S = reinterpret_cast<float*>(base + L.s);
+  s.keys = reinterpret_cast<uint32_t*>(base + L.keys);
+  s.hist = reinterpret_cast<uint32_t*>(base + L.hist);
+  s.headmax = reinterpret_cast<int*>(base + L.headmax);
+  s.f = reinterpret_cast<float*>(base + L.f);
+  s.scratch = reinterpret_cast<uint32_t*>(base + L.scratch);
+  s.full = reinterpret_cast<uint64_t*>(base + L.bars);
+  s.empty = s.full + kMaxStages;
+  return s;
+}
+
+__device__ __forceinline__ uint32_t cand_at(const SeqDesc& sd, int j) {
+  return sd.cand ? sd.cand[j] : static_cast<uint32_t>(sd.cand_begin + j);
+}
+
+__device__ __forceinline__ size_t row_index(const SeqDesc& sd, uint32_t tok, int page_size) {
+  if (page_size == 1) return static_cast<size_t>(sd.page_table[tok]);
+  return static_cast<size_t>(sd.page_table[tok / page_size]) * page_size + tok % page_size;
+}
+
+// Block-wide exclusive scan of one value per thread (all threads call).
+__device__ uint32_t block_excl_scan(uint32_t v, uint32_t* scratch, uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t inc = warp_incl_scan(v, lane);
+  __syncthreads();
+  if (lane == 31) scratch[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < kDecodeWarps ? scratch[lane] : 0u;
+    uint32_t wi = warp_incl_scan(w, lane);
+    if (lane < kDecodeWarps) scratch[32 + lane] = wi - w;
+    if (lane == 31) scratch[63] = wi;
+  }
+  __syncthreads();
+  const uint32_t r = scratch[32 + warp] + inc - v;
+  if (total) *total = scratch[63];
+  __syncthreads();
+  return r;
+}
+
+// Finds, in a histogram whose bins are ordered by key, the bin b such that
+// count(bins > b) < kk <= count(bins >= b). Returns b and count(bins > b).
+// All threads call; every CTA computes the same answer from the same data.
+__device__ void find_bin(const uint32_t* gh, int nbins, uint32_t kk, uint32_t* scratch,
+                         int* bin_out, uint32_t* above_out) {
+  // thread t covers bins [nbins - (t+1)*per, nbins - t*per) in descending order
+  const int per = (nbins + 511) / 512;
+  const int t = threadIdx.x;
+  uint32_t sum = 0;
+  if (t < 512) {
+    for (int i = 0; i < per; ++i) {
+      const int b = nbins - 1 - (t * per + i);
+      if (b >= 0) sum += __ldcg(gh + b);
+    }
+  }
+  uint32_t tot;
+  const uint32_t ex = block_excl_scan(t < 512 ? sum : 0u, scratch, &tot);
+  if (t < 512 && ex < kk && ex + sum >= kk) {
+    uint32_t acc = ex;
+    for (int i = 0; i < per; ++i) {
+      const int b = nbins - 1 - (t * per + i);
+      const uint32_t c = __ldcg(gh + b);
+      if (acc + c >= kk) {
+        scratch[64] = static_cast<uint32_t>(b);
+        scratch[65] = acc;
+        break;
+      }
+      acc += c;
+    }
+  }
+  __syncthreads();
+  *bin_out = static_cast<int>(scratch[64]);
+  *above_out = scratch[65];
+  __syncthreads();
+}
+
+// fp64 cosine Selection Cache decision (tensor.cpp:92-113,
+// selection_cache.cpp:29-35). Deterministic block reduction: every CTA that
+// evaluates it for the same sequence gets a bit-identical result.
+// Returns 1 = miss, 0 = hit, 2 = zero query (error).
+__device__ int cache_decision(const SeqDesc& sd, int width, double* scratch_d, double* cos_out) {
+  const CacheState* cs = sd.cache;
+  double dot = 0.0, nu = 0.0, nv = 0.0;
+  int nonzero = 0;
+  for (int i = threadIdx.x; i < width; i += blockDim.x) {
+    const double a = static_cast<double>(sd.q[i]);
+    const double b = static_cast<double>(sd.cached_q[i]);
+    nonzero |= (sd.q[i] != 0.0f);
+    dot = fma(a, b, dot);
+    nu = fma(a, a, nu);
+    nv = fma(b, b, nv);
+  }
+  nonzero = __syncthreads_or(nonzero);
+  dot = warp_sum_d(dot);
+  nu = warp_sum_d(nu);
+  nv = warp_sum_d(nv);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    scratch_d[warp * 3 + 0] = dot;
+    scratch_d[warp * 3 + 1] = nu;
+    scratch_d[warp * 3 + 2] = nv;
+  }
+  __syncthreads();
+  double D = 0.0, U = 0.0, V = 0.0;
+  for (int w = 0; w < kDecodeWarps; ++w) {
+    D += scratch_d[w * 3 + 0];
+    U += scratch_d[w * 3 + 1];
+    V += scratch_d[w * 3 + 2];
+  }
+  __syncthreads();
+  if (!nonzero) return 2;
+  *cos_out = NAN;
+  if (cs->first_flag) return 1;
+  if (U == 0.0 || V == 0.0) return 1;  // unreachable: cached query is never zero
+  double c;
+  if (D * D >= U * V) c = D >= 0.0 ? 1.0 : -1.0;  // exact +-1 clamp
+  else c = D / sqrt(U * V);
+  *cos_out = c;
+  return c < cs->theta ? 1 : 0;  // strict <
+}
+
+// --------------------------------------------------------------- the scan
+// Fast path: rows of H_kv*D bf16 are split in parts of 512 elements (one warp
+// each, WPR parts per row); a lane owns 16 contiguous elements of one kv head,
+// read as two 16-byte shared loads in a bank-conflict-free order. Each
+// consumer warp handles two rows per stage and reduce-scatters the 2*G
+// partial dot products over the LPH lanes of a kv head.
+template <int D, int G>
+__device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& sm, int j0,
+                          int nloc, float* Sbuf, int sstride, float* s_out_row0) {
+  constexpr int EPL = G > 4 ? 8 : 16;  // keeps the G*EPL fp32 query slice in registers
+  constexpr int LPH = D / EPL;        // lanes per kv head
+  constexpr int HPW = 32 / LPH;       // kv heads per warp
+  constexpr int NV0 = 2 * G;
+  constexpr int NVp = NV0 <= 2 ? 2 : NV0 <= 4 ? 4 : NV0 <= 8 ? 8 : 16;
+  constexpr int NV = NVp < LPH ? LPH : NVp;
+  constexpr int OWN = NV / LPH > 0 ? NV / LPH : 1;
+  static_assert(NV >= LPH, "reduce-scatter needs at least one value per lane");
+  const int row_bytes = p.H_kv * D * 2;
+  const ScanGeom geom = scan_geom(p.H, p.H_kv, D);
+  const int WPR = geom.wpr;
+  const int slots = kConsumerWarps / WPR;
+  const int R = geom.rows;  // rows per stage
+  const int kStages = geom.stages;
+  const int nit = (nloc + R - 1) / R;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- producer
+    const uint64_t pol = policy_evict_first();
+    const char* kbase = reinterpret_cast<const char*>(p.k_slab);
+    const char* src_next = nullptr;
+    if (lane < R && lane < nloc) {
+      const uint32_t tok = cand_at(sd, j0 + lane);
+      src_next = kbase + row_index(sd, tok, p.page_size) * row_bytes;
+    }
+    for (int it = 0; it < nit; ++it) {
+      const int s = it % kStages;
+      const int rbase = it * R;
+      const int nrows = min(R, nloc - rbase);
+      const char* src = src_next;
+      // prefetch the next stage's frame while this one is in flight
+      const int nr = rbase + R + lane;
+      if (lane < R && nr < nloc) {
+        const uint32_t tok = cand_at(sd, j0 + nr);
+        src_next = kbase + row_index(sd, tok, p.page_size) * row_bytes;
+      }
+      if (it >= kStages) mbar_wait(&sm.empty[s], ((it / kStages) & 1) ^ 1);
+      if (lane == 0) mbar_arrive_expect_tx(&sm.full[s], static_cast<uint32_t>(nrows * row_bytes));
+      __syncwarp();
+      if (lane < nrows)
+        bulk_g2s(sm.ring + static_cast<size_t>(s * R + lane) * row_bytes, src, row_bytes,
+                 &sm.full[s], pol);
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  const int cw = warp - 1;
+  if (cw >= slots * WPR) {
+    // idle consumer warp (slots*WPR < 16): still must arrive on empty
+    for (int it = 0; it < nit; ++it) {
+      const int s = it % kStages;
+      mbar_wait(&sm.full[s], (it / kStages) & 1);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s]);
+    }
+    return;
+  }
+  const int part = cw % WPR, slot = cw / WPR;
+  const int kvh = part * HPW + lane / LPH;
+  // EPL 16: two 16-byte halves read in a bank-conflict-free order
+  const int sw = EPL == 16 ? ((lane >> 2) & 1) : 0;
+  const int eA = (lane % LPH) * EPL + 8 * sw;
+  const int eB = (lane % LPH) * EPL + 8 * (1 - sw);
+  constexpr int NH = EPL / 8;  // 16-byte chunks per lane per row
+  float2 qv[G][NH][4];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const float* qh = sd.q + static_cast<size_t>(g * p.H_kv + kvh) * D;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      qv[g][0][i] = make_float2(qh[eA + 2 * i], qh[eA + 2 * i + 1]);
+      if constexpr (NH == 2) qv[g][NH - 1][i] = make_float2(qh[eB + 2 * i], qh[eB + 2 * i + 1]);
+    }
+  }
+  float runmax[OWN];
+#pragma unroll
+  for (int i = 0; i < OWN; ++i) runmax[i] = -INFINITY;
+  const uint32_t offA = static_cast<uint32_t>(part * 64 * EPL + lane * 2 * EPL + 16 * sw);
+  const uint32_t offB = static_cast<uint32_t>(part * 64 * EPL + lane * 2 * EPL + 16 * (1 - sw));
+
+  for (int it = 0; it < nit; ++it) {
+    const int s = it % kStages;
+    mbar_wait(&sm.full[s], (it / kStages) & 1);
+    const uint8_t* rows = sm.ring + static_cast<size_t>(s * R + 2 * slot) * row_bytes;
+    float v[NV];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      uint4 X[NH];
+      X[0] = *reinterpret_cast<const uint4*>(rows + r * row_bytes + offA);
+      if constexpr (NH == 2) X[NH - 1] = *reinterpret_cast<const uint4*>(rows + r * row_bytes + offB);
+      float2 kf[NH][4];
+#pragma unroll
+      for (int c = 0; c < NH; ++c) {
+        kf[c][0] = bf16x2_to_f2(X[c].x);
+        kf[c][1] = bf16x2_to_f2(X[c].y);
+        kf[c][2] = bf16x2_to_f2(X[c].z);
+        kf[c][3] = bf16x2_to_f2(X[c].w);
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < NH; ++c)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) ffma2(acc, kf[c][i], qv[g][c][i]);
+        v[r * G + g] = acc.x + acc.y;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[s]);  // ring slot consumed (data now in registers)
+#pragma unroll
+    for (int i = NV0; i < NV; ++i) v[i] = 0.f;
+    // reduce-scatter over the LPH lanes of this kv head
+    int n = NV;
+#pragma unroll
+    for (int o = LPH / 2; o >= 1; o >>= 1) {
+      const bool upper = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < n / 2; ++i) {
+        const float send = upper ? v[i] : v[i + n / 2];
+        const float keep = upper ? v[i + n / 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+      n >>= 1;
+    }
+    const int rbase = it * R + 2 * slot;
+#pragma unroll
+    for (int i = 0; i < OWN; ++i) {
+      const int vi = (lane % LPH) * OWN + i;
+      if (vi < NV0) {
+        const int r = vi / G, g = vi - (vi / G) * G;
+        const int row = rbase + r;
+        if (row < nloc) {
+          const int h = g * p.H_kv + kvh;
+          Sbuf[static_cast<size_t>(h) * sstride + row] = v[i];
+          if (s_out_row0) s_out_row0[static_cast<size_t>(h) * sd.n_cand + row] = v[i];
+          runmax[i] = fmaxf(runmax[i], v[i]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < OWN; ++i) {
+    const int vi = (lane % LPH) * OWN + i;
+    if (vi < NV0 && runmax[i] > -INFINITY) {
+      const int g = vi % G;
+      atomicMax(&sm.headmax[g * p.H_kv + kvh], float_ord(runmax[i]));
+    }
+  }
+}
+
+// Generic path (any H, H_kv, d, page_size): one thread per (head, token),
+// fp64 accumulation in the reference's d order, rounded to fp32 — this
+// reproduces score_paged's S bit for bit (bf16 x fp32 products are exact in
+// fp64, so the fused multiply-add equals the reference's multiply-then-add).
+__device__ void scan_generic(const DecodeParams& p, const SeqDesc& sd, const Smem& sm, int j0,
+                             int nloc, float* Sbuf, int sstride, float* s_out_row0) {
+  const int d = p.d, row = p.H_kv * d;
+  const int total = p.H * nloc;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    const int h = idx / nloc, jl = idx - (idx / nloc) * nloc;
+    const uint32_t tok = cand_at(sd, j0 + jl);
+    const uint16_t* key = p.k_slab + row_index(sd, tok, p.page_size) * row + (h % p.H_kv) * d;
+    const float* qh = sd.q + static_cast<size_t>(h) * d;
+    double acc = 0.0;
+    for (int t = 0; t < d; ++t) acc = fma(static_cast<double>(qh[t]), static_cast<double>(bf16_bits_to_f(key[t])), acc);
+    const float s = static_cast<float>(acc);
+    Sbuf[static_cast<size_t>(h) * sstride + jl] = s;
+    if (s_out_row0) s_out_row0[static_cast<size_t>(h) * sd.n_cand + jl] = s;
+    atomicMax(&sm.headmax[h], float_ord(s));
+  }
+}
+
+// ---------------------------------------------------------- attention rows
+struct AttView {
+  int n_rows;      // cached attended rows (excl. current)
+  int init_end, lo1, n1, lb2;
+};
+
+__device__ __forceinline__ int lower_bound_u32(const uint32_t* a, int n, uint32_t x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint32_t att_token(const SeqDesc& sd, const AttView& v, int i) {
+  if (sd.att_list) return sd.att_list[i];
+  if (i < v.init_end) return static_cast<uint32_t>(i);
+  i -= v.init_end;
+  if (i < v.n1) return sd.sel[v.lo1 + i];
+  i -= v.n1;
+  return static_cast<uint32_t>(v.lb2 + i);
+}
+
+// split-K flash-decoding partial over rows [r0, r1) of the merged window
+// list, plus the current token when `with_cur`; writes (o[d], m, l) per head.
+__device__ void attend_partial(const DecodeParams& p, const SeqDesc& sd, const AttView& av,
+                               const Smem& sm, int r0, int r1, bool with_cur, float* part) {
+  const int H = p.H, Hkv = p.H_kv, d = p.d;
+  const int row_elems = Hkv * d;
+  const int row_bytes = row_elems * 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kMaxDL = 8;  // d <= 256
+  const int dl = (d + 31) / 32;
+  // per (warp, head-slot) running state lives in registers
+  constexpr int kMaxHeadsPerWarp = 4;  // H <= 68
+  float m_run[kMaxHeadsPerWarp], l_run[kMaxHeadsPerWarp], o_run[kMaxHeadsPerWarp][kMaxDL];
+  float qreg[kMaxHeadsPerWarp][kMaxDL];
+#pragma unroll
+  for (int hs = 0; hs < kMaxHeadsPerWarp; ++hs) {
+    m_run[hs] = -INFINITY;
+    l_run[hs] = 0.f;
+    const int h = warp + hs * kDecodeWarps;
+#pragma unroll
+    for (int i = 0; i < kMaxDL; ++i) {
+      o_run[hs][i] = 0.f;
+      const int t = lane + 32 * i;
+      qreg[hs][i] = (h < H && i < dl && t < d) ? sd.q[static_cast<size_t>(h) * d + t] : 0.f;
+    }
+  }
+  const int cap = p.att_rows_per_cta;
+  uint16_t* kbuf = reinterpret_cast<uint16_t*>(sm.ring);
+  uint16_t* vbuf = kbuf + static_cast<size_t>(cap) * row_elems;
+  const bool vec = (row_bytes % 16) == 0;
+  for (int c0 = r0; c0 < r1; c0 += cap) {
+    const int nr = min(cap, r1 - c0);
+    __syncthreads();
+    if (vec) {
+      const int chunks = row_bytes / 16;
+      for (int idx = threadIdx.x; idx < nr * chunks * 2; idx += blockDim.x) {
+        const int which = idx / (nr * chunks);
+        const int rem = idx - which * nr * chunks;
+        const int r = rem / chunks, c = rem - (rem / chunks) * chunks;
+        const uint32_t tok = att_token(sd, av, c0 + r);
+        const uint16_t* src = (which ? p.v_slab : p.k_slab) + row_index(sd, tok, p.page_size) * row_elems;
+        uint16_t* dst = (which ? vbuf : kbuf) + static_cast<size_t>(r) * row_elems;
+        reinterpret_cast<uint4*>(dst)[c] = __ldg(reinterpret_cast<const uint4*>(src) + c);
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < nr * row_elems * 2; idx += blockDim.x) {
+        const int which = idx / (nr * row_elems);
+        const int rem = idx - which * nr * row_elems;
+        const int r = rem / row_elems, c = rem - (rem / row_elems) * row_elems;
+        const uint32_t tok = att_token(sd, av, c0 + r);
+        const uint16_t* src = (which ? p.v_slab : p.k_slab) + row_index(sd, tok, p.page_size) * row_elems;
+        ((which ? vbuf : kbuf) + static_cast<size_t>(r) * row_elems)[c] = src[c];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int hs = 0; hs < kMaxHeadsPerWarp; ++hs) {
+      const int h = warp + hs * kDecodeWarps;
+      if (h >= H) break;
+      const int kvo = (h % Hkv) * d;
+      for (int r = 0; r < nr; ++r) {
+        const uint16_t* kr = kbuf + static_cast<size_t>(r) * row_elems + kvo;
+        float part_dot = 0.f;
+#pragma unroll
+        for (int i = 0; i < kMaxDL; ++i) {
+          const int t = lane + 32 * i;
+          if (i < dl && t < d) part_dot = fmaf(qreg[hs][i], bf16_bits_to_f(kr[t]), part_dot);
+        }
+        const float s = warp_sum(part_dot) * p.attn_scale;
+        const float m_new = fmaxf(m_run[hs], s);
+        const float corr = expf(m_run[hs] - m_new);
+        const float w = expf(s - m_new);
+        l_run[hs] = l_run[hs] * corr + w;
+        const uint16_t* vr = vbuf + static_cast<size_t>(r) * row_elems + kvo;
+#pragma unroll
+        for (int i = 0; i < kMaxDL; ++i) {
+          const int t = lane + 32 * i;
+          if (i < dl && t < d) o_run[hs][i] = fmaf(w, bf16_bits_to_f(vr[t]), o_run[hs][i] * corr);
+        }
+        m_run[hs] = m_new;
+      }
+    }
+  }
+  if (with_cur) {
+#pragma unroll
+    for (int hs = 0; hs < kMaxHeadsPerWarp; ++hs) {
+      const int h = warp + hs * kDecodeWarps;
+      if (h >= H) break;
+      const int kvo = (h % Hkv) * d;
+      float part_dot = 0.f;
+#pragma unroll
+      for (int i = 0; i < kMaxDL; ++i) {
+        const int t = lane + 32 * i;
+        if (i < dl && t < d) part_dot = fmaf(qreg[hs][i], sd.k_new[kvo + t], part_dot);
+      }
+      const float s = warp_sum(part_dot) * p.attn_scale;
+      const float m_new = fmaxf(m_run[hs], s);
+      const float corr = expf(m_run[hs] - m_new);
+      const float w = expf(s - m_new);
+      l_run[hs] = l_run[hs] * corr + w;
+#pragma unroll
+      for (int i = 0; i < kMaxDL; ++i) {
+        const int t = lane + 32 * i;
+        if (i < dl && t < d) o_run[hs][i] = fmaf(w, sd.v_new[kvo + t], o_run[hs][i] * corr);
+      }
+      m_run[hs] = m_new;
+    }
+  }
+  const int stride = d + 2;
+#pragma unroll
+  for (int hs = 0; hs < kMaxHeadsPerWarp; ++hs) {
+    const int h = warp + hs * kDecodeWarps;
+    if (h >= H) break;
+    float* ph = part + static_cast<size_t>(h) * stride;
+#pragma unroll
+    for (int i = 0; i < kMaxDL; ++i) {
+      const int t = lane + 32 * i;
+      if (i < dl && t < d) ph[t] = o_run[hs][i];
+    }
+    if (lane == 0) {
+      ph[d] = m_run[hs];
+      ph[d + 1] = l_run[hs];
+    }
+  }
+}
+
+template <int D, int G, bool FAST>
+__global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const Smem sm = carve(smem_raw, p);
+  const int cta = blockIdx.x;
+  const int nblocks = gridDim.x;
+  const int seq_id = cta / p.ctas_per_seq;
+  const int cs = cta - seq_id * p.ctas_per_seq;
+  const SeqDesc sd = p.seqs[seq_id];
+  const int H = p.H;
+  const int width = H * p.d;
+  const int tid = threadIdx.x;
+  const bool do_select = (p.mode & kModeSelect) != 0;
+
+  if (FAST && tid < kMaxStages) {
+    mbar_init(&sm.full[tid], 1);
+    mbar_init(&sm.empty[tid], kConsumerWarps);
+  }
+  for (int h = tid; h < H; h += blockDim.x) sm.headmax[h] = float_ord(-INFINITY);
+  if (FAST) fence_mbar_init();
+  __syncthreads();
+
+  // ---- phase 0: append + cache decision + histogram reset
+  if ((p.mode & kModeAppend) && cs == 0 && sd.append_frame >= 0) {
+    const int row = p.H_kv * p.d;
+    const size_t off = (static_cast<size_t>(sd.append_frame) * p.page_size + sd.append_slot) * row;
+    for (int i = tid; i < row; i += blockDim.x) {
+      p.k_slab_w[off + i] = __bfloat16_as_ushort(__float2bfloat16_rn(sd.k_new[i]));
+      p.v_slab_w[off + i] = __bfloat16_as_ushort(__float2bfloat16_rn(sd.v_new[i]));
+    }
+    if (tid == 0 && sd.append_page >= 0) sd.page_table[sd.append_page] = sd.append_frame;
+  }
+  // every CTA evaluates every sequence's decision so that the grid agrees on
+  // whether any selection (and its barriers) runs this step
+  double* scratch_d = reinterpret_cast<double*>(sm.hist);  // hist is free until phase 2
+  int own = 0;        // 0 none, 1 miss (select), 2 hit
+  int any_select = 0, any_radix = 0;
+  double own_cos = NAN;
+  for (int b = 0; b < p.n_seq; ++b) {
+    const SeqDesc& s2 = (b == seq_id) ? sd : p.seqs[b];
+    int st = 0;
+    double c = NAN;
+    if (s2.select) {
+      if (p.mode & kModeCache) {
+        const int dec = cache_decision(s2, width, scratch_d, &c);
+        st = dec == 1 ? 1 : dec == 0 ? 2 : 3;
+      } else {
+        st = 1;
+      }
+    }
+    if (st == 1) {
+      any_select = 1;
+      if (do_select && s2.n_cand > p.k) any_radix = 1;
+    }
+    if (b == seq_id) {
+      own = st;
+      own_cos = c;
+    }
+  }
+  if (do_select && own == 1) {
+    uint32_t* gh = p.ws_hist + static_cast<size_t>(seq_id) * 3 * kBins;
+    for (int i = cs * blockDim.x + tid; i < 3 * kBins; i += p.ctas_per_seq * blockDim.x) gh[i] = 0u;
+  }
+  if (cs == 0 && tid == 0 && own == 3) sd.cache->error = 1;
+
+  // ---- phase 1: scan
+  const int T = sd.n_cand;
+  const int j0 = min(T, cs * p.tpc);
+  const int nloc = max(0, min(T, j0 + p.tpc) - j0);
+  float* Sbuf = p.s_in_smem ? sm.S : p.ws_s + static_cast<size_t>(cta) * H * p.tpc;
+  uint32_t* keys = p.s_in_smem ? sm.keys : p.ws_keys + static_cast<size_t>(cta) * p.tpc;
+  const int sstride = p.tpc;
+  const bool scanning = (own == 1) && ((p.mode & (kModeScore | kModeSIn)) != 0);
+  if (scanning) {
+    if (p.mode & kModeSIn) {
+      for (int idx = tid; idx < H * nloc; idx += blockDim.x) {
+        const int h = idx / nloc, jl = idx - (idx / nloc) * nloc;
+        const float s = sd.s_in[static_cast<size_t>(h) * T + j0 + jl];
+        Sbuf[static_cast<size_t>(h) * sstride + jl] = s;
+        atomicMax(&sm.headmax[h], float_ord(s));
+      }
+    } else {
+      float* so = (p.mode & kModeSOut) ? sd.s_out + j0 : nullptr;
+      if constexpr (FAST) scan_fast<D, G>(p, sd, sm, j0, nloc, Sbuf, sstride, so);
+      else scan_generic(p, sd, sm, j0, nloc, Sbuf, sstride, so);
+    }
+  }
+  __syncthreads();
+
+  if (do_select && own == 1 && p.method == 2) {
+    // per-CTA softmax partials: m = max_j S, z = sum_j exp(S - m); S <- exp(S - m)
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int h = warp; h < H; h += kDecodeWarps) {
+      const float m = ord_float(sm.headmax[h]);
+      float z = 0.f;
+      float* sr = Sbuf + static_cast<size_t>(h) * sstride;
+      if (m > -INFINITY) {
+        for (int jl = lane; jl < nloc; jl += 32) {
+          const float e = expf(sr[jl] - m);
+          sr[jl] = e;
+          z += e;
+        }
+      }
+      z = warp_sum(z);
+      if (lane == 0) {
+        p.ws_m[static_cast<size_t>(cta) * H + h] = m;
+        p.ws_z[static_cast<size_t>(cta) * H + h] = z;
+      }
+    }
+  }
+  if (any_select) grid_sync(reinterpret_cast<GridBarrier*>(p.bar), nblocks);  // #1
+
+  // ---- phase 2: crit + cache bookkeeping
+  if (own == 1 && cs == 0 && tid == 0 && (p.mode & kModeCache)) {
+    CacheState* c = sd.cache;
+    c->lookups += 1;
+    c->first_flag = 0;
+    c->last_hit = 0;
+    c->last_cos = own_cos;
+  }
+  if (own == 2 && cs == 0 && tid == 0) {
+    CacheState* c = sd.cache;
+    c->lookups += 1;
+    c->hits += 1;
+    c->last_hit = 1;
+    c->last_cos = own_cos;
+  }
+  if (own == 1 && (p.mode & kModeCache)) {
+    // the new cached query (every CTA finished reading the old one before #1)
+    for (int i = cs * blockDim.x + tid; i < width; i += p.ctas_per_seq * blockDim.x) sd.cached_q[i] = sd.q[i];
+  }
+  const int kk_total = p.k;
+  uint32_t tau = 0, kk = 0;
+  const bool radix_own = do_select && own == 1 && T > kk_total;
+  if (do_select && own == 1) {
+    if (p.method == 2) {
+      const int warp = tid >> 5, lane = tid & 31;
+      const int c0 = seq_id * p.ctas_per_seq;
+      for (int h = warp; h < H; h += kDecodeWarps) {
+        float M = -INFINITY;
+        for (int c = lane; c < p.ctas_per_seq; c += 32) M = fmaxf(M, __ldcg(p.ws_m + static_cast<size_t>(c0 + c) * H + h));
+        M = warp_max(M);
+        float Z = 0.f;
+        for (int c = lane; c < p.ctas_per_seq; c += 32) {
+          const float mc = __ldcg(p.ws_m + static_cast<size_t>(c0 + c) * H + h);
+          if (mc > -INFINITY) Z += __ldcg(p.ws_z + static_cast<size_t>(c0 + c) * H + h) * expf(mc - M);
+        }
+        Z = warp_sum(Z);
+        if (lane == 0) {
+          const float ms = ord_float(sm.headmax[h]);
+          sm.f[h] = (ms > -INFINITY) ? expf(ms - M) / Z : 0.f;
+        }
+      }
+      __syncthreads();
+      for (int jl = tid; jl < nloc; jl += blockDim.x) {
+        float c = 0.f;
+        for (int h = 0; h < H; ++h) c = fmaf(Sbuf[static_cast<size_t>(h) * sstride + jl], sm.f[h], c);
+        keys[jl] = float_key(c);
+      }
+    } else {
+      for (int jl = tid; jl < nloc; jl += blockDim.x) {
+        float c = 0.f;
+        for (int h = 0; h < H; ++h) c += Sbuf[static_cast<size_t>(h) * sstride + jl];
+        keys[jl] = float_key(c);
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- phase 3: radix select (3 passes, 11/11/10 bits)
+  if (any_radix) {
+    uint32_t prefix = 0;
+    uint32_t* gh = p.ws_hist + static_cast<size_t>(seq_id) * 3 * kBins;
+    kk = static_cast<uint32_t>(kk_total);
+    const int shifts[3] = {21, 10, 0};
+    const int widths[3] = {11, 11, 10};
+    for (int pass = 0; pass < 3; ++pass) {
+      const int sh = shifts[pass], wd = widths[pass];
+      const int nb = 1 << wd;
+      if (radix_own) {
+        for (int i = tid; i < nb; i += blockDim.x) sm.hist[i] = 0u;
+        __syncthreads();
+        const int hs = sh + wd;  // bits above this digit must match the prefix
+        for (int jl = tid; jl < nloc; jl += blockDim.x) {
+          const uint32_t key = keys[jl];
+          if (hs >= 32 || (key >> hs) == prefix) atomicAdd(&sm.hist[(key >> sh) & (nb - 1)], 1u);
+        }
+        __syncthreads();
+        for (int i = tid; i < nb; i += blockDim.x) {
+          const uint32_t c = sm.hist[i];
+          if (c) atomicAdd(gh + pass * kBins + i, c);
+        }
+      }
+      grid_sync(reinterpret_cast<GridBarrier*>(p.bar), nblocks);  // #2..#4
+      if (radix_own) {
+        int b;
+        uint32_t above;
+        find_bin(gh + pass * kBins, nb, kk, sm.scratch, &b, &above);
+        kk -= above;
+        prefix = (prefix << wd) | static_cast<uint32_t>(b);
+      }
+    }
+    tau = prefix;
+    // per-CTA (n_gt, n_eq)
+    if (radix_own) {
+      uint32_t ngt = 0, neq = 0;
+      for (int jl = tid; jl < nloc; jl += blockDim.x) {
+        const uint32_t key = keys[jl];
+        ngt += key > tau;
+        neq += key == tau;
+      }
+      uint32_t tg, te;
+      block_excl_scan(ngt, sm.scratch, &tg);
+      block_excl_scan(neq, sm.scratch, &te);
+      if (tid == 0) {
+        p.ws_cnt[static_cast<size_t>(cta) * 2 + 0] = tg;
+        p.ws_cnt[static_cast<size_t>(cta) * 2 + 1] = te;
+      }
+    }
+    grid_sync(reinterpret_cast<GridBarrier*>(p.bar), nblocks);  // #5
+  }
+
+  // ---- phase 3b: ascending compaction of the selection
+  if (do_select && own == 1) {
+    if (!radix_own) {
+      // T <= k: every candidate is selected (pick() with take = T)
+      for (int jl = tid; jl < nloc; jl += blockDim.x) {
+        sd.sel[j0 + jl] = cand_at(sd, j0 + jl);
+        sd.sel_crit[j0 + jl] = key_float(keys[jl]);
+      }
+      if (cs == 0 && tid == 0) sd.cache->n_sel = T;
+    } else {
+      uint32_t pgt = 0, peq = 0;
+      const int c0 = seq_id * p.ctas_per_seq;
+      if (tid < 32) {
+        for (int c = tid; c < cs; c += 32) {
+          pgt += __ldcg(p.ws_cnt + static_cast<size_t>(c0 + c) * 2 + 0);
+          peq += __ldcg(p.ws_cnt + static_cast<size_t>(c0 + c) * 2 + 1);
+        }
+        pgt = __reduce_add_sync(0xffffffffu, pgt);
+        peq = __reduce_add_sync(0xffffffffu, peq);
+        if (tid == 0) {
+          sm.scratch[66] = pgt;
+          sm.scratch[67] = peq;
+        }
+      }
+      __syncthreads();
+      pgt = sm.scratch[66];
+      peq = sm.scratch[67];
+      __syncthreads();
+      const uint32_t take_eq = kk > peq ? kk - peq : 0u;  // ties still available to this CTA
+      uint32_t out_base = pgt + min(peq, kk);
+      uint32_t eq_seen = 0;
+      for (int t0 = 0; t0 < nloc; t0 += blockDim.x) {
+        const int jl = t0 + tid;
+        const uint32_t key = jl < nloc ? keys[jl] : 0u;
+        const uint32_t is_eq = (jl < nloc && key == tau) ? 1u : 0u;
+        uint32_t eq_tot;
+        const uint32_t eq_rank = eq_seen + block_excl_scan(is_eq, sm.scratch, &eq_tot);
+        const uint32_t take = (jl < nloc) && (key > tau || (is_eq && eq_rank < take_eq)) ? 1u : 0u;
+        uint32_t take_tot;
+        const uint32_t pos = block_excl_scan(take, sm.scratch, &take_tot);
+        if (take) {
+          sd.sel[out_base + pos] = cand_at(sd, j0 + jl);
+          sd.sel_crit[out_base + pos] = key_float(key);
+        }
+        out_base += take_tot;
+        eq_seen += eq_tot;
+      }
+      if (cs == 0 && tid == 0) sd.cache->n_sel = kk_total;
+    }
+  }
+  if (!(p.mode & kModeAttend)) return;
+  if (any_select) grid_sync(reinterpret_cast<GridBarrier*>(p.bar), nblocks);  // #6 selection visible
+
+  // ---- phase 4: split-K sparse flash-decoding partials
+  AttView av{};
+  if (!sd.att_list) {
+    const int n_sel = (sd.select && own != 3) ? __ldcg(&sd.cache->n_sel) : 0;
+    av.init_end = sd.init_end;
+    const uint32_t ie = static_cast<uint32_t>(sd.init_end);
+    const uint32_t lb = static_cast<uint32_t>(max(sd.local_begin, sd.init_end));
+    const int lo1 = lower_bound_u32(sd.sel, n_sel, ie);
+    const int hi1 = lower_bound_u32(sd.sel, n_sel, lb < ie ? ie : static_cast<uint32_t>(sd.local_begin));
+    av.lo1 = lo1;
+    av.n1 = max(0, hi1 - lo1);
+    av.lb2 = static_cast<int>(lb);
+    av.n_rows = sd.init_end + av.n1 + (sd.n_cached - av.lb2);
+  } else {
+    av.n_rows = sd.n_att;
+  }
+  const int total_rows = av.n_rows + 1;  // + current token
+  const int per = (total_rows + p.ctas_per_seq - 1) / p.ctas_per_seq;
+  const int r0 = min(total_rows, cs * per);
+  const int r1 = min(total_rows, r0 + per);
+  const bool with_cur = (r0 < r1) && (r1 == total_rows);
+  float* part = p.ws_att + static_cast<size_t>(cta) * H * (p.d + 2);
+  attend_partial(p, sd, av, sm, r0, min(r1, av.n_rows), with_cur, part);
+  grid_sync(reinterpret_cast<GridBarrier*>(p.bar), nblocks);  // #7
+
+  // ---- phase 5: LSE merge (attention.cpp:88-110 semantics)
+  {
+    const int d = p.d, stride = d + 2;
+    const int c0 = seq_id * p.ctas_per_seq;
+    const int nparts = min(p.ctas_per_seq, (total_rows + per - 1) / per);
+    for (int h = cs; h < H; h += p.ctas_per_seq) {
+      for (int t = tid; t < d; t += blockDim.x) {
+        float M = -INFINITY;
+        for (int c = 0; c < nparts; ++c) M = fmaxf(M, __ldcg(p.ws_att + (static_cast<size_t>(c0 + c) * H + h) * stride + d));
+        float L = 0.f, O = 0.f;
+        for (int c = 0; c < nparts; ++c) {
+          const float* ph = p.ws_att + (static_cast<size_t>(c0 + c) * H + h) * stride;
+          const float mc = __ldcg(ph + d);
+          if (mc == -INFINITY) continue;
+          const float w = expf(mc - M);
+          L = fmaf(__ldcg(ph + d + 1), w, L);
+          O = fmaf(__ldcg(ph + t), w, O);
+        }
+        sd.out[static_cast<size_t>(h) * d + t] = O / L;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+const void* decode_kernel_ptr(int D, int G, bool fast) {
+  if (fast) {
+    if (D == 128) {
+      switch (G) {
+        case 1: return reinterpret_cast<const void*>(&decode_kernel<128, 1, true>);
+        case 2: return reinterpret_cast<const void*>(&decode_kernel<128, 2, true>);
+        case 4: return reinterpret_cast<const void*>(&decode_kernel<128, 4, true>);
+        case 7: return reinterpret_cast<const void*>(&decode_kernel<128, 7, true>);
+        case 8: return reinterpret_cast<const void*>(&decode_kernel<128, 8, true>);
+      }
+    }
+    if (D == 64) {
+      switch (G) {
+        case 1: return reinterpret_cast<const void*>(&decode_kernel<64, 1, true>);
+        case 2: return reinterpret_cast<const void*>(&decode_kernel<64, 2, true>);
+        case 4: return reinterpret_cast<const void*>(&decode_kernel<64, 4, true>);
+        case 8: return reinterpret_cast<const void*>(&decode_kernel<64, 8, true>);
+      }
+    }
+    return nullptr;
+  }
+  return reinterpret_cast<const void*>(&decode_kernel<0, 0, false>);
+}
+
+}  // namespace tsb

@@ -1,0 +1,319 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle
+(oracle/tsoracle.c, itself pinned to the reference in test_oracle_*.py).
+
+Tolerances (stated per assertion):
+  * generic path (small shapes): S bit-identical (fp64 accumulation, same d order)
+  * fast path (d=128 model shapes): |dS| <= 1e-4 * max(1, |S|)
+  * selected sets identical except indices whose reference criticality ties
+    the k-th value within 1e-4 relative
+  * attention output: relative Frobenius <= 1e-5 and max-abs <= 1e-4
+  * Selection Cache decisions identical
+"""
+import numpy as np
+import pytest
+
+from tests.helpers import bf16_round, check_selection, rng_normal
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sa():
+    from paper_2411_02886_b200 import selattn
+
+    return selattn
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle.oracle import Oracle
+
+    return Oracle("port")
+
+
+def rel_fro(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    n = np.linalg.norm(a)
+    return np.linalg.norm(a - b) / (n if n else 1.0)
+
+
+# --------------------------------------------------------------- scoring
+def test_score_known_answer(sa):
+    # test_selector.cpp:47-55: q = k = (1,2,3,4) -> S = 30
+    pool = sa.PagedKvPool(4, 1, 1, 4)
+    seq = pool.create_sequence()
+    q = np.arange(1, 5, dtype=np.float32).reshape(1, 4)
+    pool.append_kv(seq, q, q)
+    s, cand = sa.score_paged(q, pool, seq, [0], 8)
+    assert s[0, 0] == 30.0 and cand == [0]
+
+
+@pytest.mark.parametrize("H,H_kv,d,n", [(4, 2, 8, 83), (3, 3, 16, 120), (6, 2, 24, 64), (8, 8, 64, 300)])
+def test_score_generic_bit_exact(sa, orc, H, H_kv, d, n):
+    k = bf16_round(rng_normal(1, (n, H_kv * d)))
+    q = rng_normal(2, (H, d))
+    cand = np.arange(0, n, 2, dtype=np.uint32)
+    want = orc.score_paged(q, k, H_kv, cand)
+    for shuffle in (0, 7):
+        pool = sa.PagedKvPool(n + 4, 1, H_kv, d)
+        if shuffle:
+            pool.shuffle_free_frames(shuffle)
+        seq = pool.create_sequence()
+        pool.append_kv(seq, k, k)
+        for block in (1, 7, 64):
+            got, _ = sa.score_paged(q, pool, seq, cand, block)
+            if (H // H_kv) in (1, 2, 4, 7, 8) and d in (64, 128) and (H_kv * d) % 256 == 0:
+                assert np.all(np.abs(got - want) <= 1e-4 * np.maximum(1, np.abs(want)))
+            else:
+                assert np.array_equal(got, want), "generic path must reproduce S bit for bit"
+
+
+@pytest.mark.parametrize("H,H_kv,n,page", [(32, 8, 4000, 1), (28, 4, 3000, 1), (32, 8, 2500, 4), (16, 8, 1500, 1)])
+def test_score_fast_path(sa, orc, H, H_kv, n, page):
+    d = 128
+    k = bf16_round(rng_normal(3, (n, H_kv * d), 3.0))
+    q = rng_normal(4, (H, d))
+    cand = np.arange(128, n - 512, dtype=np.uint32)
+    want = orc.score_paged(q, k, H_kv, cand)
+    pool = sa.PagedKvPool(n + 8, page, H_kv, d)
+    pool.shuffle_free_frames(11)
+    seq = pool.create_sequence()
+    pool.append_kv(seq, k, k)
+    got, _ = sa.score_paged(q, pool, seq, cand)
+    err = np.abs(got - want) / np.maximum(1, np.abs(want))
+    assert err.max() <= 1e-4, err.max()
+
+
+def test_score_errors(sa):
+    pool = sa.PagedKvPool(12, 1, 2, 4)
+    seq = pool.create_sequence()
+    pool.append_kv(seq, np.ones((8, 8), np.float32), np.ones((8, 8), np.float32))
+    with pytest.raises(ValueError):
+        sa.score_paged(np.ones((3, 4), np.float32), pool, seq, [0], 4)
+    with pytest.raises(ValueError):
+        sa.score_paged(np.ones((2, 6), np.float32), pool, seq, [0], 4)
+    with pytest.raises(IndexError, match="index 9"):
+        sa.score_paged(np.ones((2, 4), np.float32), pool, seq, [1, 9], 4)
+
+
+# -------------------------------------------------------------- selection
+def test_select_known_answers(sa):
+    S = np.array([[5, 4.5, 0, 0], [0, 0, 500, 480]], np.float32)
+    assert sa.select(S, [0, 1, 2, 3], 2, "topk")[0] == [2, 3]
+    sel, crit = sa.select(S, [0, 1, 2, 3], 2, "head_soft_vote")
+    assert sel == [0, 2]
+    # uniform -> ties to the lower index, crit = H/T (test_selector.cpp:215-221)
+    U = np.full((3, 5), 1.25, np.float32)
+    sel, crit = sa.select(U, list(range(5)), 2, "head_soft_vote")
+    assert sel == [0, 1] and abs(crit[0] - 0.6) < 1e-6
+    # tensor.cpp ties: [7,7,7], k=2 -> {0,1}
+    assert sa.select(np.array([[7, 7, 7]], np.float32), [0, 1, 2], 2, "topk")[0] == [0, 1]
+    assert sa.select(np.array([[5, 1, 9]], np.float32), [0, 1, 2], 2, "topk")[0] == [0, 2]
+
+
+@pytest.mark.parametrize("H,T,k,method", [(2, 40, 7, "head_soft_vote"), (8, 1000, 100, "head_soft_vote"),
+                                          (32, 20000, 2048, "head_soft_vote"), (4, 5000, 600, "topk"),
+                                          (5, 300, 300, "head_soft_vote"), (3, 17, 40, "topk")])
+def test_select_vs_oracle(sa, orc, H, T, k, method):
+    S = rng_normal(10 + T, (H, T), 20.0)
+    cand = np.arange(T, dtype=np.uint32) * 3 + 5
+    got_sel, got_crit = sa.select(S, cand, k, method)
+    want_sel, want_crit = orc.select(S, cand, k, method)
+    full = orc.criticality(S, k, method)
+    check_selection(got_sel, want_sel, full, cand)
+    assert np.all(np.diff(np.asarray(got_sel, np.int64)) > 0), "ascending output"
+    m = {int(a): b for a, b in zip(want_sel, want_crit)}
+    for a, b in zip(got_sel, got_crit):
+        if a in m:
+            assert abs(b - m[a]) <= 1e-4 * max(abs(m[a]), 1e-30) + 1e-30
+
+
+def test_soft_vote_mass(sa):
+    rng = np.random.default_rng(50)
+    for _ in range(10):
+        H, T = 1 + rng.integers(6), 1 + rng.integers(50)
+        S = rng_normal(int(rng.integers(1 << 30)), (H, T), 50.0)
+        _, crit = sa.select(S, list(range(T)), T, "head_soft_vote")
+        assert abs(sum(crit) - H) <= 1e-5 * H
+
+
+# ---------------------------------------------------------------- attention
+@pytest.mark.parametrize("C", [1, 7, 64])
+def test_sparse_attend_select_all_equals_full(sa, orc, C):
+    n, H, H_kv, d = 300, 4, 2, 32
+    k = bf16_round(rng_normal(15, (n, H_kv * d)))
+    v = bf16_round(rng_normal(16, (n, H_kv * d)))
+    q = rng_normal(17, (C, H * d))
+    kc = rng_normal(18, (C, H_kv * d))
+    vc = rng_normal(19, (C, H_kv * d))
+    pool = sa.PagedKvPool(n + 4, 1, H_kv, d)
+    seq = pool.create_sequence()
+    pool.append_kv(seq, k, v)
+    got = sa.sparse_attend(q, kc, vc, pool, seq, selected=list(range(n)), num_heads=H)
+    want = orc.sdpa_full(q, np.vstack([k, kc]), np.vstack([v, vc]), H)
+    assert rel_fro(got, want) <= 1e-5
+    assert np.abs(got - want).max() <= 1e-4
+
+
+def test_sparse_attend_empty_windows(sa):
+    pool = sa.PagedKvPool(8, 1, 1, 4)
+    seq = pool.create_sequence()
+    pool.append_kv(seq, rng_normal(20, (5, 4)), rng_normal(21, (5, 4)))
+    v_cur = rng_normal(24, (1, 4))
+    out = sa.sparse_attend(rng_normal(22, (1, 4)), rng_normal(23, (1, 4)), v_cur, pool, seq, num_heads=1)
+    assert np.abs(out - v_cur).max() <= 1e-6
+
+
+# --------------------------------------------------------------- decode
+def _engine_pair(sa, orc, n, H, H_kv, d, k, n_init, n_local, theta, seed, kscale=3.0):
+    K = bf16_round(rng_normal(seed, (n, H_kv * d), kscale))
+    V = bf16_round(rng_normal(seed + 1, (n, H_kv * d)))
+    kw = dict(k=k, n_local=n_local, n_init=n_init, chunk_size=512, theta=theta, num_heads=H,
+              num_kv_heads=H_kv, head_dim=d, block_size=64)
+    eng = sa.Engine(n + 64, **kw)
+    eng.append(K, V)
+    ref = orc.engine(n + 64, **kw)
+    ref.append(K, V)
+    return eng, ref
+
+
+@pytest.mark.parametrize("H,H_kv,d,n,k", [(2, 2, 4, 64, 8), (8, 8, 64, 3000, 256), (32, 8, 128, 8192, 1024)])
+def test_decode_stream_vs_oracle(sa, orc, H, H_kv, d, n, k):
+    eng, ref = _engine_pair(sa, orc, n, H, H_kv, d, k, 16, 32, 0.9, 100 + n)
+    g = np.random.default_rng(7)
+    base = g.standard_normal(H * d).astype(np.float32)
+    hits = []
+    for step in range(6):
+        # every other step is a near-copy (hit), the rest rotate away (miss)
+        q = (base + (0.01 if step % 2 else 3.0) * g.standard_normal(H * d)).astype(np.float32).reshape(1, -1)
+        if step % 2 == 0:
+            base = q.ravel()
+        kt = bf16_round(rng_normal(500 + step, (1, H_kv * d), 3.0))
+        vt = bf16_round(rng_normal(600 + step, (1, H_kv * d)))
+        o1, h1, s1 = eng.decode(q, kt, vt)
+        o2, h2, s2 = ref.decode(q, kt, vt)
+        assert h1 == h2, f"step {step}: cache decision differs"
+        hits.append(h1)
+        if s1 != list(s2):
+            # tie tolerance against the oracle's full criticality
+            N = n + step
+            cand = np.arange(16, N - 32, dtype=np.uint32)
+            K_all = ref_rows(ref)[:N]
+            S = orc.score_paged(q.reshape(H, d), K_all, H_kv, cand)
+            check_selection(s1, s2, orc.criticality(S, k), cand)
+        assert rel_fro(o1, o2) <= 1e-5, rel_fro(o1, o2)
+        assert np.abs(o1 - o2).max() <= 1e-4
+    assert any(hits) and not all(hits)
+    st = eng.stats()
+    assert st["lookups"] == 6 and st["hits"] == sum(hits) and st["len"] == n + 6
+
+
+def ref_rows(ref):
+    import ctypes
+
+    st = ref.stats()
+    lib = ref.o.lib
+    lib.oc_engine_k_rows.restype = ctypes.POINTER(ctypes.c_float)
+    p = lib.oc_engine_k_rows(ref.h)
+    return np.ctypeslib.as_array(p, shape=(st["len"] + 1, ref.H_kv * ref.d)).copy()
+
+
+def test_decode_identical_queries_hit(sa):
+    # test_attention.cpp:341-372
+    eng = sa.Engine(96, k=8, n_init=4, n_local=0, chunk_size=16, theta=0.9, num_heads=2, num_kv_heads=2,
+                    head_dim=4, block_size=8)
+    eng.prefill(rng_normal(39, (64, 8)), rng_normal(40, (64, 8)), rng_normal(41, (64, 8)))
+    q, kt, vt = rng_normal(42, (1, 8)), rng_normal(43, (1, 8)), rng_normal(44, (1, 8))
+    o1, h1, s1 = eng.decode(q, kt, vt)
+    o2, h2, s2 = eng.decode(q, kt, vt)
+    o3, h3, s3 = eng.decode(q, kt, vt)
+    assert (h1, h2, h3) == (False, True, True)
+    assert s2 == s1 and np.array_equal(o2, o1) and np.array_equal(o3, o1)
+    assert eng.cache_hits == 2
+
+
+def test_decode_zero_query_rejected(sa):
+    eng = sa.Engine(64, k=4, n_init=2, n_local=2, num_heads=1, num_kv_heads=1, head_dim=8)
+    eng.append(rng_normal(1, (20, 8)), rng_normal(2, (20, 8)))
+    with pytest.raises(ValueError, match="zero query"):
+        eng.decode(np.zeros((1, 8), np.float32), rng_normal(3, (1, 8)), rng_normal(4, (1, 8)))
+    assert eng.stats()["lookups"] == 0 and len(eng) == 20
+
+
+def test_decode_llama_32k_parity(sa, orc):
+    """Config 1: Llama-3-8B layer, 32K cache, k=2048."""
+    n, H, H_kv, d = 32768, 32, 8, 128
+    eng, ref = _engine_pair(sa, orc, n, H, H_kv, d, 2048, 128, 512, 0.9, 4242)
+    q = rng_normal(77, (1, H * d))
+    kt = bf16_round(rng_normal(78, (1, H_kv * d), 3.0))
+    vt = bf16_round(rng_normal(79, (1, H_kv * d)))
+    o1, h1, s1 = eng.decode(q, kt, vt)
+    o2, h2, s2 = ref.decode(q, kt, vt)
+    assert not h1 and not h2
+    cand = np.arange(128, n - 512, dtype=np.uint32)
+    if s1 != list(s2):
+        S = orc.score_paged(q.reshape(H, d), ref_rows(ref)[:n], H_kv, cand)
+        check_selection(s1, s2, orc.criticality(S, 2048), cand)
+    assert rel_fro(o1, o2) <= 1e-5 and np.abs(o1 - o2).max() <= 1e-4
+
+
+# --------------------------------------------------------------- prefill
+@pytest.mark.parametrize("H,H_kv,d,n,chunk,k", [(2, 2, 4, 30, 8, 4), (2, 1, 4, 32, 16, 4096), (4, 2, 32, 1500, 256, 128)])
+def test_prefill_vs_oracle(sa, orc, H, H_kv, d, n, chunk, k):
+    kw = dict(k=k, n_local=16, n_init=8, chunk_size=chunk, theta=0.9, num_heads=H, num_kv_heads=H_kv,
+              head_dim=d, block_size=8)
+    q = rng_normal(29, (n, H * d))
+    kk = bf16_round(rng_normal(30, (n, H_kv * d)))
+    vv = bf16_round(rng_normal(31, (n, H_kv * d)))
+    eng = sa.Engine(n + 4, **kw)
+    got, tr1 = eng.prefill(q, kk, vv, trace=True)
+    ref = orc.engine(n + 4, **kw)
+    want, tr2 = ref.prefill(q, kk, vv, trace=True)
+    assert len(tr1) == len(tr2)
+    for a, b in zip(tr1, tr2):
+        assert len(a) == len(b)
+    assert rel_fro(got, want) <= 1e-5, rel_fro(got, want)
+
+
+# ------------------------------------------------------------------ pool
+def test_pool_round_trip_and_errors(sa):
+    pool = sa.PagedKvPool(64, 1, 2, 4)
+    pool.shuffle_free_frames(3)
+    seq = pool.create_sequence()
+    k = bf16_round(rng_normal(5, (20, 8)))
+    v = bf16_round(rng_normal(6, (20, 8)))
+    assert pool.append_kv(seq, k, v) == (0, 20)
+    kg, vg = pool.gather(seq, list(range(20)))
+    assert np.array_equal(kg, k) and np.array_equal(vg, v)
+    with pytest.raises(IndexError, match="index 7"):
+        pool2 = sa.PagedKvPool(16, 1, 1, 4)
+        s2 = pool2.create_sequence()
+        pool2.append_kv(s2, rng_normal(8, (4, 4)), rng_normal(9, (4, 4)))
+        pool2.gather(s2, [2, 7])
+    assert '"frames"' in pool.page_table_json(seq) and '"logical_len":20' in pool.page_table_json(seq)
+    pool.release(seq)
+    assert pool.free_frames == pool.total_frames
+    with pytest.raises(ValueError):
+        pool.release(seq)
+
+
+def test_pool_capacity_no_partial_append(sa):
+    pool = sa.PagedKvPool(8, 1, 1, 4)
+    seq = pool.create_sequence()
+    pool.append_kv(seq, rng_normal(10, (6, 4)), rng_normal(11, (6, 4)))
+    with pytest.raises(sa.CapacityError):
+        pool.append_kv(seq, rng_normal(12, (3, 4)), rng_normal(13, (3, 4)))
+    assert pool.logical_len(seq) == 6 and pool.free_frames == 2
+
+
+def test_pool_page_size_4(sa):
+    pool = sa.PagedKvPool(64, 4, 1, 4)
+    assert pool.total_frames == 16
+    seq = pool.create_sequence()
+    k = bf16_round(rng_normal(25, (10, 4)))
+    v = bf16_round(rng_normal(26, (10, 4)))
+    pool.append_kv(seq, k, v)
+    assert pool.free_frames == 13
+    kg, vg = pool.gather(seq, list(range(10)))
+    assert np.array_equal(kg, k) and np.array_equal(vg, v)
