@@ -171,6 +171,15 @@ ts_status ts_engine_decode_async(ts_engine* eng, const float* q, const float* k,
 /* Forces the next lookup of sequence `seq` to miss (first_flag = true,
  * selattn_bench.cpp:439 idiom). */
 ts_status ts_engine_force_miss(ts_engine* eng, size_t seq);
+/* Device phase trace of the fused decode kernel (tracing subsystem): when
+ * enabled, CTA 0 stamps %globaltimer (ns) at 15 phase boundaries of every
+ * decode step; ts_engine_read_trace copies the stamps of the last step. */
+ts_status ts_engine_set_trace(ts_engine* eng, int enable);
+ts_status ts_engine_read_trace(ts_engine* eng, uint64_t* stamps, size_t n);
+/* SelectionCacheEntry::theta of sequence `seq` (the reference reads theta
+ * from the entry, selection_cache.cpp:34; the bench sets it by hand,
+ * selattn_bench.cpp:239). */
+ts_status ts_engine_set_theta(ts_engine* eng, size_t seq, double theta);
 /* CacheStats + logical length (attention.hpp:102-103); blocks on the stream.
  * last_hit: -1 when the last step ran no lookup. */
 ts_status ts_engine_stats(const ts_engine* eng, size_t seq, size_t* lookups, size_t* hits,

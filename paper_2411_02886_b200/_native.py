@@ -74,6 +74,9 @@ SIGNATURES = {
     "ts_engine_decode": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _p]),
     "ts_engine_decode_async": (C.c_int, [_p, _p, _p, _p, _p]),
     "ts_engine_force_miss": (C.c_int, [_p, _sz]),
+    "ts_engine_set_theta": (C.c_int, [_p, _sz, C.c_double]),
+    "ts_engine_set_trace": (C.c_int, [_p, C.c_int]),
+    "ts_engine_read_trace": (C.c_int, [_p, _p, _sz]),
     "ts_engine_stats": (C.c_int, [_p, _sz, C.POINTER(_sz), C.POINTER(_sz), C.POINTER(_sz), C.POINTER(C.c_int),
                                   C.POINTER(C.c_double)]),
     "ts_engine_cached_selection": (C.c_int, [_p, _sz, _p, _p, C.POINTER(_sz)]),

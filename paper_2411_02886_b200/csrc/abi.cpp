@@ -136,11 +136,12 @@ struct Workspace {
       s.ensure(static_cast<size_t>(n_ctas) * H * tpc * 4);
       keys.ensure(static_cast<size_t>(n_ctas) * tpc * 4);
     }
-    m.ensure(static_cast<size_t>(n_ctas) * H * 4);
-    z.ensure(static_cast<size_t>(n_ctas) * H * 4);
+    const int cps = n_ctas / n_seq;
+    m.ensure(static_cast<size_t>(n_seq) * H * tsb::stats_stride(cps) * 4);
+    z.ensure(static_cast<size_t>(n_seq) * H * tsb::stats_stride(cps) * 4);
     hist.ensure(static_cast<size_t>(n_seq) * 3 * 2048 * 4);
     cnt.ensure(static_cast<size_t>(n_ctas) * 2 * 4);
-    att.ensure(static_cast<size_t>(n_ctas) * H * (d + 2) * 4);
+    att.ensure(static_cast<size_t>(n_ctas) * H * tsb::att_stride(d) * 4);
     if (!bar_init) {
       bar.ensure(64);
       ck(cudaMemsetAsync(bar.p, 0, 64, st), "memset barrier");
@@ -180,6 +181,12 @@ Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows) {
   const size_t ring = tsb::smem_layout(H, row_bytes, 1, 0).s - tsb::smem_layout(H, row_bytes, 1, 0).ring;
   pl.att_rows = static_cast<int>(ring / (2 * static_cast<size_t>(row_bytes)));
   if (H > 16 * 4) fail(TS_INVALID_ARGUMENT, "num_heads > 64 is not supported by the decode kernel");
+  {
+    const size_t qb = tsb::align_up(static_cast<size_t>(H) * d * 4, 128);
+    const size_t rs = static_cast<size_t>(H_kv * d + 8) * 2;
+    if (qb >= tsb::kRingBudget || (tsb::kRingBudget - qb) / (2 * rs) < 1)
+      fail(TS_INVALID_ARGUMENT, "attention rows do not fit the decode kernel's staging ring");
+  }
   if (d > 256) fail(TS_INVALID_ARGUMENT, "head_dim > 256 is not supported by the decode kernel");
   return pl;
 }
@@ -329,6 +336,9 @@ struct ts_engine {
   float* h_out = nullptr;
   CacheState* h_cache = nullptr;
   Workspace ws;
+  // device phase trace (%globaltimer stamps of CTA 0), when enabled
+  DevBuf trace;
+  bool trace_on = false;
   // prefill scratch
   DevBuf p_qmean, p_sel, p_crit, p_state, p_att, p_natt, p_bad, p_q, p_k, p_v, p_out;
 
@@ -912,6 +922,8 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
     }
     const Plan pl = make_plan(static_cast<int>(c.num_heads), static_cast<int>(c.num_kv_heads),
                               static_cast<int>(c.head_dim), static_cast<int>(gn), max_T, max_rows);
+    p.trace = e->trace_on ? e->trace.as<unsigned long long>() : nullptr;
+    if (p.trace) ck(cudaMemsetAsync(p.trace, 0, 32 * 8, st), "memset trace");
     launch_decode(p, pl, e->ws, st);
     for (size_t i = 0; i < gn; ++i)
       if (!cap_fail[g0 + i]) pool.state(e->seq_ids[g0 + i]).len += 1;
@@ -988,6 +1000,33 @@ ts_status ts_engine_force_miss(ts_engine* e, size_t seq) {
     if (seq >= e->B) fail(TS_INVALID_ARGUMENT, "engine: sequence index out of range");
     const int one = 1;
     ck(cudaMemcpyAsync(&e->cache(seq)->first_flag, &one, sizeof(int), cudaMemcpyHostToDevice, e->stream), "H2D");
+    ck(cudaStreamSynchronize(e->stream), "sync");
+  });
+}
+
+ts_status ts_engine_set_trace(ts_engine* e, int enable) {
+  return guarded([&] {
+    e->trace_on = enable != 0;
+    if (e->trace_on) {
+      e->trace.ensure(32 * 8);
+      ck(cudaMemsetAsync(e->trace.p, 0, 32 * 8, e->stream), "memset");
+      ck(cudaStreamSynchronize(e->stream), "sync");
+    }
+  });
+}
+
+ts_status ts_engine_read_trace(ts_engine* e, uint64_t* stamps, size_t n) {
+  return guarded([&] {
+    if (!e->trace.p) fail(TS_INVALID_ARGUMENT, "trace not enabled");
+    ck(cudaStreamSynchronize(e->stream), "sync");
+    ck(cudaMemcpy(stamps, e->trace.p, std::min<size_t>(n, 32) * 8, cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
+ts_status ts_engine_set_theta(ts_engine* e, size_t seq, double theta) {
+  return guarded([&] {
+    if (seq >= e->B) fail(TS_INVALID_ARGUMENT, "engine: sequence index out of range");
+    ck(cudaMemcpyAsync(&e->cache(seq)->theta, &theta, sizeof(double), cudaMemcpyHostToDevice, e->stream), "H2D");
     ck(cudaStreamSynchronize(e->stream), "sync");
   });
 }

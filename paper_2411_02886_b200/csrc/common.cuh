@@ -164,22 +164,32 @@ __device__ __forceinline__ unsigned int atom_add_acqrel_u32(unsigned int* p, uns
   return old;
 }
 
-__device__ __forceinline__ void grid_sync(GridBarrier* bar, unsigned int nblocks) {
+__device__ __forceinline__ unsigned int atom_add_release_u32(unsigned int* p, unsigned int v) {
+  unsigned int old;
+  asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// Generation barrier. `gen` is read once per launch (grid_sync_begin, before
+// any barrier of the launch can complete) and then tracked locally, so an
+// arrival costs one release-add and the wait one acquire-poll.
+__device__ __forceinline__ unsigned int grid_sync_begin(GridBarrier* bar) {
+  return ld_acquire_u32(&bar->gen);
+}
+
+__device__ __forceinline__ void grid_sync(GridBarrier* bar, unsigned int nblocks, unsigned int& gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned int gen = ld_acquire_u32(&bar->gen);
-    __threadfence();
     const unsigned int arrived = atom_add_acqrel_u32(&bar->count, 1u);
     if (arrived == nblocks - 1) {
       bar->count = 0;
-      __threadfence();
       st_release_u32(&bar->gen, gen + 1);
     } else {
       while (ld_acquire_u32(&bar->gen) == gen) {
       }
     }
-    __threadfence();
   }
+  ++gen;
   __syncthreads();
 }
 

@@ -44,8 +44,11 @@ struct Smem {
   int* headmax;    // [H] ordered-int max
   float* f;        // [H]
   uint32_t* scratch;  // [64]
+  int32_t* frames; // [tpc] slab row of each local candidate
   uint64_t* full;  // [kMaxStages]
   uint64_t* empty; // [kMaxStages]
+  uint64_t* att;   // attention staging barrier
+  uint64_t* aux;   // bulk staging barrier (stats, partials)
 };
 
 __device__ __forceinline__ Smem carve(uint8_t* base, const DecodeParams& p) {
@@ -60,6 +63,9 @@ __device__ __forceinline__ Smem carve(uint8_t* base, const DecodeParams& p) {
   s.scratch = reinterpret_cast<uint32_t*>(base + L.scratch);
   s.full = reinterpret_cast<uint64_t*>(base + L.bars);
   s.empty = s.full + kMaxStages;
+  s.att = s.full + 2 * kMaxStages;
+  s.aux = s.att + 1;
+  s.frames = reinterpret_cast<int32_t*>(base + L.frames);
   return s;
 }
 
@@ -70,6 +76,15 @@ __device__ __forceinline__ uint32_t cand_at(const SeqDesc& sd, int j) {
 __device__ __forceinline__ size_t row_index(const SeqDesc& sd, uint32_t tok, int page_size) {
   if (page_size == 1) return static_cast<size_t>(sd.page_table[tok]);
   return static_cast<size_t>(sd.page_table[tok / page_size]) * page_size + tok % page_size;
+}
+
+// Phase trace: CTA 0 records %globaltimer at phase boundaries when enabled.
+__device__ __forceinline__ void trace_pt(const DecodeParams& p, int i) {
+  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[i] = t;
+  }
 }
 
 // Block-wide exclusive scan of one value per thread (all threads call).
@@ -136,13 +151,24 @@ __device__ int cache_decision(const SeqDesc& sd, int width, double* scratch_d, d
   const CacheState* cs = sd.cache;
   double dot = 0.0, nu = 0.0, nv = 0.0;
   int nonzero = 0;
-  for (int i = threadIdx.x; i < width; i += blockDim.x) {
-    const double a = static_cast<double>(sd.q[i]);
-    const double b = static_cast<double>(sd.cached_q[i]);
-    nonzero |= (sd.q[i] != 0.0f);
-    dot = fma(a, b, dot);
-    nu = fma(a, a, nu);
-    nv = fma(b, b, nv);
+  constexpr int kU = 8;  // loads in flight per thread
+  for (int base = threadIdx.x; base < width; base += kU * blockDim.x) {
+    float qa[kU], qb[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = base + u * blockDim.x;
+      qa[u] = i < width ? __ldg(sd.q + i) : 0.f;
+      qb[u] = i < width ? __ldcg(sd.cached_q + i) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const double a = static_cast<double>(qa[u]);
+      const double b = static_cast<double>(qb[u]);
+      nonzero |= (qa[u] != 0.0f);
+      dot = fma(a, b, dot);
+      nu = fma(a, a, nu);
+      nv = fma(b, b, nv);
+    }
   }
   nonzero = __syncthreads_or(nonzero);
   dot = warp_sum_d(dot);
@@ -155,12 +181,13 @@ __device__ int cache_decision(const SeqDesc& sd, int width, double* scratch_d, d
     scratch_d[warp * 3 + 2] = nv;
   }
   __syncthreads();
-  double D = 0.0, U = 0.0, V = 0.0;
-  for (int w = 0; w < kDecodeWarps; ++w) {
-    D += scratch_d[w * 3 + 0];
-    U += scratch_d[w * 3 + 1];
-    V += scratch_d[w * 3 + 2];
-  }
+  // every warp reduces the per-warp partials in the same fixed tree order
+  double D = lane < kDecodeWarps ? scratch_d[lane * 3 + 0] : 0.0;
+  double U = lane < kDecodeWarps ? scratch_d[lane * 3 + 1] : 0.0;
+  double V = lane < kDecodeWarps ? scratch_d[lane * 3 + 2] : 0.0;
+  D = warp_sum_d(D);
+  U = warp_sum_d(U);
+  V = warp_sum_d(V);
   __syncthreads();
   if (!nonzero) return 2;
   *cos_out = NAN;
@@ -201,30 +228,20 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
 
   if (warp == 0) {
     // ---------------------------------------------------------- producer
+    // slab rows of all local candidates were staged in smem (sm.frames)
+    // before the scan, so issuing a stage is latency-free.
     const uint64_t pol = policy_evict_first();
     const char* kbase = reinterpret_cast<const char*>(p.k_slab);
-    const char* src_next = nullptr;
-    if (lane < R && lane < nloc) {
-      const uint32_t tok = cand_at(sd, j0 + lane);
-      src_next = kbase + row_index(sd, tok, p.page_size) * row_bytes;
-    }
     for (int it = 0; it < nit; ++it) {
       const int s = it % kStages;
       const int rbase = it * R;
       const int nrows = min(R, nloc - rbase);
-      const char* src = src_next;
-      // prefetch the next stage's frame while this one is in flight
-      const int nr = rbase + R + lane;
-      if (lane < R && nr < nloc) {
-        const uint32_t tok = cand_at(sd, j0 + nr);
-        src_next = kbase + row_index(sd, tok, p.page_size) * row_bytes;
-      }
       if (it >= kStages) mbar_wait(&sm.empty[s], ((it / kStages) & 1) ^ 1);
       if (lane == 0) mbar_arrive_expect_tx(&sm.full[s], static_cast<uint32_t>(nrows * row_bytes));
       __syncwarp();
       if (lane < nrows)
-        bulk_g2s(sm.ring + static_cast<size_t>(s * R + lane) * row_bytes, src, row_bytes,
-                 &sm.full[s], pol);
+        bulk_g2s(sm.ring + static_cast<size_t>(s * R + lane) * row_bytes,
+                 kbase + static_cast<size_t>(sm.frames[rbase + lane]) * row_bytes, row_bytes, &sm.full[s], pol);
     }
     return;
   }
@@ -345,8 +362,7 @@ __device__ void scan_generic(const DecodeParams& p, const SeqDesc& sd, const Sme
   const int total = p.H * nloc;
   for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
     const int h = idx / nloc, jl = idx - (idx / nloc) * nloc;
-    const uint32_t tok = cand_at(sd, j0 + jl);
-    const uint16_t* key = p.k_slab + row_index(sd, tok, p.page_size) * row + (h % p.H_kv) * d;
+    const uint16_t* key = p.k_slab + static_cast<size_t>(sm.frames[jl]) * row + (h % p.H_kv) * d;
     const float* qh = sd.q + static_cast<size_t>(h) * d;
     double acc = 0.0;
     for (int t = 0; t < d; ++t) acc = fma(static_cast<double>(qh[t]), static_cast<double>(bf16_bits_to_f(key[t])), acc);
@@ -384,48 +400,63 @@ __device__ __forceinline__ uint32_t att_token(const SeqDesc& sd, const AttView& 
 
 // split-K flash-decoding partial over rows [r0, r1) of the merged window
 // list, plus the current token when `with_cur`; writes (o[d], m, l) per head.
+// Rows are staged in smem (bulk copies, padded stride); per head a warp
+// scores all staged rows at once (lane = row, q broadcast from smem), then
+// does one online-softmax update and the P.V accumulation (lane = d slice).
 __device__ void attend_partial(const DecodeParams& p, const SeqDesc& sd, const AttView& av,
                                const Smem& sm, int r0, int r1, bool with_cur, float* part) {
   const int H = p.H, Hkv = p.H_kv, d = p.d;
   const int row_elems = Hkv * d;
   const int row_bytes = row_elems * 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kMaxDL = 8;  // d <= 256
-  const int dl = (d + 31) / 32;
-  // per (warp, head-slot) running state lives in registers
-  constexpr int kMaxHeadsPerWarp = 4;  // H <= 68
+  constexpr int kMaxDL = 8;            // d <= 256
+  constexpr int kMaxHeadsPerWarp = 4;  // H <= 64
+  const bool vec = (row_bytes % 16) == 0 && (d % 8) == 0;
+  const int rstride = vec ? row_elems + 8 : row_elems;  // bf16 elements; +16 B breaks bank aliasing
+  const bool d128 = vec && d == 128;                   // vectorised P.V layout (see below)
+  // carve the ring: q (fp32, H*d) then K rows then V rows
+  float* qs = reinterpret_cast<float*>(sm.ring);
+  uint16_t* kbuf = reinterpret_cast<uint16_t*>(sm.ring + align_up(static_cast<size_t>(H) * d * 4, 128));
+  const size_t avail = kRingBudget - align_up(static_cast<size_t>(H) * d * 4, 128);
+  int cap = static_cast<int>(avail / (2 * static_cast<size_t>(rstride) * 2));
+  if (cap > 32) cap = 32;
+  uint16_t* vbuf = kbuf + static_cast<size_t>(cap) * rstride;
+  for (int base = threadIdx.x; base < H * d; base += 8 * blockDim.x) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * blockDim.x;
+      v[u] = i < H * d ? __ldg(sd.q + i) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * blockDim.x;
+      if (i < H * d) qs[i] = v[u];
+    }
+  }
   float m_run[kMaxHeadsPerWarp], l_run[kMaxHeadsPerWarp], o_run[kMaxHeadsPerWarp][kMaxDL];
-  float qreg[kMaxHeadsPerWarp][kMaxDL];
 #pragma unroll
   for (int hs = 0; hs < kMaxHeadsPerWarp; ++hs) {
     m_run[hs] = -INFINITY;
     l_run[hs] = 0.f;
-    const int h = warp + hs * kDecodeWarps;
 #pragma unroll
-    for (int i = 0; i < kMaxDL; ++i) {
-      o_run[hs][i] = 0.f;
-      const int t = lane + 32 * i;
-      qreg[hs][i] = (h < H && i < dl && t < d) ? sd.q[static_cast<size_t>(h) * d + t] : 0.f;
-    }
+    for (int i = 0; i < kMaxDL; ++i) o_run[hs][i] = 0.f;
   }
-  const int cap = p.att_rows_per_cta;
-  uint16_t* kbuf = reinterpret_cast<uint16_t*>(sm.ring);
-  uint16_t* vbuf = kbuf + static_cast<size_t>(cap) * row_elems;
-  const bool vec = (row_bytes % 16) == 0;
+  uint32_t att_phase = 0;
   for (int c0 = r0; c0 < r1; c0 += cap) {
     const int nr = min(cap, r1 - c0);
-    __syncthreads();
+    __syncthreads();  // previous sub-chunk consumed; qs visible
     if (vec) {
-      const int chunks = row_bytes / 16;
-      for (int idx = threadIdx.x; idx < nr * chunks * 2; idx += blockDim.x) {
-        const int which = idx / (nr * chunks);
-        const int rem = idx - which * nr * chunks;
-        const int r = rem / chunks, c = rem - (rem / chunks) * chunks;
-        const uint32_t tok = att_token(sd, av, c0 + r);
-        const uint16_t* src = (which ? p.v_slab : p.k_slab) + row_index(sd, tok, p.page_size) * row_elems;
-        uint16_t* dst = (which ? vbuf : kbuf) + static_cast<size_t>(r) * row_elems;
-        reinterpret_cast<uint4*>(dst)[c] = __ldg(reinterpret_cast<const uint4*>(src) + c);
+      if (threadIdx.x == 0) mbar_arrive_expect_tx(sm.att, static_cast<uint32_t>(nr * 2 * row_bytes));
+      __syncthreads();
+      if (static_cast<int>(threadIdx.x) < nr) {
+        const int r = threadIdx.x;
+        const size_t ri = row_index(sd, att_token(sd, av, c0 + r), p.page_size);
+        bulk_g2s_nohint(kbuf + static_cast<size_t>(r) * rstride, p.k_slab + ri * row_elems, row_bytes, sm.att);
+        bulk_g2s_nohint(vbuf + static_cast<size_t>(r) * rstride, p.v_slab + ri * row_elems, row_bytes, sm.att);
       }
+      mbar_wait(sm.att, att_phase);
+      att_phase ^= 1u;
     } else {
       for (int idx = threadIdx.x; idx < nr * row_elems * 2; idx += blockDim.x) {
         const int which = idx / (nr * row_elems);
@@ -433,36 +464,66 @@ __device__ void attend_partial(const DecodeParams& p, const SeqDesc& sd, const A
         const int r = rem / row_elems, c = rem - (rem / row_elems) * row_elems;
         const uint32_t tok = att_token(sd, av, c0 + r);
         const uint16_t* src = (which ? p.v_slab : p.k_slab) + row_index(sd, tok, p.page_size) * row_elems;
-        ((which ? vbuf : kbuf) + static_cast<size_t>(r) * row_elems)[c] = src[c];
+        ((which ? vbuf : kbuf) + static_cast<size_t>(r) * rstride)[c] = src[c];
       }
+      __syncthreads();
     }
-    __syncthreads();
 #pragma unroll
     for (int hs = 0; hs < kMaxHeadsPerWarp; ++hs) {
       const int h = warp + hs * kDecodeWarps;
       if (h >= H) break;
       const int kvo = (h % Hkv) * d;
-      for (int r = 0; r < nr; ++r) {
-        const uint16_t* kr = kbuf + static_cast<size_t>(r) * row_elems + kvo;
-        float part_dot = 0.f;
-#pragma unroll
-        for (int i = 0; i < kMaxDL; ++i) {
-          const int t = lane + 32 * i;
-          if (i < dl && t < d) part_dot = fmaf(qreg[hs][i], bf16_bits_to_f(kr[t]), part_dot);
+      const float* qh = qs + static_cast<size_t>(h) * d;
+      // scores: lane r owns row r
+      float s = -INFINITY;
+      if (lane < nr) {
+        const uint16_t* kr = kbuf + static_cast<size_t>(lane) * rstride + kvo;
+        float2 acc = make_float2(0.f, 0.f);
+        if (vec) {
+          for (int t = 0; t < d; t += 8) {
+            const uint4 kx = *reinterpret_cast<const uint4*>(kr + t);
+            const float4 qa = *reinterpret_cast<const float4*>(qh + t);
+            const float4 qb = *reinterpret_cast<const float4*>(qh + t + 4);
+            ffma2(acc, bf16x2_to_f2(kx.x), make_float2(qa.x, qa.y));
+            ffma2(acc, bf16x2_to_f2(kx.y), make_float2(qa.z, qa.w));
+            ffma2(acc, bf16x2_to_f2(kx.z), make_float2(qb.x, qb.y));
+            ffma2(acc, bf16x2_to_f2(kx.w), make_float2(qb.z, qb.w));
+          }
+        } else {
+          for (int t = 0; t < d; ++t) acc.x = fmaf(qh[t], bf16_bits_to_f(kr[t]), acc.x);
         }
-        const float s = warp_sum(part_dot) * p.attn_scale;
-        const float m_new = fmaxf(m_run[hs], s);
-        const float corr = expf(m_run[hs] - m_new);
-        const float w = expf(s - m_new);
-        l_run[hs] = l_run[hs] * corr + w;
-        const uint16_t* vr = vbuf + static_cast<size_t>(r) * row_elems + kvo;
-#pragma unroll
-        for (int i = 0; i < kMaxDL; ++i) {
-          const int t = lane + 32 * i;
-          if (i < dl && t < d) o_run[hs][i] = fmaf(w, bf16_bits_to_f(vr[t]), o_run[hs][i] * corr);
-        }
-        m_run[hs] = m_new;
+        s = (acc.x + acc.y) * p.attn_scale;
       }
+      const float mt = warp_max(s);
+      const float m_new = fmaxf(m_run[hs], mt);
+      const float corr = expf(m_run[hs] - m_new);
+      const float w = lane < nr ? expf(s - m_new) : 0.f;
+      l_run[hs] = l_run[hs] * corr + warp_sum(w);
+#pragma unroll
+      for (int i = 0; i < kMaxDL; ++i) o_run[hs][i] *= corr;
+      if (d == 128 && vec) {
+        // lane owns d-elements [4*lane, 4*lane+4): one 8-byte smem load per row
+        for (int r = 0; r < nr; ++r) {
+          const float wr = __shfl_sync(0xffffffffu, w, r);
+          const uint2 vv = *reinterpret_cast<const uint2*>(vbuf + static_cast<size_t>(r) * rstride + kvo + 4 * lane);
+          const float2 v01 = bf16x2_to_f2(vv.x), v23 = bf16x2_to_f2(vv.y);
+          o_run[hs][0] = fmaf(wr, v01.x, o_run[hs][0]);
+          o_run[hs][1] = fmaf(wr, v01.y, o_run[hs][1]);
+          o_run[hs][2] = fmaf(wr, v23.x, o_run[hs][2]);
+          o_run[hs][3] = fmaf(wr, v23.y, o_run[hs][3]);
+        }
+      } else {
+        for (int r = 0; r < nr; ++r) {
+          const float wr = __shfl_sync(0xffffffffu, w, r);
+          const uint16_t* vr = vbuf + static_cast<size_t>(r) * rstride + kvo;
+#pragma unroll
+          for (int i = 0; i < kMaxDL; ++i) {
+            const int t = lane + 32 * i;
+            if (t < d) o_run[hs][i] = fmaf(wr, bf16_bits_to_f(vr[t]), o_run[hs][i]);
+          }
+        }
+      }
+      m_run[hs] = m_new;
     }
   }
   if (with_cur) {
@@ -475,7 +536,7 @@ __device__ void attend_partial(const DecodeParams& p, const SeqDesc& sd, const A
 #pragma unroll
       for (int i = 0; i < kMaxDL; ++i) {
         const int t = lane + 32 * i;
-        if (i < dl && t < d) part_dot = fmaf(qreg[hs][i], sd.k_new[kvo + t], part_dot);
+        if (t < d) part_dot = fmaf(sd.q[static_cast<size_t>(h) * d + t], sd.k_new[kvo + t], part_dot);
       }
       const float s = warp_sum(part_dot) * p.attn_scale;
       const float m_new = fmaxf(m_run[hs], s);
@@ -484,13 +545,13 @@ __device__ void attend_partial(const DecodeParams& p, const SeqDesc& sd, const A
       l_run[hs] = l_run[hs] * corr + w;
 #pragma unroll
       for (int i = 0; i < kMaxDL; ++i) {
-        const int t = lane + 32 * i;
-        if (i < dl && t < d) o_run[hs][i] = fmaf(w, sd.v_new[kvo + t], o_run[hs][i] * corr);
+        const int t = d128 ? 4 * lane + i : lane + 32 * i;
+        if ((d128 ? i < 4 : t < d)) o_run[hs][i] = fmaf(w, sd.v_new[kvo + t], o_run[hs][i] * corr);
       }
       m_run[hs] = m_new;
     }
   }
-  const int stride = d + 2;
+  const int stride = att_stride(d);
 #pragma unroll
   for (int hs = 0; hs < kMaxHeadsPerWarp; ++hs) {
     const int h = warp + hs * kDecodeWarps;
@@ -498,8 +559,8 @@ __device__ void attend_partial(const DecodeParams& p, const SeqDesc& sd, const A
     float* ph = part + static_cast<size_t>(h) * stride;
 #pragma unroll
     for (int i = 0; i < kMaxDL; ++i) {
-      const int t = lane + 32 * i;
-      if (i < dl && t < d) ph[t] = o_run[hs][i];
+      const int t = d128 ? 4 * lane + i : lane + 32 * i;
+      if ((d128 ? i < 4 : t < d)) ph[t] = o_run[hs][i];
     }
     if (lane == 0) {
       ph[d] = m_run[hs];
@@ -526,10 +587,19 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     mbar_init(&sm.full[tid], 1);
     mbar_init(&sm.empty[tid], kConsumerWarps);
   }
+  if (tid == 0) {
+    mbar_init(sm.att, 1);
+    mbar_init(sm.aux, 1);
+  }
+  uint32_t aux_phase = 0;
   for (int h = tid; h < H; h += blockDim.x) sm.headmax[h] = float_ord(-INFINITY);
-  if (FAST) fence_mbar_init();
+  fence_mbar_init();
+  GridBarrier* gbar = reinterpret_cast<GridBarrier*>(p.bar);
+  unsigned int bar_gen = 0;
+  if (tid == 0) bar_gen = grid_sync_begin(gbar);  // only thread 0 uses it
   __syncthreads();
 
+  trace_pt(p, 0);
   // ---- phase 0: append + cache decision + histogram reset
   if ((p.mode & kModeAppend) && cs == 0 && sd.append_frame >= 0) {
     const int row = p.H_kv * p.d;
@@ -573,6 +643,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   }
   if (cs == 0 && tid == 0 && own == 3) sd.cache->error = 1;
 
+  trace_pt(p, 1);
   // ---- phase 1: scan
   const int T = sd.n_cand;
   const int j0 = min(T, cs * p.tpc);
@@ -591,11 +662,24 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       }
     } else {
       float* so = (p.mode & kModeSOut) ? sd.s_out + j0 : nullptr;
+      for (int base = tid; base < nloc; base += 4 * blockDim.x) {
+        int32_t fr[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int jl = base + u * blockDim.x;
+          fr[u] = jl < nloc ? static_cast<int32_t>(row_index(sd, cand_at(sd, j0 + jl), p.page_size)) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (base + u * static_cast<int>(blockDim.x) < nloc) sm.frames[base + u * blockDim.x] = fr[u];
+      }
+      __syncthreads();
       if constexpr (FAST) scan_fast<D, G>(p, sd, sm, j0, nloc, Sbuf, sstride, so);
       else scan_generic(p, sd, sm, j0, nloc, Sbuf, sstride, so);
     }
   }
   __syncthreads();
+  trace_pt(p, 2);
 
   if (do_select && own == 1 && p.method == 2) {
     // per-CTA softmax partials: m = max_j S, z = sum_j exp(S - m); S <- exp(S - m)
@@ -605,20 +689,38 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       float z = 0.f;
       float* sr = Sbuf + static_cast<size_t>(h) * sstride;
       if (m > -INFINITY) {
-        for (int jl = lane; jl < nloc; jl += 32) {
+        float z1 = 0.f, z2 = 0.f, z3 = 0.f;
+        int jl = lane;
+        for (; jl + 96 < nloc; jl += 128) {
+          const float e0 = expf(sr[jl] - m), e1 = expf(sr[jl + 32] - m);
+          const float e2 = expf(sr[jl + 64] - m), e3 = expf(sr[jl + 96] - m);
+          sr[jl] = e0;
+          sr[jl + 32] = e1;
+          sr[jl + 64] = e2;
+          sr[jl + 96] = e3;
+          z += e0;
+          z1 += e1;
+          z2 += e2;
+          z3 += e3;
+        }
+        for (; jl < nloc; jl += 32) {
           const float e = expf(sr[jl] - m);
           sr[jl] = e;
           z += e;
         }
+        z = (z + z1) + (z2 + z3);
       }
       z = warp_sum(z);
       if (lane == 0) {
-        p.ws_m[static_cast<size_t>(cta) * H + h] = m;
-        p.ws_z[static_cast<size_t>(cta) * H + h] = z;
+        const size_t o = (static_cast<size_t>(seq_id) * H + h) * stats_stride(p.ctas_per_seq) + cs;
+        p.ws_m[o] = m;
+        p.ws_z[o] = z;
       }
     }
   }
-  if (any_select) grid_sync(reinterpret_cast<GridBarrier*>(p.bar), nblocks);  // #1
+  trace_pt(p, 3);
+  if (any_select) grid_sync(gbar, nblocks, bar_gen);  // #1
+  trace_pt(p, 4);
 
   // ---- phase 2: crit + cache bookkeeping
   if (own == 1 && cs == 0 && tid == 0 && (p.mode & kModeCache)) {
@@ -646,14 +748,30 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     if (p.method == 2) {
       const int warp = tid >> 5, lane = tid & 31;
       const int c0 = seq_id * p.ctas_per_seq;
+      // stage every CTA's (m, z) of this sequence in smem with one coalesced pass
+      float* pm = reinterpret_cast<float*>(sm.ring);
+      float* pz = pm;
+      const int nc = p.ctas_per_seq;
+      const int ncp = stats_stride(nc);
+      // the sequence's [h][cta] stats are two contiguous rows blocks: 2 bulk copies
+      const size_t sbytes = static_cast<size_t>(H) * ncp * 4;
+      if (tid == 0) {
+        mbar_arrive_expect_tx(sm.aux, static_cast<uint32_t>(2 * sbytes));
+        bulk_g2s_nohint(pm, p.ws_m + static_cast<size_t>(seq_id) * H * ncp, static_cast<uint32_t>(sbytes), sm.aux);
+        bulk_g2s_nohint(pm + H * ncp, p.ws_z + static_cast<size_t>(seq_id) * H * ncp, static_cast<uint32_t>(sbytes), sm.aux);
+      }
+      pz = pm + H * ncp;
+      mbar_wait(sm.aux, aux_phase);
+      aux_phase ^= 1u;
+      trace_pt(p, 15);
       for (int h = warp; h < H; h += kDecodeWarps) {
         float M = -INFINITY;
-        for (int c = lane; c < p.ctas_per_seq; c += 32) M = fmaxf(M, __ldcg(p.ws_m + static_cast<size_t>(c0 + c) * H + h));
+        for (int c = lane; c < nc; c += 32) M = fmaxf(M, pm[h * ncp + c]);
         M = warp_max(M);
         float Z = 0.f;
-        for (int c = lane; c < p.ctas_per_seq; c += 32) {
-          const float mc = __ldcg(p.ws_m + static_cast<size_t>(c0 + c) * H + h);
-          if (mc > -INFINITY) Z += __ldcg(p.ws_z + static_cast<size_t>(c0 + c) * H + h) * expf(mc - M);
+        for (int c = lane; c < nc; c += 32) {
+          const float mc = pm[h * ncp + c];
+          if (mc > -INFINITY) Z += pz[h * ncp + c] * expf(mc - M);
         }
         Z = warp_sum(Z);
         if (lane == 0) {
@@ -661,6 +779,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
           sm.f[h] = (ms > -INFINITY) ? expf(ms - M) / Z : 0.f;
         }
       }
+      trace_pt(p, 16);
       __syncthreads();
       for (int jl = tid; jl < nloc; jl += blockDim.x) {
         float c = 0.f;
@@ -677,6 +796,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     __syncthreads();
   }
 
+  trace_pt(p, 5);
   // ---- phase 3: radix select (3 passes, 11/11/10 bits)
   if (any_radix) {
     uint32_t prefix = 0;
@@ -701,7 +821,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
           if (c) atomicAdd(gh + pass * kBins + i, c);
         }
       }
-      grid_sync(reinterpret_cast<GridBarrier*>(p.bar), nblocks);  // #2..#4
+      grid_sync(gbar, nblocks, bar_gen);  // #2..#4
+      trace_pt(p, 6 + pass);
       if (radix_own) {
         int b;
         uint32_t above;
@@ -727,7 +848,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
         p.ws_cnt[static_cast<size_t>(cta) * 2 + 1] = te;
       }
     }
-    grid_sync(reinterpret_cast<GridBarrier*>(p.bar), nblocks);  // #5
+    grid_sync(gbar, nblocks, bar_gen);  // #5
+    trace_pt(p, 9);
   }
 
   // ---- phase 3b: ascending compaction of the selection
@@ -780,8 +902,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       if (cs == 0 && tid == 0) sd.cache->n_sel = kk_total;
     }
   }
+  trace_pt(p, 10);
   if (!(p.mode & kModeAttend)) return;
-  if (any_select) grid_sync(reinterpret_cast<GridBarrier*>(p.bar), nblocks);  // #6 selection visible
+  if (any_select) grid_sync(gbar, nblocks, bar_gen);  // #6 selection visible
+  trace_pt(p, 11);
 
   // ---- phase 4: split-K sparse flash-decoding partials
   AttView av{};
@@ -790,8 +914,27 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     av.init_end = sd.init_end;
     const uint32_t ie = static_cast<uint32_t>(sd.init_end);
     const uint32_t lb = static_cast<uint32_t>(max(sd.local_begin, sd.init_end));
-    const int lo1 = lower_bound_u32(sd.sel, n_sel, ie);
-    const int hi1 = lower_bound_u32(sd.sel, n_sel, lb < ie ? ie : static_cast<uint32_t>(sd.local_begin));
+    // sorted selection: lower_bound(x) == count(sel < x), counted in parallel
+    const uint32_t lbs = lb < ie ? ie : static_cast<uint32_t>(sd.local_begin);
+    uint32_t cie = 0, clb = 0;
+    for (int base = tid; base < n_sel; base += 4 * blockDim.x) {
+      uint32_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * blockDim.x;
+        v[u] = i < n_sel ? __ldcg(sd.sel + i) : 0xffffffffu;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        cie += v[u] < ie;
+        clb += v[u] < lbs;
+      }
+    }
+    uint32_t tot_ie, tot_lb;
+    block_excl_scan(cie, sm.scratch, &tot_ie);
+    block_excl_scan(clb, sm.scratch, &tot_lb);
+    const int lo1 = static_cast<int>(tot_ie), hi1 = static_cast<int>(tot_lb);
+    trace_pt(p, 17);
     av.lo1 = lo1;
     av.n1 = max(0, hi1 - lo1);
     av.lb2 = static_cast<int>(lb);
@@ -804,32 +947,86 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   const int r0 = min(total_rows, cs * per);
   const int r1 = min(total_rows, r0 + per);
   const bool with_cur = (r0 < r1) && (r1 == total_rows);
-  float* part = p.ws_att + static_cast<size_t>(cta) * H * (p.d + 2);
+  float* part = p.ws_att + static_cast<size_t>(cta) * H * att_stride(p.d);
   attend_partial(p, sd, av, sm, r0, min(r1, av.n_rows), with_cur, part);
-  grid_sync(reinterpret_cast<GridBarrier*>(p.bar), nblocks);  // #7
+  trace_pt(p, 12);
+  grid_sync(gbar, nblocks, bar_gen);  // #7
+  trace_pt(p, 13);
 
   // ---- phase 5: LSE merge (attention.cpp:88-110 semantics)
+  // Per head: weights w_c = exp(m_c - M) for all partials in parallel, then
+  // the d output columns are summed by blockDim/d thread groups over
+  // interleaved partials (independent loads, no serial L2 chain).
   {
-    const int d = p.d, stride = d + 2;
+    const int d = p.d, stride = att_stride(d);
     const int c0 = seq_id * p.ctas_per_seq;
     const int nparts = min(p.ctas_per_seq, (total_rows + per - 1) / per);
+    float* wsm = reinterpret_cast<float*>(sm.hist);        // [nparts] weights (<= 2048)
+    float* red = reinterpret_cast<float*>(sm.ring);        // [groups][d] partial sums
+    float* bred = reinterpret_cast<float*>(sm.scratch);    // block reduction slots
+    const int warp = tid >> 5, lane = tid & 31;
+    const int groups = max(1, static_cast<int>(blockDim.x) / d);
+    // partials are staged in smem chunk by chunk (one parallel load each) and
+    // merged online, so every global read is independent
+    float* stg = reinterpret_cast<float*>(sm.ring + 4096);
+    const int pc = max(1, min(nparts, static_cast<int>((kRingBudget - 4096) / 4) / stride));
     for (int h = cs; h < H; h += p.ctas_per_seq) {
-      for (int t = tid; t < d; t += blockDim.x) {
-        float M = -INFINITY;
-        for (int c = 0; c < nparts; ++c) M = fmaxf(M, __ldcg(p.ws_att + (static_cast<size_t>(c0 + c) * H + h) * stride + d));
-        float L = 0.f, O = 0.f;
-        for (int c = 0; c < nparts; ++c) {
-          const float* ph = p.ws_att + (static_cast<size_t>(c0 + c) * H + h) * stride;
-          const float mc = __ldcg(ph + d);
-          if (mc == -INFINITY) continue;
-          const float w = expf(mc - M);
-          L = fmaf(__ldcg(ph + d + 1), w, L);
-          O = fmaf(__ldcg(ph + t), w, O);
+      const float* base = p.ws_att + (static_cast<size_t>(c0) * H + h) * stride;
+      const size_t cstride = static_cast<size_t>(H) * stride;
+      const int g = tid / d, t = tid - (tid / d) * d;
+      float acc = 0.f, Mrun = -INFINITY, Lrun = 0.f;
+      for (int cb = 0; cb < nparts; cb += pc) {
+        const int n = min(pc, nparts - cb);
+        // one bulk copy per partial record (16-byte padded), one barrier wait
+        if (tid == 0) mbar_arrive_expect_tx(sm.aux, static_cast<uint32_t>(n * stride * 4));
+        __syncthreads();
+        for (int c = tid; c < n; c += blockDim.x)
+          bulk_g2s_nohint(stg + c * stride, base + (cb + c) * cstride, static_cast<uint32_t>(stride * 4), sm.aux);
+        mbar_wait(sm.aux, aux_phase);
+        aux_phase ^= 1u;
+        __syncthreads();
+        float mloc = -INFINITY;
+        for (int c = tid; c < n; c += blockDim.x) mloc = fmaxf(mloc, stg[c * stride + d]);
+        mloc = warp_max(mloc);
+        if (lane == 0) bred[warp] = mloc;
+        __syncthreads();
+        float Mc = lane < kDecodeWarps ? bred[lane] : -INFINITY;
+        Mc = warp_max(Mc);
+        const float Mnew = fmaxf(Mrun, Mc);
+        const float scale = (Mrun == -INFINITY) ? 0.f : expf(Mrun - Mnew);
+        __syncthreads();
+        float lsum = 0.f;
+        for (int c = tid; c < n; c += blockDim.x) {
+          const float mc = stg[c * stride + d];
+          const float w = (mc == -INFINITY) ? 0.f : expf(mc - Mnew);
+          wsm[c] = w;
+          lsum += w * stg[c * stride + d + 1];
         }
-        sd.out[static_cast<size_t>(h) * d + t] = O / L;
+        lsum = warp_sum(lsum);
+        if (lane == 0) bred[warp] = lsum;
+        __syncthreads();
+        float Lc = lane < kDecodeWarps ? bred[lane] : 0.f;
+        Lc = warp_sum(Lc);
+        Lrun = Lrun * scale + Lc;
+        if (g < groups) {
+          float a = 0.f;
+          for (int c = g; c < n; c += groups) a = fmaf(wsm[c], stg[c * stride + t], a);
+          acc = acc * scale + a;
+        }
+        Mrun = Mnew;
+        __syncthreads();
       }
+      if (g < groups) red[g * d + t] = acc;
+      __syncthreads();
+      for (int tt = tid; tt < d; tt += blockDim.x) {
+        float O = 0.f;
+        for (int gg = 0; gg < groups; ++gg) O += red[gg * d + tt];
+        sd.out[static_cast<size_t>(h) * d + tt] = O / Lrun;
+      }
+      __syncthreads();
     }
   }
+  trace_pt(p, 14);
 }
 
 }  // namespace

@@ -59,7 +59,7 @@ TSB_HD inline ScanGeom scan_geom(int H, int H_kv, int d) {
 }
 
 struct SmemLayout {
-  size_t ring, s, keys, hist, headmax, f, scratch, bars, total;
+  size_t ring, s, keys, frames, hist, headmax, f, scratch, bars, total;
 };
 
 TSB_HD inline SmemLayout smem_layout(int H, int row_bytes, int tpc, int s_in_smem) {
@@ -74,6 +74,8 @@ TSB_HD inline SmemLayout smem_layout(int H, int row_bytes, int tpc, int s_in_sme
   if (s_in_smem) o += align_up(static_cast<size_t>(H) * tpc * 4, 128);
   L.keys = o;
   if (s_in_smem) o += align_up(static_cast<size_t>(tpc) * 4, 128);
+  L.frames = o;  // slab row of every candidate of the CTA (TMA producer lookahead)
+  o += align_up(static_cast<size_t>(tpc) * 4, 128);
   L.hist = o;
   o += 2048 * 4;
   L.headmax = o;
@@ -83,10 +85,15 @@ TSB_HD inline SmemLayout smem_layout(int H, int row_bytes, int tpc, int s_in_sme
   L.scratch = o;
   o += 128 * 4;
   L.bars = o;
-  o += 2 * kMaxStages * 8;
+  o += (2 * kMaxStages + 2) * 8;  // full/empty ring barriers + attention barrier
   L.total = align_up(o, 128);
   return L;
 }
+
+// Attention partial (o[d], m, l) record, padded to 16 bytes for bulk copies.
+TSB_HD inline int att_stride(int d) { return (d + 2 + 3) & ~3; }
+// Per-sequence stats rows [h][ctas], padded to 16 bytes for bulk copies.
+TSB_HD inline int stats_stride(int ctas) { return (ctas + 3) & ~3; }
 
 const void* decode_kernel_ptr(int D, int G, bool fast);
 

@@ -76,13 +76,14 @@ struct DecodeParams {
   int s_in_smem;               // S lives in shared memory (else ws_s)
   float* ws_s;                 // [n_ctas][H][tpc] S / exp(S - m) spill
   uint32_t* ws_keys;           // [n_ctas][tpc] selection keys spill
-  float* ws_m;                 // [n_ctas][H] per-CTA head max
-  float* ws_z;                 // [n_ctas][H] per-CTA head sum exp(S - m)
+  float* ws_m;                 // [n_seq][H][stats_stride] per-CTA head max
+  float* ws_z;                 // [n_seq][H][stats_stride] per-CTA head sum exp(S - m)
   uint32_t* ws_hist;           // [n_seq][3][2048] radix histograms
   uint32_t* ws_cnt;            // [n_ctas][2] (n_gt, n_eq)
-  float* ws_att;               // [n_ctas][H][d + 2] attention partials (o, m, l)
+  float* ws_att;               // [n_ctas][H][att_stride(d)] attention partials (o, m, l)
   unsigned int* bar;           // GridBarrier
   int att_rows_per_cta;        // attention rows per CTA per sub-chunk (ring capacity)
+  unsigned long long* trace;   // optional [16] %globaltimer phase stamps (CTA 0)
   SeqDesc seqs[kMaxSeqPerLaunch];  // passed by value in the kernel parameter space
 };
 

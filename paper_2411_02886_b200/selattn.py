@@ -92,7 +92,7 @@ class PagedKvPool:
         self.row_width = self.num_kv_heads * self.head_dim
 
     def __del__(self):
-        if getattr(self, "_owned", False) and self._h:
+        if getattr(self, "_owned", False) and self._h and lib is not None:
             lib.ts_pool_destroy(self._h)
             self._h = None
 
@@ -246,7 +246,7 @@ class Engine:
         self.pool = PagedKvPool(0, 1, 1, 1, _handle=C.c_void_p(lib.ts_engine_pool(h)))
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.ts_engine_destroy(self._h)
             self._h = None
 
@@ -319,6 +319,31 @@ class Engine:
 
     def force_miss(self, seq=0):
         check(lib.ts_engine_force_miss(self._h, seq))
+
+    TRACE_POINTS = ["start", "decision", "scan", "exp_pass", "sync1", "crit", "radix0", "radix1", "radix2",
+                    "counts", "compact", "sync6", "attend", "sync7", "merge"]
+
+    def set_trace(self, enable=True):
+        check(lib.ts_engine_set_trace(self._h, 1 if enable else 0))
+
+    def read_trace(self):
+        """Per-phase device time (us) of the last decode step, from %globaltimer stamps."""
+        st = np.zeros(32, np.uint64)
+        check(lib.ts_engine_read_trace(self._h, st.ctypes.data_as(C.c_void_p), 32))
+        t = st[: len(self.TRACE_POINTS)].astype(np.int64)
+        out, prev = {}, int(t[0])
+        for name, v in zip(self.TRACE_POINTS[1:], t[1:]):
+            if v:
+                out[name] = (int(v) - prev) / 1000.0
+                prev = int(v)
+        out["total"] = (prev - int(t[0])) / 1000.0
+        for i in range(len(self.TRACE_POINTS), 32):  # optional sub-phase stamps, relative to start
+            if st[i]:
+                out[f"t{i}@"] = (int(st[i]) - int(t[0])) / 1000.0
+        return out
+
+    def set_theta(self, theta, seq=0):
+        check(lib.ts_engine_set_theta(self._h, seq, theta))
 
     def sync(self):
         check(lib.ts_engine_sync(self._h))

@@ -1,4 +1,5 @@
-"""Quick decode-step timing (dev tool): Llama-3-8B layer, N tokens, miss and hit steps."""
+"""Quick decode-step timing (dev tool): Llama-3-8B layer, N tokens, miss-only and hit-only streams,
+R steps back to back between CUDA events (host launch overlapped)."""
 import sys
 import time
 
@@ -9,27 +10,39 @@ from paper_2411_02886_b200 import selattn as sa
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
 H, Hkv, d = 32, 8, 128
-eng = sa.Engine(N + 256, k=2048, n_local=512, n_init=128, num_heads=H, num_kv_heads=Hkv, head_dim=d)
+R = 20
+eng = sa.Engine(N + 512, k=2048, n_local=512, n_init=128, num_heads=H, num_kv_heads=Hkv, head_dim=d)
 g = torch.Generator(device="cuda").manual_seed(0)
 K = (torch.randn(N, Hkv * d, device="cuda", generator=g) * 3).to(torch.bfloat16)
 V = torch.randn(N, Hkv * d, device="cuda", generator=g).to(torch.bfloat16)
 eng.append_bf16(K, V)
+del K, V
 q = torch.randn(1, H * d, device="cuda", generator=g)
 kt = torch.randn(1, Hkv * d, device="cuda", generator=g)
 vt = torch.randn(1, Hkv * d, device="cuda", generator=g)
 out = torch.empty(1, H * d, device="cuda")
 st = torch.cuda.Stream()
 eng.set_stream(st.cuda_stream)
-for mode in ("miss", "hit"):
-    ts = []
-    for it in range(12):
-        if mode == "miss":
-            eng.force_miss()
-        torch.cuda.synchronize()
+flush = torch.empty(256 * 1024 * 1024, dtype=torch.int8, device="cuda")
+for mode, theta in (("miss", 2.0), ("hit", -2.0)):
+    eng.set_theta(theta)
+    eng.decode_async(q, kt, vt, out)
+    torch.cuda.synchronize()
+    for rep in range(3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
         e0.record(st)
-        eng.decode_async(q, kt, vt, out)
+        for it in range(R):
+            eng.decode_async(q, kt, vt, out)
         e1.record(st)
+        t1 = time.perf_counter()
         torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1) * 1000)
-    print(mode, "us/step median", np.median(ts[2:]), "min", min(ts[2:]), eng.stats())
+        print(f"{mode}: {e0.elapsed_time(e1) * 1000 / R:.1f} us/step (gpu, back-to-back, L2 warm); host {1e6 * (t1 - t0) / R:.1f} us/launch")
+    print(eng.stats())
+eng.set_trace(True)
+for mode, theta in (("miss", 2.0), ("hit", -2.0)):
+    eng.set_theta(theta)
+    for _ in range(3):
+        eng.decode_async(q, kt, vt, out)
+    torch.cuda.synchronize()
+    print(mode, "phase trace (us):", {k: round(v, 2) for k, v in eng.read_trace().items()})
