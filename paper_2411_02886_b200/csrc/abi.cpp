@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -29,6 +30,12 @@ using tsb::SeqDesc;
 namespace {
 
 thread_local std::string g_err;
+int g_prefetch_stages = [] {
+  const char* e = std::getenv("TS_PREFETCH_STAGES");
+  return e ? std::atoi(e) : 0;
+}();
+const bool g_force_global_s = std::getenv("TS_FORCE_GLOBAL_S") != nullptr && std::getenv("TS_FORCE_GLOBAL_S")[0];
+const int g_debug_flags = std::getenv("TS_DEBUG_FLAGS") ? std::atoi(std::getenv("TS_DEBUG_FLAGS")) : 0;
 std::atomic<uint64_t> g_launches{0};
 
 struct ts_error : std::runtime_error {
@@ -151,7 +158,7 @@ struct Workspace {
 };
 
 struct Plan {
-  int ctas_per_seq, tpc, s_in_smem;
+  int ctas_per_seq, tpc, s_in_smem, ring_bytes;
   size_t smem;
   const void* fn;
   int att_rows;
@@ -169,14 +176,18 @@ Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows) {
   pl.ctas_per_seq = c;
   pl.tpc = std::max(1, (max_T + c - 1) / c);
   const int row_bytes = H_kv * d * 2;
+  const size_t optin = static_cast<size_t>(di.smem_optin);
   tsb::SmemLayout L = tsb::smem_layout(H, row_bytes, pl.tpc, 1);
-  if (L.total <= static_cast<size_t>(di.smem_optin)) {
+  if (L.total <= optin && !g_force_global_s) {
     pl.s_in_smem = 1;
   } else {
     pl.s_in_smem = 0;
     L = tsb::smem_layout(H, row_bytes, pl.tpc, 0);
-    if (L.total > static_cast<size_t>(di.smem_optin)) fail(TS_INVALID_ARGUMENT, "row too wide for the decode kernel");
+    if (L.total > optin) fail(TS_INVALID_ARGUMENT, "row too wide for the decode kernel");
   }
+  // whatever shared memory is left deepens the K ring
+  pl.ring_bytes = static_cast<int>(tsb::kRingBudget + (optin - L.total) / 1024 * 1024);
+  L = tsb::smem_layout(H, row_bytes, pl.tpc, pl.s_in_smem, static_cast<size_t>(pl.ring_bytes));
   pl.smem = L.total;
   const size_t ring = tsb::smem_layout(H, row_bytes, 1, 0).s - tsb::smem_layout(H, row_bytes, 1, 0).ring;
   pl.att_rows = static_cast<int>(ring / (2 * static_cast<size_t>(row_bytes)));
@@ -206,6 +217,9 @@ void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t 
   p.ws_att = ws.att.as<float>();
   p.bar = ws.bar.as<unsigned int>();
   p.att_rows_per_cta = pl.att_rows;
+  p.prefetch_stages = g_prefetch_stages;
+  p.ring_bytes = pl.ring_bytes;
+  p.debug_flags = g_debug_flags;
   ck(cudaFuncSetAttribute(pl.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)),
      "cudaFuncSetAttribute");
   void* args[] = {&p};

@@ -75,6 +75,14 @@ __device__ __forceinline__ void bulk_g2s_nohint(void* dst, const void* src, uint
       : "memory");
 }
 
+// Bulk L2 prefetch (SASS UBLKPF.L2): pulls `bytes` into L2 without touching
+// shared memory, so the scan keeps many more HBM requests in flight than its
+// shared-memory ring alone would allow.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes, uint64_t policy) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src), "r"(bytes), "l"(policy)
+               : "memory");
+}
+
 // ------------------------------------------------------------------- math
 // Packed fp32x2 FMA (sm_100 FFMA2): d = a*b + d, IEEE round-to-nearest.
 __device__ __forceinline__ void ffma2(float2& d, const float2 a, const float2 b) {

@@ -52,7 +52,7 @@ struct Smem {
 };
 
 __device__ __forceinline__ Smem carve(uint8_t* base, const DecodeParams& p) {
-  SmemLayout L = smem_layout(p.H, p.H_kv * p.d * 2, p.tpc, p.s_in_smem);
+  SmemLayout L = smem_layout(p.H, p.H_kv * p.d * 2, p.tpc, p.s_in_smem, p.ring_bytes);
   Smem s;
   s.ring = base + L.ring;
   s.S = reinterpret_cast<float*>(base + L.s);
@@ -201,35 +201,60 @@ __device__ int cache_decision(const SeqDesc& sd, int width, double* scratch_d, d
 }
 
 // --------------------------------------------------------------- the scan
-// Fast path: rows of H_kv*D bf16 are split in parts of 512 elements (one warp
-// each, WPR parts per row); a lane owns 16 contiguous elements of one kv head,
-// read as two 16-byte shared loads in a bank-conflict-free order. Each
-// consumer warp handles two rows per stage and reduce-scatters the 2*G
-// partial dot products over the LPH lanes of a kv head.
+// Fast path (sm_100a tensor cores, mma.sync bf16 -> fp32). The K rows of a
+// stage (16 tokens, padded stride so ldmatrix is bank-conflict free) are the
+// M x K operand; the query, exactly split into three bf16 parts
+// (q = q_hi + q_mid + q_lo, 8+8+8 mantissa bits), is the K x N operand with
+// one column per query head of the GQA group (h = g*H_kv + kvh, the
+// reference's h mod H_kv map, selector.cpp:51). bf16 x bf16 products are
+// exact in fp32, so S = sum_d q*k is formed from exact products with fp32
+// accumulation. Consumer warp c owns kv head c % H_kv and every
+// (16/H_kv)-th stage; one warp task = 16 tokens x one kv head.
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  const uint32_t l = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
+  const uint32_t h = __bfloat16_as_ushort(__float2bfloat16_rn(hi));
+  return l | (h << 16);
+}
+
+// x = hi + mid + lo exactly (bf16 parts, each residual exact in fp32)
+__device__ __forceinline__ void split3(float x, float& hi, float& mid, float& lo) {
+  hi = __bfloat162float(__float2bfloat16_rn(x));
+  const float r1 = x - hi;
+  mid = __bfloat162float(__float2bfloat16_rn(r1));
+  lo = r1 - mid;
+}
+
 template <int D, int G>
 __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& sm, int j0,
                           int nloc, float* Sbuf, int sstride, float* s_out_row0) {
-  constexpr int EPL = G > 4 ? 8 : 16;  // keeps the G*EPL fp32 query slice in registers
-  constexpr int LPH = D / EPL;        // lanes per kv head
-  constexpr int HPW = 32 / LPH;       // kv heads per warp
-  constexpr int NV0 = 2 * G;
-  constexpr int NVp = NV0 <= 2 ? 2 : NV0 <= 4 ? 4 : NV0 <= 8 ? 8 : 16;
-  constexpr int NV = NVp < LPH ? LPH : NVp;
-  constexpr int OWN = NV / LPH > 0 ? NV / LPH : 1;
-  static_assert(NV >= LPH, "reduce-scatter needs at least one value per lane");
-  const int row_bytes = p.H_kv * D * 2;
-  const ScanGeom geom = scan_geom(p.H, p.H_kv, D);
-  const int WPR = geom.wpr;
-  const int slots = kConsumerWarps / WPR;
-  const int R = geom.rows;  // rows per stage
+  constexpr int KC = D / 16;  // k-chunks of 16 along d
+  const int Hkv = p.H_kv;
+  const int row_bytes = Hkv * D * 2;
+  const int rstride = row_bytes + 16;  // padded ring row (ldmatrix conflict-free)
+  const ScanGeom geom = scan_geom(p.H, p.H_kv, D, p.ring_bytes);
+  const int R = geom.rows;  // 16 tokens per stage
   const int kStages = geom.stages;
   const int nit = (nloc + R - 1) / R;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0) {
     // ---------------------------------------------------------- producer
-    // slab rows of all local candidates were staged in smem (sm.frames)
-    // before the scan, so issuing a stage is latency-free.
+    // slab rows of all local candidates were staged in smem (sm.frames), so
+    // issuing a stage is latency-free; rows land at a padded stride.
     const uint64_t pol = policy_evict_first();
     const char* kbase = reinterpret_cast<const char*>(p.k_slab);
     for (int it = 0; it < nit; ++it) {
@@ -240,7 +265,7 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
       if (lane == 0) mbar_arrive_expect_tx(&sm.full[s], static_cast<uint32_t>(nrows * row_bytes));
       __syncwarp();
       if (lane < nrows)
-        bulk_g2s(sm.ring + static_cast<size_t>(s * R + lane) * row_bytes,
+        bulk_g2s(sm.ring + static_cast<size_t>(s * R + lane) * rstride,
                  kbase + static_cast<size_t>(sm.frames[rbase + lane]) * row_bytes, row_bytes, &sm.full[s], pol);
     }
     return;
@@ -248,108 +273,72 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
 
   // ------------------------------------------------------------ consumers
   const int cw = warp - 1;
-  if (cw >= slots * WPR) {
-    // idle consumer warp (slots*WPR < 16): still must arrive on empty
-    for (int it = 0; it < nit; ++it) {
-      const int s = it % kStages;
-      mbar_wait(&sm.full[s], (it / kStages) & 1);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[s]);
+  const int nphase = kDecodeConsumers / Hkv;
+  const int kvh = cw % Hkv, phase = cw / Hkv;
+  // B fragments: lane holds q[head g = lane/4][d = kc*16 + (lane%4)*2 + {0,1,8,9}]
+  uint32_t bq[KC][3][2];
+  {
+    const int g = lane >> 2;
+    const float* qh = sd.q + static_cast<size_t>(g * Hkv + kvh) * D;
+#pragma unroll
+    for (int kc = 0; kc < KC; ++kc) {
+      float v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int dd = kc * 16 + (lane & 3) * 2 + (e & 1) + (e >> 1) * 8;
+        v[e] = g < G ? qh[dd] : 0.f;
+      }
+      float hi[4], mi[4], lo[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) split3(v[e], hi[e], mi[e], lo[e]);
+      bq[kc][0][0] = pack_bf16x2(hi[0], hi[1]);
+      bq[kc][0][1] = pack_bf16x2(hi[2], hi[3]);
+      bq[kc][1][0] = pack_bf16x2(mi[0], mi[1]);
+      bq[kc][1][1] = pack_bf16x2(mi[2], mi[3]);
+      bq[kc][2][0] = pack_bf16x2(lo[0], lo[1]);
+      bq[kc][2][1] = pack_bf16x2(lo[2], lo[3]);
     }
-    return;
   }
-  const int part = cw % WPR, slot = cw / WPR;
-  const int kvh = part * HPW + lane / LPH;
-  // EPL 16: two 16-byte halves read in a bank-conflict-free order
-  const int sw = EPL == 16 ? ((lane >> 2) & 1) : 0;
-  const int eA = (lane % LPH) * EPL + 8 * sw;
-  const int eB = (lane % LPH) * EPL + 8 * (1 - sw);
-  constexpr int NH = EPL / 8;  // 16-byte chunks per lane per row
-  float2 qv[G][NH][4];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const float* qh = sd.q + static_cast<size_t>(g * p.H_kv + kvh) * D;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      qv[g][0][i] = make_float2(qh[eA + 2 * i], qh[eA + 2 * i + 1]);
-      if constexpr (NH == 2) qv[g][NH - 1][i] = make_float2(qh[eB + 2 * i], qh[eB + 2 * i + 1]);
-    }
-  }
-  float runmax[OWN];
-#pragma unroll
-  for (int i = 0; i < OWN; ++i) runmax[i] = -INFINITY;
-  const uint32_t offA = static_cast<uint32_t>(part * 64 * EPL + lane * 2 * EPL + 16 * sw);
-  const uint32_t offB = static_cast<uint32_t>(part * 64 * EPL + lane * 2 * EPL + 16 * (1 - sw));
-
-  for (int it = 0; it < nit; ++it) {
+  // this lane's C fragment: rows lane/4 (+8), columns (heads) 2*(lane%4) + {0,1}
+  const int g0 = (lane & 3) * 2;
+  float runmax0 = -INFINITY, runmax1 = -INFINITY;
+  // ldmatrix row address: matrix lane/8 -> rows +8 for odd, cols +8 for >= 16
+  const uint32_t lrow = static_cast<uint32_t>((lane & 7) + ((lane >> 3) & 1) * 8);
+  const uint32_t lcol = static_cast<uint32_t>((lane >> 4) * 16 + kvh * D * 2);
+  const uint32_t ring_base = smem_u32(sm.ring) + lrow * rstride + lcol;
+  for (int it = phase; it < nit; it += nphase) {
     const int s = it % kStages;
     mbar_wait(&sm.full[s], (it / kStages) & 1);
-    const uint8_t* rows = sm.ring + static_cast<size_t>(s * R + 2 * slot) * row_bytes;
-    float v[NV];
+    float c[4] = {0.f, 0.f, 0.f, 0.f};
+    if (!(p.debug_flags & 1)) {
+      const uint32_t abase = ring_base + static_cast<uint32_t>(s * R * rstride);
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      uint4 X[NH];
-      X[0] = *reinterpret_cast<const uint4*>(rows + r * row_bytes + offA);
-      if constexpr (NH == 2) X[NH - 1] = *reinterpret_cast<const uint4*>(rows + r * row_bytes + offB);
-      float2 kf[NH][4];
-#pragma unroll
-      for (int c = 0; c < NH; ++c) {
-        kf[c][0] = bf16x2_to_f2(X[c].x);
-        kf[c][1] = bf16x2_to_f2(X[c].y);
-        kf[c][2] = bf16x2_to_f2(X[c].z);
-        kf[c][3] = bf16x2_to_f2(X[c].w);
-      }
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int c = 0; c < NH; ++c)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) ffma2(acc, kf[c][i], qv[g][c][i]);
-        v[r * G + g] = acc.x + acc.y;
+      for (int kc = 0; kc < KC; ++kc) {
+        uint32_t a[4];
+        ldmatrix_x4(a, abase + kc * 32);
+        mma_bf16_16816(c, a, bq[kc][0][0], bq[kc][0][1]);
+        mma_bf16_16816(c, a, bq[kc][1][0], bq[kc][1][1]);
+        mma_bf16_16816(c, a, bq[kc][2][0], bq[kc][2][1]);
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[s]);  // ring slot consumed (data now in registers)
+    if (lane == 0) mbar_arrive(&sm.empty[s]);  // operands consumed
+    const int rbase = it * R + (lane >> 2);
 #pragma unroll
-    for (int i = NV0; i < NV; ++i) v[i] = 0.f;
-    // reduce-scatter over the LPH lanes of this kv head
-    int n = NV;
-#pragma unroll
-    for (int o = LPH / 2; o >= 1; o >>= 1) {
-      const bool upper = (lane & o) != 0;
-#pragma unroll
-      for (int i = 0; i < n / 2; ++i) {
-        const float send = upper ? v[i] : v[i + n / 2];
-        const float keep = upper ? v[i + n / 2] : v[i];
-        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-      }
-      n >>= 1;
-    }
-    const int rbase = it * R + 2 * slot;
-#pragma unroll
-    for (int i = 0; i < OWN; ++i) {
-      const int vi = (lane % LPH) * OWN + i;
-      if (vi < NV0) {
-        const int r = vi / G, g = vi - (vi / G) * G;
-        const int row = rbase + r;
-        if (row < nloc) {
-          const int h = g * p.H_kv + kvh;
-          Sbuf[static_cast<size_t>(h) * sstride + row] = v[i];
-          if (s_out_row0) s_out_row0[static_cast<size_t>(h) * sd.n_cand + row] = v[i];
-          runmax[i] = fmaxf(runmax[i], v[i]);
-        }
+    for (int e = 0; e < 4; ++e) {
+      const int g = g0 + (e & 1);
+      const int row = rbase + (e >> 1) * 8;
+      if (g < G && row < nloc) {
+        const int h = g * Hkv + kvh;
+        Sbuf[static_cast<size_t>(h) * sstride + row] = c[e];
+        if (s_out_row0) s_out_row0[static_cast<size_t>(h) * sd.n_cand + row] = c[e];
+        if (e & 1) runmax1 = fmaxf(runmax1, c[e]);
+        else runmax0 = fmaxf(runmax0, c[e]);
       }
     }
   }
-#pragma unroll
-  for (int i = 0; i < OWN; ++i) {
-    const int vi = (lane % LPH) * OWN + i;
-    if (vi < NV0 && runmax[i] > -INFINITY) {
-      const int g = vi % G;
-      atomicMax(&sm.headmax[g * p.H_kv + kvh], float_ord(runmax[i]));
-    }
-  }
+  if (g0 < G && runmax0 > -INFINITY) atomicMax(&sm.headmax[g0 * Hkv + kvh], float_ord(runmax0));
+  if (g0 + 1 < G && runmax1 > -INFINITY) atomicMax(&sm.headmax[(g0 + 1) * Hkv + kvh], float_ord(runmax1));
 }
 
 // Generic path (any H, H_kv, d, page_size): one thread per (head, token),
@@ -585,7 +574,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
 
   if (FAST && tid < kMaxStages) {
     mbar_init(&sm.full[tid], 1);
-    mbar_init(&sm.empty[tid], kConsumerWarps);
+    mbar_init(&sm.empty[tid], p.H_kv);  // the H_kv consumer warps of a stage
   }
   if (tid == 0) {
     mbar_init(sm.att, 1);

@@ -13,47 +13,35 @@
 
 namespace tsb {
 
-constexpr int kDecodeWarps = 16;                 // warp 0: TMA producer, 1..15: consumers
+constexpr int kDecodeConsumers = 16;            // tensor-core consumer warps of the scan
+constexpr int kDecodeWarps = kDecodeConsumers + 1;  // + warp 0: TMA producer
 constexpr int kDecodeThreads = kDecodeWarps * 32;
-constexpr int kConsumerWarps = kDecodeWarps - 1;
-constexpr int kMaxStages = 8;
-constexpr size_t kRingBudget = 96 * 1024;        // K-row ring (also attention staging)
+constexpr int kMaxStages = 16;
+constexpr size_t kRingBudget = 96 * 1024;        // minimum K-row ring (also attention staging)
 
 TSB_HD inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// Fast-path geometry: a lane owns EPL contiguous elements of one kv head,
-// WPR warps cover one K row (H_kv*d bf16), each consumer warp handles two
-// rows per stage, so a stage holds R = 2*floor(15/WPR) rows.
+// Fast-path geometry: stages of 16 tokens (one m16 MMA tile), rows at a
+// 16-byte padded stride; consumer warp c takes kv head c % H_kv of every
+// (16 / H_kv)-th stage.
 struct ScanGeom {
-  int fast;     // 1: templated TMA path, 0: generic path
-  int epl;      // elements per lane (8 or 16)
-  int wpr;      // warps per row
-  int rows;     // R: rows per stage
+  int fast;     // 1: tensor-core TMA path, 0: generic path
+  int rows;     // R: tokens per stage
   int stages;   // ring depth
 };
 
-TSB_HD inline int fast_group_ok(int G) { return G == 1 || G == 2 || G == 4 || G == 7 || G == 8; }
-
-TSB_HD inline ScanGeom scan_geom(int H, int H_kv, int d) {
-  ScanGeom g{0, 0, 0, 0, 0};
+TSB_HD inline ScanGeom scan_geom(int H, int H_kv, int d, size_t ring_bytes = kRingBudget) {
+  ScanGeom g{0, 0, 0};
   if (H_kv <= 0 || H % H_kv != 0) return g;
   const int G = H / H_kv;
-  if (!(d == 128 || d == 64) || !fast_group_ok(G)) return g;
-  const int epl = G > 4 ? 8 : 16;
-  const int E = H_kv * d;
-  if (E % (32 * epl) != 0) return g;
-  const int wpr = E / (32 * epl);
-  if (wpr > kConsumerWarps) return g;
-  const int rows = 2 * (kConsumerWarps / wpr);
-  if (rows > 32) return g;  // one producer lane per row
-  const size_t stage = static_cast<size_t>(rows) * E * 2;
-  int stages = static_cast<int>(kRingBudget / stage);
+  if (!(d == 128 || d == 64) || G > 8 || G < 1) return g;
+  if (H_kv > kDecodeConsumers || kDecodeConsumers % H_kv != 0) return g;
+  const size_t stage = static_cast<size_t>(16) * (H_kv * d * 2 + 16);
+  int stages = static_cast<int>(ring_bytes / stage);
   if (stages > kMaxStages) stages = kMaxStages;
   if (stages < 2) return g;
   g.fast = 1;
-  g.epl = epl;
-  g.wpr = wpr;
-  g.rows = rows;
+  g.rows = 16;
   g.stages = stages;
   return g;
 }
@@ -62,11 +50,12 @@ struct SmemLayout {
   size_t ring, s, keys, frames, hist, headmax, f, scratch, bars, total;
 };
 
-TSB_HD inline SmemLayout smem_layout(int H, int row_bytes, int tpc, int s_in_smem) {
+TSB_HD inline SmemLayout smem_layout(int H, int row_bytes, int tpc, int s_in_smem,
+                                     size_t ring_bytes = kRingBudget) {
   SmemLayout L{};
   size_t o = 0;
   L.ring = o;
-  size_t ring = kRingBudget;
+  size_t ring = ring_bytes;
   const size_t att = static_cast<size_t>(2) * 8 * row_bytes;  // >= 8 attended K+V rows
   if (att > ring) ring = att;
   o += align_up(ring, 128);

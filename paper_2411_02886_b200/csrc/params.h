@@ -83,6 +83,9 @@ struct DecodeParams {
   float* ws_att;               // [n_ctas][H][att_stride(d)] attention partials (o, m, l)
   unsigned int* bar;           // GridBarrier
   int att_rows_per_cta;        // attention rows per CTA per sub-chunk (ring capacity)
+  int prefetch_stages;
+  int ring_bytes;
+  int debug_flags;             // dev experiments: bit0 = scan consumers skip the math              // shared-memory K ring (>= kRingBudget)         // L2 bulk-prefetch distance of the scan, in ring stages
   unsigned long long* trace;   // optional [16] %globaltimer phase stamps (CTA 0)
   SeqDesc seqs[kMaxSeqPerLaunch];  // passed by value in the kernel parameter space
 };
