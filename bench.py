@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Benchmark: TokenSelect decode step (Selection Cache -> paged Q.K scoring ->
+soft vote -> top-k -> sparse paged attention -> KV append) on B200.
+
+Workload (BASELINE.json configs[1]): one Llama-3-8B attention layer (32 query /
+8 KV heads, d=128), 128K-token paged bf16 KV cache, k=2048 selected tokens,
+n_init=128, n_local=512, Selection Cache on at theta=0.9, batch 1. The decode
+query stream is the reference's `rotating` stream (workload.cpp:261-274) at
+consecutive similarity 0.95, rescaled to unit per-element variance, so the cache
+alternates miss / hit like the reference's cache-stats experiment. A step is one
+decode step; metric = mean device microseconds per step over the stream, L2
+flushed before every step (a real model runs 31 other layers in between).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1 (torchrun, one rank per GPU): every rank decodes its own independent
+request (replicas, weak scaling); the step time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_CTX = 131072
+H, H_KV, D = 32, 8, 128
+K_SEL, N_INIT, N_LOCAL, THETA = 2048, 128, 512, 0.9
+SIMILARITY = 0.95
+METRIC = "decode select+sparse-attn µs/step at 128K–1M ctx; HBM GB/s vs peak"
+UNIT = "us/step"
+
+
+# --------------------------------------------------------------- workload
+def rotating_stream(steps: int, seed: int, sim: float = SIMILARITY) -> np.ndarray:
+    """generate_query_stream kRotating (workload.cpp:261-274), x sqrt(H*d)."""
+    dim = H * D
+    g = np.random.default_rng(seed)
+    e1 = g.standard_normal(dim)
+    e1 /= np.linalg.norm(e1)
+    e2 = g.standard_normal(dim)
+    e2 -= (e2 @ e1) * e1
+    e2 /= np.linalg.norm(e2)
+    phi = math.acos(sim)
+    qs = [(math.cos(phi * t) * e1 + math.sin(phi * t) * e2) * math.sqrt(dim) for t in range(steps)]
+    return np.asarray(qs, dtype=np.float32).reshape(steps, 1, dim)
+
+
+def step_kv(steps: int, seed: int):
+    g = np.random.default_rng(seed ^ 0x9E3779B97F4A7C15)
+    k = (g.standard_normal((steps, 1, H_KV * D)) * 3.0).astype(np.float32)
+    v = g.standard_normal((steps, 1, H_KV * D)).astype(np.float32)
+    return k, v
+
+
+def algorithmic_bytes(n_cached: int, miss: bool) -> int:
+    """B_miss = T(R+4) + A(2R+4) + 2R + 2*H*d*4 + 2R;
+    B_hit = A(2R+4) + 2R + 2*H*d*4 + k*4 + 2R (R = H_kv*d*2 bytes per row)."""
+    R = H_KV * D * 2
+    T = n_cached - N_INIT - N_LOCAL
+    A = N_INIT + K_SEL + N_LOCAL
+    common = A * (2 * R + 4) + 2 * R + 2 * H * D * 4 + 2 * R
+    return T * (R + 4) + common if miss else common + K_SEL * 4
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock + clock-event reasons (NVML) during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# -------------------------------------------------------------- CPU side
+def reference_engine(kind: str):
+    from oracle.oracle import Oracle, ref_available  # cpu baseline / reference arm only
+
+    if kind == "reference" and not ref_available():
+        kind = "port"
+    o = Oracle(kind)
+    return o, kind
+
+
+def time_reference(steps: int, warmup: int, seed: int = 1):
+    """The reference's own decode_step (attention.cpp:172-200) on this host,
+    same config and stream shape. Single-threaded by design (README:192-193)."""
+    o, kind = reference_engine("reference")
+    g = np.random.default_rng(seed)
+    eng = o.engine(N_CTX + warmup + steps + 8, k=K_SEL, n_local=N_LOCAL, n_init=N_INIT, chunk_size=512,
+                   theta=THETA, num_heads=H, num_kv_heads=H_KV, head_dim=D, block_size=64)
+    chunk = 16384
+    for s0 in range(0, N_CTX, chunk):
+        kk = (g.standard_normal((chunk, H_KV * D)) * 3.0).astype(np.float32)
+        vv = g.standard_normal((chunk, H_KV * D)).astype(np.float32)
+        eng.append(kk, vv)
+    qs = rotating_stream(warmup + steps, seed)
+    ks, vs = step_kv(warmup + steps, seed)
+    times, hits = [], 0
+    for t in range(warmup + steps):
+        t0 = time.perf_counter()
+        _, hit, _ = eng.decode(qs[t], ks[t], vs[t])
+        dt = time.perf_counter() - t0
+        if t >= warmup:
+            times.append(dt)
+            hits += int(hit)
+    us = 1e6 * sum(times) / len(times)
+    sample = (f"{len(times)} reference decode_step calls at {N_CTX // 1024}K context after {warmup} warm-up, "
+              f"rotating stream sim {SIMILARITY}, theta {THETA}: {len(times) - hits} misses / {hits} hits")
+    return us, kind, sample
+
+
+# ------------------------------------------------------------------ GPU
+def run_gpu(args, rank, world, local_rank):
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    from paper_2411_02886_b200 import selattn as sa
+
+    dev = torch.device("cuda", local_rank)
+    seed = 1234 + rank
+    steps, warmup = args.steps, args.warmup
+    total_steps = warmup + steps
+    eng = sa.Engine(N_CTX + 2 * total_steps + 16, k=K_SEL, n_local=N_LOCAL, n_init=N_INIT, chunk_size=512,
+                    theta=THETA, num_heads=H, num_kv_heads=H_KV, head_dim=D, block_size=64)
+    # synthetic bf16 KV cache of N_CTX tokens, generated on the device
+    gen = torch.Generator(device=dev).manual_seed(seed)
+    chunk = 16384
+    for s0 in range(0, N_CTX, chunk):
+        kk = (torch.randn(chunk, H_KV * D, device=dev, generator=gen) * 3.0).to(torch.bfloat16)
+        vv = torch.randn(chunk, H_KV * D, device=dev, generator=gen).to(torch.bfloat16)
+        eng.append_bf16(kk, vv)
+    del kk, vv
+    qs_h = rotating_stream(total_steps, seed)
+    ks_h, vs_h = step_kv(total_steps, seed)
+    qs = torch.from_numpy(qs_h).to(dev)
+    ks = torch.from_numpy(ks_h).to(dev)
+    vs = torch.from_numpy(vs_h).to(dev)
+    out = torch.empty(1, H * D, device=dev)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.Stream(dev)  # flush, events and the decode kernel share this stream
+    eng.set_stream(stream.cuda_stream)
+
+    # ---- device-resident arm: inputs in HBM, per-step CUDA events
+    def one_pass(n_steps, offset, record):
+        evs, kinds = [], []
+        for t in range(n_steps):
+            i = offset + t
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            n_before = eng.pool.logical_len(eng.sequence())
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            eng.decode_async(qs[i], ks[i], vs[i], out)
+            e1.record(stream)
+            if record:
+                evs.append((e0, e1))
+                kinds.append(n_before)
+        return evs, kinds
+
+    one_pass(warmup, 0, False)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    launches0 = sa.launch_count()
+    st0 = eng.stats()
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize(dev)
+        evs, kinds = one_pass(steps, warmup, True)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    launches = sa.launch_count() - launches0
+    st1 = eng.stats()
+    # per-step hit/miss from the cache trace: replay the decisions via the trace
+    step_us = [e0.elapsed_time(e1) * 1000.0 for e0, e1 in evs]
+    total_us = sum(step_us)
+    hits = st1["hits"] - st0["hits"]
+    lookups = st1["lookups"] - st0["lookups"]
+    # identify miss/hit steps by duration split (hits are ~5x shorter) for the breakdown
+    srt = sorted(step_us)
+    gap = max(range(1, len(srt)), key=lambda i: srt[i] / max(srt[i - 1], 1e-9)) if len(srt) > 1 else 1
+    thr = srt[gap - 1] if hits and hits < len(srt) else None
+    miss_us = [u for u in step_us if thr is None or u > thr]
+    hit_us = [u for u in step_us if thr is not None and u <= thr]
+    if hits == 0:
+        miss_us, hit_us = step_us, []
+    n_ctx_mean = int(np.mean(kinds))
+    alg_bytes = ((lookups - hits) * algorithmic_bytes(n_ctx_mean, True) + hits * algorithmic_bytes(n_ctx_mean, False)) / max(steps, 1)
+
+    # ---- end-to-end arm: host buffers through the public API (H2D + D2H inside)
+    eng.set_stream(None)
+    e2e_steps = min(steps, total_steps)
+    qs_e, ks_e, vs_e = rotating_stream(e2e_steps, seed + 7), *step_kv(e2e_steps, seed + 7)
+    e2e_t = []
+    out_h = np.zeros((1, H * D), np.float32)
+    hit_h = np.zeros(1, np.int32)
+    for t in range(e2e_steps):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        # C-ABI call with host buffers: H2D of q/k/v, the step, D2H of the output + cache flag
+        eng.decode_into(qs_e[t], ks_e[t], vs_e[t], out_h, hit_h)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_us = 1e6 * sum(e2e_t) / len(e2e_t)
+
+    # max over ranks
+    if world > 1:
+        tt = torch.tensor([total_us, e2e_us], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        total_us, e2e_us = tt.tolist()
+    return {
+        "step_us": total_us / steps, "miss_us": statistics.mean(miss_us) if miss_us else None,
+        "hit_us": statistics.mean(hit_us) if hit_us else None, "hits": hits, "lookups": lookups,
+        "alg_bytes": alg_bytes, "launches": launches, "clocks": clk.summary(), "e2e_us": e2e_us,
+        "miss_bytes": algorithmic_bytes(n_ctx_mean, True), "hit_bytes": algorithmic_bytes(n_ctx_mean, False),
+    }
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def traffic_per_launch():
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", args.gpus if args.gpus == 1 else 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    config = {"workload": "Llama-3-8B layer decode, 128K paged bf16 KV, k=2048, Selection Cache theta=0.9 (configs[1])",
+              "context_tokens": N_CTX, "num_heads": H, "num_kv_heads": H_KV, "head_dim": D, "k": K_SEL,
+              "n_init": N_INIT, "n_local": N_LOCAL, "theta": THETA, "batch": 1,
+              "stream": f"rotating, consecutive cos {SIMILARITY}", "parallelism": f"replicas x{max(world, 1)}",
+              "l2": "flushed (512 MB write) before every timed step"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        steps = min(args.steps, 10)
+        us, kind, sample = time_reference(steps, 2)
+        line = {"impl": "reference", "metric": METRIC, "value": round(us, 1), "unit": UNIT, "n_gpus": args.gpus,
+                "steps": steps, "warmup": 2, "ms_per_step": round(us / 1000, 3), "higher_is_better": False,
+                "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic", "config": config,
+                "cpu_baseline": {"value": round(us, 1), "unit": UNIT, "cores": 1, "kind": kind, "sample": sample},
+                "e2e": {"value": round(us, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    if world > 1:
+        import torch
+
+        torch.distributed.init_process_group("nccl")
+    r = run_gpu(args, rank, world, local_rank)
+    peak, peak_kind = peaks()
+    # dominant kernel = the fused decode kernel, one launch per step
+    achieved = r["alg_bytes"] / (r["step_us"] * 1e-6) / 1e9
+    miss_ach = r["miss_bytes"] / (r["miss_us"] * 1e-6) / 1e9 if r["miss_us"] else None
+    traffic = traffic_per_launch()
+    line = {
+        "metric": METRIC, "value": round(r["step_us"], 2), "unit": UNIT, "n_gpus": max(world, 1),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["step_us"] / 1000, 5),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random bf16 KV, rotating query stream)", "config": config,
+        "cache": {"lookups": r["lookups"], "hits": r["hits"]},
+        "miss_step_us": round(r["miss_us"], 2) if r["miss_us"] else None,
+        "hit_step_us": round(r["hit_us"], 2) if r["hit_us"] else None,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
+                     "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                     "algorithmic_bytes_per_launch": int(r["alg_bytes"]),
+                     "miss_step": {"achieved": round(miss_ach, 1) if miss_ach else None,
+                                   "frac": round(miss_ach / peak, 4) if miss_ach else None,
+                                   "algorithmic_bytes": r["miss_bytes"]}},
+        "e2e": {"value": round(r["e2e_us"], 2), "unit": UNIT,
+                "h2d_bytes_per_step": (H * D + 2 * H_KV * D) * 4, "d2h_bytes_per_step": H * D * 4 + 48},
+        "clocks": r["clocks"], "gpu_launches": r["launches"],
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            us, kind, sample = time_reference(4, 1)
+            line["cpu_baseline"] = {"value": round(us, 1), "unit": UNIT, "cores": 1, "kind": kind, "sample": sample}
+        except Exception as e:  # the oracle build is test infrastructure; report, do not fail the bench
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        import torch
+
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -349,6 +349,7 @@ struct ts_engine {
   float* h_v = nullptr;
   float* h_out = nullptr;
   CacheState* h_cache = nullptr;
+  uint32_t* h_sel = nullptr;
   Workspace ws;
   // device phase trace (%globaltimer stamps of CTA 0), when enabled
   DevBuf trace;
@@ -362,6 +363,7 @@ struct ts_engine {
     if (h_v) cudaFreeHost(h_v);
     if (h_out) cudaFreeHost(h_out);
     if (h_cache) cudaFreeHost(h_cache);
+    if (h_sel) cudaFreeHost(h_sel);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
   size_t W() const { return cfg.num_heads * cfg.head_dim; }
@@ -976,8 +978,15 @@ ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const f
     const bool out_dev = is_device_ptr(out);
     float* od = out_dev ? out : e->d_out.as<float>();
     std::vector<int> cap_fail = engine_step(e, qd, kd, vd, od);
+    // every result rides one stream sync: output, cache states and (when
+    // requested) the full selection slots
+    const size_t kk = std::max<size_t>(e->cfg.k, 1);
     if (!out_dev) ck(cudaMemcpyAsync(e->h_out, od, B * W * 4, cudaMemcpyDeviceToHost, st), "D2H");
     ck(cudaMemcpyAsync(e->h_cache, e->cache_state.p, B * sizeof(CacheState), cudaMemcpyDeviceToHost, st), "D2H");
+    if (sel_out) {
+      if (!e->h_sel) ck(cudaMallocHost(&e->h_sel, B * kk * 4), "pinned");
+      ck(cudaMemcpyAsync(e->h_sel, e->sel.p, B * kk * 4, cudaMemcpyDeviceToHost, st), "D2H sel");
+    }
     ck(cudaStreamSynchronize(st), "decode sync");
     if (!out_dev) std::memcpy(out, e->h_out, B * W * 4);
     ts_pool& pool = *e->pool;
@@ -991,8 +1000,7 @@ ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const f
       if (cache_hit) cache_hit[b] = sel_on ? cs.last_hit : 0;
       if (sel_out) {
         const size_t n = sel_on ? static_cast<size_t>(cs.n_sel) : 0;
-        const size_t kk = std::max<size_t>(e->cfg.k, 1);
-        if (n) ck(cudaMemcpy(sel_out + b * kk, e->sl(b), n * 4, cudaMemcpyDeviceToHost), "D2H sel");
+        std::memcpy(sel_out + b * kk, e->h_sel + b * kk, n * 4);
         if (n_sel) n_sel[b] = n;
       }
     }

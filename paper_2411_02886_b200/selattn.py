@@ -312,6 +312,13 @@ class Engine:
             return o, bool(hits[0]), sels[0]
         return o, [bool(h) for h in hits], sels
 
+    def decode_into(self, q, k, v, out, hits=None, sel=None, n_sel=None):
+        """decode_step through the C ABI with caller-owned host buffers (no
+        Python-side conversion): q/k/v/out are C-contiguous float32 numpy
+        arrays; optional hits (int32[B]), sel (uint32[B*k]), n_sel (uint64[B])."""
+        ptr = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)
+        check(lib.ts_engine_decode(self._h, ptr(q), ptr(k), ptr(v), ptr(out), ptr(hits), ptr(sel), ptr(n_sel)))
+
     def decode_async(self, q, k, v, out):
         """Stream-ordered decode on device tensors (no host sync)."""
         check(lib.ts_engine_decode_async(self._h, C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()),
