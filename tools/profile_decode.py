@@ -3,9 +3,11 @@ of the fused decode kernel at N tokens (Llama-3-8B layer). Run under ncu with
 -k regex:decode_kernel -s 2 -c 2."""
 import sys
 
+import os
 import torch
 
-from paper_2411_02886_b200 import selattn as sa
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2411_02886_b200 import selattn as sa  # noqa: E402
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
 H, Hkv, d = 32, 8, 128

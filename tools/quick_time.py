@@ -4,9 +4,11 @@ import sys
 import time
 
 import numpy as np
+import os
 import torch
 
-from paper_2411_02886_b200 import selattn as sa
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2411_02886_b200 import selattn as sa  # noqa: E402
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
 H, Hkv, d = 32, 8, 128
