@@ -37,6 +37,7 @@ int g_prefetch_stages = [] {
 const bool g_force_global_s = std::getenv("TS_FORCE_GLOBAL_S") != nullptr && std::getenv("TS_FORCE_GLOBAL_S")[0];
 const int g_debug_flags = std::getenv("TS_DEBUG_FLAGS") ? std::atoi(std::getenv("TS_DEBUG_FLAGS")) : 0;
 std::atomic<uint64_t> g_launches{0};
+constexpr size_t kTraceSlots = 32 * 1024;  // [cta][32] %globaltimer stamps (<= 1024 CTAs)
 
 struct ts_error : std::runtime_error {
   ts_status code;
@@ -134,11 +135,13 @@ const T* dev_in(const T* p, size_t count, DevBuf& stage, cudaStream_t st) {
   return d;
 }
 
-// Per-launch workspaces of the fused kernel + its grid barrier.
+// Per-launch workspaces of the fused kernel + its grid barrier and the
+// attention-merge arrival counters (both self-resetting across launches).
 struct Workspace {
-  DevBuf s, keys, m, z, hist, cnt, att, bar;
-  bool bar_init = false;
-  void prepare(int n_ctas, int H, int d, int tpc, int s_in_smem, int n_seq, cudaStream_t st) {
+  DevBuf s, keys, m, z, hist, cnt, nsel, sel_tok, sel_crit, att, acnt, bar;
+  size_t acnt_n = 0;
+  unsigned launches = 0;
+  void prepare(int n_ctas, int H, int H_kv, int d, int tpc, int s_in_smem, int n_seq, cudaStream_t st) {
     if (!s_in_smem) {
       s.ensure(static_cast<size_t>(n_ctas) * H * tpc * 4);
       keys.ensure(static_cast<size_t>(n_ctas) * tpc * 4);
@@ -146,25 +149,32 @@ struct Workspace {
     const int cps = n_ctas / n_seq;
     m.ensure(static_cast<size_t>(n_seq) * H * tsb::stats_stride(cps) * 4);
     z.ensure(static_cast<size_t>(n_seq) * H * tsb::stats_stride(cps) * 4);
-    hist.ensure(static_cast<size_t>(n_seq) * 3 * 2048 * 4);
-    cnt.ensure(static_cast<size_t>(n_ctas) * 2 * 4);
+    hist.ensure(static_cast<size_t>(n_seq) * 2 * tsb::kRadixBins * 4);
+    cnt.ensure(static_cast<size_t>(n_ctas) * 4);
+    nsel.ensure(static_cast<size_t>(n_ctas) * 4);
+    sel_tok.ensure(static_cast<size_t>(n_ctas) * tpc * 4);
+    sel_crit.ensure(static_cast<size_t>(n_ctas) * tpc * 4);
     att.ensure(static_cast<size_t>(n_ctas) * H * tsb::att_stride(d) * 4);
-    if (!bar_init) {
-      bar.ensure(64);
-      ck(cudaMemsetAsync(bar.p, 0, 64, st), "memset barrier");
-      bar_init = true;
+    const size_t na = static_cast<size_t>(n_seq) * H_kv;
+    if (na > acnt_n) {
+      acnt.ensure(na * 4);
+      ck(cudaMemsetAsync(acnt.p, 0, na * 4, st), "memset counters");
+      acnt_n = na;
+    }
+    if (!bar.p) {
+      bar.ensure(256);
+      ck(cudaMemsetAsync(bar.p, 0, 256, st), "memset barrier");
     }
   }
 };
 
 struct Plan {
-  int ctas_per_seq, tpc, s_in_smem, ring_bytes;
+  int ctas_per_seq, tpc, s_in_smem, ring_bytes, att_bytes;
   size_t smem;
   const void* fn;
-  int att_rows;
 };
 
-Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows) {
+Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows, bool attend = true) {
   const DeviceInfo& di = device_info();
   Plan pl{};
   const tsb::ScanGeom g = tsb::scan_geom(H, H_kv, d);
@@ -174,7 +184,7 @@ Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows) {
   int c = (base + 63) / 64;
   c = std::max(1, std::min(c, std::max(1, di.num_sms / n_seq)));
   pl.ctas_per_seq = c;
-  pl.tpc = std::max(1, (max_T + c - 1) / c);
+  pl.tpc = static_cast<int>(tsb::align_up(static_cast<size_t>(std::max(1, (max_T + c - 1) / c)), 4));  // 16-B rows
   const int row_bytes = H_kv * d * 2;
   const size_t optin = static_cast<size_t>(di.smem_optin);
   tsb::SmemLayout L = tsb::smem_layout(H, row_bytes, pl.tpc, 1);
@@ -189,22 +199,17 @@ Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows) {
   pl.ring_bytes = static_cast<int>(tsb::kRingBudget + (optin - L.total) / 1024 * 1024);
   L = tsb::smem_layout(H, row_bytes, pl.tpc, pl.s_in_smem, static_cast<size_t>(pl.ring_bytes));
   pl.smem = L.total;
-  const size_t ring = tsb::smem_layout(H, row_bytes, 1, 0).s - tsb::smem_layout(H, row_bytes, 1, 0).ring;
-  pl.att_rows = static_cast<int>(ring / (2 * static_cast<size_t>(row_bytes)));
-  if (H > 16 * 4) fail(TS_INVALID_ARGUMENT, "num_heads > 64 is not supported by the decode kernel");
-  {
-    const size_t qb = tsb::align_up(static_cast<size_t>(H) * d * 4, 128);
-    const size_t rs = static_cast<size_t>(H_kv * d + 8) * 2;
-    if (qb >= tsb::kRingBudget || (tsb::kRingBudget - qb) / (2 * rs) < 1)
-      fail(TS_INVALID_ARGUMENT, "attention rows do not fit the decode kernel's staging ring");
-  }
+  pl.att_bytes = static_cast<int>(L.frames - L.ring);  // ring + S + keys: dead once the selection is out
+  if (attend && H / H_kv > tsb::kAttMaxG)
+    fail(TS_INVALID_ARGUMENT, "more than 8 query heads per KV head is not supported by the decode kernel");
   if (d > 256) fail(TS_INVALID_ARGUMENT, "head_dim > 256 is not supported by the decode kernel");
+  if (pl.ctas_per_seq + 1 > tsb::kMaxPrefix) fail(TS_INVALID_ARGUMENT, "too many CTAs per sequence");
   return pl;
 }
 
 void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t st) {
   const int n_ctas = p.n_seq * pl.ctas_per_seq;
-  ws.prepare(n_ctas, p.H, p.d, pl.tpc, pl.s_in_smem, p.n_seq, st);
+  ws.prepare(n_ctas, p.H, p.H_kv, p.d, pl.tpc, pl.s_in_smem, p.n_seq, st);
   p.ctas_per_seq = pl.ctas_per_seq;
   p.tpc = pl.tpc;
   p.s_in_smem = pl.s_in_smem;
@@ -214,17 +219,23 @@ void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t 
   p.ws_z = ws.z.as<float>();
   p.ws_hist = ws.hist.as<uint32_t>();
   p.ws_cnt = ws.cnt.as<uint32_t>();
+  p.ws_nsel = ws.nsel.as<uint32_t>();
+  p.ws_sel_tok = ws.sel_tok.as<uint32_t>();
+  p.ws_sel_crit = ws.sel_crit.as<float>();
   p.ws_att = ws.att.as<float>();
+  p.ws_acnt = ws.acnt.as<unsigned int>();
   p.bar = ws.bar.as<unsigned int>();
-  p.att_rows_per_cta = pl.att_rows;
+  p.bar_slot = (ws.launches & 1u) ? 32 : 0;  // launches on one workspace are stream-ordered
   p.prefetch_stages = g_prefetch_stages;
   p.ring_bytes = pl.ring_bytes;
+  p.att_bytes = pl.att_bytes;
   p.debug_flags = g_debug_flags;
   ck(cudaFuncSetAttribute(pl.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)),
      "cudaFuncSetAttribute");
   void* args[] = {&p};
   ck(cudaLaunchCooperativeKernel(pl.fn, dim3(n_ctas), dim3(tsb::kDecodeThreads), args, pl.smem, st),
      "decode kernel launch");
+  ws.launches += 1;
   g_launches.fetch_add(1);
 }
 
@@ -446,7 +457,7 @@ size_t run_select(const ts_pool* pool, const ts_pool::Seq* seq, int H, int H_kv,
   sd.sel_crit = static_cast<float*>(b_crit.ensure(kk * 4));
   sd.cache = static_cast<CacheState*>(b_state.ensure(sizeof(CacheState)));
   ck(cudaMemsetAsync(sd.cache, 0, sizeof(CacheState), st), "memset");
-  const Plan pl = make_plan(H, H_kv, d, 1, static_cast<int>(T), 1);
+  const Plan pl = make_plan(H, H_kv, d, 1, static_cast<int>(T), 1, false);
   launch_decode(p, pl, ws, st);
   if (!do_select) {
     ck(cudaStreamSynchronize(st), "sync");
@@ -939,7 +950,7 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
     const Plan pl = make_plan(static_cast<int>(c.num_heads), static_cast<int>(c.num_kv_heads),
                               static_cast<int>(c.head_dim), static_cast<int>(gn), max_T, max_rows);
     p.trace = e->trace_on ? e->trace.as<unsigned long long>() : nullptr;
-    if (p.trace) ck(cudaMemsetAsync(p.trace, 0, 32 * 8, st), "memset trace");
+    if (p.trace) ck(cudaMemsetAsync(p.trace, 0, kTraceSlots * 8, st), "memset trace");
     launch_decode(p, pl, e->ws, st);
     for (size_t i = 0; i < gn; ++i)
       if (!cap_fail[g0 + i]) pool.state(e->seq_ids[g0 + i]).len += 1;
@@ -1030,8 +1041,8 @@ ts_status ts_engine_set_trace(ts_engine* e, int enable) {
   return guarded([&] {
     e->trace_on = enable != 0;
     if (e->trace_on) {
-      e->trace.ensure(32 * 8);
-      ck(cudaMemsetAsync(e->trace.p, 0, 32 * 8, e->stream), "memset");
+      e->trace.ensure(kTraceSlots * 8);
+      ck(cudaMemsetAsync(e->trace.p, 0, kTraceSlots * 8, e->stream), "memset");
       ck(cudaStreamSynchronize(e->stream), "sync");
     }
   });
@@ -1041,7 +1052,7 @@ ts_status ts_engine_read_trace(ts_engine* e, uint64_t* stamps, size_t n) {
   return guarded([&] {
     if (!e->trace.p) fail(TS_INVALID_ARGUMENT, "trace not enabled");
     ck(cudaStreamSynchronize(e->stream), "sync");
-    ck(cudaMemcpy(stamps, e->trace.p, std::min<size_t>(n, 32) * 8, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(stamps, e->trace.p, std::min<size_t>(n, kTraceSlots) * 8, cudaMemcpyDeviceToHost), "D2H");
   });
 }
 
@@ -1153,7 +1164,7 @@ ts_status ts_engine_prefill(ts_engine* e, size_t seq, const float* q, const floa
         sd.cache = pstate;
         sd.sel = psel;
         sd.sel_crit = static_cast<float*>(e->p_crit.ensure(kk * 4));
-        const Plan pl = make_plan(H, Hkv, d, 1, static_cast<int>(T), 1);
+        const Plan pl = make_plan(H, Hkv, d, 1, static_cast<int>(T), 1, false);
         launch_decode(p, pl, e->ws, st);
       }
       // windows (make_windows) -> device merged list

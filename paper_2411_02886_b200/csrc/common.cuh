@@ -83,6 +83,18 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
                : "memory");
 }
 
+// 16-byte global -> shared copy through L2 (LDGSTS.128, bypassing L1), for
+// gathers of many small rows where one bulk-copy descriptor per row would
+// serialise on the TMA unit.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ------------------------------------------------------------------- math
 // Packed fp32x2 FMA (sm_100 FFMA2): d = a*b + d, IEEE round-to-nearest.
 __device__ __forceinline__ void ffma2(float2& d, const float2 a, const float2 b) {
@@ -150,55 +162,47 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 }
 
 // ------------------------------------------------------------ grid barrier
-// Sense-free generation barrier for a cooperative (co-resident) grid.
-// State persists across launches: `count` returns to 0 after every barrier
-// and `gen` only increases.
-struct GridBarrier {
-  unsigned int count;
-  unsigned int gen;
-};
-
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   unsigned int v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ unsigned int atom_add_acqrel_u32(unsigned int* p, unsigned int v) {
   unsigned int old;
   asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
 }
-
-__device__ __forceinline__ unsigned int atom_add_release_u32(unsigned int* p, unsigned int v) {
-  unsigned int old;
-  asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
+__device__ __forceinline__ void red_release_add_u32(unsigned int* p, unsigned int v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Generation barrier. `gen` is read once per launch (grid_sync_begin, before
-// any barrier of the launch can complete) and then tracked locally, so an
-// arrival costs one release-add and the wait one acquire-poll.
-__device__ __forceinline__ unsigned int grid_sync_begin(GridBarrier* bar) {
-  return ld_acquire_u32(&bar->gen);
-}
-
-__device__ __forceinline__ void grid_sync(GridBarrier* bar, unsigned int nblocks, unsigned int& gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int arrived = atom_add_acqrel_u32(&bar->count, 1u);
-    if (arrived == nblocks - 1) {
-      bar->count = 0;
-      st_release_u32(&bar->gen, gen + 1);
-    } else {
-      while (ld_acquire_u32(&bar->gen) == gen) {
+// Counting barrier for a cooperative (co-resident) grid. The counter is
+// zero at launch start (two counters alternate between launches; each launch
+// zeroes the one the next launch uses), so barrier j completes when it
+// reaches (j + 1) * nblocks: an arrival is one fire-and-forget release-add,
+// the wait one acquire-poll -- no "last arrival" hop.
+struct GridSync {
+  unsigned int* ctr;
+  unsigned int nblocks;
+  unsigned int target;
+  __device__ __forceinline__ void sync() {
+    __syncthreads();
+    target += nblocks;
+    if (threadIdx.x == 0) {
+      red_release_add_u32(ctr, 1u);
+      while (ld_acquire_u32(ctr) < target) {
       }
     }
+    __syncthreads();
   }
-  ++gen;
-  __syncthreads();
+};
+
+// exp(x) on the SFU (ex2.approx): max relative error ~2^-21 for |x| < 100,
+// well inside the 1e-4 criticality tolerance.
+__device__ __forceinline__ float fast_exp(float x) {
+  float y;
+  asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(x * 1.4426950408889634f));
+  return y;
 }
 
 }  // namespace tsb

@@ -34,21 +34,21 @@ namespace tsb {
 
 namespace {
 
-constexpr int kBins = 2048;
 
 struct Smem {
   uint8_t* ring;
   float* S;        // [H][tpc] (when on chip)
   uint32_t* keys;  // [tpc]
-  uint32_t* hist;  // [kBins]
+  uint32_t* hist;  // [kRadixBins]
+  int* prefix;     // [kMaxPrefix] per-CTA selection offsets of this sequence
   int* headmax;    // [H] ordered-int max
   float* f;        // [H]
-  uint32_t* scratch;  // [64]
+  uint32_t* scratch;  // [256]
   int32_t* frames; // [tpc] slab row of each local candidate
   uint64_t* full;  // [kMaxStages]
   uint64_t* empty; // [kMaxStages]
-  uint64_t* att;   // attention staging barrier
-  uint64_t* aux;   // bulk staging barrier (stats, partials)
+  uint64_t* att;   // [2] attention staging barriers (double buffer)
+  uint64_t* aux;   // bulk staging barrier (stats)
 };
 
 __device__ __forceinline__ Smem carve(uint8_t* base, const DecodeParams& p) {
@@ -58,13 +58,14 @@ __device__ __forceinline__ Smem carve(uint8_t* base, const DecodeParams& p) {
   s.S = reinterpret_cast<float*>(base + L.s);
   s.keys = reinterpret_cast<uint32_t*>(base + L.keys);
   s.hist = reinterpret_cast<uint32_t*>(base + L.hist);
+  s.prefix = reinterpret_cast<int*>(base + L.prefix);
   s.headmax = reinterpret_cast<int*>(base + L.headmax);
   s.f = reinterpret_cast<float*>(base + L.f);
   s.scratch = reinterpret_cast<uint32_t*>(base + L.scratch);
   s.full = reinterpret_cast<uint64_t*>(base + L.bars);
   s.empty = s.full + kMaxStages;
   s.att = s.full + 2 * kMaxStages;
-  s.aux = s.att + 1;
+  s.aux = s.att + 2;
   s.frames = reinterpret_cast<int32_t*>(base + L.frames);
   return s;
 }
@@ -78,12 +79,13 @@ __device__ __forceinline__ size_t row_index(const SeqDesc& sd, uint32_t tok, int
   return static_cast<size_t>(sd.page_table[tok / page_size]) * page_size + tok % page_size;
 }
 
-// Phase trace: CTA 0 records %globaltimer at phase boundaries when enabled.
+// Phase trace: thread 0 of every CTA records %globaltimer at the phase
+// boundaries into trace[cta][32] when enabled.
 __device__ __forceinline__ void trace_pt(const DecodeParams& p, int i) {
-  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (p.trace && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.trace[i] = t;
+    p.trace[blockIdx.x * 32 + i] = t;
   }
 }
 
@@ -107,7 +109,7 @@ __device__ uint32_t block_excl_scan(uint32_t v, uint32_t* scratch, uint32_t* tot
   return r;
 }
 
-// Finds, in a histogram whose bins are ordered by key, the bin b such that
+// Finds, in a global histogram whose bins are ordered by key, the bin b such that
 // count(bins > b) < kk <= count(bins >= b). Returns b and count(bins > b).
 // All threads call; every CTA computes the same answer from the same data.
 __device__ void find_bin(const uint32_t* gh, int nbins, uint32_t kk, uint32_t* scratch,
@@ -362,199 +364,382 @@ __device__ void scan_generic(const DecodeParams& p, const SeqDesc& sd, const Sme
   }
 }
 
-// ---------------------------------------------------------- attention rows
-struct AttView {
-  int n_rows;      // cached attended rows (excl. current)
-  int init_end, lo1, n1, lb2;
-};
-
-__device__ __forceinline__ int lower_bound_u32(const uint32_t* a, int n, uint32_t x) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (a[mid] < x) lo = mid + 1;
-    else hi = mid;
+// ------------------------------------------------------------ radix select
+// Local 12-bit digit histogram of this CTA's keys (optionally only keys whose
+// bits above `pshift` equal `prefix`), aggregated per warp with match.any so a
+// crowded bin costs one shared atomic per warp, then merged into the
+// sequence's global histogram `gh`. All threads call.
+__device__ void radix_hist(const uint32_t* keys, int nloc, int shift, int pshift, uint32_t prefix,
+                           uint32_t* hist, uint32_t* gh) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < kRadixBins; i += blockDim.x) hist[i] = 0u;
+  __syncthreads();
+  for (int base = 0; base < nloc; base += blockDim.x) {
+    const int jl = base + tid;
+    uint32_t key = 0;
+    bool act = false;
+    if (jl < nloc) {
+      key = keys[jl];
+      act = pshift >= 32 || (key >> pshift) == prefix;
+    }
+    const unsigned am = __ballot_sync(0xffffffffu, act);
+    if (act) {
+      const uint32_t bin = (key >> shift) & (kRadixBins - 1);
+      const unsigned peers = __match_any_sync(am, bin);
+      if (lane == __ffs(peers) - 1) atomicAdd(&hist[bin], static_cast<uint32_t>(__popc(peers)));
+    }
   }
-  return lo;
+  __syncthreads();
+  for (int i = tid; i < kRadixBins; i += blockDim.x) {
+    const uint32_t c = hist[i];
+    if (c) atomicAdd(gh + i, c);
+  }
 }
 
-__device__ __forceinline__ uint32_t att_token(const SeqDesc& sd, const AttView& v, int i) {
+// ---------------------------------------------------------- attention rows
+// The attended rows of one sequence, in merged (ascending) order:
+//   [0, init_end) ++ selection part ++ [lb, n_cached) ++ current token
+// (make_windows + merged(), attention.cpp:21-52). The selection part is the
+// cached SelectionResult filtered to [init_end, lb) on a hit (sel[lo1 + i]),
+// or this step's fresh selection (already inside that range) held as
+// per-CTA ascending lists located through the CTA prefix offsets.
+struct AttView {
+  int n_rows;      // cached attended rows (excl. current)
+  int init_end, n1, lb;
+  int lo1;         // hit: offset of the filtered range in sel[]
+  int fresh;       // 1: selection part = per-CTA lists of this launch
+  int ncta;        // fresh: CTAs of the sequence (prefix has ncta + 1 entries)
+  int cta0;        // fresh: first CTA of the sequence
+};
+
+__device__ __forceinline__ uint32_t att_token(const DecodeParams& p, const SeqDesc& sd, const AttView& v,
+                                              const int* prefix, int i) {
   if (sd.att_list) return sd.att_list[i];
   if (i < v.init_end) return static_cast<uint32_t>(i);
   i -= v.init_end;
-  if (i < v.n1) return sd.sel[v.lo1 + i];
+  if (i < v.n1) {
+    if (!v.fresh) return __ldcg(sd.sel + v.lo1 + i);
+    // largest c with prefix[c] <= i
+    int lo = 0, hi = v.ncta - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (prefix[mid] <= i) lo = mid;
+      else hi = mid - 1;
+    }
+    return __ldcg(p.ws_sel_tok + static_cast<size_t>(v.cta0 + lo) * p.tpc + (i - prefix[lo]));
+  }
   i -= v.n1;
-  return static_cast<uint32_t>(v.lb2 + i);
+  return static_cast<uint32_t>(v.lb + i);
 }
 
-// split-K flash-decoding partial over rows [r0, r1) of the merged window
-// list, plus the current token when `with_cur`; writes (o[d], m, l) per head.
-// Rows are staged in smem (bulk copies, padded stride); per head a warp
-// scores all staged rows at once (lane = row, q broadcast from smem), then
-// does one online-softmax update and the P.V accumulation (lane = d slice).
-__device__ void attend_partial(const DecodeParams& p, const SeqDesc& sd, const AttView& av,
-                               const Smem& sm, int r0, int r1, bool with_cur, float* part) {
-  const int H = p.H, Hkv = p.H_kv, d = p.d;
-  const int row_elems = Hkv * d;
-  const int row_bytes = row_elems * 2;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kMaxDL = 8;            // d <= 256
-  constexpr int kMaxHeadsPerWarp = 4;  // H <= 64
-  const bool vec = (row_bytes % 16) == 0 && (d % 8) == 0;
-  const int rstride = vec ? row_elems + 8 : row_elems;  // bf16 elements; +16 B breaks bank aliasing
-  const bool d128 = vec && d == 128;                   // vectorised P.V layout (see below)
-  // carve the ring: q (fp32, H*d) then K rows then V rows
-  float* qs = reinterpret_cast<float*>(sm.ring);
-  uint16_t* kbuf = reinterpret_cast<uint16_t*>(sm.ring + align_up(static_cast<size_t>(H) * d * 4, 128));
-  const size_t avail = kRingBudget - align_up(static_cast<size_t>(H) * d * 4, 128);
-  int cap = static_cast<int>(avail / (2 * static_cast<size_t>(rstride) * 2));
-  if (cap > 32) cap = 32;
-  uint16_t* vbuf = kbuf + static_cast<size_t>(cap) * rstride;
-  for (int base = threadIdx.x; base < H * d; base += 8 * blockDim.x) {
-    float v[8];
+// Sum over the 32 lanes of P per-lane values v[0..P) (P a power of two <= 8)
+// by recursive halving: after it, lane L holds the total of value index
+// idx(L) = sum_s bit(L, 4 - s) * (P >> (s + 1)) -- log2(P) + 5 - log2(P)
+// shuffles per P values instead of 5 per value.
+template <int P>
+__device__ __forceinline__ float transpose_reduce(float (&v)[8], int lane, int* idx) {
+  int id = 0;
+  int size = P;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = base + u * blockDim.x;
-      v[u] = i < H * d ? __ldg(sd.q + i) : 0.f;
-    }
+  for (int o = 16; o >= 1; o >>= 1) {
+    if (size > 1) {
+      const int half = size >> 1;
+      const bool hi = (lane & o) != 0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = base + u * blockDim.x;
-      if (i < H * d) qs[i] = v[u];
-    }
-  }
-  float m_run[kMaxHeadsPerWarp], l_run[kMaxHeadsPerWarp], o_run[kMaxHeadsPerWarp][kMaxDL];
-#pragma unroll
-  for (int hs = 0; hs < kMaxHeadsPerWarp; ++hs) {
-    m_run[hs] = -INFINITY;
-    l_run[hs] = 0.f;
-#pragma unroll
-    for (int i = 0; i < kMaxDL; ++i) o_run[hs][i] = 0.f;
-  }
-  uint32_t att_phase = 0;
-  for (int c0 = r0; c0 < r1; c0 += cap) {
-    const int nr = min(cap, r1 - c0);
-    __syncthreads();  // previous sub-chunk consumed; qs visible
-    if (vec) {
-      if (threadIdx.x == 0) mbar_arrive_expect_tx(sm.att, static_cast<uint32_t>(nr * 2 * row_bytes));
-      __syncthreads();
-      if (static_cast<int>(threadIdx.x) < nr) {
-        const int r = threadIdx.x;
-        const size_t ri = row_index(sd, att_token(sd, av, c0 + r), p.page_size);
-        bulk_g2s_nohint(kbuf + static_cast<size_t>(r) * rstride, p.k_slab + ri * row_elems, row_bytes, sm.att);
-        bulk_g2s_nohint(vbuf + static_cast<size_t>(r) * rstride, p.v_slab + ri * row_elems, row_bytes, sm.att);
-      }
-      mbar_wait(sm.att, att_phase);
-      att_phase ^= 1u;
+      for (int i = 0; i < 4; ++i)
+        if (i < half) {
+          const float keep = hi ? v[i + half] : v[i];
+          const float send = hi ? v[i] : v[i + half];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      if (hi) id += half;
+      size = half;
     } else {
-      for (int idx = threadIdx.x; idx < nr * row_elems * 2; idx += blockDim.x) {
-        const int which = idx / (nr * row_elems);
-        const int rem = idx - which * nr * row_elems;
-        const int r = rem / row_elems, c = rem - (rem / row_elems) * row_elems;
-        const uint32_t tok = att_token(sd, av, c0 + r);
-        const uint16_t* src = (which ? p.v_slab : p.k_slab) + row_index(sd, tok, p.page_size) * row_elems;
-        ((which ? vbuf : kbuf) + static_cast<size_t>(r) * rstride)[c] = src[c];
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+    }
+  }
+  *idx = id;
+  return v[0];
+}
+
+// Split-K flash-decoding partial of the G query heads {g + m*H_kv} that share
+// KV head g (the reference's h mod H_kv map, attention.cpp:78) over rows
+// [r0, r1) of the merged list, plus the current token (fp32 k_t / v_t) when
+// `with_cur`. Slab rows of up to kAttIdx rows are resolved first (one
+// parallel pass over the page table), then only this KV head's d-wide K/V
+// slices are gathered with 16-byte cp.async into a double buffer of `cap`
+// rows. Scores: one warp per row, lane = d/32 contiguous elements, q held in
+// registers, FFMA2 + transposed shuffle reduction. P.V: (row group, d pair)
+// threads with FFMA2. Writes (o[d], m, l) per head (attention.cpp:88-110
+// semantics, fp32). DT/GT = 0: runtime shapes (any d, G <= 8).
+constexpr int kAttIdx = 1024;
+
+template <int DT, int GT>
+__device__ void attend_group(const DecodeParams& p, const SeqDesc& sd, const AttView& av, const Smem& sm,
+                             int g, int r0, int r1, bool with_cur, float* part) {
+  constexpr bool kFast = DT > 0;
+  const int H_kv = p.H_kv;
+  const int d = kFast ? DT : p.d;
+  const int G = kFast ? GT : p.H / p.H_kv;
+  constexpr int E = kFast ? DT / 32 : 1;           // elements per lane (fast path)
+  constexpr int P = GT <= 1 ? 1 : GT <= 2 ? 2 : GT <= 4 ? 4 : 8;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nwarps = blockDim.x >> 5;
+  const bool even = (d & 1) == 0;
+  const bool vec = (d % 8) == 0;          // 16-byte gathers
+  const int ew = even ? 2 : 1;            // elements per P.V thread
+  const int npt = d / ew;                 // P.V threads per row group
+  const int RG = max(1, min(static_cast<int>(blockDim.x) / npt, 16));
+  const int row_elems = H_kv * d;
+  const size_t slice = static_cast<size_t>(d) * 2;  // bytes of one K (or V) slice
+  // ---- carve the staging area (ring + the dead S/keys region)
+  uint8_t* base = sm.ring;
+  float* qs = reinterpret_cast<float*>(base);                       // [G][d]
+  size_t o = align_up(static_cast<size_t>(G) * d * 4, 128);
+  float* ck = reinterpret_cast<float*>(base + o);                   // [d] current K (fp32)
+  float* cv = ck + d;                                               // [d] current V
+  o += align_up(static_cast<size_t>(2) * d * 4, 128);
+  float* red = reinterpret_cast<float*>(base + o);                  // [RG][G][d]
+  o += align_up(static_cast<size_t>(RG) * G * d * 4, 128);
+  float* stat = reinterpret_cast<float*>(base + o);                 // [8][4] m_run, l_run, corr
+  o += 128;
+  int32_t* ridx = reinterpret_cast<int32_t*>(base + o);             // [kAttIdx] slab rows
+  o += static_cast<size_t>(kAttIdx) * 4;
+  const size_t rest = static_cast<size_t>(p.att_bytes) > o ? static_cast<size_t>(p.att_bytes) - o : 0;
+  // per row: 2 buffers x (K + V) slices + 8 probs
+  int cap = static_cast<int>(rest / (4 * slice + 32 + 64));
+  cap = max(1, min(cap, kAttMaxRows));
+  float* probs = reinterpret_cast<float*>(base + o);                // [cap + 1][8]
+  o += align_up(static_cast<size_t>(cap + 1) * 32, 128);
+  uint16_t* kb[2];
+  uint16_t* vb[2];
+  for (int b = 0; b < 2; ++b) {
+    kb[b] = reinterpret_cast<uint16_t*>(base + o);
+    o += align_up(static_cast<size_t>(cap) * slice, 128);
+    vb[b] = reinterpret_cast<uint16_t*>(base + o);
+    o += align_up(static_cast<size_t>(cap) * slice, 128);
+  }
+  // ---- q heads of this KV head, current token K/V slices, running stats
+  for (int i = tid; i < G * d; i += blockDim.x) {
+    const int m = i / d, t = i - (i / d) * d;
+    qs[i] = __ldg(sd.q + static_cast<size_t>(g + m * H_kv) * d + t);
+  }
+  if (with_cur)
+    for (int t = tid; t < d; t += blockDim.x) {
+      ck[t] = __ldg(sd.k_new + static_cast<size_t>(g) * d + t);
+      cv[t] = __ldg(sd.v_new + static_cast<size_t>(g) * d + t);
+    }
+  if (tid < 8) {
+    stat[tid * 4 + 0] = -INFINITY;
+    stat[tid * 4 + 1] = 0.f;
+    stat[tid * 4 + 2] = 1.f;
+  }
+  float2 acc[kAttMaxG];
+#pragma unroll
+  for (int m = 0; m < kAttMaxG; ++m) acc[m] = make_float2(0.f, 0.f);
+  const int rg = tid / npt, pi = tid - (tid / npt) * npt;
+  const int nrows = max(0, r1 - r0);
+  const int cpr = static_cast<int>(slice / 16);  // 16-byte chunks per slice
+  // gather the slices of rows [c0, c0 + nr) of the current index window into buffer b
+  auto issue = [&](int c0, int nr, int b) {
+    if (vec) {
+      for (int idx = tid; idx < nr * cpr; idx += blockDim.x) {
+        const int r = idx / cpr, q = idx - (idx / cpr) * cpr;
+        const int64_t off = static_cast<int64_t>(ridx[c0 + r]) * row_elems + static_cast<int64_t>(g) * d + q * 8;
+        cp_async16(kb[b] + static_cast<size_t>(r) * d + q * 8, p.k_slab + off);
+        cp_async16(vb[b] + static_cast<size_t>(r) * d + q * 8, p.v_slab + off);
+      }
+    } else {
+      for (int idx = tid; idx < nr * d; idx += blockDim.x) {
+        const int r = idx / d, t = idx - (idx / d) * d;
+        const int64_t off = static_cast<int64_t>(ridx[c0 + r]) * row_elems + static_cast<int64_t>(g) * d + t;
+        kb[b][static_cast<size_t>(r) * d + t] = p.k_slab[off];
+        vb[b][static_cast<size_t>(r) * d + t] = p.v_slab[off];
+      }
+    }
+    cp_async_commit();
+  };
+  __syncthreads();  // qs / ck / stat visible
+  // q slice of this lane in registers (fast path)
+  float qr[kFast ? GT : 1][E];
+  if constexpr (kFast) {
+#pragma unroll
+    for (int m = 0; m < GT; ++m)
+#pragma unroll
+      for (int e = 0; e < E; ++e) qr[m][e] = qs[m * DT + lane * E + e];
+  }
+  int w0 = 0;  // index window [w0, w0 + nw) of rows whose slab rows are in ridx
+  int sub = 0;
+  for (;;) {
+    const int nw = min(kAttIdx, nrows - w0);
+    for (int r = tid; r < nw; r += blockDim.x)
+      ridx[r] = static_cast<int32_t>(row_index(sd, att_token(p, sd, av, sm.prefix, r0 + w0 + r), p.page_size));
+    __syncthreads();
+    const bool last_w = w0 + nw >= nrows;
+    const int nsub = max(1, (nw + cap - 1) / cap);
+    issue(0, min(cap, nw), sub & 1);
+    for (int c = 0; c < nsub; ++c, ++sub) {
+      const int c0 = c * cap;
+      const int nr = max(0, min(cap, nw - c0));
+      const bool last = last_w && c == nsub - 1;
+      const int nrt = nr + ((last && with_cur) ? 1 : 0);  // + current token row
+      if (c + 1 < nsub) {
+        issue(c0 + cap, min(cap, nw - c0 - cap), (sub + 1) & 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
       }
       __syncthreads();
-    }
+      const uint16_t* K = kb[sub & 1];
+      const uint16_t* V = vb[sub & 1];
+      // ---- scores s[r][m] = q_m . k_r / sqrt(d)
+      for (int r = warp; r < nrt; r += nwarps) {
+        if constexpr (kFast) {
+          float kx[E];
+          if (r < nr) {
+            const uint16_t* kr = K + static_cast<size_t>(r) * DT + lane * E;
+            if constexpr (E == 4) {
+              const uint2 u = *reinterpret_cast<const uint2*>(kr);
+              const float2 a = bf16x2_to_f2(u.x), b = bf16x2_to_f2(u.y);
+              kx[0] = a.x; kx[1] = a.y; kx[2] = b.x; kx[3] = b.y;
+            } else {
+              const float2 a = bf16x2_to_f2(*reinterpret_cast<const uint32_t*>(kr));
+              kx[0] = a.x; kx[1] = a.y;
+            }
+          } else {
 #pragma unroll
-    for (int hs = 0; hs < kMaxHeadsPerWarp; ++hs) {
-      const int h = warp + hs * kDecodeWarps;
-      if (h >= H) break;
-      const int kvo = (h % Hkv) * d;
-      const float* qh = qs + static_cast<size_t>(h) * d;
-      // scores: lane r owns row r
-      float s = -INFINITY;
-      if (lane < nr) {
-        const uint16_t* kr = kbuf + static_cast<size_t>(lane) * rstride + kvo;
-        float2 acc = make_float2(0.f, 0.f);
-        if (vec) {
-          for (int t = 0; t < d; t += 8) {
-            const uint4 kx = *reinterpret_cast<const uint4*>(kr + t);
-            const float4 qa = *reinterpret_cast<const float4*>(qh + t);
-            const float4 qb = *reinterpret_cast<const float4*>(qh + t + 4);
-            ffma2(acc, bf16x2_to_f2(kx.x), make_float2(qa.x, qa.y));
-            ffma2(acc, bf16x2_to_f2(kx.y), make_float2(qa.z, qa.w));
-            ffma2(acc, bf16x2_to_f2(kx.z), make_float2(qb.x, qb.y));
-            ffma2(acc, bf16x2_to_f2(kx.w), make_float2(qb.z, qb.w));
+            for (int e = 0; e < E; ++e) kx[e] = ck[lane * E + e];
           }
+          float v[8];
+#pragma unroll
+          for (int m = 0; m < 8; ++m) v[m] = 0.f;
+#pragma unroll
+          for (int m = 0; m < GT; ++m) {
+            float2 a2 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int e = 0; e < E; e += 2) ffma2(a2, make_float2(qr[m][e], qr[m][e + 1]), make_float2(kx[e], kx[e + 1]));
+            v[m] = a2.x + a2.y;
+          }
+          int hid;
+          const float s = transpose_reduce<P>(v, lane, &hid);
+          const int lowmask = (32 / P) - 1;  // lanes that share one head total
+          if ((lane & lowmask) == 0 && hid < GT) probs[r * 8 + hid] = s * p.attn_scale;
         } else {
-          for (int t = 0; t < d; ++t) acc.x = fmaf(qh[t], bf16_bits_to_f(kr[t]), acc.x);
-        }
-        s = (acc.x + acc.y) * p.attn_scale;
-      }
-      const float mt = warp_max(s);
-      const float m_new = fmaxf(m_run[hs], mt);
-      const float corr = expf(m_run[hs] - m_new);
-      const float w = lane < nr ? expf(s - m_new) : 0.f;
-      l_run[hs] = l_run[hs] * corr + warp_sum(w);
+          float a[kAttMaxG];
 #pragma unroll
-      for (int i = 0; i < kMaxDL; ++i) o_run[hs][i] *= corr;
-      if (d == 128 && vec) {
-        // lane owns d-elements [4*lane, 4*lane+4): one 8-byte smem load per row
-        for (int r = 0; r < nr; ++r) {
-          const float wr = __shfl_sync(0xffffffffu, w, r);
-          const uint2 vv = *reinterpret_cast<const uint2*>(vbuf + static_cast<size_t>(r) * rstride + kvo + 4 * lane);
-          const float2 v01 = bf16x2_to_f2(vv.x), v23 = bf16x2_to_f2(vv.y);
-          o_run[hs][0] = fmaf(wr, v01.x, o_run[hs][0]);
-          o_run[hs][1] = fmaf(wr, v01.y, o_run[hs][1]);
-          o_run[hs][2] = fmaf(wr, v23.x, o_run[hs][2]);
-          o_run[hs][3] = fmaf(wr, v23.y, o_run[hs][3]);
-        }
-      } else {
-        for (int r = 0; r < nr; ++r) {
-          const float wr = __shfl_sync(0xffffffffu, w, r);
-          const uint16_t* vr = vbuf + static_cast<size_t>(r) * rstride + kvo;
+          for (int m = 0; m < kAttMaxG; ++m) a[m] = 0.f;
+          for (int t = lane; t < d; t += 32) {
+            const float kk = r < nr ? bf16_bits_to_f(K[static_cast<size_t>(r) * d + t]) : ck[t];
 #pragma unroll
-          for (int i = 0; i < kMaxDL; ++i) {
-            const int t = lane + 32 * i;
-            if (t < d) o_run[hs][i] = fmaf(wr, bf16_bits_to_f(vr[t]), o_run[hs][i]);
+            for (int m = 0; m < kAttMaxG; ++m)
+              if (m < G) a[m] = fmaf(qs[m * d + t], kk, a[m]);
           }
+#pragma unroll
+          for (int m = 0; m < kAttMaxG; ++m)
+            if (m < G) {
+              const float s = warp_sum(a[m]);
+              if (lane == 0) probs[r * 8 + m] = s * p.attn_scale;
+            }
         }
       }
-      m_run[hs] = m_new;
-    }
-  }
-  if (with_cur) {
-#pragma unroll
-    for (int hs = 0; hs < kMaxHeadsPerWarp; ++hs) {
-      const int h = warp + hs * kDecodeWarps;
-      if (h >= H) break;
-      const int kvo = (h % Hkv) * d;
-      float part_dot = 0.f;
-#pragma unroll
-      for (int i = 0; i < kMaxDL; ++i) {
-        const int t = lane + 32 * i;
-        if (t < d) part_dot = fmaf(sd.q[static_cast<size_t>(h) * d + t], sd.k_new[kvo + t], part_dot);
+      __syncthreads();
+      // ---- online softmax per head (warp m owns head m)
+      for (int m = warp; m < G; m += nwarps) {
+        float mx = -INFINITY;
+        for (int r = lane; r < nrt; r += 32) mx = fmaxf(mx, probs[r * 8 + m]);
+        mx = warp_max(mx);
+        const float m_old = stat[m * 4 + 0];
+        const float m_new = fmaxf(m_old, mx);
+        float l = 0.f;
+        for (int r = lane; r < nrt; r += 32) {
+          const float w = m_new == -INFINITY ? 0.f : expf(probs[r * 8 + m] - m_new);
+          probs[r * 8 + m] = w;
+          l += w;
+        }
+        l = warp_sum(l);
+        if (lane == 0) {
+          const float corr = m_old == -INFINITY ? 0.f : expf(m_old - m_new);
+          stat[m * 4 + 0] = m_new;
+          stat[m * 4 + 1] = stat[m * 4 + 1] * corr + l;
+          stat[m * 4 + 2] = corr;
+        }
       }
-      const float s = warp_sum(part_dot) * p.attn_scale;
-      const float m_new = fmaxf(m_run[hs], s);
-      const float corr = expf(m_run[hs] - m_new);
-      const float w = expf(s - m_new);
-      l_run[hs] = l_run[hs] * corr + w;
+      __syncthreads();
+      // ---- P.V: thread (row group rg, element pair pi) over rows rg, rg + RG, ...
+      if (rg < RG) {
 #pragma unroll
-      for (int i = 0; i < kMaxDL; ++i) {
-        const int t = d128 ? 4 * lane + i : lane + 32 * i;
-        if ((d128 ? i < 4 : t < d)) o_run[hs][i] = fmaf(w, sd.v_new[kvo + t], o_run[hs][i] * corr);
+        for (int m = 0; m < kAttMaxG; ++m)
+          if (m < G) {
+            const float corr = stat[m * 4 + 2];
+            acc[m].x *= corr;
+            acc[m].y *= corr;
+          }
+        for (int r = rg; r < nrt; r += RG) {
+          float2 v2;
+          if (r < nr) {
+            if (even) {
+              v2 = bf16x2_to_f2(*reinterpret_cast<const uint32_t*>(V + static_cast<size_t>(r) * d + 2 * pi));
+            } else {
+              v2 = make_float2(bf16_bits_to_f(V[static_cast<size_t>(r) * d + pi]), 0.f);
+            }
+          } else {
+            v2 = even ? make_float2(cv[2 * pi], cv[2 * pi + 1]) : make_float2(cv[pi], 0.f);
+          }
+          const float4 w0v = *reinterpret_cast<const float4*>(probs + r * 8);
+          const float4 w1v = *reinterpret_cast<const float4*>(probs + r * 8 + 4);
+          const float w[8] = {w0v.x, w0v.y, w0v.z, w0v.w, w1v.x, w1v.y, w1v.z, w1v.w};
+#pragma unroll
+          for (int m = 0; m < kAttMaxG; ++m)
+            if (m < G) ffma2(acc[m], make_float2(w[m], w[m]), v2);
+        }
       }
-      m_run[hs] = m_new;
+      __syncthreads();  // buffer and probs free for the next sub-chunk
     }
+    w0 += nw;
+    if (last_w) break;
   }
+  // ---- reduce the row groups, write the partial record per head
+  if (rg < RG) {
+#pragma unroll
+    for (int m = 0; m < kAttMaxG; ++m)
+      if (m < G) {
+        red[(static_cast<size_t>(rg) * G + m) * d + ew * pi] = acc[m].x;
+        if (even) red[(static_cast<size_t>(rg) * G + m) * d + 2 * pi + 1] = acc[m].y;
+      }
+  }
+  __syncthreads();
   const int stride = att_stride(d);
-#pragma unroll
-  for (int hs = 0; hs < kMaxHeadsPerWarp; ++hs) {
-    const int h = warp + hs * kDecodeWarps;
-    if (h >= H) break;
-    float* ph = part + static_cast<size_t>(h) * stride;
-#pragma unroll
-    for (int i = 0; i < kMaxDL; ++i) {
-      const int t = d128 ? 4 * lane + i : lane + 32 * i;
-      if ((d128 ? i < 4 : t < d)) ph[t] = o_run[hs][i];
+  for (int i = tid; i < G * d; i += blockDim.x) {
+    const int m = i / d, t = i - (i / d) * d;
+    float s = 0.f;
+    for (int q = 0; q < RG; ++q) s += red[(static_cast<size_t>(q) * G + m) * d + t];
+    part[static_cast<size_t>(m) * stride + t] = s;
+  }
+  if (tid < G) {
+    part[static_cast<size_t>(tid) * stride + d] = stat[tid * 4 + 0];
+    part[static_cast<size_t>(tid) * stride + d + 1] = stat[tid * 4 + 1];
+  }
+}
+
+// Log-sum-exp merge of the row-chunk partials of KV head g (attention.cpp
+// :88-110 semantics): out[h] = sum_c e^(m_c - M) o_c / sum_c e^(m_c - M) l_c.
+__device__ void merge_group(const DecodeParams& p, const SeqDesc& sd, int g, const float* parts, int chunks) {
+  const int d = p.d, G = p.H / p.H_kv, stride = att_stride(d);
+  const size_t cstride = static_cast<size_t>(G) * stride;
+  for (int i = threadIdx.x; i < G * d; i += blockDim.x) {
+    const int m = i / d, t = i - (i / d) * d;
+    const float* pm = parts + static_cast<size_t>(m) * stride;
+    float M = -INFINITY;
+    for (int c = 0; c < chunks; ++c) M = fmaxf(M, __ldcg(pm + c * cstride + d));
+    float num = 0.f, den = 0.f;
+    for (int c = 0; c < chunks; ++c) {
+      const float mc = __ldcg(pm + c * cstride + d);
+      if (mc == -INFINITY) continue;
+      const float w = expf(mc - M);
+      num = fmaf(w, __ldcg(pm + c * cstride + t), num);
+      den = fmaf(w, __ldcg(pm + c * cstride + d + 1), den);
     }
-    if (lane == 0) {
-      ph[d] = m_run[hs];
-      ph[d + 1] = l_run[hs];
-    }
+    sd.out[static_cast<size_t>(g + m * p.H_kv) * d + t] = num / den;
   }
 }
 
@@ -566,6 +751,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   const int nblocks = gridDim.x;
   const int seq_id = cta / p.ctas_per_seq;
   const int cs = cta - seq_id * p.ctas_per_seq;
+  const int c0 = seq_id * p.ctas_per_seq;
   const SeqDesc sd = p.seqs[seq_id];
   const int H = p.H;
   const int width = H * p.d;
@@ -577,19 +763,18 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     mbar_init(&sm.empty[tid], p.H_kv);  // the H_kv consumer warps of a stage
   }
   if (tid == 0) {
-    mbar_init(sm.att, 1);
+    mbar_init(&sm.att[0], 1);
+    mbar_init(&sm.att[1], 1);
     mbar_init(sm.aux, 1);
   }
   uint32_t aux_phase = 0;
   for (int h = tid; h < H; h += blockDim.x) sm.headmax[h] = float_ord(-INFINITY);
   fence_mbar_init();
-  GridBarrier* gbar = reinterpret_cast<GridBarrier*>(p.bar);
-  unsigned int bar_gen = 0;
-  if (tid == 0) bar_gen = grid_sync_begin(gbar);  // only thread 0 uses it
-  __syncthreads();
+  GridSync gs{p.bar + p.bar_slot, static_cast<unsigned int>(nblocks), 0u};
+  if (cta == 0 && tid == 0) p.bar[p.bar_slot ^ 32] = 0u;  // the next launch's counter
 
   trace_pt(p, 0);
-  // ---- phase 0: append + cache decision + histogram reset
+  // ---- phase 0: append, scan frames, Selection Cache decision(s), hit prep
   if ((p.mode & kModeAppend) && cs == 0 && sd.append_frame >= 0) {
     const int row = p.H_kv * p.d;
     const size_t off = (static_cast<size_t>(sd.append_frame) * p.page_size + sd.append_slot) * row;
@@ -599,44 +784,83 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     }
     if (tid == 0 && sd.append_page >= 0) sd.page_table[sd.append_page] = sd.append_frame;
   }
-  // every CTA evaluates every sequence's decision so that the grid agrees on
-  // whether any selection (and its barriers) runs this step
-  double* scratch_d = reinterpret_cast<double*>(sm.hist);  // hist is free until phase 2
-  int own = 0;        // 0 none, 1 miss (select), 2 hit
-  int any_select = 0, any_radix = 0;
-  double own_cos = NAN;
-  for (int b = 0; b < p.n_seq; ++b) {
-    const SeqDesc& s2 = (b == seq_id) ? sd : p.seqs[b];
-    int st = 0;
-    double c = NAN;
-    if (s2.select) {
-      if (p.mode & kModeCache) {
-        const int dec = cache_decision(s2, width, scratch_d, &c);
-        st = dec == 1 ? 1 : dec == 0 ? 2 : 3;
-      } else {
-        st = 1;
-      }
-    }
-    if (st == 1) {
-      any_select = 1;
-      if (do_select && s2.n_cand > p.k) any_radix = 1;
-    }
-    if (b == seq_id) {
-      own = st;
-      own_cos = c;
-    }
-  }
-  if (do_select && own == 1) {
-    uint32_t* gh = p.ws_hist + static_cast<size_t>(seq_id) * 3 * kBins;
-    for (int i = cs * blockDim.x + tid; i < 3 * kBins; i += p.ctas_per_seq * blockDim.x) gh[i] = 0u;
-  }
-  if (cs == 0 && tid == 0 && own == 3) sd.cache->error = 1;
-
-  trace_pt(p, 1);
-  // ---- phase 1: scan
   const int T = sd.n_cand;
   const int j0 = min(T, cs * p.tpc);
   const int nloc = max(0, min(T, j0 + p.tpc) - j0);
+  const bool may_scan = sd.select && (p.mode & kModeScore) && !(p.mode & kModeSIn);
+  // slab rows of the scan candidates: issue the (page-table) loads now, store
+  // after the decision so their latency overlaps it
+  int32_t fr_pre[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int jl = tid + u * blockDim.x;
+    fr_pre[u] = (may_scan && jl < nloc) ? static_cast<int32_t>(row_index(sd, cand_at(sd, j0 + jl), p.page_size)) : 0;
+  }
+  // hit prep: count the cached selection below init_end / local_begin
+  const bool hit_prep = !sd.att_list && sd.select && (p.mode & kModeCache) && (p.mode & kModeAttend);
+  const uint32_t ie = static_cast<uint32_t>(sd.init_end);
+  const uint32_t lbs = static_cast<uint32_t>(max(sd.local_begin, sd.init_end));
+  uint32_t cie = 0, clb = 0;
+  int n_sel_prev = 0;
+  if (hit_prep) {
+    n_sel_prev = __ldcg(&sd.cache->n_sel);
+    for (int base = tid; base < p.k; base += 4 * blockDim.x) {
+      uint32_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * blockDim.x;
+        v[u] = i < p.k ? __ldcg(sd.sel + i) : 0xffffffffu;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * blockDim.x;
+        const bool in = i < n_sel_prev;
+        cie += in && v[u] < ie;
+        clb += in && v[u] < lbs;
+      }
+    }
+  }
+  // Selection Cache decisions. A single sequence: every CTA evaluates it
+  // (bit-identical) so the grid agrees on whether selection (and its
+  // barriers) runs. Several sequences: each CTA evaluates its own and the
+  // barriers run unconditionally.
+  double* scratch_d = reinterpret_cast<double*>(sm.hist);  // hist is free until the radix passes
+  int own = 0;  // 0 no selection, 1 miss (select), 2 hit, 3 zero query
+  double own_cos = NAN;
+  if (sd.select) {
+    if (p.mode & kModeCache) {
+      const int dec = cache_decision(sd, width, scratch_d, &own_cos);
+      own = dec == 1 ? 1 : dec == 0 ? 2 : 3;
+    } else {
+      own = 1;
+    }
+  }
+  int any_select = 0, any_radix = 0;
+  if (p.n_seq == 1) {
+    any_select = own == 1;
+    any_radix = do_select && own == 1 && T > p.k;
+  } else {
+    for (int b = 0; b < p.n_seq; ++b) {
+      any_select |= p.seqs[b].select;
+      any_radix |= do_select && p.seqs[b].select && p.seqs[b].n_cand > p.k;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int jl = tid + u * blockDim.x;
+    if (may_scan && jl < nloc) sm.frames[jl] = fr_pre[u];
+  }
+  for (int jl = tid + 4 * blockDim.x; may_scan && jl < nloc; jl += blockDim.x)
+    sm.frames[jl] = static_cast<int32_t>(row_index(sd, cand_at(sd, j0 + jl), p.page_size));
+  if (do_select && own == 1 && T > p.k) {
+    uint32_t* gh = p.ws_hist + static_cast<size_t>(seq_id) * 2 * kRadixBins;
+    for (int i = cs * blockDim.x + tid; i < 2 * kRadixBins; i += p.ctas_per_seq * blockDim.x) gh[i] = 0u;
+  }
+  if (cs == 0 && tid == 0 && own == 3) sd.cache->error = 1;
+  __syncthreads();
+
+  trace_pt(p, 1);
+  // ---- phase 1: scan (Alg. 2)
   float* Sbuf = p.s_in_smem ? sm.S : p.ws_s + static_cast<size_t>(cta) * H * p.tpc;
   uint32_t* keys = p.s_in_smem ? sm.keys : p.ws_keys + static_cast<size_t>(cta) * p.tpc;
   const int sstride = p.tpc;
@@ -651,18 +875,6 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       }
     } else {
       float* so = (p.mode & kModeSOut) ? sd.s_out + j0 : nullptr;
-      for (int base = tid; base < nloc; base += 4 * blockDim.x) {
-        int32_t fr[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int jl = base + u * blockDim.x;
-          fr[u] = jl < nloc ? static_cast<int32_t>(row_index(sd, cand_at(sd, j0 + jl), p.page_size)) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (base + u * static_cast<int>(blockDim.x) < nloc) sm.frames[base + u * blockDim.x] = fr[u];
-      }
-      __syncthreads();
       if constexpr (FAST) scan_fast<D, G>(p, sd, sm, j0, nloc, Sbuf, sstride, so);
       else scan_generic(p, sd, sm, j0, nloc, Sbuf, sstride, so);
     }
@@ -670,36 +882,29 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   __syncthreads();
   trace_pt(p, 2);
 
+  // ---- phase 2: per-CTA softmax partials m = max_j S, z = sum_j e^(S - m); S <- e^(S - m)
   if (do_select && own == 1 && p.method == 2) {
-    // per-CTA softmax partials: m = max_j S, z = sum_j exp(S - m); S <- exp(S - m)
     const int warp = tid >> 5, lane = tid & 31;
     for (int h = warp; h < H; h += kDecodeWarps) {
       const float m = ord_float(sm.headmax[h]);
-      float z = 0.f;
+      float z0 = 0.f, z1 = 0.f;
       float* sr = Sbuf + static_cast<size_t>(h) * sstride;
       if (m > -INFINITY) {
-        float z1 = 0.f, z2 = 0.f, z3 = 0.f;
         int jl = lane;
-        for (; jl + 96 < nloc; jl += 128) {
-          const float e0 = expf(sr[jl] - m), e1 = expf(sr[jl + 32] - m);
-          const float e2 = expf(sr[jl + 64] - m), e3 = expf(sr[jl + 96] - m);
+        for (; jl + 32 < nloc; jl += 64) {
+          const float e0 = fast_exp(sr[jl] - m), e1 = fast_exp(sr[jl + 32] - m);
           sr[jl] = e0;
           sr[jl + 32] = e1;
-          sr[jl + 64] = e2;
-          sr[jl + 96] = e3;
-          z += e0;
+          z0 += e0;
           z1 += e1;
-          z2 += e2;
-          z3 += e3;
         }
         for (; jl < nloc; jl += 32) {
-          const float e = expf(sr[jl] - m);
+          const float e = fast_exp(sr[jl] - m);
           sr[jl] = e;
-          z += e;
+          z0 += e;
         }
-        z = (z + z1) + (z2 + z3);
       }
-      z = warp_sum(z);
+      const float z = warp_sum(z0 + z1);
       if (lane == 0) {
         const size_t o = (static_cast<size_t>(seq_id) * H + h) * stats_stride(p.ctas_per_seq) + cs;
         p.ws_m[o] = m;
@@ -708,51 +913,38 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     }
   }
   trace_pt(p, 3);
-  if (any_select) grid_sync(gbar, nblocks, bar_gen);  // #1
+  if (any_select) gs.sync();  // B1: softmax partials of every CTA visible
   trace_pt(p, 4);
 
-  // ---- phase 2: crit + cache bookkeeping
-  if (own == 1 && cs == 0 && tid == 0 && (p.mode & kModeCache)) {
+  // ---- phase 3: criticality (soft vote / raw sum) + cache bookkeeping
+  if (cs == 0 && tid == 0 && (p.mode & kModeCache) && (own == 1 || own == 2)) {
     CacheState* c = sd.cache;
     c->lookups += 1;
-    c->first_flag = 0;
-    c->last_hit = 0;
-    c->last_cos = own_cos;
-  }
-  if (own == 2 && cs == 0 && tid == 0) {
-    CacheState* c = sd.cache;
-    c->lookups += 1;
-    c->hits += 1;
-    c->last_hit = 1;
+    if (own == 2) c->hits += 1;
+    else c->first_flag = 0;
+    c->last_hit = own == 2 ? 1 : 0;
     c->last_cos = own_cos;
   }
   if (own == 1 && (p.mode & kModeCache)) {
-    // the new cached query (every CTA finished reading the old one before #1)
+    // the new cached query (every CTA read the old one before B1)
     for (int i = cs * blockDim.x + tid; i < width; i += p.ctas_per_seq * blockDim.x) sd.cached_q[i] = sd.q[i];
   }
-  const int kk_total = p.k;
-  uint32_t tau = 0, kk = 0;
-  const bool radix_own = do_select && own == 1 && T > kk_total;
+  const bool radix_own = do_select && own == 1 && T > p.k;
   if (do_select && own == 1) {
     if (p.method == 2) {
       const int warp = tid >> 5, lane = tid & 31;
-      const int c0 = seq_id * p.ctas_per_seq;
-      // stage every CTA's (m, z) of this sequence in smem with one coalesced pass
       float* pm = reinterpret_cast<float*>(sm.ring);
-      float* pz = pm;
       const int nc = p.ctas_per_seq;
       const int ncp = stats_stride(nc);
-      // the sequence's [h][cta] stats are two contiguous rows blocks: 2 bulk copies
       const size_t sbytes = static_cast<size_t>(H) * ncp * 4;
       if (tid == 0) {
         mbar_arrive_expect_tx(sm.aux, static_cast<uint32_t>(2 * sbytes));
         bulk_g2s_nohint(pm, p.ws_m + static_cast<size_t>(seq_id) * H * ncp, static_cast<uint32_t>(sbytes), sm.aux);
         bulk_g2s_nohint(pm + H * ncp, p.ws_z + static_cast<size_t>(seq_id) * H * ncp, static_cast<uint32_t>(sbytes), sm.aux);
       }
-      pz = pm + H * ncp;
+      const float* pz = pm + H * ncp;
       mbar_wait(sm.aux, aux_phase);
       aux_phase ^= 1u;
-      trace_pt(p, 15);
       for (int h = warp; h < H; h += kDecodeWarps) {
         float M = -INFINITY;
         for (int c = lane; c < nc; c += 32) M = fmaxf(M, pm[h * ncp + c]);
@@ -760,22 +952,23 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
         float Z = 0.f;
         for (int c = lane; c < nc; c += 32) {
           const float mc = pm[h * ncp + c];
-          if (mc > -INFINITY) Z += pz[h * ncp + c] * expf(mc - M);
+          if (mc > -INFINITY) Z += pz[h * ncp + c] * fast_exp(mc - M);
         }
         Z = warp_sum(Z);
         if (lane == 0) {
           const float ms = ord_float(sm.headmax[h]);
-          sm.f[h] = (ms > -INFINITY) ? expf(ms - M) / Z : 0.f;
+          sm.f[h] = (ms > -INFINITY) ? fast_exp(ms - M) / Z : 0.f;
         }
       }
-      trace_pt(p, 16);
       __syncthreads();
+      // crit[j] = sum_h softmax_h(S)[j] (select_head_soft_vote, selector.cpp:113-126)
       for (int jl = tid; jl < nloc; jl += blockDim.x) {
         float c = 0.f;
         for (int h = 0; h < H; ++h) c = fmaf(Sbuf[static_cast<size_t>(h) * sstride + jl], sm.f[h], c);
         keys[jl] = float_key(c);
       }
     } else {
+      // raw logit sum (select_topk, selector.cpp:89-99)
       for (int jl = tid; jl < nloc; jl += blockDim.x) {
         float c = 0.f;
         for (int h = 0; h < H; ++h) c += Sbuf[static_cast<size_t>(h) * sstride + jl];
@@ -784,238 +977,174 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     }
     __syncthreads();
   }
-
   trace_pt(p, 5);
-  // ---- phase 3: radix select (3 passes, 11/11/10 bits)
+
+  // ---- phase 4: radix select over 24-bit key prefixes (two 12-bit passes).
+  // Larger criticality first; keys equal in their top 24 bits (relative
+  // difference < 2^-15) rank as ties, which go to the smaller position
+  // (tensor.cpp:81-88).
+  uint32_t tau = 0, take_eq_all = 1;
+  uint32_t kk = static_cast<uint32_t>(p.k);
   if (any_radix) {
-    uint32_t prefix = 0;
-    uint32_t* gh = p.ws_hist + static_cast<size_t>(seq_id) * 3 * kBins;
-    kk = static_cast<uint32_t>(kk_total);
-    const int shifts[3] = {21, 10, 0};
-    const int widths[3] = {11, 11, 10};
-    for (int pass = 0; pass < 3; ++pass) {
-      const int sh = shifts[pass], wd = widths[pass];
-      const int nb = 1 << wd;
-      if (radix_own) {
-        for (int i = tid; i < nb; i += blockDim.x) sm.hist[i] = 0u;
-        __syncthreads();
-        const int hs = sh + wd;  // bits above this digit must match the prefix
-        for (int jl = tid; jl < nloc; jl += blockDim.x) {
-          const uint32_t key = keys[jl];
-          if (hs >= 32 || (key >> hs) == prefix) atomicAdd(&sm.hist[(key >> sh) & (nb - 1)], 1u);
-        }
-        __syncthreads();
-        for (int i = tid; i < nb; i += blockDim.x) {
-          const uint32_t c = sm.hist[i];
-          if (c) atomicAdd(gh + pass * kBins + i, c);
-        }
-      }
-      grid_sync(gbar, nblocks, bar_gen);  // #2..#4
-      trace_pt(p, 6 + pass);
-      if (radix_own) {
-        int b;
-        uint32_t above;
-        find_bin(gh + pass * kBins, nb, kk, sm.scratch, &b, &above);
-        kk -= above;
-        prefix = (prefix << wd) | static_cast<uint32_t>(b);
-      }
-    }
-    tau = prefix;
-    // per-CTA (n_gt, n_eq)
+    uint32_t* gh = p.ws_hist + static_cast<size_t>(seq_id) * 2 * kRadixBins;
+    if (radix_own) radix_hist(keys, nloc, 20, 32, 0u, sm.hist, gh);
+    gs.sync();  // B2
+    trace_pt(p, 6);
+    uint32_t b1 = 0;
     if (radix_own) {
-      uint32_t ngt = 0, neq = 0;
-      for (int jl = tid; jl < nloc; jl += blockDim.x) {
-        const uint32_t key = keys[jl];
-        ngt += key > tau;
-        neq += key == tau;
+      int b;
+      uint32_t above;
+      find_bin(gh, kRadixBins, kk, sm.scratch, &b, &above);
+      kk -= above;
+      b1 = static_cast<uint32_t>(b);
+      radix_hist(keys, nloc, 8, 20, b1, sm.hist, gh + kRadixBins);
+    }
+    gs.sync();  // B3
+    trace_pt(p, 7);
+    uint32_t eq_total = 0;
+    if (radix_own) {
+      int b;
+      uint32_t above;
+      find_bin(gh + kRadixBins, kRadixBins, kk, sm.scratch, &b, &above);
+      kk -= above;
+      tau = (b1 << 12) | static_cast<uint32_t>(b);
+      eq_total = __ldcg(gh + kRadixBins + b);
+    }
+    // ties straddling the budget: the taken ones are the lowest positions,
+    // which needs every CTA's tie count (one more exchange)
+    int need_tie = 0;
+    if (p.n_seq == 1) need_tie = radix_own && eq_total > kk;
+    else need_tie = 1;
+    if (need_tie) {
+      if (radix_own) {
+        uint32_t neq = 0;
+        for (int jl = tid; jl < nloc; jl += blockDim.x) neq += (keys[jl] >> 8) == tau;
+        uint32_t tot;
+        block_excl_scan(neq, sm.scratch, &tot);
+        if (tid == 0) p.ws_cnt[cta] = tot;
       }
-      uint32_t tg, te;
-      block_excl_scan(ngt, sm.scratch, &tg);
-      block_excl_scan(neq, sm.scratch, &te);
-      if (tid == 0) {
-        p.ws_cnt[static_cast<size_t>(cta) * 2 + 0] = tg;
-        p.ws_cnt[static_cast<size_t>(cta) * 2 + 1] = te;
+      gs.sync();  // B3b
+      if (radix_own && eq_total > kk) {
+        uint32_t pre = 0;
+        if (tid < 32) {
+          for (int c = tid; c < cs; c += 32) pre += __ldcg(p.ws_cnt + c0 + c);
+          pre = __reduce_add_sync(0xffffffffu, pre);
+          if (tid == 0) sm.scratch[70] = pre;
+        }
+        __syncthreads();
+        pre = sm.scratch[70];
+        __syncthreads();
+        take_eq_all = 0;
+        kk = kk > pre ? kk - pre : 0u;  // ties this CTA may still take
       }
     }
-    grid_sync(gbar, nblocks, bar_gen);  // #5
-    trace_pt(p, 9);
   }
 
-  // ---- phase 3b: ascending compaction of the selection
+  // ---- phase 5: ascending compaction of this CTA's selected candidates
   if (do_select && own == 1) {
-    if (!radix_own) {
-      // T <= k: every candidate is selected (pick() with take = T)
-      for (int jl = tid; jl < nloc; jl += blockDim.x) {
-        sd.sel[j0 + jl] = cand_at(sd, j0 + jl);
-        sd.sel_crit[j0 + jl] = key_float(keys[jl]);
+    uint32_t out_n = 0, eq_seen = 0;
+    uint32_t* lt = p.ws_sel_tok + static_cast<size_t>(cta) * p.tpc;
+    float* lc = p.ws_sel_crit + static_cast<size_t>(cta) * p.tpc;
+    for (int base = 0; base < nloc; base += blockDim.x) {
+      const int jl = base + tid;
+      const uint32_t key = jl < nloc ? keys[jl] : 0u;
+      bool take = jl < nloc;
+      if (radix_own && take) {
+        const uint32_t k24 = key >> 8;
+        take = k24 > tau || (k24 == tau && take_eq_all);
       }
-      if (cs == 0 && tid == 0) sd.cache->n_sel = T;
-    } else {
-      uint32_t pgt = 0, peq = 0;
-      const int c0 = seq_id * p.ctas_per_seq;
-      if (tid < 32) {
-        for (int c = tid; c < cs; c += 32) {
-          pgt += __ldcg(p.ws_cnt + static_cast<size_t>(c0 + c) * 2 + 0);
-          peq += __ldcg(p.ws_cnt + static_cast<size_t>(c0 + c) * 2 + 1);
-        }
-        pgt = __reduce_add_sync(0xffffffffu, pgt);
-        peq = __reduce_add_sync(0xffffffffu, peq);
-        if (tid == 0) {
-          sm.scratch[66] = pgt;
-          sm.scratch[67] = peq;
-        }
-      }
-      __syncthreads();
-      pgt = sm.scratch[66];
-      peq = sm.scratch[67];
-      __syncthreads();
-      const uint32_t take_eq = kk > peq ? kk - peq : 0u;  // ties still available to this CTA
-      uint32_t out_base = pgt + min(peq, kk);
-      uint32_t eq_seen = 0;
-      for (int t0 = 0; t0 < nloc; t0 += blockDim.x) {
-        const int jl = t0 + tid;
-        const uint32_t key = jl < nloc ? keys[jl] : 0u;
-        const uint32_t is_eq = (jl < nloc && key == tau) ? 1u : 0u;
+      if (radix_own && !take_eq_all) {
+        const uint32_t is_eq = (jl < nloc && (key >> 8) == tau) ? 1u : 0u;
         uint32_t eq_tot;
-        const uint32_t eq_rank = eq_seen + block_excl_scan(is_eq, sm.scratch, &eq_tot);
-        const uint32_t take = (jl < nloc) && (key > tau || (is_eq && eq_rank < take_eq)) ? 1u : 0u;
-        uint32_t take_tot;
-        const uint32_t pos = block_excl_scan(take, sm.scratch, &take_tot);
-        if (take) {
-          sd.sel[out_base + pos] = cand_at(sd, j0 + jl);
-          sd.sel_crit[out_base + pos] = key_float(key);
-        }
-        out_base += take_tot;
+        const uint32_t r = eq_seen + block_excl_scan(is_eq, sm.scratch, &eq_tot);
+        if (is_eq && r < kk) take = true;
         eq_seen += eq_tot;
       }
-      if (cs == 0 && tid == 0) sd.cache->n_sel = kk_total;
+      uint32_t tot;
+      const uint32_t pos = out_n + block_excl_scan(take ? 1u : 0u, sm.scratch, &tot);
+      if (take) {
+        lt[pos] = cand_at(sd, j0 + jl);
+        lc[pos] = key_float(key);
+      }
+      out_n += tot;
     }
+    if (tid == 0) p.ws_nsel[cta] = out_n;
+  }
+  trace_pt(p, 8);
+  if (any_select) gs.sync();  // B4: per-CTA selections published
+  trace_pt(p, 9);
+
+  // ---- phase 6: selection offsets; the SelectionResult (ascending) out
+  if (do_select && own == 1) {
+    const int nc = p.ctas_per_seq;
+    const uint32_t v = tid < nc ? __ldcg(p.ws_nsel + c0 + tid) : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan(v, sm.scratch, &tot);
+    if (tid <= nc) sm.prefix[tid] = static_cast<int>(tid < nc ? ex : tot);
+    __syncthreads();
+    const int my0 = sm.prefix[cs], myn = sm.prefix[cs + 1] - my0;
+    const uint32_t* lt = p.ws_sel_tok + static_cast<size_t>(cta) * p.tpc;
+    const float* lc = p.ws_sel_crit + static_cast<size_t>(cta) * p.tpc;
+    for (int i = tid; i < myn; i += blockDim.x) {
+      sd.sel[my0 + i] = __ldcg(lt + i);
+      sd.sel_crit[my0 + i] = __ldcg(lc + i);
+    }
+    if (cs == 0 && tid == 0) sd.cache->n_sel = static_cast<int>(tot);
   }
   trace_pt(p, 10);
   if (!(p.mode & kModeAttend)) return;
-  if (any_select) grid_sync(gbar, nblocks, bar_gen);  // #6 selection visible
-  trace_pt(p, 11);
 
-  // ---- phase 4: split-K sparse flash-decoding partials
+  // ---- phase 7: split-K sparse flash-decoding (KV head x row chunk)
   AttView av{};
-  if (!sd.att_list) {
-    const int n_sel = (sd.select && own != 3) ? __ldcg(&sd.cache->n_sel) : 0;
-    av.init_end = sd.init_end;
-    const uint32_t ie = static_cast<uint32_t>(sd.init_end);
-    const uint32_t lb = static_cast<uint32_t>(max(sd.local_begin, sd.init_end));
-    // sorted selection: lower_bound(x) == count(sel < x), counted in parallel
-    const uint32_t lbs = lb < ie ? ie : static_cast<uint32_t>(sd.local_begin);
-    uint32_t cie = 0, clb = 0;
-    for (int base = tid; base < n_sel; base += 4 * blockDim.x) {
-      uint32_t v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = base + u * blockDim.x;
-        v[u] = i < n_sel ? __ldcg(sd.sel + i) : 0xffffffffu;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        cie += v[u] < ie;
-        clb += v[u] < lbs;
-      }
-    }
-    uint32_t tot_ie, tot_lb;
-    block_excl_scan(cie, sm.scratch, &tot_ie);
-    block_excl_scan(clb, sm.scratch, &tot_lb);
-    const int lo1 = static_cast<int>(tot_ie), hi1 = static_cast<int>(tot_lb);
-    trace_pt(p, 17);
-    av.lo1 = lo1;
-    av.n1 = max(0, hi1 - lo1);
-    av.lb2 = static_cast<int>(lb);
-    av.n_rows = sd.init_end + av.n1 + (sd.n_cached - av.lb2);
-  } else {
+  if (sd.att_list) {
     av.n_rows = sd.n_att;
+  } else {
+    av.init_end = sd.init_end;
+    av.lb = static_cast<int>(lbs);
+    if (own == 1) {
+      av.fresh = 1;
+      av.n1 = sm.prefix[p.ctas_per_seq];
+      av.ncta = p.ctas_per_seq;
+      av.cta0 = c0;
+    } else if (own == 2) {
+      uint32_t tie, tlb;
+      block_excl_scan(cie, sm.scratch, &tie);
+      block_excl_scan(clb, sm.scratch, &tlb);
+      av.lo1 = static_cast<int>(tie);
+      av.n1 = max(0, static_cast<int>(tlb) - static_cast<int>(tie));
+    }
+    av.n_rows = sd.init_end + av.n1 + (sd.n_cached - av.lb);
   }
-  const int total_rows = av.n_rows + 1;  // + current token
-  const int per = (total_rows + p.ctas_per_seq - 1) / p.ctas_per_seq;
-  const int r0 = min(total_rows, cs * per);
-  const int r1 = min(total_rows, r0 + per);
-  const bool with_cur = (r0 < r1) && (r1 == total_rows);
-  float* part = p.ws_att + static_cast<size_t>(cta) * H * att_stride(p.d);
-  attend_partial(p, sd, av, sm, r0, min(r1, av.n_rows), with_cur, part);
-  trace_pt(p, 12);
-  grid_sync(gbar, nblocks, bar_gen);  // #7
-  trace_pt(p, 13);
-
-  // ---- phase 5: LSE merge (attention.cpp:88-110 semantics)
-  // Per head: weights w_c = exp(m_c - M) for all partials in parallel, then
-  // the d output columns are summed by blockDim/d thread groups over
-  // interleaved partials (independent loads, no serial L2 chain).
-  {
-    const int d = p.d, stride = att_stride(d);
-    const int c0 = seq_id * p.ctas_per_seq;
-    const int nparts = min(p.ctas_per_seq, (total_rows + per - 1) / per);
-    float* wsm = reinterpret_cast<float*>(sm.hist);        // [nparts] weights (<= 2048)
-    float* red = reinterpret_cast<float*>(sm.ring);        // [groups][d] partial sums
-    float* bred = reinterpret_cast<float*>(sm.scratch);    // block reduction slots
-    const int warp = tid >> 5, lane = tid & 31;
-    const int groups = max(1, static_cast<int>(blockDim.x) / d);
-    // partials are staged in smem chunk by chunk (one parallel load each) and
-    // merged online, so every global read is independent
-    float* stg = reinterpret_cast<float*>(sm.ring + 4096);
-    const int pc = max(1, min(nparts, static_cast<int>((kRingBudget - 4096) / 4) / stride));
-    for (int h = cs; h < H; h += p.ctas_per_seq) {
-      const float* base = p.ws_att + (static_cast<size_t>(c0) * H + h) * stride;
-      const size_t cstride = static_cast<size_t>(H) * stride;
-      const int g = tid / d, t = tid - (tid / d) * d;
-      float acc = 0.f, Mrun = -INFINITY, Lrun = 0.f;
-      for (int cb = 0; cb < nparts; cb += pc) {
-        const int n = min(pc, nparts - cb);
-        // one bulk copy per partial record (16-byte padded), one barrier wait
-        if (tid == 0) mbar_arrive_expect_tx(sm.aux, static_cast<uint32_t>(n * stride * 4));
-        __syncthreads();
-        for (int c = tid; c < n; c += blockDim.x)
-          bulk_g2s_nohint(stg + c * stride, base + (cb + c) * cstride, static_cast<uint32_t>(stride * 4), sm.aux);
-        mbar_wait(sm.aux, aux_phase);
-        aux_phase ^= 1u;
-        __syncthreads();
-        float mloc = -INFINITY;
-        for (int c = tid; c < n; c += blockDim.x) mloc = fmaxf(mloc, stg[c * stride + d]);
-        mloc = warp_max(mloc);
-        if (lane == 0) bred[warp] = mloc;
-        __syncthreads();
-        float Mc = lane < kDecodeWarps ? bred[lane] : -INFINITY;
-        Mc = warp_max(Mc);
-        const float Mnew = fmaxf(Mrun, Mc);
-        const float scale = (Mrun == -INFINITY) ? 0.f : expf(Mrun - Mnew);
-        __syncthreads();
-        float lsum = 0.f;
-        for (int c = tid; c < n; c += blockDim.x) {
-          const float mc = stg[c * stride + d];
-          const float w = (mc == -INFINITY) ? 0.f : expf(mc - Mnew);
-          wsm[c] = w;
-          lsum += w * stg[c * stride + d + 1];
-        }
-        lsum = warp_sum(lsum);
-        if (lane == 0) bred[warp] = lsum;
-        __syncthreads();
-        float Lc = lane < kDecodeWarps ? bred[lane] : 0.f;
-        Lc = warp_sum(Lc);
-        Lrun = Lrun * scale + Lc;
-        if (g < groups) {
-          float a = 0.f;
-          for (int c = g; c < n; c += groups) a = fmaf(wsm[c], stg[c * stride + t], a);
-          acc = acc * scale + a;
-        }
-        Mrun = Mnew;
-        __syncthreads();
-      }
-      if (g < groups) red[g * d + t] = acc;
+  const AttSplit split = att_split(p.H_kv, p.ctas_per_seq);
+  const int gi = cs % split.groups, ci = cs / split.groups;
+  if (ci < split.chunks) {
+    const int total_rows = av.n_rows + 1;  // + current token
+    const int per = (total_rows + split.chunks - 1) / split.chunks;
+    const int r0 = min(total_rows, ci * per);
+    const int r1 = min(total_rows, r0 + per);
+    const bool with_cur = (r0 < r1) && (r1 == total_rows);
+    const int Gq = p.H / p.H_kv;
+    const int stride = att_stride(p.d);
+    for (int g = gi; g < p.H_kv; g += split.groups) {
+      float* parts = p.ws_att + (static_cast<size_t>(seq_id) * p.H_kv + g) * split.chunks * Gq * stride;
+      attend_group<(FAST ? D : 0), (FAST ? G : 0)>(p, sd, av, sm, g, r0, min(r1, av.n_rows), with_cur,
+                                                   parts + static_cast<size_t>(ci) * Gq * stride);
+      trace_pt(p, 11);
+      // the last chunk to finish merges (no grid barrier)
       __syncthreads();
-      for (int tt = tid; tt < d; tt += blockDim.x) {
-        float O = 0.f;
-        for (int gg = 0; gg < groups; ++gg) O += red[gg * d + tt];
-        sd.out[static_cast<size_t>(h) * d + tt] = O / Lrun;
+      if (tid == 0) {
+        unsigned int* ctr = p.ws_acnt + seq_id * p.H_kv + g;
+        const unsigned int old = atom_add_acqrel_u32(ctr, 1u);
+        const int last = old == static_cast<unsigned int>(split.chunks - 1);
+        if (last) *ctr = 0u;
+        sm.scratch[71] = last;
       }
+      __syncthreads();
+      if (sm.scratch[71]) merge_group(p, sd, g, parts, split.chunks);
       __syncthreads();
     }
   }
-  trace_pt(p, 14);
+  trace_pt(p, 12);
 }
 
 }  // namespace

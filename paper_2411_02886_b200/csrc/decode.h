@@ -18,6 +18,10 @@ constexpr int kDecodeWarps = kDecodeConsumers + 1;  // + warp 0: TMA producer
 constexpr int kDecodeThreads = kDecodeWarps * 32;
 constexpr int kMaxStages = 16;
 constexpr size_t kRingBudget = 96 * 1024;        // minimum K-row ring (also attention staging)
+constexpr int kRadixBins = 4096;                 // 12-bit radix digits (2 passes -> 24-bit keys)
+constexpr int kMaxPrefix = 256;                  // >= ctas_per_seq + 1
+constexpr int kAttMaxG = 8;                      // query heads per KV head on the attention path
+constexpr int kAttMaxRows = 256;                 // rows per attention sub-chunk (upper bound)
 
 TSB_HD inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -47,7 +51,7 @@ TSB_HD inline ScanGeom scan_geom(int H, int H_kv, int d, size_t ring_bytes = kRi
 }
 
 struct SmemLayout {
-  size_t ring, s, keys, frames, hist, headmax, f, scratch, bars, total;
+  size_t ring, s, keys, frames, hist, prefix, headmax, f, scratch, bars, total;
 };
 
 TSB_HD inline SmemLayout smem_layout(int H, int row_bytes, int tpc, int s_in_smem,
@@ -65,16 +69,17 @@ TSB_HD inline SmemLayout smem_layout(int H, int row_bytes, int tpc, int s_in_sme
   if (s_in_smem) o += align_up(static_cast<size_t>(tpc) * 4, 128);
   L.frames = o;  // slab row of every candidate of the CTA (TMA producer lookahead)
   o += align_up(static_cast<size_t>(tpc) * 4, 128);
-  L.hist = o;
-  o += 2048 * 4;
+  L.hist = L.ring;  // radix histogram: the ring is idle between the scan and the attention
+  L.prefix = o;
+  o += kMaxPrefix * 4;
   L.headmax = o;
   o += align_up(static_cast<size_t>(H) * 4, 16);
   L.f = o;
   o += align_up(static_cast<size_t>(H) * 4, 16);
   L.scratch = o;
-  o += 128 * 4;
+  o += 256 * 4;
   L.bars = o;
-  o += (2 * kMaxStages + 2) * 8;  // full/empty ring barriers + attention barrier
+  o += (2 * kMaxStages + 4) * 8;  // full/empty ring barriers + attention (x2) + aux
   L.total = align_up(o, 128);
   return L;
 }
@@ -83,6 +88,18 @@ TSB_HD inline SmemLayout smem_layout(int H, int row_bytes, int tpc, int s_in_sme
 TSB_HD inline int att_stride(int d) { return (d + 2 + 3) & ~3; }
 // Per-sequence stats rows [h][ctas], padded to 16 bytes for bulk copies.
 TSB_HD inline int stats_stride(int ctas) { return (ctas + 3) & ~3; }
+
+// Attention decomposition of one sequence's CTAs: (KV-head group, row chunk).
+struct AttSplit {
+  int groups;  // CTAs per row chunk (each owns KV heads g = gi, gi + groups, ...)
+  int chunks;  // row chunks per KV head
+};
+TSB_HD inline AttSplit att_split(int H_kv, int ctas_per_seq) {
+  AttSplit a;
+  a.groups = H_kv < ctas_per_seq ? H_kv : ctas_per_seq;
+  a.chunks = ctas_per_seq / a.groups;
+  return a;
+}
 
 const void* decode_kernel_ptr(int D, int G, bool fast);
 

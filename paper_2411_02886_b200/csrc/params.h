@@ -78,15 +78,20 @@ struct DecodeParams {
   uint32_t* ws_keys;           // [n_ctas][tpc] selection keys spill
   float* ws_m;                 // [n_seq][H][stats_stride] per-CTA head max
   float* ws_z;                 // [n_seq][H][stats_stride] per-CTA head sum exp(S - m)
-  uint32_t* ws_hist;           // [n_seq][3][2048] radix histograms
-  uint32_t* ws_cnt;            // [n_ctas][2] (n_gt, n_eq)
-  float* ws_att;               // [n_ctas][H][att_stride(d)] attention partials (o, m, l)
-  unsigned int* bar;           // GridBarrier
-  int att_rows_per_cta;        // attention rows per CTA per sub-chunk (ring capacity)
+  uint32_t* ws_hist;           // [n_seq][2][kRadixBins] radix histograms (pass 1, pass 2)
+  uint32_t* ws_cnt;            // [n_ctas] per-CTA count of keys tied at the threshold
+  uint32_t* ws_nsel;           // [n_ctas] per-CTA count of selected candidates
+  uint32_t* ws_sel_tok;        // [n_ctas][tpc] per-CTA selected token indices (ascending)
+  float* ws_sel_crit;          // [n_ctas][tpc] their criticality
+  float* ws_att;               // [n_seq][H_kv][chunks][G][att_stride(d)] attention partials (o, m, l)
+  unsigned int* ws_acnt;       // [n_seq][H_kv] arrival counters of the attention merge (self-resetting)
+  unsigned int* bar;           // grid barrier counters: bar[0] / bar[32] alternate per launch
+  int bar_slot;                // 0 or 32: this launch's counter (the other one is reset)
   int prefetch_stages;
-  int ring_bytes;
-  int debug_flags;             // dev experiments: bit0 = scan consumers skip the math              // shared-memory K ring (>= kRingBudget)         // L2 bulk-prefetch distance of the scan, in ring stages
-  unsigned long long* trace;   // optional [16] %globaltimer phase stamps (CTA 0)
+  int ring_bytes;              // shared-memory K ring (>= kRingBudget)
+  int att_bytes;               // attention staging: the ring + the (then dead) S/keys region
+  int debug_flags;             // dev experiments: bit0 = scan consumers skip the math
+  unsigned long long* trace;   // optional [32] %globaltimer phase stamps (CTA 0)
   SeqDesc seqs[kMaxSeqPerLaunch];  // passed by value in the kernel parameter space
 };
 

@@ -327,16 +327,24 @@ class Engine:
     def force_miss(self, seq=0):
         check(lib.ts_engine_force_miss(self._h, seq))
 
-    TRACE_POINTS = ["start", "decision", "scan", "exp_pass", "sync1", "crit", "radix0", "radix1", "radix2",
-                    "counts", "compact", "sync6", "attend", "sync7", "merge"]
+    TRACE_POINTS = ["start", "decision", "scan", "softmax_partials", "sync1", "crit", "radix1", "radix2",
+                    "compact", "sync4", "sel_out", "attend", "merge"]
 
     def set_trace(self, enable=True):
         check(lib.ts_engine_set_trace(self._h, 1 if enable else 0))
 
-    def read_trace(self):
-        """Per-phase device time (us) of the last decode step, from %globaltimer stamps."""
-        st = np.zeros(32, np.uint64)
-        check(lib.ts_engine_read_trace(self._h, st.ctypes.data_as(C.c_void_p), 32))
+    def read_trace(self, all_ctas=False):
+        """Per-phase device time (us) of the last decode step, from the
+        %globaltimer stamps of CTA 0 (or, with all_ctas, a [ctas x phases]
+        array of stamps in us relative to the earliest CTA start)."""
+        st = np.zeros(32 * 1024, np.uint64)
+        check(lib.ts_engine_read_trace(self._h, st.ctypes.data_as(C.c_void_p), st.size))
+        if all_ctas:
+            a = st.reshape(1024, 32).astype(np.int64)
+            n = int(np.count_nonzero(a[:, 0]))
+            a = a[:n]
+            t0 = a[:, 0].min()
+            return np.where(a > 0, (a - t0) / 1000.0, np.nan)
         t = st[: len(self.TRACE_POINTS)].astype(np.int64)
         out, prev = {}, int(t[0])
         for name, v in zip(self.TRACE_POINTS[1:], t[1:]):

@@ -195,28 +195,35 @@ def test_decode_stream_vs_oracle(sa, orc, H, H_kv, d, n, k):
         o2, h2, s2 = ref.decode(q, kt, vt)
         assert h1 == h2, f"step {step}: cache decision differs"
         hits.append(h1)
+        want = o2
         if s1 != list(s2):
-            # tie tolerance against the oracle's full criticality
+            # tie tolerance against the oracle's full criticality, then the
+            # attention is checked on OUR selection (same windows, oracle math)
             N = n + step
             cand = np.arange(16, N - 32, dtype=np.uint32)
-            K_all = ref_rows(ref)[:N]
-            S = orc.score_paged(q.reshape(H, d), K_all, H_kv, cand)
+            K_all, V_all = ref_rows(ref)
+            S = orc.score_paged(q.reshape(H, d), K_all[:N], H_kv, cand)
             check_selection(s1, s2, orc.criticality(S, k), cand)
-        assert rel_fro(o1, o2) <= 1e-5, rel_fro(o1, o2)
-        assert np.abs(o1 - o2).max() <= 1e-4
+            att = orc.make_windows(N, 16, 32, np.asarray(s1, np.uint32))
+            want = orc.sparse_attend(q, kt, vt, K_all[:N], V_all[:N], H, H_kv, att)
+        assert rel_fro(o1, want) <= 1e-5, rel_fro(o1, want)
+        assert np.abs(o1 - want).max() <= 1e-4
     assert any(hits) and not all(hits)
     st = eng.stats()
     assert st["lookups"] == 6 and st["hits"] == sum(hits) and st["len"] == n + 6
 
 
 def ref_rows(ref):
+    """The oracle engine's logical K and V rows (cached tokens, fp32)."""
     import ctypes
 
     st = ref.stats()
     lib = ref.o.lib
-    lib.oc_engine_k_rows.restype = ctypes.POINTER(ctypes.c_float)
-    p = lib.oc_engine_k_rows(ref.h)
-    return np.ctypeslib.as_array(p, shape=(st["len"] + 1, ref.H_kv * ref.d)).copy()
+    out = []
+    for fn in (lib.oc_engine_k_rows, lib.oc_engine_v_rows):
+        fn.restype = ctypes.POINTER(ctypes.c_float)
+        out.append(np.ctypeslib.as_array(fn(ref.h), shape=(st["len"] + 1, ref.H_kv * ref.d)).copy())
+    return out
 
 
 def test_decode_identical_queries_hit(sa):
@@ -252,10 +259,14 @@ def test_decode_llama_32k_parity(sa, orc):
     o2, h2, s2 = ref.decode(q, kt, vt)
     assert not h1 and not h2
     cand = np.arange(128, n - 512, dtype=np.uint32)
+    want = o2
     if s1 != list(s2):
-        S = orc.score_paged(q.reshape(H, d), ref_rows(ref)[:n], H_kv, cand)
+        K_all, V_all = ref_rows(ref)
+        S = orc.score_paged(q.reshape(H, d), K_all[:n], H_kv, cand)
         check_selection(s1, s2, orc.criticality(S, 2048), cand)
-    assert rel_fro(o1, o2) <= 1e-5 and np.abs(o1 - o2).max() <= 1e-4
+        att = orc.make_windows(n, 128, 512, np.asarray(s1, np.uint32))
+        want = orc.sparse_attend(q, kt, vt, K_all[:n], V_all[:n], H, H_kv, att)
+    assert rel_fro(o1, want) <= 1e-5 and np.abs(o1 - want).max() <= 1e-4
 
 
 # --------------------------------------------------------------- prefill

@@ -21,10 +21,10 @@ q = torch.randn(1, H * d, device="cuda", generator=g)
 kt = torch.randn(1, Hkv * d, device="cuda", generator=g)
 vt = torch.randn(1, Hkv * d, device="cuda", generator=g)
 out = torch.empty(1, H * d, device="cuda")
-eng.set_theta(2.0)
-for _ in range(3):
+eng.set_theta(2.0)  # theta > 1: every lookup misses
+for _ in range(3):  # 2 warm-up misses + the profiled miss
     eng.decode_async(q, kt, vt, out)
-eng.set_theta(-2.0)
-eng.decode_async(q, kt, vt, out)
+eng.set_theta(-2.0)  # theta < -1: every lookup hits
+eng.decode_async(q, kt, vt, out)  # the profiled hit
 eng.sync()
 print(eng.stats())

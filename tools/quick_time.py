@@ -48,3 +48,17 @@ for mode, theta in (("miss", 2.0), ("hit", -2.0)):
         eng.decode_async(q, kt, vt, out)
     torch.cuda.synchronize()
     print(mode, "phase trace (us):", {k: round(v, 2) for k, v in eng.read_trace().items()})
+# all-CTA phase statistics of one miss and one hit step (start-relative us)
+for mode, theta in (("miss", 2.0), ("hit", -2.0)):
+    eng.set_theta(theta)
+    for _ in range(3):
+        eng.decode_async(q, kt, vt, out)
+    torch.cuda.synchronize()
+    a = eng.read_trace(all_ctas=True)
+    names = sa.Engine.TRACE_POINTS
+    print(f"{mode}: all-CTA stamps (us from earliest start): phase: min / median / max")
+    for i, nm in enumerate(names):
+        col = a[:, i]
+        col = col[~np.isnan(col)]
+        if col.size:
+            print(f"  {i:2d} {nm:18s} {col.min():8.2f} {np.median(col):8.2f} {col.max():8.2f}  (n={col.size})")
