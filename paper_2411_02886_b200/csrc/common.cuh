@@ -197,6 +197,12 @@ struct GridSync {
   }
 };
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // exp(x) on the SFU (ex2.approx): max relative error ~2^-21 for |x| < 100,
 // well inside the 1e-4 criticality tolerance.
 __device__ __forceinline__ float fast_exp(float x) {

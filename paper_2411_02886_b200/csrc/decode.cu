@@ -90,7 +90,9 @@ __device__ __forceinline__ void trace_pt(const DecodeParams& p, int i) {
 }
 
 // Block-wide exclusive scan of one value per thread (all threads call).
-__device__ uint32_t block_excl_scan(uint32_t v, uint32_t* scratch, uint32_t* total) {
+// Out of line (like find_bin / radix_hist): the fused kernel's one-shot phases
+// are instruction-fetch bound, so shared helpers are kept as single copies.
+__device__ __noinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* scratch, uint32_t* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t inc = warp_incl_scan(v, lane);
   __syncthreads();
@@ -112,32 +114,34 @@ __device__ uint32_t block_excl_scan(uint32_t v, uint32_t* scratch, uint32_t* tot
 // Finds, in a global histogram whose bins are ordered by key, the bin b such that
 // count(bins > b) < kk <= count(bins >= b). Returns b and count(bins > b).
 // All threads call; every CTA computes the same answer from the same data.
-__device__ void find_bin(const uint32_t* gh, int nbins, uint32_t kk, uint32_t* scratch,
-                         int* bin_out, uint32_t* above_out) {
-  // thread t covers bins [nbins - (t+1)*per, nbins - t*per) in descending order
-  const int per = (nbins + 511) / 512;
+__device__ __noinline__ void find_bin(const uint32_t* gh, uint32_t kk, uint32_t* scratch, int* bin_out,
+                                      uint32_t* above_out) {
+  // thread t < 512 covers bins [B - 8(t+1), B - 8t) in descending order; all
+  // 8 loads are in flight together and kept for the in-bin search
+  constexpr int kPer = kRadixBins / 512;
   const int t = threadIdx.x;
+  uint32_t c[kPer];
   uint32_t sum = 0;
-  if (t < 512) {
-    for (int i = 0; i < per; ++i) {
-      const int b = nbins - 1 - (t * per + i);
-      if (b >= 0) sum += __ldcg(gh + b);
-    }
-  }
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) c[i] = t < 512 ? __ldcg(gh + (kRadixBins - 1 - (t * kPer + i))) : 0u;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) sum += c[i];
   uint32_t tot;
-  const uint32_t ex = block_excl_scan(t < 512 ? sum : 0u, scratch, &tot);
+  const uint32_t ex = block_excl_scan(sum, scratch, &tot);
   if (t < 512 && ex < kk && ex + sum >= kk) {
     uint32_t acc = ex;
-    for (int i = 0; i < per; ++i) {
-      const int b = nbins - 1 - (t * per + i);
-      const uint32_t c = __ldcg(gh + b);
-      if (acc + c >= kk) {
-        scratch[64] = static_cast<uint32_t>(b);
-        scratch[65] = acc;
-        break;
+    int found = -1;
+    uint32_t above = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      if (found < 0 && acc + c[i] >= kk) {
+        found = kRadixBins - 1 - (t * kPer + i);
+        above = acc;
       }
-      acc += c;
+      acc += c[i];
     }
+    scratch[64] = static_cast<uint32_t>(found);
+    scratch[65] = above;
   }
   __syncthreads();
   *bin_out = static_cast<int>(scratch[64]);
@@ -146,60 +150,82 @@ __device__ void find_bin(const uint32_t* gh, int nbins, uint32_t kk, uint32_t* s
 }
 
 // fp64 cosine Selection Cache decision (tensor.cpp:92-113,
-// selection_cache.cpp:29-35). Deterministic block reduction: every CTA that
-// evaluates it for the same sequence gets a bit-identical result.
-// Returns 1 = miss, 0 = hit, 2 = zero query (error).
-__device__ int cache_decision(const SeqDesc& sd, int width, double* scratch_d, double* cos_out) {
-  const CacheState* cs = sd.cache;
+// selection_cache.cpp:29-35). The first kDecU * blockDim elements of q and
+// the cached query arrive preloaded in registers (issued together with the
+// other phase-0 loads); any rest is loaded here. Deterministic block
+// reduction: every CTA that evaluates it for the same sequence gets a
+// bit-identical result. Returns 1 = miss, 0 = hit, 2 = zero query (error).
+constexpr int kDecU = 8;
+
+struct DecisionLoads {
+  float qa[kDecU], qb[kDecU];
+  int first_flag;
+  double theta;
+};
+
+__device__ __forceinline__ void decision_issue(const SeqDesc& sd, int width, DecisionLoads& L) {
+#pragma unroll
+  for (int u = 0; u < kDecU; ++u) {
+    const int i = threadIdx.x + u * blockDim.x;
+    L.qa[u] = i < width ? __ldg(sd.q + i) : 0.f;
+    L.qb[u] = i < width ? __ldcg(sd.cached_q + i) : 0.f;
+  }
+  L.first_flag = __ldcg(&sd.cache->first_flag);
+  L.theta = __ldcg(&sd.cache->theta);
+}
+
+__device__ int cache_decision(const SeqDesc& sd, int width, const DecisionLoads& L, double* scratch_d,
+                              double* cos_out) {
   double dot = 0.0, nu = 0.0, nv = 0.0;
   int nonzero = 0;
-  constexpr int kU = 8;  // loads in flight per thread
-  for (int base = threadIdx.x; base < width; base += kU * blockDim.x) {
-    float qa[kU], qb[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int i = base + u * blockDim.x;
-      qa[u] = i < width ? __ldg(sd.q + i) : 0.f;
-      qb[u] = i < width ? __ldcg(sd.cached_q + i) : 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const double a = static_cast<double>(qa[u]);
-      const double b = static_cast<double>(qb[u]);
-      nonzero |= (qa[u] != 0.0f);
-      dot = fma(a, b, dot);
-      nu = fma(a, a, nu);
-      nv = fma(b, b, nv);
-    }
+  for (int u = 0; u < kDecU; ++u) {
+    const double a = static_cast<double>(L.qa[u]);
+    const double b = static_cast<double>(L.qb[u]);
+    nonzero |= (L.qa[u] != 0.0f);
+    dot = fma(a, b, dot);
+    nu = fma(a, a, nu);
+    nv = fma(b, b, nv);
   }
-  nonzero = __syncthreads_or(nonzero);
+  for (int i = threadIdx.x + kDecU * blockDim.x; i < width; i += blockDim.x) {
+    const float fa = __ldg(sd.q + i), fb = __ldcg(sd.cached_q + i);
+    const double a = static_cast<double>(fa), b = static_cast<double>(fb);
+    nonzero |= (fa != 0.0f);
+    dot = fma(a, b, dot);
+    nu = fma(a, a, nu);
+    nv = fma(b, b, nv);
+  }
   dot = warp_sum_d(dot);
   nu = warp_sum_d(nu);
   nv = warp_sum_d(nv);
+  nonzero = __any_sync(0xffffffffu, nonzero);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) {
-    scratch_d[warp * 3 + 0] = dot;
-    scratch_d[warp * 3 + 1] = nu;
-    scratch_d[warp * 3 + 2] = nv;
+    scratch_d[warp * 4 + 0] = dot;
+    scratch_d[warp * 4 + 1] = nu;
+    scratch_d[warp * 4 + 2] = nv;
+    scratch_d[warp * 4 + 3] = nonzero ? 1.0 : 0.0;
   }
   __syncthreads();
   // every warp reduces the per-warp partials in the same fixed tree order
-  double D = lane < kDecodeWarps ? scratch_d[lane * 3 + 0] : 0.0;
-  double U = lane < kDecodeWarps ? scratch_d[lane * 3 + 1] : 0.0;
-  double V = lane < kDecodeWarps ? scratch_d[lane * 3 + 2] : 0.0;
+  const int nw = blockDim.x >> 5;
+  double D = lane < nw ? scratch_d[lane * 4 + 0] : 0.0;
+  double U = lane < nw ? scratch_d[lane * 4 + 1] : 0.0;
+  double V = lane < nw ? scratch_d[lane * 4 + 2] : 0.0;
+  const int nz = __any_sync(0xffffffffu, lane < nw && scratch_d[lane * 4 + 3] != 0.0);
   D = warp_sum_d(D);
   U = warp_sum_d(U);
   V = warp_sum_d(V);
   __syncthreads();
-  if (!nonzero) return 2;
+  if (!nz) return 2;
   *cos_out = NAN;
-  if (cs->first_flag) return 1;
+  if (L.first_flag) return 1;
   if (U == 0.0 || V == 0.0) return 1;  // unreachable: cached query is never zero
   double c;
   if (D * D >= U * V) c = D >= 0.0 ? 1.0 : -1.0;  // exact +-1 clamp
   else c = D / sqrt(U * V);
   *cos_out = c;
-  return c < cs->theta ? 1 : 0;  // strict <
+  return c < L.theta ? 1 : 0;  // strict <
 }
 
 // --------------------------------------------------------------- the scan
@@ -303,7 +329,10 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
   }
   // this lane's C fragment: rows lane/4 (+8), columns (heads) 2*(lane%4) + {0,1}
   const int g0 = (lane & 3) * 2;
-  float runmax0 = -INFINITY, runmax1 = -INFINITY;
+  // online softmax partials of this lane's two heads: m = running max,
+  // z = sum exp(S - m) (rescaled when m grows) -- the per-CTA (m, z) of
+  // softmax_rows (tensor.cpp:31-52) come out of the scan with no extra pass
+  float runmax0 = -INFINITY, runmax1 = -INFINITY, z0 = 0.f, z1 = 0.f;
   // ldmatrix row address: matrix lane/8 -> rows +8 for odd, cols +8 for >= 16
   const uint32_t lrow = static_cast<uint32_t>((lane & 7) + ((lane >> 3) & 1) * 8);
   const uint32_t lcol = static_cast<uint32_t>((lane >> 4) * 16 + kvh * D * 2);
@@ -326,21 +355,55 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[s]);  // operands consumed
     const int rbase = it * R + (lane >> 2);
+    float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int g = g0 + (e & 1);
       const int row = rbase + (e >> 1) * 8;
+      v[e] = -INFINITY;
       if (g < G && row < nloc) {
         const int h = g * Hkv + kvh;
         Sbuf[static_cast<size_t>(h) * sstride + row] = c[e];
         if (s_out_row0) s_out_row0[static_cast<size_t>(h) * sd.n_cand + row] = c[e];
-        if (e & 1) runmax1 = fmaxf(runmax1, c[e]);
-        else runmax0 = fmaxf(runmax0, c[e]);
+        v[e] = c[e];
+      }
+    }
+    {
+      const float mA = fmaxf(runmax0, fmaxf(v[0], v[2]));
+      if (mA > -INFINITY) {
+        z0 = z0 * fast_exp(runmax0 - mA) + fast_exp(v[0] - mA) + fast_exp(v[2] - mA);
+        runmax0 = mA;
+      }
+      const float mB = fmaxf(runmax1, fmaxf(v[1], v[3]));
+      if (mB > -INFINITY) {
+        z1 = z1 * fast_exp(runmax1 - mB) + fast_exp(v[1] - mB) + fast_exp(v[3] - mB);
+        runmax1 = mB;
       }
     }
   }
-  if (g0 < G && runmax0 > -INFINITY) atomicMax(&sm.headmax[g0 * Hkv + kvh], float_ord(runmax0));
-  if (g0 + 1 < G && runmax1 > -INFINITY) atomicMax(&sm.headmax[(g0 + 1) * Hkv + kvh], float_ord(runmax1));
+  // combine the 8 lanes (rows) of each head pair, then hand (m, z) of this
+  // warp's heads to shared memory: mz[(h * nphase + phase) * 2]
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    const float m2a = __shfl_xor_sync(0xffffffffu, runmax0, o), z2a = __shfl_xor_sync(0xffffffffu, z0, o);
+    const float m2b = __shfl_xor_sync(0xffffffffu, runmax1, o), z2b = __shfl_xor_sync(0xffffffffu, z1, o);
+    const float ma = fmaxf(runmax0, m2a), mb = fmaxf(runmax1, m2b);
+    z0 = (runmax0 == -INFINITY ? 0.f : z0 * fast_exp(runmax0 - ma)) + (m2a == -INFINITY ? 0.f : z2a * fast_exp(m2a - ma));
+    z1 = (runmax1 == -INFINITY ? 0.f : z1 * fast_exp(runmax1 - mb)) + (m2b == -INFINITY ? 0.f : z2b * fast_exp(m2b - mb));
+    runmax0 = ma;
+    runmax1 = mb;
+  }
+  float* mz = reinterpret_cast<float*>(sm.scratch);
+  if (lane < 4) {
+    if (g0 < G) {
+      mz[((g0 * Hkv + kvh) * nphase + phase) * 2 + 0] = runmax0;
+      mz[((g0 * Hkv + kvh) * nphase + phase) * 2 + 1] = z0;
+    }
+    if (g0 + 1 < G) {
+      mz[(((g0 + 1) * Hkv + kvh) * nphase + phase) * 2 + 0] = runmax1;
+      mz[(((g0 + 1) * Hkv + kvh) * nphase + phase) * 2 + 1] = z1;
+    }
+  }
 }
 
 // Generic path (any H, H_kv, d, page_size): one thread per (head, token),
@@ -369,7 +432,7 @@ __device__ void scan_generic(const DecodeParams& p, const SeqDesc& sd, const Sme
 // bits above `pshift` equal `prefix`), aggregated per warp with match.any so a
 // crowded bin costs one shared atomic per warp, then merged into the
 // sequence's global histogram `gh`. All threads call.
-__device__ void radix_hist(const uint32_t* keys, int nloc, int shift, int pshift, uint32_t prefix,
+__device__ __noinline__ void radix_hist(const uint32_t* keys, int nloc, int shift, int pshift, uint32_t prefix,
                            uint32_t* hist, uint32_t* gh) {
   const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < kRadixBins; i += blockDim.x) hist[i] = 0u;
@@ -393,6 +456,25 @@ __device__ void radix_hist(const uint32_t* keys, int nloc, int shift, int pshift
   for (int i = tid; i < kRadixBins; i += blockDim.x) {
     const uint32_t c = hist[i];
     if (c) atomicAdd(gh + i, c);
+  }
+}
+
+// Adds this CTA's non-empty shared-histogram bins into the global one.
+__device__ __noinline__ void hist_merge(const uint32_t* hist, uint32_t* gh) {
+  for (int i = threadIdx.x; i < kRadixBins; i += blockDim.x) {
+    const uint32_t c = hist[i];
+    if (c) atomicAdd(gh + i, c);
+  }
+}
+
+// One key into the shared histogram, aggregated over the warp's lanes that
+// hit the same bin (all lanes call; `act` marks the lanes with a key).
+__device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t key, bool act, int shift) {
+  const unsigned am = __ballot_sync(0xffffffffu, act);
+  if (act) {
+    const uint32_t bin = (key >> shift) & (kRadixBins - 1);
+    const unsigned peers = __match_any_sync(am, bin);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], static_cast<uint32_t>(__popc(peers)));
   }
 }
 
@@ -575,6 +657,7 @@ __device__ void attend_group(const DecodeParams& p, const SeqDesc& sd, const Att
     for (int r = tid; r < nw; r += blockDim.x)
       ridx[r] = static_cast<int32_t>(row_index(sd, att_token(p, sd, av, sm.prefix, r0 + w0 + r), p.page_size));
     __syncthreads();
+    trace_pt(p, 20);
     const bool last_w = w0 + nw >= nrows;
     const int nsub = max(1, (nw + cap - 1) / cap);
     issue(0, min(cap, nw), sub & 1);
@@ -592,6 +675,7 @@ __device__ void attend_group(const DecodeParams& p, const SeqDesc& sd, const Att
       __syncthreads();
       const uint16_t* K = kb[sub & 1];
       const uint16_t* V = vb[sub & 1];
+      if (sub == 0) trace_pt(p, 21);
       // ---- scores s[r][m] = q_m . k_r / sqrt(d)
       for (int r = warp; r < nrt; r += nwarps) {
         if constexpr (kFast) {
@@ -643,6 +727,7 @@ __device__ void attend_group(const DecodeParams& p, const SeqDesc& sd, const Att
         }
       }
       __syncthreads();
+      if (sub == 0) trace_pt(p, 22);
       // ---- online softmax per head (warp m owns head m)
       for (int m = warp; m < G; m += nwarps) {
         float mx = -INFINITY;
@@ -665,6 +750,7 @@ __device__ void attend_group(const DecodeParams& p, const SeqDesc& sd, const Att
         }
       }
       __syncthreads();
+      if (sub == 0) trace_pt(p, 23);
       // ---- P.V: thread (row group rg, element pair pi) over rows rg, rg + RG, ...
       if (rg < RG) {
 #pragma unroll
@@ -694,10 +780,12 @@ __device__ void attend_group(const DecodeParams& p, const SeqDesc& sd, const Att
         }
       }
       __syncthreads();  // buffer and probs free for the next sub-chunk
+      if (sub == 0) trace_pt(p, 24);
     }
     w0 += nw;
     if (last_w) break;
   }
+  trace_pt(p, 25);
   // ---- reduce the row groups, write the partial record per head
   if (rg < RG) {
 #pragma unroll
@@ -723,23 +811,63 @@ __device__ void attend_group(const DecodeParams& p, const SeqDesc& sd, const Att
 
 // Log-sum-exp merge of the row-chunk partials of KV head g (attention.cpp
 // :88-110 semantics): out[h] = sum_c e^(m_c - M) o_c / sum_c e^(m_c - M) l_c.
-__device__ void merge_group(const DecodeParams& p, const SeqDesc& sd, int g, const float* parts, int chunks) {
+// All (m, l) pairs are loaded in one parallel pass, the weights formed in
+// shared memory, then the o vectors are staged batch by batch with 16-byte
+// loads (every global load of a batch in flight at once).
+__device__ void merge_group(const DecodeParams& p, const SeqDesc& sd, const Smem& sm, int g, const float* parts,
+                            int chunks) {
   const int d = p.d, G = p.H / p.H_kv, stride = att_stride(d);
-  const size_t cstride = static_cast<size_t>(G) * stride;
-  for (int i = threadIdx.x; i < G * d; i += blockDim.x) {
-    const int m = i / d, t = i - (i / d) * d;
-    const float* pm = parts + static_cast<size_t>(m) * stride;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+  float* wts = reinterpret_cast<float*>(sm.ring);                  // [chunks][G] (m, then weight)
+  float* ls = wts + align_up(static_cast<size_t>(chunks) * G, 32);  // [chunks][G] l
+  float* linv = ls + align_up(static_cast<size_t>(chunks) * G, 32); // [G]
+  float* obuf = linv + 32;                                          // [batch][G][stride]
+  for (int i = tid; i < chunks * G; i += blockDim.x) {
+    wts[i] = __ldcg(parts + static_cast<size_t>(i) * stride + d);
+    ls[i] = __ldcg(parts + static_cast<size_t>(i) * stride + d + 1);
+  }
+  __syncthreads();
+  for (int m = warp; m < G; m += nwarps) {
     float M = -INFINITY;
-    for (int c = 0; c < chunks; ++c) M = fmaxf(M, __ldcg(pm + c * cstride + d));
-    float num = 0.f, den = 0.f;
-    for (int c = 0; c < chunks; ++c) {
-      const float mc = __ldcg(pm + c * cstride + d);
-      if (mc == -INFINITY) continue;
-      const float w = expf(mc - M);
-      num = fmaf(w, __ldcg(pm + c * cstride + t), num);
-      den = fmaf(w, __ldcg(pm + c * cstride + d + 1), den);
+    for (int c = lane; c < chunks; c += 32) M = fmaxf(M, wts[c * G + m]);
+    M = warp_max(M);
+    float L = 0.f;
+    for (int c = lane; c < chunks; c += 32) {
+      const float mc = wts[c * G + m];
+      const float w = mc == -INFINITY ? 0.f : expf(mc - M);
+      wts[c * G + m] = w;
+      L = fmaf(w, ls[c * G + m], L);
     }
-    sd.out[static_cast<size_t>(g + m * p.H_kv) * d + t] = num / den;
+    L = warp_sum(L);
+    if (lane == 0) linv[m] = 1.f / L;
+  }
+  const size_t rec = static_cast<size_t>(G) * stride;  // floats per chunk
+  const size_t room = static_cast<size_t>(p.att_bytes) / 4 - (obuf - wts);
+  const bool staged = static_cast<size_t>(chunks) * rec <= room;
+  if (staged) {  // every o vector in one parallel pass (the usual case)
+    const int n4 = static_cast<int>(chunks * rec / 4);
+    const float4* src = reinterpret_cast<const float4*>(parts);
+    float4* dst = reinterpret_cast<float4*>(obuf);
+    const int bd = blockDim.x;
+#pragma unroll 1
+    for (int i0 = tid; i0 < n4; i0 += 8 * bd) {  // 8 loads in flight per thread
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = i0 + u * bd < n4 ? __ldcg(src + i0 + u * bd) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (i0 + u * bd < n4) dst[i0 + u * bd] = v[u];
+    }
+  }
+  __syncthreads();
+  const float* ob = staged ? obuf : parts;
+#pragma unroll 1
+  for (int i = tid; i < G * d; i += blockDim.x) {
+    const int m = i / d, t = i - (i / d) * d;
+    float a = 0.f;
+#pragma unroll 1
+    for (int c = 0; c < chunks; ++c) a = fmaf(wts[c * G + m], ob[c * rec + m * stride + t], a);
+    sd.out[static_cast<size_t>(g + m * p.H_kv) * d + t] = a * linv[m];
   }
 }
 
@@ -774,6 +902,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   if (cta == 0 && tid == 0) p.bar[p.bar_slot ^ 32] = 0u;  // the next launch's counter
 
   trace_pt(p, 0);
+  if (p.debug_flags & 16) return;  // dev timing: launch + prologue only
   // ---- phase 0: append, scan frames, Selection Cache decision(s), hit prep
   if ((p.mode & kModeAppend) && cs == 0 && sd.append_frame >= 0) {
     const int row = p.H_kv * p.d;
@@ -796,28 +925,19 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     const int jl = tid + u * blockDim.x;
     fr_pre[u] = (may_scan && jl < nloc) ? static_cast<int32_t>(row_index(sd, cand_at(sd, j0 + jl), p.page_size)) : 0;
   }
-  // hit prep: count the cached selection below init_end / local_begin
+  // hit prep: the cached selection (counted below init_end / local_begin after the decision)
   const bool hit_prep = !sd.att_list && sd.select && (p.mode & kModeCache) && (p.mode & kModeAttend);
   const uint32_t ie = static_cast<uint32_t>(sd.init_end);
   const uint32_t lbs = static_cast<uint32_t>(max(sd.local_begin, sd.init_end));
-  uint32_t cie = 0, clb = 0;
+  uint32_t selv[4];
   int n_sel_prev = 0;
+  const bool sel_small = p.k <= 4 * static_cast<int>(blockDim.x);
   if (hit_prep) {
     n_sel_prev = __ldcg(&sd.cache->n_sel);
-    for (int base = tid; base < p.k; base += 4 * blockDim.x) {
-      uint32_t v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = base + u * blockDim.x;
-        v[u] = i < p.k ? __ldcg(sd.sel + i) : 0xffffffffu;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = base + u * blockDim.x;
-        const bool in = i < n_sel_prev;
-        cie += in && v[u] < ie;
-        clb += in && v[u] < lbs;
-      }
+    for (int u = 0; u < 4; ++u) {
+      const int i = tid + u * blockDim.x;
+      selv[u] = i < p.k ? __ldcg(sd.sel + i) : 0xffffffffu;
     }
   }
   // Selection Cache decisions. A single sequence: every CTA evaluates it
@@ -829,11 +949,31 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   double own_cos = NAN;
   if (sd.select) {
     if (p.mode & kModeCache) {
-      const int dec = cache_decision(sd, width, scratch_d, &own_cos);
+      DecisionLoads dl;
+      decision_issue(sd, width, dl);
+      trace_pt(p, 26);
+      const int dec = cache_decision(sd, width, dl, scratch_d, &own_cos);
       own = dec == 1 ? 1 : dec == 0 ? 2 : 3;
     } else {
       own = 1;
     }
+  }
+  trace_pt(p, 27);
+  uint32_t cie = 0, clb = 0;
+  if (hit_prep && own == 2) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = tid + u * blockDim.x;
+      const bool in = i < n_sel_prev;
+      cie += in && selv[u] < ie;
+      clb += in && selv[u] < lbs;
+    }
+    if (!sel_small)
+      for (int i = tid + 4 * blockDim.x; i < n_sel_prev; i += blockDim.x) {
+        const uint32_t v = __ldcg(sd.sel + i);
+        cie += v < ie;
+        clb += v < lbs;
+      }
   }
   int any_select = 0, any_radix = 0;
   if (p.n_seq == 1) {
@@ -881,40 +1021,48 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   }
   __syncthreads();
   trace_pt(p, 2);
+  if (p.debug_flags & 2) return;  // dev timing: stop after the scan
 
-  // ---- phase 2: per-CTA softmax partials m = max_j S, z = sum_j e^(S - m); S <- e^(S - m)
+  // ---- phase 2: per-CTA softmax partials (m, z) per head (softmax_rows, tensor.cpp:31-52)
   if (do_select && own == 1 && p.method == 2) {
-    const int warp = tid >> 5, lane = tid & 31;
-    for (int h = warp; h < H; h += kDecodeWarps) {
-      const float m = ord_float(sm.headmax[h]);
-      float z0 = 0.f, z1 = 0.f;
-      float* sr = Sbuf + static_cast<size_t>(h) * sstride;
-      if (m > -INFINITY) {
-        int jl = lane;
-        for (; jl + 32 < nloc; jl += 64) {
-          const float e0 = fast_exp(sr[jl] - m), e1 = fast_exp(sr[jl + 32] - m);
-          sr[jl] = e0;
-          sr[jl + 32] = e1;
-          z0 += e0;
-          z1 += e1;
-        }
-        for (; jl < nloc; jl += 32) {
-          const float e = fast_exp(sr[jl] - m);
-          sr[jl] = e;
-          z0 += e;
-        }
+    const size_t so = static_cast<size_t>(seq_id) * H * stats_stride(p.ctas_per_seq) + cs;
+    const size_t sh = stats_stride(p.ctas_per_seq);
+    if (FAST && !(p.mode & kModeSIn)) {
+      // the scan's per-warp online partials (scan_fast epilogue)
+      const float* mz = reinterpret_cast<const float*>(sm.scratch);
+      const int nphase = kDecodeConsumers / p.H_kv;
+      for (int h = tid; h < H; h += blockDim.x) {
+        float m = -INFINITY;
+        for (int ph = 0; ph < nphase; ++ph) m = fmaxf(m, mz[(h * nphase + ph) * 2]);
+        float z = 0.f;
+        if (m > -INFINITY)
+          for (int ph = 0; ph < nphase; ++ph) {
+            const float mp = mz[(h * nphase + ph) * 2];
+            if (mp > -INFINITY) z += mz[(h * nphase + ph) * 2 + 1] * fast_exp(mp - m);
+          }
+        p.ws_m[so + h * sh] = m;
+        p.ws_z[so + h * sh] = z;
       }
-      const float z = warp_sum(z0 + z1);
-      if (lane == 0) {
-        const size_t o = (static_cast<size_t>(seq_id) * H + h) * stats_stride(p.ctas_per_seq) + cs;
-        p.ws_m[o] = m;
-        p.ws_z[o] = z;
+    } else {
+      const int warp = tid >> 5, lane = tid & 31;
+      for (int h = warp; h < H; h += kDecodeWarps) {
+        const float m = ord_float(sm.headmax[h]);
+        float z = 0.f;
+        const float* sr = Sbuf + static_cast<size_t>(h) * sstride;
+        if (m > -INFINITY)
+          for (int jl = lane; jl < nloc; jl += 32) z += fast_exp(sr[jl] - m);
+        z = warp_sum(z);
+        if (lane == 0) {
+          p.ws_m[so + h * sh] = m;
+          p.ws_z[so + h * sh] = z;
+        }
       }
     }
   }
   trace_pt(p, 3);
   if (any_select) gs.sync();  // B1: softmax partials of every CTA visible
   trace_pt(p, 4);
+  if (p.debug_flags & 4) return;  // dev timing: stop after B1
 
   // ---- phase 3: criticality (soft vote / raw sum) + cache bookkeeping
   if (cs == 0 && tid == 0 && (p.mode & kModeCache) && (own == 1 || own == 2)) {
@@ -931,8 +1079,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   }
   const bool radix_own = do_select && own == 1 && T > p.k;
   if (do_select && own == 1) {
+    float* ml = sm.f;                                   // [H] M_h * log2(e)
+    float* iz = reinterpret_cast<float*>(sm.headmax);  // [H] 1 / Z_h (headmax is dead)
     if (p.method == 2) {
-      const int warp = tid >> 5, lane = tid & 31;
       float* pm = reinterpret_cast<float*>(sm.ring);
       const int nc = p.ctas_per_seq;
       const int ncp = stats_stride(nc);
@@ -945,34 +1094,74 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       const float* pz = pm + H * ncp;
       mbar_wait(sm.aux, aux_phase);
       aux_phase ^= 1u;
-      for (int h = warp; h < H; h += kDecodeWarps) {
+      trace_pt(p, 13);
+      // M_h = max_c m_c, Z_h = sum_c z_c e^(m_c - M_h): 16 threads per head
+      const int sub = tid & 15;
+      for (int h0 = 0; h0 < H; h0 += blockDim.x >> 4) {  // warp-uniform trip count
+        const int h = h0 + (tid >> 4);
+        const bool hv = h < H;
         float M = -INFINITY;
-        for (int c = lane; c < nc; c += 32) M = fmaxf(M, pm[h * ncp + c]);
-        M = warp_max(M);
+        if (hv)
+          for (int c = sub; c < nc; c += 16) M = fmaxf(M, pm[h * ncp + c]);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
         float Z = 0.f;
-        for (int c = lane; c < nc; c += 32) {
-          const float mc = pm[h * ncp + c];
-          if (mc > -INFINITY) Z += pz[h * ncp + c] * fast_exp(mc - M);
-        }
-        Z = warp_sum(Z);
-        if (lane == 0) {
-          const float ms = ord_float(sm.headmax[h]);
-          sm.f[h] = (ms > -INFINITY) ? fast_exp(ms - M) / Z : 0.f;
+        if (hv)
+          for (int c = sub; c < nc; c += 16) {
+            const float mc = pm[h * ncp + c];
+            if (mc > -INFINITY) Z += pz[h * ncp + c] * fast_exp(mc - M);
+          }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);
+        if (hv && sub == 0) {
+          ml[h] = M * 1.4426950408889634f;
+          iz[h] = 1.f / Z;
         }
       }
       __syncthreads();
-      // crit[j] = sum_h softmax_h(S)[j] (select_head_soft_vote, selector.cpp:113-126)
-      for (int jl = tid; jl < nloc; jl += blockDim.x) {
-        float c = 0.f;
-        for (int h = 0; h < H; ++h) c = fmaf(Sbuf[static_cast<size_t>(h) * sstride + jl], sm.f[h], c);
-        keys[jl] = float_key(c);
+      trace_pt(p, 14);
+    }
+    if (radix_own) {
+      for (int i = tid; i < kRadixBins; i += blockDim.x) sm.hist[i] = 0u;
+      __syncthreads();
+    }
+    // crit[j] = sum_h softmax_h(S)[j] (select_head_soft_vote, selector.cpp:113-126)
+    // or the raw logit sum (select_topk, selector.cpp:89-99); four
+    // candidates per thread, keys straight into the pass-1 histogram
+    const int n4 = (nloc + 3) >> 2;
+    for (int base = 0; base < n4; base += blockDim.x) {
+      const int q = base + tid;
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
+      if (q < n4) {
+        const float* s4 = Sbuf + 4 * q;
+        if (p.method == 2) {
+#pragma unroll 2
+          for (int h = 0; h < H; ++h) {
+            const float4 sv = *reinterpret_cast<const float4*>(s4 + static_cast<size_t>(h) * sstride);
+            const float mh = ml[h], ih = iz[h];
+            c[0] = fmaf(ex2_approx(fmaf(sv.x, 1.4426950408889634f, -mh)), ih, c[0]);
+            c[1] = fmaf(ex2_approx(fmaf(sv.y, 1.4426950408889634f, -mh)), ih, c[1]);
+            c[2] = fmaf(ex2_approx(fmaf(sv.z, 1.4426950408889634f, -mh)), ih, c[2]);
+            c[3] = fmaf(ex2_approx(fmaf(sv.w, 1.4426950408889634f, -mh)), ih, c[3]);
+          }
+        } else {
+#pragma unroll 2
+          for (int h = 0; h < H; ++h) {
+            const float4 sv = *reinterpret_cast<const float4*>(s4 + static_cast<size_t>(h) * sstride);
+            c[0] += sv.x;
+            c[1] += sv.y;
+            c[2] += sv.z;
+            c[3] += sv.w;
+          }
+        }
       }
-    } else {
-      // raw logit sum (select_topk, selector.cpp:89-99)
-      for (int jl = tid; jl < nloc; jl += blockDim.x) {
-        float c = 0.f;
-        for (int h = 0; h < H; ++h) c += Sbuf[static_cast<size_t>(h) * sstride + jl];
-        keys[jl] = float_key(c);
+      uint32_t kq[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) kq[e] = float_key(c[e]);
+      if (q < n4) *reinterpret_cast<uint4*>(keys + 4 * q) = make_uint4(kq[0], kq[1], kq[2], kq[3]);
+      if (radix_own) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) hist_add(sm.hist, kq[e], q < n4 && 4 * q + e < nloc, 20);
       }
     }
     __syncthreads();
@@ -987,29 +1176,34 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   uint32_t kk = static_cast<uint32_t>(p.k);
   if (any_radix) {
     uint32_t* gh = p.ws_hist + static_cast<size_t>(seq_id) * 2 * kRadixBins;
-    if (radix_own) radix_hist(keys, nloc, 20, 32, 0u, sm.hist, gh);
+    if (radix_own) hist_merge(sm.hist, gh);
+    trace_pt(p, 15);
     gs.sync();  // B2
     trace_pt(p, 6);
     uint32_t b1 = 0;
     if (radix_own) {
       int b;
       uint32_t above;
-      find_bin(gh, kRadixBins, kk, sm.scratch, &b, &above);
+      find_bin(gh, kk, sm.scratch, &b, &above);
       kk -= above;
       b1 = static_cast<uint32_t>(b);
+      trace_pt(p, 16);
       radix_hist(keys, nloc, 8, 20, b1, sm.hist, gh + kRadixBins);
     }
+    trace_pt(p, 17);
     gs.sync();  // B3
     trace_pt(p, 7);
+    if (p.debug_flags & 32) return;  // dev timing: stop after B3
     uint32_t eq_total = 0;
     if (radix_own) {
       int b;
       uint32_t above;
-      find_bin(gh + kRadixBins, kRadixBins, kk, sm.scratch, &b, &above);
+      find_bin(gh + kRadixBins, kk, sm.scratch, &b, &above);
       kk -= above;
       tau = (b1 << 12) | static_cast<uint32_t>(b);
       eq_total = __ldcg(gh + kRadixBins + b);
     }
+    trace_pt(p, 18);
     // ties straddling the budget: the taken ones are the lowest positions,
     // which needs every CTA's tie count (one more exchange)
     int need_tie = 0;
@@ -1027,6 +1221,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       if (radix_own && eq_total > kk) {
         uint32_t pre = 0;
         if (tid < 32) {
+#pragma unroll 1
           for (int c = tid; c < cs; c += 32) pre += __ldcg(p.ws_cnt + c0 + c);
           pre = __reduce_add_sync(0xffffffffu, pre);
           if (tid == 0) sm.scratch[70] = pre;
@@ -1040,6 +1235,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     }
   }
 
+  trace_pt(p, 19);
   // ---- phase 5: ascending compaction of this CTA's selected candidates
   if (do_select && own == 1) {
     uint32_t out_n = 0, eq_seen = 0;
@@ -1092,7 +1288,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     if (cs == 0 && tid == 0) sd.cache->n_sel = static_cast<int>(tot);
   }
   trace_pt(p, 10);
-  if (!(p.mode & kModeAttend)) return;
+  if (!(p.mode & kModeAttend) || (p.debug_flags & 8)) return;
 
   // ---- phase 7: split-K sparse flash-decoding (KV head x row chunk)
   AttView av{};
@@ -1140,7 +1336,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
         sm.scratch[71] = last;
       }
       __syncthreads();
-      if (sm.scratch[71]) merge_group(p, sd, g, parts, split.chunks);
+      if (sm.scratch[71]) merge_group(p, sd, sm, g, parts, split.chunks);
       __syncthreads();
     }
   }

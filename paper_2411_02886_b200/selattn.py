@@ -329,6 +329,11 @@ class Engine:
 
     TRACE_POINTS = ["start", "decision", "scan", "softmax_partials", "sync1", "crit", "radix1", "radix2",
                     "compact", "sync4", "sel_out", "attend", "merge"]
+    # sub-phase stamps (slots 13..31) of read_trace(all_ctas=True)
+    SUB_POINTS = {13: "crit:stats_staged", 14: "crit:f_done", 15: "radix:hist1", 16: "radix:find1",
+                  17: "radix:hist2", 18: "radix:find2", 19: "radix:ties", 20: "att:ridx", 21: "att:data",
+                  22: "att:scores", 23: "att:softmax", 24: "att:pv", 25: "att:end", 26: "dec:issued",
+                  27: "dec:done"}
 
     def set_trace(self, enable=True):
         check(lib.ts_engine_set_trace(self._h, 1 if enable else 0))

@@ -55,9 +55,10 @@ for mode, theta in (("miss", 2.0), ("hit", -2.0)):
         eng.decode_async(q, kt, vt, out)
     torch.cuda.synchronize()
     a = eng.read_trace(all_ctas=True)
-    names = sa.Engine.TRACE_POINTS
+    names = dict(enumerate(sa.Engine.TRACE_POINTS))
+    names.update(sa.Engine.SUB_POINTS)
     print(f"{mode}: all-CTA stamps (us from earliest start): phase: min / median / max")
-    for i, nm in enumerate(names):
+    for i, nm in sorted(names.items(), key=lambda kv: np.nanmedian(a[:, kv[0]]) if np.any(~np.isnan(a[:, kv[0]])) else 1e9):
         col = a[:, i]
         col = col[~np.isnan(col)]
         if col.size:
