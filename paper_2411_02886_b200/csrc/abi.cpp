@@ -7,11 +7,13 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -37,7 +39,14 @@ int g_prefetch_stages = [] {
 const bool g_force_global_s = std::getenv("TS_FORCE_GLOBAL_S") != nullptr && std::getenv("TS_FORCE_GLOBAL_S")[0];
 const int g_debug_flags = std::getenv("TS_DEBUG_FLAGS") ? std::atoi(std::getenv("TS_DEBUG_FLAGS")) : 0;
 std::atomic<uint64_t> g_launches{0};
-constexpr size_t kTraceSlots = 32 * 1024;  // [cta][32] %globaltimer stamps (<= 1024 CTAs)
+constexpr size_t kTraceSlots = 32 * 1024;
+// host-side profile of the decode launch path (TS_HOST_PROF=1): ns per stage
+const bool g_host_prof = std::getenv("TS_HOST_PROF") != nullptr;
+double g_prof[4] = {0, 0, 0, 0};
+uint64_t g_prof_n = 0;
+inline double now_ns() {
+  return std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}  // [cta][32] %globaltimer stamps (<= 1024 CTAs)
 
 struct ts_error : std::runtime_error {
   ts_status code;
@@ -110,13 +119,16 @@ struct DevBuf {
   ~DevBuf() {
     if (p) cudaFree(p);
   }
+  // grows geometrically: workspaces track the context length step by step,
+  // and every reallocation (cudaFree) synchronises the device
   void* ensure(size_t bytes) {
     if (bytes <= n) return p;
     if (p) cudaFree(p);
     p = nullptr;
+    const size_t want = std::max<size_t>({bytes, n + n / 2, 256});
     n = 0;
-    ck(cudaMalloc(&p, std::max<size_t>(bytes, 256)), "cudaMalloc");
-    n = std::max<size_t>(bytes, 256);
+    ck(cudaMalloc(&p, want), "cudaMalloc");
+    n = want;
     return p;
   }
   template <typename T>
@@ -138,7 +150,7 @@ const T* dev_in(const T* p, size_t count, DevBuf& stage, cudaStream_t st) {
 // Per-launch workspaces of the fused kernel + its grid barrier and the
 // attention-merge arrival counters (both self-resetting across launches).
 struct Workspace {
-  DevBuf s, keys, m, z, hist, cnt, nsel, sel_tok, sel_crit, att, acnt, bar;
+  DevBuf s, keys, m, z, hist, cnt, nsel, sel_tok, sel_crit, sel_row, att, acnt, bar;
   size_t acnt_n = 0;
   unsigned launches = 0;
   void prepare(int n_ctas, int H, int H_kv, int d, int tpc, int s_in_smem, int n_seq, cudaStream_t st) {
@@ -154,6 +166,7 @@ struct Workspace {
     nsel.ensure(static_cast<size_t>(n_ctas) * 4);
     sel_tok.ensure(static_cast<size_t>(n_ctas) * tpc * 4);
     sel_crit.ensure(static_cast<size_t>(n_ctas) * tpc * 4);
+    sel_row.ensure(static_cast<size_t>(n_ctas) * tpc * 4);
     att.ensure(static_cast<size_t>(n_ctas) * H * tsb::att_stride(d) * 4);
     const size_t na = static_cast<size_t>(n_seq) * H_kv;
     if (na > acnt_n) {
@@ -222,6 +235,7 @@ void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t 
   p.ws_nsel = ws.nsel.as<uint32_t>();
   p.ws_sel_tok = ws.sel_tok.as<uint32_t>();
   p.ws_sel_crit = ws.sel_crit.as<float>();
+  p.ws_sel_row = ws.sel_row.as<int32_t>();
   p.ws_att = ws.att.as<float>();
   p.ws_acnt = ws.acnt.as<unsigned int>();
   p.bar = ws.bar.as<unsigned int>();
@@ -230,11 +244,21 @@ void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t 
   p.ring_bytes = pl.ring_bytes;
   p.att_bytes = pl.att_bytes;
   p.debug_flags = g_debug_flags;
-  ck(cudaFuncSetAttribute(pl.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)),
-     "cudaFuncSetAttribute");
+  // the dynamic shared-memory limit is set once per kernel (largest request so far)
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> smem_set;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = smem_set[pl.fn];
+  if (pl.smem > have) {
+    ck(cudaFuncSetAttribute(pl.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)),
+       "cudaFuncSetAttribute");
+    have = pl.smem;
+  }
   void* args[] = {&p};
+  const double t0 = g_host_prof ? now_ns() : 0.0;
   ck(cudaLaunchCooperativeKernel(pl.fn, dim3(n_ctas), dim3(tsb::kDecodeThreads), args, pl.smem, st),
      "decode kernel launch");
+  if (g_host_prof) g_prof[3] += now_ns() - t0;
   ws.launches += 1;
   g_launches.fetch_add(1);
 }
@@ -352,7 +376,7 @@ struct ts_engine {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   // per-sequence Selection Cache entries (device)
-  DevBuf cache_state, cached_q, sel, sel_crit;
+  DevBuf cache_state, cached_q, sel, sel_crit, sel_rows;
   // step IO staging (device) + pinned host mirrors
   DevBuf d_q, d_k, d_v, d_out;
   float* h_q = nullptr;
@@ -383,6 +407,7 @@ struct ts_engine {
   float* cq(size_t b) const { return cached_q.as<float>() + b * W(); }
   uint32_t* sl(size_t b) const { return sel.as<uint32_t>() + b * std::max<size_t>(cfg.k, 1); }
   float* sc(size_t b) const { return sel_crit.as<float>() + b * std::max<size_t>(cfg.k, 1); }
+  int32_t* sr(size_t b) const { return sel_rows.as<int32_t>() + b * std::max<size_t>(cfg.k, 1); }
 };
 
 namespace {
@@ -843,6 +868,7 @@ ts_status ts_engine_create(const ts_engine_config* cfg, size_t capacity_tokens, 
     e->cached_q.ensure(n_seqs * W * 4);
     e->sel.ensure(n_seqs * kk * 4);
     e->sel_crit.ensure(n_seqs * kk * 4);
+    e->sel_rows.ensure(n_seqs * kk * 4);
     e->d_q.ensure(n_seqs * W * 4);
     e->d_k.ensure(n_seqs * KW * 4);
     e->d_v.ensure(n_seqs * KW * 4);
@@ -866,7 +892,13 @@ ts_status ts_engine_create(const ts_engine_config* cfg, size_t capacity_tokens, 
   });
 }
 
-void ts_engine_destroy(ts_engine* eng) { delete eng; }
+void ts_engine_destroy(ts_engine* eng) {
+  if (g_host_prof && g_prof_n)
+    std::fprintf(stderr, "[tokenselect host prof] per step: params %.0f ns, plan %.0f ns, launch api %.0f ns (%llu steps)\n",
+                 g_prof[0] / g_prof_n, g_prof[1] / g_prof_n, g_prof[3] / g_prof_n,
+                 static_cast<unsigned long long>(g_prof_n));
+  delete eng;
+}
 
 ts_status ts_engine_set_stream(ts_engine* eng, void* stream) {
   return guarded([&] { eng->stream = stream ? static_cast<cudaStream_t>(stream) : eng->own_stream; });
@@ -901,6 +933,7 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
   std::vector<int> cap_fail(e->B, 0);
   cudaStream_t st = e->stream;
   for (size_t g0 = 0; g0 < e->B; g0 += tsb::kMaxSeqPerLaunch) {
+    const double t0 = g_host_prof ? now_ns() : 0.0;
     const size_t gn = std::min<size_t>(tsb::kMaxSeqPerLaunch, e->B - g0);
     DecodeParams p = base_params(&pool, static_cast<int>(c.num_heads), static_cast<int>(c.num_kv_heads),
                                  static_cast<int>(c.head_dim), static_cast<int>(c.k), c.selection_method,
@@ -931,6 +964,7 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
       sd.cached_q = e->cq(b);
       sd.sel = e->sl(b);
       sd.sel_crit = e->sc(b);
+      sd.sel_rows = e->sr(b);
       // frame for logical position N (page_size 1): LIFO pop, after-the-step failure
       if (pool.free_list.empty()) {
         cap_fail[b] = 1;
@@ -947,8 +981,15 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
       max_T = std::max(max_T, sd.n_cand);
       max_rows = std::max(max_rows, static_cast<int>(std::min(c.n_init, N) + std::min(c.k, N) + c.n_local + 1));
     }
+    const double t1 = g_host_prof ? now_ns() : 0.0;
     const Plan pl = make_plan(static_cast<int>(c.num_heads), static_cast<int>(c.num_kv_heads),
                               static_cast<int>(c.head_dim), static_cast<int>(gn), max_T, max_rows);
+    const double t2 = g_host_prof ? now_ns() : 0.0;
+    if (g_host_prof) {
+      g_prof[0] += t1 - t0;
+      g_prof[1] += t2 - t1;
+      g_prof_n += 1;
+    }
     p.trace = e->trace_on ? e->trace.as<unsigned long long>() : nullptr;
     if (p.trace) ck(cudaMemsetAsync(p.trace, 0, kTraceSlots * 8, st), "memset trace");
     launch_decode(p, pl, e->ws, st);

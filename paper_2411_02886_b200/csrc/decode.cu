@@ -252,6 +252,12 @@ __device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], uint32_t addr) {
                : "r"(addr));
 }
 
+__device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   const uint32_t l = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
   const uint32_t h = __bfloat16_as_ushort(__float2bfloat16_rn(hi));
@@ -329,10 +335,9 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
   }
   // this lane's C fragment: rows lane/4 (+8), columns (heads) 2*(lane%4) + {0,1}
   const int g0 = (lane & 3) * 2;
-  // online softmax partials of this lane's two heads: m = running max,
-  // z = sum exp(S - m) (rescaled when m grows) -- the per-CTA (m, z) of
-  // softmax_rows (tensor.cpp:31-52) come out of the scan with no extra pass
-  float runmax0 = -INFINITY, runmax1 = -INFINITY, z0 = 0.f, z1 = 0.f;
+  // running max of this lane's two heads (the consumers stay lean: they
+  // gate the ring's refill, so the scan's speed is theirs)
+  float runmax0 = -INFINITY, runmax1 = -INFINITY;
   // ldmatrix row address: matrix lane/8 -> rows +8 for odd, cols +8 for >= 16
   const uint32_t lrow = static_cast<uint32_t>((lane & 7) + ((lane >> 3) & 1) * 8);
   const uint32_t lcol = static_cast<uint32_t>((lane >> 4) * 16 + kvh * D * 2);
@@ -368,41 +373,18 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
         v[e] = c[e];
       }
     }
-    {
-      const float mA = fmaxf(runmax0, fmaxf(v[0], v[2]));
-      if (mA > -INFINITY) {
-        z0 = z0 * fast_exp(runmax0 - mA) + fast_exp(v[0] - mA) + fast_exp(v[2] - mA);
-        runmax0 = mA;
-      }
-      const float mB = fmaxf(runmax1, fmaxf(v[1], v[3]));
-      if (mB > -INFINITY) {
-        z1 = z1 * fast_exp(runmax1 - mB) + fast_exp(v[1] - mB) + fast_exp(v[3] - mB);
-        runmax1 = mB;
-      }
-    }
+    runmax0 = fmaxf(runmax0, fmaxf(v[0], v[2]));
+    runmax1 = fmaxf(runmax1, fmaxf(v[1], v[3]));
   }
-  // combine the 8 lanes (rows) of each head pair, then hand (m, z) of this
-  // warp's heads to shared memory: mz[(h * nphase + phase) * 2]
-#pragma unroll
-  for (int o = 4; o < 32; o <<= 1) {
-    const float m2a = __shfl_xor_sync(0xffffffffu, runmax0, o), z2a = __shfl_xor_sync(0xffffffffu, z0, o);
-    const float m2b = __shfl_xor_sync(0xffffffffu, runmax1, o), z2b = __shfl_xor_sync(0xffffffffu, z1, o);
-    const float ma = fmaxf(runmax0, m2a), mb = fmaxf(runmax1, m2b);
-    z0 = (runmax0 == -INFINITY ? 0.f : z0 * fast_exp(runmax0 - ma)) + (m2a == -INFINITY ? 0.f : z2a * fast_exp(m2a - ma));
-    z1 = (runmax1 == -INFINITY ? 0.f : z1 * fast_exp(runmax1 - mb)) + (m2b == -INFINITY ? 0.f : z2b * fast_exp(m2b - mb));
-    runmax0 = ma;
-    runmax1 = mb;
-  }
-  float* mz = reinterpret_cast<float*>(sm.scratch);
+  runmax0 = fmaxf(runmax0, __shfl_xor_sync(0xffffffffu, runmax0, 4));
+  runmax1 = fmaxf(runmax1, __shfl_xor_sync(0xffffffffu, runmax1, 4));
+  runmax0 = fmaxf(runmax0, __shfl_xor_sync(0xffffffffu, runmax0, 8));
+  runmax1 = fmaxf(runmax1, __shfl_xor_sync(0xffffffffu, runmax1, 8));
+  runmax0 = fmaxf(runmax0, __shfl_xor_sync(0xffffffffu, runmax0, 16));
+  runmax1 = fmaxf(runmax1, __shfl_xor_sync(0xffffffffu, runmax1, 16));
   if (lane < 4) {
-    if (g0 < G) {
-      mz[((g0 * Hkv + kvh) * nphase + phase) * 2 + 0] = runmax0;
-      mz[((g0 * Hkv + kvh) * nphase + phase) * 2 + 1] = z0;
-    }
-    if (g0 + 1 < G) {
-      mz[(((g0 + 1) * Hkv + kvh) * nphase + phase) * 2 + 0] = runmax1;
-      mz[(((g0 + 1) * Hkv + kvh) * nphase + phase) * 2 + 1] = z1;
-    }
+    if (g0 < G && runmax0 > -INFINITY) atomicMax(&sm.headmax[g0 * Hkv + kvh], float_ord(runmax0));
+    if (g0 + 1 < G && runmax1 > -INFINITY) atomicMax(&sm.headmax[(g0 + 1) * Hkv + kvh], float_ord(runmax1));
   }
 }
 
@@ -494,26 +476,6 @@ struct AttView {
   int cta0;        // fresh: first CTA of the sequence
 };
 
-__device__ __forceinline__ uint32_t att_token(const DecodeParams& p, const SeqDesc& sd, const AttView& v,
-                                              const int* prefix, int i) {
-  if (sd.att_list) return sd.att_list[i];
-  if (i < v.init_end) return static_cast<uint32_t>(i);
-  i -= v.init_end;
-  if (i < v.n1) {
-    if (!v.fresh) return __ldcg(sd.sel + v.lo1 + i);
-    // largest c with prefix[c] <= i
-    int lo = 0, hi = v.ncta - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (prefix[mid] <= i) lo = mid;
-      else hi = mid - 1;
-    }
-    return __ldcg(p.ws_sel_tok + static_cast<size_t>(v.cta0 + lo) * p.tpc + (i - prefix[lo]));
-  }
-  i -= v.n1;
-  return static_cast<uint32_t>(v.lb + i);
-}
-
 // Sum over the 32 lanes of P per-lane values v[0..P) (P a power of two <= 8)
 // by recursive halving: after it, lane L holds the total of value index
 // idx(L) = sum_s bit(L, 4 - s) * (P >> (s + 1)) -- log2(P) + 5 - log2(P)
@@ -544,6 +506,316 @@ __device__ __forceinline__ float transpose_reduce(float (&v)[8], int lane, int* 
   return v[0];
 }
 
+constexpr int kAttIdx = 1024;  // slab rows resolved per index window
+
+// Slab row of merged row i: the selection part comes with its slab rows
+// (published by the selecting CTAs, or cached with the SelectionResult),
+// only the windows go through the page table.
+__device__ __forceinline__ int32_t att_row(const DecodeParams& p, const SeqDesc& sd, const AttView& v,
+                                           const int* prefix, int i) {
+  if (sd.att_list) return static_cast<int32_t>(row_index(sd, sd.att_list[i], p.page_size));
+  if (i < v.init_end) return static_cast<int32_t>(row_index(sd, static_cast<uint32_t>(i), p.page_size));
+  i -= v.init_end;
+  if (i < v.n1) {
+    if (!v.fresh) {
+      if (sd.sel_rows) return __ldcg(sd.sel_rows + v.lo1 + i);
+      return static_cast<int32_t>(row_index(sd, __ldcg(sd.sel + v.lo1 + i), p.page_size));
+    }
+    int lo = 0, hi = v.ncta - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (prefix[mid] <= i) lo = mid;
+      else hi = mid - 1;
+    }
+    return __ldcg(p.ws_sel_row + static_cast<size_t>(v.cta0 + lo) * p.tpc + (i - prefix[lo]));
+  }
+  i -= v.n1;
+  return static_cast<int32_t>(row_index(sd, static_cast<uint32_t>(v.lb + i), p.page_size));
+}
+
+// Tensor-core split-K flash-decoding partial (D = 64 / 128, G <= 8) of the
+// query heads {g + m*H_kv} sharing KV head g over merged rows [r0, r1), plus
+// the current token (fp32 k_t / v_t, CUDA cores) when `with_cur`.
+//   * q staging and the slab-row pass issue their loads together, then the
+//     K/V slices (d wide, this KV head only) are gathered with 16-byte
+//     cp.async into padded rows (ldmatrix conflict-free), double-buffered;
+//   * scores: S[16 rows x 8 heads] per m16n8k16 tile, K rows as A (ldmatrix),
+//     q split exactly into three bf16 parts as B (bf16 x bf16 products are
+//     exact in fp32) -- one warp per 16-row tile;
+//   * P.V: O^T[16 d x 8 heads] += V^T (ldmatrix.trans) x P^T (P split into
+//     three bf16 parts) -- warp = (d tile, row group);
+//   * online softmax per head between them, fp32 (attention.cpp:88-110).
+template <int D>
+__device__ void attend_group_mma(const DecodeParams& p, const SeqDesc& sd, const AttView& av, const Smem& sm,
+                                 int g, int r0, int r1, bool with_cur, float* part) {
+  constexpr int KC = D / 16;                 // k-chunks of the score MMA
+  constexpr int DT = D / 16;                 // d tiles of the P.V MMA
+  constexpr int RS = D + 8;                  // padded smem row stride (bf16 elements)
+  const int H_kv = p.H_kv, G = p.H / p.H_kv;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nwarps = blockDim.x >> 5;
+  const int RGP = max(1, (nwarps - (nwarps % DT)) / DT);  // row groups of the P.V warps
+  const int row_elems = H_kv * D;
+  // ---- carve the staging area
+  uint8_t* base = sm.ring;
+  float* qs = reinterpret_cast<float*>(base);                 // [8][D] (heads >= G zero)
+  size_t o = static_cast<size_t>(8) * D * 4;
+  float* ck = reinterpret_cast<float*>(base + o);             // [D] current K (fp32)
+  float* cv = ck + D;                                         // [D] current V
+  o += static_cast<size_t>(2) * D * 4;
+  float* red = reinterpret_cast<float*>(base + o);            // [RGP][8][D]
+  o += align_up(static_cast<size_t>(RGP) * 8 * D * 4, 128);
+  float* stat = reinterpret_cast<float*>(base + o);           // [8][4] m_run, l_run, corr
+  o += 128;
+  int32_t* ridx = reinterpret_cast<int32_t*>(base + o);       // [kAttIdx] slab rows
+  o += static_cast<size_t>(kAttIdx) * 4;
+  uint2* qf = reinterpret_cast<uint2*>(base + o);             // [KC][3][32] B fragments of q (hi/mid/lo)
+  o += static_cast<size_t>(KC) * 3 * 32 * 8;
+  const size_t rest = static_cast<size_t>(p.att_bytes) > o ? static_cast<size_t>(p.att_bytes) - o : 0;
+  // per row: 2 buffers x (K + V) padded slices + 8 probs + P fragments
+  int cap = static_cast<int>(rest / (4 * RS * 2 + 32 + 32 + 48)) & ~15;
+  cap = max(16, min(cap, kAttMaxRows));
+  float* probs = reinterpret_cast<float*>(base + o);          // [cap + 16][8]
+  o += align_up(static_cast<size_t>(cap + 16) * 32, 128);
+  uint2* pf = reinterpret_cast<uint2*>(base + o);             // [cap / 16][3][32] B fragments of P^T
+  o += align_up(static_cast<size_t>(cap / 16) * 3 * 32 * 8, 128);
+  uint16_t* kb[2];
+  uint16_t* vb[2];
+  for (int b = 0; b < 2; ++b) {
+    kb[b] = reinterpret_cast<uint16_t*>(base + o);
+    o += static_cast<size_t>(cap) * RS * 2;
+    vb[b] = reinterpret_cast<uint16_t*>(base + o);
+    o += static_cast<size_t>(cap) * RS * 2;
+  }
+  const int nrows = max(0, r1 - r0);
+  // ---- q (one element per thread, loads issued with the first slab-row pass)
+  float qv = 0.f;
+  {
+    const int m = tid / D, t = tid - (tid / D) * D;
+    if (tid < 8 * D) qv = m < G ? __ldg(sd.q + static_cast<size_t>(g + m * H_kv) * D + t) : 0.f;
+    for (int i = tid + blockDim.x; i < 8 * D; i += blockDim.x) {
+      const int m2 = i / D, t2 = i - (i / D) * D;
+      qs[i] = m2 < G ? __ldg(sd.q + static_cast<size_t>(g + m2 * H_kv) * D + t2) : 0.f;
+    }
+  }
+  if (with_cur)
+    for (int t = tid; t < D; t += blockDim.x) {
+      ck[t] = __ldg(sd.k_new + static_cast<size_t>(g) * D + t);
+      cv[t] = __ldg(sd.v_new + static_cast<size_t>(g) * D + t);
+    }
+  if (tid < 8) {
+    stat[tid * 4 + 0] = -INFINITY;
+    stat[tid * 4 + 1] = 0.f;
+    stat[tid * 4 + 2] = 1.f;
+  }
+  // P.V accumulators: warp (d tile dt, row group rgp)
+  const int dt = warp % DT, rgp = warp / DT;
+  const bool pv_warp = rgp < RGP;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  // gather the slices of index-window rows [c0, c0 + nr) into buffer b
+  constexpr int CPR = D * 2 / 16;  // 16-byte chunks per slice
+  auto issue = [&](int c0, int nr, int b) {
+    for (int idx = tid; idx < nr * CPR; idx += blockDim.x) {
+      const int r = idx / CPR, q = idx - (idx / CPR) * CPR;
+      const int64_t off = static_cast<int64_t>(ridx[c0 + r]) * row_elems + static_cast<int64_t>(g) * D + q * 8;
+      cp_async16(kb[b] + static_cast<size_t>(r) * RS + q * 8, p.k_slab + off);
+      cp_async16(vb[b] + static_cast<size_t>(r) * RS + q * 8, p.v_slab + off);
+    }
+    cp_async_commit();
+  };
+  int w0 = 0, sub = 0;
+  bool first = true;
+  for (;;) {
+    const int nw = min(kAttIdx, nrows - w0);
+    for (int r = tid; r < nw; r += blockDim.x) ridx[r] = att_row(p, sd, av, sm.prefix, r0 + w0 + r);
+    const bool build_qf = first;
+    if (first && tid < 8 * D) qs[tid] = qv;
+    first = false;
+    __syncthreads();
+    trace_pt(p, 20);
+    if (build_qf && tid < KC * 32) {
+      // q^T as the score MMA's B operand, split exactly into three bf16 parts:
+      // lane l holds q[head l/4][kc*16 + 2(l%4) + {0,1,8,9}]
+      const int kc = tid >> 5, l = tid & 31;
+      const int n = l >> 2, dd = kc * 16 + (l & 3) * 2;
+      float h[4], m[4], lo[4];
+      split3(qs[n * D + dd], h[0], m[0], lo[0]);
+      split3(qs[n * D + dd + 1], h[1], m[1], lo[1]);
+      split3(qs[n * D + dd + 8], h[2], m[2], lo[2]);
+      split3(qs[n * D + dd + 9], h[3], m[3], lo[3]);
+      qf[(kc * 3 + 0) * 32 + l] = make_uint2(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]));
+      qf[(kc * 3 + 1) * 32 + l] = make_uint2(pack_bf16x2(m[0], m[1]), pack_bf16x2(m[2], m[3]));
+      qf[(kc * 3 + 2) * 32 + l] = make_uint2(pack_bf16x2(lo[0], lo[1]), pack_bf16x2(lo[2], lo[3]));
+    }
+    const bool last_w = w0 + nw >= nrows;
+    const int nsub = max(1, (nw + cap - 1) / cap);
+    issue(0, min(cap, nw), sub & 1);
+    for (int c = 0; c < nsub; ++c, ++sub) {
+      const int c0 = c * cap;
+      const int nr = max(0, min(cap, nw - c0));
+      const int nr16 = (nr + 15) & ~15;
+      const bool last = last_w && c == nsub - 1;
+      const bool cur_here = last && with_cur;
+      if (c + 1 < nsub) {
+        issue(c0 + cap, min(cap, nw - c0 - cap), (sub + 1) & 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      if (sub == 0) trace_pt(p, 21);
+      const uint16_t* K = kb[sub & 1];
+      uint16_t* V = vb[sub & 1];
+      // zero the padding rows of V (P is zero there; keep 0 * garbage finite)
+      for (int i = tid; i < (nr16 - nr) * (D / 8); i += blockDim.x) {
+        const int r = nr + i / (D / 8), q = i - (i / (D / 8)) * (D / 8);
+        *reinterpret_cast<uint4*>(V + static_cast<size_t>(r) * RS + q * 8) = make_uint4(0u, 0u, 0u, 0u);
+      }
+      // ---- scores: warp w -> rows [16w, 16w + 16)
+      for (int mt = warp; mt * 16 < nr; mt += nwarps) {
+        float ch[4] = {0.f, 0.f, 0.f, 0.f}, cm[4] = {0.f, 0.f, 0.f, 0.f}, cl[4] = {0.f, 0.f, 0.f, 0.f};
+        const uint32_t abase = smem_u32(K) +
+                               static_cast<uint32_t>(((mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * RS + (lane >> 4) * 8) * 2);
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) {
+          uint32_t a[4];
+          ldmatrix_x4(a, abase + kc * 32);
+          const uint2 bh = qf[(kc * 3 + 0) * 32 + lane], bm = qf[(kc * 3 + 1) * 32 + lane];
+          const uint2 bl = qf[(kc * 3 + 2) * 32 + lane];
+          mma_bf16_16816(ch, a, bh.x, bh.y);
+          mma_bf16_16816(cm, a, bm.x, bm.y);
+          mma_bf16_16816(cl, a, bl.x, bl.y);
+        }
+        float cacc[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cacc[e] = ch[e] + (cm[e] + cl[e]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int row = mt * 16 + (lane >> 2) + (e >> 1) * 8;
+          const int col = (lane & 3) * 2 + (e & 1);
+          if (row < nr) probs[row * 8 + col] = col < G ? cacc[e] * p.attn_scale : -INFINITY;
+        }
+      }
+      if (cur_here && warp == nwarps - 1) {
+        // current token row (fp32 K): one warp, G dot products
+        for (int m = 0; m < G; ++m) {
+          float a = 0.f;
+          for (int t = lane; t < D; t += 32) a = fmaf(qs[m * D + t], ck[t], a);
+          a = warp_sum(a);
+          if (lane == 0) probs[cap * 8 + m] = a * p.attn_scale;  // slot past the tiles
+        }
+      }
+      __syncthreads();
+      if (sub == 0) trace_pt(p, 22);
+      // ---- online softmax per head (warp m owns head m); rows >= nr get P = 0
+      for (int m = warp; m < 8; m += nwarps) {
+        if (m >= G) {
+          for (int r = lane; r < nr16; r += 32) probs[r * 8 + m] = 0.f;
+          continue;
+        }
+        float mx = -INFINITY;
+        for (int r = lane; r < nr; r += 32) mx = fmaxf(mx, probs[r * 8 + m]);
+        if (cur_here && lane == 0) mx = fmaxf(mx, probs[cap * 8 + m]);
+        mx = warp_max(mx);
+        const float m_old = stat[m * 4 + 0];
+        const float m_new = fmaxf(m_old, mx);
+        float l = 0.f;
+        for (int r = lane; r < nr16; r += 32) {
+          const float w = (r < nr && m_new > -INFINITY) ? expf(probs[r * 8 + m] - m_new) : 0.f;
+          probs[r * 8 + m] = w;
+          l += w;
+        }
+        if (cur_here && lane == 0) {
+          const float w = expf(probs[cap * 8 + m] - m_new);
+          probs[cap * 8 + m] = w;
+          l += w;
+        }
+        l = warp_sum(l);
+        if (lane == 0) {
+          const float corr = m_old == -INFINITY ? 0.f : expf(m_old - m_new);
+          stat[m * 4 + 0] = m_new;
+          stat[m * 4 + 1] = stat[m * 4 + 1] * corr + l;
+          stat[m * 4 + 2] = corr;
+        }
+      }
+      __syncthreads();
+      // P^T as the P.V MMA's B operand (three exact bf16 parts), built once
+      const int nk = nr16 / 16;
+      if (tid < nk * 32) {
+        const int ks = tid >> 5, l = tid & 31;
+        const int n = l >> 2, k0 = ks * 16 + (l & 3) * 2;
+        float h[4], m[4], lo[4];
+        split3(probs[k0 * 8 + n], h[0], m[0], lo[0]);
+        split3(probs[(k0 + 1) * 8 + n], h[1], m[1], lo[1]);
+        split3(probs[(k0 + 8) * 8 + n], h[2], m[2], lo[2]);
+        split3(probs[(k0 + 9) * 8 + n], h[3], m[3], lo[3]);
+        pf[(ks * 3 + 0) * 32 + l] = make_uint2(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]));
+        pf[(ks * 3 + 1) * 32 + l] = make_uint2(pack_bf16x2(m[0], m[1]), pack_bf16x2(m[2], m[3]));
+        pf[(ks * 3 + 2) * 32 + l] = make_uint2(pack_bf16x2(lo[0], lo[1]), pack_bf16x2(lo[2], lo[3]));
+      }
+      __syncthreads();
+      if (sub == 0) trace_pt(p, 23);
+      // ---- P.V on tensor cores
+      if (pv_warp) {
+        const int n0 = (lane & 3) * 2;
+        const float c0f = stat[n0 * 4 + 2], c1f = stat[(n0 + 1) * 4 + 2];
+        acc[0] *= c0f;
+        acc[1] *= c1f;
+        acc[2] *= c0f;
+        acc[3] *= c1f;
+        const int jm = lane >> 3, im = lane & 7;
+        const uint32_t vbase = smem_u32(V) +
+                               static_cast<uint32_t>((((jm >> 1) * 8 + im) * RS + dt * 16 + (jm & 1) * 8) * 2);
+        for (int ks = rgp; ks < nk; ks += RGP) {
+          uint32_t a[4];
+          ldmatrix_x4_trans(a, vbase + static_cast<uint32_t>(ks * 16 * RS * 2));
+          const uint2 bh = pf[(ks * 3 + 0) * 32 + lane], bm = pf[(ks * 3 + 1) * 32 + lane];
+          const uint2 bl = pf[(ks * 3 + 2) * 32 + lane];
+          mma_bf16_16816(acc, a, bh.x, bh.y);
+          mma_bf16_16816(acc, a, bm.x, bm.y);
+          mma_bf16_16816(acc, a, bl.x, bl.y);
+        }
+      }
+      if (cur_here) {
+        // the current token's P.V term, added once by row group 0
+        if (pv_warp && rgp == 0) {
+          const int n0 = (lane & 3) * 2, d0 = dt * 16 + (lane >> 2);
+          acc[0] = fmaf(probs[cap * 8 + n0], cv[d0], acc[0]);
+          acc[1] = fmaf(probs[cap * 8 + n0 + 1], cv[d0], acc[1]);
+          acc[2] = fmaf(probs[cap * 8 + n0], cv[d0 + 8], acc[2]);
+          acc[3] = fmaf(probs[cap * 8 + n0 + 1], cv[d0 + 8], acc[3]);
+        }
+      }
+      __syncthreads();  // buffer and probs free for the next sub-chunk
+      if (sub == 0) trace_pt(p, 24);
+    }
+    w0 += nw;
+    if (last_w) break;
+  }
+  trace_pt(p, 25);
+  // ---- reduce the row groups, write the partial record per head
+  if (pv_warp) {
+    const int n0 = (lane & 3) * 2, d0 = dt * 16 + (lane >> 2);
+    float* rr = red + static_cast<size_t>(rgp) * 8 * D;
+    rr[n0 * D + d0] = acc[0];
+    rr[(n0 + 1) * D + d0] = acc[1];
+    rr[n0 * D + d0 + 8] = acc[2];
+    rr[(n0 + 1) * D + d0 + 8] = acc[3];
+  }
+  __syncthreads();
+  const int stride = att_stride(D);
+  for (int i = tid; i < G * D; i += blockDim.x) {
+    const int m = i / D, t = i - (i / D) * D;
+    float sacc = 0.f;
+    for (int q = 0; q < RGP; ++q) sacc += red[(static_cast<size_t>(q) * 8 + m) * D + t];
+    part[static_cast<size_t>(m) * stride + t] = sacc;
+  }
+  if (tid < G) {
+    part[static_cast<size_t>(tid) * stride + D] = stat[tid * 4 + 0];
+    part[static_cast<size_t>(tid) * stride + D + 1] = stat[tid * 4 + 1];
+  }
+}
+
 // Split-K flash-decoding partial of the G query heads {g + m*H_kv} that share
 // KV head g (the reference's h mod H_kv map, attention.cpp:78) over rows
 // [r0, r1) of the merged list, plus the current token (fp32 k_t / v_t) when
@@ -554,7 +826,6 @@ __device__ __forceinline__ float transpose_reduce(float (&v)[8], int lane, int* 
 // registers, FFMA2 + transposed shuffle reduction. P.V: (row group, d pair)
 // threads with FFMA2. Writes (o[d], m, l) per head (attention.cpp:88-110
 // semantics, fp32). DT/GT = 0: runtime shapes (any d, G <= 8).
-constexpr int kAttIdx = 1024;
 
 template <int DT, int GT>
 __device__ void attend_group(const DecodeParams& p, const SeqDesc& sd, const AttView& av, const Smem& sm,
@@ -655,7 +926,7 @@ __device__ void attend_group(const DecodeParams& p, const SeqDesc& sd, const Att
   for (;;) {
     const int nw = min(kAttIdx, nrows - w0);
     for (int r = tid; r < nw; r += blockDim.x)
-      ridx[r] = static_cast<int32_t>(row_index(sd, att_token(p, sd, av, sm.prefix, r0 + w0 + r), p.page_size));
+      ridx[r] = att_row(p, sd, av, sm.prefix, r0 + w0 + r);
     __syncthreads();
     trace_pt(p, 20);
     const bool last_w = w0 + nw >= nrows;
@@ -811,46 +1082,26 @@ __device__ void attend_group(const DecodeParams& p, const SeqDesc& sd, const Att
 
 // Log-sum-exp merge of the row-chunk partials of KV head g (attention.cpp
 // :88-110 semantics): out[h] = sum_c e^(m_c - M) o_c / sum_c e^(m_c - M) l_c.
-// All (m, l) pairs are loaded in one parallel pass, the weights formed in
-// shared memory, then the o vectors are staged batch by batch with 16-byte
-// loads (every global load of a batch in flight at once).
+// Every partial record (o, m, l) is staged in shared memory in one parallel
+// pass (8 16-byte loads in flight per thread), then combined there.
 __device__ void merge_group(const DecodeParams& p, const SeqDesc& sd, const Smem& sm, int g, const float* parts,
                             int chunks) {
   const int d = p.d, G = p.H / p.H_kv, stride = att_stride(d);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
-  float* wts = reinterpret_cast<float*>(sm.ring);                  // [chunks][G] (m, then weight)
-  float* ls = wts + align_up(static_cast<size_t>(chunks) * G, 32);  // [chunks][G] l
-  float* linv = ls + align_up(static_cast<size_t>(chunks) * G, 32); // [G]
-  float* obuf = linv + 32;                                          // [batch][G][stride]
-  for (int i = tid; i < chunks * G; i += blockDim.x) {
-    wts[i] = __ldcg(parts + static_cast<size_t>(i) * stride + d);
-    ls[i] = __ldcg(parts + static_cast<size_t>(i) * stride + d + 1);
-  }
-  __syncthreads();
-  for (int m = warp; m < G; m += nwarps) {
-    float M = -INFINITY;
-    for (int c = lane; c < chunks; c += 32) M = fmaxf(M, wts[c * G + m]);
-    M = warp_max(M);
-    float L = 0.f;
-    for (int c = lane; c < chunks; c += 32) {
-      const float mc = wts[c * G + m];
-      const float w = mc == -INFINITY ? 0.f : expf(mc - M);
-      wts[c * G + m] = w;
-      L = fmaf(w, ls[c * G + m], L);
-    }
-    L = warp_sum(L);
-    if (lane == 0) linv[m] = 1.f / L;
-  }
   const size_t rec = static_cast<size_t>(G) * stride;  // floats per chunk
+  float* wts = reinterpret_cast<float*>(sm.ring);      // [chunks][G] weights
+  float* linv = wts + align_up(static_cast<size_t>(chunks) * G, 32);  // [G]
+  float* obuf = linv + 32;                             // [chunks][G][stride]
   const size_t room = static_cast<size_t>(p.att_bytes) / 4 - (obuf - wts);
   const bool staged = static_cast<size_t>(chunks) * rec <= room;
-  if (staged) {  // every o vector in one parallel pass (the usual case)
+  const float* ob = parts;
+  if (staged) {
     const int n4 = static_cast<int>(chunks * rec / 4);
     const float4* src = reinterpret_cast<const float4*>(parts);
     float4* dst = reinterpret_cast<float4*>(obuf);
     const int bd = blockDim.x;
 #pragma unroll 1
-    for (int i0 = tid; i0 < n4; i0 += 8 * bd) {  // 8 loads in flight per thread
+    for (int i0 = tid; i0 < n4; i0 += 8 * bd) {
       float4 v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) v[u] = i0 + u * bd < n4 ? __ldcg(src + i0 + u * bd) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -858,16 +1109,36 @@ __device__ void merge_group(const DecodeParams& p, const SeqDesc& sd, const Smem
       for (int u = 0; u < 8; ++u)
         if (i0 + u * bd < n4) dst[i0 + u * bd] = v[u];
     }
+    ob = obuf;
+    __syncthreads();
+  }
+  for (int m = warp; m < G; m += nwarps) {
+    float M = -INFINITY;
+    for (int c = lane; c < chunks; c += 32) M = fmaxf(M, staged ? ob[c * rec + m * stride + d] : __ldcg(ob + c * rec + m * stride + d));
+    M = warp_max(M);
+    float L = 0.f;
+    for (int c = lane; c < chunks; c += 32) {
+      const float mc = staged ? ob[c * rec + m * stride + d] : __ldcg(ob + c * rec + m * stride + d);
+      const float lc = staged ? ob[c * rec + m * stride + d + 1] : __ldcg(ob + c * rec + m * stride + d + 1);
+      const float w = mc == -INFINITY ? 0.f : expf(mc - M);
+      wts[c * G + m] = w;
+      L = fmaf(w, lc, L);
+    }
+    L = warp_sum(L);
+    if (lane == 0) linv[m] = 1.f / L;
   }
   __syncthreads();
-  const float* ob = staged ? obuf : parts;
 #pragma unroll 1
   for (int i = tid; i < G * d; i += blockDim.x) {
     const int m = i / d, t = i - (i / d) * d;
-    float a = 0.f;
-#pragma unroll 1
-    for (int c = 0; c < chunks; ++c) a = fmaf(wts[c * G + m], ob[c * rec + m * stride + t], a);
-    sd.out[static_cast<size_t>(g + m * p.H_kv) * d + t] = a * linv[m];
+    float a0 = 0.f, a1 = 0.f;
+    int c = 0;
+    for (; c + 1 < chunks; c += 2) {
+      a0 = fmaf(wts[c * G + m], staged ? ob[c * rec + m * stride + t] : __ldcg(ob + c * rec + m * stride + t), a0);
+      a1 = fmaf(wts[(c + 1) * G + m], staged ? ob[(c + 1) * rec + m * stride + t] : __ldcg(ob + (c + 1) * rec + m * stride + t), a1);
+    }
+    if (c < chunks) a0 = fmaf(wts[c * G + m], staged ? ob[c * rec + m * stride + t] : __ldcg(ob + c * rec + m * stride + t), a0);
+    sd.out[static_cast<size_t>(g + m * p.H_kv) * d + t] = (a0 + a1) * linv[m];
   }
 }
 
@@ -1023,39 +1294,33 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   trace_pt(p, 2);
   if (p.debug_flags & 2) return;  // dev timing: stop after the scan
 
-  // ---- phase 2: per-CTA softmax partials (m, z) per head (softmax_rows, tensor.cpp:31-52)
+  // ---- phase 2: per-CTA softmax partials m = max_j S, z = sum_j e^(S - m) per
+  // head (softmax_rows, tensor.cpp:31-52): warp per head, float4 rows, four
+  // independent SFU chains per lane
   if (do_select && own == 1 && p.method == 2) {
-    const size_t so = static_cast<size_t>(seq_id) * H * stats_stride(p.ctas_per_seq) + cs;
     const size_t sh = stats_stride(p.ctas_per_seq);
-    if (FAST && !(p.mode & kModeSIn)) {
-      // the scan's per-warp online partials (scan_fast epilogue)
-      const float* mz = reinterpret_cast<const float*>(sm.scratch);
-      const int nphase = kDecodeConsumers / p.H_kv;
-      for (int h = tid; h < H; h += blockDim.x) {
-        float m = -INFINITY;
-        for (int ph = 0; ph < nphase; ++ph) m = fmaxf(m, mz[(h * nphase + ph) * 2]);
-        float z = 0.f;
-        if (m > -INFINITY)
-          for (int ph = 0; ph < nphase; ++ph) {
-            const float mp = mz[(h * nphase + ph) * 2];
-            if (mp > -INFINITY) z += mz[(h * nphase + ph) * 2 + 1] * fast_exp(mp - m);
-          }
+    const size_t so = static_cast<size_t>(seq_id) * H * sh + cs;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int n4 = (nloc + 3) >> 2;
+    for (int h = warp; h < H; h += kDecodeWarps) {
+      const float m = ord_float(sm.headmax[h]);
+      const float ml = m * 1.4426950408889634f;
+      const float4* sr = reinterpret_cast<const float4*>(Sbuf + static_cast<size_t>(h) * sstride);
+      float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+      if (m > -INFINITY) {
+        for (int q = lane; q < n4; q += 32) {
+          const float4 v = sr[q];
+          const int j = 4 * q;
+          z0 += j + 0 < nloc ? ex2_approx(fmaf(v.x, 1.4426950408889634f, -ml)) : 0.f;
+          z1 += j + 1 < nloc ? ex2_approx(fmaf(v.y, 1.4426950408889634f, -ml)) : 0.f;
+          z2 += j + 2 < nloc ? ex2_approx(fmaf(v.z, 1.4426950408889634f, -ml)) : 0.f;
+          z3 += j + 3 < nloc ? ex2_approx(fmaf(v.w, 1.4426950408889634f, -ml)) : 0.f;
+        }
+      }
+      const float z = warp_sum((z0 + z1) + (z2 + z3));
+      if (lane == 0) {
         p.ws_m[so + h * sh] = m;
         p.ws_z[so + h * sh] = z;
-      }
-    } else {
-      const int warp = tid >> 5, lane = tid & 31;
-      for (int h = warp; h < H; h += kDecodeWarps) {
-        const float m = ord_float(sm.headmax[h]);
-        float z = 0.f;
-        const float* sr = Sbuf + static_cast<size_t>(h) * sstride;
-        if (m > -INFINITY)
-          for (int jl = lane; jl < nloc; jl += 32) z += fast_exp(sr[jl] - m);
-        z = warp_sum(z);
-        if (lane == 0) {
-          p.ws_m[so + h * sh] = m;
-          p.ws_z[so + h * sh] = z;
-        }
       }
     }
   }
@@ -1241,6 +1506,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     uint32_t out_n = 0, eq_seen = 0;
     uint32_t* lt = p.ws_sel_tok + static_cast<size_t>(cta) * p.tpc;
     float* lc = p.ws_sel_crit + static_cast<size_t>(cta) * p.tpc;
+    int32_t* lr = p.ws_sel_row + static_cast<size_t>(cta) * p.tpc;
     for (int base = 0; base < nloc; base += blockDim.x) {
       const int jl = base + tid;
       const uint32_t key = jl < nloc ? keys[jl] : 0u;
@@ -1261,6 +1527,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       if (take) {
         lt[pos] = cand_at(sd, j0 + jl);
         lc[pos] = key_float(key);
+        lr[pos] = may_scan ? sm.frames[jl] : -1;
       }
       out_n += tot;
     }
@@ -1281,9 +1548,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     const int my0 = sm.prefix[cs], myn = sm.prefix[cs + 1] - my0;
     const uint32_t* lt = p.ws_sel_tok + static_cast<size_t>(cta) * p.tpc;
     const float* lc = p.ws_sel_crit + static_cast<size_t>(cta) * p.tpc;
+    const int32_t* lr = p.ws_sel_row + static_cast<size_t>(cta) * p.tpc;
     for (int i = tid; i < myn; i += blockDim.x) {
       sd.sel[my0 + i] = __ldcg(lt + i);
       sd.sel_crit[my0 + i] = __ldcg(lc + i);
+      if (sd.sel_rows) sd.sel_rows[my0 + i] = __ldcg(lr + i);
     }
     if (cs == 0 && tid == 0) sd.cache->n_sel = static_cast<int>(tot);
   }
@@ -1323,8 +1592,12 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     const int stride = att_stride(p.d);
     for (int g = gi; g < p.H_kv; g += split.groups) {
       float* parts = p.ws_att + (static_cast<size_t>(seq_id) * p.H_kv + g) * split.chunks * Gq * stride;
-      attend_group<(FAST ? D : 0), (FAST ? G : 0)>(p, sd, av, sm, g, r0, min(r1, av.n_rows), with_cur,
-                                                   parts + static_cast<size_t>(ci) * Gq * stride);
+      if constexpr (FAST)
+        attend_group_mma<D>(p, sd, av, sm, g, r0, min(r1, av.n_rows), with_cur,
+                            parts + static_cast<size_t>(ci) * Gq * stride);
+      else
+        attend_group<0, 0>(p, sd, av, sm, g, r0, min(r1, av.n_rows), with_cur,
+                           parts + static_cast<size_t>(ci) * Gq * stride);
       trace_pt(p, 11);
       // the last chunk to finish merges (no grid barrier)
       __syncthreads();

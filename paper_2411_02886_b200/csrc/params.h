@@ -52,6 +52,7 @@ struct SeqDesc {
   float* cached_q;             // [H * d]
   uint32_t* sel;               // [k] selected logical indices (the cached SelectionResult)
   float* sel_crit;             // [k] their criticality
+  int32_t* sel_rows;           // [k] their slab rows (nullptr: resolve through the page table)
   // optional I/O for the standalone APIs
   float* s_out;                // [H x n_cand] scores out (kModeSOut)
   const float* s_in;           // [H x n_cand] scores in (kModeSIn)
@@ -83,6 +84,7 @@ struct DecodeParams {
   uint32_t* ws_nsel;           // [n_ctas] per-CTA count of selected candidates
   uint32_t* ws_sel_tok;        // [n_ctas][tpc] per-CTA selected token indices (ascending)
   float* ws_sel_crit;          // [n_ctas][tpc] their criticality
+  int32_t* ws_sel_row;         // [n_ctas][tpc] their slab rows
   float* ws_att;               // [n_seq][H_kv][chunks][G][att_stride(d)] attention partials (o, m, l)
   unsigned int* ws_acnt;       // [n_seq][H_kv] arrival counters of the attention merge (self-resetting)
   unsigned int* bar;           // grid barrier counters: bar[0] / bar[32] alternate per launch
