@@ -197,9 +197,11 @@ struct GridSync {
   }
 };
 
+// 2^x on the SFU, subnormal results flushed to zero (probabilities below
+// 2^-126 carry no ranking information: SURVEY.md §8(c) tie floor 1e-30)
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
-  asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
@@ -207,7 +209,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // well inside the 1e-4 criticality tolerance.
 __device__ __forceinline__ float fast_exp(float x) {
   float y;
-  asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(x * 1.4426950408889634f));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x * 1.4426950408889634f));
   return y;
 }
 

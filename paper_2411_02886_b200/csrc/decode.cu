@@ -274,7 +274,7 @@ __device__ __forceinline__ void split3(float x, float& hi, float& mid, float& lo
 
 template <int D, int G>
 __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& sm, int j0,
-                          int nloc, float* Sbuf, int sstride, float* s_out_row0) {
+                          int nloc, float* Sbuf, int sstride, float* s_out_row0, int pre) {
   constexpr int KC = D / 16;  // k-chunks of 16 along d
   const int Hkv = p.H_kv;
   const int row_bytes = Hkv * D * 2;
@@ -291,7 +291,7 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
     // issuing a stage is latency-free; rows land at a padded stride.
     const uint64_t pol = policy_evict_first();
     const char* kbase = reinterpret_cast<const char*>(p.k_slab);
-    for (int it = 0; it < nit; ++it) {
+    for (int it = pre; it < nit; ++it) {  // stages [0, pre) were issued in phase 0
       const int s = it % kStages;
       const int rbase = it * R;
       const int nrows = min(R, nloc - rbase);
@@ -1211,11 +1211,43 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       selv[u] = i < p.k ? __ldcg(sd.sel + i) : 0xffffffffu;
     }
   }
+  // Speculative scan start: the TMA producer issues the first ring stages of
+  // the K scan before the Selection Cache decision is known. On a miss the
+  // scan starts a decision-time earlier; on a hit the (few) stages are
+  // drained unused before the ring is reused.
+  int pre = 0;
+  if constexpr (FAST) {
+    const ScanGeom geom = scan_geom(p.H, p.H_kv, D, p.ring_bytes);
+    if ((p.debug_flags & 64) && may_scan && (p.mode & kModeCache))  // experimental (measured: no gain)
+      pre = min(min((nloc + geom.rows - 1) / geom.rows, geom.stages), 4);
+    if (pre > 0 && tid < 32) {
+      const int row_bytes = p.H_kv * D * 2, rstride = row_bytes + 16;
+      const uint64_t pol = policy_evict_first();
+      const char* kbase = reinterpret_cast<const char*>(p.k_slab);
+      int32_t fr[4];
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {  // all page-table loads in flight together
+        const int jl = it * geom.rows + tid;
+        fr[it] = (it < pre && tid < geom.rows && jl < nloc)
+                     ? static_cast<int32_t>(row_index(sd, cand_at(sd, j0 + jl), p.page_size)) : 0;
+      }
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        if (it >= pre) break;
+        const int nrows = min(geom.rows, nloc - it * geom.rows);
+        if (tid == 0) mbar_arrive_expect_tx(&sm.full[it], static_cast<uint32_t>(nrows * row_bytes));
+        __syncwarp();
+        if (tid < nrows)
+          bulk_g2s(sm.ring + static_cast<size_t>(it * geom.rows + tid) * rstride,
+                   kbase + static_cast<size_t>(fr[it]) * row_bytes, row_bytes, &sm.full[it], pol);
+      }
+    }
+  }
   // Selection Cache decisions. A single sequence: every CTA evaluates it
   // (bit-identical) so the grid agrees on whether selection (and its
   // barriers) runs. Several sequences: each CTA evaluates its own and the
   // barriers run unconditionally.
-  double* scratch_d = reinterpret_cast<double*>(sm.hist);  // hist is free until the radix passes
+  double* scratch_d = reinterpret_cast<double*>(sm.scratch);  // the ring may be filling (speculative scan)
   int own = 0;  // 0 no selection, 1 miss (select), 2 hit, 3 zero query
   double own_cos = NAN;
   if (sd.select) {
@@ -1268,6 +1300,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     for (int i = cs * blockDim.x + tid; i < 2 * kRadixBins; i += p.ctas_per_seq * blockDim.x) gh[i] = 0u;
   }
   if (cs == 0 && tid == 0 && own == 3) sd.cache->error = 1;
+  if (pre > 0 && own != 1)
+    for (int it = 0; it < pre; ++it) mbar_wait(&sm.full[it], 0);  // speculative stages landed
   __syncthreads();
 
   trace_pt(p, 1);
@@ -1286,10 +1320,17 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       }
     } else {
       float* so = (p.mode & kModeSOut) ? sd.s_out + j0 : nullptr;
-      if constexpr (FAST) scan_fast<D, G>(p, sd, sm, j0, nloc, Sbuf, sstride, so);
+      if constexpr (FAST) scan_fast<D, G>(p, sd, sm, j0, nloc, Sbuf, sstride, so, pre);
       else scan_generic(p, sd, sm, j0, nloc, Sbuf, sstride, so);
     }
   }
+  // S rows are read four candidates at a time: pad each row to a multiple
+  // of 4 with -inf (exp -> 0, never selected)
+  if (scanning && (nloc & 3))
+    for (int i = tid; i < H * 4; i += blockDim.x) {
+      const int h = i >> 2, jl = nloc + (i & 3);
+      if (jl < ((nloc + 3) & ~3)) Sbuf[static_cast<size_t>(h) * sstride + jl] = -INFINITY;
+    }
   __syncthreads();
   trace_pt(p, 2);
   if (p.debug_flags & 2) return;  // dev timing: stop after the scan
@@ -1305,16 +1346,21 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     for (int h = warp; h < H; h += kDecodeWarps) {
       const float m = ord_float(sm.headmax[h]);
       const float ml = m * 1.4426950408889634f;
-      const float4* sr = reinterpret_cast<const float4*>(Sbuf + static_cast<size_t>(h) * sstride);
+      float4* sr = reinterpret_cast<float4*>(Sbuf + static_cast<size_t>(h) * sstride);
       float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
       if (m > -INFINITY) {
+        // S <- e^(S - m) in place (the soft vote then needs FMAs only)
         for (int q = lane; q < n4; q += 32) {
-          const float4 v = sr[q];
-          const int j = 4 * q;
-          z0 += j + 0 < nloc ? ex2_approx(fmaf(v.x, 1.4426950408889634f, -ml)) : 0.f;
-          z1 += j + 1 < nloc ? ex2_approx(fmaf(v.y, 1.4426950408889634f, -ml)) : 0.f;
-          z2 += j + 2 < nloc ? ex2_approx(fmaf(v.z, 1.4426950408889634f, -ml)) : 0.f;
-          z3 += j + 3 < nloc ? ex2_approx(fmaf(v.w, 1.4426950408889634f, -ml)) : 0.f;
+          float4 v = sr[q];
+          v.x = ex2_approx(fmaf(v.x, 1.4426950408889634f, -ml));
+          v.y = ex2_approx(fmaf(v.y, 1.4426950408889634f, -ml));
+          v.z = ex2_approx(fmaf(v.z, 1.4426950408889634f, -ml));
+          v.w = ex2_approx(fmaf(v.w, 1.4426950408889634f, -ml));
+          sr[q] = v;
+          z0 += v.x;
+          z1 += v.y;
+          z2 += v.z;
+          z3 += v.w;
         }
       }
       const float z = warp_sum((z0 + z1) + (z2 + z3));
@@ -1344,8 +1390,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   }
   const bool radix_own = do_select && own == 1 && T > p.k;
   if (do_select && own == 1) {
-    float* ml = sm.f;                                   // [H] M_h * log2(e)
-    float* iz = reinterpret_cast<float*>(sm.headmax);  // [H] 1 / Z_h (headmax is dead)
+    float* ml = sm.f;                                   // [H] f_h = e^(m_c - M_h) / Z_h
     if (p.method == 2) {
       float* pm = reinterpret_cast<float*>(sm.ring);
       const int nc = p.ctas_per_seq;
@@ -1379,8 +1424,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);
         if (hv && sub == 0) {
-          ml[h] = M * 1.4426950408889634f;
-          iz[h] = 1.f / Z;
+          const float mc = ord_float(sm.headmax[h]);
+          ml[h] = mc > -INFINITY ? fast_exp(mc - M) / Z : 0.f;  // f_h: local e^(S - m_c) -> softmax
         }
       }
       __syncthreads();
@@ -1391,42 +1436,38 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       __syncthreads();
     }
     // crit[j] = sum_h softmax_h(S)[j] (select_head_soft_vote, selector.cpp:113-126)
-    // or the raw logit sum (select_topk, selector.cpp:89-99); four
-    // candidates per thread, keys straight into the pass-1 histogram
-    const int n4 = (nloc + 3) >> 2;
-    for (int base = 0; base < n4; base += blockDim.x) {
+    // = sum_h e^(S - m_c) f_h, or the raw logit sum (select_topk,
+    // selector.cpp:89-99); two candidates per thread, keys straight into the
+    // pass-1 histogram
+    const int n2 = (nloc + 1) >> 1;
+    const bool soft = p.method == 2;
+    for (int base = 0; base < n2; base += blockDim.x) {
       const int q = base + tid;
-      float c[4] = {0.f, 0.f, 0.f, 0.f};
-      if (q < n4) {
-        const float* s4 = Sbuf + 4 * q;
-        if (p.method == 2) {
-#pragma unroll 2
-          for (int h = 0; h < H; ++h) {
-            const float4 sv = *reinterpret_cast<const float4*>(s4 + static_cast<size_t>(h) * sstride);
-            const float mh = ml[h], ih = iz[h];
-            c[0] = fmaf(ex2_approx(fmaf(sv.x, 1.4426950408889634f, -mh)), ih, c[0]);
-            c[1] = fmaf(ex2_approx(fmaf(sv.y, 1.4426950408889634f, -mh)), ih, c[1]);
-            c[2] = fmaf(ex2_approx(fmaf(sv.z, 1.4426950408889634f, -mh)), ih, c[2]);
-            c[3] = fmaf(ex2_approx(fmaf(sv.w, 1.4426950408889634f, -mh)), ih, c[3]);
-          }
-        } else {
-#pragma unroll 2
-          for (int h = 0; h < H; ++h) {
-            const float4 sv = *reinterpret_cast<const float4*>(s4 + static_cast<size_t>(h) * sstride);
-            c[0] += sv.x;
-            c[1] += sv.y;
-            c[2] += sv.z;
-            c[3] += sv.w;
-          }
+      float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+      if (q < n2) {
+        const float* s2 = Sbuf + 2 * q;
+        int h = 0;
+        for (; h + 1 < H; h += 2) {
+          const float2 a = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h) * sstride);
+          const float2 b = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h + 1) * sstride);
+          const float fa = soft ? ml[h] : 1.f, fb = soft ? ml[h + 1] : 1.f;
+          c0 = fmaf(a.x, fa, c0);
+          c1 = fmaf(a.y, fa, c1);
+          c2 = fmaf(b.x, fb, c2);
+          c3 = fmaf(b.y, fb, c3);
+        }
+        if (h < H) {
+          const float2 a = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h) * sstride);
+          const float fa = soft ? ml[h] : 1.f;
+          c0 = fmaf(a.x, fa, c0);
+          c1 = fmaf(a.y, fa, c1);
         }
       }
-      uint32_t kq[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) kq[e] = float_key(c[e]);
-      if (q < n4) *reinterpret_cast<uint4*>(keys + 4 * q) = make_uint4(kq[0], kq[1], kq[2], kq[3]);
+      const uint32_t k0 = float_key(c0 + c2), k1 = float_key(c1 + c3);
+      if (q < n2) *reinterpret_cast<uint2*>(keys + 2 * q) = make_uint2(k0, k1);
       if (radix_own) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) hist_add(sm.hist, kq[e], q < n4 && 4 * q + e < nloc, 20);
+        hist_add(sm.hist, k0, q < n2 && 2 * q < nloc, 20);
+        hist_add(sm.hist, k1, q < n2 && 2 * q + 1 < nloc, 20);
       }
     }
     __syncthreads();
