@@ -339,7 +339,10 @@ def main():
         "hit_step_us": round(r["hit_us"], 2) if r["hit_us"] else None,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
-                     "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                     "traffic": (int((r["lookups"] - r["hits"]) / max(r["lookups"], 1) * traffic["miss_bytes_per_launch"]
+                                     + r["hits"] / max(r["lookups"], 1) * traffic["hit_bytes_per_launch"])
+                                 if traffic else None),
+                     "traffic_source": traffic.get("source") if traffic else None,
                      "algorithmic_bytes_per_launch": int(r["alg_bytes"]),
                      "miss_step": {"achieved": round(miss_ach, 1) if miss_ach else None,
                                    "frac": round(miss_ach / peak, 4) if miss_ach else None,
