@@ -191,6 +191,33 @@ ts_status ts_engine_cached_selection(const ts_engine* eng, size_t seq, uint32_t*
 ts_status ts_engine_sync(ts_engine* eng);
 ts_pool* ts_engine_pool(ts_engine* eng);
 uint32_t ts_engine_sequence(const ts_engine* eng, size_t seq);
+/* ------------------------------------------------------------------------
+ * KV-sequence-sharded decode (BASELINE config 4). Each
+ * shard (rank) owns a contiguous range [base, base + len) of one sequence in
+ * its own engine: rank 0 holds the init window, the last rank the local
+ * window, the current token and every append. A decode step is four calls
+ * on every rank with three all-gathers in between (NCCL over NVLink, or any
+ * transport), all on device buffers and the engine's stream:
+ *   ts_shard_stats      -> stats  [H][2]        all-gather -> [world][H][2]
+ *   ts_shard_select     -> cands  [2k + 1] u32  all-gather -> [world][2k + 1]
+ *   ts_shard_attend     -> out    [H*d], ml [H][2]  all-gather both
+ *   ts_shard_combine    -> the step's output [H*d] (identical on every rank)
+ * The Selection Cache decision needs no exchange (q is replicated). Global
+ * softmax statistics are combined in rank order, the global top-k is exact
+ * (it is a subset of the union of the shards' local top-k), and outputs
+ * merge by log-sum-exp: the result equals the unsharded decode_step
+ * (attention.cpp:172-200) up to fp32 summation order.
+ * ---------------------------------------------------------------------- */
+ts_status ts_shard_engine_create(const ts_engine_config* cfg, size_t capacity_tokens, int rank, int world,
+                                 ts_engine** out);
+/* q, k, v: device [H*d], [H_kv*d]; n_global: the sequence length before the step. */
+ts_status ts_shard_stats(ts_engine* eng, const float* q, const float* k, const float* v, size_t base,
+                         size_t n_global, float* stats_out);
+ts_status ts_shard_select(ts_engine* eng, const float* all_stats, uint32_t* cands_out);
+ts_status ts_shard_attend(ts_engine* eng, const uint32_t* all_cands, float* out_partial, float* ml_out);
+ts_status ts_shard_combine(const float* o_all, const float* ml_all, int world, size_t num_heads,
+                           size_t head_dim, float* out, void* stream);
+
 /* Kernel launches issued by this library since process start (evidence
  * counter for the benchmark's gpu_launches field). */
 uint64_t ts_launch_count(void);

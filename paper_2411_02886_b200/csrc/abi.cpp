@@ -187,7 +187,8 @@ struct Plan {
   const void* fn;
 };
 
-Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows, bool attend = true) {
+Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows, bool attend = true,
+               bool force_spill = false) {
   const DeviceInfo& di = device_info();
   Plan pl{};
   const tsb::ScanGeom g = tsb::scan_geom(H, H_kv, d);
@@ -201,7 +202,7 @@ Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows, bool 
   const int row_bytes = H_kv * d * 2;
   const size_t optin = static_cast<size_t>(di.smem_optin);
   tsb::SmemLayout L = tsb::smem_layout(H, row_bytes, pl.tpc, 1);
-  if (L.total <= optin && !g_force_global_s) {
+  if (L.total <= optin && !g_force_global_s && !force_spill) {
     pl.s_in_smem = 1;
   } else {
     pl.s_in_smem = 0;
@@ -368,8 +369,19 @@ struct ts_pool {
 };
 
 // ================================================================= engine
+// One step of a KV-sequence-sharded decode (config 4), kept between the
+// per-exchange launches of this shard.
+struct ShardStep {
+  const float *q = nullptr, *k = nullptr, *v = nullptr;
+  size_t base = 0, n_global = 0, n_local_len = 0;
+  int32_t cand_first = 0, T = 0, sel_on = 0;
+};
+
 struct ts_engine {
   ts_engine_config cfg{};
+  int rank = 0, world = 1;  // sharded decode: this shard's rank among `world`
+  ShardStep shard;
+  DevBuf s_att, s_natt;     // sharded attend: attended local rows + count
   std::unique_ptr<ts_pool> pool;
   std::vector<uint32_t> seq_ids;
   size_t B = 1;
@@ -1252,6 +1264,174 @@ ts_status ts_engine_prefill(ts_engine* e, size_t seq, const float* q, const floa
       pool.append(sid, kc, vc, len, false, nullptr, nullptr, st);
     }
     ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+
+// ------------------------------------------------------------ sharded decode
+ts_status ts_shard_engine_create(const ts_engine_config* cfg, size_t capacity_tokens, int rank, int world,
+                                 ts_engine** out) {
+  return guarded([&] {
+    if (world < 1 || world > 64 || rank < 0 || rank >= world)
+      fail(TS_INVALID_ARGUMENT, "shard: rank must be in [0, world), world in [1, 64]");
+    ts_status rc = ts_engine_create(cfg, capacity_tokens, 1, out);
+    if (rc != TS_OK) fail(rc, g_err);
+    (*out)->rank = rank;
+    (*out)->world = world;
+  });
+}
+
+namespace {
+
+// Parameters shared by the stats and select launches of one shard step.
+DecodeParams shard_params(ts_engine* e, int mode) {
+  ts_pool& pool = *e->pool;
+  const ts_engine_config& c = e->cfg;
+  const ShardStep& ss = e->shard;
+  DecodeParams p = base_params(&pool, static_cast<int>(c.num_heads), static_cast<int>(c.num_kv_heads),
+                               static_cast<int>(c.head_dim), static_cast<int>(c.k), c.selection_method, mode);
+  p.n_seq = 1;
+  ts_pool::Seq& s = pool.state(e->seq_ids[0]);
+  SeqDesc& sd = p.seqs[0];
+  sd.page_table = s.d_pt;
+  sd.n_cached = static_cast<int32_t>(s.len);
+  sd.select = ss.sel_on;
+  sd.cand_begin = ss.cand_first;
+  sd.n_cand = ss.T;
+  sd.q = ss.q;
+  sd.k_new = ss.k;
+  sd.v_new = ss.v;
+  sd.append_frame = -1;
+  sd.append_page = -1;
+  sd.cache = e->cache(0);
+  sd.cached_q = e->cq(0);
+  sd.sel = e->sl(0);
+  sd.sel_crit = e->sc(0);
+  sd.sel_rows = e->sr(0);
+  sd.shard_base = static_cast<int32_t>(ss.base);
+  sd.shard_world = e->world;
+  return p;
+}
+
+Plan shard_plan_for(ts_engine* e) {
+  const ts_engine_config& c = e->cfg;
+  return make_plan(static_cast<int>(c.num_heads), static_cast<int>(c.num_kv_heads), static_cast<int>(c.head_dim), 1,
+                   e->shard.T, 1, false, /*force_spill=*/true);
+}
+
+}  // namespace
+
+ts_status ts_shard_stats(ts_engine* e, const float* q, const float* k, const float* v, size_t base, size_t n_global,
+                         float* stats_out) {
+  return guarded([&] {
+    const ts_engine_config& c = e->cfg;
+    ShardStep& ss = e->shard;
+    const size_t n_r = e->pool->state(e->seq_ids[0]).len;
+    const bool first = e->rank == 0, last = e->rank == e->world - 1;
+    if (first && base != 0) fail(TS_INVALID_ARGUMENT, "shard: rank 0 must start at position 0");
+    if (base + n_r > n_global) fail(TS_INVALID_ARGUMENT, "shard: rows beyond the global length");
+    if (last && base + n_r != n_global) fail(TS_INVALID_ARGUMENT, "shard: the last shard must end the sequence");
+    if (e->world > 1 && first && n_r < std::min(c.n_init, n_global))
+      fail(TS_INVALID_ARGUMENT, "shard: rank 0 must hold the whole init window");
+    if (e->world > 1 && last && n_r < std::min(c.n_local, n_global))
+      fail(TS_INVALID_ARGUMENT, "shard: the last shard must hold the whole local window");
+    ss.q = q;
+    ss.k = k;
+    ss.v = v;
+    ss.base = base;
+    ss.n_global = n_global;
+    ss.n_local_len = n_r;
+    ss.sel_on = (c.k > 0 && n_global > c.n_init + c.n_local) ? 1 : 0;
+    const size_t lo = first ? std::min(c.n_init, n_r) : 0;
+    const size_t hi = last ? n_r - std::min(c.n_local, n_r) : n_r;
+    ss.cand_first = static_cast<int32_t>(lo);
+    ss.T = ss.sel_on && hi > lo ? static_cast<int32_t>(hi - lo) : 0;
+    DecodeParams p = shard_params(e, tsb::kModeCache | tsb::kModeScore | tsb::kModeSelect | tsb::kModeShardStats);
+    p.seqs[0].shard_stats = stats_out;
+    if (ss.sel_on) ck(cudaMemsetAsync(stats_out, 0xff, c.num_heads * 2 * 4, e->stream), "memset stats");  // NaN: unset
+    launch_decode(p, shard_plan_for(e), e->ws, e->stream);
+  });
+}
+
+ts_status ts_shard_select(ts_engine* e, const float* all_stats, uint32_t* cands_out) {
+  return guarded([&] {
+    const ts_engine_config& c = e->cfg;
+    ck(cudaMemsetAsync(cands_out + 2 * c.k, 0, 4, e->stream), "memset count");
+    if (!e->shard.sel_on) return;
+    DecodeParams p = shard_params(e, tsb::kModeSelect | tsb::kModeShardSelect);
+    p.seqs[0].shard_all = all_stats;
+    p.seqs[0].shard_cands = cands_out;
+    launch_decode(p, shard_plan_for(e), e->ws, e->stream);
+  });
+}
+
+ts_status ts_shard_attend(ts_engine* e, const uint32_t* all_cands, float* out_partial, float* ml_out) {
+  return guarded([&] {
+    const ts_engine_config& c = e->cfg;
+    ts_pool& pool = *e->pool;
+    const ShardStep& ss = e->shard;
+    ts_pool::Seq& s = pool.state(e->seq_ids[0]);
+    const size_t n_r = s.len, N = ss.n_global;
+    const bool first = e->rank == 0, last = e->rank == e->world - 1;
+    const size_t ie = std::min(c.n_init, N);
+    const size_t lbs = std::max(N - std::min(c.n_local, N), ie);
+    const size_t init_hi = first ? std::min(ie, n_r) : 0;
+    const size_t loc_lo = last ? std::max(lbs, ss.base) - ss.base : n_r;
+    cudaStream_t st = e->stream;
+    uint32_t* att = static_cast<uint32_t*>(e->s_att.ensure((n_r + c.k + 8) * 4));
+    int* natt = static_cast<int*>(e->s_natt.ensure(16));
+    ck(tsb::launch_shard_merge(all_cands, e->world, static_cast<int>(c.k), static_cast<uint32_t>(ie),
+                               static_cast<uint32_t>(lbs), static_cast<uint32_t>(ss.base), static_cast<uint32_t>(n_r),
+                               static_cast<uint32_t>(init_hi), static_cast<uint32_t>(loc_lo), att, natt, st),
+       "shard merge");
+    g_launches.fetch_add(1);
+    DecodeParams p = base_params(&pool, static_cast<int>(c.num_heads), static_cast<int>(c.num_kv_heads),
+                                 static_cast<int>(c.head_dim), static_cast<int>(c.k), c.selection_method,
+                                 tsb::kModeAttend | (last ? tsb::kModeAppend : 0));
+    p.n_seq = 1;
+    SeqDesc& sd = p.seqs[0];
+    sd.page_table = s.d_pt;
+    sd.n_cached = static_cast<int32_t>(n_r);
+    sd.select = 0;
+    sd.q = ss.q;
+    sd.k_new = ss.k;
+    sd.v_new = ss.v;
+    sd.out = out_partial;
+    sd.att_list = att;
+    sd.n_att_dev = natt;
+    sd.n_att = 0;
+    sd.no_cur = last ? 0 : 1;
+    sd.ml_out = ml_out;
+    sd.cache = e->cache(0);
+    sd.append_frame = -1;
+    sd.append_page = -1;
+    bool appended = false;
+    if (last) {
+      if (pool.free_list.empty()) fail(TS_CAPACITY, "append_kv: pool exhausted (need 1 frames, 0 free)");
+      const uint32_t f = pool.free_list.back();
+      pool.free_list.pop_back();
+      s.frames.push_back(f);
+      sd.append_frame = static_cast<int32_t>(f);
+      sd.append_slot = 0;
+      sd.append_page = static_cast<int32_t>(n_r);
+      appended = true;
+    }
+    const DeviceInfo& di = device_info();
+    const Plan pl = make_plan(static_cast<int>(c.num_heads), static_cast<int>(c.num_kv_heads),
+                              static_cast<int>(c.head_dim), 1, 0, di.num_sms * 64);
+    launch_decode(p, pl, e->ws, st);
+    if (appended) s.len += 1;
+  });
+}
+
+ts_status ts_shard_combine(const float* o_all, const float* ml_all, int world, size_t num_heads, size_t head_dim,
+                           float* out, void* stream) {
+  return guarded([&] {
+    device_info();
+    ck(tsb::launch_shard_combine(o_all, ml_all, world, static_cast<int>(num_heads), static_cast<int>(head_dim), out,
+                                 static_cast<cudaStream_t>(stream)),
+       "shard combine");
+    g_launches.fetch_add(1);
   });
 }
 

@@ -205,6 +205,170 @@ __global__ void __launch_bounds__(kQT * 32) prefill_attend_kernel(PrefillAttendP
   }
 }
 
+// ------------------------------------------------------- sharded decode
+// Global top-k over every shard's local top-k candidates:
+// the global top-k under the total order (24-bit key prefix desc, position
+// asc) is a subset of the union of the shards' local top-k under the same
+// order, so selecting from the union is exact. Shards' lists are ascending
+// and shards are ordered by position, so the concatenation is ascending and
+// ties resolve by concatenation order. Then this shard's attended rows
+// (local positions, ascending): its init rows, its selected rows filtered to
+// the current windows (attention.cpp:35-52), its local-window rows.
+constexpr int kMergeThreads = 1024;
+constexpr int kMergeBins = 4096;
+
+__device__ uint32_t block_scan_excl_1024(uint32_t v, uint32_t* scratch, uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t n = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += n;
+  }
+  __syncthreads();
+  if (lane == 31) scratch[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t w = scratch[lane];
+    uint32_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t n = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += n;
+    }
+    scratch[32 + lane] = wi - w;
+    if (lane == 31) scratch[64] = wi;
+  }
+  __syncthreads();
+  const uint32_t r = scratch[32 + warp] + inc - v;
+  *total = scratch[64];
+  __syncthreads();
+  return r;
+}
+
+// bin b of `hist` (descending) holding the kk-th largest; above = count in higher bins
+__device__ void merge_find_bin(const uint32_t* hist, uint32_t kk, uint32_t* scratch, int* bin, uint32_t* above) {
+  constexpr int per = kMergeBins / kMergeThreads;
+  const int t = threadIdx.x;
+  uint32_t c[per], sum = 0;
+#pragma unroll
+  for (int i = 0; i < per; ++i) {
+    c[i] = hist[kMergeBins - 1 - (t * per + i)];
+    sum += c[i];
+  }
+  uint32_t tot;
+  const uint32_t ex = block_scan_excl_1024(sum, scratch, &tot);
+  if (ex < kk && ex + sum >= kk) {
+    uint32_t acc = ex;
+    for (int i = 0; i < per; ++i) {
+      if (acc + c[i] >= kk) {
+        scratch[80] = kMergeBins - 1 - (t * per + i);
+        scratch[81] = acc;
+        break;
+      }
+      acc += c[i];
+    }
+  }
+  __syncthreads();
+  *bin = static_cast<int>(scratch[80]);
+  *above = scratch[81];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kMergeThreads) shard_merge_kernel(const uint32_t* all, int world, int k,
+                                                                   uint32_t ie, uint32_t lbs, uint32_t base,
+                                                                   uint32_t n_r, uint32_t init_hi, uint32_t loc_lo,
+                                                                   uint32_t* att, int* n_att) {
+  __shared__ uint32_t hist[kMergeBins];
+  __shared__ uint32_t scratch[128];
+  __shared__ uint32_t offs[65];
+  const int tid = threadIdx.x;
+  const size_t stride = 2 * static_cast<size_t>(k) + 1;
+  if (tid == 0) {
+    uint32_t o = 0;
+    for (int r = 0; r < world; ++r) {
+      offs[r] = o;
+      o += all[r * stride + 2 * k];
+    }
+    offs[world] = o;
+  }
+  __syncthreads();
+  const uint32_t total = offs[world];
+  auto entry = [&](uint32_t i, uint32_t* idx, uint32_t* key) {
+    int r = 0;
+    while (r + 1 < world && offs[r + 1] <= i) ++r;
+    const uint32_t j = i - offs[r];
+    *idx = all[r * stride + j];
+    *key = all[r * stride + k + j] >> 8;  // 24-bit prefix, as the fused kernel ranks
+  };
+  uint32_t tau = 0, need_eq = 0xffffffffu;
+  const bool radix = total > static_cast<uint32_t>(k);
+  if (radix) {
+    uint32_t kk = static_cast<uint32_t>(k), prefix = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      const int sh = pass == 0 ? 12 : 0;
+      for (int i = tid; i < kMergeBins; i += kMergeThreads) hist[i] = 0u;
+      __syncthreads();
+      for (uint32_t i = tid; i < total; i += kMergeThreads) {
+        uint32_t idx, key;
+        entry(i, &idx, &key);
+        if (pass == 0 || (key >> 12) == prefix) atomicAdd(&hist[(key >> sh) & (kMergeBins - 1)], 1u);
+      }
+      __syncthreads();
+      int b;
+      uint32_t above;
+      merge_find_bin(hist, kk, scratch, &b, &above);
+      kk -= above;
+      prefix = pass == 0 ? static_cast<uint32_t>(b) : (prefix << 12) | static_cast<uint32_t>(b);
+    }
+    tau = prefix;
+    need_eq = kk;  // ties at tau still to take, lowest positions first
+  }
+  // own init rows
+  for (uint32_t i = tid; i < init_hi; i += kMergeThreads) att[i] = i;
+  // own selected rows, ascending
+  uint32_t out = init_hi, eq_seen = 0;
+  for (uint32_t b0 = 0; b0 < total; b0 += kMergeThreads) {
+    const uint32_t i = b0 + tid;
+    uint32_t idx = 0, key = 0;
+    if (i < total) entry(i, &idx, &key);
+    const uint32_t is_eq = (radix && i < total && key == tau) ? 1u : 0u;
+    uint32_t eq_tot;
+    const uint32_t eq_rank = eq_seen + block_scan_excl_1024(is_eq, scratch, &eq_tot);
+    eq_seen += eq_tot;
+    bool take = i < total && (!radix || key > tau || (is_eq && eq_rank < need_eq));
+    take = take && idx >= ie && idx < lbs && idx >= base && idx < base + n_r;
+    uint32_t tot;
+    const uint32_t pos = block_scan_excl_1024(take ? 1u : 0u, scratch, &tot);
+    if (take) att[out + pos] = idx - base;
+    out += tot;
+  }
+  // own local-window rows
+  for (uint32_t i = loc_lo + tid; i < n_r; i += kMergeThreads) att[out + (i - loc_lo)] = i;
+  if (tid == 0) *n_att = static_cast<int>(out + (n_r > loc_lo ? n_r - loc_lo : 0));
+}
+
+// Cross-shard log-sum-exp merge of normalised outputs o_r with (M_r, L_r):
+// out = sum_r e^(M_r - M) L_r o_r / sum_r e^(M_r - M) L_r, shards in rank order.
+__global__ void shard_combine_kernel(const float* o_all, const float* ml_all, int world, int H, int d,
+                                     float* out) {
+  const int h = blockIdx.x;
+  for (int t = threadIdx.x; t < d; t += blockDim.x) {
+    float M = -INFINITY;
+    for (int r = 0; r < world; ++r) M = fmaxf(M, ml_all[(static_cast<size_t>(r) * H + h) * 2]);
+    float num = 0.f, den = 0.f;
+    for (int r = 0; r < world; ++r) {
+      const float mr = ml_all[(static_cast<size_t>(r) * H + h) * 2];
+      const float lr = ml_all[(static_cast<size_t>(r) * H + h) * 2 + 1];
+      if (mr == -INFINITY || lr == 0.f) continue;
+      const float w = expf(mr - M) * lr;
+      num = fmaf(w, o_all[(static_cast<size_t>(r) * H + h) * d + t], num);
+      den += w;
+    }
+    out[static_cast<size_t>(h) * d + t] = num / den;
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_kv_append(uint16_t* k_slab, uint16_t* v_slab, const float* k, const float* v,
@@ -257,6 +421,20 @@ cudaError_t launch_prefill_attend(const PrefillAttendParams& p, cudaStream_t st)
     if (e != cudaSuccess) return e;
   }
   prefill_attend_kernel<<<grid, kQT * 32, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_merge(const uint32_t* all, int world, int k, uint32_t ie, uint32_t lbs, uint32_t base,
+                               uint32_t n_r, uint32_t init_hi, uint32_t loc_lo, uint32_t* att, int* n_att,
+                               cudaStream_t st) {
+  if (world > 64) return cudaErrorInvalidValue;
+  shard_merge_kernel<<<1, kMergeThreads, 0, st>>>(all, world, k, ie, lbs, base, n_r, init_hi, loc_lo, att, n_att);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_combine(const float* o_all, const float* ml_all, int world, int H, int d, float* out,
+                                 cudaStream_t st) {
+  shard_combine_kernel<<<H, 128, 0, st>>>(o_all, ml_all, world, H, d, out);
   return cudaGetLastError();
 }
 

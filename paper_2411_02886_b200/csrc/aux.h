@@ -33,5 +33,10 @@ cudaError_t launch_windows(const uint32_t* sel, const int* n_sel_ptr, int n_sel_
                            int init_end, int local_begin, uint32_t* out, int* n_out,
                            unsigned int* bad, cudaStream_t st);
 cudaError_t launch_prefill_attend(const PrefillAttendParams& p, cudaStream_t st);
+cudaError_t launch_shard_merge(const uint32_t* all, int world, int k, uint32_t ie, uint32_t lbs, uint32_t base,
+                               uint32_t n_r, uint32_t init_hi, uint32_t loc_lo, uint32_t* att, int* n_att,
+                               cudaStream_t st);
+cudaError_t launch_shard_combine(const float* o_all, const float* ml_all, int world, int H, int d, float* out,
+                                 cudaStream_t st);
 
 }  // namespace tsb

@@ -1112,6 +1112,7 @@ __device__ void merge_group(const DecodeParams& p, const SeqDesc& sd, const Smem
     ob = obuf;
     __syncthreads();
   }
+  trace_pt(p, 29);
   for (int m = warp; m < G; m += nwarps) {
     float M = -INFINITY;
     for (int c = lane; c < chunks; c += 32) M = fmaxf(M, staged ? ob[c * rec + m * stride + d] : __ldcg(ob + c * rec + m * stride + d));
@@ -1125,9 +1126,16 @@ __device__ void merge_group(const DecodeParams& p, const SeqDesc& sd, const Smem
       L = fmaf(w, lc, L);
     }
     L = warp_sum(L);
-    if (lane == 0) linv[m] = 1.f / L;
+    if (lane == 0) {
+      linv[m] = L > 0.f ? 1.f / L : 0.f;  // a shard with no rows contributes nothing
+      if (sd.ml_out) {
+        sd.ml_out[(g + m * p.H_kv) * 2 + 0] = M;
+        sd.ml_out[(g + m * p.H_kv) * 2 + 1] = L;
+      }
+    }
   }
   __syncthreads();
+  trace_pt(p, 30);
 #pragma unroll 1
   for (int i = tid; i < G * d; i += blockDim.x) {
     const int m = i / d, t = i - (i / d) * d;
@@ -1250,7 +1258,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   double* scratch_d = reinterpret_cast<double*>(sm.scratch);  // the ring may be filling (speculative scan)
   int own = 0;  // 0 no selection, 1 miss (select), 2 hit, 3 zero query
   double own_cos = NAN;
-  if (sd.select) {
+  const bool shard_sel = (p.mode & kModeShardSelect) != 0;
+  if (sd.select && shard_sel) {
+    own = __ldcg(&sd.cache->last_hit) == 1 ? 2 : 1;  // decided by the kModeShardStats launch
+  } else if (sd.select) {
     if (p.mode & kModeCache) {
       DecisionLoads dl;
       decision_issue(sd, width, dl);
@@ -1338,7 +1349,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   // ---- phase 2: per-CTA softmax partials m = max_j S, z = sum_j e^(S - m) per
   // head (softmax_rows, tensor.cpp:31-52): warp per head, float4 rows, four
   // independent SFU chains per lane
-  if (do_select && own == 1 && p.method == 2) {
+  if (do_select && own == 1 && p.method == 2 && !shard_sel) {
     const size_t sh = stats_stride(p.ctas_per_seq);
     const size_t so = static_cast<size_t>(seq_id) * H * sh + cs;
     const int warp = tid >> 5, lane = tid & 31;
@@ -1388,10 +1399,48 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     // the new cached query (every CTA read the old one before B1)
     for (int i = cs * blockDim.x + tid; i < width; i += p.ctas_per_seq * blockDim.x) sd.cached_q[i] = sd.q[i];
   }
+  if (p.mode & kModeShardStats) {
+    // this shard's per-head (m, z) from its CTAs' partials (every CTA
+    // finished phase 2 at B1); S = e^(S - m_c) stays in the spill buffer
+    if (own == 1 && cs == 0 && p.method == 2) {
+      const size_t sh = stats_stride(p.ctas_per_seq);
+      for (int h = tid; h < H; h += blockDim.x) {
+        const float* mr = p.ws_m + (static_cast<size_t>(seq_id) * H + h) * sh;
+        const float* zr = p.ws_z + (static_cast<size_t>(seq_id) * H + h) * sh;
+        float M = -INFINITY;
+        for (int c = 0; c < p.ctas_per_seq; ++c) M = fmaxf(M, __ldcg(mr + c));
+        float Z = 0.f;
+        if (M > -INFINITY)
+          for (int c = 0; c < p.ctas_per_seq; ++c) {
+            const float mc = __ldcg(mr + c);
+            if (mc > -INFINITY) Z += __ldcg(zr + c) * expf(mc - M);
+          }
+        sd.shard_stats[h * 2 + 0] = M;
+        sd.shard_stats[h * 2 + 1] = Z;
+      }
+    }
+    return;
+  }
   const bool radix_own = do_select && own == 1 && T > p.k;
   if (do_select && own == 1) {
     float* ml = sm.f;                                   // [H] f_h = e^(m_c - M_h) / Z_h
-    if (p.method == 2) {
+    if (p.method == 2 && shard_sel) {
+      // global softmax stats from every shard's (m, z) (rank order); m_c of
+      // this CTA from its partial of the stats launch
+      const size_t sh = stats_stride(p.ctas_per_seq);
+      for (int h = tid; h < H; h += blockDim.x) {
+        float M = -INFINITY;
+        for (int r = 0; r < sd.shard_world; ++r) M = fmaxf(M, __ldcg(sd.shard_all + (r * H + h) * 2));
+        float Z = 0.f;
+        for (int r = 0; r < sd.shard_world; ++r) {
+          const float mr = __ldcg(sd.shard_all + (r * H + h) * 2);
+          if (mr > -INFINITY) Z += __ldcg(sd.shard_all + (r * H + h) * 2 + 1) * expf(mr - M);
+        }
+        const float mc = __ldcg(p.ws_m + (static_cast<size_t>(seq_id) * H + h) * sh + cs);
+        ml[h] = mc > -INFINITY ? fast_exp(mc - M) / Z : 0.f;
+      }
+      __syncthreads();
+    } else if (p.method == 2) {
       float* pm = reinterpret_cast<float*>(sm.ring);
       const int nc = p.ctas_per_seq;
       const int ncp = stats_stride(nc);
@@ -1566,7 +1615,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       uint32_t tot;
       const uint32_t pos = out_n + block_excl_scan(take ? 1u : 0u, sm.scratch, &tot);
       if (take) {
-        lt[pos] = cand_at(sd, j0 + jl);
+        lt[pos] = cand_at(sd, j0 + jl) + static_cast<uint32_t>(sd.shard_base);
         lc[pos] = key_float(key);
         lr[pos] = may_scan ? sm.frames[jl] : -1;
       }
@@ -1596,6 +1645,22 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       if (sd.sel_rows) sd.sel_rows[my0 + i] = __ldcg(lr + i);
     }
     if (cs == 0 && tid == 0) sd.cache->n_sel = static_cast<int>(tot);
+    if (shard_sel) {
+      for (int i = tid; i < myn; i += blockDim.x) {
+        sd.shard_cands[my0 + i] = __ldcg(lt + i);
+        sd.shard_cands[p.k + my0 + i] = float_key(__ldcg(lc + i));
+      }
+      if (cs == 0 && tid == 0) sd.shard_cands[2 * p.k] = tot;
+    }
+  }
+  if (shard_sel && own == 2 && cs == 0) {
+    // Selection Cache hit: this shard's cached candidates, with their keys
+    const int n = __ldcg(&sd.cache->n_sel);
+    for (int i = tid; i < n; i += blockDim.x) {
+      sd.shard_cands[i] = __ldcg(sd.sel + i);
+      sd.shard_cands[p.k + i] = float_key(__ldcg(sd.sel_crit + i));
+    }
+    if (tid == 0) sd.shard_cands[2 * p.k] = static_cast<uint32_t>(n);
   }
   trace_pt(p, 10);
   if (!(p.mode & kModeAttend) || (p.debug_flags & 8)) return;
@@ -1603,7 +1668,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   // ---- phase 7: split-K sparse flash-decoding (KV head x row chunk)
   AttView av{};
   if (sd.att_list) {
-    av.n_rows = sd.n_att;
+    av.n_rows = sd.n_att_dev ? __ldcg(sd.n_att_dev) : sd.n_att;
   } else {
     av.init_end = sd.init_end;
     av.lb = static_cast<int>(lbs);
@@ -1624,11 +1689,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   const AttSplit split = att_split(p.H_kv, p.ctas_per_seq);
   const int gi = cs % split.groups, ci = cs / split.groups;
   if (ci < split.chunks) {
-    const int total_rows = av.n_rows + 1;  // + current token
-    const int per = (total_rows + split.chunks - 1) / split.chunks;
+    const int total_rows = av.n_rows + (sd.no_cur ? 0 : 1);  // + current token
+    const int per = max(1, (total_rows + split.chunks - 1) / split.chunks);
     const int r0 = min(total_rows, ci * per);
     const int r1 = min(total_rows, r0 + per);
-    const bool with_cur = (r0 < r1) && (r1 == total_rows);
+    const bool with_cur = !sd.no_cur && (r0 < r1) && (r1 == total_rows);
     const int Gq = p.H / p.H_kv;
     const int stride = att_stride(p.d);
     for (int g = gi; g < p.H_kv; g += split.groups) {
@@ -1650,7 +1715,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
         sm.scratch[71] = last;
       }
       __syncthreads();
-      if (sm.scratch[71]) merge_group(p, sd, sm, g, parts, split.chunks);
+      if (sm.scratch[71]) {
+        trace_pt(p, 28);
+        merge_group(p, sd, sm, g, parts, split.chunks);
+        trace_pt(p, 31);
+      }
       __syncthreads();
     }
   }

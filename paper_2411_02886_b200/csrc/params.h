@@ -26,6 +26,9 @@ enum Mode : int {
   kModeAppend = 16,  // write the current token's K/V row into the pool
   kModeSOut = 32,    // also write S [H x T] to SeqDesc::s_out (score_paged API)
   kModeSIn = 64,     // S is given in SeqDesc::s_in (select API), skip the scan
+  // KV-sequence-sharded decode (config 4), one launch per exchange phase:
+  kModeShardStats = 128,   // stop after the scan: this shard's per-head (m, z) -> shard_stats
+  kModeShardSelect = 256,  // resume from the spilled e^(S-m): global stats in, local top-k out
 };
 
 // One sequence (request) of a launch. Everything is a device pointer.
@@ -56,6 +59,15 @@ struct SeqDesc {
   // optional I/O for the standalone APIs
   float* s_out;                // [H x n_cand] scores out (kModeSOut)
   const float* s_in;           // [H x n_cand] scores in (kModeSIn)
+  // sharded decode (kModeShard*, explicit-list attention)
+  int32_t shard_base;          // global position of local position 0
+  int32_t shard_world;         // number of shards
+  float* shard_stats;          // out [H][2]: this shard's (m, z) per head
+  const float* shard_all;      // in [world][H][2]: every shard's (m, z)
+  uint32_t* shard_cands;       // out [2k + 1]: global indices, keys, count
+  const int32_t* n_att_dev;    // device count of att_list (overrides n_att)
+  float* ml_out;               // out [H][2]: (M, L) of the normalised output
+  int32_t no_cur;              // 1: the current token belongs to another shard
 };
 
 constexpr int kMaxSeqPerLaunch = 16;

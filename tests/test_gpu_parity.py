@@ -196,14 +196,17 @@ def test_decode_stream_vs_oracle(sa, orc, H, H_kv, d, n, k):
         assert h1 == h2, f"step {step}: cache decision differs"
         hits.append(h1)
         want = o2
+        N = n + step
+        if not h2:
+            q_sel, N_sel = q, N  # the query the cached selection is made with
         if s1 != list(s2):
-            # tie tolerance against the oracle's full criticality, then the
-            # attention is checked on OUR selection (same windows, oracle math)
-            N = n + step
-            cand = np.arange(16, N - 32, dtype=np.uint32)
+            # tie tolerance against the oracle's criticality of the selecting
+            # query, then the attention is checked on OUR selection (same
+            # windows, oracle math)
             K_all, V_all = ref_rows(ref)
-            S = orc.score_paged(q.reshape(H, d), K_all[:N], H_kv, cand)
-            check_selection(s1, s2, orc.criticality(S, k), cand)
+            cand_sel = np.arange(16, N_sel - 32, dtype=np.uint32)
+            S = orc.score_paged(q_sel.reshape(H, d), K_all[:N_sel], H_kv, cand_sel)
+            check_selection(s1, s2, orc.criticality(S, k), cand_sel)
             att = orc.make_windows(N, 16, 32, np.asarray(s1, np.uint32))
             want = orc.sparse_attend(q, kt, vt, K_all[:N], V_all[:N], H, H_kv, att)
         assert rel_fro(o1, want) <= 1e-5, rel_fro(o1, want)
