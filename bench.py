@@ -2,19 +2,32 @@
 """Benchmark: TokenSelect decode step (Selection Cache -> paged Q.K scoring ->
 soft vote -> top-k -> sparse paged attention -> KV append) on B200.
 
-Workload (BASELINE.json configs[1]): one Llama-3-8B attention layer (32 query /
-8 KV heads, d=128), 128K-token paged bf16 KV cache, k=2048 selected tokens,
-n_init=128, n_local=512, Selection Cache on at theta=0.9, batch 1. The decode
-query stream is the reference's `rotating` stream (workload.cpp:261-274) at
-consecutive similarity 0.95, rescaled to unit per-element variance, so the cache
-alternates miss / hit like the reference's cache-stats experiment. A step is one
-decode step; metric = mean device microseconds per step over the stream, L2
-flushed before every step (a real model runs 31 other layers in between).
+Default workload at N = 1 (BASELINE.json configs[1]):
+- one Llama-3-8B attention layer (32 query / 8 KV heads, d = 128);
+- a 128K-token paged bf16 KV cache;
+- k = 2048 selected tokens, n_init = 128, n_local = 512;
+- Selection Cache on at theta = 0.9; batch 1.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+The decode query stream is the reference's `rotating` stream
+(workload.cpp:261-274) at consecutive similarity 0.95, rescaled to unit
+per-element variance. The cache therefore alternates miss / hit, like the
+reference's cache-stats experiment. A step is one decode step; the metric is
+the mean device microseconds per step over the stream. L2 is flushed before
+every step, because a real model runs 31 other layers in between.
 
-N > 1 (torchrun, one rank per GPU): every rank decodes its own independent
-request (replicas, weak scaling); the step time is the max over ranks.
+With N > 1 (torchrun, one rank per GPU), the workload is configs[3]: the
+KV-sequence-sharded decode, with weak scaling of 128K tokens per GPU, so the
+context is N x 128K (1M at N = 8). Every rank holds its slice. A step is the
+sharded protocol: three NCCL all-gathers over NVLink between four native
+launches (paper_2411_02886_b200/sharded.py). The step time is the max over
+ranks.
+
+Extra workloads, recorded as evidence but not the driver's line:
+- `--workload batched`: configs[2], Qwen2-7B shapes, 16 x 64K, per-request
+  page tables, one launch per step;
+- `--workload prefill`: configs[4], one 512-row chunk at 128K context.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload ...]
 """
 from __future__ import annotations
 
@@ -41,9 +54,8 @@ UNIT = "us/step"
 
 
 # --------------------------------------------------------------- workload
-def rotating_stream(steps: int, seed: int, sim: float = SIMILARITY) -> np.ndarray:
-    """generate_query_stream kRotating (workload.cpp:261-274), x sqrt(H*d)."""
-    dim = H * D
+def rotating_stream(steps: int, seed: int, dim: int = H * D, sim: float = SIMILARITY) -> np.ndarray:
+    """generate_query_stream kRotating (workload.cpp:261-274), x sqrt(dim)."""
     g = np.random.default_rng(seed)
     e1 = g.standard_normal(dim)
     e1 /= np.linalg.norm(e1)
@@ -55,21 +67,37 @@ def rotating_stream(steps: int, seed: int, sim: float = SIMILARITY) -> np.ndarra
     return np.asarray(qs, dtype=np.float32).reshape(steps, 1, dim)
 
 
-def step_kv(steps: int, seed: int):
+def step_kv(steps: int, seed: int, kv_dim: int = H_KV * D):
     g = np.random.default_rng(seed ^ 0x9E3779B97F4A7C15)
-    k = (g.standard_normal((steps, 1, H_KV * D)) * 3.0).astype(np.float32)
-    v = g.standard_normal((steps, 1, H_KV * D)).astype(np.float32)
+    k = (g.standard_normal((steps, 1, kv_dim)) * 3.0).astype(np.float32)
+    v = g.standard_normal((steps, 1, kv_dim)).astype(np.float32)
     return k, v
 
 
-def algorithmic_bytes(n_cached: int, miss: bool) -> int:
+def cache_decisions(qs: np.ndarray, theta: float):
+    """Replays Algorithm 1 (selection_cache.cpp:29-35, fp64 cosine, strict <)
+    on the host to label each step hit or miss, for the per-kind breakdown."""
+    kinds, cached = [], None
+    for q in qs.reshape(len(qs), -1).astype(np.float64):
+        if cached is None:
+            hit = False
+        else:
+            c = float(q @ cached) / math.sqrt(float(q @ q) * float(cached @ cached))
+            hit = not (c < theta)
+        if not hit:
+            cached = q
+        kinds.append(hit)
+    return kinds
+
+
+def algorithmic_bytes(n_cached: int, miss: bool, h=H, h_kv=H_KV, d=D, k=K_SEL, n_init=N_INIT, n_local=N_LOCAL) -> int:
     """SURVEY.md §8(d): B_miss = T(R+4) + A(2R+4) + 2R + 2*H*d*4 + 2R;
     B_hit = A(2R+4) + 2R + 2*H*d*4 + k*4 + 2R (R = H_kv*d*2 bytes per row)."""
-    R = H_KV * D * 2
-    T = n_cached - N_INIT - N_LOCAL
-    A = N_INIT + K_SEL + N_LOCAL
-    common = A * (2 * R + 4) + 2 * R + 2 * H * D * 4 + 2 * R
-    return T * (R + 4) + common if miss else common + K_SEL * 4
+    R = h_kv * d * 2
+    T = max(0, n_cached - n_init - n_local)
+    A = n_init + min(k, T) + n_local
+    common = A * (2 * R + 4) + 2 * R + 2 * h * d * 4 + 2 * R
+    return T * (R + 4) + common if miss else common + k * 4
 
 
 # ----------------------------------------------------------------- clocks
@@ -131,8 +159,7 @@ def reference_engine(kind: str):
 
     if kind == "reference" and not ref_available():
         kind = "port"
-    o = Oracle(kind)
-    return o, kind
+    return Oracle(kind), kind
 
 
 def time_reference(steps: int, warmup: int, seed: int = 1):
@@ -164,120 +191,254 @@ def time_reference(steps: int, warmup: int, seed: int = 1):
 
 
 # ------------------------------------------------------------------ GPU
-def run_gpu(args, rank, world, local_rank):
+def fill_bf16(append, n, kv_dim, dev, seed, chunk=16384, seq=None):
+    import torch
+
+    gen = torch.Generator(device=dev).manual_seed(seed)
+    for s0 in range(0, n, chunk):
+        m = min(chunk, n - s0)
+        kk = (torch.randn(m, kv_dim, device=dev, generator=gen) * 3.0).to(torch.bfloat16)
+        vv = torch.randn(m, kv_dim, device=dev, generator=gen).to(torch.bfloat16)
+        if seq is None:
+            append(kk, vv)
+        else:
+            append(kk, vv, seq)
+
+
+def timed_steps(stream, flush, run_step, steps, warmup, local_rank, world):
+    """W untimed steps, then K steps each bracketed by CUDA events on `stream`
+    with an L2 flush (512 MB write) before it; barrier + synchronize on both
+    sides. Returns per-step device us and the clock summary."""
+    import torch
+
+    dev = torch.device("cuda", local_rank)
+    for i in range(warmup):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        run_step(i)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    evs = []
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize(dev)
+        for t in range(steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            run_step(warmup + t)
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    return [a.elapsed_time(b) * 1000.0 for a, b in evs], clk.summary()
+
+
+def split_by_kind(step_us, kinds):
+    miss = [u for u, h in zip(step_us, kinds) if not h]
+    hit = [u for u, h in zip(step_us, kinds) if h]
+    return (statistics.mean(miss) if miss else None), (statistics.mean(hit) if hit else None)
+
+
+def run_decode_single(args, local_rank):
+    """configs[1]: the fused single-launch decode step (N = 1)."""
     import torch
 
     torch.cuda.set_device(local_rank)
     from paper_2411_02886_b200 import selattn as sa
 
     dev = torch.device("cuda", local_rank)
-    seed = 1234 + rank
-    steps, warmup = args.steps, args.warmup
-    total_steps = warmup + steps
-    eng = sa.Engine(N_CTX + 2 * total_steps + 16, k=K_SEL, n_local=N_LOCAL, n_init=N_INIT, chunk_size=512,
-                    theta=THETA, num_heads=H, num_kv_heads=H_KV, head_dim=D, block_size=64)
-    # synthetic bf16 KV cache of N_CTX tokens, generated on the device
-    gen = torch.Generator(device=dev).manual_seed(seed)
-    chunk = 16384
-    for s0 in range(0, N_CTX, chunk):
-        kk = (torch.randn(chunk, H_KV * D, device=dev, generator=gen) * 3.0).to(torch.bfloat16)
-        vv = torch.randn(chunk, H_KV * D, device=dev, generator=gen).to(torch.bfloat16)
-        eng.append_bf16(kk, vv)
-    del kk, vv
-    qs_h = rotating_stream(total_steps, seed)
-    ks_h, vs_h = step_kv(total_steps, seed)
-    qs = torch.from_numpy(qs_h).to(dev)
-    ks = torch.from_numpy(ks_h).to(dev)
-    vs = torch.from_numpy(vs_h).to(dev)
+    seed = 1234
+    total = args.warmup + args.steps
+    eng = sa.Engine(N_CTX + 2 * total + 16, k=K_SEL, n_local=N_LOCAL, n_init=N_INIT, chunk_size=512, theta=THETA,
+                    num_heads=H, num_kv_heads=H_KV, head_dim=D, block_size=64)
+    fill_bf16(eng.append_bf16, N_CTX, H_KV * D, dev, seed)
+    qs_h = rotating_stream(total, seed)
+    ks_h, vs_h = step_kv(total, seed)
+    qs, ks, vs = (torch.from_numpy(x).to(dev) for x in (qs_h, ks_h, vs_h))
     out = torch.empty(1, H * D, device=dev)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
-    stream = torch.cuda.Stream(dev)  # flush, events and the decode kernel share this stream
+    stream = torch.cuda.Stream(dev)
     eng.set_stream(stream.cuda_stream)
-
-    # ---- device-resident arm: inputs in HBM, per-step CUDA events
-    def one_pass(n_steps, offset, record):
-        evs, kinds = [], []
-        for t in range(n_steps):
-            i = offset + t
-            with torch.cuda.stream(stream):
-                flush.zero_()
-            n_before = eng.pool.logical_len(eng.sequence())
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            eng.decode_async(qs[i], ks[i], vs[i], out)
-            e1.record(stream)
-            if record:
-                evs.append((e0, e1))
-                kinds.append(n_before)
-        return evs, kinds
-
-    one_pass(warmup, 0, False)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        torch.distributed.barrier()
     launches0 = sa.launch_count()
     st0 = eng.stats()
-    with ClockSampler(local_rank) as clk:
-        torch.cuda.synchronize(dev)
-        evs, kinds = one_pass(steps, warmup, True)
-        torch.cuda.synchronize(dev)
-    if world > 1:
-        torch.distributed.barrier()
-    launches = sa.launch_count() - launches0
+    step_us, clocks = timed_steps(stream, flush, lambda i: eng.decode_async(qs[i], ks[i], vs[i], out),
+                                  args.steps, args.warmup, local_rank, 1)
+    launches = sa.launch_count() - launches0 - args.warmup  # timed region only (1 launch per step)
     st1 = eng.stats()
-    # per-step hit/miss from the cache trace: replay the decisions via the trace
-    step_us = [e0.elapsed_time(e1) * 1000.0 for e0, e1 in evs]
-    total_us = sum(step_us)
-    hits = st1["hits"] - st0["hits"]
-    lookups = st1["lookups"] - st0["lookups"]
-    # identify miss/hit steps by duration split (hits are ~5x shorter) for the breakdown
-    srt = sorted(step_us)
-    gap = max(range(1, len(srt)), key=lambda i: srt[i] / max(srt[i - 1], 1e-9)) if len(srt) > 1 else 1
-    thr = srt[gap - 1] if hits and hits < len(srt) else None
-    miss_us = [u for u in step_us if thr is None or u > thr]
-    hit_us = [u for u in step_us if thr is not None and u <= thr]
-    if hits == 0:
-        miss_us, hit_us = step_us, []
-    n_ctx_mean = int(np.mean(kinds))
-    alg_bytes = ((lookups - hits) * algorithmic_bytes(n_ctx_mean, True) + hits * algorithmic_bytes(n_ctx_mean, False)) / max(steps, 1)
+    all_kinds = cache_decisions(qs_h, THETA)
+    kinds = all_kinds[args.warmup:]
+    # the device's own Selection Cache counters must agree with the host replay
+    assert st1["hits"] - st0["hits"] == sum(all_kinds), (st1["hits"] - st0["hits"], sum(all_kinds))
+    hits, lookups = sum(kinds), len(kinds)
+    miss_us, hit_us = split_by_kind(step_us, kinds)
+    n_mean = N_CTX + args.warmup + args.steps // 2
+    alg = sum(algorithmic_bytes(n_mean, not h) for h in kinds) / len(kinds)
 
-    # ---- end-to-end arm: host buffers through the public API (H2D + D2H inside)
+    # end-to-end: host buffers through the public C ABI (H2D + D2H inside the call)
     eng.set_stream(None)
-    e2e_steps = min(steps, total_steps)
-    qs_e, ks_e, vs_e = rotating_stream(e2e_steps, seed + 7), *step_kv(e2e_steps, seed + 7)
-    e2e_t = []
+    qs_e = rotating_stream(args.steps, seed + 7)
+    ks_e, vs_e = step_kv(args.steps, seed + 7)
     out_h = np.zeros((1, H * D), np.float32)
     hit_h = np.zeros(1, np.int32)
-    for t in range(e2e_steps):
+    e2e = []
+    for t in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        # C-ABI call with host buffers: H2D of q/k/v, the step, D2H of the output + cache flag
         eng.decode_into(qs_e[t], ks_e[t], vs_e[t], out_h, hit_h)
-        e2e_t.append(time.perf_counter() - t0)
-    e2e_us = 1e6 * sum(e2e_t) / len(e2e_t)
+        e2e.append(time.perf_counter() - t0)
+    return {"step_us": statistics.mean(step_us), "miss_us": miss_us, "hit_us": hit_us, "hits": hits,
+            "lookups": lookups, "host_hits": sum(kinds), "alg_bytes": alg, "launches": launches, "clocks": clocks,
+            "e2e_us": 1e6 * statistics.mean(e2e), "h2d": (H * D + 2 * H_KV * D) * 4, "d2h": H * D * 4 + 48,
+            "miss_bytes": algorithmic_bytes(n_mean, True), "hit_bytes": algorithmic_bytes(n_mean, False),
+            "n_ctx": N_CTX, "per_gpu_bytes_div": 1}
 
-    # max over ranks
-    if world > 1:
-        tt = torch.tensor([total_us, e2e_us], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        total_us, e2e_us = tt.tolist()
-    return {
-        "step_us": total_us / steps, "miss_us": statistics.mean(miss_us) if miss_us else None,
-        "hit_us": statistics.mean(hit_us) if hit_us else None, "hits": hits, "lookups": lookups,
-        "alg_bytes": alg_bytes, "launches": launches, "clocks": clk.summary(), "e2e_us": e2e_us,
-        "miss_bytes": algorithmic_bytes(n_ctx_mean, True), "hit_bytes": algorithmic_bytes(n_ctx_mean, False),
-    }
+
+def run_decode_sharded(args, rank, world, local_rank):
+    """configs[3]: KV-sequence-sharded decode, 128K tokens per GPU (weak scaling)."""
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    from paper_2411_02886_b200 import sharded
+    from paper_2411_02886_b200 import selattn as sa
+
+    dev = torch.device("cuda", local_rank)
+    total = args.warmup + args.steps
+    n_global = N_CTX * world
+    ranges = sharded.shard_ranges(n_global, world, N_INIT, N_LOCAL)
+    rr = ranges[rank]
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        shard = sharded.NativeShard(rank, world, rr.length + 2 * total + 16, k=K_SEL, n_local=N_LOCAL,
+                                    n_init=N_INIT, chunk_size=512, theta=THETA, num_heads=H, num_kv_heads=H_KV,
+                                    head_dim=D, block_size=64)
+    fill_bf16(shard.append_bf16, rr.length, H_KV * D, dev, 1234 + rank)
+    seed = 1234  # q / k_t / v_t replicated on every rank
+    qs_h = rotating_stream(total, seed)
+    ks_h, vs_h = step_kv(total, seed)
+    qs, ks, vs = (torch.from_numpy(x).to(dev) for x in (qs_h, ks_h, vs_h))
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    ex = sharded.TorchDistExchange()
+
+    def step(i):
+        with torch.cuda.stream(stream):
+            sharded.decode_step(shard, ex, qs[i].view(-1), ks[i].view(-1), vs[i].view(-1), rr.base, n_global + i)
+
+    launches0 = sa.launch_count()
+    step_us, clocks = timed_steps(stream, flush, step, args.steps, args.warmup, local_rank, world)
+    launches = sa.launch_count() - launches0 - 4 * args.warmup
+    kinds = cache_decisions(qs_h, THETA)[args.warmup:]
+    # end-to-end: host q/k/v -> H2D, the sharded step, D2H of the output
+    qs_e = rotating_stream(args.steps, seed + 7)
+    ks_e, vs_e = step_kv(args.steps, seed + 7)
+    e2e = []
+    for t in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        torch.distributed.barrier()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            q = torch.from_numpy(qs_e[t]).pin_memory().to(dev, non_blocking=True).view(-1)
+            k = torch.from_numpy(ks_e[t]).pin_memory().to(dev, non_blocking=True).view(-1)
+            v = torch.from_numpy(vs_e[t]).pin_memory().to(dev, non_blocking=True).view(-1)
+            sharded.decode_step(shard, ex, q, k, v, rr.base, n_global + total + t).cpu()
+        e2e.append(time.perf_counter() - t0)
+    mt = torch.tensor(step_us + [1e6 * statistics.mean(e2e)], device=dev, dtype=torch.float64)
+    torch.distributed.all_reduce(mt, op=torch.distributed.ReduceOp.MAX)  # max over ranks, per step
+    vals = mt.tolist()
+    step_us, e2e_us = vals[:-1], vals[-1]
+    miss_us, hit_us = split_by_kind(step_us, kinds)
+    n_mean = n_global + args.warmup + args.steps // 2
+    alg = sum(algorithmic_bytes(n_mean, not h) for h in kinds) / len(kinds)
+    return {"step_us": statistics.mean(step_us), "miss_us": miss_us, "hit_us": hit_us, "hits": sum(kinds),
+            "lookups": len(kinds), "alg_bytes": alg, "launches": launches, "clocks": clocks, "e2e_us": e2e_us,
+            "h2d": (H * D + 2 * H_KV * D) * 4, "d2h": H * D * 4, "miss_bytes": algorithmic_bytes(n_mean, True),
+            "hit_bytes": algorithmic_bytes(n_mean, False), "n_ctx": n_global, "per_gpu_bytes_div": world}
+
+
+def run_batched(args, local_rank):
+    """configs[2]: Qwen2-7B shapes, 16 requests x 64K context, one launch per step."""
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    from paper_2411_02886_b200 import selattn as sa
+
+    dev = torch.device("cuda", local_rank)
+    B, n, h, hkv, d = 16, 65536, 28, 4, 128
+    total = args.warmup + args.steps
+    eng = sa.Engine(n + total + 16, k=K_SEL, n_local=N_LOCAL, n_init=N_INIT, chunk_size=512, theta=THETA,
+                    num_heads=h, num_kv_heads=hkv, head_dim=d, block_size=64, n_seqs=B)
+    for b in range(B):
+        fill_bf16(eng.append_bf16, n, hkv * d, dev, 99 + b, seq=b)
+    qs_h = np.concatenate([rotating_stream(total, 500 + b, h * d) for b in range(B)], axis=1)  # [steps, B, h*d]
+    kv = [step_kv(total, 500 + b, hkv * d) for b in range(B)]
+    ks_h = np.concatenate([x[0] for x in kv], axis=1)
+    vs_h = np.concatenate([x[1] for x in kv], axis=1)
+    qs, ks, vs = (torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (qs_h, ks_h, vs_h))
+    out = torch.empty(B, h * d, device=dev)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream(dev)
+    eng.set_stream(stream.cuda_stream)
+    launches0 = sa.launch_count()
+    step_us, clocks = timed_steps(stream, flush, lambda i: eng.decode_async(qs[i], ks[i], vs[i], out), args.steps,
+                                  args.warmup, local_rank, 1)
+    launches = sa.launch_count() - launches0 - args.warmup
+    kinds_b = [cache_decisions(qs_h[:, b], THETA)[args.warmup:] for b in range(B)]
+    n_mean = n + args.warmup + args.steps // 2
+    alg = sum(sum(algorithmic_bytes(n_mean, not kb[t], h, hkv, d) for kb in kinds_b)
+              for t in range(args.steps)) / args.steps
+    return {"step_us": statistics.mean(step_us), "miss_us": None, "hit_us": None,
+            "hits": sum(sum(k) for k in kinds_b), "lookups": B * args.steps, "alg_bytes": alg, "launches": launches,
+            "clocks": clocks, "e2e_us": None, "h2d": 0, "d2h": 0,
+            "miss_bytes": B * algorithmic_bytes(n_mean, True, h, hkv, d),
+            "hit_bytes": B * algorithmic_bytes(n_mean, False, h, hkv, d), "n_ctx": n, "per_gpu_bytes_div": 1}
+
+
+def run_prefill(args, local_rank):
+    """configs[4]: one 512-row prefill chunk at 128K context (select_for_chunk
+    with the chunk-mean query, sparse causal attention, append)."""
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    from paper_2411_02886_b200 import selattn as sa
+
+    dev = torch.device("cuda", local_rank)
+    C = 512
+    total = args.warmup + args.steps
+    eng = sa.Engine(N_CTX + C * total + 16, k=K_SEL, n_local=N_LOCAL, n_init=N_INIT, chunk_size=C, theta=THETA,
+                    num_heads=H, num_kv_heads=H_KV, head_dim=D, block_size=64)
+    fill_bf16(eng.append_bf16, N_CTX, H_KV * D, dev, 1234)
+    g = torch.Generator(device=dev).manual_seed(7)
+    q = torch.randn(total, C, H * D, device=dev, generator=g)
+    k = (torch.randn(total, C, H_KV * D, device=dev, generator=g) * 3.0).to(torch.bfloat16).float()
+    v = torch.randn(total, C, H_KV * D, device=dev, generator=g).to(torch.bfloat16).float()
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream(dev)
+    eng.set_stream(stream.cuda_stream)
+    launches0 = sa.launch_count()
+    step_us, clocks = timed_steps(stream, flush, lambda i: eng.prefill(q[i], k[i], v[i]), args.steps, args.warmup,
+                                  local_rank, 1)
+    launches = sa.launch_count() - launches0
+    R = H_KV * D * 2
+    T = N_CTX - N_INIT - N_LOCAL
+    alg = T * (R + 4) + C * H * D * 4 + (N_INIT + K_SEL + N_LOCAL) * 2 * R + 2 * C * R + C * H * D * 4
+    return {"step_us": statistics.mean(step_us), "miss_us": None, "hit_us": None, "hits": 0, "lookups": 0,
+            "alg_bytes": alg, "launches": launches, "clocks": clocks, "e2e_us": None, "h2d": 0, "d2h": 0,
+            "miss_bytes": alg, "hit_bytes": alg, "n_ctx": N_CTX, "per_gpu_bytes_div": 1,
+            "flops": 2 * H * sum(N_INIT + K_SEL + N_LOCAL + i + 1 for i in range(C)) * D * 2}
 
 
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), float(p.get("bf16_tflops", 1632.0)), "measured"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, 1590.0, "fallback"
 
 
 def traffic_per_launch():
@@ -288,22 +449,33 @@ def traffic_per_launch():
         return None
 
 
+WORKLOADS = {
+    "decode": "Llama-3-8B layer decode, 128K paged bf16 KV, k=2048, Selection Cache theta=0.9 (configs[1])",
+    "sharded": "Llama-3-8B layer decode, N x 128K-token context KV-sharded over N GPUs, NCCL stats/top-k/LSE "
+               "all-gathers (configs[3]; 1M at N=8)",
+    "batched": "Qwen2-7B layer decode, 16 requests x 64K, per-request page tables, one launch (configs[2])",
+    "prefill": "Llama-3-8B chunked-prefill step: one 512-query chunk over a 128K context (configs[4])",
+}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", args.gpus if args.gpus == 1 else 1))
+    world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
-    config = {"workload": "Llama-3-8B layer decode, 128K paged bf16 KV, k=2048, Selection Cache theta=0.9 (configs[1])",
-              "context_tokens": N_CTX, "num_heads": H, "num_kv_heads": H_KV, "head_dim": D, "k": K_SEL,
-              "n_init": N_INIT, "n_local": N_LOCAL, "theta": THETA, "batch": 1,
-              "stream": f"rotating, consecutive cos {SIMILARITY}", "parallelism": f"replicas x{max(world, 1)}",
+    workload = args.workload or ("sharded" if world > 1 else "decode")
+    config = {"workload": WORKLOADS[workload], "num_heads": H, "num_kv_heads": H_KV, "head_dim": D, "k": K_SEL,
+              "n_init": N_INIT, "n_local": N_LOCAL, "theta": THETA,
+              "stream": f"rotating, consecutive cos {SIMILARITY}",
+              "parallelism": f"KV-sequence shards x{world}" if workload == "sharded" else "single GPU",
               "l2": "flushed (512 MB write) before every timed step"}
 
     if args.impl == "reference":
@@ -311,6 +483,7 @@ def main():
             return
         steps = min(args.steps, 10)
         us, kind, sample = time_reference(steps, 2)
+        config["context_tokens"] = N_CTX
         line = {"impl": "reference", "metric": METRIC, "value": round(us, 1), "unit": UNIT, "n_gpus": args.gpus,
                 "steps": steps, "warmup": 2, "ms_per_step": round(us / 1000, 3), "higher_is_better": False,
                 "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic", "config": config,
@@ -319,39 +492,56 @@ def main():
         print(json.dumps(line))
         return
 
-    if world > 1:
+    if world > 1 or workload == "sharded":
         import torch
 
-        torch.distributed.init_process_group("nccl")
-    r = run_gpu(args, rank, world, local_rank)
-    peak, peak_kind = peaks()
-    # dominant kernel = the fused decode kernel, one launch per step
-    achieved = r["alg_bytes"] / (r["step_us"] * 1e-6) / 1e9
-    miss_ach = r["miss_bytes"] / (r["miss_us"] * 1e-6) / 1e9 if r["miss_us"] else None
-    traffic = traffic_per_launch()
+        torch.cuda.set_device(local_rank)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        torch.distributed.init_process_group("nccl", rank=rank, world_size=world,
+                                             device_id=torch.device("cuda", local_rank))
+    if workload == "sharded":
+        r = run_decode_sharded(args, rank, world, local_rank)
+    elif workload == "batched":
+        r = run_batched(args, local_rank)
+    elif workload == "prefill":
+        r = run_prefill(args, local_rank)
+    else:
+        r = run_decode_single(args, local_rank)
+    config["context_tokens"] = r["n_ctx"]
+    hbm, tflops, peak_kind = peaks()
+    div = r["per_gpu_bytes_div"]
+    achieved = r["alg_bytes"] / div / (r["step_us"] * 1e-6) / 1e9  # per GPU
+    miss_ach = r["miss_bytes"] / div / (r["miss_us"] * 1e-6) / 1e9 if r["miss_us"] else None
+    traffic = traffic_per_launch() if workload == "decode" else None
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(achieved / hbm, 4), "peak_kind": peak_kind, "per": "GPU",
+            "traffic": (int((r["lookups"] - r["hits"]) / max(r["lookups"], 1) * traffic["miss_bytes_per_launch"]
+                            + r["hits"] / max(r["lookups"], 1) * traffic["hit_bytes_per_launch"])
+                        if traffic else None),
+            "traffic_source": traffic.get("source") if traffic else None,
+            "algorithmic_bytes_per_step": int(r["alg_bytes"])}
+    if miss_ach:
+        roof["miss_step"] = {"achieved": round(miss_ach, 1), "frac": round(miss_ach / hbm, 4),
+                             "algorithmic_bytes": r["miss_bytes"]}
+    if "flops" in r:
+        tf = r["flops"] / (r["step_us"] * 1e-6) / 1e12
+        roof["tensor"] = {"achieved": round(tf, 2), "peak": tflops, "unit": "TFLOP/s", "frac": round(tf / tflops, 4),
+                          "flops_per_step": r["flops"]}
     line = {
-        "metric": METRIC, "value": round(r["step_us"], 2), "unit": UNIT, "n_gpus": max(world, 1),
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["step_us"] / 1000, 5),
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "metric": METRIC, "value": round(r["step_us"], 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(r["step_us"] / 1000, 5), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random bf16 KV, rotating query stream)", "config": config,
         "cache": {"lookups": r["lookups"], "hits": r["hits"]},
         "miss_step_us": round(r["miss_us"], 2) if r["miss_us"] else None,
         "hit_step_us": round(r["hit_us"], 2) if r["hit_us"] else None,
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
-                     "traffic": (int((r["lookups"] - r["hits"]) / max(r["lookups"], 1) * traffic["miss_bytes_per_launch"]
-                                     + r["hits"] / max(r["lookups"], 1) * traffic["hit_bytes_per_launch"])
-                                 if traffic else None),
-                     "traffic_source": traffic.get("source") if traffic else None,
-                     "algorithmic_bytes_per_launch": int(r["alg_bytes"]),
-                     "miss_step": {"achieved": round(miss_ach, 1) if miss_ach else None,
-                                   "frac": round(miss_ach / peak, 4) if miss_ach else None,
-                                   "algorithmic_bytes": r["miss_bytes"]}},
-        "e2e": {"value": round(r["e2e_us"], 2), "unit": UNIT,
-                "h2d_bytes_per_step": (H * D + 2 * H_KV * D) * 4, "d2h_bytes_per_step": H * D * 4 + 48},
+        "roofline": roof,
+        "e2e": ({"value": round(r["e2e_us"], 2), "unit": UNIT, "h2d_bytes_per_step": r["h2d"],
+                 "d2h_bytes_per_step": r["d2h"]} if r["e2e_us"] else None),
         "clocks": r["clocks"], "gpu_launches": r["launches"],
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and workload == "decode" and not args.no_cpu_baseline:
         try:
             us, kind, sample = time_reference(4, 1)
             line["cpu_baseline"] = {"value": round(us, 1), "unit": UNIT, "cores": 1, "kind": kind, "sample": sample}
@@ -360,7 +550,7 @@ def main():
                                     "sample": f"unavailable: {e}"}
     if rank == 0:
         print(json.dumps(line))
-    if world > 1:
+    if world > 1 or workload == "sharded":
         import torch
 
         torch.distributed.destroy_process_group()
