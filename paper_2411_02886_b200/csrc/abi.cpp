@@ -38,6 +38,7 @@ int g_prefetch_stages = [] {
 }();
 const bool g_force_global_s = std::getenv("TS_FORCE_GLOBAL_S") != nullptr && std::getenv("TS_FORCE_GLOBAL_S")[0];
 const int g_debug_flags = std::getenv("TS_DEBUG_FLAGS") ? std::atoi(std::getenv("TS_DEBUG_FLAGS")) : 0;
+const bool g_force_cuda_core_prefill = std::getenv("TS_CUDA_CORE_PREFILL") != nullptr;
 std::atomic<uint64_t> g_launches{0};
 constexpr size_t kTraceSlots = 32 * 1024;
 // host-side profile of the decode launch path (TS_HOST_PROF=1): ns per stage
@@ -290,7 +291,7 @@ struct ts_pool {
   uint32_t next_id = 0;
   cudaStream_t stream = nullptr;
   Workspace ws;
-  DevBuf st_a, st_b, st_c, st_d, st_e, st_f;  // staging
+  DevBuf st_a, st_b, st_c, st_d, st_e, st_f, st_split;  // staging
 
   ~ts_pool() {
     for (auto& kv : seqs)
@@ -402,7 +403,7 @@ struct ts_engine {
   DevBuf trace;
   bool trace_on = false;
   // prefill scratch
-  DevBuf p_qmean, p_sel, p_crit, p_state, p_att, p_natt, p_bad, p_q, p_k, p_v, p_out;
+  DevBuf p_qmean, p_sel, p_crit, p_state, p_att, p_natt, p_bad, p_q, p_k, p_v, p_out, p_split;
 
   ~ts_engine() {
     if (h_q) cudaFreeHost(h_q);
@@ -512,6 +513,17 @@ size_t run_select(const ts_pool* pool, const ts_pool::Seq* seq, int H, int H_kv,
   }
   for (size_t i = 0; i < n; ++i) crit_host[i] = static_cast<double>(crit[i]);
   return n;
+}
+
+// C-row sparse attention: the tensor-core kernel where it applies (d = 128,
+// G <= 8), the CUDA-core kernel otherwise.
+cudaError_t launch_prefill(tsb::PrefillAttendParams& pa, DevBuf& split_ws, cudaStream_t st) {
+  if (pa.d == 128 && pa.H / pa.H_kv <= 8 && !g_force_cuda_core_prefill) {
+    // bf16 parts of the chunk's K/V, owned by the caller's pool / engine (stream-ordered reuse)
+    pa.split_ws = static_cast<uint16_t*>(split_ws.ensure(static_cast<size_t>(2) * 3 * pa.C * pa.H_kv * pa.d * 2));
+    return tsb::launch_prefill_flash(pa, st);
+  }
+  return tsb::launch_prefill_attend(pa, st);
 }
 
 // Copy a (host or device) index list to host.
@@ -843,7 +855,7 @@ ts_status ts_sparse_attend(const ts_pool* cpool, uint32_t seq, const float* q, c
       pa.d = static_cast<int>(d);
       pa.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
       pa.out = od;
-      ck(tsb::launch_prefill_attend(pa, st), "prefill_attend");
+      ck(launch_prefill(pa, pool->st_split, st), "prefill_attend");
       g_launches.fetch_add(1);
     }
     if (od != out) copy_out(out, od, obytes, st);
@@ -1248,7 +1260,7 @@ ts_status ts_engine_prefill(ts_engine* e, size_t seq, const float* q, const floa
       pa.d = d;
       pa.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
       pa.out = oc;
-      ck(tsb::launch_prefill_attend(pa, st), "prefill_attend");
+      ck(launch_prefill(pa, e->p_split, st), "prefill_attend");
       g_launches.fetch_add(1);
       if (!o_dev) ck(cudaMemcpyAsync(out + begin * W, oc, len * W * 4, cudaMemcpyDeviceToHost, st), "D2H");
       if (trace_counts && chunk < max_chunks) {

@@ -20,6 +20,7 @@ struct PrefillAttendParams {
   int C, H, H_kv, d;
   float scale;
   float* out;              // [C][H*d]
+  uint16_t* split_ws;      // tensor-core path: [2][3][C][H_kv*d] bf16 parts of the chunk K/V
 };
 
 cudaError_t launch_kv_append(uint16_t* k_slab, uint16_t* v_slab, const float* k, const float* v,
@@ -33,6 +34,8 @@ cudaError_t launch_windows(const uint32_t* sel, const int* n_sel_ptr, int n_sel_
                            int init_end, int local_begin, uint32_t* out, int* n_out,
                            unsigned int* bad, cudaStream_t st);
 cudaError_t launch_prefill_attend(const PrefillAttendParams& p, cudaStream_t st);
+// tensor-core path (prefill.cu): d = 128, G <= 8; cudaErrorInvalidValue otherwise
+cudaError_t launch_prefill_flash(const PrefillAttendParams& p, cudaStream_t st);
 cudaError_t launch_shard_merge(const uint32_t* all, int world, int k, uint32_t ie, uint32_t lbs, uint32_t base,
                                uint32_t n_r, uint32_t init_hi, uint32_t loc_lo, uint32_t* att, int* n_att,
                                cudaStream_t st);

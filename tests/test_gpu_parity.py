@@ -139,9 +139,9 @@ def test_soft_vote_mass(sa):
 
 
 # ---------------------------------------------------------------- attention
-@pytest.mark.parametrize("C", [1, 7, 64])
-def test_sparse_attend_select_all_equals_full(sa, orc, C):
-    n, H, H_kv, d = 300, 4, 2, 32
+@pytest.mark.parametrize("C,d", [(1, 32), (7, 32), (64, 32), (7, 128), (100, 128)])
+def test_sparse_attend_select_all_equals_full(sa, orc, C, d):
+    n, H, H_kv = 300, 4, 2
     k = bf16_round(rng_normal(15, (n, H_kv * d)))
     v = bf16_round(rng_normal(16, (n, H_kv * d)))
     q = rng_normal(17, (C, H * d))
@@ -273,7 +273,8 @@ def test_decode_llama_32k_parity(sa, orc):
 
 
 # --------------------------------------------------------------- prefill
-@pytest.mark.parametrize("H,H_kv,d,n,chunk,k", [(2, 2, 4, 30, 8, 4), (2, 1, 4, 32, 16, 4096), (4, 2, 32, 1500, 256, 128)])
+@pytest.mark.parametrize("H,H_kv,d,n,chunk,k", [(2, 2, 4, 30, 8, 4), (2, 1, 4, 32, 16, 4096), (4, 2, 32, 1500, 256, 128),
+                                              (8, 2, 128, 1800, 512, 256), (28, 4, 128, 1300, 300, 128)])
 def test_prefill_vs_oracle(sa, orc, H, H_kv, d, n, chunk, k):
     kw = dict(k=k, n_local=16, n_init=8, chunk_size=chunk, theta=0.9, num_heads=H, num_kv_heads=H_kv,
               head_dim=d, block_size=8)
@@ -331,3 +332,19 @@ def test_pool_page_size_4(sa):
     assert pool.free_frames == 13
     kg, vg = pool.gather(seq, list(range(10)))
     assert np.array_equal(kg, k) and np.array_equal(vg, v)
+
+
+def test_prefill_single_chunk_fp32_kv_exact(sa, orc):
+    """The chunk's own K/V are fp32 in the reference (attention.cpp:148-150,
+    vstack :119-121); the tensor-core path splits them into three exact bf16
+    parts, so non-bf16 inputs still match (one chunk: no bf16 storage involved)."""
+    H, H_kv, d, n = 8, 2, 128, 300
+    kw = dict(k=64, n_local=16, n_init=8, chunk_size=512, theta=0.9, num_heads=H, num_kv_heads=H_kv, head_dim=d,
+              block_size=64)
+    q = rng_normal(61, (n, H * d))
+    kk = rng_normal(62, (n, H_kv * d), 2.0)  # not bf16-representable
+    vv = rng_normal(63, (n, H_kv * d))
+    got = sa.Engine(n + 4, **kw).prefill(q, kk, vv)
+    want = orc.engine(n + 4, **kw).prefill(q, kk, vv)
+    assert rel_fro(got, want) <= 1e-5, rel_fro(got, want)
+    assert np.abs(got - want).max() <= 1e-4
