@@ -162,17 +162,17 @@ struct Workspace {
     const int cps = n_ctas / n_seq;
     m.ensure(static_cast<size_t>(n_seq) * H * tsb::stats_stride(cps) * 4);
     z.ensure(static_cast<size_t>(n_seq) * H * tsb::stats_stride(cps) * 4);
-    hist.ensure(static_cast<size_t>(n_seq) * 2 * tsb::kRadixBins * 4);
+    hist.ensure(static_cast<size_t>(n_seq) * 2 * tsb::kHistPass * 4);
     cnt.ensure(static_cast<size_t>(n_ctas) * 4);
     nsel.ensure(static_cast<size_t>(n_ctas) * 4);
     sel_tok.ensure(static_cast<size_t>(n_ctas) * tpc * 4);
     sel_crit.ensure(static_cast<size_t>(n_ctas) * tpc * 4);
     sel_row.ensure(static_cast<size_t>(n_ctas) * tpc * 4);
     att.ensure(static_cast<size_t>(n_ctas) * H * tsb::att_stride(d) * 4);
-    const size_t na = static_cast<size_t>(n_seq) * H_kv;
+    const size_t na = static_cast<size_t>(tsb::kMaxSeqPerLaunch) * H_kv * 2;  // two slots alternate per launch
     if (na > acnt_n) {
       acnt.ensure(na * 4);
-      ck(cudaMemsetAsync(acnt.p, 0, na * 4, st), "memset counters");
+      ck(cudaMemsetAsync(acnt.p, 0, acnt.n, st), "memset counters");
       acnt_n = na;
     }
     if (!bar.p) {
@@ -893,11 +893,11 @@ ts_status ts_engine_create(const ts_engine_config* cfg, size_t capacity_tokens, 
     e->sel.ensure(n_seqs * kk * 4);
     e->sel_crit.ensure(n_seqs * kk * 4);
     e->sel_rows.ensure(n_seqs * kk * 4);
-    e->d_q.ensure(n_seqs * W * 4);
+    e->d_q.ensure(n_seqs * (W + 2 * KW) * 4);  // q | k | v staging block
     e->d_k.ensure(n_seqs * KW * 4);
     e->d_v.ensure(n_seqs * KW * 4);
     e->d_out.ensure(n_seqs * W * 4);
-    ck(cudaMallocHost(&e->h_q, n_seqs * W * 4), "pinned");
+    ck(cudaMallocHost(&e->h_q, n_seqs * (W + 2 * KW) * 4), "pinned");
     ck(cudaMallocHost(&e->h_k, n_seqs * KW * 4), "pinned");
     ck(cudaMallocHost(&e->h_v, n_seqs * KW * 4), "pinned");
     ck(cudaMallocHost(&e->h_out, n_seqs * W * 4), "pinned");
@@ -1048,9 +1048,21 @@ ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const f
       ck(cudaMemcpyAsync(dbuf.p, pinned, n * 4, cudaMemcpyHostToDevice, st), "H2D");
       return dbuf.as<float>();
     };
-    const float* qd = stage(q, e->h_q, e->d_q, B * W);
-    const float* kd = stage(k, e->h_k, e->d_k, B * KW);
-    const float* vd = stage(v, e->h_v, e->d_v, B * KW);
+    const float *qd, *kd, *vd;
+    if (!is_device_ptr(q) && !is_device_ptr(k) && !is_device_ptr(v)) {
+      // host inputs: one pinned staging block, one H2D copy
+      std::memcpy(e->h_q, q, B * W * 4);
+      std::memcpy(e->h_q + B * W, k, B * KW * 4);
+      std::memcpy(e->h_q + B * W + B * KW, v, B * KW * 4);
+      ck(cudaMemcpyAsync(e->d_q.p, e->h_q, (B * W + 2 * B * KW) * 4, cudaMemcpyHostToDevice, st), "H2D");
+      qd = e->d_q.as<float>();
+      kd = qd + B * W;
+      vd = kd + B * KW;
+    } else {
+      qd = stage(q, e->h_q, e->d_q, B * W);
+      kd = stage(k, e->h_k, e->d_k, B * KW);
+      vd = stage(v, e->h_v, e->d_v, B * KW);
+    }
     const bool out_dev = is_device_ptr(out);
     float* od = out_dev ? out : e->d_out.as<float>();
     std::vector<int> cap_fail = engine_step(e, qd, kd, vd, od);

@@ -114,38 +114,69 @@ __device__ __noinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* scratch, 
 // Finds, in a global histogram whose bins are ordered by key, the bin b such that
 // count(bins > b) < kk <= count(bins >= b). Returns b and count(bins > b).
 // All threads call; every CTA computes the same answer from the same data.
-__device__ __noinline__ void find_bin(const uint32_t* gh, uint32_t kk, uint32_t* scratch, int* bin_out,
-                                      uint32_t* above_out) {
-  // thread t < 512 covers bins [B - 8(t+1), B - 8t) in descending order; all
-  // 8 loads are in flight together and kept for the in-bin search
-  constexpr int kPer = kRadixBins / 512;
-  const int t = threadIdx.x;
-  uint32_t c[kPer];
-  uint32_t sum = 0;
+// Finds, in a pass histogram, the bin holding the kk-th largest key: 512
+// threads load 8 bins each (one parallel pass over the 16 KB) into shared
+// memory with 64-bin coarse sums, then warp 0 searches coarse then fine bins
+// with shuffles. Returns the bin, the count in higher bins and the bin's own
+// count. All threads call; `work` is >= 4096 + 64 words of shared memory.
+__device__ __noinline__ void find_bin(const uint32_t* gh, uint32_t kk, uint32_t* scratch, uint32_t* work,
+                                      int* bin_out, uint32_t* above_out, uint32_t* count_out) {
+  const int t = threadIdx.x, lane = t & 31;
+  uint32_t* coarse = work + kRadixBins;
+  if (t < 512) {
+    uint4 a = __ldcg(reinterpret_cast<const uint4*>(gh) + 2 * t);
+    uint4 b = __ldcg(reinterpret_cast<const uint4*>(gh) + 2 * t + 1);
+    reinterpret_cast<uint4*>(work)[2 * t] = a;
+    reinterpret_cast<uint4*>(work)[2 * t + 1] = b;
+    uint32_t sum = a.x + a.y + a.z + a.w + b.x + b.y + b.z + b.w;
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+    if ((t & 7) == 0) coarse[t >> 3] = sum;
+  }
+  __syncthreads();
+  if (t < 32) {
+    uint32_t base = 0, bin = 0, cnt = 0;
 #pragma unroll
-  for (int i = 0; i < kPer; ++i) c[i] = t < 512 ? __ldcg(gh + (kRadixBins - 1 - (t * kPer + i))) : 0u;
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) sum += c[i];
-  uint32_t tot;
-  const uint32_t ex = block_excl_scan(sum, scratch, &tot);
-  if (t < 512 && ex < kk && ex + sum >= kk) {
-    uint32_t acc = ex;
-    int found = -1;
-    uint32_t above = 0;
-#pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      if (found < 0 && acc + c[i] >= kk) {
-        found = kRadixBins - 1 - (t * kPer + i);
-        above = acc;
+    for (int level = 0; level < 2; ++level) {
+      // lane l covers bins (63 - 2l, 62 - 2l) of this level, descending
+      const uint32_t* src = level == 0 ? coarse : work + bin * 64;
+      const uint32_t c0 = src[63 - 2 * lane], c1 = src[62 - 2 * lane];
+      const uint32_t sum = c0 + c1;
+      const uint32_t incl = warp_incl_scan(sum, lane);
+      const uint32_t excl = incl - sum;
+      const uint32_t need = kk - base;
+      const bool here = excl < need && incl >= need;
+      const int src_lane = __ffs(__ballot_sync(0xffffffffu, here)) - 1;
+      uint32_t b = 0, ab = 0, c = 0;
+      if (here) {
+        if (excl + c0 >= need) {
+          b = 63 - 2 * lane;
+          ab = excl;
+          c = c0;
+        } else {
+          b = 62 - 2 * lane;
+          ab = excl + c0;
+          c = c1;
+        }
       }
-      acc += c[i];
+      b = __shfl_sync(0xffffffffu, b, src_lane);
+      ab = __shfl_sync(0xffffffffu, ab, src_lane);
+      c = __shfl_sync(0xffffffffu, c, src_lane);
+      base += ab;
+      bin = level == 0 ? b : bin * 64 + b;
+      cnt = c;
     }
-    scratch[64] = static_cast<uint32_t>(found);
-    scratch[65] = above;
+    if (lane == 0) {
+      scratch[64] = bin;
+      scratch[65] = base;
+      scratch[66] = cnt;
+    }
   }
   __syncthreads();
   *bin_out = static_cast<int>(scratch[64]);
   *above_out = scratch[65];
+  *count_out = scratch[66];
   __syncthreads();
 }
 
@@ -410,12 +441,20 @@ __device__ void scan_generic(const DecodeParams& p, const SeqDesc& sd, const Sme
 }
 
 // ------------------------------------------------------------ radix select
+// Adds this CTA's non-empty shared-histogram bins into the global one.
+__device__ __noinline__ void hist_merge(const uint32_t* hist, uint32_t* gh) {
+  for (int i = threadIdx.x; i < kRadixBins; i += blockDim.x) {
+    const uint32_t c = hist[i];
+    if (c) atomicAdd(gh + i, c);
+  }
+}
+
 // Local 12-bit digit histogram of this CTA's keys (optionally only keys whose
 // bits above `pshift` equal `prefix`), aggregated per warp with match.any so a
 // crowded bin costs one shared atomic per warp, then merged into the
 // sequence's global histogram `gh`. All threads call.
 __device__ __noinline__ void radix_hist(const uint32_t* keys, int nloc, int shift, int pshift, uint32_t prefix,
-                           uint32_t* hist, uint32_t* gh) {
+                                        uint32_t* hist, uint32_t* gh) {
   const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < kRadixBins; i += blockDim.x) hist[i] = 0u;
   __syncthreads();
@@ -435,19 +474,9 @@ __device__ __noinline__ void radix_hist(const uint32_t* keys, int nloc, int shif
     }
   }
   __syncthreads();
-  for (int i = tid; i < kRadixBins; i += blockDim.x) {
-    const uint32_t c = hist[i];
-    if (c) atomicAdd(gh + i, c);
-  }
+  hist_merge(hist, gh);
 }
 
-// Adds this CTA's non-empty shared-histogram bins into the global one.
-__device__ __noinline__ void hist_merge(const uint32_t* hist, uint32_t* gh) {
-  for (int i = threadIdx.x; i < kRadixBins; i += blockDim.x) {
-    const uint32_t c = hist[i];
-    if (c) atomicAdd(gh + i, c);
-  }
-}
 
 // One key into the shared histogram, aggregated over the warp's lanes that
 // hit the same bin (all lanes call; `act` marks the lanes with a key).
@@ -1082,71 +1111,39 @@ __device__ void attend_group(const DecodeParams& p, const SeqDesc& sd, const Att
 
 // Log-sum-exp merge of the row-chunk partials of KV head g (attention.cpp
 // :88-110 semantics): out[h] = sum_c e^(m_c - M) o_c / sum_c e^(m_c - M) l_c.
-// Every partial record (o, m, l) is staged in shared memory in one parallel
-// pass (8 16-byte loads in flight per thread), then combined there.
-__device__ void merge_group(const DecodeParams& p, const SeqDesc& sd, const Smem& sm, int g, const float* parts,
-                            int chunks) {
+// Every chunk CTA of the group merges its own slice of the G*d outputs once
+// all partials are in: one warp per output, lane c holding chunk c.
+__device__ void merge_slice(const DecodeParams& p, const SeqDesc& sd, int g, const float* parts, int chunks,
+                            int ci) {
   const int d = p.d, G = p.H / p.H_kv, stride = att_stride(d);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
   const size_t rec = static_cast<size_t>(G) * stride;  // floats per chunk
-  float* wts = reinterpret_cast<float*>(sm.ring);      // [chunks][G] weights
-  float* linv = wts + align_up(static_cast<size_t>(chunks) * G, 32);  // [G]
-  float* obuf = linv + 32;                             // [chunks][G][stride]
-  const size_t room = static_cast<size_t>(p.att_bytes) / 4 - (obuf - wts);
-  const bool staged = static_cast<size_t>(chunks) * rec <= room;
-  const float* ob = parts;
-  if (staged) {
-    const int n4 = static_cast<int>(chunks * rec / 4);
-    const float4* src = reinterpret_cast<const float4*>(parts);
-    float4* dst = reinterpret_cast<float4*>(obuf);
-    const int bd = blockDim.x;
-#pragma unroll 1
-    for (int i0 = tid; i0 < n4; i0 += 8 * bd) {
-      float4 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = i0 + u * bd < n4 ? __ldcg(src + i0 + u * bd) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (i0 + u * bd < n4) dst[i0 + u * bd] = v[u];
+  const int n_out = G * d, per = (n_out + chunks - 1) / chunks;
+  const int o0 = ci * per, o1 = min(n_out, o0 + per);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int o = o0 + warp; o < o1; o += nwarps) {
+    const int m = o / d, t = o - (o / d) * d;
+    const float* pm = parts + static_cast<size_t>(m) * stride;
+    float M = -INFINITY, L = 0.f, acc = 0.f;
+    for (int c0 = 0; c0 < chunks; c0 += 32) {
+      const int c = c0 + lane;
+      const float mc = c < chunks ? __ldcg(pm + c * rec + d) : -INFINITY;
+      const float lc = c < chunks ? __ldcg(pm + c * rec + d + 1) : 0.f;
+      const float oc = c < chunks ? __ldcg(pm + c * rec + t) : 0.f;
+      const float Mn = fmaxf(M, warp_max(mc));
+      if (Mn == -INFINITY) continue;
+      const float w = mc == -INFINITY ? 0.f : expf(mc - Mn);
+      const float a = M == -INFINITY ? 0.f : expf(M - Mn);
+      L = L * a + warp_sum(w * lc);
+      acc = acc * a + warp_sum(w * oc);
+      M = Mn;
     }
-    ob = obuf;
-    __syncthreads();
-  }
-  trace_pt(p, 29);
-  for (int m = warp; m < G; m += nwarps) {
-    float M = -INFINITY;
-    for (int c = lane; c < chunks; c += 32) M = fmaxf(M, staged ? ob[c * rec + m * stride + d] : __ldcg(ob + c * rec + m * stride + d));
-    M = warp_max(M);
-    float L = 0.f;
-    for (int c = lane; c < chunks; c += 32) {
-      const float mc = staged ? ob[c * rec + m * stride + d] : __ldcg(ob + c * rec + m * stride + d);
-      const float lc = staged ? ob[c * rec + m * stride + d + 1] : __ldcg(ob + c * rec + m * stride + d + 1);
-      const float w = mc == -INFINITY ? 0.f : expf(mc - M);
-      wts[c * G + m] = w;
-      L = fmaf(w, lc, L);
-    }
-    L = warp_sum(L);
     if (lane == 0) {
-      linv[m] = L > 0.f ? 1.f / L : 0.f;  // a shard with no rows contributes nothing
-      if (sd.ml_out) {
+      sd.out[static_cast<size_t>(g + m * p.H_kv) * d + t] = L > 0.f ? acc / L : 0.f;  // empty shard: 0
+      if (sd.ml_out && t == 0) {
         sd.ml_out[(g + m * p.H_kv) * 2 + 0] = M;
         sd.ml_out[(g + m * p.H_kv) * 2 + 1] = L;
       }
     }
-  }
-  __syncthreads();
-  trace_pt(p, 30);
-#pragma unroll 1
-  for (int i = tid; i < G * d; i += blockDim.x) {
-    const int m = i / d, t = i - (i / d) * d;
-    float a0 = 0.f, a1 = 0.f;
-    int c = 0;
-    for (; c + 1 < chunks; c += 2) {
-      a0 = fmaf(wts[c * G + m], staged ? ob[c * rec + m * stride + t] : __ldcg(ob + c * rec + m * stride + t), a0);
-      a1 = fmaf(wts[(c + 1) * G + m], staged ? ob[(c + 1) * rec + m * stride + t] : __ldcg(ob + (c + 1) * rec + m * stride + t), a1);
-    }
-    if (c < chunks) a0 = fmaf(wts[c * G + m], staged ? ob[c * rec + m * stride + t] : __ldcg(ob + c * rec + m * stride + t), a0);
-    sd.out[static_cast<size_t>(g + m * p.H_kv) * d + t] = (a0 + a1) * linv[m];
   }
 }
 
@@ -1178,7 +1175,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   for (int h = tid; h < H; h += blockDim.x) sm.headmax[h] = float_ord(-INFINITY);
   fence_mbar_init();
   GridSync gs{p.bar + p.bar_slot, static_cast<unsigned int>(nblocks), 0u};
-  if (cta == 0 && tid == 0) p.bar[p.bar_slot ^ 32] = 0u;  // the next launch's counter
+  if (cta == 0) {  // the next launch's grid-barrier and merge counters
+    if (tid == 0) p.bar[p.bar_slot ^ 32] = 0u;
+    unsigned int* nxt = p.ws_acnt + (p.bar_slot ? 0 : kMaxSeqPerLaunch * p.H_kv);
+    for (int i = tid; i < kMaxSeqPerLaunch * p.H_kv; i += blockDim.x) nxt[i] = 0u;
+  }
 
   trace_pt(p, 0);
   if (p.debug_flags & 16) return;  // dev timing: launch + prologue only
@@ -1307,8 +1308,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   for (int jl = tid + 4 * blockDim.x; may_scan && jl < nloc; jl += blockDim.x)
     sm.frames[jl] = static_cast<int32_t>(row_index(sd, cand_at(sd, j0 + jl), p.page_size));
   if (do_select && own == 1 && T > p.k) {
-    uint32_t* gh = p.ws_hist + static_cast<size_t>(seq_id) * 2 * kRadixBins;
-    for (int i = cs * blockDim.x + tid; i < 2 * kRadixBins; i += p.ctas_per_seq * blockDim.x) gh[i] = 0u;
+    uint32_t* gh = p.ws_hist + static_cast<size_t>(seq_id) * 2 * kHistPass;
+    for (int i = cs * blockDim.x + tid; i < 2 * kHistPass; i += p.ctas_per_seq * blockDim.x) gh[i] = 0u;
   }
   if (cs == 0 && tid == 0 && own == 3) sd.cache->error = 1;
   if (pre > 0 && own != 1)
@@ -1530,7 +1531,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   uint32_t tau = 0, take_eq_all = 1;
   uint32_t kk = static_cast<uint32_t>(p.k);
   if (any_radix) {
-    uint32_t* gh = p.ws_hist + static_cast<size_t>(seq_id) * 2 * kRadixBins;
+    uint32_t* gh = p.ws_hist + static_cast<size_t>(seq_id) * 2 * kHistPass;
     if (radix_own) hist_merge(sm.hist, gh);
     trace_pt(p, 15);
     gs.sync();  // B2
@@ -1539,11 +1540,12 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     if (radix_own) {
       int b;
       uint32_t above;
-      find_bin(gh, kk, sm.scratch, &b, &above);
+      uint32_t cnt;
+      find_bin(gh, kk, sm.scratch, sm.hist, &b, &above, &cnt);
       kk -= above;
       b1 = static_cast<uint32_t>(b);
       trace_pt(p, 16);
-      radix_hist(keys, nloc, 8, 20, b1, sm.hist, gh + kRadixBins);
+      radix_hist(keys, nloc, 8, 20, b1, sm.hist, gh + kHistPass);
     }
     trace_pt(p, 17);
     gs.sync();  // B3
@@ -1553,10 +1555,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     if (radix_own) {
       int b;
       uint32_t above;
-      find_bin(gh + kRadixBins, kk, sm.scratch, &b, &above);
+      find_bin(gh + kHistPass, kk, sm.scratch, sm.hist, &b, &above, &eq_total);
       kk -= above;
       tau = (b1 << 12) | static_cast<uint32_t>(b);
-      eq_total = __ldcg(gh + kRadixBins + b);
     }
     trace_pt(p, 18);
     // ties straddling the budget: the taken ones are the lowest positions,
@@ -1705,22 +1706,19 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
         attend_group<0, 0>(p, sd, av, sm, g, r0, min(r1, av.n_rows), with_cur,
                            parts + static_cast<size_t>(ci) * Gq * stride);
       trace_pt(p, 11);
-      // the last chunk to finish merges (no grid barrier)
+      // the group's chunks wait for each other (all co-resident), then each
+      // merges its slice of the outputs (no grid barrier)
       __syncthreads();
       if (tid == 0) {
-        unsigned int* ctr = p.ws_acnt + seq_id * p.H_kv + g;
-        const unsigned int old = atom_add_acqrel_u32(ctr, 1u);
-        const int last = old == static_cast<unsigned int>(split.chunks - 1);
-        if (last) *ctr = 0u;
-        sm.scratch[71] = last;
+        unsigned int* ctr = p.ws_acnt + (p.bar_slot ? kMaxSeqPerLaunch * p.H_kv : 0) + seq_id * p.H_kv + g;
+        red_release_add_u32(ctr, 1u);
+        while (ld_acquire_u32(ctr) < static_cast<unsigned int>(split.chunks)) {
+        }
       }
       __syncthreads();
-      if (sm.scratch[71]) {
-        trace_pt(p, 28);
-        merge_group(p, sd, sm, g, parts, split.chunks);
-        trace_pt(p, 31);
-      }
-      __syncthreads();
+      trace_pt(p, 28);
+      merge_slice(p, sd, g, parts, split.chunks, ci);
+      trace_pt(p, 31);
     }
   }
   trace_pt(p, 12);

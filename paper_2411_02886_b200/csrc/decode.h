@@ -19,6 +19,7 @@ constexpr int kDecodeThreads = kDecodeWarps * 32;
 constexpr int kMaxStages = 16;
 constexpr size_t kRingBudget = 96 * 1024;        // minimum K-row ring (also attention staging)
 constexpr int kRadixBins = 4096;                 // 12-bit radix digits (2 passes -> 24-bit keys)
+constexpr int kHistPass = kRadixBins;            // global histogram words per pass
 constexpr int kMaxPrefix = 256;                  // >= ctas_per_seq + 1
 constexpr int kAttMaxG = 8;                      // query heads per KV head on the attention path
 constexpr int kAttMaxRows = 256;                 // rows per attention sub-chunk (upper bound)

@@ -333,7 +333,7 @@ class Engine:
     SUB_POINTS = {13: "crit:stats_staged", 14: "crit:f_done", 15: "radix:hist1", 16: "radix:find1",
                   17: "radix:hist2", 18: "radix:find2", 19: "radix:ties", 20: "att:ridx", 21: "att:data",
                   22: "att:scores", 23: "att:softmax", 24: "att:pv", 25: "att:end", 26: "dec:issued",
-                  27: "dec:done", 28: "merge:arrived", 29: "merge:staged", 30: "merge:weights", 31: "merge:end"}
+                  27: "dec:done", 28: "merge:all_in", 31: "merge:end"}
 
     def set_trace(self, enable=True):
         check(lib.ts_engine_set_trace(self._h, 1 if enable else 0))
