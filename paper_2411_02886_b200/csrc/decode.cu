@@ -1623,6 +1623,17 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       out_n += tot;
     }
     if (tid == 0) p.ws_nsel[cta] = out_n;
+    if (FAST && (p.mode & kModeAttend)) {
+      // the attention CTAs gather these rows after B4: pull them into L2 now
+      __syncthreads();
+      const uint32_t rb = static_cast<uint32_t>(p.H_kv * p.d * 2);
+      const uint64_t pol = policy_evict_last();
+      for (uint32_t i = tid; i < 2 * out_n; i += blockDim.x) {
+        const int32_t r = __ldcg(lr + (i >> 1));
+        bulk_prefetch_l2((i & 1 ? reinterpret_cast<const char*>(p.v_slab) : reinterpret_cast<const char*>(p.k_slab)) +
+                             static_cast<size_t>(r) * rb, rb, pol);
+      }
+    }
   }
   trace_pt(p, 8);
   if (any_select) gs.sync();  // B4: per-CTA selections published
@@ -1639,12 +1650,6 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     const int my0 = sm.prefix[cs], myn = sm.prefix[cs + 1] - my0;
     const uint32_t* lt = p.ws_sel_tok + static_cast<size_t>(cta) * p.tpc;
     const float* lc = p.ws_sel_crit + static_cast<size_t>(cta) * p.tpc;
-    const int32_t* lr = p.ws_sel_row + static_cast<size_t>(cta) * p.tpc;
-    for (int i = tid; i < myn; i += blockDim.x) {
-      sd.sel[my0 + i] = __ldcg(lt + i);
-      sd.sel_crit[my0 + i] = __ldcg(lc + i);
-      if (sd.sel_rows) sd.sel_rows[my0 + i] = __ldcg(lr + i);
-    }
     if (cs == 0 && tid == 0) sd.cache->n_sel = static_cast<int>(tot);
     if (shard_sel) {
       for (int i = tid; i < myn; i += blockDim.x) {
@@ -1664,7 +1669,24 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     if (tid == 0) sd.shard_cands[2 * p.k] = static_cast<uint32_t>(n);
   }
   trace_pt(p, 10);
-  if (!(p.mode & kModeAttend) || (p.debug_flags & 8)) return;
+  // the SelectionResult (ascending) into the cache entry: nobody reads it in
+  // this launch, so it is written off the critical path (after the attention)
+  auto publish_selection = [&]() {
+    if (!(do_select && own == 1)) return;
+    const int my0 = sm.prefix[cs], myn = sm.prefix[cs + 1] - my0;
+    const uint32_t* lt = p.ws_sel_tok + static_cast<size_t>(cta) * p.tpc;
+    const float* lc = p.ws_sel_crit + static_cast<size_t>(cta) * p.tpc;
+    const int32_t* lr = p.ws_sel_row + static_cast<size_t>(cta) * p.tpc;
+    for (int i = tid; i < myn; i += blockDim.x) {
+      sd.sel[my0 + i] = __ldcg(lt + i);
+      sd.sel_crit[my0 + i] = __ldcg(lc + i);
+      if (sd.sel_rows) sd.sel_rows[my0 + i] = __ldcg(lr + i);
+    }
+  };
+  if (!(p.mode & kModeAttend) || (p.debug_flags & 8)) {
+    publish_selection();
+    return;
+  }
 
   // ---- phase 7: split-K sparse flash-decoding (KV head x row chunk)
   AttView av{};
@@ -1721,6 +1743,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       trace_pt(p, 31);
     }
   }
+  publish_selection();
   trace_pt(p, 12);
 }
 
