@@ -525,6 +525,7 @@ def main():
         import torch
 
         torch.cuda.set_device(local_rank)
+        os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29531")
         torch.distributed.init_process_group("nccl", rank=rank, world_size=world,

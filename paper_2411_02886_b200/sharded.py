@@ -78,6 +78,11 @@ class NativeShard:
         check(lib.ts_shard_engine_create(C.byref(self.cfg), capacity_tokens, rank, world, C.byref(h)))
         self._h = h
         self.H, self.H_kv, self.d, self.k = num_heads, num_kv_heads, head_dim, k
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self._stats = torch.empty(num_heads * 2, dtype=torch.float32, device=dev)
+        self._cands = torch.empty(2 * k + 1, dtype=torch.int32, device=dev)
+        self._part = torch.empty(num_heads * head_dim, dtype=torch.float32, device=dev)
+        self._ml = torch.empty(num_heads * 2, dtype=torch.float32, device=dev)
         # torch's default stream has handle 0, which the C ABI reads as "the
         # engine's own stream": pass cudaStreamLegacy (0x1) instead so both
         # sides order on the same stream
@@ -104,19 +109,18 @@ class NativeShard:
 
     # -- the four phases ----------------------------------------------------
     def stats(self, q, k, v, base: int, n_global: int):
-        out = self.torch.empty(self.H * 2, dtype=self.torch.float32, device=q.device)
+        out = self._stats
         check(lib.ts_shard_stats(self._h, self._p(q), self._p(k), self._p(v), base, n_global, self._p(out)))
         self._qkv = (q, k, v)  # keep alive until attend
         return out
 
     def select(self, all_stats):
-        out = self.torch.empty(2 * self.k + 1, dtype=self.torch.int32, device=all_stats.device)
+        out = self._cands
         check(lib.ts_shard_select(self._h, self._p(all_stats), self._p(out)))
         return out
 
     def attend(self, all_cands):
-        part = self.torch.empty(self.H * self.d, dtype=self.torch.float32, device=all_cands.device)
-        ml = self.torch.empty(self.H * 2, dtype=self.torch.float32, device=all_cands.device)
+        part, ml = self._part, self._ml
         check(lib.ts_shard_attend(self._h, self._p(all_cands), self._p(part), self._p(ml)))
         return part, ml
 
@@ -128,19 +132,30 @@ class NativeShard:
 
 
 class TorchDistExchange:
-    """all-gather of one flat tensor per rank via torch.distributed (rank order)."""
+    """all-gather of one flat tensor per rank via torch.distributed (rank
+    order): all_gather_into_tensor on NCCL (one collective, into a reused
+    output buffer per shape), the list form elsewhere (gloo)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
 
         self.dist, self.group = dist, group
+        self.nccl = dist.get_backend(group) == "nccl"
+        self.world = dist.get_world_size(group)
+        self._out = {}
 
     def all_gather(self, t):
         import torch
 
-        world = self.dist.get_world_size(self.group)
         t = t.contiguous()
-        parts = [torch.empty_like(t) for _ in range(world)]
+        if self.nccl:
+            key = (t.numel(), t.dtype, t.device)
+            out = self._out.get(key)
+            if out is None:
+                out = self._out[key] = torch.empty(self.world * t.numel(), dtype=t.dtype, device=t.device)
+            self.dist.all_gather_into_tensor(out, t, group=self.group)
+            return out
+        parts = [torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(parts, t, group=self.group)
         return torch.cat(parts)
 
@@ -156,14 +171,16 @@ def decode_step(shard, exchange, q, k, v, base: int, n_global: int):
 
 def simulate_step(shards: Sequence, qkv_per_shard, bases: Sequence[int], n_global: int):
     """All shards of one sequence in one process (single GPU): the exchanges
-    are concatenations in rank order -- the same bytes NCCL would deliver."""
+    are concatenations in rank order -- the same bytes NCCL would deliver
+    (each shard's phase outputs are copied before the next shard reuses its
+    buffers)."""
     import torch
 
-    stats = [s.stats(*qkv_per_shard[i], bases[i], n_global) for i, s in enumerate(shards)]
+    stats = [s.stats(*qkv_per_shard[i], bases[i], n_global).clone() for i, s in enumerate(shards)]
     all_stats = torch.cat(stats)
-    cands = [s.select(all_stats) for s in shards]
+    cands = [s.select(all_stats).clone() for s in shards]
     all_cands = torch.cat(cands)
-    parts = [s.attend(all_cands) for s in shards]
+    parts = [tuple(x.clone() for x in s.attend(all_cands)) for s in shards]
     all_part = torch.cat([p for p, _ in parts])
     all_ml = torch.cat([m for _, m in parts])
     outs = [s.combine(all_part, all_ml) for s in shards]
