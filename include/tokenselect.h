@@ -172,9 +172,11 @@ ts_status ts_engine_decode_async(ts_engine* eng, const float* q, const float* k,
  * selattn_bench.cpp:439 idiom). */
 ts_status ts_engine_force_miss(ts_engine* eng, size_t seq);
 /* Device phase trace of the fused decode kernel (tracing subsystem): when
- * enabled, every CTA stamps %globaltimer (ns) at the phase boundaries of the
- * decode step into stamps[cta * 32 + phase]; ts_engine_read_trace copies the
- * first n stamps of the last step (n <= 32768). */
+ * enabled, thread 0 of every CTA stamps its SM clock64 at the phase
+ * boundaries of the decode step into stamps[cta * 64 + phase]; slots 0 and 30
+ * hold %globaltimer (ns) at the start and at the end (slot 12), slot 29 the
+ * start clock. ts_engine_read_trace copies the first n stamps of the last
+ * step (n <= 65536). */
 ts_status ts_engine_set_trace(ts_engine* eng, int enable);
 ts_status ts_engine_read_trace(ts_engine* eng, uint64_t* stamps, size_t n);
 /* SelectionCacheEntry::theta of sequence `seq` (the reference reads theta

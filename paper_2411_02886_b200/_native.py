@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_build", "libtokenselect.so")
+# TS_LIB_PATH: an alternative build of the same library (dev A/B timing)
+LIB_PATH = os.environ.get("TS_LIB_PATH") or os.path.join(HERE, "_build", "libtokenselect.so")
 
 _sz = C.c_size_t
 _p = C.c_void_p

@@ -40,7 +40,7 @@ const bool g_force_global_s = std::getenv("TS_FORCE_GLOBAL_S") != nullptr && std
 const int g_debug_flags = std::getenv("TS_DEBUG_FLAGS") ? std::atoi(std::getenv("TS_DEBUG_FLAGS")) : 0;
 const bool g_force_cuda_core_prefill = std::getenv("TS_CUDA_CORE_PREFILL") != nullptr;
 std::atomic<uint64_t> g_launches{0};
-constexpr size_t kTraceSlots = 32 * 1024;
+constexpr size_t kTraceSlots = tsb::kTraceStride * 1024;
 // host-side profile of the decode launch path (TS_HOST_PROF=1): ns per stage
 const bool g_host_prof = std::getenv("TS_HOST_PROF") != nullptr;
 double g_prof[4] = {0, 0, 0, 0};

@@ -79,15 +79,34 @@ __device__ __forceinline__ size_t row_index(const SeqDesc& sd, uint32_t tok, int
   return static_cast<size_t>(sd.page_table[tok / page_size]) * page_size + tok % page_size;
 }
 
-// Phase trace: thread 0 of every CTA records %globaltimer at the phase
-// boundaries into trace[cta][32] when enabled.
+// Phase trace (thread 0 of every CTA, trace[cta][kTraceStride] when enabled):
+// SM clock64 stamps at the phase boundaries. The start (slot 0) and the end
+// (slot 12) also record %globaltimer (slots 0 / 30, ns; the start clock goes
+// to slot 29) so the host aligns the CTAs and converts cycles to ns.
 __device__ __forceinline__ void trace_pt(const DecodeParams& p, int i) {
   if (p.trace && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.trace[blockIdx.x * 32 + i] = t;
+    unsigned long long* t = p.trace + blockIdx.x * kTraceStride;
+    const unsigned long long c = clock64();
+    if (i == 0 || i == 12) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      t[i == 0 ? 0 : 30] = g;
+      t[i == 0 ? 29 : 12] = c;
+    } else {
+      t[i] = c;
+    }
   }
 }
+
+// Sub-phase stamp into a CTA's trace row (nullptr: off); thread 0 only.
+__device__ __forceinline__ void stamp(unsigned long long* tr, int i) {
+  if (tr && threadIdx.x == 0) tr[i] = clock64();
+}
+
+// Dev timing: TS_DEBUG_FLAGS = n << 8 ends the launch at stop point n
+// (uniform over the grid, so no barrier is left waiting).
+#define TSB_STOP_AT(n) \
+  if ((p.debug_flags >> 8) == (n)) return
 
 // Block-wide exclusive scan of one value per thread (all threads call).
 // Out of line (like find_bin / radix_hist): the fused kernel's one-shot phases
@@ -120,7 +139,8 @@ __device__ __noinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* scratch, 
 // with shuffles. Returns the bin, the count in higher bins and the bin's own
 // count. All threads call; `work` is >= 4096 + 64 words of shared memory.
 __device__ __noinline__ void find_bin(const uint32_t* gh, uint32_t kk, uint32_t* scratch, uint32_t* work,
-                                      int* bin_out, uint32_t* above_out, uint32_t* count_out) {
+                                      int* bin_out, uint32_t* above_out, uint32_t* count_out,
+                                      unsigned long long* tr, int ts) {
   const int t = threadIdx.x, lane = t & 31;
   uint32_t* coarse = work + kRadixBins;
   if (t < 512) {
@@ -135,6 +155,7 @@ __device__ __noinline__ void find_bin(const uint32_t* gh, uint32_t kk, uint32_t*
     if ((t & 7) == 0) coarse[t >> 3] = sum;
   }
   __syncthreads();
+  stamp(tr, ts);
   if (t < 32) {
     uint32_t base = 0, bin = 0, cnt = 0;
 #pragma unroll
@@ -260,6 +281,7 @@ __device__ int cache_decision(const SeqDesc& sd, int width, const DecisionLoads&
 }
 
 // --------------------------------------------------------------- the scan
+constexpr float kLog2e = 1.4426950408889634f;
 // Fast path (sm_100a tensor cores, mma.sync bf16 -> fp32). The K rows of a
 // stage (16 tokens, padded stride so ldmatrix is bank-conflict free) are the
 // M x K operand; the query, exactly split into three bf16 parts
@@ -454,10 +476,11 @@ __device__ __noinline__ void hist_merge(const uint32_t* hist, uint32_t* gh) {
 // crowded bin costs one shared atomic per warp, then merged into the
 // sequence's global histogram `gh`. All threads call.
 __device__ __noinline__ void radix_hist(const uint32_t* keys, int nloc, int shift, int pshift, uint32_t prefix,
-                                        uint32_t* hist, uint32_t* gh) {
+                                        uint32_t* hist, uint32_t* gh, unsigned long long* tr) {
   const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < kRadixBins; i += blockDim.x) hist[i] = 0u;
   __syncthreads();
+  stamp(tr, 38);
   for (int base = 0; base < nloc; base += blockDim.x) {
     const int jl = base + tid;
     uint32_t key = 0;
@@ -474,6 +497,7 @@ __device__ __noinline__ void radix_hist(const uint32_t* keys, int nloc, int shif
     }
   }
   __syncthreads();
+  stamp(tr, 39);
   hist_merge(hist, gh);
 }
 
@@ -1112,37 +1136,101 @@ __device__ void attend_group(const DecodeParams& p, const SeqDesc& sd, const Att
 // Log-sum-exp merge of the row-chunk partials of KV head g (attention.cpp
 // :88-110 semantics): out[h] = sum_c e^(m_c - M) o_c / sum_c e^(m_c - M) l_c.
 // Every chunk CTA of the group merges its own slice of the G*d outputs once
-// all partials are in: one warp per output, lane c holding chunk c.
+// all partials are in. One L2 round trip: the (m, l) of every chunk and this
+// slice's o values are loaded together into shared memory (`buf`, free
+// staging), then warp per head forms M, L and the chunk weights, and thread
+// per output sums its chunks.
 __device__ void merge_slice(const DecodeParams& p, const SeqDesc& sd, int g, const float* parts, int chunks,
-                            int ci) {
+                            int ci, float* buf) {
   const int d = p.d, G = p.H / p.H_kv, stride = att_stride(d);
   const size_t rec = static_cast<size_t>(G) * stride;  // floats per chunk
   const int n_out = G * d, per = (n_out + chunks - 1) / chunks;
-  const int o0 = ci * per, o1 = min(n_out, o0 + per);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  for (int o = o0 + warp; o < o1; o += nwarps) {
-    const int m = o / d, t = o - (o / d) * d;
-    const float* pm = parts + static_cast<size_t>(m) * stride;
-    float M = -INFINITY, L = 0.f, acc = 0.f;
-    for (int c0 = 0; c0 < chunks; c0 += 32) {
-      const int c = c0 + lane;
-      const float mc = c < chunks ? __ldcg(pm + c * rec + d) : -INFINITY;
-      const float lc = c < chunks ? __ldcg(pm + c * rec + d + 1) : 0.f;
-      const float oc = c < chunks ? __ldcg(pm + c * rec + t) : 0.f;
-      const float Mn = fmaxf(M, warp_max(mc));
-      if (Mn == -INFINITY) continue;
-      const float w = mc == -INFINITY ? 0.f : expf(mc - Mn);
-      const float a = M == -INFINITY ? 0.f : expf(M - Mn);
-      L = L * a + warp_sum(w * lc);
-      acc = acc * a + warp_sum(w * oc);
-      M = Mn;
+  const int o0 = ci * per, nout = min(n_out, o0 + per) - o0;
+  if (nout <= 0) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+  float* hdr = buf;                                // [G][2] M, L
+  float* wts = buf + 2 * kAttMaxG;                 // [G][chunks] (m_c, then the weight e^(m_c - M))
+  float* lcs = wts + G * chunks;                   // [G][chunks] l_c
+  float* ov = lcs + G * chunks;                    // [chunks][nout]
+  for (int i = tid; i < G * chunks; i += blockDim.x) {
+    const int m = i / chunks, c = i - (i / chunks) * chunks;
+    const float* r = parts + c * rec + static_cast<size_t>(m) * stride + d;
+    wts[i] = __ldcg(r);
+    lcs[i] = __ldcg(r + 1);
+  }
+  for (int i = tid; i < nout * chunks; i += blockDim.x) {
+    const int c = i / nout, oo = i - (i / nout) * nout;
+    const int o = o0 + oo, m = o / d, t = o - (o / d) * d;
+    ov[i] = __ldcg(parts + c * rec + static_cast<size_t>(m) * stride + t);
+  }
+  __syncthreads();
+  unsigned long long* const trc = p.trace ? p.trace + blockIdx.x * kTraceStride : nullptr;
+  stamp(trc, 42);
+  for (int m = warp; m < G; m += nwarps) {
+    float M = -INFINITY;
+    for (int c = lane; c < chunks; c += 32) M = fmaxf(M, wts[m * chunks + c]);
+    M = warp_max(M);
+    float L = 0.f;
+    for (int c = lane; c < chunks; c += 32) {
+      const float mc = wts[m * chunks + c];
+      const float w = (M == -INFINITY || mc == -INFINITY) ? 0.f : expf(mc - M);
+      wts[m * chunks + c] = w;
+      L = fmaf(w, lcs[m * chunks + c], L);
     }
+    L = warp_sum(L);
     if (lane == 0) {
-      sd.out[static_cast<size_t>(g + m * p.H_kv) * d + t] = L > 0.f ? acc / L : 0.f;  // empty shard: 0
-      if (sd.ml_out && t == 0) {
-        sd.ml_out[(g + m * p.H_kv) * 2 + 0] = M;
-        sd.ml_out[(g + m * p.H_kv) * 2 + 1] = L;
+      hdr[m * 2 + 0] = M;
+      hdr[m * 2 + 1] = L;
+    }
+  }
+  __syncthreads();
+  stamp(trc, 43);
+  for (int oo = tid; oo < nout; oo += blockDim.x) {
+    const int o = o0 + oo, m = o / d, t = o - (o / d) * d;
+    const float* wm = wts + m * chunks;
+    float acc = 0.f;
+    for (int c = 0; c < chunks; ++c) acc = fmaf(wm[c], ov[c * nout + oo], acc);
+    const float L = hdr[m * 2 + 1];
+    sd.out[static_cast<size_t>(g + m * p.H_kv) * d + t] = L > 0.f ? acc / L : 0.f;  // empty shard: 0
+    if (sd.ml_out && t == 0) {
+      sd.ml_out[(g + m * p.H_kv) * 2 + 0] = hdr[m * 2 + 0];
+      sd.ml_out[(g + m * p.H_kv) * 2 + 1] = L;
+    }
+  }
+  __syncthreads();  // buf is the next group's attention staging
+}
+
+// Per-CTA softmax partials m = max_j S, z = sum_j e^(S - m) per head
+// (softmax_rows, tensor.cpp:31-52), S <- e^(S - m) in place: warp per head,
+// float4 rows, four independent SFU chains per lane.
+__device__ __noinline__ void softmax_partials(float* Sbuf, int sstride, int nloc, int H, const int* headmax,
+                                              float* m_out, float* z_out, size_t sh) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n4 = (nloc + 3) >> 2;
+  for (int h = warp; h < H; h += kDecodeWarps) {
+    const float m = ord_float(headmax[h]);
+    const float ml = m * kLog2e;
+    float4* sr = reinterpret_cast<float4*>(Sbuf + static_cast<size_t>(h) * sstride);
+    float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+    if (m > -INFINITY) {
+      // S <- e^(S - m) in place (the soft vote then needs FMAs only)
+      for (int q = lane; q < n4; q += 32) {
+        float4 v = sr[q];
+        v.x = ex2_approx(fmaf(v.x, kLog2e, -ml));
+        v.y = ex2_approx(fmaf(v.y, kLog2e, -ml));
+        v.z = ex2_approx(fmaf(v.z, kLog2e, -ml));
+        v.w = ex2_approx(fmaf(v.w, kLog2e, -ml));
+        sr[q] = v;
+        z0 += v.x;
+        z1 += v.y;
+        z2 += v.z;
+        z3 += v.w;
       }
+    }
+    const float z = warp_sum((z0 + z1) + (z2 + z3));
+    if (lane == 0) {
+      m_out[h * sh] = m;
+      z_out[h * sh] = z;
     }
   }
 }
@@ -1182,6 +1270,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   }
 
   trace_pt(p, 0);
+  unsigned long long* const trc = p.trace ? p.trace + blockIdx.x * kTraceStride : nullptr;
   if (p.debug_flags & 16) return;  // dev timing: launch + prologue only
   // ---- phase 0: append, scan frames, Selection Cache decision(s), hit prep
   if ((p.mode & kModeAppend) && cs == 0 && sd.append_frame >= 0) {
@@ -1316,6 +1405,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     for (int it = 0; it < pre; ++it) mbar_wait(&sm.full[it], 0);  // speculative stages landed
   __syncthreads();
 
+  TSB_STOP_AT(1);
   trace_pt(p, 1);
   // ---- phase 1: scan (Alg. 2)
   float* Sbuf = p.s_in_smem ? sm.S : p.ws_s + static_cast<size_t>(cta) * H * p.tpc;
@@ -1332,7 +1422,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       }
     } else {
       float* so = (p.mode & kModeSOut) ? sd.s_out + j0 : nullptr;
-      if constexpr (FAST) scan_fast<D, G>(p, sd, sm, j0, nloc, Sbuf, sstride, so, pre);
+      if (p.debug_flags & 16384) {  // dev: no K streaming (S = 0), for cache-state experiments
+        for (int i = tid; i < H * sstride; i += blockDim.x) Sbuf[i] = 0.f;
+        for (int h = tid; h < H; h += blockDim.x) sm.headmax[h] = float_ord(0.f);
+      } else if constexpr (FAST) scan_fast<D, G>(p, sd, sm, j0, nloc, Sbuf, sstride, so, pre);
       else scan_generic(p, sd, sm, j0, nloc, Sbuf, sstride, so);
     }
   }
@@ -1353,37 +1446,12 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   if (do_select && own == 1 && p.method == 2 && !shard_sel) {
     const size_t sh = stats_stride(p.ctas_per_seq);
     const size_t so = static_cast<size_t>(seq_id) * H * sh + cs;
-    const int warp = tid >> 5, lane = tid & 31;
-    const int n4 = (nloc + 3) >> 2;
-    for (int h = warp; h < H; h += kDecodeWarps) {
-      const float m = ord_float(sm.headmax[h]);
-      const float ml = m * 1.4426950408889634f;
-      float4* sr = reinterpret_cast<float4*>(Sbuf + static_cast<size_t>(h) * sstride);
-      float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
-      if (m > -INFINITY) {
-        // S <- e^(S - m) in place (the soft vote then needs FMAs only)
-        for (int q = lane; q < n4; q += 32) {
-          float4 v = sr[q];
-          v.x = ex2_approx(fmaf(v.x, 1.4426950408889634f, -ml));
-          v.y = ex2_approx(fmaf(v.y, 1.4426950408889634f, -ml));
-          v.z = ex2_approx(fmaf(v.z, 1.4426950408889634f, -ml));
-          v.w = ex2_approx(fmaf(v.w, 1.4426950408889634f, -ml));
-          sr[q] = v;
-          z0 += v.x;
-          z1 += v.y;
-          z2 += v.z;
-          z3 += v.w;
-        }
-      }
-      const float z = warp_sum((z0 + z1) + (z2 + z3));
-      if (lane == 0) {
-        p.ws_m[so + h * sh] = m;
-        p.ws_z[so + h * sh] = z;
-      }
-    }
+    softmax_partials(Sbuf, sstride, nloc, H, sm.headmax, p.ws_m + so, p.ws_z + so, sh);
   }
+  TSB_STOP_AT(3);
   trace_pt(p, 3);
   if (any_select) gs.sync();  // B1: softmax partials of every CTA visible
+  TSB_STOP_AT(4);
   trace_pt(p, 4);
   if (p.debug_flags & 4) return;  // dev timing: stop after B1
 
@@ -1398,7 +1466,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   }
   if (own == 1 && (p.mode & kModeCache)) {
     // the new cached query (every CTA read the old one before B1)
-    for (int i = cs * blockDim.x + tid; i < width; i += p.ctas_per_seq * blockDim.x) sd.cached_q[i] = sd.q[i];
+    const uint64_t pol = policy_evict_last();
+    for (int i = cs * blockDim.x + tid; i < width; i += p.ctas_per_seq * blockDim.x)
+      st_hint_u32(sd.cached_q + i, __float_as_uint(sd.q[i]), pol);
   }
   if (p.mode & kModeShardStats) {
     // this shard's per-head (m, z) from its CTAs' partials (every CTA
@@ -1485,6 +1555,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       for (int i = tid; i < kRadixBins; i += blockDim.x) sm.hist[i] = 0u;
       __syncthreads();
     }
+    stamp(trc, 32);
     // crit[j] = sum_h softmax_h(S)[j] (select_head_soft_vote, selector.cpp:113-126)
     // = sum_h e^(S - m_c) f_h, or the raw logit sum (select_topk,
     // selector.cpp:89-99); two candidates per thread, keys straight into the
@@ -1522,6 +1593,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     }
     __syncthreads();
   }
+  TSB_STOP_AT(5);
   trace_pt(p, 5);
 
   // ---- phase 4: radix select over 24-bit key prefixes (two 12-bit passes).
@@ -1535,27 +1607,30 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     if (radix_own) hist_merge(sm.hist, gh);
     trace_pt(p, 15);
     gs.sync();  // B2
+    TSB_STOP_AT(6);
     trace_pt(p, 6);
     uint32_t b1 = 0;
     if (radix_own) {
       int b;
       uint32_t above;
       uint32_t cnt;
-      find_bin(gh, kk, sm.scratch, sm.hist, &b, &above, &cnt);
+      find_bin(gh, kk, sm.scratch, sm.hist, &b, &above, &cnt, trc, 33);
       kk -= above;
       b1 = static_cast<uint32_t>(b);
       trace_pt(p, 16);
-      radix_hist(keys, nloc, 8, 20, b1, sm.hist, gh + kHistPass);
+      radix_hist(keys, nloc, 8, 20, b1, sm.hist, gh + kHistPass, trc);
     }
+    TSB_STOP_AT(7);
     trace_pt(p, 17);
     gs.sync();  // B3
+    TSB_STOP_AT(8);
     trace_pt(p, 7);
     if (p.debug_flags & 32) return;  // dev timing: stop after B3
     uint32_t eq_total = 0;
     if (radix_own) {
       int b;
       uint32_t above;
-      find_bin(gh + kHistPass, kk, sm.scratch, sm.hist, &b, &above, &eq_total);
+      find_bin(gh + kHistPass, kk, sm.scratch, sm.hist, &b, &above, &eq_total, trc, 36);
       kk -= above;
       tau = (b1 << 12) | static_cast<uint32_t>(b);
     }
@@ -1593,6 +1668,12 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
 
   trace_pt(p, 19);
   // ---- phase 5: ascending compaction of this CTA's selected candidates
+  // up to two compacted entries per thread stay in registers for the
+  // SelectionResult write after the offsets are known (no read back)
+  const bool pub_regs = nloc <= 2 * static_cast<int>(blockDim.x);
+  uint32_t pub_pos[2] = {0xffffffffu, 0xffffffffu}, pub_tok[2] = {0u, 0u};
+  float pub_crit[2] = {0.f, 0.f};
+  int32_t pub_row[2] = {-1, -1};
   if (do_select && own == 1) {
     uint32_t out_n = 0, eq_seen = 0;
     uint32_t* lt = p.ws_sel_tok + static_cast<size_t>(cta) * p.tpc;
@@ -1616,27 +1697,36 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       uint32_t tot;
       const uint32_t pos = out_n + block_excl_scan(take ? 1u : 0u, sm.scratch, &tot);
       if (take) {
-        lt[pos] = cand_at(sd, j0 + jl) + static_cast<uint32_t>(sd.shard_base);
-        lc[pos] = key_float(key);
-        lr[pos] = may_scan ? sm.frames[jl] : -1;
+        const int32_t row = may_scan ? sm.frames[jl] : -1;
+        const uint32_t tok = cand_at(sd, j0 + jl) + static_cast<uint32_t>(sd.shard_base);
+        const float cr = key_float(key);
+        lt[pos] = tok;
+        lc[pos] = cr;
+        lr[pos] = row;
+        if (pub_regs) {
+          const int u = base == 0 ? 0 : 1;
+          pub_pos[u] = pos;
+          pub_tok[u] = tok;
+          pub_crit[u] = cr;
+          pub_row[u] = row;
+        }
+        if (FAST && (p.mode & kModeAttend) && row >= 0) {
+          // the attention CTAs gather this row after B4: pull it into L2 now
+          const uint32_t rb = static_cast<uint32_t>(p.H_kv * p.d * 2);
+          const uint64_t pol = policy_evict_last();
+          bulk_prefetch_l2(reinterpret_cast<const char*>(p.k_slab) + static_cast<size_t>(row) * rb, rb, pol);
+          bulk_prefetch_l2(reinterpret_cast<const char*>(p.v_slab) + static_cast<size_t>(row) * rb, rb, pol);
+        }
       }
       out_n += tot;
+      stamp(trc, 40);
     }
     if (tid == 0) p.ws_nsel[cta] = out_n;
-    if (FAST && (p.mode & kModeAttend)) {
-      // the attention CTAs gather these rows after B4: pull them into L2 now
-      __syncthreads();
-      const uint32_t rb = static_cast<uint32_t>(p.H_kv * p.d * 2);
-      const uint64_t pol = policy_evict_last();
-      for (uint32_t i = tid; i < 2 * out_n; i += blockDim.x) {
-        const int32_t r = __ldcg(lr + (i >> 1));
-        bulk_prefetch_l2((i & 1 ? reinterpret_cast<const char*>(p.v_slab) : reinterpret_cast<const char*>(p.k_slab)) +
-                             static_cast<size_t>(r) * rb, rb, pol);
-      }
-    }
   }
+  TSB_STOP_AT(9);
   trace_pt(p, 8);
   if (any_select) gs.sync();  // B4: per-CTA selections published
+  TSB_STOP_AT(10);
   trace_pt(p, 9);
 
   // ---- phase 6: selection offsets; the SelectionResult (ascending) out
@@ -1647,6 +1737,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     const uint32_t ex = block_excl_scan(v, sm.scratch, &tot);
     if (tid <= nc) sm.prefix[tid] = static_cast<int>(tid < nc ? ex : tot);
     __syncthreads();
+    stamp(trc, 41);
     const int my0 = sm.prefix[cs], myn = sm.prefix[cs + 1] - my0;
     const uint32_t* lt = p.ws_sel_tok + static_cast<size_t>(cta) * p.tpc;
     const float* lc = p.ws_sel_crit + static_cast<size_t>(cta) * p.tpc;
@@ -1668,25 +1759,36 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     }
     if (tid == 0) sd.shard_cands[2 * p.k] = static_cast<uint32_t>(n);
   }
+  TSB_STOP_AT(11);
   trace_pt(p, 10);
-  // the SelectionResult (ascending) into the cache entry: nobody reads it in
-  // this launch, so it is written off the critical path (after the attention)
-  auto publish_selection = [&]() {
-    if (!(do_select && own == 1)) return;
-    const int my0 = sm.prefix[cs], myn = sm.prefix[cs + 1] - my0;
-    const uint32_t* lt = p.ws_sel_tok + static_cast<size_t>(cta) * p.tpc;
-    const float* lc = p.ws_sel_crit + static_cast<size_t>(cta) * p.tpc;
-    const int32_t* lr = p.ws_sel_row + static_cast<size_t>(cta) * p.tpc;
-    for (int i = tid; i < myn; i += blockDim.x) {
-      sd.sel[my0 + i] = __ldcg(lt + i);
-      sd.sel_crit[my0 + i] = __ldcg(lc + i);
-      if (sd.sel_rows) sd.sel_rows[my0 + i] = __ldcg(lr + i);
+  // the SelectionResult (ascending) into the cache entry, evict_last: the
+  // next launch stages it. Nobody reads it in this launch, so the stores are
+  // fire-and-forget (from registers; read back only for large CTA lists).
+  if (do_select && own == 1) {
+    const int my0 = sm.prefix[cs];
+    const uint64_t pol = policy_evict_last();
+    if (pub_regs) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (pub_pos[u] != 0xffffffffu) {
+          const int i = my0 + static_cast<int>(pub_pos[u]);
+          st_hint_u32(sd.sel + i, pub_tok[u], pol);
+          st_hint_u32(sd.sel_crit + i, __float_as_uint(pub_crit[u]), pol);
+          if (sd.sel_rows) st_hint_u32(sd.sel_rows + i, static_cast<uint32_t>(pub_row[u]), pol);
+        }
+    } else {
+      const int myn = sm.prefix[cs + 1] - my0;
+      const uint32_t* lt = p.ws_sel_tok + static_cast<size_t>(cta) * p.tpc;
+      const float* lc = p.ws_sel_crit + static_cast<size_t>(cta) * p.tpc;
+      const int32_t* lr = p.ws_sel_row + static_cast<size_t>(cta) * p.tpc;
+      for (int i = tid; i < myn; i += blockDim.x) {
+        st_hint_u32(sd.sel + my0 + i, __ldcg(lt + i), pol);
+        st_hint_u32(sd.sel_crit + my0 + i, __float_as_uint(__ldcg(lc + i)), pol);
+        if (sd.sel_rows) st_hint_u32(sd.sel_rows + my0 + i, static_cast<uint32_t>(__ldcg(lr + i)), pol);
+      }
     }
-  };
-  if (!(p.mode & kModeAttend) || (p.debug_flags & 8)) {
-    publish_selection();
-    return;
   }
+  if (!(p.mode & kModeAttend) || (p.debug_flags & 8)) return;
 
   // ---- phase 7: split-K sparse flash-decoding (KV head x row chunk)
   AttView av{};
@@ -1727,6 +1829,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       else
         attend_group<0, 0>(p, sd, av, sm, g, r0, min(r1, av.n_rows), with_cur,
                            parts + static_cast<size_t>(ci) * Gq * stride);
+      TSB_STOP_AT(12);
       trace_pt(p, 11);
       // the group's chunks wait for each other (all co-resident), then each
       // merges its slice of the outputs (no grid barrier)
@@ -1738,12 +1841,12 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
         }
       }
       __syncthreads();
+      TSB_STOP_AT(13);
       trace_pt(p, 28);
-      merge_slice(p, sd, g, parts, split.chunks, ci);
+      merge_slice(p, sd, g, parts, split.chunks, ci, reinterpret_cast<float*>(sm.ring));
       trace_pt(p, 31);
     }
   }
-  publish_selection();
   trace_pt(p, 12);
 }
 

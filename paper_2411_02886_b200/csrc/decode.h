@@ -23,6 +23,7 @@ constexpr int kHistPass = kRadixBins;            // global histogram words per p
 constexpr int kMaxPrefix = 256;                  // >= ctas_per_seq + 1
 constexpr int kAttMaxG = 8;                      // query heads per KV head on the attention path
 constexpr int kAttMaxRows = 256;                 // rows per attention sub-chunk (upper bound)
+constexpr int kTraceStride = 64;                 // phase-trace slots per CTA
 
 TSB_HD inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -66,8 +67,9 @@ TSB_HD inline SmemLayout smem_layout(int H, int row_bytes, int tpc, int s_in_sme
   o += align_up(ring, 128);
   L.s = o;
   if (s_in_smem) o += align_up(static_cast<size_t>(H) * tpc * 4, 128);
-  L.keys = o;
-  if (s_in_smem) o += align_up(static_cast<size_t>(tpc) * 4, 128);
+  // criticality keys overwrite S row 0 in place (each thread writes the keys
+  // of the candidates whose S column it has just read)
+  L.keys = L.s;
   L.frames = o;  // slab row of every candidate of the CTA (TMA producer lookahead)
   o += align_up(static_cast<size_t>(tpc) * 4, 128);
   L.hist = L.ring;  // radix histogram: the ring is idle between the scan and the attention

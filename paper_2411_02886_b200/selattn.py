@@ -329,37 +329,56 @@ class Engine:
 
     TRACE_POINTS = ["start", "decision", "scan", "softmax_partials", "sync1", "crit", "radix1", "radix2",
                     "compact", "sync4", "sel_out", "attend", "merge"]
-    # sub-phase stamps (slots 13..31) of read_trace(all_ctas=True)
+    # sub-phase stamps (slots 13..63, 29 / 30 reserved) of read_trace(all_ctas=True)
     SUB_POINTS = {13: "crit:stats_staged", 14: "crit:f_done", 15: "radix:hist1", 16: "radix:find1",
                   17: "radix:hist2", 18: "radix:find2", 19: "radix:ties", 20: "att:ridx", 21: "att:data",
-                  22: "att:scores", 23: "att:softmax", 24: "att:pv", 25: "att:end", 26: "dec:issued",
-                  27: "dec:done", 28: "merge:all_in", 31: "merge:end"}
+                  22: "att:scores", 23: "att:softmax", 24: "att:pv", 25: "att:end", 27: "dec:done", 28: "merge:all_in", 31: "merge:end", 32: "crit:hist_zeroed",
+                  33: "find1:loaded", 36: "find2:loaded", 38: "hist2:zeroed", 39: "hist2:counted",
+                  40: "compact:iter", 41: "sel_out:prefix", 42: "merge:loaded", 43: "merge:weights",
+                  26: "dec:issued"}
 
     def set_trace(self, enable=True):
         check(lib.ts_engine_set_trace(self._h, 1 if enable else 0))
 
     def read_trace(self, all_ctas=False):
-        """Per-phase device time (us) of the last decode step, from the
-        %globaltimer stamps of CTA 0 (or, with all_ctas, a [ctas x phases]
-        array of stamps in us relative to the earliest CTA start)."""
-        st = np.zeros(32 * 1024, np.uint64)
+        """Per-phase device time (us) of the last decode step from CTA 0's
+        stamps (or, with all_ctas, a [ctas x 32] array of stamps in us
+        relative to the earliest CTA start; NaN where a CTA did not pass).
+
+        Stamps are SM clock64 values; slot 0 / 30 hold %globaltimer (ns) at the
+        start / end (slot 12) and slot 29 the start clock, which align the CTAs
+        and give each CTA's clock rate."""
+        st = np.zeros(64 * 1024, np.uint64)
         check(lib.ts_engine_read_trace(self._h, st.ctypes.data_as(C.c_void_p), st.size))
+        raw = st.reshape(1024, 64).astype(np.int64)
+        raw = raw[: int(np.count_nonzero(raw[:, 0]))]
+        # rebase before going to float64 (ns since the epoch exceed its 2^53 mantissa)
+        gmin, cmin = raw[:, 0].min(), raw[:, 29].min()
+        a = np.where(raw == 0, 0.0, (raw - cmin).astype(np.float64))
+        a[:, 0] = (raw[:, 0] - gmin).astype(np.float64)
+        a[:, 30] = np.where(raw[:, 30] == 0, 0.0, (raw[:, 30] - gmin).astype(np.float64))
+        g0, c0, c_end, g_end = a[:, 0], a[:, 29], a[:, 12], a[:, 30]
+        ok = (g_end > g0) & (c_end > c0)
+        rate = np.where(ok, (c_end - c0) / np.where(ok, g_end - g0, 1.0), np.nan)  # cycles per ns
+        r = np.nanmedian(rate) if np.any(ok) else 1.9
+        ns = g0[:, None] + (a - c0[:, None]) / r
+        ns[:, 0] = g0
+        ns[raw == 0] = np.nan
+        ns[:, 29] = np.nan
+        ns[:, 30] = np.nan
+        us = ns / 1000.0
         if all_ctas:
-            a = st.reshape(1024, 32).astype(np.int64)
-            n = int(np.count_nonzero(a[:, 0]))
-            a = a[:n]
-            t0 = a[:, 0].min()
-            return np.where(a > 0, (a - t0) / 1000.0, np.nan)
-        t = st[: len(self.TRACE_POINTS)].astype(np.int64)
-        out, prev = {}, int(t[0])
-        for name, v in zip(self.TRACE_POINTS[1:], t[1:]):
-            if v:
-                out[name] = (int(v) - prev) / 1000.0
-                prev = int(v)
-        out["total"] = (prev - int(t[0])) / 1000.0
-        for i in range(len(self.TRACE_POINTS), 32):  # optional sub-phase stamps, relative to start
-            if st[i]:
-                out[f"t{i}@"] = (int(st[i]) - int(t[0])) / 1000.0
+            return us
+        t = us[0]
+        out, prev = {}, 0.0
+        for i, name in enumerate(self.TRACE_POINTS[1:], start=1):
+            if not np.isnan(t[i]):
+                out[name] = round(t[i] - prev, 3)
+                prev = t[i]
+        out["total"] = prev
+        for i in range(len(self.TRACE_POINTS), 64):  # optional sub-phase stamps, relative to start
+            if i not in (29, 30) and not np.isnan(t[i]):
+                out[f"t{i}@"] = round(t[i], 3)
         return out
 
     def set_theta(self, theta, seq=0):
