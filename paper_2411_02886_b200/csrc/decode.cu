@@ -628,8 +628,10 @@ __device__ void attend_group_mma(const DecodeParams& p, const SeqDesc& sd, const
   o += static_cast<size_t>(2) * D * 4;
   float* red = reinterpret_cast<float*>(base + o);            // [RGP][8][D]
   o += align_up(static_cast<size_t>(RGP) * 8 * D * 4, 128);
-  float* stat = reinterpret_cast<float*>(base + o);           // [8][4] m_run, l_run, corr
-  o += 128;
+  float* stat = reinterpret_cast<float*>(base + o);           // [8][4] m_run, l_run
+  int* hmax = reinterpret_cast<int*>(stat + 32);              // [2][8] sub-chunk score max (ordered ints)
+  float* lpart = stat + 48;                                   // [kAttMaxRows / 16][8] row-slice sums of P
+  o += align_up(static_cast<size_t>(48 + kAttMaxRows / 16 * 8) * 4, 128);
   int32_t* ridx = reinterpret_cast<int32_t*>(base + o);       // [kAttIdx] slab rows
   o += static_cast<size_t>(kAttIdx) * 4;
   uint2* qf = reinterpret_cast<uint2*>(base + o);             // [KC][3][32] B fragments of q (hi/mid/lo)
@@ -670,6 +672,7 @@ __device__ void attend_group_mma(const DecodeParams& p, const SeqDesc& sd, const
     stat[tid * 4 + 0] = -INFINITY;
     stat[tid * 4 + 1] = 0.f;
     stat[tid * 4 + 2] = 1.f;
+    hmax[tid] = hmax[8 + tid] = float_ord(-INFINITY);
   }
   // P.V accumulators: warp (d tile dt, row group rgp)
   const int dt = warp % DT, rgp = warp / DT;
@@ -752,11 +755,26 @@ __device__ void attend_group_mma(const DecodeParams& p, const SeqDesc& sd, const
         float cacc[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) cacc[e] = ch[e] + (cm[e] + cl[e]);
+        float tmax[2] = {-INFINITY, -INFINITY};  // this lane's two heads over its two rows
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int row = mt * 16 + (lane >> 2) + (e >> 1) * 8;
           const int col = (lane & 3) * 2 + (e & 1);
-          if (row < nr) probs[row * 8 + col] = col < G ? cacc[e] * p.attn_scale : -INFINITY;
+          const float sc = cacc[e] * p.attn_scale;
+          if (row < nr) {
+            probs[row * 8 + col] = sc;
+            if (col < G) tmax[e & 1] = fmaxf(tmax[e & 1], sc);
+          }
+        }
+        // the tile's max per head (lanes with equal lane % 4 share the heads)
+#pragma unroll
+        for (int o2 = 4; o2 < 32; o2 <<= 1) {
+          tmax[0] = fmaxf(tmax[0], __shfl_xor_sync(0xffffffffu, tmax[0], o2));
+          tmax[1] = fmaxf(tmax[1], __shfl_xor_sync(0xffffffffu, tmax[1], o2));
+        }
+        if (lane < 4) {
+          if (2 * lane < G) atomicMax(&hmax[(sub & 1) * 8 + 2 * lane], float_ord(tmax[0]));
+          if (2 * lane + 1 < G) atomicMax(&hmax[(sub & 1) * 8 + 2 * lane + 1], float_ord(tmax[1]));
         }
       }
       if (cur_here && warp == nwarps - 1) {
@@ -764,64 +782,58 @@ __device__ void attend_group_mma(const DecodeParams& p, const SeqDesc& sd, const
         for (int m = 0; m < G; ++m) {
           float a = 0.f;
           for (int t = lane; t < D; t += 32) a = fmaf(qs[m * D + t], ck[t], a);
-          a = warp_sum(a);
-          if (lane == 0) probs[cap * 8 + m] = a * p.attn_scale;  // slot past the tiles
+          a = warp_sum(a) * p.attn_scale;
+          if (lane == 0) {
+            probs[cap * 8 + m] = a;  // slot past the tiles
+            atomicMax(&hmax[(sub & 1) * 8 + m], float_ord(a));
+          }
         }
       }
       __syncthreads();
       if (sub == 0) trace_pt(p, 22);
-      // ---- online softmax per head (warp m owns head m); rows >= nr get P = 0
-      for (int m = warp; m < 8; m += nwarps) {
-        if (m >= G) {
-          for (int r = lane; r < nr16; r += 32) probs[r * 8 + m] = 0.f;
-          continue;
-        }
-        float mx = -INFINITY;
-        for (int r = lane; r < nr; r += 32) mx = fmaxf(mx, probs[r * 8 + m]);
-        if (cur_here && lane == 0) mx = fmaxf(mx, probs[cap * 8 + m]);
-        mx = warp_max(mx);
-        const float m_old = stat[m * 4 + 0];
-        const float m_new = fmaxf(m_old, mx);
-        float l = 0.f;
-        for (int r = lane; r < nr16; r += 32) {
-          const float w = (r < nr && m_new > -INFINITY) ? expf(probs[r * 8 + m] - m_new) : 0.f;
-          probs[r * 8 + m] = w;
-          l += w;
-        }
-        if (cur_here && lane == 0) {
-          const float w = expf(probs[cap * 8 + m] - m_new);
-          probs[cap * 8 + m] = w;
-          l += w;
-        }
-        l = warp_sum(l);
-        if (lane == 0) {
-          const float corr = m_old == -INFINITY ? 0.f : expf(m_old - m_new);
-          stat[m * 4 + 0] = m_new;
-          stat[m * 4 + 1] = stat[m * 4 + 1] * corr + l;
-          stat[m * 4 + 2] = corr;
-        }
-      }
-      __syncthreads();
-      // P^T as the P.V MMA's B operand (three exact bf16 parts), built once
+      // ---- online softmax fused into the P^T build (P.V's B operand, three
+      // exact bf16 parts): P = e^(s - m_new) with m_new = max(m_run, this
+      // sub-chunk's max); rows >= nr and heads >= G get P = 0. Row-slice sums
+      // go to lpart (summed in a fixed order below: deterministic).
       const int nk = nr16 / 16;
       if (tid < nk * 32) {
         const int ks = tid >> 5, l = tid & 31;
         const int n = l >> 2, k0 = ks * 16 + (l & 3) * 2;
+        const float m_new = fmaxf(stat[n * 4 + 0], ord_float(hmax[(sub & 1) * 8 + n]));
+        const bool live = n < G && m_new > -INFINITY;
+        float w[4];
+        const int rr[4] = {k0, k0 + 1, k0 + 8, k0 + 9};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          w[e] = (live && rr[e] < nr) ? ex2_approx((probs[rr[e] * 8 + n] - m_new) * kLog2e) : 0.f;
         float h[4], m[4], lo[4];
-        split3(probs[k0 * 8 + n], h[0], m[0], lo[0]);
-        split3(probs[(k0 + 1) * 8 + n], h[1], m[1], lo[1]);
-        split3(probs[(k0 + 8) * 8 + n], h[2], m[2], lo[2]);
-        split3(probs[(k0 + 9) * 8 + n], h[3], m[3], lo[3]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) split3(w[e], h[e], m[e], lo[e]);
         pf[(ks * 3 + 0) * 32 + l] = make_uint2(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]));
         pf[(ks * 3 + 1) * 32 + l] = make_uint2(pack_bf16x2(m[0], m[1]), pack_bf16x2(m[2], m[3]));
         pf[(ks * 3 + 2) * 32 + l] = make_uint2(pack_bf16x2(lo[0], lo[1]), pack_bf16x2(lo[2], lo[3]));
+        float ls = (w[0] + w[1]) + (w[2] + w[3]);
+        ls += __shfl_xor_sync(0xffffffffu, ls, 1);
+        ls += __shfl_xor_sync(0xffffffffu, ls, 2);
+        if ((l & 3) == 0) lpart[ks * 8 + n] = ls;
+      }
+      if (tid < 8) hmax[((sub + 1) & 1) * 8 + tid] = float_ord(-INFINITY);  // the next sub-chunk's
+      if (cur_here && tid >= 32 * 16 && tid < 32 * 16 + G) {
+        const int m = tid - 32 * 16;
+        const float m_new = fmaxf(stat[m * 4 + 0], ord_float(hmax[(sub & 1) * 8 + m]));
+        probs[cap * 8 + m] = ex2_approx((probs[cap * 8 + m] - m_new) * kLog2e);
       }
       __syncthreads();
       if (sub == 0) trace_pt(p, 23);
       // ---- P.V on tensor cores
       if (pv_warp) {
         const int n0 = (lane & 3) * 2;
-        const float c0f = stat[n0 * 4 + 2], c1f = stat[(n0 + 1) * 4 + 2];
+        // rescale by e^(m_run - m_new) (0 while m_run = -inf)
+        const float mo0 = stat[n0 * 4 + 0], mo1 = stat[(n0 + 1) * 4 + 0];
+        const float mn0 = fmaxf(mo0, ord_float(hmax[(sub & 1) * 8 + n0]));
+        const float mn1 = fmaxf(mo1, ord_float(hmax[(sub & 1) * 8 + n0 + 1]));
+        const float c0f = mo0 == -INFINITY ? 0.f : ex2_approx((mo0 - mn0) * kLog2e);
+        const float c1f = mo1 == -INFINITY ? 0.f : ex2_approx((mo1 - mn1) * kLog2e);
         acc[0] *= c0f;
         acc[1] *= c1f;
         acc[2] *= c0f;
@@ -850,6 +862,16 @@ __device__ void attend_group_mma(const DecodeParams& p, const SeqDesc& sd, const
         }
       }
       __syncthreads();  // buffer and probs free for the next sub-chunk
+      if (tid < G) {
+        // running (m, l) of head tid; read by the next sub-chunk after its first barrier
+        const float mo = stat[tid * 4 + 0];
+        const float mn = fmaxf(mo, ord_float(hmax[(sub & 1) * 8 + tid]));
+        float ls = cur_here ? probs[cap * 8 + tid] : 0.f;
+        for (int ks = 0; ks < nk; ++ks) ls += lpart[ks * 8 + tid];
+        const float corr = mo == -INFINITY ? 0.f : ex2_approx((mo - mn) * kLog2e);
+        stat[tid * 4 + 0] = mn;
+        stat[tid * 4 + 1] = stat[tid * 4 + 1] * corr + ls;
+      }
       if (sub == 0) trace_pt(p, 24);
     }
     w0 += nw;
@@ -1853,9 +1875,16 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     const int stride = att_stride(p.d);
     for (int g = gi; g < p.H_kv; g += split.groups) {
       float* parts = p.ws_att + (static_cast<size_t>(seq_id) * p.H_kv + g) * split.chunks * Gq * stride;
-      if constexpr (FAST)
+      if constexpr (FAST) {
+        if (p.debug_flags & 4096) {  // dev: run the attention twice (warm instruction cache timing)
+          attend_group_mma<D>(p, sd, av, sm, g, r0, min(r1, av.n_rows), with_cur,
+                              parts + static_cast<size_t>(ci) * Gq * stride);
+          __syncthreads();
+          stamp(trc, 44);
+        }
         attend_group_mma<D>(p, sd, av, sm, g, r0, min(r1, av.n_rows), with_cur,
                             parts + static_cast<size_t>(ci) * Gq * stride);
+      }
       else
         attend_group<0, 0>(p, sd, av, sm, g, r0, min(r1, av.n_rows), with_cur,
                            parts + static_cast<size_t>(ci) * Gq * stride);
