@@ -500,7 +500,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     workload = args.workload or ("sharded" if world > 1 else "decode")
-    config = {"workload": WORKLOADS[workload], "num_heads": H, "num_kv_heads": H_KV, "head_dim": D, "k": K_SEL,
+    shapes = (28, 4, 128) if workload == "batched" else (H, H_KV, D)  # configs[2] is Qwen2-7B
+    config = {"workload": WORKLOADS[workload], "num_heads": shapes[0], "num_kv_heads": shapes[1], "head_dim": shapes[2],
+              "k": K_SEL,
               "n_init": N_INIT, "n_local": N_LOCAL, "theta": THETA,
               "stream": f"rotating, consecutive cos {SIMILARITY}",
               "parallelism": f"KV-sequence shards x{world}" if workload == "sharded" else "single GPU",

@@ -39,6 +39,7 @@ int g_prefetch_stages = [] {
 const bool g_force_global_s = std::getenv("TS_FORCE_GLOBAL_S") != nullptr && std::getenv("TS_FORCE_GLOBAL_S")[0];
 const int g_debug_flags = std::getenv("TS_DEBUG_FLAGS") ? std::atoi(std::getenv("TS_DEBUG_FLAGS")) : 0;
 const bool g_force_cuda_core_prefill = std::getenv("TS_CUDA_CORE_PREFILL") != nullptr;
+const bool g_no_lean = std::getenv("TS_NO_LEAN") != nullptr;  // dev: always the general kernel
 std::atomic<uint64_t> g_launches{0};
 constexpr size_t kTraceSlots = tsb::kTraceStride * 1024;
 // host-side profile of the decode launch path (TS_HOST_PROF=1): ns per stage
@@ -186,6 +187,7 @@ struct Plan {
   int ctas_per_seq, tpc, s_in_smem, ring_bytes, att_bytes;
   size_t smem;
   const void* fn;
+  const void* fn_lean;  // the single-sequence decode-step specialisation (nullptr: none)
 };
 
 Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows, bool attend = true,
@@ -193,8 +195,9 @@ Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows, bool 
   const DeviceInfo& di = device_info();
   Plan pl{};
   const tsb::ScanGeom g = tsb::scan_geom(H, H_kv, d);
-  pl.fn = tsb::decode_kernel_ptr(d, H / H_kv, g.fast != 0);
-  if (!pl.fn) pl.fn = tsb::decode_kernel_ptr(0, 0, false);
+  pl.fn = tsb::decode_kernel_ptr(d, H / H_kv, g.fast != 0, false);
+  pl.fn_lean = pl.fn ? tsb::decode_kernel_ptr(d, H / H_kv, g.fast != 0, true) : nullptr;
+  if (!pl.fn) pl.fn = tsb::decode_kernel_ptr(0, 0, false, false);
   const int base = std::max(max_T, att_rows);
   int c = (base + 63) / 64;
   c = std::max(1, std::min(c, std::max(1, di.num_sms / n_seq)));
@@ -246,19 +249,26 @@ void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t 
   p.ring_bytes = pl.ring_bytes;
   p.att_bytes = pl.att_bytes;
   p.debug_flags = g_debug_flags;
+  // the engine's plain single-sequence step runs the specialisation with the
+  // other modes compiled out (decode.cu, LEAN)
+  const tsb::SeqDesc& s0 = p.seqs[0];
+  const bool lean = pl.fn_lean && !g_no_lean && p.n_seq == 1 && pl.s_in_smem && p.method == 2 &&
+                    p.mode == (tsb::kModeSelect | tsb::kModeScore | tsb::kModeCache | tsb::kModeAttend | tsb::kModeAppend) &&
+                    !s0.att_list && !s0.no_cur && s0.shard_base == 0 && !s0.cand && s0.sel_rows;
+  const void* fn = lean ? pl.fn_lean : pl.fn;
   // the dynamic shared-memory limit is set once per kernel (largest request so far)
   static std::mutex mu;
   static std::unordered_map<const void*, size_t> smem_set;
   std::lock_guard<std::mutex> lock(mu);
-  size_t& have = smem_set[pl.fn];
+  size_t& have = smem_set[fn];
   if (pl.smem > have) {
-    ck(cudaFuncSetAttribute(pl.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)),
+    ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)),
        "cudaFuncSetAttribute");
     have = pl.smem;
   }
   void* args[] = {&p};
   const double t0 = g_host_prof ? now_ns() : 0.0;
-  ck(cudaLaunchCooperativeKernel(pl.fn, dim3(n_ctas), dim3(tsb::kDecodeThreads), args, pl.smem, st),
+  ck(cudaLaunchCooperativeKernel(fn, dim3(n_ctas), dim3(tsb::kDecodeThreads), args, pl.smem, st),
      "decode kernel launch");
   if (g_host_prof) g_prof[3] += now_ns() - t0;
   ws.launches += 1;

@@ -292,6 +292,7 @@ __device__ int cache_decision(const SeqDesc& sd, int width, const DecisionLoads&
 
 // --------------------------------------------------------------- the scan
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kLeanMode = kModeSelect | kModeScore | kModeCache | kModeAttend | kModeAppend;
 // Fast path (sm_100a tensor cores, mma.sync bf16 -> fp32). The K rows of a
 // stage (16 tokens, padded stride so ldmatrix is bank-conflict free) are the
 // M x K operand; the query, exactly split into three bf16 parts
@@ -1273,20 +1274,29 @@ __device__ __noinline__ void softmax_partials(float* Sbuf, int sstride, int nloc
   }
 }
 
-template <int D, int G, bool FAST>
+// LEAN: the engine's single-sequence decode step (mode kLeanMode, soft vote,
+// S on chip, no shard / explicit-list / S-in options). Those settings fold to
+// constants, so the instantiation carries no code for the other modes: the
+// one-shot phases run from a cold instruction cache, and their code size and
+// branch count are their latency.
+template <int D, int G, bool FAST, bool LEAN>
 __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Smem sm = carve(smem_raw, p);
   const int cta = blockIdx.x;
   const int nblocks = gridDim.x;
-  const int seq_id = cta / p.ctas_per_seq;
+  const int pmode = LEAN ? kLeanMode : p.mode;
+  const int n_seq = LEAN ? 1 : p.n_seq;
+  const int s_in_smem = LEAN ? 1 : p.s_in_smem;
+  const int method = LEAN ? 2 : p.method;
+  const int seq_id = LEAN ? 0 : cta / p.ctas_per_seq;
   const int cs = cta - seq_id * p.ctas_per_seq;
   const int c0 = seq_id * p.ctas_per_seq;
   const SeqDesc sd = p.seqs[seq_id];
   const int H = p.H;
   const int width = H * p.d;
   const int tid = threadIdx.x;
-  const bool do_select = (p.mode & kModeSelect) != 0;
+  const bool do_select = (pmode & kModeSelect) != 0;
 
   if (FAST && tid < kMaxStages) {
     mbar_init(&sm.full[tid], 1);
@@ -1311,7 +1321,12 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   unsigned long long* const trc = p.trace ? p.trace + blockIdx.x * kTraceStride : nullptr;
   if (p.debug_flags & 16) return;  // dev timing: launch + prologue only
   // ---- phase 0: append, scan frames, Selection Cache decision(s), hit prep
-  if ((p.mode & kModeAppend) && cs == 0 && sd.append_frame >= 0) {
+  // the decision's loads first: they head the critical path
+  DecisionLoads dl{};
+  const bool dec_early = sd.select && !(pmode & kModeShardSelect) && (pmode & kModeCache);
+  if (dec_early) decision_issue(sd, width, dl);
+  stamp(trc, 45);
+  if ((pmode & kModeAppend) && cs == 0 && sd.append_frame >= 0) {
     const int row = p.H_kv * p.d;
     const size_t off = (static_cast<size_t>(sd.append_frame) * p.page_size + sd.append_slot) * row;
     for (int i = tid; i < row; i += blockDim.x) {
@@ -1323,17 +1338,31 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   const int T = sd.n_cand;
   const int j0 = min(T, cs * p.tpc);
   const int nloc = max(0, min(T, j0 + p.tpc) - j0);
-  const bool may_scan = sd.select && (p.mode & kModeScore) && !(p.mode & kModeSIn);
+  const bool may_scan = sd.select && (pmode & kModeScore) && !(pmode & kModeSIn);
   // slab rows of the scan candidates: issue the (page-table) loads now, store
-  // after the decision so their latency overlaps it
+  // after the decision so their latency overlaps it. Long CTA ranges
+  // (batched / sharded contexts) load each page entry once instead (parked in
+  // sm.prefix, idle until phase 6): per-token loads would be a chain of
+  // round trips.
   int32_t fr_pre[4];
+  const int psh = (p.page_size & (p.page_size - 1)) == 0 ? __ffs(p.page_size) - 1 : -1;
+  const int pg0 = psh >= 0 ? (sd.cand_begin + j0) >> psh : 0;
+  const int npg = (may_scan && nloc > 4 * static_cast<int>(blockDim.x) && psh >= 0 && !sd.cand)
+                      ? ((sd.cand_begin + j0 + nloc - 1) >> psh) - pg0 + 1 : 0;
+  const bool by_page = npg > 0 && npg <= kMaxPrefix;
+  int32_t pg_pre = 0;
+  if (by_page) {
+    if (tid < npg) pg_pre = __ldcg(sd.page_table + pg0 + tid);
+  } else {
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int jl = tid + u * blockDim.x;
-    fr_pre[u] = (may_scan && jl < nloc) ? static_cast<int32_t>(row_index(sd, cand_at(sd, j0 + jl), p.page_size)) : 0;
+    for (int u = 0; u < 4; ++u) {
+      const int jl = tid + u * blockDim.x;
+      fr_pre[u] = (may_scan && jl < nloc) ? static_cast<int32_t>(row_index(sd, cand_at(sd, j0 + jl), p.page_size)) : 0;
+    }
   }
+  stamp(trc, 46);
   // hit prep: the cached selection (counted below init_end / local_begin after the decision)
-  const bool hit_prep = !sd.att_list && sd.select && (p.mode & kModeCache) && (p.mode & kModeAttend);
+  const bool hit_prep = (LEAN || !sd.att_list) && sd.select && (pmode & kModeCache) && (pmode & kModeAttend);
   const uint32_t ie = static_cast<uint32_t>(sd.init_end);
   const uint32_t lbs = static_cast<uint32_t>(max(sd.local_begin, sd.init_end));
   uint32_t selv[4];
@@ -1347,6 +1376,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       selv[u] = i < p.k ? __ldcg(sd.sel + i) : 0xffffffffu;
     }
   }
+  stamp(trc, 47);
   // Speculative scan start: the TMA producer issues the first ring stages of
   // the K scan before the Selection Cache decision is known. On a miss the
   // scan starts a decision-time earlier; on a hit the (few) stages are
@@ -1354,7 +1384,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   int pre = 0;
   if constexpr (FAST) {
     const ScanGeom geom = scan_geom(p.H, p.H_kv, D, p.ring_bytes);
-    if ((p.debug_flags & 64) && may_scan && (p.mode & kModeCache))  // experimental (measured: no gain)
+    if ((p.debug_flags & 64) && may_scan && (pmode & kModeCache))  // experimental (measured: no gain)
       pre = min(min((nloc + geom.rows - 1) / geom.rows, geom.stages), 4);
     if (pre > 0 && tid < 32) {
       const int row_bytes = p.H_kv * D * 2, rstride = row_bytes + 16;
@@ -1386,13 +1416,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   double* scratch_d = reinterpret_cast<double*>(sm.scratch);  // the ring may be filling (speculative scan)
   int own = 0;  // 0 no selection, 1 miss (select), 2 hit, 3 zero query
   double own_cos = NAN;
-  const bool shard_sel = (p.mode & kModeShardSelect) != 0;
+  const bool shard_sel = (pmode & kModeShardSelect) != 0;
   if (sd.select && shard_sel) {
     own = __ldcg(&sd.cache->last_hit) == 1 ? 2 : 1;  // decided by the kModeShardStats launch
   } else if (sd.select) {
-    if (p.mode & kModeCache) {
-      DecisionLoads dl;
-      decision_issue(sd, width, dl);
+    if (pmode & kModeCache) {
       trace_pt(p, 26);
       const int dec = cache_decision(sd, width, dl, scratch_d, &own_cos);
       own = dec == 1 ? 1 : dec == 0 ? 2 : 3;
@@ -1418,22 +1446,32 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       }
   }
   int any_select = 0, any_radix = 0;
-  if (p.n_seq == 1) {
+  if (n_seq == 1) {
     any_select = own == 1;
     any_radix = do_select && own == 1 && T > p.k;
   } else {
-    for (int b = 0; b < p.n_seq; ++b) {
+    for (int b = 0; b < n_seq; ++b) {
       any_select |= p.seqs[b].select;
       any_radix |= do_select && p.seqs[b].select && p.seqs[b].n_cand > p.k;
     }
   }
+  if (by_page) {
+    if (tid < npg) sm.prefix[tid] = pg_pre;
+    __syncthreads();
+    const int pm = p.page_size - 1;
+    for (int jl = tid; jl < nloc; jl += blockDim.x) {
+      const int tok = sd.cand_begin + j0 + jl;
+      sm.frames[jl] = (sm.prefix[(tok >> psh) - pg0] << psh) | (tok & pm);
+    }
+  } else {
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int jl = tid + u * blockDim.x;
-    if (may_scan && jl < nloc) sm.frames[jl] = fr_pre[u];
+    for (int u = 0; u < 4; ++u) {
+      const int jl = tid + u * blockDim.x;
+      if (may_scan && jl < nloc) sm.frames[jl] = fr_pre[u];
+    }
+    for (int jl = tid + 4 * blockDim.x; may_scan && jl < nloc; jl += blockDim.x)
+      sm.frames[jl] = static_cast<int32_t>(row_index(sd, cand_at(sd, j0 + jl), p.page_size));
   }
-  for (int jl = tid + 4 * blockDim.x; may_scan && jl < nloc; jl += blockDim.x)
-    sm.frames[jl] = static_cast<int32_t>(row_index(sd, cand_at(sd, j0 + jl), p.page_size));
   if (do_select && own == 1 && T > p.k) {
     uint32_t* gh = p.ws_hist + static_cast<size_t>(seq_id) * 2 * kHistPass;
     for (int i = cs * blockDim.x + tid; i < 2 * kHistPass; i += p.ctas_per_seq * blockDim.x) gh[i] = 0u;
@@ -1446,12 +1484,12 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   TSB_STOP_AT(1);
   trace_pt(p, 1);
   // ---- phase 1: scan (Alg. 2)
-  float* Sbuf = p.s_in_smem ? sm.S : p.ws_s + static_cast<size_t>(cta) * H * p.tpc;
-  uint32_t* keys = p.s_in_smem ? sm.keys : p.ws_keys + static_cast<size_t>(cta) * p.tpc;
+  float* Sbuf = s_in_smem ? sm.S : p.ws_s + static_cast<size_t>(cta) * H * p.tpc;
+  uint32_t* keys = s_in_smem ? sm.keys : p.ws_keys + static_cast<size_t>(cta) * p.tpc;
   const int sstride = p.tpc;
-  const bool scanning = (own == 1) && ((p.mode & (kModeScore | kModeSIn)) != 0);
+  const bool scanning = (own == 1) && ((pmode & (kModeScore | kModeSIn)) != 0);
   if (scanning) {
-    if (p.mode & kModeSIn) {
+    if (pmode & kModeSIn) {
       for (int idx = tid; idx < H * nloc; idx += blockDim.x) {
         const int h = idx / nloc, jl = idx - (idx / nloc) * nloc;
         const float s = sd.s_in[static_cast<size_t>(h) * T + j0 + jl];
@@ -1459,7 +1497,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
         atomicMax(&sm.headmax[h], float_ord(s));
       }
     } else {
-      float* so = (p.mode & kModeSOut) ? sd.s_out + j0 : nullptr;
+      float* so = (pmode & kModeSOut) ? sd.s_out + j0 : nullptr;
       if (p.debug_flags & 16384) {  // dev: no K streaming (S = 0), for cache-state experiments
         for (int i = tid; i < H * sstride; i += blockDim.x) Sbuf[i] = 0.f;
         for (int h = tid; h < H; h += blockDim.x) sm.headmax[h] = float_ord(0.f);
@@ -1481,7 +1519,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   // ---- phase 2: per-CTA softmax partials m = max_j S, z = sum_j e^(S - m) per
   // head (softmax_rows, tensor.cpp:31-52): warp per head, float4 rows, four
   // independent SFU chains per lane
-  if (do_select && own == 1 && p.method == 2 && !shard_sel) {
+  if (do_select && own == 1 && method == 2 && !shard_sel) {
     const size_t sh = stats_stride(p.ctas_per_seq);
     const size_t so = static_cast<size_t>(seq_id) * H * sh + cs;
     softmax_partials(Sbuf, sstride, nloc, H, sm.headmax, p.ws_m + so, p.ws_z + so, sh);
@@ -1494,7 +1532,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   if (p.debug_flags & 4) return;  // dev timing: stop after B1
 
   // ---- phase 3: criticality (soft vote / raw sum) + cache bookkeeping
-  if (cs == 0 && tid == 0 && (p.mode & kModeCache) && (own == 1 || own == 2)) {
+  if (cs == 0 && tid == 0 && (pmode & kModeCache) && (own == 1 || own == 2)) {
     CacheState* c = sd.cache;
     c->lookups += 1;
     if (own == 2) c->hits += 1;
@@ -1502,16 +1540,16 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     c->last_hit = own == 2 ? 1 : 0;
     c->last_cos = own_cos;
   }
-  if (own == 1 && (p.mode & kModeCache)) {
+  if (own == 1 && (pmode & kModeCache)) {
     // the new cached query (every CTA read the old one before B1)
     const uint64_t pol = policy_evict_last();
     for (int i = cs * blockDim.x + tid; i < width; i += p.ctas_per_seq * blockDim.x)
       st_hint_u32(sd.cached_q + i, __float_as_uint(sd.q[i]), pol);
   }
-  if (p.mode & kModeShardStats) {
+  if (pmode & kModeShardStats) {
     // this shard's per-head (m, z) from its CTAs' partials (every CTA
     // finished phase 2 at B1); S = e^(S - m_c) stays in the spill buffer
-    if (own == 1 && cs == 0 && p.method == 2) {
+    if (own == 1 && cs == 0 && method == 2) {
       const size_t sh = stats_stride(p.ctas_per_seq);
       for (int h = tid; h < H; h += blockDim.x) {
         const float* mr = p.ws_m + (static_cast<size_t>(seq_id) * H + h) * sh;
@@ -1535,7 +1573,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   const bool radix_own = do_select && own == 1 && T > p.k;
   if (do_select && own == 1) {
     float* ml = sm.f;                                   // [H] f_h = e^(m_c - M_h) / Z_h
-    if (p.method == 2 && shard_sel) {
+    if (method == 2 && shard_sel) {
       // global softmax stats from every shard's (m, z) (rank order); m_c of
       // this CTA from its partial of the stats launch
       const size_t sh = stats_stride(p.ctas_per_seq);
@@ -1553,7 +1591,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
         ml[h] = mc > -INFINITY ? fast_exp(mc - M) / Z : 0.f;
       }
       __syncthreads();
-    } else if (p.method == 2) {
+    } else if (method == 2) {
       float* pm = reinterpret_cast<float*>(sm.ring);
       const int nc = p.ctas_per_seq;
       const int ncp = stats_stride(nc);
@@ -1605,7 +1643,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     // selector.cpp:89-99); two candidates per thread, keys straight into the
     // pass-1 histogram
     const int n2 = (nloc + 1) >> 1;
-    const bool soft = p.method == 2;
+    const bool soft = method == 2;
     for (int base = 0; base < n2; base += blockDim.x) {
       const int q = base + tid;
       float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
@@ -1682,7 +1720,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     // ties straddling the budget: the taken ones are the lowest positions,
     // which needs every CTA's tie count (one more exchange)
     int need_tie = 0;
-    if (p.n_seq == 1) need_tie = radix_own && eq_total > kk;
+    if (n_seq == 1) need_tie = radix_own && eq_total > kk;
     else need_tie = 1;
     if (need_tie) {
       if (radix_own) {
@@ -1742,7 +1780,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       const uint32_t pos = out_n + block_excl_scan(take ? 1u : 0u, sm.scratch, &tot);
       if (take) {
         const int32_t row = may_scan ? sm.frames[jl] : -1;
-        const uint32_t tok = cand_at(sd, j0 + jl) + static_cast<uint32_t>(sd.shard_base);
+        const uint32_t tok = cand_at(sd, j0 + jl) + (LEAN ? 0u : static_cast<uint32_t>(sd.shard_base));
         const float cr = key_float(key);
         lt[pos] = tok;
         lc[pos] = cr;
@@ -1754,7 +1792,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
           pub_crit[u] = cr;
           pub_row[u] = row;
         }
-        if (FAST && (p.mode & kModeAttend) && row >= 0) {
+        if (FAST && (pmode & kModeAttend) && row >= 0) {
           // the attention CTAs gather this row after B4: pull it into L2 now
           const uint32_t rb = static_cast<uint32_t>(p.H_kv * p.d * 2);
           const uint64_t pol = policy_evict_last();
@@ -1832,11 +1870,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       }
     }
   }
-  if (!(p.mode & kModeAttend) || (p.debug_flags & 8)) return;
+  if (!(pmode & kModeAttend) || (p.debug_flags & 8)) return;
 
   // ---- phase 7: split-K sparse flash-decoding (KV head x row chunk)
   AttView av{};
-  if (sd.att_list) {
+  if (!LEAN && sd.att_list) {
     av.n_rows = sd.n_att_dev ? __ldcg(sd.n_att_dev) : sd.n_att;
   } else {
     av.init_end = sd.init_end;
@@ -1866,11 +1904,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   const AttSplit split = att_split(p.H_kv, p.ctas_per_seq);
   const int gi = cs % split.groups, ci = cs / split.groups;
   if (ci < split.chunks) {
-    const int total_rows = av.n_rows + (sd.no_cur ? 0 : 1);  // + current token
+    const int total_rows = av.n_rows + ((!LEAN && sd.no_cur) ? 0 : 1);  // + current token
     const int per = max(1, (total_rows + split.chunks - 1) / split.chunks);
     const int r0 = min(total_rows, ci * per);
     const int r1 = min(total_rows, r0 + per);
-    const bool with_cur = !sd.no_cur && (r0 < r1) && (r1 == total_rows);
+    const bool with_cur = !(!LEAN && sd.no_cur) && (r0 < r1) && (r1 == total_rows);
     const int Gq = p.H / p.H_kv;
     const int stride = att_stride(p.d);
     for (int g = gi; g < p.H_kv; g += split.groups) {
@@ -1917,28 +1955,32 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
 
 }  // namespace
 
-const void* decode_kernel_ptr(int D, int G, bool fast) {
+const void* decode_kernel_ptr(int D, int G, bool fast, bool lean) {
+#define TSB_K(d, g) \
+  return lean ? reinterpret_cast<const void*>(&decode_kernel<d, g, true, true>) \
+              : reinterpret_cast<const void*>(&decode_kernel<d, g, true, false>)
   if (fast) {
     if (D == 128) {
       switch (G) {
-        case 1: return reinterpret_cast<const void*>(&decode_kernel<128, 1, true>);
-        case 2: return reinterpret_cast<const void*>(&decode_kernel<128, 2, true>);
-        case 4: return reinterpret_cast<const void*>(&decode_kernel<128, 4, true>);
-        case 7: return reinterpret_cast<const void*>(&decode_kernel<128, 7, true>);
-        case 8: return reinterpret_cast<const void*>(&decode_kernel<128, 8, true>);
+        case 1: TSB_K(128, 1);
+        case 2: TSB_K(128, 2);
+        case 4: TSB_K(128, 4);
+        case 7: TSB_K(128, 7);
+        case 8: TSB_K(128, 8);
       }
     }
     if (D == 64) {
       switch (G) {
-        case 1: return reinterpret_cast<const void*>(&decode_kernel<64, 1, true>);
-        case 2: return reinterpret_cast<const void*>(&decode_kernel<64, 2, true>);
-        case 4: return reinterpret_cast<const void*>(&decode_kernel<64, 4, true>);
-        case 8: return reinterpret_cast<const void*>(&decode_kernel<64, 8, true>);
+        case 1: TSB_K(64, 1);
+        case 2: TSB_K(64, 2);
+        case 4: TSB_K(64, 4);
+        case 8: TSB_K(64, 8);
       }
     }
     return nullptr;
   }
-  return reinterpret_cast<const void*>(&decode_kernel<0, 0, false>);
+#undef TSB_K
+  return reinterpret_cast<const void*>(&decode_kernel<0, 0, false, false>);
 }
 
 }  // namespace tsb

@@ -104,6 +104,6 @@ TSB_HD inline AttSplit att_split(int H_kv, int ctas_per_seq) {
   return a;
 }
 
-const void* decode_kernel_ptr(int D, int G, bool fast);
+const void* decode_kernel_ptr(int D, int G, bool fast, bool lean);
 
 }  // namespace tsb

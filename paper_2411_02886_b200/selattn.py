@@ -335,7 +335,8 @@ class Engine:
                   22: "att:scores", 23: "att:softmax", 24: "att:pv", 25: "att:end", 27: "dec:done", 28: "merge:all_in", 31: "merge:end", 32: "crit:hist_zeroed",
                   33: "find1:loaded", 36: "find2:loaded", 38: "hist2:zeroed", 39: "hist2:counted",
                   40: "compact:iter", 41: "sel_out:prefix", 42: "merge:loaded", 43: "merge:weights",
-                  26: "dec:issued", 44: "dev:att_rep"}
+                  26: "dec:issued", 44: "dev:att_rep",
+                  45: "p0:dec_loads", 46: "p0:frames", 47: "p0:hit_prep"}
 
     def set_trace(self, enable=True):
         check(lib.ts_engine_set_trace(self._h, 1 if enable else 0))

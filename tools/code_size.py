@@ -1,6 +1,6 @@
 """Static SASS instructions of the fused decode kernel per source region
 (dev tool: the post-scan phases run once per launch from a cold instruction
-cache, so their code size is latency). usage: python tools/code_size.py [D G]"""
+cache, so their code size is latency). usage: python tools/code_size.py [D G [LEAN]]"""
 import bisect
 import os
 import re
@@ -10,12 +10,13 @@ import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 D, G = (sys.argv[1], sys.argv[2]) if len(sys.argv) > 2 else ("128", "4")
+LEAN = sys.argv[3] if len(sys.argv) > 3 else "1"
 obj = os.path.join(ROOT, "paper_2411_02886_b200", "_build", "decode.cu.o")
 with tempfile.TemporaryDirectory() as td:
     subprocess.run(["cuobjdump", "-xelf", "all", obj], cwd=td, capture_output=True)
     cubin = [f for f in os.listdir(td) if f.endswith(".cubin")][0]
     dis = subprocess.run(["nvdisasm", "-g", os.path.join(td, cubin)], capture_output=True, text=True).stdout
-name = f"decode_kernelILi{D}ELi{G}ELb1EEEvNS_12DecodeParamsE:"
+name = f"decode_kernelILi{D}ELi{G}ELb1ELb{LEAN}EEEvNS_12DecodeParamsE:"
 start = dis.index(name)
 body = dis[start:]
 end = body.find("//---------------------", 10)
