@@ -45,7 +45,7 @@ def _compile(src, force):
     if not force and not _newer(deps, obj):
         return obj, None
     lang = ["-x", "cu"] if src.endswith(".cu") else ["-x", "c++"]
-    cmd = [NVCC] + ARCH + COMMON + lang + ["-c", path, "-o", obj]
+    cmd = [NVCC] + ARCH + COMMON + lang + ["-c", path, "-o", obj] + os.environ.get("TS_NVCC_FLAGS", "").split()
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

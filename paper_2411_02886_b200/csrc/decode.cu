@@ -94,6 +94,9 @@ __device__ __forceinline__ size_t row_index(const SeqDesc& sd, uint32_t tok, int
 // (slot 12) also record %globaltimer (slots 0 / 30, ns; the start clock goes
 // to slot 29) so the host aligns the CTAs and converts cycles to ns.
 __device__ __forceinline__ void trace_pt(const DecodeParams& p, int i) {
+#ifdef TSB_NO_TRACE
+  return;
+#endif
   if (p.trace && threadIdx.x == 0) {
     unsigned long long* t = p.trace + blockIdx.x * kTraceStride;
     const unsigned long long c = clock64();
@@ -110,13 +113,19 @@ __device__ __forceinline__ void trace_pt(const DecodeParams& p, int i) {
 
 // Sub-phase stamp into a CTA's trace row (nullptr: off); thread 0 only.
 __device__ __forceinline__ void stamp(unsigned long long* tr, int i) {
+#ifdef TSB_NO_TRACE
+  return;
+#endif
   if (tr && threadIdx.x == 0) tr[i] = clock64();
 }
 
 // Dev timing: TS_DEBUG_FLAGS = n << 8 ends the launch at stop point n
 // (uniform over the grid, so no barrier is left waiting).
+#ifndef TSB_LEAN_DEV
+#define TSB_LEAN_DEV 1
+#endif
 #define TSB_STOP_AT(n) \
-  if ((p.debug_flags >> 8) == (n)) return
+  if ((!LEAN || TSB_LEAN_DEV) && (p.debug_flags >> 8) == (n)) return
 
 // Block-wide exclusive scan of one value per thread (all threads call).
 // Out of line (like find_bin / radix_hist): the fused kernel's one-shot phases
@@ -410,7 +419,7 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
     const int s = it % kStages;
     mbar_wait(&sm.full[s], (it / kStages) & 1);
     float c[4] = {0.f, 0.f, 0.f, 0.f};
-    if (!(p.debug_flags & 1)) {
+    {
       const uint32_t abase = ring_base + static_cast<uint32_t>(s * R * rstride);
 #pragma unroll
       for (int kc = 0; kc < KC; ++kc) {
@@ -1319,7 +1328,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
 
   trace_pt(p, 0);
   unsigned long long* const trc = p.trace ? p.trace + blockIdx.x * kTraceStride : nullptr;
-  if (p.debug_flags & 16) return;  // dev timing: launch + prologue only
+  TSB_STOP_AT(15);  // launch + prologue only
   // ---- phase 0: append, scan frames, Selection Cache decision(s), hit prep
   // the decision's loads first: they head the critical path
   DecisionLoads dl{};
@@ -1377,38 +1386,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     }
   }
   stamp(trc, 47);
-  // Speculative scan start: the TMA producer issues the first ring stages of
-  // the K scan before the Selection Cache decision is known. On a miss the
-  // scan starts a decision-time earlier; on a hit the (few) stages are
-  // drained unused before the ring is reused.
-  int pre = 0;
-  if constexpr (FAST) {
-    const ScanGeom geom = scan_geom(p.H, p.H_kv, D, p.ring_bytes);
-    if ((p.debug_flags & 64) && may_scan && (pmode & kModeCache))  // experimental (measured: no gain)
-      pre = min(min((nloc + geom.rows - 1) / geom.rows, geom.stages), 4);
-    if (pre > 0 && tid < 32) {
-      const int row_bytes = p.H_kv * D * 2, rstride = row_bytes + 16;
-      const uint64_t pol = policy_evict_first();
-      const char* kbase = reinterpret_cast<const char*>(p.k_slab);
-      int32_t fr[4];
-#pragma unroll
-      for (int it = 0; it < 4; ++it) {  // all page-table loads in flight together
-        const int jl = it * geom.rows + tid;
-        fr[it] = (it < pre && tid < geom.rows && jl < nloc)
-                     ? static_cast<int32_t>(row_index(sd, cand_at(sd, j0 + jl), p.page_size)) : 0;
-      }
-#pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        if (it >= pre) break;
-        const int nrows = min(geom.rows, nloc - it * geom.rows);
-        if (tid == 0) mbar_arrive_expect_tx(&sm.full[it], static_cast<uint32_t>(nrows * row_bytes));
-        __syncwarp();
-        if (tid < nrows)
-          bulk_g2s(sm.ring + static_cast<size_t>(it * geom.rows + tid) * rstride,
-                   kbase + static_cast<size_t>(fr[it]) * row_bytes, row_bytes, &sm.full[it], pol);
-      }
-    }
-  }
+  const int pre = 0;  // ring stages issued before the decision (none)
   // Selection Cache decisions. A single sequence: every CTA evaluates it
   // (bit-identical) so the grid agrees on whether selection (and its
   // barriers) runs. Several sequences: each CTA evaluates its own and the
@@ -1477,8 +1455,6 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     for (int i = cs * blockDim.x + tid; i < 2 * kHistPass; i += p.ctas_per_seq * blockDim.x) gh[i] = 0u;
   }
   if (cs == 0 && tid == 0 && own == 3) sd.cache->error = 1;
-  if (pre > 0 && own != 1)
-    for (int it = 0; it < pre; ++it) mbar_wait(&sm.full[it], 0);  // speculative stages landed
   __syncthreads();
 
   TSB_STOP_AT(1);
@@ -1498,10 +1474,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       }
     } else {
       float* so = (pmode & kModeSOut) ? sd.s_out + j0 : nullptr;
-      if (p.debug_flags & 16384) {  // dev: no K streaming (S = 0), for cache-state experiments
-        for (int i = tid; i < H * sstride; i += blockDim.x) Sbuf[i] = 0.f;
-        for (int h = tid; h < H; h += blockDim.x) sm.headmax[h] = float_ord(0.f);
-      } else if constexpr (FAST) scan_fast<D, G>(p, sd, sm, j0, nloc, Sbuf, sstride, so, pre);
+      if constexpr (FAST) scan_fast<D, G>(p, sd, sm, j0, nloc, Sbuf, sstride, so, pre);
       else scan_generic(p, sd, sm, j0, nloc, Sbuf, sstride, so);
     }
   }
@@ -1514,7 +1487,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     }
   __syncthreads();
   trace_pt(p, 2);
-  if (p.debug_flags & 2) return;  // dev timing: stop after the scan
+  TSB_STOP_AT(2);
 
   // ---- phase 2: per-CTA softmax partials m = max_j S, z = sum_j e^(S - m) per
   // head (softmax_rows, tensor.cpp:31-52): warp per head, float4 rows, four
@@ -1529,7 +1502,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   if (any_select) gs.sync();  // B1: softmax partials of every CTA visible
   TSB_STOP_AT(4);
   trace_pt(p, 4);
-  if (p.debug_flags & 4) return;  // dev timing: stop after B1
+
 
   // ---- phase 3: criticality (soft vote / raw sum) + cache bookkeeping
   if (cs == 0 && tid == 0 && (pmode & kModeCache) && (own == 1 || own == 2)) {
@@ -1707,7 +1680,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     gs.sync();  // B3
     TSB_STOP_AT(8);
     trace_pt(p, 7);
-    if (p.debug_flags & 32) return;  // dev timing: stop after B3
+
     uint32_t eq_total = 0;
     if (radix_own) {
       int b;
@@ -1870,7 +1843,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       }
     }
   }
-  if (!(pmode & kModeAttend) || (p.debug_flags & 8)) return;
+  if (!(pmode & kModeAttend)) return;
 
   // ---- phase 7: split-K sparse flash-decoding (KV head x row chunk)
   AttView av{};
@@ -1914,12 +1887,6 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     for (int g = gi; g < p.H_kv; g += split.groups) {
       float* parts = p.ws_att + (static_cast<size_t>(seq_id) * p.H_kv + g) * split.chunks * Gq * stride;
       if constexpr (FAST) {
-        if (p.debug_flags & 4096) {  // dev: run the attention twice (warm instruction cache timing)
-          attend_group_mma<D>(p, sd, av, sm, g, r0, min(r1, av.n_rows), with_cur,
-                              parts + static_cast<size_t>(ci) * Gq * stride);
-          __syncthreads();
-          stamp(trc, 44);
-        }
         attend_group_mma<D>(p, sd, av, sm, g, r0, min(r1, av.n_rows), with_cur,
                             parts + static_cast<size_t>(ci) * Gq * stride);
       }
