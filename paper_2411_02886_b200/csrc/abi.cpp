@@ -254,7 +254,8 @@ void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t 
   const tsb::SeqDesc& s0 = p.seqs[0];
   const bool lean = pl.fn_lean && !g_no_lean && p.n_seq == 1 && pl.s_in_smem && p.method == 2 &&
                     p.mode == (tsb::kModeSelect | tsb::kModeScore | tsb::kModeCache | tsb::kModeAttend | tsb::kModeAppend) &&
-                    !s0.att_list && !s0.no_cur && s0.shard_base == 0 && !s0.cand && s0.sel_rows;
+                    !s0.att_list && !s0.no_cur && s0.shard_base == 0 && !s0.cand && s0.sel_rows && !s0.ml_out &&
+                    (p.page_size & (p.page_size - 1)) == 0;
   const void* fn = lean ? pl.fn_lean : pl.fn;
   // the dynamic shared-memory limit is set once per kernel (largest request so far)
   static std::mutex mu;

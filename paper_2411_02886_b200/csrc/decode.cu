@@ -70,7 +70,10 @@ __device__ __forceinline__ Smem carve(uint8_t* base, const DecodeParams& p) {
   return s;
 }
 
+// LEAN launches have implicit candidates and power-of-two pages (abi.cpp).
+template <bool LEAN = false>
 __device__ __forceinline__ uint32_t cand_at(const SeqDesc& sd, int j) {
+  if (LEAN) return static_cast<uint32_t>(sd.cand_begin + j);
   return sd.cand ? sd.cand[j] : static_cast<uint32_t>(sd.cand_begin + j);
 }
 
@@ -81,8 +84,9 @@ __device__ __forceinline__ uint32_t cand_at(const SeqDesc& sd, int j) {
 __device__ __noinline__ size_t row_index_div(const int32_t* page_table, uint32_t tok, int page_size) {
   return static_cast<size_t>(page_table[tok / page_size]) * page_size + tok % page_size;
 }
+template <bool LEAN = false>
 __device__ __forceinline__ size_t row_index(const SeqDesc& sd, uint32_t tok, int page_size) {
-  if ((page_size & (page_size - 1)) == 0) {
+  if (LEAN || (page_size & (page_size - 1)) == 0) {
     const int sh = __ffs(page_size) - 1;
     return (static_cast<size_t>(sd.page_table[tok >> sh]) << sh) | (tok & (page_size - 1));
   }
@@ -584,14 +588,15 @@ constexpr int kAttIdx = 1024;  // slab rows resolved per index window
 // Slab row of merged row i: the selection part comes with its slab rows
 // (published by the selecting CTAs, or cached with the SelectionResult),
 // only the windows go through the page table.
+template <bool LEAN>
 __device__ __forceinline__ int32_t att_row(const DecodeParams& p, const SeqDesc& sd, const AttView& v,
                                            const int* prefix, int i) {
-  if (sd.att_list) return static_cast<int32_t>(row_index(sd, sd.att_list[i], p.page_size));
-  if (i < v.init_end) return static_cast<int32_t>(row_index(sd, static_cast<uint32_t>(i), p.page_size));
+  if (!LEAN && sd.att_list) return static_cast<int32_t>(row_index(sd, sd.att_list[i], p.page_size));
+  if (i < v.init_end) return static_cast<int32_t>(row_index<LEAN>(sd, static_cast<uint32_t>(i), p.page_size));
   i -= v.init_end;
   if (i < v.n1) {
     if (!v.fresh) {
-      if (sd.sel_rows) return __ldcg(sd.sel_rows + v.lo1 + i);
+      if (LEAN || sd.sel_rows) return __ldcg(sd.sel_rows + v.lo1 + i);
       return static_cast<int32_t>(row_index(sd, __ldcg(sd.sel + v.lo1 + i), p.page_size));
     }
     int lo = 0, hi = v.ncta - 1;
@@ -603,7 +608,7 @@ __device__ __forceinline__ int32_t att_row(const DecodeParams& p, const SeqDesc&
     return __ldcg(p.ws_sel_row + static_cast<size_t>(v.cta0 + lo) * p.tpc + (i - prefix[lo]));
   }
   i -= v.n1;
-  return static_cast<int32_t>(row_index(sd, static_cast<uint32_t>(v.lb + i), p.page_size));
+  return static_cast<int32_t>(row_index<LEAN>(sd, static_cast<uint32_t>(v.lb + i), p.page_size));
 }
 
 // Tensor-core split-K flash-decoding partial (D = 64 / 128, G <= 8) of the
@@ -618,7 +623,7 @@ __device__ __forceinline__ int32_t att_row(const DecodeParams& p, const SeqDesc&
 //   * P.V: O^T[16 d x 8 heads] += V^T (ldmatrix.trans) x P^T (P split into
 //     three bf16 parts) -- warp = (d tile, row group);
 //   * online softmax per head between them, fp32 (attention.cpp:88-110).
-template <int D>
+template <int D, bool LEAN>
 __device__ void attend_group_mma(const DecodeParams& p, const SeqDesc& sd, const AttView& av, const Smem& sm,
                                  int g, int r0, int r1, bool with_cur, float* part) {
   constexpr int KC = D / 16;                 // k-chunks of the score MMA
@@ -703,7 +708,7 @@ __device__ void attend_group_mma(const DecodeParams& p, const SeqDesc& sd, const
   bool first = true;
   for (;;) {
     const int nw = min(kAttIdx, nrows - w0);
-    for (int r = tid; r < nw; r += blockDim.x) ridx[r] = att_row(p, sd, av, sm.prefix, r0 + w0 + r);
+    for (int r = tid; r < nw; r += blockDim.x) ridx[r] = att_row<LEAN>(p, sd, av, sm.prefix, r0 + w0 + r);
     const bool build_qf = first;
     if (first && tid < 8 * D) qs[tid] = qv;
     first = false;
@@ -1021,7 +1026,7 @@ __device__ void attend_group(const DecodeParams& p, const SeqDesc& sd, const Att
   for (;;) {
     const int nw = min(kAttIdx, nrows - w0);
     for (int r = tid; r < nw; r += blockDim.x)
-      ridx[r] = att_row(p, sd, av, sm.prefix, r0 + w0 + r);
+      ridx[r] = att_row<false>(p, sd, av, sm.prefix, r0 + w0 + r);
     __syncthreads();
     trace_pt(p, 20);
     const bool last_w = w0 + nw >= nrows;
@@ -1182,6 +1187,7 @@ __device__ void attend_group(const DecodeParams& p, const SeqDesc& sd, const Att
 // loaded together into shared memory (`buf`, free staging), then warp per
 // head forms M, L and the chunk weights, and thread per output sums its
 // chunks.
+template <bool LEAN>
 __device__ void merge_outputs(const DecodeParams& p, const SeqDesc& sd, int g, const float* parts, int chunks,
                               int o0, int nout, float* buf) {
   const int d = p.d, G = p.H / p.H_kv, stride = att_stride(d);
@@ -1240,7 +1246,7 @@ __device__ void merge_outputs(const DecodeParams& p, const SeqDesc& sd, int g, c
     for (int c = 0; c < chunks; ++c) acc = fmaf(wm[c], ov[c * nout + oo], acc);
     const float L = hdr[m * 2 + 1];
     sd.out[static_cast<size_t>(g + m * p.H_kv) * d + t] = L > 0.f ? acc / L : 0.f;  // empty shard: 0
-    if (sd.ml_out && t == 0) {
+    if (!LEAN && sd.ml_out && t == 0) {
       sd.ml_out[(g + m * p.H_kv) * 2 + 0] = hdr[m * 2 + 0];
       sd.ml_out[(g + m * p.H_kv) * 2 + 1] = L;
     }
@@ -1366,7 +1372,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int jl = tid + u * blockDim.x;
-      fr_pre[u] = (may_scan && jl < nloc) ? static_cast<int32_t>(row_index(sd, cand_at(sd, j0 + jl), p.page_size)) : 0;
+      fr_pre[u] = (may_scan && jl < nloc)
+                      ? static_cast<int32_t>(row_index<LEAN>(sd, cand_at<LEAN>(sd, j0 + jl), p.page_size)) : 0;
     }
   }
   stamp(trc, 46);
@@ -1448,7 +1455,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       if (may_scan && jl < nloc) sm.frames[jl] = fr_pre[u];
     }
     for (int jl = tid + 4 * blockDim.x; may_scan && jl < nloc; jl += blockDim.x)
-      sm.frames[jl] = static_cast<int32_t>(row_index(sd, cand_at(sd, j0 + jl), p.page_size));
+      sm.frames[jl] = static_cast<int32_t>(row_index<LEAN>(sd, cand_at<LEAN>(sd, j0 + jl), p.page_size));
   }
   if (do_select && own == 1 && T > p.k) {
     uint32_t* gh = p.ws_hist + static_cast<size_t>(seq_id) * 2 * kHistPass;
@@ -1753,7 +1760,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       const uint32_t pos = out_n + block_excl_scan(take ? 1u : 0u, sm.scratch, &tot);
       if (take) {
         const int32_t row = may_scan ? sm.frames[jl] : -1;
-        const uint32_t tok = cand_at(sd, j0 + jl) + (LEAN ? 0u : static_cast<uint32_t>(sd.shard_base));
+        const uint32_t tok = cand_at<LEAN>(sd, j0 + jl) + (LEAN ? 0u : static_cast<uint32_t>(sd.shard_base));
         const float cr = key_float(key);
         lt[pos] = tok;
         lc[pos] = cr;
@@ -1829,7 +1836,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
           const int i = my0 + static_cast<int>(pub_pos[u]);
           st_hint_u32(sd.sel + i, pub_tok[u], pol);
           st_hint_u32(sd.sel_crit + i, __float_as_uint(pub_crit[u]), pol);
-          if (sd.sel_rows) st_hint_u32(sd.sel_rows + i, static_cast<uint32_t>(pub_row[u]), pol);
+          if (LEAN || sd.sel_rows) st_hint_u32(sd.sel_rows + i, static_cast<uint32_t>(pub_row[u]), pol);
         }
     } else {
       const int myn = sm.prefix[cs + 1] - my0;
@@ -1839,7 +1846,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       for (int i = tid; i < myn; i += blockDim.x) {
         st_hint_u32(sd.sel + my0 + i, __ldcg(lt + i), pol);
         st_hint_u32(sd.sel_crit + my0 + i, __float_as_uint(__ldcg(lc + i)), pol);
-        if (sd.sel_rows) st_hint_u32(sd.sel_rows + my0 + i, static_cast<uint32_t>(__ldcg(lr + i)), pol);
+        if (LEAN || sd.sel_rows) st_hint_u32(sd.sel_rows + my0 + i, static_cast<uint32_t>(__ldcg(lr + i)), pol);
       }
     }
   }
@@ -1887,7 +1894,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     for (int g = gi; g < p.H_kv; g += split.groups) {
       float* parts = p.ws_att + (static_cast<size_t>(seq_id) * p.H_kv + g) * split.chunks * Gq * stride;
       if constexpr (FAST) {
-        attend_group_mma<D>(p, sd, av, sm, g, r0, min(r1, av.n_rows), with_cur,
+        attend_group_mma<D, LEAN>(p, sd, av, sm, g, r0, min(r1, av.n_rows), with_cur,
                             parts + static_cast<size_t>(ci) * Gq * stride);
       }
       else
@@ -1911,7 +1918,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       {
         const int n_out = Gq * p.d, per = (n_out + split.chunks - 1) / split.chunks;
         const int o0 = min(n_out, ci * per);
-        merge_outputs(p, sd, g, parts, split.chunks, o0, min(n_out, o0 + per) - o0,
+        merge_outputs<LEAN>(p, sd, g, parts, split.chunks, o0, min(n_out, o0 + per) - o0,
                       reinterpret_cast<float*>(sm.ring));
       }
       trace_pt(p, 31);
