@@ -204,7 +204,16 @@ Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows, bool 
   pl.ctas_per_seq = c;
   pl.tpc = static_cast<int>(tsb::align_up(static_cast<size_t>(std::max(1, (max_T + c - 1) / c)), 4));  // 16-B rows
   const int row_bytes = H_kv * d * 2;
-  const size_t optin = static_cast<size_t>(di.smem_optin);
+  // dynamic shared memory left next to the kernel's static allocation
+  cudaFuncAttributes fa{};
+  ck(cudaFuncGetAttributes(&fa, pl.fn), "cudaFuncGetAttributes");
+  size_t stat = fa.sharedSizeBytes;
+  if (pl.fn_lean) {
+    cudaFuncAttributes fl{};
+    ck(cudaFuncGetAttributes(&fl, pl.fn_lean), "cudaFuncGetAttributes");
+    stat = std::max(stat, static_cast<size_t>(fl.sharedSizeBytes));
+  }
+  const size_t optin = static_cast<size_t>(di.smem_optin) - stat;
   tsb::SmemLayout L = tsb::smem_layout(H, row_bytes, pl.tpc, 1);
   if (L.total <= optin && !g_force_global_s && !force_spill) {
     pl.s_in_smem = 1;

@@ -45,8 +45,8 @@ struct Smem {
   float* f;        // [H]
   uint32_t* scratch;  // [256]
   int32_t* frames; // [tpc] slab row of each local candidate
-  uint64_t* full;  // [kMaxStages]
-  uint64_t* empty; // [kMaxStages]
+  uint64_t* full;  // [nphase][kStages] (kMaxBarPairs)
+  uint64_t* empty; // [nphase][kStages]
   uint64_t* att;   // [2] attention staging barriers (double buffer)
   uint64_t* aux;   // bulk staging barrier (stats)
 };
@@ -63,8 +63,8 @@ __device__ __forceinline__ Smem carve(uint8_t* base, const DecodeParams& p) {
   s.f = reinterpret_cast<float*>(base + L.f);
   s.scratch = reinterpret_cast<uint32_t*>(base + L.scratch);
   s.full = reinterpret_cast<uint64_t*>(base + L.bars);
-  s.empty = s.full + kMaxStages;
-  s.att = s.full + 2 * kMaxStages;
+  s.empty = s.full + kMaxBarPairs;
+  s.att = s.full + 2 * kMaxBarPairs;
   s.aux = s.att + 2;
   s.frames = reinterpret_cast<int32_t*>(base + L.frames);
   return s;
@@ -349,6 +349,16 @@ __device__ __forceinline__ void split3(float x, float& hi, float& mid, float& lo
   lo = r1 - mid;
 }
 
+__device__ __forceinline__ int ring_lcm(int a, int b) {
+  int x = a, y = b;
+  while (y) {
+    const int t = x % y;
+    x = y;
+    y = t;
+  }
+  return a / x * b;
+}
+
 template <int D, int G>
 __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& sm, int j0,
                           int nloc, float* Sbuf, int sstride, float* s_out_row0, int pre) {
@@ -366,18 +376,26 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
     // ---------------------------------------------------------- producer
     // slab rows of all local candidates were staged in smem (sm.frames), so
     // issuing a stage is latency-free; rows land at a padded stride.
+    // Stage it: slot it % kStages, consumed by phase it % nphase; its
+    // barrier pair is used every lcm(nphase, kStages) stages, so the use
+    // index it / lcm gives the parity.
     const uint64_t pol = policy_evict_first();
     const char* kbase = reinterpret_cast<const char*>(p.k_slab);
+    const int nph = kDecodeConsumers / Hkv, lcm = ring_lcm(nph, kStages);
     for (int it = pre; it < nit; ++it) {  // stages [0, pre) were issued in phase 0
       const int s = it % kStages;
       const int rbase = it * R;
       const int nrows = min(R, nloc - rbase);
-      if (it >= kStages) mbar_wait(&sm.empty[s], ((it / kStages) & 1) ^ 1);
-      if (lane == 0) mbar_arrive_expect_tx(&sm.full[s], static_cast<uint32_t>(nrows * row_bytes));
+      if (it >= kStages) {  // the slot's previous stage has been consumed
+        const int prev = it - kStages;
+        mbar_wait(&sm.empty[(prev % nph) * kStages + s], (prev / lcm) & 1);
+      }
+      uint64_t* fb = &sm.full[(it % nph) * kStages + s];
+      if (lane == 0) mbar_arrive_expect_tx(fb, static_cast<uint32_t>(nrows * row_bytes));
       __syncwarp();
       if (lane < nrows)
         bulk_g2s(sm.ring + static_cast<size_t>(s * R + lane) * rstride,
-                 kbase + static_cast<size_t>(sm.frames[rbase + lane]) * row_bytes, row_bytes, &sm.full[s], pol);
+                 kbase + static_cast<size_t>(sm.frames[rbase + lane]) * row_bytes, row_bytes, fb, pol);
     }
     return;
   }
@@ -386,6 +404,7 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
   const int cw = warp - 1;
   const int nphase = kDecodeConsumers / Hkv;
   const int kvh = cw % Hkv, phase = cw / Hkv;
+  const int lcm = ring_lcm(nphase, kStages);  // uses of a (phase, slot) barrier pair are lcm stages apart
   // B fragments: lane holds q[head g = lane/4][d = kc*16 + (lane%4)*2 + {0,1,8,9}]
   uint32_t bq[KC][3][2];
   {
@@ -421,7 +440,7 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
   const uint32_t ring_base = smem_u32(sm.ring) + lrow * rstride + lcol;
   for (int it = phase; it < nit; it += nphase) {
     const int s = it % kStages;
-    mbar_wait(&sm.full[s], (it / kStages) & 1);
+    mbar_wait(&sm.full[phase * kStages + s], (it / lcm) & 1);
     float c[4] = {0.f, 0.f, 0.f, 0.f};
     {
       const uint32_t abase = ring_base + static_cast<uint32_t>(s * R * rstride);
@@ -435,7 +454,7 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[s]);  // operands consumed
+    if (lane == 0) mbar_arrive(&sm.empty[phase * kStages + s]);  // operands consumed
     const int rbase = it * R + (lane >> 2);
     float v[4];
 #pragma unroll
@@ -1296,7 +1315,7 @@ __device__ __noinline__ void softmax_partials(float* Sbuf, int sstride, int nloc
 // branch count are their latency.
 template <int D, int G, bool FAST, bool LEAN>
 __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeParams p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
   const Smem sm = carve(smem_raw, p);
   const int cta = blockIdx.x;
   const int nblocks = gridDim.x;
@@ -1313,9 +1332,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   const int tid = threadIdx.x;
   const bool do_select = (pmode & kModeSelect) != 0;
 
-  if (FAST && tid < kMaxStages) {
+  if (FAST && tid < kMaxBarPairs) {
     mbar_init(&sm.full[tid], 1);
-    mbar_init(&sm.empty[tid], p.H_kv);  // the H_kv consumer warps of a stage
+    mbar_init(&sm.empty[tid], p.H_kv);  // the H_kv consumer warps of a phase
   }
   if (tid == 0) {
     mbar_init(&sm.att[0], 1);

@@ -17,6 +17,10 @@ constexpr int kDecodeConsumers = 16;            // tensor-core consumer warps of
 constexpr int kDecodeWarps = kDecodeConsumers + 1;  // + warp 0: TMA producer
 constexpr int kDecodeThreads = kDecodeWarps * 32;
 constexpr int kMaxStages = 16;
+// Ring barriers are per (consumer phase, slot): a consumer warp takes every
+// nphase-th stage, so with kStages % nphase != 0 one barrier per slot would be
+// shared by the phases and a warp's parity wait could alias a phase it skipped.
+constexpr int kMaxBarPairs = 64;
 constexpr size_t kRingBudget = 96 * 1024;        // minimum K-row ring (also attention staging)
 constexpr int kRadixBins = 4096;                 // 12-bit radix digits (2 passes -> 24-bit keys)
 constexpr int kHistPass = kRadixBins;            // global histogram words per pass
@@ -45,6 +49,8 @@ TSB_HD inline ScanGeom scan_geom(int H, int H_kv, int d, size_t ring_bytes = kRi
   const size_t stage = static_cast<size_t>(16) * (H_kv * d * 2 + 16);
   int stages = static_cast<int>(ring_bytes / stage);
   if (stages > kMaxStages) stages = kMaxStages;
+  const int nphase = kDecodeConsumers / H_kv;
+  if (stages * nphase > kMaxBarPairs) stages = kMaxBarPairs / nphase;
   if (stages < 2) return g;
   g.fast = 1;
   g.rows = 16;
@@ -82,7 +88,7 @@ TSB_HD inline SmemLayout smem_layout(int H, int row_bytes, int tpc, int s_in_sme
   L.scratch = o;
   o += 256 * 4;
   L.bars = o;
-  o += (2 * kMaxStages + 4) * 8;  // full/empty ring barriers + attention (x2) + aux
+  o += (2 * kMaxBarPairs + 4) * 8;  // full/empty ring barriers + attention (x2) + aux
   L.total = align_up(o, 128);
   return L;
 }

@@ -272,6 +272,34 @@ def test_decode_llama_32k_parity(sa, orc):
     assert rel_fro(o1, want) <= 1e-5 and np.abs(o1 - want).max() <= 1e-4
 
 
+@pytest.mark.parametrize("n", [131072, 142336])
+def test_decode_llama_128k_parity(sa, orc, n):
+    """Config 2 size: 128K+ cache, three consecutive misses.
+    142 336 tokens puts 960 candidates (60 ring stages) on every CTA with a
+    3-stage ring: the (phase, slot) ring barriers must keep every consumer on
+    its own stage (a shared per-slot barrier let a warp's parity wait alias a
+    skipped phase there)."""
+    H, H_kv, d = 32, 8, 128
+    eng, ref = _engine_pair(sa, orc, n, H, H_kv, d, 2048, 128, 512, 2.0, 4343)  # theta > 1: every step misses
+    for step in range(3):
+        q = rng_normal(90 + step, (1, H * d))
+        kt = bf16_round(rng_normal(190 + step, (1, H_kv * d), 3.0))
+        vt = bf16_round(rng_normal(290 + step, (1, H_kv * d)))
+        o1, h1, s1 = eng.decode(q, kt, vt)
+        o2, h2, s2 = ref.decode(q, kt, vt)
+        assert not h1 and not h2
+        m = n + step
+        cand = np.arange(128, m - 512, dtype=np.uint32)
+        want = o2
+        if s1 != list(s2):
+            K_all, V_all = ref_rows(ref)
+            S = orc.score_paged(q.reshape(H, d), K_all[:m], H_kv, cand)
+            check_selection(s1, s2, orc.criticality(S, 2048), cand)
+            att = orc.make_windows(m, 128, 512, np.asarray(s1, np.uint32))
+            want = orc.sparse_attend(q, kt, vt, K_all[:m], V_all[:m], H, H_kv, att)
+        assert rel_fro(o1, want) <= 1e-5 and np.abs(o1 - want).max() <= 1e-4, step
+
+
 # --------------------------------------------------------------- prefill
 @pytest.mark.parametrize("H,H_kv,d,n,chunk,k", [(2, 2, 4, 30, 8, 4), (2, 1, 4, 32, 16, 4096), (4, 2, 32, 1500, 256, 128),
                                               (8, 2, 128, 1800, 512, 256), (28, 4, 128, 1300, 300, 128)])
