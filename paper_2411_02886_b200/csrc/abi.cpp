@@ -188,6 +188,10 @@ struct Plan {
   size_t smem;
   const void* fn;
   const void* fn_lean;  // the single-sequence decode-step specialisation (nullptr: none)
+  // the LEAN kernel's layout: S in tensor memory, the rest of smem to the ring
+  bool lean_ok;
+  int lean_ring_bytes, lean_att_bytes;
+  size_t lean_smem;
 };
 
 Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows, bool attend = true,
@@ -227,6 +231,17 @@ Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows, bool 
   L = tsb::smem_layout(H, row_bytes, pl.tpc, pl.s_in_smem, static_cast<size_t>(pl.ring_bytes));
   pl.smem = L.total;
   pl.att_bytes = static_cast<int>(L.frames - L.ring);  // ring + S + keys: dead once the selection is out
+  pl.lean_ok = pl.fn_lean && tsb::tmem_fits(H_kv, pl.tpc);
+  if (pl.lean_ok) {
+    tsb::SmemLayout LL = tsb::smem_layout(H, row_bytes, pl.tpc, tsb::kSTmem);
+    pl.lean_ok = LL.total <= optin;
+    if (pl.lean_ok) {
+      pl.lean_ring_bytes = static_cast<int>(tsb::kRingBudget + (optin - LL.total) / 1024 * 1024);
+      LL = tsb::smem_layout(H, row_bytes, pl.tpc, tsb::kSTmem, static_cast<size_t>(pl.lean_ring_bytes));
+      pl.lean_smem = LL.total;
+      pl.lean_att_bytes = static_cast<int>(LL.frames - LL.ring);
+    }
+  }
   if (attend && H / H_kv > tsb::kAttMaxG)
     fail(TS_INVALID_ARGUMENT, "more than 8 query heads per KV head is not supported by the decode kernel");
   if (d > 256) fail(TS_INVALID_ARGUMENT, "head_dim > 256 is not supported by the decode kernel");
@@ -236,10 +251,19 @@ Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows, bool 
 
 void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t st) {
   const int n_ctas = p.n_seq * pl.ctas_per_seq;
-  ws.prepare(n_ctas, p.H, p.H_kv, p.d, pl.tpc, pl.s_in_smem, p.n_seq, st);
+  // the engine's plain single-sequence step runs the specialisation with the
+  // other modes compiled out and S in tensor memory (decode.cu, LEAN)
+  const tsb::SeqDesc& s0 = p.seqs[0];
+  const bool lean = pl.lean_ok && !g_no_lean && !g_force_global_s && p.n_seq == 1 && p.method == 2 &&
+                    p.mode == (tsb::kModeSelect | tsb::kModeScore | tsb::kModeCache | tsb::kModeAttend | tsb::kModeAppend) &&
+                    !s0.att_list && !s0.no_cur && s0.shard_base == 0 && !s0.cand && s0.sel_rows && !s0.ml_out &&
+                    (p.page_size & (p.page_size - 1)) == 0;
+  const void* fn = lean ? pl.fn_lean : pl.fn;
+  const size_t smem = lean ? pl.lean_smem : pl.smem;
+  ws.prepare(n_ctas, p.H, p.H_kv, p.d, pl.tpc, lean ? 1 : pl.s_in_smem, p.n_seq, st);
   p.ctas_per_seq = pl.ctas_per_seq;
   p.tpc = pl.tpc;
-  p.s_in_smem = pl.s_in_smem;
+  p.s_in_smem = lean ? tsb::kSTmem : pl.s_in_smem;
   p.ws_s = ws.s.as<float>();
   p.ws_keys = ws.keys.as<uint32_t>();
   p.ws_m = ws.m.as<float>();
@@ -255,30 +279,22 @@ void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t 
   p.bar = ws.bar.as<unsigned int>();
   p.bar_slot = (ws.launches & 1u) ? 32 : 0;  // launches on one workspace are stream-ordered
   p.prefetch_stages = g_prefetch_stages;
-  p.ring_bytes = pl.ring_bytes;
-  p.att_bytes = pl.att_bytes;
+  p.ring_bytes = lean ? pl.lean_ring_bytes : pl.ring_bytes;
+  p.att_bytes = lean ? pl.lean_att_bytes : pl.att_bytes;
   p.debug_flags = g_debug_flags;
-  // the engine's plain single-sequence step runs the specialisation with the
-  // other modes compiled out (decode.cu, LEAN)
-  const tsb::SeqDesc& s0 = p.seqs[0];
-  const bool lean = pl.fn_lean && !g_no_lean && p.n_seq == 1 && pl.s_in_smem && p.method == 2 &&
-                    p.mode == (tsb::kModeSelect | tsb::kModeScore | tsb::kModeCache | tsb::kModeAttend | tsb::kModeAppend) &&
-                    !s0.att_list && !s0.no_cur && s0.shard_base == 0 && !s0.cand && s0.sel_rows && !s0.ml_out &&
-                    (p.page_size & (p.page_size - 1)) == 0;
-  const void* fn = lean ? pl.fn_lean : pl.fn;
   // the dynamic shared-memory limit is set once per kernel (largest request so far)
   static std::mutex mu;
   static std::unordered_map<const void*, size_t> smem_set;
   std::lock_guard<std::mutex> lock(mu);
   size_t& have = smem_set[fn];
-  if (pl.smem > have) {
-    ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)),
+  if (smem > have) {
+    ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
        "cudaFuncSetAttribute");
-    have = pl.smem;
+    have = smem;
   }
   void* args[] = {&p};
   const double t0 = g_host_prof ? now_ns() : 0.0;
-  ck(cudaLaunchCooperativeKernel(fn, dim3(n_ctas), dim3(tsb::kDecodeThreads), args, pl.smem, st),
+  ck(cudaLaunchCooperativeKernel(fn, dim3(n_ctas), dim3(tsb::kDecodeThreads), args, smem, st),
      "decode kernel launch");
   if (g_host_prof) g_prof[3] += now_ns() - t0;
   ws.launches += 1;

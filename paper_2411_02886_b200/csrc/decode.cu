@@ -305,6 +305,8 @@ __device__ int cache_decision(const SeqDesc& sd, int width, const DecisionLoads&
 
 // --------------------------------------------------------------- the scan
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kScratchTmem = 250;  // sm.scratch word holding the TMEM base address
+constexpr size_t kCritPartOffset = 64 * 1024;  // TMEM mode: per-kv-head criticality partials in the ring
 constexpr int kLeanMode = kModeSelect | kModeScore | kModeCache | kModeAttend | kModeAppend;
 // Fast path (sm_100a tensor cores, mma.sync bf16 -> fp32). The K rows of a
 // stage (16 tokens, padded stride so ldmatrix is bank-conflict free) are the
@@ -349,19 +351,17 @@ __device__ __forceinline__ void split3(float x, float& hi, float& mid, float& lo
   lo = r1 - mid;
 }
 
-__device__ __forceinline__ int ring_lcm(int a, int b) {
-  int x = a, y = b;
-  while (y) {
-    const int t = x % y;
-    x = y;
-    y = t;
-  }
-  return a / x * b;
+
+// TM: the S fragments stay in tensor memory (tbase: the CTA's allocation);
+// consumer warp w keeps its r-th stage at columns r*4 .. r*4+3 of lane
+// quarter w % 4, column block (w - 1) / 4 (decode.h, kTmemColsPerWarp).
+__device__ __forceinline__ uint32_t tmem_warp_base(uint32_t tbase, int warp) {
+  return tbase + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>(((warp - 1) >> 2) * kTmemColsPerWarp);
 }
 
-template <int D, int G>
+template <int D, int G, bool TM>
 __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& sm, int j0,
-                          int nloc, float* Sbuf, int sstride, float* s_out_row0, int pre) {
+                          int nloc, float* Sbuf, int sstride, float* s_out_row0, int pre, uint32_t tbase) {
   constexpr int KC = D / 16;  // k-chunks of 16 along d
   const int Hkv = p.H_kv;
   const int row_bytes = Hkv * D * 2;
@@ -379,23 +379,30 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
     // Stage it: slot it % kStages, consumed by phase it % nphase; its
     // barrier pair is used every lcm(nphase, kStages) stages, so the use
     // index it / lcm gives the parity.
+    // (running slot / phase counters and per-pair parity bits: no divisions
+    // in the issue loop)
     const uint64_t pol = policy_evict_first();
     const char* kbase = reinterpret_cast<const char*>(p.k_slab);
-    const int nph = kDecodeConsumers / Hkv, lcm = ring_lcm(nph, kStages);
-    for (int it = pre; it < nit; ++it) {  // stages [0, pre) were issued in phase 0
-      const int s = it % kStages;
+    const int nph = kDecodeConsumers / Hkv;
+    uint64_t eparity = 0;  // bit k: parity of the next completion of empty[k] to wait for
+    int s = 0, ph = 0, ph_prev = 0;
+    for (int it = 0; it < nit; ++it) {
       const int rbase = it * R;
       const int nrows = min(R, nloc - rbase);
-      if (it >= kStages) {  // the slot's previous stage has been consumed
-        const int prev = it - kStages;
-        mbar_wait(&sm.empty[(prev % nph) * kStages + s], (prev / lcm) & 1);
+      if (it >= kStages) {  // the slot's previous stage (consumed by phase ph_prev) is free
+        const int k = ph_prev * kStages + s;
+        mbar_wait(&sm.empty[k], static_cast<uint32_t>(eparity >> k) & 1u);
+        eparity ^= 1ull << k;
+        ph_prev = ph_prev + 1 == nph ? 0 : ph_prev + 1;
       }
-      uint64_t* fb = &sm.full[(it % nph) * kStages + s];
+      uint64_t* fb = &sm.full[ph * kStages + s];
       if (lane == 0) mbar_arrive_expect_tx(fb, static_cast<uint32_t>(nrows * row_bytes));
       __syncwarp();
       if (lane < nrows)
         bulk_g2s(sm.ring + static_cast<size_t>(s * R + lane) * rstride,
                  kbase + static_cast<size_t>(sm.frames[rbase + lane]) * row_bytes, row_bytes, fb, pol);
+      s = s + 1 == kStages ? 0 : s + 1;
+      ph = ph + 1 == nph ? 0 : ph + 1;
     }
     return;
   }
@@ -404,7 +411,7 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
   const int cw = warp - 1;
   const int nphase = kDecodeConsumers / Hkv;
   const int kvh = cw % Hkv, phase = cw / Hkv;
-  const int lcm = ring_lcm(nphase, kStages);  // uses of a (phase, slot) barrier pair are lcm stages apart
+  uint32_t fparity = 0;  // bit s: parity of the next completion of full[phase][s]
   // B fragments: lane holds q[head g = lane/4][d = kc*16 + (lane%4)*2 + {0,1,8,9}]
   uint32_t bq[KC][3][2];
   {
@@ -438,9 +445,10 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
   const uint32_t lrow = static_cast<uint32_t>((lane & 7) + ((lane >> 3) & 1) * 8);
   const uint32_t lcol = static_cast<uint32_t>((lane >> 4) * 16 + kvh * D * 2);
   const uint32_t ring_base = smem_u32(sm.ring) + lrow * rstride + lcol;
-  for (int it = phase; it < nit; it += nphase) {
-    const int s = it % kStages;
-    mbar_wait(&sm.full[phase * kStages + s], (it / lcm) & 1);
+  int s = phase % kStages, r = 0;  // this warp's slot and stage count
+  for (int it = phase; it < nit; it += nphase, ++r) {
+    mbar_wait(&sm.full[phase * kStages + s], (fparity >> s) & 1u);
+    fparity ^= 1u << s;
     float c[4] = {0.f, 0.f, 0.f, 0.f};
     {
       const uint32_t abase = ring_base + static_cast<uint32_t>(s * R * rstride);
@@ -455,6 +463,8 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[phase * kStages + s]);  // operands consumed
+    s += nphase;
+    while (s >= kStages) s -= kStages;
     const int rbase = it * R + (lane >> 2);
     float v[4];
 #pragma unroll
@@ -464,14 +474,16 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
       v[e] = -INFINITY;
       if (g < G && row < nloc) {
         const int h = g * Hkv + kvh;
-        Sbuf[static_cast<size_t>(h) * sstride + row] = c[e];
+        if constexpr (!TM) Sbuf[static_cast<size_t>(h) * sstride + row] = c[e];
         if (s_out_row0) s_out_row0[static_cast<size_t>(h) * sd.n_cand + row] = c[e];
         v[e] = c[e];
       }
     }
     runmax0 = fmaxf(runmax0, fmaxf(v[0], v[2]));
     runmax1 = fmaxf(runmax1, fmaxf(v[1], v[3]));
+    if constexpr (TM) tmem_st4(tmem_warp_base(tbase, warp) + static_cast<uint32_t>(r * 4), c[0], c[1], c[2], c[3]);
   }
+  if constexpr (TM) tmem_wait_st();
   runmax0 = fmaxf(runmax0, __shfl_xor_sync(0xffffffffu, runmax0, 4));
   runmax1 = fmaxf(runmax1, __shfl_xor_sync(0xffffffffu, runmax1, 4));
   runmax0 = fmaxf(runmax0, __shfl_xor_sync(0xffffffffu, runmax0, 8));
@@ -1321,7 +1333,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   const int nblocks = gridDim.x;
   const int pmode = LEAN ? kLeanMode : p.mode;
   const int n_seq = LEAN ? 1 : p.n_seq;
-  const int s_in_smem = LEAN ? 1 : p.s_in_smem;
+  const int s_in_smem = LEAN ? kSTmem : p.s_in_smem;
   const int method = LEAN ? 2 : p.method;
   const int seq_id = LEAN ? 0 : cta / p.ctas_per_seq;
   const int cs = cta - seq_id * p.ctas_per_seq;
@@ -1481,13 +1493,40 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     for (int i = cs * blockDim.x + tid; i < 2 * kHistPass; i += p.ctas_per_seq * blockDim.x) gh[i] = 0u;
   }
   if (cs == 0 && tid == 0 && own == 3) sd.cache->error = 1;
+  // LEAN miss: S goes to tensor memory (the whole 512 columns; one CTA per SM)
+  const bool use_tmem = LEAN && own == 1;
+  if (use_tmem && tid < 32) tmem_alloc512(&sm.scratch[kScratchTmem]);
+  if (use_tmem) tmem_fence_before_sync();
   __syncthreads();
+  uint32_t tbase = 0;
+  if (use_tmem) {
+    tmem_fence_after_sync();
+    tbase = sm.scratch[kScratchTmem];
+  }
+  // releases the tensor memory (all threads call; uniform)
+  bool tmem_held = use_tmem;
+  auto tmem_release = [&]() {
+    if (!tmem_held) return;
+    tmem_fence_before_sync();
+    __syncthreads();
+    if (tid < 32) {
+      tmem_fence_after_sync();
+      tmem_dealloc512(tbase);
+    }
+    tmem_held = false;
+  };
+#undef TSB_STOP_AT
+#define TSB_STOP_AT(n)                                                       \
+  if ((!LEAN || TSB_LEAN_DEV) && (p.debug_flags >> 8) == (n)) {              \
+    tmem_release();                                                          \
+    return;                                                                  \
+  }
 
   TSB_STOP_AT(1);
   trace_pt(p, 1);
   // ---- phase 1: scan (Alg. 2)
-  float* Sbuf = s_in_smem ? sm.S : p.ws_s + static_cast<size_t>(cta) * H * p.tpc;
-  uint32_t* keys = s_in_smem ? sm.keys : p.ws_keys + static_cast<size_t>(cta) * p.tpc;
+  float* Sbuf = s_in_smem == kSSmem ? sm.S : p.ws_s + static_cast<size_t>(cta) * H * p.tpc;  // unused for kSTmem
+  uint32_t* keys = s_in_smem != kSGlobal ? sm.keys : p.ws_keys + static_cast<size_t>(cta) * p.tpc;
   const int sstride = p.tpc;
   const bool scanning = (own == 1) && ((pmode & (kModeScore | kModeSIn)) != 0);
   if (scanning) {
@@ -1500,13 +1539,13 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       }
     } else {
       float* so = (pmode & kModeSOut) ? sd.s_out + j0 : nullptr;
-      if constexpr (FAST) scan_fast<D, G>(p, sd, sm, j0, nloc, Sbuf, sstride, so, pre);
+      if constexpr (FAST) scan_fast<D, G, LEAN>(p, sd, sm, j0, nloc, Sbuf, sstride, so, pre, tbase);
       else scan_generic(p, sd, sm, j0, nloc, Sbuf, sstride, so);
     }
   }
   // S rows are read four candidates at a time: pad each row to a multiple
   // of 4 with -inf (exp -> 0, never selected)
-  if (scanning && (nloc & 3))
+  if (!LEAN && scanning && (nloc & 3))
     for (int i = tid; i < H * 4; i += blockDim.x) {
       const int h = i >> 2, jl = nloc + (i & 3);
       if (jl < ((nloc + 3) & ~3)) Sbuf[static_cast<size_t>(h) * sstride + jl] = -INFINITY;
@@ -1518,7 +1557,62 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   // ---- phase 2: per-CTA softmax partials m = max_j S, z = sum_j e^(S - m) per
   // head (softmax_rows, tensor.cpp:31-52): warp per head, float4 rows, four
   // independent SFU chains per lane
-  if (do_select && own == 1 && method == 2 && !shard_sel) {
+  if (LEAN && own == 1) {
+    // S in TMEM: each consumer warp turns its own fragments into e^(S - m_h)
+    // (m_h: the CTA's head max from the scan) and sums them per head; the
+    // (phase, head) sums meet in shared memory (the idle ring)
+    float* wz = reinterpret_cast<float*>(sm.ring);  // [nphase][H]
+    const int nph = kDecodeConsumers / p.H_kv;
+    const int warp = tid >> 5, lane = tid & 31;
+    if (warp >= 1) {
+      const int cw = warp - 1, kvh = cw % p.H_kv, ph = cw / p.H_kv;
+      const int g0 = (lane & 3) * 2;
+      const int h0 = g0 * p.H_kv + kvh, h1 = (g0 + 1) * p.H_kv + kvh;
+      const float ml0 = g0 < G ? ord_float(sm.headmax[h0]) * kLog2e : 0.f;
+      const float ml1 = g0 + 1 < G ? ord_float(sm.headmax[h1]) * kLog2e : 0.f;
+      const int nit = (nloc + 15) >> 4, nr = nit > ph ? (nit - ph + nph - 1) / nph : 0;
+      const uint32_t tw = tmem_warp_base(tbase, warp);
+      float z0 = 0.f, z1 = 0.f;
+#pragma unroll 1
+      for (int r0 = 0; r0 < nr; r0 += 4) {
+        float v[16];
+        tmem_ld16(tw + static_cast<uint32_t>(r0 * 4), v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int rbase = (ph + (r0 + q) * nph) * 16 + (lane >> 2);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int g = g0 + (e & 1), row = rbase + (e >> 1) * 8;
+            const bool ok = r0 + q < nr && g < G && row < nloc;
+            const float w = ok ? ex2_approx(fmaf(v[q * 4 + e], kLog2e, -((e & 1) ? ml1 : ml0))) : 0.f;
+            v[q * 4 + e] = w;
+            if (e & 1) z1 += w;
+            else z0 += w;
+          }
+        }
+        tmem_st16(tw + static_cast<uint32_t>(r0 * 4), v);
+      }
+      tmem_wait_st();
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        z0 += __shfl_xor_sync(0xffffffffu, z0, o);
+        z1 += __shfl_xor_sync(0xffffffffu, z1, o);
+      }
+      if (lane < 4) {
+        if (g0 < G) wz[ph * H + h0] = z0;
+        if (g0 + 1 < G) wz[ph * H + h1] = z1;
+      }
+    }
+    __syncthreads();
+    const size_t sh = stats_stride(p.ctas_per_seq);
+    const size_t so = static_cast<size_t>(seq_id) * H * sh + cs;
+    for (int h = tid; h < H; h += blockDim.x) {
+      float z = 0.f;
+      for (int q = 0; q < nph; ++q) z += wz[q * H + h];  // fixed order
+      p.ws_m[so + h * sh] = ord_float(sm.headmax[h]);
+      p.ws_z[so + h * sh] = z;
+    }
+  } else if (do_select && own == 1 && method == 2 && !shard_sel) {
     const size_t sh = stats_stride(p.ctas_per_seq);
     const size_t so = static_cast<size_t>(seq_id) * H * sh + cs;
     softmax_partials(Sbuf, sstride, nloc, H, sm.headmax, p.ws_m + so, p.ws_z + so, sh);
@@ -1641,37 +1735,85 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     // = sum_h e^(S - m_c) f_h, or the raw logit sum (select_topk,
     // selector.cpp:89-99); two candidates per thread, keys straight into the
     // pass-1 histogram
+    if constexpr (LEAN) {
+      // S in TMEM: each consumer warp forms its rows' partial over its kv
+      // head's query heads (sum_g e f_h), the four lanes of a row add up, and
+      // the H_kv partials meet in shared memory (after the radix histogram
+      // in the idle ring); then one pass per candidate in a fixed order
+      float* cpart = reinterpret_cast<float*>(sm.ring + kCritPartOffset);  // [H_kv][tpc]
+      const int nph = kDecodeConsumers / p.H_kv;
+      const int warp = tid >> 5, lane = tid & 31;
+      if (warp >= 1) {
+        const int cw = warp - 1, kvh = cw % p.H_kv, ph = cw / p.H_kv;
+        const int g0 = (lane & 3) * 2;
+        const float f0 = g0 < G ? ml[g0 * p.H_kv + kvh] : 0.f;
+        const float f1 = g0 + 1 < G ? ml[(g0 + 1) * p.H_kv + kvh] : 0.f;
+        const int nit = (nloc + 15) >> 4, nr = nit > ph ? (nit - ph + nph - 1) / nph : 0;
+        const uint32_t tw = tmem_warp_base(tbase, warp);
+        float* cp = cpart + kvh * p.tpc;
+#pragma unroll 1
+        for (int r0 = 0; r0 < nr; r0 += 4) {
+          float v[16];
+          tmem_ld16(tw + static_cast<uint32_t>(r0 * 4), v);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float lo = fmaf(v[q * 4 + 1], f1, v[q * 4 + 0] * f0);  // row lane/4
+            float hi = fmaf(v[q * 4 + 3], f1, v[q * 4 + 2] * f0);  // row lane/4 + 8
+            lo += __shfl_xor_sync(0xffffffffu, lo, 1);
+            hi += __shfl_xor_sync(0xffffffffu, hi, 1);
+            lo += __shfl_xor_sync(0xffffffffu, lo, 2);
+            hi += __shfl_xor_sync(0xffffffffu, hi, 2);
+            const int row = (ph + (r0 + q) * nph) * 16 + (lane >> 2);
+            if ((lane & 3) == 0 && r0 + q < nr) {
+              if (row < nloc) cp[row] = lo;
+              if (row + 8 < nloc) cp[row + 8] = hi;
+            }
+          }
+        }
+      }
+      tmem_release();  // (its barrier also publishes cpart)
+      for (int base = 0; base < nloc; base += blockDim.x) {
+        const int jl = base + tid;
+        float c = 0.f;
+        if (jl < nloc)
+          for (int g = 0; g < p.H_kv; ++g) c += cpart[g * p.tpc + jl];
+        const uint32_t key = float_key(c);
+        if (jl < nloc) keys[jl] = key;
+        if (radix_own) hist_add(sm.hist, key, jl < nloc, 20);
+      }
+    } else {
     const int n2 = (nloc + 1) >> 1;
-    const bool soft = method == 2;
-    for (int base = 0; base < n2; base += blockDim.x) {
-      const int q = base + tid;
-      float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
-      if (q < n2) {
-        const float* s2 = Sbuf + 2 * q;
-        int h = 0;
-        for (; h + 1 < H; h += 2) {
-          const float2 a = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h) * sstride);
-          const float2 b = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h + 1) * sstride);
-          const float fa = soft ? ml[h] : 1.f, fb = soft ? ml[h + 1] : 1.f;
-          c0 = fmaf(a.x, fa, c0);
-          c1 = fmaf(a.y, fa, c1);
-          c2 = fmaf(b.x, fb, c2);
-          c3 = fmaf(b.y, fb, c3);
+      const bool soft = method == 2;
+      for (int base = 0; base < n2; base += blockDim.x) {
+        const int q = base + tid;
+        float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+        if (q < n2) {
+          const float* s2 = Sbuf + 2 * q;
+          int h = 0;
+          for (; h + 1 < H; h += 2) {
+            const float2 a = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h) * sstride);
+            const float2 b = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h + 1) * sstride);
+            const float fa = soft ? ml[h] : 1.f, fb = soft ? ml[h + 1] : 1.f;
+            c0 = fmaf(a.x, fa, c0);
+            c1 = fmaf(a.y, fa, c1);
+            c2 = fmaf(b.x, fb, c2);
+            c3 = fmaf(b.y, fb, c3);
+          }
+          if (h < H) {
+            const float2 a = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h) * sstride);
+            const float fa = soft ? ml[h] : 1.f;
+            c0 = fmaf(a.x, fa, c0);
+            c1 = fmaf(a.y, fa, c1);
+          }
         }
-        if (h < H) {
-          const float2 a = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h) * sstride);
-          const float fa = soft ? ml[h] : 1.f;
-          c0 = fmaf(a.x, fa, c0);
-          c1 = fmaf(a.y, fa, c1);
+        const uint32_t k0 = float_key(c0 + c2), k1 = float_key(c1 + c3);
+        if (q < n2) *reinterpret_cast<uint2*>(keys + 2 * q) = make_uint2(k0, k1);
+        if (radix_own) {
+          hist_add(sm.hist, k0, q < n2 && 2 * q < nloc, 20);
+          hist_add(sm.hist, k1, q < n2 && 2 * q + 1 < nloc, 20);
         }
       }
-      const uint32_t k0 = float_key(c0 + c2), k1 = float_key(c1 + c3);
-      if (q < n2) *reinterpret_cast<uint2*>(keys + 2 * q) = make_uint2(k0, k1);
-      if (radix_own) {
-        hist_add(sm.hist, k0, q < n2 && 2 * q < nloc, 20);
-        hist_add(sm.hist, k1, q < n2 && 2 * q + 1 < nloc, 20);
       }
-    }
     __syncthreads();
   }
   TSB_STOP_AT(5);
@@ -1973,6 +2115,7 @@ const void* decode_kernel_ptr(int D, int G, bool fast, bool lean) {
     return nullptr;
   }
 #undef TSB_K
+  if (lean) return nullptr;  // the LEAN specialisation exists for the tensor-core path only
   return reinterpret_cast<const void*>(&decode_kernel<0, 0, false, false>);
 }
 

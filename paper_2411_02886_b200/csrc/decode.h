@@ -62,6 +62,19 @@ struct SmemLayout {
   size_t ring, s, keys, frames, hist, prefix, headmax, f, scratch, bars, total;
 };
 
+// S storage modes (DecodeParams::s_in_smem): 0 spilled to global (ws_s),
+// 1 shared memory, 2 tensor memory (the LEAN kernel; keys stay in smem).
+constexpr int kSGlobal = 0, kSSmem = 1, kSTmem = 2;
+// TMEM mode: every consumer warp keeps its own stages' S fragments in its lane
+// quarter, 4 columns per stage, 128 columns per warp (4 warps per quarter).
+constexpr int kTmemColsPerWarp = 128;
+TSB_HD inline bool tmem_fits(int H_kv, int tpc) {
+  if (H_kv <= 0 || H_kv > 8 || kDecodeConsumers % H_kv) return false;
+  const int nphase = kDecodeConsumers / H_kv;
+  const int nit = (tpc + 15) / 16;
+  return (nit + nphase - 1) / nphase * 4 <= kTmemColsPerWarp;
+}
+
 TSB_HD inline SmemLayout smem_layout(int H, int row_bytes, int tpc, int s_in_smem,
                                      size_t ring_bytes = kRingBudget) {
   SmemLayout L{};
@@ -72,10 +85,12 @@ TSB_HD inline SmemLayout smem_layout(int H, int row_bytes, int tpc, int s_in_sme
   if (att > ring) ring = att;
   o += align_up(ring, 128);
   L.s = o;
-  if (s_in_smem) o += align_up(static_cast<size_t>(H) * tpc * 4, 128);
+  if (s_in_smem == kSSmem) o += align_up(static_cast<size_t>(H) * tpc * 4, 128);
   // criticality keys overwrite S row 0 in place (each thread writes the keys
-  // of the candidates whose S column it has just read)
+  // of the candidates whose S column it has just read); with S in TMEM they
+  // get their own array
   L.keys = L.s;
+  if (s_in_smem == kSTmem) o += align_up(static_cast<size_t>(tpc) * 4, 128);
   L.frames = o;  // slab row of every candidate of the CTA (TMA producer lookahead)
   o += align_up(static_cast<size_t>(tpc) * 4, 128);
   L.hist = L.ring;  // radix histogram: the ring is idle between the scan and the attention
