@@ -178,7 +178,8 @@ def _engine_pair(sa, orc, n, H, H_kv, d, k, n_init, n_local, theta, seed, kscale
     return eng, ref
 
 
-@pytest.mark.parametrize("H,H_kv,d,n,k", [(2, 2, 4, 64, 8), (8, 8, 64, 3000, 256), (32, 8, 128, 8192, 1024)])
+@pytest.mark.parametrize("H,H_kv,d,n,k", [(2, 2, 4, 64, 8), (8, 8, 64, 3000, 256), (32, 8, 128, 8192, 1024),
+                                         (28, 4, 128, 20000, 2048), (16, 2, 128, 9000, 512)])
 def test_decode_stream_vs_oracle(sa, orc, H, H_kv, d, n, k):
     eng, ref = _engine_pair(sa, orc, n, H, H_kv, d, k, 16, 32, 0.9, 100 + n)
     g = np.random.default_rng(7)
