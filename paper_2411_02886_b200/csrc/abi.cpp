@@ -322,6 +322,7 @@ struct ts_pool {
     std::vector<uint32_t> frames;
     size_t len = 0;
     int32_t* d_pt = nullptr;
+    int32_t* h_pt = nullptr;  // pinned mirror of the page table (uploads stay asynchronous)
   };
   std::unordered_map<uint32_t, Seq> seqs;
   uint32_t next_id = 0;
@@ -332,6 +333,8 @@ struct ts_pool {
   ~ts_pool() {
     for (auto& kv : seqs)
       if (kv.second.d_pt) cudaFree(kv.second.d_pt);
+    for (auto& kv : seqs)
+      if (kv.second.h_pt) cudaFreeHost(kv.second.h_pt);
     if (k_slab) cudaFree(k_slab);
     if (v_slab) cudaFree(v_slab);
     if (stream) cudaStreamDestroy(stream);
@@ -350,57 +353,54 @@ struct ts_pool {
   }
 
   // Allocates frames for t more tokens (kv_pool.cpp:63-76) and uploads the
-  // new page-table entries; returns the slab rows of the new positions.
-  std::vector<int64_t> reserve(Seq& s, size_t t, cudaStream_t st) {
+  // new page-table entries (the slab rows follow from the page table on the
+  // device).
+  void reserve(Seq& s, size_t t, cudaStream_t st) {
     const size_t frames_now = (s.len + page_size - 1) / page_size;
     const size_t frames_after = (s.len + t + page_size - 1) / page_size;
     const size_t need = frames_after - frames_now;
     if (need > free_list.size())
       fail(TS_CAPACITY, "append_kv: pool exhausted (need " + std::to_string(need) + " frames, " +
                             std::to_string(free_list.size()) + " free)");
-    std::vector<int32_t> fresh;
-    fresh.reserve(need);
     for (size_t i = 0; i < need; ++i) {
       s.frames.push_back(free_list.back());
-      fresh.push_back(static_cast<int32_t>(free_list.back()));
+      s.h_pt[frames_now + i] = static_cast<int32_t>(free_list.back());  // entries are written once per sequence
       free_list.pop_back();
     }
-    if (need) {
-      ck(cudaMemcpyAsync(s.d_pt + frames_now, fresh.data(), need * sizeof(int32_t), cudaMemcpyHostToDevice, st),
+    if (need)
+      ck(cudaMemcpyAsync(s.d_pt + frames_now, s.h_pt + frames_now, need * sizeof(int32_t), cudaMemcpyHostToDevice,
+                         st),
          "page table upload");
-      ck(cudaStreamSynchronize(st), "sync");  // `fresh` is pageable and goes out of scope
-    }
-    std::vector<int64_t> rows(t);
-    for (size_t r = 0; r < t; ++r) rows[r] = slab_row(s, s.len + r);
-    return rows;
   }
 
+  // sync = false: the caller's later work on `st` is stream-ordered after
+  // the append (the engine's prefill); the public pool API stays synchronous.
   void append(uint32_t id, const void* k, const void* v, size_t t, bool bf16, size_t* first,
-              size_t* last, cudaStream_t st) {
+              size_t* last, cudaStream_t st, bool sync = true) {
     Seq& s = state(id);
     const size_t f = s.len;
     if (first) *first = f;
     if (last) *last = f + t;
     if (t == 0) return;
-    std::vector<int64_t> rows = reserve(s, t, st);
-    int64_t* d_rows = static_cast<int64_t*>(st_a.ensure(t * sizeof(int64_t)));
-    ck(cudaMemcpyAsync(d_rows, rows.data(), t * sizeof(int64_t), cudaMemcpyHostToDevice, st), "H2D rows");
+    reserve(s, t, st);  // rows come from the page table on the device (no host round trip)
     const size_t n = t * row;
     if (bf16) {
       const uint16_t* kd = dev_in(static_cast<const uint16_t*>(k), n, st_b, st);
       const uint16_t* vd = dev_in(static_cast<const uint16_t*>(v), n, st_c, st);
-      ck(tsb::launch_kv_append(k_slab, v_slab, nullptr, nullptr, kd, vd, d_rows, static_cast<int>(t),
-                               static_cast<int>(row), st),
+      ck(tsb::launch_kv_append(k_slab, v_slab, nullptr, nullptr, kd, vd, nullptr, static_cast<int>(t),
+                               static_cast<int>(row), st, s.d_pt, static_cast<int64_t>(s.len),
+                               static_cast<int>(page_size)),
          "kv_append");
     } else {
       const float* kd = dev_in(static_cast<const float*>(k), n, st_b, st);
       const float* vd = dev_in(static_cast<const float*>(v), n, st_c, st);
-      ck(tsb::launch_kv_append(k_slab, v_slab, kd, vd, nullptr, nullptr, d_rows, static_cast<int>(t),
-                               static_cast<int>(row), st),
+      ck(tsb::launch_kv_append(k_slab, v_slab, kd, vd, nullptr, nullptr, nullptr, static_cast<int>(t),
+                               static_cast<int>(row), st, s.d_pt, static_cast<int64_t>(s.len),
+                               static_cast<int>(page_size)),
          "kv_append");
     }
     g_launches.fetch_add(1);
-    ck(cudaStreamSynchronize(st), "append sync");
+    if (sync) ck(cudaStreamSynchronize(st), "append sync");
     s.len += t;
   }
 };
@@ -636,6 +636,7 @@ ts_status ts_pool_create_sequence(ts_pool* pool, uint32_t* seq_id) {
   return guarded([&] {
     ts_pool::Seq s;
     ck(cudaMalloc(&s.d_pt, std::max<size_t>(pool->total_frames, 1) * sizeof(int32_t)), "cudaMalloc page table");
+    ck(cudaMallocHost(&s.h_pt, std::max<size_t>(pool->total_frames, 1) * sizeof(int32_t)), "cudaMallocHost page table");
     const uint32_t id = pool->next_id++;
     pool->seqs.emplace(id, std::move(s));
     *seq_id = id;
@@ -688,6 +689,7 @@ ts_status ts_pool_release(ts_pool* pool, uint32_t seq) {
       fail(TS_INVALID_ARGUMENT, "release: unknown or already released sequence " + std::to_string(seq));
     for (uint32_t f : it->second.frames) pool->free_list.push_back(f);
     if (it->second.d_pt) cudaFree(it->second.d_pt);
+    if (it->second.h_pt) cudaFreeHost(it->second.h_pt);
     pool->seqs.erase(it);
   });
 }
@@ -1321,7 +1323,7 @@ ts_status ts_engine_prefill(ts_engine* e, size_t seq, const float* q, const floa
         trace_off += ns;
       }
       // append the chunk after attending (attention.cpp:167)
-      pool.append(sid, kc, vc, len, false, nullptr, nullptr, st);
+      pool.append(sid, kc, vc, len, false, nullptr, nullptr, st, false);
     }
     ck(cudaStreamSynchronize(st), "sync");
   });

@@ -17,14 +17,18 @@ namespace tsb {
 
 namespace {
 
+// Destination slab rows: dst_rows[r], or (dst_rows == nullptr) through the
+// sequence's page table for logical positions pos0 + r.
 __global__ void kv_append_kernel(uint16_t* k_slab, uint16_t* v_slab, const float* k, const float* v,
                                  const uint16_t* kb, const uint16_t* vb, const int64_t* dst_rows,
-                                 int t, int row) {
+                                 const int32_t* pt, int64_t pos0, int page_size, int t, int row) {
   const int64_t total = static_cast<int64_t>(t) * row;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t r = i / row, c = i - (i / row) * row;
-    const int64_t off = dst_rows[r] * row + c;
+    const int64_t tok = pos0 + r;
+    const int64_t dst = dst_rows ? dst_rows[r] : static_cast<int64_t>(pt[tok / page_size]) * page_size + tok % page_size;
+    const int64_t off = dst * row + c;
     if (k) {
       k_slab[off] = __bfloat16_as_ushort(__float2bfloat16_rn(k[i]));
       v_slab[off] = __bfloat16_as_ushort(__float2bfloat16_rn(v[i]));
@@ -51,8 +55,16 @@ __global__ void kv_gather_kernel(const uint16_t* k_slab, const uint16_t* v_slab,
 __global__ void chunk_mean_kernel(const float* q, int c, int width, float* out) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= width) return;
-  double acc = 0.0;
-  for (int i = 0; i < c; ++i) acc += static_cast<double>(q[static_cast<size_t>(i) * width + j]);
+  double acc = 0.0;  // row order, as tensor.cpp:133-150 (16 loads in flight ahead of the adds)
+  int i = 0;
+  for (; i + 16 <= c; i += 16) {
+    float v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = __ldg(q + static_cast<size_t>(i + u) * width + j);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc += static_cast<double>(v[u]);
+  }
+  for (; i < c; ++i) acc += static_cast<double>(q[static_cast<size_t>(i) * width + j]);
   out[j] = static_cast<float>(acc * (1.0 / static_cast<double>(c)));
 }
 
@@ -373,11 +385,11 @@ __global__ void shard_combine_kernel(const float* o_all, const float* ml_all, in
 
 cudaError_t launch_kv_append(uint16_t* k_slab, uint16_t* v_slab, const float* k, const float* v,
                              const uint16_t* kb, const uint16_t* vb, const int64_t* dst_rows, int t,
-                             int row, cudaStream_t st) {
+                             int row, cudaStream_t st, const int32_t* pt, int64_t pos0, int page_size) {
   if (t <= 0) return cudaSuccess;
   const int64_t total = static_cast<int64_t>(t) * row;
   const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-  kv_append_kernel<<<blocks, 256, 0, st>>>(k_slab, v_slab, k, v, kb, vb, dst_rows, t, row);
+  kv_append_kernel<<<blocks, 256, 0, st>>>(k_slab, v_slab, k, v, kb, vb, dst_rows, pt, pos0, page_size, t, row);
   return cudaGetLastError();
 }
 
@@ -391,7 +403,7 @@ cudaError_t launch_kv_gather(const uint16_t* k_slab, const uint16_t* v_slab, con
 }
 
 cudaError_t launch_chunk_mean(const float* q, int c, int width, float* out, cudaStream_t st) {
-  chunk_mean_kernel<<<(width + 127) / 128, 128, 0, st>>>(q, c, width, out);
+  chunk_mean_kernel<<<(width + 31) / 32, 32, 0, st>>>(q, c, width, out);  // spread over the SMs
   return cudaGetLastError();
 }
 

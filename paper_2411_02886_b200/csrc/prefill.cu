@@ -4,8 +4,8 @@
 // attends every merged cached row (init U selected U local windows, gathered
 // through the page table) and the chunk's own rows j <= i (causal, :83).
 //
-// One CTA = 16 chunk rows x the G query heads sharing KV head g (h mod H_kv,
-// :78); one warp per head (G <= 8 warps). Per key tile of 64 rows:
+// One CTA = 32 (or 16) chunk rows x the G query heads sharing KV head g
+// (h mod H_kv, :78); one warp per (head, 16-row tile). Per key tile of 32 rows:
 //   S = Q K^T   mma.sync m16n8k16 bf16 -> fp32; Q (fp32) split exactly into
 //               three bf16 parts; cached K is bf16 (exact); the chunk's own K
 //               (fp32 in the reference) is split into three parts as well, so
@@ -14,7 +14,8 @@
 //   O += P V    P split into three bf16 parts (A from the S accumulators,
 //               FA2 register reuse), V^T via ldmatrix.trans; chunk V split too
 // Cached K/V slices (d wide, this KV head) arrive by 16-byte cp.async into
-// padded rows (ldmatrix conflict-free), double-buffered, 32 keys per tile.
+// padded rows (ldmatrix conflict-free), double-buffered (the next tile's
+// gather is in flight while this one is computed), 32 keys per tile.
 #include <cfloat>
 #include <cmath>
 
@@ -28,7 +29,6 @@ namespace {
 constexpr int kPD = 128;          // head dim of the tensor-core path
 constexpr int kPRS = kPD + 8;     // padded smem row (bf16 elements)
 constexpr int kPKT = 32;          // keys per tile
-constexpr int kPQ = 16;           // chunk rows per CTA (one m16 tile)
 constexpr int kPMaxG = 8;
 
 __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -176,13 +176,22 @@ __global__ void split3_kernel(const float* __restrict__ x, int n, uint16_t* __re
   }
 }
 
-__global__ void __launch_bounds__(kPMaxG * 32) prefill_flash_kernel(PrefillAttendParams p, const uint16_t* kc3,
-                                                                    const uint16_t* vc3) {
+// One CTA = kPQ (32) chunk rows x the G query heads of KV head g; warp w
+// takes head w % G and the 16-row tile w / G. The merged cached rows' slab
+// rows are resolved once per CTA (att list -> page table) into shared memory,
+// and the 32-key K/V tiles are double-buffered: tile t + 1's cp.async gather
+// is in flight while tile t is computed.
+constexpr int kPRowsMax = 4096;  // merged cached rows resolved up front (else per tile)
+
+template <int kPQ>  // chunk rows per CTA: 32 (two m16 tiles) when the smem fits, else 16
+__global__ void __launch_bounds__(256) prefill_flash_kernel(PrefillAttendParams p, const uint16_t* kc3,  // <= 8 warps (rq 32: G <= 4)
+                                                                        const uint16_t* vc3) {
   extern __shared__ __align__(128) uint8_t psm_raw[];
   const int G = p.H / p.H_kv;
   const int g = blockIdx.y;
   const int i0 = blockIdx.x * kPQ;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp % G, wt = warp / G;  // head, 16-row tile
   const int nthr = blockDim.x;
   const int row_elems = p.H_kv * kPD;
   const int n_cached = p.n_att_ptr ? *p.n_att_ptr : p.n_att;
@@ -191,12 +200,19 @@ __global__ void __launch_bounds__(kPMaxG * 32) prefill_flash_kernel(PrefillAtten
   const int n_tiles = nct + (n_cur + kPKT - 1) / kPKT;
   const size_t qbytes = static_cast<size_t>(3) * G * kPQ * kPRS * 2;
   const size_t tbytes = static_cast<size_t>(3) * kPKT * kPRS * 2;
-  uint16_t* sq = reinterpret_cast<uint16_t*>(psm_raw);                 // [3][G*16][kPRS]
-  uint16_t* kb = reinterpret_cast<uint16_t*>(psm_raw + qbytes);        // [3][32][kPRS]
-  uint16_t* vb = reinterpret_cast<uint16_t*>(psm_raw + qbytes + tbytes);
-  int32_t* rows = reinterpret_cast<int32_t*>(psm_raw + qbytes + 2 * tbytes);  // [32]
+  uint16_t* sq = reinterpret_cast<uint16_t*>(psm_raw);  // [3][G * kPQ][kPRS], row = head * kPQ + i
+  uint16_t* kbuf[2] = {reinterpret_cast<uint16_t*>(psm_raw + qbytes), reinterpret_cast<uint16_t*>(psm_raw + qbytes + 2 * tbytes)};
+  uint16_t* vbuf[2] = {reinterpret_cast<uint16_t*>(psm_raw + qbytes + tbytes),
+                       reinterpret_cast<uint16_t*>(psm_raw + qbytes + 3 * tbytes)};
+  int32_t* rows_all = reinterpret_cast<int32_t*>(psm_raw + qbytes + 4 * tbytes);  // [kPRowsMax]
+  const bool rows_up_front = n_cached <= kPRowsMax;
+  auto lookup = [&](int key) -> int32_t {
+    const uint32_t tok = p.att[key];
+    return p.page_size == 1 ? p.page_table[tok]
+                            : p.page_table[tok / p.page_size] * p.page_size + static_cast<int32_t>(tok % p.page_size);
+  };
 
-  // ---- Q parts: row (m, i) = q[i0 + i][(g + m*H_kv) * d + :]
+  // ---- Q parts: row (m, i) = q[i0 + i][(g + m*H_kv) * d + :]; slab rows of the cached keys
   for (int idx = threadIdx.x; idx < G * kPQ * kPD; idx += nthr) {
     const int r = idx / kPD, t = idx - (idx / kPD) * kPD;
     const int m = r / kPQ, i = r - (r / kPQ) * kPQ;
@@ -207,37 +223,22 @@ __global__ void __launch_bounds__(kPMaxG * 32) prefill_flash_kernel(PrefillAtten
     sq[(1 * G * kPQ + r) * kPRS + t] = bf(mm);
     sq[(2 * G * kPQ + r) * kPRS + t] = bf(l);
   }
+  if (rows_up_front)
+    for (int key = threadIdx.x; key < n_cached; key += nthr) rows_all[key] = lookup(key);
+  __syncthreads();
 
-  float o[kPD / 8][4];
-#pragma unroll
-  for (int n = 0; n < kPD / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
-  const int r_lo = lane >> 2;  // fragment rows r_lo, r_lo + 8 of this warp's 16
-  const uint32_t qbase = smem_u32(sq) +
-                         static_cast<uint32_t>(((warp * kPQ + (lane & 7) + ((lane >> 3) & 1) * 8) * kPRS + (lane >> 4) * 8) * 2);
-  const uint32_t qpart = static_cast<uint32_t>(G * kPQ * kPRS * 2);
   constexpr int CPR = kPD * 2 / 16;  // 16-byte chunks per row slice
-
-  for (int tile = 0; tile < n_tiles; ++tile) {
-    const bool chunk_tile = tile >= nct;
-    __syncthreads();  // previous tile consumed (and Q written)
-    if (!chunk_tile) {
+  auto issue = [&](int tile, int b) {
+    uint16_t* kb = kbuf[b];
+    uint16_t* vb = vbuf[b];
+    if (tile < nct) {
       const int k0 = tile * kPKT;
-      for (int r = threadIdx.x; r < kPKT; r += nthr) {
-        const int key = k0 + r;
-        int32_t ri = -1;
-        if (key < n_cached) {
-          const uint32_t tok = p.att[key];
-          ri = p.page_size == 1 ? p.page_table[tok]
-                                : p.page_table[tok / p.page_size] * p.page_size + static_cast<int32_t>(tok % p.page_size);
-        }
-        rows[r] = ri;
-      }
-      __syncthreads();
       for (int idx = threadIdx.x; idx < kPKT * CPR; idx += nthr) {
         const int r = idx / CPR, c = idx - (idx / CPR) * CPR;
-        if (rows[r] >= 0) {
-          const int64_t off = static_cast<int64_t>(rows[r]) * row_elems + static_cast<int64_t>(g) * kPD + c * 8;
+        const int key = k0 + r;
+        const int32_t ri = key < n_cached ? (rows_up_front ? rows_all[key] : lookup(key)) : -1;
+        if (ri >= 0) {
+          const int64_t off = static_cast<int64_t>(ri) * row_elems + static_cast<int64_t>(g) * kPD + c * 8;
           cp_async16(kb + r * kPRS + c * 8, p.k_slab + off);
           cp_async16(vb + r * kPRS + c * 8, p.v_slab + off);
         } else {  // padding row: zero (P is zero there; keep 0 * V finite)
@@ -265,21 +266,42 @@ __global__ void __launch_bounds__(kPMaxG * 32) prefill_flash_kernel(PrefillAtten
       }
     }
     cp_async_commit();
-    cp_async_wait<0>();
+  };
+
+  float o[kPD / 8][4];
+#pragma unroll
+  for (int n = 0; n < kPD / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+  const int r_lo = lane >> 2;  // fragment rows r_lo, r_lo + 8 of this warp's 16
+  const uint32_t qbase = smem_u32(sq) + static_cast<uint32_t>(
+                             ((wm * kPQ + wt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * kPRS + (lane >> 4) * 8) * 2);
+  const uint32_t qpart = static_cast<uint32_t>(G * kPQ * kPRS * 2);
+  const int i_lo = i0 + wt * 16 + r_lo;
+
+  if (n_tiles > 0) issue(0, 0);
+  for (int tile = 0; tile < n_tiles; ++tile) {
+    if (tile + 1 < n_tiles) {
+      issue(tile + 1, (tile + 1) & 1);  // that buffer's tile (tile - 1) was consumed before the last barrier
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     __syncthreads();
-    if (chunk_tile)
-      flash_tile<3>(qbase, qpart, kb, vb, p.scale, lane, true, (tile - nct) * kPKT, n_cur, i0 + r_lo, o, mrow, lrow);
+    const int b = tile & 1;
+    if (tile >= nct)
+      flash_tile<3>(qbase, qpart, kbuf[b], vbuf[b], p.scale, lane, true, (tile - nct) * kPKT, n_cur, i_lo, o, mrow,
+                    lrow);
     else
-      flash_tile<1>(qbase, qpart, kb, vb, p.scale, lane, false, tile * kPKT, n_cached, 0, o, mrow, lrow);
+      flash_tile<1>(qbase, qpart, kbuf[b], vbuf[b], p.scale, lane, false, tile * kPKT, n_cached, 0, o, mrow, lrow);
+    __syncthreads();  // buffer b is free for tile + 2
   }
-  // ---- normalise and store rows r_lo, r_lo + 8 of head m = warp
-  const int m = warp;
+  // ---- normalise and store rows r_lo, r_lo + 8 of head wm, tile wt
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const int i = i0 + r_lo + h * 8;
+    const int i = i_lo + h * 8;
     if (i >= p.C) continue;
     const float inv = 1.f / lrow[h];
-    float* orow = p.out + static_cast<size_t>(i) * p.H * kPD + (g + m * p.H_kv) * kPD;
+    float* orow = p.out + static_cast<size_t>(i) * p.H * kPD + (g + wm * p.H_kv) * kPD;
 #pragma unroll
     for (int n = 0; n < kPD / 8; ++n) {
       const int t = n * 8 + (lane & 3) * 2;
@@ -290,28 +312,34 @@ __global__ void __launch_bounds__(kPMaxG * 32) prefill_flash_kernel(PrefillAtten
 
 }  // namespace
 
-size_t prefill_flash_smem(int G) {
-  return static_cast<size_t>(3) * G * kPQ * kPRS * 2 + static_cast<size_t>(2) * 3 * kPKT * kPRS * 2 + kPKT * 4;
+size_t prefill_flash_smem(int G, int rq) {
+  return static_cast<size_t>(3) * G * rq * kPRS * 2 + static_cast<size_t>(4) * 3 * kPKT * kPRS * 2 + kPRowsMax * 4;
 }
 
 cudaError_t launch_prefill_flash(const PrefillAttendParams& p, cudaStream_t st) {
   const int G = p.H / p.H_kv;
   if (p.d != kPD || G > kPMaxG || p.page_size < 1 || !p.split_ws) return cudaErrorInvalidValue;
-  const size_t smem = prefill_flash_smem(G);
-  static size_t set = 0;
-  if (smem > set) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_flash_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int rq = (G <= 4 && prefill_flash_smem(G, 32) <= static_cast<size_t>(optin)) ? 32 : 16;  // <= 8 warps
+  const size_t smem = prefill_flash_smem(G, rq);
+  const void* fn = rq == 32 ? reinterpret_cast<const void*>(&prefill_flash_kernel<32>)
+                            : reinterpret_cast<const void*>(&prefill_flash_kernel<16>);
+  static size_t set[2] = {0, 0};
+  if (smem > set[rq == 32]) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    set = smem;
+    set[rq == 32] = smem;
   }
   const int n = p.C * p.H_kv * kPD;
   uint16_t* kc3 = p.split_ws;
   uint16_t* vc3 = p.split_ws + 3 * static_cast<size_t>(n);
   split3_kernel<<<148, 512, 0, st>>>(p.k_cur, n, kc3);
   split3_kernel<<<148, 512, 0, st>>>(p.v_cur, n, vc3);
-  dim3 grid((p.C + kPQ - 1) / kPQ, p.H_kv);
-  prefill_flash_kernel<<<grid, G * 32, smem, st>>>(p, kc3, vc3);
+  dim3 grid((p.C + rq - 1) / rq, p.H_kv);
+  if (rq == 32) prefill_flash_kernel<32><<<grid, G * 2 * 32, smem, st>>>(p, kc3, vc3);
+  else prefill_flash_kernel<16><<<grid, G * 32, smem, st>>>(p, kc3, vc3);
   return cudaGetLastError();
 }
 
