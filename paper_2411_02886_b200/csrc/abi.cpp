@@ -3,6 +3,7 @@
 // selection / attention entry points, all launching the sm_100a kernels in
 // decode.cu and aux.cu. Validation happens before any device work and
 // reports the reference's exception type + message (see tokenselect.h).
+#include <cuda.h>  // CUtensorMap (the encoder is fetched through the runtime's driver entry point)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -40,6 +41,8 @@ const bool g_force_global_s = std::getenv("TS_FORCE_GLOBAL_S") != nullptr && std
 const int g_debug_flags = std::getenv("TS_DEBUG_FLAGS") ? std::atoi(std::getenv("TS_DEBUG_FLAGS")) : 0;
 const bool g_force_cuda_core_prefill = std::getenv("TS_CUDA_CORE_PREFILL") != nullptr;
 const bool g_no_lean = std::getenv("TS_NO_LEAN") != nullptr;  // dev: always the general kernel
+const bool g_no_tma = std::getenv("TS_NO_TMA") != nullptr;      // dev: row-by-row scan copies
+const bool g_debug_tma = std::getenv("TS_DEBUG_TMA") != nullptr;
 std::atomic<uint64_t> g_launches{0};
 constexpr size_t kTraceSlots = tsb::kTraceStride * 1024;
 // host-side profile of the decode launch path (TS_HOST_PROF=1): ns per stage
@@ -183,6 +186,41 @@ struct Workspace {
   }
 };
 
+// TMA tensor map of a K slab for the scan: the slab viewed as
+// [128-B chunk][slab row][64 bf16] (strides: the row, 128 B per chunk), box =
+// 16 rows x the whole row, 128B swizzle keyed by the row
+// (tools/ubench/tmap.cu). nullptr when the row is not a whole number of 128-B
+// chunks or the encoder is unavailable.
+using TmapEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+void* encode_k_tmap(uint16_t* slab, size_t rows, size_t row_bytes, cudaStream_t st) {
+  if (row_bytes % 128 || row_bytes / 128 > 256 || rows < 16 || rows >= (1ull << 32) || g_no_tma) return nullptr;
+  static TmapEncodeFn enc = []() {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    const cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+    if (g_debug_tma) std::fprintf(stderr, "[tokenselect] cuTensorMapEncodeTiled entry point: %d / %d\n", int(e), int(q));
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess) return static_cast<TmapEncodeFn>(nullptr);
+    return reinterpret_cast<TmapEncodeFn>(f);
+  }();
+  if (!enc) return nullptr;
+  alignas(64) CUtensorMap m;
+  const cuuint64_t dims[3] = {64, rows, row_bytes / 128};
+  const cuuint64_t strides[2] = {row_bytes, 128};
+  const cuuint32_t box[3] = {64, 16, static_cast<cuuint32_t>(row_bytes / 128)};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, slab, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (g_debug_tma) std::fprintf(stderr, "[tokenselect] K tensor map encode: %d\n", int(r));
+  if (r != CUDA_SUCCESS) return nullptr;
+  void* d = nullptr;
+  ck(cudaMalloc(&d, sizeof(CUtensorMap)), "cudaMalloc tensor map");
+  ck(cudaMemcpyAsync(d, &m, sizeof(CUtensorMap), cudaMemcpyHostToDevice, st), "H2D tensor map");
+  ck(cudaStreamSynchronize(st), "sync");
+  return d;
+}
+
 struct Plan {
   int ctas_per_seq, tpc, s_in_smem, ring_bytes, att_bytes;
   size_t smem;
@@ -206,7 +244,8 @@ Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows, bool 
   int c = (base + 63) / 64;
   c = std::max(1, std::min(c, std::max(1, di.num_sms / n_seq)));
   pl.ctas_per_seq = c;
-  pl.tpc = static_cast<int>(tsb::align_up(static_cast<size_t>(std::max(1, (max_T + c - 1) / c)), 4));  // 16-B rows
+  // 16 candidates: 16-B S rows, and whole 16-token scan stages per CTA (TMA)
+  pl.tpc = static_cast<int>(tsb::align_up(static_cast<size_t>(std::max(1, (max_T + c - 1) / c)), 16));
   const int row_bytes = H_kv * d * 2;
   // dynamic shared memory left next to the kernel's static allocation
   cudaFuncAttributes fa{};
@@ -280,6 +319,16 @@ void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t 
   p.bar_slot = (ws.launches & 1u) ? 32 : 0;  // launches on one workspace are stream-ordered
   p.prefetch_stages = g_prefetch_stages;
   p.ring_bytes = lean ? pl.lean_ring_bytes : pl.ring_bytes;
+  // whole-stage TMA (general kernel): the kernel checks per stage that its
+  // 16 slab rows are consecutive (ascending or descending) and else copies rows
+  p.scan_tma = !lean && p.k_tmap ? 1 : 0;
+  if (g_debug_tma) {
+    static std::atomic<int> once{0};
+    if (once.fetch_add(1) < 4)
+      std::fprintf(stderr, "[tokenselect] launch: lean %d, k_tmap %p, scan_tma %d (page %d, tpc %d, cand_begin %d, cand %p)\n",
+                   int(lean), p.k_tmap, p.scan_tma, p.page_size, pl.tpc, p.seqs[0].cand_begin,
+                   static_cast<const void*>(p.seqs[0].cand));
+  }
   p.att_bytes = lean ? pl.lean_att_bytes : pl.att_bytes;
   p.debug_flags = g_debug_flags;
   // the dynamic shared-memory limit is set once per kernel (largest request so far)
@@ -317,6 +366,7 @@ struct ts_pool {
   size_t page_size = 1, H_kv = 0, d = 0, row = 0, total_frames = 0;
   uint16_t* k_slab = nullptr;
   uint16_t* v_slab = nullptr;
+  void* k_tmap = nullptr;  // device CUtensorMap over the K slab (scan stages in one TMA op), or nullptr
   std::vector<uint32_t> free_list;
   struct Seq {
     std::vector<uint32_t> frames;
@@ -337,6 +387,7 @@ struct ts_pool {
       if (kv.second.h_pt) cudaFreeHost(kv.second.h_pt);
     if (k_slab) cudaFree(k_slab);
     if (v_slab) cudaFree(v_slab);
+    if (k_tmap) cudaFree(k_tmap);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -479,6 +530,7 @@ void check_method_supported(int m) {
 DecodeParams base_params(const ts_pool* pool, int H, int H_kv, int d, int k, int method, int mode) {
   DecodeParams p{};
   p.k_slab = pool ? pool->k_slab : nullptr;
+  p.k_tmap = pool ? pool->k_tmap : nullptr;
   p.v_slab = pool ? pool->v_slab : nullptr;
   p.k_slab_w = pool ? pool->k_slab : nullptr;
   p.v_slab_w = pool ? pool->v_slab : nullptr;
@@ -622,6 +674,7 @@ ts_status ts_pool_create(size_t capacity_tokens, size_t page_size, size_t num_kv
     ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "stream");
     ck(cudaMemsetAsync(p->k_slab, 0, elems * 2, p->stream), "memset");
     ck(cudaMemsetAsync(p->v_slab, 0, elems * 2, p->stream), "memset");
+    p->k_tmap = encode_k_tmap(p->k_slab, p->total_frames * page_size, p->row * 2, p->stream);
     p->free_list.resize(p->total_frames);
     // highest frame handed out first (kv_pool.cpp:24-27)
     for (size_t i = 0; i < p->total_frames; ++i) p->free_list[i] = static_cast<uint32_t>(i);

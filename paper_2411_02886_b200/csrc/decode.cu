@@ -306,6 +306,7 @@ __device__ int cache_decision(const SeqDesc& sd, int width, const DecisionLoads&
 // --------------------------------------------------------------- the scan
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kScratchTmem = 250;  // sm.scratch word holding the TMEM base address
+constexpr int kScratchStageMode = 200;  // sm.scratch words [200, 216): the scan ring's per-slot layout
 constexpr size_t kCritPartOffset = 64 * 1024;  // TMEM mode: per-kv-head criticality partials in the ring
 constexpr int kLeanMode = kModeSelect | kModeScore | kModeCache | kModeAttend | kModeAppend;
 // Fast path (sm_100a tensor cores, mma.sync bf16 -> fp32). The K rows of a
@@ -366,7 +367,15 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
   const int Hkv = p.H_kv;
   const int row_bytes = Hkv * D * 2;
   const int rstride = row_bytes + 16;  // padded ring row (ldmatrix conflict-free)
-  const ScanGeom geom = scan_geom(p.H, p.H_kv, D, p.ring_bytes);
+  // whole stages through the tensor map where a stage's 16 rows are
+  // consecutive slab rows, ascending or descending (page_size 1 pools hand
+  // out frames downwards), else row copies; the general kernel only (TM /
+  // LEAN keeps the row copies, whose code is smaller). Slots are 1024-B
+  // aligned (swizzle atoms) and hold either layout; smode[slot] says which.
+  const bool tma = !TM && p.scan_tma != 0 && (smem_u32(sm.ring) & 1023u) == 0;
+  const ScanGeom geom = scan_geom(p.H, p.H_kv, D, p.ring_bytes, tma);
+  const int sbytes = static_cast<int>(scan_stage_bytes(row_bytes, tma));
+  volatile uint32_t* smode = sm.scratch + kScratchStageMode;  // [kMaxStages]: 0 rows, 1 ascending, 2 descending
   const int R = geom.rows;  // 16 tokens per stage
   const int kStages = geom.stages;
   const int nit = (nloc + R - 1) / R;
@@ -396,11 +405,32 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
         ph_prev = ph_prev + 1 == nph ? 0 : ph_prev + 1;
       }
       uint64_t* fb = &sm.full[ph * kStages + s];
-      if (lane == 0) mbar_arrive_expect_tx(fb, static_cast<uint32_t>(nrows * row_bytes));
-      __syncwarp();
-      if (lane < nrows)
-        bulk_g2s(sm.ring + static_cast<size_t>(s * R + lane) * rstride,
-                 kbase + static_cast<size_t>(sm.frames[rbase + lane]) * row_bytes, row_bytes, fb, pol);
+      int mode = 0;
+      if (tma) {
+        const int32_t f0 = sm.frames[rbase];
+        const int32_t fl = lane < nrows ? sm.frames[rbase + lane] : f0;
+        mode = __all_sync(0xffffffffu, lane >= nrows || fl == f0 + lane) ? 1
+               : __all_sync(0xffffffffu, lane >= nrows || fl == f0 - lane) ? 2 : 0;
+      }
+      if (mode) {
+        // one op for the 16 rows (a partial stage loads its neighbours, or
+        // zero fill outside the slab, unused)
+        if (lane == 0) {
+          smode[s] = static_cast<uint32_t>(mode);
+          mbar_arrive_expect_tx(fb, static_cast<uint32_t>(R * row_bytes));
+          const int32_t f0 = sm.frames[rbase];
+          tma_load_3d(sm.ring + static_cast<size_t>(s) * sbytes, p.k_tmap, 0, mode == 1 ? f0 : f0 - (R - 1), 0, fb, pol);
+        }
+      } else {
+        if (lane == 0) {
+          smode[s] = 0u;
+          mbar_arrive_expect_tx(fb, static_cast<uint32_t>(nrows * row_bytes));
+        }
+        __syncwarp();
+        if (lane < nrows)
+          bulk_g2s(sm.ring + static_cast<size_t>(s) * sbytes + static_cast<size_t>(lane) * rstride,
+                   kbase + static_cast<size_t>(sm.frames[rbase + lane]) * row_bytes, row_bytes, fb, pol);
+      }
       s = s + 1 == kStages ? 0 : s + 1;
       ph = ph + 1 == nph ? 0 : ph + 1;
     }
@@ -445,17 +475,27 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
   const uint32_t lrow = static_cast<uint32_t>((lane & 7) + ((lane >> 3) & 1) * 8);
   const uint32_t lcol = static_cast<uint32_t>((lane >> 4) * 16 + kvh * D * 2);
   const uint32_t ring_base = smem_u32(sm.ring) + lrow * rstride + lcol;
+  // tensor-map layout: line z*16 + box row holds 128-B chunk z of that
+  // row, its 16-B units XOR-swizzled with (box row & 7); this lane's ldmatrix
+  // row is token lrow (box row lrow, or 15 - lrow for a descending stage),
+  // k half lane / 16 of each 16-wide k chunk
+  const int e0 = kvh * D + (lane >> 4) * 8;  // element of the row at kc = 0
   int s = phase % kStages, r = 0;  // this warp's slot and stage count
   for (int it = phase; it < nit; it += nphase, ++r) {
     mbar_wait(&sm.full[phase * kStages + s], (fparity >> s) & 1u);
     fparity ^= 1u << s;
     float c[4] = {0.f, 0.f, 0.f, 0.f};
     {
-      const uint32_t abase = ring_base + static_cast<uint32_t>(s * R * rstride);
+      const uint32_t abase = ring_base + static_cast<uint32_t>(s * sbytes);
+      const uint32_t tbase_s = smem_u32(sm.ring) + static_cast<uint32_t>(s * sbytes);
+      const uint32_t mode = tma ? smode[s] : 0u;
+      const int br = mode == 2 ? 15 - static_cast<int>(lrow) : static_cast<int>(lrow);
 #pragma unroll
       for (int kc = 0; kc < KC; ++kc) {
         uint32_t a[4];
-        ldmatrix_x4(a, abase + kc * 32);
+        const int e = e0 + kc * 16;
+        ldmatrix_x4(a, mode ? tbase_s + static_cast<uint32_t>(((e >> 6) * 16 + br) * 128 + ((((e >> 3) & 7) ^ (br & 7)) << 4))
+                            : abase + kc * 32);
         mma_bf16_16816(c, a, bq[kc][0][0], bq[kc][0][1]);
         mma_bf16_16816(c, a, bq[kc][1][0], bq[kc][1][1]);
         mma_bf16_16816(c, a, bq[kc][2][0], bq[kc][2][1]);
@@ -1327,7 +1367,7 @@ __device__ __noinline__ void softmax_partials(float* Sbuf, int sstride, int nloc
 // branch count are their latency.
 template <int D, int G, bool FAST, bool LEAN>
 __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeParams p) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];  // TMA 128B-swizzle atoms (checked: else row copies)
   const Smem sm = carve(smem_raw, p);
   const int cta = blockIdx.x;
   const int nblocks = gridDim.x;

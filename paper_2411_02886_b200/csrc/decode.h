@@ -40,13 +40,20 @@ struct ScanGeom {
   int stages;   // ring depth
 };
 
-TSB_HD inline ScanGeom scan_geom(int H, int H_kv, int d, size_t ring_bytes = kRingBudget) {
+// Stage bytes: padded rows (row-by-row bulk copies), or with the tensor map a
+// slot that takes either those or 16 dense swizzled rows.
+TSB_HD inline size_t scan_stage_bytes(int row_bytes, bool tma) {
+  // with the tensor map a slot holds either layout, at a 1024-B aligned stride
+  return tma ? align_up(static_cast<size_t>(16) * (row_bytes + 16), 1024) : static_cast<size_t>(16) * (row_bytes + 16);
+}
+
+TSB_HD inline ScanGeom scan_geom(int H, int H_kv, int d, size_t ring_bytes = kRingBudget, bool tma = false) {
   ScanGeom g{0, 0, 0};
   if (H_kv <= 0 || H % H_kv != 0) return g;
   const int G = H / H_kv;
   if (!(d == 128 || d == 64) || G > 8 || G < 1) return g;
   if (H_kv > kDecodeConsumers || kDecodeConsumers % H_kv != 0) return g;
-  const size_t stage = static_cast<size_t>(16) * (H_kv * d * 2 + 16);
+  const size_t stage = scan_stage_bytes(H_kv * d * 2, tma);
   int stages = static_cast<int>(ring_bytes / stage);
   if (stages > kMaxStages) stages = kMaxStages;
   const int nphase = kDecodeConsumers / H_kv;

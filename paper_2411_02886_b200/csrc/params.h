@@ -107,6 +107,13 @@ struct DecodeParams {
   int debug_flags;             // dev experiments: bit0 = scan consumers skip the math
   unsigned long long* trace;   // optional [32] %globaltimer phase stamps (CTA 0)
   SeqDesc seqs[kMaxSeqPerLaunch];  // passed by value in the kernel parameter space
+  // (kept last: the fields above keep their constant-bank offsets)
+  // TMA tensor map (device memory) viewing the K slab as [128-B chunk][slab
+  // row][64 bf16] with the 128B swizzle: one op brings a whole 16-row stage
+  // (abi.cpp, encode_k_tmap); used by the general kernel when every stage is
+  // 16 consecutive slab rows. nullptr: row-by-row copies.
+  const void* k_tmap;
+  int scan_tma;
 };
 
 }  // namespace tsb
