@@ -1338,18 +1338,26 @@ __device__ __noinline__ void softmax_partials(float* Sbuf, int sstride, int nloc
     float4* sr = reinterpret_cast<float4*>(Sbuf + static_cast<size_t>(h) * sstride);
     float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
     if (m > -INFINITY) {
-      // S <- e^(S - m) in place (the soft vote then needs FMAs only)
-      for (int q = lane; q < n4; q += 32) {
-        float4 v = sr[q];
-        v.x = ex2_approx(fmaf(v.x, kLog2e, -ml));
-        v.y = ex2_approx(fmaf(v.y, kLog2e, -ml));
-        v.z = ex2_approx(fmaf(v.z, kLog2e, -ml));
-        v.w = ex2_approx(fmaf(v.w, kLog2e, -ml));
-        sr[q] = v;
-        z0 += v.x;
-        z1 += v.y;
-        z2 += v.z;
-        z3 += v.w;
+      // S <- e^(S - m) in place (the soft vote then needs FMAs only); four
+      // float4 per lane in flight (S may be spilled to global memory)
+      for (int q0 = lane; q0 < n4; q0 += 4 * 32) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (q0 + u * 32 < n4) v[u] = sr[q0 + u * 32];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (q0 + u * 32 < n4) {
+            v[u].x = ex2_approx(fmaf(v[u].x, kLog2e, -ml));
+            v[u].y = ex2_approx(fmaf(v[u].y, kLog2e, -ml));
+            v[u].z = ex2_approx(fmaf(v[u].z, kLog2e, -ml));
+            v[u].w = ex2_approx(fmaf(v[u].w, kLog2e, -ml));
+            sr[q0 + u * 32] = v[u];
+            z0 += v[u].x;
+            z1 += v[u].y;
+            z2 += v[u].z;
+            z3 += v[u].w;
+          }
       }
     }
     const float z = warp_sum((z0 + z1) + (z2 + z3));
@@ -1830,6 +1838,19 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
         if (q < n2) {
           const float* s2 = Sbuf + 2 * q;
           int h = 0;
+          for (; h + 7 < H; h += 8) {  // eight loads in flight (S may be spilled to global memory)
+            float2 a[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h + u) * sstride);
+#pragma unroll
+            for (int u = 0; u < 8; u += 2) {
+              const float fa = soft ? ml[h + u] : 1.f, fb = soft ? ml[h + u + 1] : 1.f;
+              c0 = fmaf(a[u].x, fa, c0);
+              c1 = fmaf(a[u].y, fa, c1);
+              c2 = fmaf(a[u + 1].x, fb, c2);
+              c3 = fmaf(a[u + 1].y, fb, c3);
+            }
+          }
           for (; h + 1 < H; h += 2) {
             const float2 a = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h) * sstride);
             const float2 b = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h + 1) * sstride);
