@@ -322,6 +322,11 @@ void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t 
   // whole-stage TMA (general kernel): the kernel checks per stage that its
   // 16 slab rows are consecutive (ascending or descending) and else copies rows
   p.scan_tma = !lean && p.k_tmap ? 1 : 0;
+  p.any_select = p.any_radix = 0;
+  for (int b = 0; b < p.n_seq; ++b) {
+    p.any_select |= p.seqs[b].select;
+    p.any_radix |= p.seqs[b].select && p.seqs[b].n_cand > p.k;
+  }
   if (g_debug_tma) {
     static std::atomic<int> once{0};
     if (once.fetch_add(1) < 4)

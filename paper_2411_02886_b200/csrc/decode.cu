@@ -1514,10 +1514,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     any_select = own == 1;
     any_radix = do_select && own == 1 && T > p.k;
   } else {
-    for (int b = 0; b < n_seq; ++b) {
-      any_select |= p.seqs[b].select;
-      any_radix |= do_select && p.seqs[b].select && p.seqs[b].n_cand > p.k;
-    }
+    // (host-computed: a loop over the sequences' descriptors would be a chain
+    // of dynamically indexed constant-bank loads)
+    any_select = p.any_select;
+    any_radix = do_select && p.any_radix;
   }
   if (by_page) {
     if (tid < npg) sm.prefix[tid] = pg_pre;
@@ -1533,8 +1533,19 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       const int jl = tid + u * blockDim.x;
       if (may_scan && jl < nloc) sm.frames[jl] = fr_pre[u];
     }
-    for (int jl = tid + 4 * blockDim.x; may_scan && jl < nloc; jl += blockDim.x)
-      sm.frames[jl] = static_cast<int32_t>(row_index<LEAN>(sd, cand_at<LEAN>(sd, j0 + jl), p.page_size));
+    // long ranges (page size 1, > 4 candidates per thread): eight page-table
+    // loads in flight per thread
+    for (int jb = tid + 4 * blockDim.x; may_scan && jb < nloc; jb += 8 * blockDim.x) {
+      int32_t fr[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int jl = jb + u * blockDim.x;
+        fr[u] = jl < nloc ? static_cast<int32_t>(row_index<LEAN>(sd, cand_at<LEAN>(sd, j0 + jl), p.page_size)) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (jb + u * static_cast<int>(blockDim.x) < nloc) sm.frames[jb + u * blockDim.x] = fr[u];
+    }
   }
   if (do_select && own == 1 && T > p.k) {
     uint32_t* gh = p.ws_hist + static_cast<size_t>(seq_id) * 2 * kHistPass;

@@ -114,6 +114,8 @@ struct DecodeParams {
   // 16 consecutive slab rows. nullptr: row-by-row copies.
   const void* k_tmap;
   int scan_tma;
+  int any_select;  // some sequence of the launch selects (seqs[b].select)
+  int any_radix;   // some selecting sequence has more candidates than k
 };
 
 }  // namespace tsb
