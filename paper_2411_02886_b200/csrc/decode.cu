@@ -1533,17 +1533,17 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       const int jl = tid + u * blockDim.x;
       if (may_scan && jl < nloc) sm.frames[jl] = fr_pre[u];
     }
-    // long ranges (page size 1, > 4 candidates per thread): eight page-table
+    // long ranges (page size 1, > 4 candidates per thread): sixteen page-table
     // loads in flight per thread
-    for (int jb = tid + 4 * blockDim.x; may_scan && jb < nloc; jb += 8 * blockDim.x) {
-      int32_t fr[8];
+    for (int jb = tid + 4 * blockDim.x; may_scan && jb < nloc; jb += 16 * blockDim.x) {
+      int32_t fr[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 16; ++u) {
         const int jl = jb + u * blockDim.x;
         fr[u] = jl < nloc ? static_cast<int32_t>(row_index<LEAN>(sd, cand_at<LEAN>(sd, j0 + jl), p.page_size)) : 0;
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < 16; ++u)
         if (jb + u * static_cast<int>(blockDim.x) < nloc) sm.frames[jb + u * blockDim.x] = fr[u];
     }
   }
