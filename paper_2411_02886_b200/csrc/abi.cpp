@@ -33,10 +33,6 @@ using tsb::SeqDesc;
 namespace {
 
 thread_local std::string g_err;
-int g_prefetch_stages = [] {
-  const char* e = std::getenv("TS_PREFETCH_STAGES");
-  return e ? std::atoi(e) : 0;
-}();
 const bool g_force_global_s = std::getenv("TS_FORCE_GLOBAL_S") != nullptr && std::getenv("TS_FORCE_GLOBAL_S")[0];
 const int g_debug_flags = std::getenv("TS_DEBUG_FLAGS") ? std::atoi(std::getenv("TS_DEBUG_FLAGS")) : 0;
 const bool g_force_cuda_core_prefill = std::getenv("TS_CUDA_CORE_PREFILL") != nullptr;
@@ -317,7 +313,6 @@ void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t 
   p.ws_acnt = ws.acnt.as<unsigned int>();
   p.bar = ws.bar.as<unsigned int>();
   p.bar_slot = (ws.launches & 1u) ? 32 : 0;  // launches on one workspace are stream-ordered
-  p.prefetch_stages = g_prefetch_stages;
   p.ring_bytes = lean ? pl.lean_ring_bytes : pl.ring_bytes;
   // whole-stage TMA (general kernel): the kernel checks per stage that its
   // 16 slab rows are consecutive (ascending or descending) and else copies rows

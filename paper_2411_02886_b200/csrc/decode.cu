@@ -1841,7 +1841,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
         if (radix_own) hist_add(sm.hist, key, jl < nloc, 20);
       }
     } else {
-    const int n2 = (nloc + 1) >> 1;
+      const int n2 = (nloc + 1) >> 1;
       const bool soft = method == 2;
       for (int base = 0; base < n2; base += blockDim.x) {
         const int q = base + tid;

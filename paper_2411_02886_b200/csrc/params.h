@@ -101,11 +101,10 @@ struct DecodeParams {
   unsigned int* ws_acnt;       // [n_seq][H_kv] arrival counters of the attention merge (self-resetting)
   unsigned int* bar;           // grid barrier counters: bar[0] / bar[32] alternate per launch
   int bar_slot;                // 0 or 32: this launch's counter (the other one is reset)
-  int prefetch_stages;
   int ring_bytes;              // shared-memory K ring (>= kRingBudget)
   int att_bytes;               // attention staging: the ring + the (then dead) S/keys region
-  int debug_flags;             // dev experiments: bit0 = scan consumers skip the math
-  unsigned long long* trace;   // optional [32] %globaltimer phase stamps (CTA 0)
+  int debug_flags;             // dev timing: n << 8 ends the launch at stop point n (decode.cu)
+  unsigned long long* trace;   // optional phase trace, [CTA][kTraceStride] clock64 stamps
   SeqDesc seqs[kMaxSeqPerLaunch];  // passed by value in the kernel parameter space
   // (kept last: the fields above keep their constant-bank offsets)
   // TMA tensor map (device memory) viewing the K slab as [128-B chunk][slab
