@@ -301,6 +301,47 @@ def test_decode_llama_128k_parity(sa, orc, n):
         assert rel_fro(o1, want) <= 1e-5 and np.abs(o1 - want).max() <= 1e-4, step
 
 
+@pytest.mark.parametrize("H,H_kv,lens", [(28, 4, (6000, 4700, 7300, 5200)), (32, 8, (3000, 5200))])
+def test_decode_batched_vs_oracle(sa, orc, H, H_kv, lens):
+    """Config 3 (batched decode, per-request page tables, one launch): every
+    sequence of the batch matches its own oracle engine, over a miss step and
+    a hit step. The sequences are filled one after another, so each one's
+    slab rows are consecutive (descending) and the general kernel's scan loads
+    whole stages through the TMA tensor map."""
+    d, k, n_init, n_local = 128, 512, 64, 128
+    B = len(lens)
+    kw = dict(k=k, n_local=n_local, n_init=n_init, chunk_size=512, theta=0.9, num_heads=H, num_kv_heads=H_kv,
+              head_dim=d, block_size=64)
+    eng = sa.Engine(max(lens) + 16, n_seqs=B, **kw)
+    refs = []
+    for b, n in enumerate(lens):
+        K = bf16_round(rng_normal(700 + b, (n, H_kv * d), 3.0))
+        V = bf16_round(rng_normal(800 + b, (n, H_kv * d)))
+        eng.append(K, V, b)
+        ref = orc.engine(max(lens) + 16, **kw)
+        ref.append(K, V)
+        refs.append(ref)
+    base = rng_normal(900, (B, H * d))
+    for step in range(2):  # a miss, then the same queries again (a hit)
+        q = base if step == 0 else base.copy()
+        kt = bf16_round(rng_normal(910 + step, (B, H_kv * d), 3.0))
+        vt = bf16_round(rng_normal(920 + step, (B, H_kv * d)))
+        o1, h1, s1 = eng.decode(q, kt, vt)
+        for b in range(B):
+            o2, h2, s2 = refs[b].decode(q[b:b + 1], kt[b:b + 1], vt[b:b + 1])
+            assert h1[b] == h2 == (step == 1), (b, step, h1[b], h2)
+            want = o2
+            if s1[b] != list(s2):
+                m = lens[b] + step
+                cand = np.arange(n_init, m - n_local, dtype=np.uint32)
+                K_all, V_all = ref_rows(refs[b])
+                S = orc.score_paged(q[b].reshape(H, d), K_all[:m], H_kv, cand)
+                check_selection(s1[b], s2, orc.criticality(S, k), cand)
+                att = orc.make_windows(m, n_init, n_local, np.asarray(s1[b], np.uint32))
+                want = orc.sparse_attend(q[b:b + 1], kt[b:b + 1], vt[b:b + 1], K_all[:m], V_all[:m], H, H_kv, att)
+            assert rel_fro(o1[b:b + 1], want) <= 1e-5 and np.abs(o1[b:b + 1] - want).max() <= 1e-4, (b, step)
+
+
 # --------------------------------------------------------------- prefill
 @pytest.mark.parametrize("H,H_kv,d,n,chunk,k", [(2, 2, 4, 30, 8, 4), (2, 1, 4, 32, 16, 4096), (4, 2, 32, 1500, 256, 128),
                                               (8, 2, 128, 1800, 512, 256), (28, 4, 128, 1300, 300, 128)])
