@@ -45,6 +45,11 @@ constexpr size_t kTraceSlots = tsb::kTraceStride * 1024;
 const bool g_host_prof = std::getenv("TS_HOST_PROF") != nullptr;
 double g_prof[4] = {0, 0, 0, 0};
 uint64_t g_prof_n = 0;
+// ts_engine_decode (host buffers): pointer queries, stage+H2D, engine_step, D2H issue, sync wait, unpack
+double g_e2e_prof[6] = {0, 0, 0, 0, 0, 0};
+uint64_t g_e2e_n = 0;
+double g_e2e_memcpy = 0;  // zero check + host packing part of stage+h2d
+double g_e2e_h2dapi = 0;  // the cudaMemcpyAsync call
 inline double now_ns() {
   return std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }  // [cta][32] %globaltimer stamps (<= 1024 CTAs)
@@ -228,6 +233,19 @@ struct Plan {
   size_t lean_smem;
 };
 
+// a kernel's static shared memory (cudaFuncGetAttributes costs microseconds
+// of host time; make_plan runs every step)
+size_t static_smem(const void* fn) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> known;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = known.find(fn);
+  if (it != known.end()) return it->second;
+  cudaFuncAttributes fa{};
+  ck(cudaFuncGetAttributes(&fa, fn), "cudaFuncGetAttributes");
+  return known[fn] = fa.sharedSizeBytes;
+}
+
 Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows, bool attend = true,
                bool force_spill = false) {
   const DeviceInfo& di = device_info();
@@ -244,14 +262,8 @@ Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows, bool 
   pl.tpc = static_cast<int>(tsb::align_up(static_cast<size_t>(std::max(1, (max_T + c - 1) / c)), 16));
   const int row_bytes = H_kv * d * 2;
   // dynamic shared memory left next to the kernel's static allocation
-  cudaFuncAttributes fa{};
-  ck(cudaFuncGetAttributes(&fa, pl.fn), "cudaFuncGetAttributes");
-  size_t stat = fa.sharedSizeBytes;
-  if (pl.fn_lean) {
-    cudaFuncAttributes fl{};
-    ck(cudaFuncGetAttributes(&fl, pl.fn_lean), "cudaFuncGetAttributes");
-    stat = std::max(stat, static_cast<size_t>(fl.sharedSizeBytes));
-  }
+  size_t stat = static_smem(pl.fn);
+  if (pl.fn_lean) stat = std::max(stat, static_smem(pl.fn_lean));
   const size_t optin = static_cast<size_t>(di.smem_optin) - stat;
   tsb::SmemLayout L = tsb::smem_layout(H, row_bytes, pl.tpc, 1);
   if (L.total <= optin && !g_force_global_s && !force_spill) {
@@ -476,7 +488,7 @@ struct ts_engine {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   // per-sequence Selection Cache entries (device)
-  DevBuf cache_state, cached_q, sel, sel_crit, sel_rows;
+  DevBuf cached_q, sel, sel_crit, sel_rows;
   // step IO staging (device) + pinned host mirrors
   DevBuf d_q, d_k, d_v, d_out;
   float* h_q = nullptr;
@@ -497,13 +509,17 @@ struct ts_engine {
     if (h_k) cudaFreeHost(h_k);
     if (h_v) cudaFreeHost(h_v);
     if (h_out) cudaFreeHost(h_out);
-    if (h_cache) cudaFreeHost(h_cache);
     if (h_sel) cudaFreeHost(h_sel);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
   size_t W() const { return cfg.num_heads * cfg.head_dim; }
   size_t KW() const { return cfg.num_kv_heads * cfg.head_dim; }
-  CacheState* cache(size_t b) const { return cache_state.as<CacheState>() + b; }
+  // [B x H*d output | B cache states], 256-B aligned split
+  size_t out_bytes() const { return (B * W() * 4 + 255) / 256 * 256; }
+  size_t out_block_bytes() const { return out_bytes() + B * sizeof(CacheState); }
+  CacheState* cache(size_t b) const {
+    return reinterpret_cast<CacheState*>(d_out.as<char>() + out_bytes()) + b;
+  }
   float* cq(size_t b) const { return cached_q.as<float>() + b * W(); }
   uint32_t* sl(size_t b) const { return sel.as<uint32_t>() + b * std::max<size_t>(cfg.k, 1); }
   float* sc(size_t b) const { return sel_crit.as<float>() + b * std::max<size_t>(cfg.k, 1); }
@@ -979,7 +995,6 @@ ts_status ts_engine_create(const ts_engine_config* cfg, size_t capacity_tokens, 
     ck(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking), "stream");
     e->stream = e->own_stream;
     const size_t W = e->W(), KW = e->KW(), kk = std::max<size_t>(cfg->k, 1);
-    e->cache_state.ensure(n_seqs * sizeof(CacheState));
     e->cached_q.ensure(n_seqs * W * 4);
     e->sel.ensure(n_seqs * kk * 4);
     e->sel_crit.ensure(n_seqs * kk * 4);
@@ -987,12 +1002,12 @@ ts_status ts_engine_create(const ts_engine_config* cfg, size_t capacity_tokens, 
     e->d_q.ensure(n_seqs * (W + 2 * KW) * 4);  // q | k | v staging block
     e->d_k.ensure(n_seqs * KW * 4);
     e->d_v.ensure(n_seqs * KW * 4);
-    e->d_out.ensure(n_seqs * W * 4);
+    e->d_out.ensure(e->out_block_bytes());  // output | cache states
     ck(cudaMallocHost(&e->h_q, n_seqs * (W + 2 * KW) * 4), "pinned");
     ck(cudaMallocHost(&e->h_k, n_seqs * KW * 4), "pinned");
     ck(cudaMallocHost(&e->h_v, n_seqs * KW * 4), "pinned");
-    ck(cudaMallocHost(&e->h_out, n_seqs * W * 4), "pinned");
-    ck(cudaMallocHost(&e->h_cache, n_seqs * sizeof(CacheState)), "pinned");
+    ck(cudaMallocHost(&e->h_out, e->out_block_bytes()), "pinned");
+    e->h_cache = reinterpret_cast<CacheState*>(reinterpret_cast<char*>(e->h_out) + e->out_bytes());
     std::vector<CacheState> init(n_seqs);
     for (auto& c : init) {
       c = CacheState{};
@@ -1001,7 +1016,7 @@ ts_status ts_engine_create(const ts_engine_config* cfg, size_t capacity_tokens, 
       c.first_flag = 1;
       c.last_hit = -1;
     }
-    ck(cudaMemcpy(e->cache_state.p, init.data(), n_seqs * sizeof(CacheState), cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemcpy(e->cache(0), init.data(), n_seqs * sizeof(CacheState), cudaMemcpyHostToDevice), "H2D");
     ck(cudaMemset(e->cached_q.p, 0, n_seqs * W * 4), "memset");
     *out = e.release();
   });
@@ -1009,9 +1024,21 @@ ts_status ts_engine_create(const ts_engine_config* cfg, size_t capacity_tokens, 
 
 void ts_engine_destroy(ts_engine* eng) {
   if (g_host_prof && g_prof_n)
-    std::fprintf(stderr, "[tokenselect host prof] per step: params %.0f ns, plan %.0f ns, launch api %.0f ns (%llu steps)\n",
-                 g_prof[0] / g_prof_n, g_prof[1] / g_prof_n, g_prof[3] / g_prof_n,
+    std::fprintf(stderr, "[tokenselect host prof] per step: params %.0f ns, plan %.0f ns, launch_decode %.0f ns (launch api %.0f ns) (%llu steps)\n",
+                 g_prof[0] / g_prof_n, g_prof[1] / g_prof_n, g_prof[2] / g_prof_n, g_prof[3] / g_prof_n,
                  static_cast<unsigned long long>(g_prof_n));
+  if (g_host_prof && g_e2e_n)
+    std::fprintf(stderr, "[tokenselect host prof] decode(host bufs): ptr queries %.0f ns, stage+h2d %.0f ns, step %.0f ns, "
+                 "d2h issue %.0f ns, sync wait %.0f ns, unpack %.0f ns (%llu calls; packing %.0f ns, h2d api %.0f ns)\n", g_e2e_prof[0] / g_e2e_n,
+                 g_e2e_prof[1] / g_e2e_n, g_e2e_prof[2] / g_e2e_n, g_e2e_prof[3] / g_e2e_n, g_e2e_prof[4] / g_e2e_n,
+                 g_e2e_prof[5] / g_e2e_n,
+                 static_cast<unsigned long long>(g_e2e_n), g_e2e_memcpy / g_e2e_n, g_e2e_h2dapi / g_e2e_n);
+  if (g_host_prof) {  // per-engine figures
+    std::fill(std::begin(g_prof), std::end(g_prof), 0.0);
+    std::fill(std::begin(g_e2e_prof), std::end(g_e2e_prof), 0.0);
+    g_prof_n = g_e2e_n = 0;
+    g_e2e_memcpy = g_e2e_h2dapi = 0;
+  }
   delete eng;
 }
 
@@ -1107,7 +1134,9 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
     }
     p.trace = e->trace_on ? e->trace.as<unsigned long long>() : nullptr;
     if (p.trace) ck(cudaMemsetAsync(p.trace, 0, kTraceSlots * 8, st), "memset trace");
+    const double t3 = g_host_prof ? now_ns() : 0.0;
     launch_decode(p, pl, e->ws, st);
+    if (g_host_prof) g_prof[2] += now_ns() - t3;
     for (size_t i = 0; i < gn; ++i)
       if (!cap_fail[g0 + i]) pool.state(e->seq_ids[g0 + i]).len += 1;
   }
@@ -1121,7 +1150,11 @@ ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const f
   return guarded([&] {
     const size_t W = e->W(), KW = e->KW(), B = e->B;
     cudaStream_t st = e->stream;
-    const bool q_dev = is_device_ptr(q);
+    double tp[7];
+    if (g_host_prof) tp[0] = now_ns();
+    const bool q_dev = is_device_ptr(q), k_dev = is_device_ptr(k), v_dev = is_device_ptr(v);
+    const bool out_dev = is_device_ptr(out);
+    if (g_host_prof) tp[1] = now_ns();
     // zero-query check before any mutation (selection_cache.cpp:18-27)
     if (!q_dev) {
       ts_pool& pool = *e->pool;
@@ -1133,40 +1166,50 @@ ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const f
         if (!nz) fail(TS_INVALID_ARGUMENT, "lookup_or_select: zero query vector");
       }
     }
-    auto stage = [&](const float* src, float* pinned, DevBuf& dbuf, size_t n) -> const float* {
-      if (is_device_ptr(src)) return src;
+    auto stage = [&](const float* src, bool dev, float* pinned, DevBuf& dbuf, size_t n) -> const float* {
+      if (dev) return src;
       std::memcpy(pinned, src, n * 4);
       ck(cudaMemcpyAsync(dbuf.p, pinned, n * 4, cudaMemcpyHostToDevice, st), "H2D");
       return dbuf.as<float>();
     };
     const float *qd, *kd, *vd;
-    if (!is_device_ptr(q) && !is_device_ptr(k) && !is_device_ptr(v)) {
+    float* od = out_dev ? out : e->d_out.as<float>();
+    if (!q_dev && !k_dev && !v_dev) {
       // host inputs: one pinned staging block, one H2D copy
       std::memcpy(e->h_q, q, B * W * 4);
       std::memcpy(e->h_q + B * W, k, B * KW * 4);
       std::memcpy(e->h_q + B * W + B * KW, v, B * KW * 4);
+      const double tc = g_host_prof ? now_ns() : 0.0;
+      if (g_host_prof) g_e2e_memcpy += tc - tp[1];
       ck(cudaMemcpyAsync(e->d_q.p, e->h_q, (B * W + 2 * B * KW) * 4, cudaMemcpyHostToDevice, st), "H2D");
+      if (g_host_prof) g_e2e_h2dapi += now_ns() - tc;
       qd = e->d_q.as<float>();
       kd = qd + B * W;
       vd = kd + B * KW;
     } else {
-      qd = stage(q, e->h_q, e->d_q, B * W);
-      kd = stage(k, e->h_k, e->d_k, B * KW);
-      vd = stage(v, e->h_v, e->d_v, B * KW);
+      qd = stage(q, q_dev, e->h_q, e->d_q, B * W);
+      kd = stage(k, k_dev, e->h_k, e->d_k, B * KW);
+      vd = stage(v, v_dev, e->h_v, e->d_v, B * KW);
     }
-    const bool out_dev = is_device_ptr(out);
-    float* od = out_dev ? out : e->d_out.as<float>();
+    if (g_host_prof) tp[2] = now_ns();
     std::vector<int> cap_fail = engine_step(e, qd, kd, vd, od);
+    if (g_host_prof) tp[3] = now_ns();
     // every result rides one stream sync: output, cache states and (when
     // requested) the full selection slots
     const size_t kk = std::max<size_t>(e->cfg.k, 1);
-    if (!out_dev) ck(cudaMemcpyAsync(e->h_out, od, B * W * 4, cudaMemcpyDeviceToHost, st), "D2H");
-    ck(cudaMemcpyAsync(e->h_cache, e->cache_state.p, B * sizeof(CacheState), cudaMemcpyDeviceToHost, st), "D2H");
+    // d_out and the cache states are one device block (and h_out / h_cache
+    // one pinned block): a host output rides the same D2H copy
+    if (!out_dev)
+      ck(cudaMemcpyAsync(e->h_out, od, e->out_block_bytes(), cudaMemcpyDeviceToHost, st), "D2H");
+    else
+      ck(cudaMemcpyAsync(e->h_cache, e->cache(0), B * sizeof(CacheState), cudaMemcpyDeviceToHost, st), "D2H");
     if (sel_out) {
       if (!e->h_sel) ck(cudaMallocHost(&e->h_sel, B * kk * 4), "pinned");
       ck(cudaMemcpyAsync(e->h_sel, e->sel.p, B * kk * 4, cudaMemcpyDeviceToHost, st), "D2H sel");
     }
+    if (g_host_prof) tp[4] = now_ns();
     ck(cudaStreamSynchronize(st), "decode sync");
+    if (g_host_prof) tp[5] = now_ns();
     if (!out_dev) std::memcpy(out, e->h_out, B * W * 4);
     ts_pool& pool = *e->pool;
     for (size_t b = 0; b < B; ++b) {
@@ -1182,6 +1225,11 @@ ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const f
         std::memcpy(sel_out + b * kk, e->h_sel + b * kk, n * 4);
         if (n_sel) n_sel[b] = n;
       }
+    }
+    if (g_host_prof) {
+      tp[6] = now_ns();
+      for (int i = 0; i < 6; ++i) g_e2e_prof[i] += tp[i + 1] - tp[i];
+      g_e2e_n += 1;
     }
     for (size_t b = 0; b < B; ++b)
       if (cap_fail[b]) fail(TS_CAPACITY, "append_kv: pool exhausted (need 1 frames, 0 free)");

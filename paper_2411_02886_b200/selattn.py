@@ -316,7 +316,9 @@ class Engine:
         """decode_step through the C ABI with caller-owned host buffers (no
         Python-side conversion): q/k/v/out are C-contiguous float32 numpy
         arrays; optional hits (int32[B]), sel (uint32[B*k]), n_sel (uint64[B])."""
-        ptr = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)
+        # plain addresses: c_void_p argtypes take ints (ndarray.ctypes.data_as
+        # costs about twice as much per array)
+        ptr = lambda a: None if a is None else a.ctypes.data
         check(lib.ts_engine_decode(self._h, ptr(q), ptr(k), ptr(v), ptr(out), ptr(hits), ptr(sel), ptr(n_sel)))
 
     def decode_async(self, q, k, v, out):

@@ -1,0 +1,68 @@
+// Host-side API cost of the small copies a decode call makes (dev microbench):
+// H2D of the 24 KB q|k|v block and D2H of the 16 KB output, pinned vs pageable,
+// plus an empty kernel launch for scale. nvcc -O2 -arch=sm_100a copyapi.cu -o copyapi
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+#include <cuda_runtime.h>
+
+__global__ void empty_kernel() {}
+
+static double now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+template <typename F>
+static void bench(const char* name, F f, cudaStream_t st) {
+  for (int i = 0; i < 20; ++i) f();
+  cudaStreamSynchronize(st);
+  const int n = 500;
+  double api = 0, tot = 0;
+  for (int i = 0; i < n; ++i) {
+    const double t0 = now_us();
+    f();
+    const double t1 = now_us();
+    cudaStreamSynchronize(st);
+    const double t2 = now_us();
+    api += t1 - t0;
+    tot += t2 - t0;
+  }
+  std::printf("%-40s api %6.2f us   api+sync %6.2f us\n", name, api / n, tot / n);
+}
+
+int main() {
+  const size_t in_bytes = 24576, out_bytes = 16384 + 256;
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  void *d_in, *d_out, *h_pin, *h_pin_out, *h_wc, *h_mapped, *d_mapped;
+  cudaMalloc(&d_in, in_bytes);
+  cudaMalloc(&d_out, out_bytes);
+  cudaMallocHost(&h_pin, in_bytes);
+  cudaMallocHost(&h_pin_out, out_bytes);
+  cudaHostAlloc(&h_wc, in_bytes, cudaHostAllocWriteCombined);
+  cudaHostAlloc(&h_mapped, in_bytes, cudaHostAllocMapped);
+  cudaHostGetDevicePointer(&d_mapped, h_mapped, 0);
+  std::vector<char> pageable(in_bytes), pageable_out(out_bytes);
+  bench("empty kernel launch", [&] { empty_kernel<<<1, 32, 0, st>>>(); }, st);
+  bench("empty kernel launch x148 CTAs", [&] { empty_kernel<<<148, 544, 0, st>>>(); }, st);
+  bench("H2D 24KB pinned", [&] { cudaMemcpyAsync(d_in, h_pin, in_bytes, cudaMemcpyHostToDevice, st); }, st);
+  bench("H2D 24KB write-combined", [&] { cudaMemcpyAsync(d_in, h_wc, in_bytes, cudaMemcpyHostToDevice, st); }, st);
+  bench("H2D 24KB pageable", [&] { cudaMemcpyAsync(d_in, pageable.data(), in_bytes, cudaMemcpyHostToDevice, st); }, st);
+  bench("H2D 4KB pinned", [&] { cudaMemcpyAsync(d_in, h_pin, 4096, cudaMemcpyHostToDevice, st); }, st);
+  bench("H2D 24KB pinned, cudaMemcpyDefault", [&] { cudaMemcpyAsync(d_in, h_pin, in_bytes, cudaMemcpyDefault, st); }, st);
+  bench("D2H 16KB pinned", [&] { cudaMemcpyAsync(h_pin_out, d_out, out_bytes, cudaMemcpyDeviceToHost, st); }, st);
+  bench("D2H 16KB pageable", [&] { cudaMemcpyAsync(pageable_out.data(), d_out, out_bytes, cudaMemcpyDeviceToHost, st); }, st);
+  bench("H2D pinned + launch + D2H pinned", [&] {
+    cudaMemcpyAsync(d_in, h_pin, in_bytes, cudaMemcpyHostToDevice, st);
+    empty_kernel<<<148, 544, 0, st>>>();
+    cudaMemcpyAsync(h_pin_out, d_out, out_bytes, cudaMemcpyDeviceToHost, st);
+  }, st);
+  bench("memcpy 24KB host->pinned", [&] { std::memcpy(h_pin, pageable.data(), in_bytes); }, st);
+  bench("cudaPointerGetAttributes", [&] {
+    cudaPointerAttributes a{};
+    cudaPointerGetAttributes(&a, h_pin);
+  }, st);
+  bench("cudaStreamSynchronize (idle)", [&] {}, st);
+  return 0;
+}
