@@ -96,3 +96,6 @@ for _ in range(300):
     api.append(t1 - t0)
     tot.append(time.perf_counter() - t0)
 print(f"torch pinned H2D 24KB: call {1e6 * statistics.median(api):.2f} us, +sync {1e6 * statistics.median(tot):.2f} us")
+if os.path.exists(os.path.join(os.path.dirname(os.path.abspath(__file__)), "ubench", "libcopyapi.so")):
+    print("--- tools/ubench/copyapi in this process", flush=True)
+    C.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "ubench", "libcopyapi.so")).bench_main()

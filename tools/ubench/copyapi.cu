@@ -31,7 +31,7 @@ static void bench(const char* name, F f, cudaStream_t st) {
   std::printf("%-40s api %6.2f us   api+sync %6.2f us\n", name, api / n, tot / n);
 }
 
-int main() {
+extern "C" int bench_main() {
   const size_t in_bytes = 24576, out_bytes = 16384 + 256;
   cudaStream_t st;
   cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
@@ -58,6 +58,49 @@ int main() {
     empty_kernel<<<148, 544, 0, st>>>();
     cudaMemcpyAsync(h_pin_out, d_out, out_bytes, cudaMemcpyDeviceToHost, st);
   }, st);
+  bench("H2D 24KB pinned (again)", [&] { cudaMemcpyAsync(d_in, h_pin, in_bytes, cudaMemcpyHostToDevice, st); }, st);
+  bench("H2D 24KB pinned, Default (again)", [&] { cudaMemcpyAsync(d_in, h_pin, in_bytes, cudaMemcpyDefault, st); }, st);
+  {
+    // the library's pattern: pack into the pinned block, time only the copy call
+    for (int i = 0; i < 20; ++i) cudaMemcpyAsync(d_in, h_pin, in_bytes, cudaMemcpyHostToDevice, st);
+    cudaStreamSynchronize(st);
+    double api = 0;
+    for (int i = 0; i < 500; ++i) {
+      std::memcpy(h_pin, pageable.data(), in_bytes);
+      const double t0 = now_us();
+      cudaMemcpyAsync(d_in, h_pin, in_bytes, cudaMemcpyHostToDevice, st);
+      api += now_us() - t0;
+      cudaStreamSynchronize(st);
+    }
+    std::printf("%-40s api %6.2f us\n", "H2D 24KB pinned after host packing", api / 500);
+  }
+  for (int coop = 0; coop < 2; ++coop) {
+    // H2D api time when each iteration is H2D, a (cooperative) 148x544 launch, D2H, sync
+    double api_h2d = 0, api_launch = 0, api_d2h = 0;
+    const int n = 300;
+    for (int i = 0; i < n + 20; ++i) {
+      const double t0 = now_us();
+      cudaMemcpyAsync(d_in, h_pin, in_bytes, cudaMemcpyHostToDevice, st);
+      const double t1 = now_us();
+      if (coop) {
+        void* args[] = {nullptr};
+        cudaLaunchCooperativeKernel((const void*)empty_kernel, dim3(148), dim3(544), args, 0, st);
+      } else {
+        empty_kernel<<<148, 544, 0, st>>>();
+      }
+      const double t2 = now_us();
+      cudaMemcpyAsync(h_pin_out, d_out, out_bytes, cudaMemcpyDeviceToHost, st);
+      const double t3 = now_us();
+      cudaStreamSynchronize(st);
+      if (i >= 20) {
+        api_h2d += t1 - t0;
+        api_launch += t2 - t1;
+        api_d2h += t3 - t2;
+      }
+    }
+    std::printf("%s step: h2d api %.2f us, launch api %.2f us, d2h api %.2f us\n", coop ? "cooperative" : "plain",
+                api_h2d / n, api_launch / n, api_d2h / n);
+  }
   bench("memcpy 24KB host->pinned", [&] { std::memcpy(h_pin, pageable.data(), in_bytes); }, st);
   bench("cudaPointerGetAttributes", [&] {
     cudaPointerAttributes a{};
@@ -66,3 +109,7 @@ int main() {
   bench("cudaStreamSynchronize (idle)", [&] {}, st);
   return 0;
 }
+
+#ifndef COPYAPI_LIB
+int main() { return bench_main(); }
+#endif
