@@ -46,6 +46,7 @@ constexpr size_t kTraceSlots = tsb::kTraceStride * 1024;
 const bool g_host_prof = std::getenv("TS_HOST_PROF") != nullptr;
 double g_prof[4] = {0, 0, 0, 0};
 uint64_t g_prof_n = 0;
+double g_prof_ld[2] = {0, 0};  // launch_decode: params fill, everything before the launch API
 // ts_engine_decode (host buffers): pointer queries, stage+H2D, engine_step, D2H issue, sync wait, unpack
 double g_e2e_prof[6] = {0, 0, 0, 0, 0, 0};
 uint64_t g_e2e_n = 0;
@@ -308,6 +309,7 @@ void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t 
                     (p.page_size & (p.page_size - 1)) == 0;
   const void* fn = lean ? pl.fn_lean : pl.fn;
   const size_t smem = lean ? pl.lean_smem : pl.smem;
+  const double tq0 = g_host_prof ? now_ns() : 0.0;
   ws.prepare(n_ctas, p.H, p.H_kv, p.d, pl.tpc, lean ? 1 : pl.s_in_smem, p.n_seq, st);
   p.ctas_per_seq = pl.ctas_per_seq;
   p.tpc = pl.tpc;
@@ -344,6 +346,7 @@ void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t 
   }
   p.att_bytes = lean ? pl.lean_att_bytes : pl.att_bytes;
   p.debug_flags = g_debug_flags;
+  if (g_host_prof) g_prof_ld[0] += now_ns() - tq0;
   // the dynamic shared-memory limit is set once per kernel (largest request so far)
   static std::mutex mu;
   static std::unordered_map<const void*, size_t> smem_set;
@@ -356,6 +359,7 @@ void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t 
   }
   void* args[] = {&p};
   const double t0 = g_host_prof ? now_ns() : 0.0;
+  if (g_host_prof) g_prof_ld[1] += t0 - tq0;
   ck(cudaLaunchCooperativeKernel(fn, dim3(n_ctas), dim3(tsb::kDecodeThreads), args, smem, st),
      "decode kernel launch");
   if (g_host_prof) g_prof[3] += now_ns() - t0;
@@ -1028,6 +1032,9 @@ void ts_engine_destroy(ts_engine* eng) {
     std::fprintf(stderr, "[tokenselect host prof] per step: params %.0f ns, plan %.0f ns, launch_decode %.0f ns (launch api %.0f ns) (%llu steps)\n",
                  g_prof[0] / g_prof_n, g_prof[1] / g_prof_n, g_prof[2] / g_prof_n, g_prof[3] / g_prof_n,
                  static_cast<unsigned long long>(g_prof_n));
+  if (g_host_prof && g_prof_n)
+    std::fprintf(stderr, "[tokenselect host prof] launch_decode: prepare+fill %.0f ns, before launch api %.0f ns\n",
+                 g_prof_ld[0] / g_prof_n, g_prof_ld[1] / g_prof_n);
   if (g_host_prof && g_e2e_n)
     std::fprintf(stderr, "[tokenselect host prof] decode(host bufs): ptr queries %.0f ns, stage+h2d %.0f ns, step %.0f ns, "
                  "d2h issue %.0f ns, sync wait %.0f ns, unpack %.0f ns (%llu calls; packing %.0f ns, h2d api %.0f ns)\n", g_e2e_prof[0] / g_e2e_n,
@@ -1038,6 +1045,7 @@ void ts_engine_destroy(ts_engine* eng) {
     std::fill(std::begin(g_prof), std::end(g_prof), 0.0);
     std::fill(std::begin(g_e2e_prof), std::end(g_e2e_prof), 0.0);
     g_prof_n = g_e2e_n = 0;
+    g_prof_ld[0] = g_prof_ld[1] = 0;
     g_e2e_memcpy = g_e2e_h2dapi = 0;
   }
   delete eng;

@@ -8,6 +8,18 @@
 #include <cuda_runtime.h>
 
 __global__ void empty_kernel() {}
+struct BigParams {
+  char b[3816];
+};
+struct SmallParams {
+  char b[440];
+};
+__global__ void big_kernel(const __grid_constant__ BigParams p) {
+  if (p.b[threadIdx.x] == 123) asm volatile("trap;");
+}
+__global__ void small_kernel(const __grid_constant__ SmallParams p) {
+  if (p.b[threadIdx.x % 440] == 123) asm volatile("trap;");
+}
 
 static double now_us() {
   return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -100,6 +112,22 @@ extern "C" int bench_main() {
     }
     std::printf("%s step: h2d api %.2f us, launch api %.2f us, d2h api %.2f us\n", coop ? "cooperative" : "plain",
                 api_h2d / n, api_launch / n, api_d2h / n);
+  }
+  {
+    BigParams bp{};
+    SmallParams sp{};
+    cudaFuncSetAttribute((const void*)big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute((const void*)small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    void* bargs[] = {&bp};
+    void* sargs[] = {&sp};
+    bench("coop launch, 3816-B params, 200KB smem", [&] {
+      cudaLaunchCooperativeKernel((const void*)big_kernel, dim3(148), dim3(544), bargs, 200 * 1024, st);
+    }, st);
+    bench("coop launch, 440-B params, 200KB smem", [&] {
+      cudaLaunchCooperativeKernel((const void*)small_kernel, dim3(148), dim3(544), sargs, 200 * 1024, st);
+    }, st);
+    bench("plain launch, 3816-B params, 200KB smem", [&] { big_kernel<<<148, 544, 200 * 1024, st>>>(bp); }, st);
+    bench("plain launch, 440-B params, 200KB smem", [&] { small_kernel<<<148, 544, 200 * 1024, st>>>(sp); }, st);
   }
   bench("memcpy 24KB host->pinned", [&] { std::memcpy(h_pin, pageable.data(), in_bytes); }, st);
   bench("cudaPointerGetAttributes", [&] {
