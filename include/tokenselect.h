@@ -202,8 +202,9 @@ uint32_t ts_engine_sequence(const ts_engine* eng, size_t seq);
  * transport), all on device buffers and the engine's stream:
  *   ts_shard_stats      -> stats  [H][2]        all-gather -> [world][H][2]
  *   ts_shard_select     -> cands  [2k + 1] u32  all-gather -> [world][2k + 1]
- *   ts_shard_attend     -> out    [H*d], ml [H][2]  all-gather both
- *   ts_shard_combine    -> the step's output [H*d] (identical on every rank)
+ *   ts_shard_attend     -> out    [H*d], ml [H][2]  all-gather both (or, packed
+ *                          into one [H*d + 2H] block, one all-gather)
+ *   ts_shard_combine[_packed] -> the step's output [H*d] (identical on every rank)
  * The Selection Cache decision needs no exchange (q is replicated). Global
  * softmax statistics are combined in rank order, the global top-k is exact
  * (it is a subset of the union of the shards' local top-k), and outputs
@@ -219,6 +220,11 @@ ts_status ts_shard_select(ts_engine* eng, const float* all_stats, uint32_t* cand
 ts_status ts_shard_attend(ts_engine* eng, const uint32_t* all_cands, float* out_partial, float* ml_out);
 ts_status ts_shard_combine(const float* o_all, const float* ml_all, int world, size_t num_heads,
                            size_t head_dim, float* out, void* stream);
+/* ts_shard_combine over one all-gather instead of two: every rank's block is
+ * [H*d partial output | H x (M, L)], i.e. ts_shard_attend called with
+ * ml_out = out_partial + H*d; packed_all is [world][H*d + 2H]. */
+ts_status ts_shard_combine_packed(const float* packed_all, int world, size_t num_heads, size_t head_dim,
+                                  float* out, void* stream);
 
 /* Kernel launches issued by this library since process start (evidence
  * counter for the benchmark's gpu_launches field). */

@@ -87,6 +87,7 @@ SIGNATURES = {
     "ts_shard_select": (C.c_int, [_p, _p, _p]),
     "ts_shard_attend": (C.c_int, [_p, _p, _p, _p]),
     "ts_shard_combine": (C.c_int, [_p, _p, C.c_int, _sz, _sz, _p, _p]),
+    "ts_shard_combine_packed": (C.c_int, [_p, C.c_int, _sz, _sz, _p, _p]),
     "ts_engine_pool": (_p, [_p]),
     "ts_engine_sequence": (C.c_uint32, [_p, _sz]),
 }

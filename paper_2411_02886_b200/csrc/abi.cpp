@@ -1615,4 +1615,15 @@ ts_status ts_shard_combine(const float* o_all, const float* ml_all, int world, s
   });
 }
 
+ts_status ts_shard_combine_packed(const float* packed_all, int world, size_t num_heads, size_t head_dim, float* out,
+                                  void* stream) {
+  return guarded([&] {
+    device_info();
+    ck(tsb::launch_shard_combine(packed_all, packed_all + num_heads * head_dim, world, static_cast<int>(num_heads),
+                                 static_cast<int>(head_dim), out, static_cast<cudaStream_t>(stream), true),
+       "shard combine");
+    g_launches.fetch_add(1);
+  });
+}
+
 }  // extern "C"

@@ -362,19 +362,21 @@ __global__ void __launch_bounds__(kMergeThreads) shard_merge_kernel(const uint32
 
 // Cross-shard log-sum-exp merge of normalised outputs o_r with (M_r, L_r):
 // out = sum_r e^(M_r - M) L_r o_r / sum_r e^(M_r - M) L_r, shards in rank order.
+// Rank r's o block starts at o_all + r * o_stride, its (M, L) pairs at
+// ml_all + r * ml_stride (separate arrays, or one packed [H*d | H*2] block).
 __global__ void shard_combine_kernel(const float* o_all, const float* ml_all, int world, int H, int d,
-                                     float* out) {
+                                     size_t o_stride, size_t ml_stride, float* out) {
   const int h = blockIdx.x;
   for (int t = threadIdx.x; t < d; t += blockDim.x) {
     float M = -INFINITY;
-    for (int r = 0; r < world; ++r) M = fmaxf(M, ml_all[(static_cast<size_t>(r) * H + h) * 2]);
+    for (int r = 0; r < world; ++r) M = fmaxf(M, ml_all[r * ml_stride + h * 2]);
     float num = 0.f, den = 0.f;
     for (int r = 0; r < world; ++r) {
-      const float mr = ml_all[(static_cast<size_t>(r) * H + h) * 2];
-      const float lr = ml_all[(static_cast<size_t>(r) * H + h) * 2 + 1];
+      const float mr = ml_all[r * ml_stride + h * 2];
+      const float lr = ml_all[r * ml_stride + h * 2 + 1];
       if (mr == -INFINITY || lr == 0.f) continue;
       const float w = expf(mr - M) * lr;
-      num = fmaf(w, o_all[(static_cast<size_t>(r) * H + h) * d + t], num);
+      num = fmaf(w, o_all[r * o_stride + static_cast<size_t>(h) * d + t], num);
       den += w;
     }
     out[static_cast<size_t>(h) * d + t] = num / den;
@@ -445,8 +447,10 @@ cudaError_t launch_shard_merge(const uint32_t* all, int world, int k, uint32_t i
 }
 
 cudaError_t launch_shard_combine(const float* o_all, const float* ml_all, int world, int H, int d, float* out,
-                                 cudaStream_t st) {
-  shard_combine_kernel<<<H, 128, 0, st>>>(o_all, ml_all, world, H, d, out);
+                                 cudaStream_t st, bool packed) {
+  const size_t hd = static_cast<size_t>(H) * d;
+  const size_t o_stride = packed ? hd + 2 * H : hd, ml_stride = packed ? hd + 2 * H : 2 * static_cast<size_t>(H);
+  shard_combine_kernel<<<H, 128, 0, st>>>(o_all, ml_all, world, H, d, o_stride, ml_stride, out);
   return cudaGetLastError();
 }
 

@@ -40,7 +40,8 @@ cudaError_t launch_prefill_flash(const PrefillAttendParams& p, cudaStream_t st);
 cudaError_t launch_shard_merge(const uint32_t* all, int world, int k, uint32_t ie, uint32_t lbs, uint32_t base,
                                uint32_t n_r, uint32_t init_hi, uint32_t loc_lo, uint32_t* att, int* n_att,
                                cudaStream_t st);
+// packed: rank blocks of [H*d outputs | H x (M, L)] (ml_all = o_all + H*d)
 cudaError_t launch_shard_combine(const float* o_all, const float* ml_all, int world, int H, int d, float* out,
-                                 cudaStream_t st);
+                                 cudaStream_t st, bool packed = false);
 
 }  // namespace tsb

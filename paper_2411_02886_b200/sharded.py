@@ -12,7 +12,7 @@ ts_shard_*) with three all-gathers in between:
 
     stats   [H][2]       per-head (m, z) of the rank's scores -> global softmax stats
     cands   [2k + 1]     the rank's local top-k (global index, key, count) -> exact global top-k
-    partial [H*d] + ml   the rank's attention (o, M, L) -> log-sum-exp combine
+    partial [H*d | H*2]  the rank's attention (o, then M, L), one packed block -> log-sum-exp combine
 
 The Selection Cache decision needs no exchange: q and the cached query are
 replicated, so every rank decides identically.
@@ -81,8 +81,11 @@ class NativeShard:
         dev = torch.device("cuda", torch.cuda.current_device())
         self._stats = torch.empty(num_heads * 2, dtype=torch.float32, device=dev)
         self._cands = torch.empty(2 * k + 1, dtype=torch.int32, device=dev)
-        self._part = torch.empty(num_heads * head_dim, dtype=torch.float32, device=dev)
-        self._ml = torch.empty(num_heads * 2, dtype=torch.float32, device=dev)
+        # partial output and (M, L) pairs are one block, so a step needs one
+        # all-gather for both (ts_shard_combine_packed)
+        self._pm = torch.empty(num_heads * head_dim + num_heads * 2, dtype=torch.float32, device=dev)
+        self._part = self._pm[: num_heads * head_dim]
+        self._ml = self._pm[num_heads * head_dim:]
         # torch's default stream has handle 0, which the C ABI reads as "the
         # engine's own stream": pass cudaStreamLegacy (0x1) instead so both
         # sides order on the same stream
@@ -123,6 +126,17 @@ class NativeShard:
         part, ml = self._part, self._ml
         check(lib.ts_shard_attend(self._h, self._p(all_cands), self._p(part), self._p(ml)))
         return part, ml
+
+    def attend_packed(self, all_cands):
+        """attend, returning the [H*d | H*2] block (a view reused next step)."""
+        self.attend(all_cands)
+        return self._pm
+
+    def combine_packed(self, all_packed):
+        out = self.torch.empty(1, self.H * self.d, dtype=self.torch.float32, device=all_packed.device)
+        check(lib.ts_shard_combine_packed(self._p(all_packed), self.world, self.H, self.d, self._p(out),
+                                          C.c_void_p(self.torch.cuda.current_stream().cuda_stream)))
+        return out
 
     def combine(self, all_part, all_ml):
         out = self.torch.empty(1, self.H * self.d, dtype=self.torch.float32, device=all_part.device)
@@ -165,8 +179,8 @@ def decode_step(shard, exchange, q, k, v, base: int, n_global: int):
     returns the [1 x H*d] output, identical on every rank."""
     stats = shard.stats(q, k, v, base, n_global)
     cands = shard.select(exchange.all_gather(stats))
-    part, ml = shard.attend(exchange.all_gather(cands))
-    return shard.combine(exchange.all_gather(part), exchange.all_gather(ml))
+    packed = shard.attend_packed(exchange.all_gather(cands))
+    return shard.combine_packed(exchange.all_gather(packed))
 
 
 def simulate_step(shards: Sequence, qkv_per_shard, bases: Sequence[int], n_global: int):
@@ -180,8 +194,7 @@ def simulate_step(shards: Sequence, qkv_per_shard, bases: Sequence[int], n_globa
     all_stats = torch.cat(stats)
     cands = [s.select(all_stats).clone() for s in shards]
     all_cands = torch.cat(cands)
-    parts = [tuple(x.clone() for x in s.attend(all_cands)) for s in shards]
-    all_part = torch.cat([p for p, _ in parts])
-    all_ml = torch.cat([m for _, m in parts])
-    outs = [s.combine(all_part, all_ml) for s in shards]
+    all_packed = torch.cat([s.attend_packed(all_cands).clone() for s in shards])
+    outs = [s.combine_packed(all_packed) for s in shards]
+    simulate_step.last_packed = all_packed  # for tests: the gathered [world][H*d | H*2] blocks
     return outs, all_cands

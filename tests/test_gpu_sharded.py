@@ -70,6 +70,10 @@ def test_sharded_decode_matches_oracle(world):
         qd, kd, vd = (torch.from_numpy(x).cuda() for x in (q, kt, vt))
         outs, all_cands = sharded.simulate_step(shards, [(qd, kd, vd)] * world, bases, N)
         torch.cuda.synchronize()
+        # the two-array combine over the same blocks is the same merge
+        blocks = sharded.simulate_step.last_packed.view(world, -1)
+        two = shards[0].combine(blocks[:, : H * d].reshape(-1), blocks[:, H * d:].reshape(-1))
+        assert torch.equal(two, outs[0]), "packed and two-array combines disagree"
         outs = [o.cpu().numpy() for o in outs]
         for o in outs[1:]:
             assert np.array_equal(o, outs[0]), "ranks disagree"

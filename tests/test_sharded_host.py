@@ -100,6 +100,14 @@ class NumpyShard:
             self.V = np.vstack([self.V, self.vt])
         return t.tensor(o.ravel(), dtype=t.float64), t.tensor(ml.ravel(), dtype=t.float64)
 
+    def attend_packed(self, all_cands):
+        o, ml = self.attend(all_cands)
+        return self.torch.cat([o, ml])
+
+    def combine_packed(self, all_packed):
+        a = all_packed.reshape(self.world, H * D + 2 * H)
+        return self.combine(a[:, : H * D].reshape(-1), a[:, H * D:].reshape(-1))
+
     def combine(self, all_part, all_ml):
         t = self.torch
         o = all_part.numpy().reshape(self.world, H, D)
