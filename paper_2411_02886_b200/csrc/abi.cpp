@@ -1490,6 +1490,8 @@ DecodeParams shard_params(ts_engine* e, int mode) {
   sd.sel_rows = e->sr(0);
   sd.shard_base = static_cast<int32_t>(ss.base);
   sd.shard_world = e->world;
+  p.trace = e->trace_on ? e->trace.as<unsigned long long>() : nullptr;
+  if (p.trace) ck(cudaMemsetAsync(p.trace, 0, kTraceSlots * 8, e->stream), "memset trace");
   return p;
 }
 

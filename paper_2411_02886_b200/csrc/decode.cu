@@ -1701,23 +1701,39 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   if (pmode & kModeShardStats) {
     // this shard's per-head (m, z) from its CTAs' partials (every CTA
     // finished phase 2 at B1); S = e^(S - m_c) stays in the spill buffer
+    // One warp per head, the CTAs' partials strided over the lanes (all loads
+    // in flight; a thread walking them one by one spent ~130 us in L2
+    // round trips). Fixed order: lane-ordered partial sums, then a butterfly.
     if (own == 1 && cs == 0 && method == 2) {
       const size_t sh = stats_stride(p.ctas_per_seq);
-      for (int h = tid; h < H; h += blockDim.x) {
+      const int lane = tid & 31, nw = static_cast<int>(blockDim.x >> 5);
+      for (int h = tid >> 5; h < H; h += nw) {
         const float* mr = p.ws_m + (static_cast<size_t>(seq_id) * H + h) * sh;
         const float* zr = p.ws_z + (static_cast<size_t>(seq_id) * H + h) * sh;
+        constexpr int kPer = (kMaxPrefix + 31) / 32;
+        float mv[kPer], zv[kPer];
         float M = -INFINITY;
-        #pragma unroll 1
-        for (int c = 0; c < p.ctas_per_seq; ++c) M = fmaxf(M, __ldcg(mr + c));
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+          const int c = lane + 32 * j;
+          const bool ok = c < p.ctas_per_seq;
+          mv[j] = ok ? __ldcg(mr + c) : -INFINITY;
+          zv[j] = ok ? __ldcg(zr + c) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) M = fmaxf(M, mv[j]);
+        M = warp_max(M);
         float Z = 0.f;
-        if (M > -INFINITY)
-          #pragma unroll 1
-          for (int c = 0; c < p.ctas_per_seq; ++c) {
-            const float mc = __ldcg(mr + c);
-            if (mc > -INFINITY) Z += __ldcg(zr + c) * expf(mc - M);
-          }
-        sd.shard_stats[h * 2 + 0] = M;
-        sd.shard_stats[h * 2 + 1] = Z;
+        if (M > -INFINITY) {
+#pragma unroll
+          for (int j = 0; j < kPer; ++j)
+            if (mv[j] > -INFINITY) Z += zv[j] * expf(mv[j] - M);
+        }
+        Z = warp_sum(Z);
+        if (lane == 0) {
+          sd.shard_stats[h * 2 + 0] = M;
+          sd.shard_stats[h * 2 + 1] = Z;
+        }
       }
     }
     return;
