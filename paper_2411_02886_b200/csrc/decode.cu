@@ -1746,16 +1746,28 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       // this CTA from its partial of the stats launch
       const size_t sh = stats_stride(p.ctas_per_seq);
       for (int h = tid; h < H; h += blockDim.x) {
-        float M = -INFINITY;
-        #pragma unroll 1
-        for (int r = 0; r < sd.shard_world; ++r) M = fmaxf(M, __ldcg(sd.shard_all + (r * H + h) * 2));
-        float Z = 0.f;
-        #pragma unroll 1
-        for (int r = 0; r < sd.shard_world; ++r) {
-          const float mr = __ldcg(sd.shard_all + (r * H + h) * 2);
-          if (mr > -INFINITY) Z += __ldcg(sd.shard_all + (r * H + h) * 2 + 1) * expf(mr - M);
-        }
         const float mc = __ldcg(p.ws_m + (static_cast<size_t>(seq_id) * H + h) * sh + cs);
+        // ranks' (m, z) pairs 8 at a time (loads in flight), merged in rank order
+        constexpr int kR = 8;
+        const float2* all = reinterpret_cast<const float2*>(sd.shard_all);
+        float M = -INFINITY, Z = 0.f;
+#pragma unroll 1
+        for (int r0 = 0; r0 < sd.shard_world; r0 += kR) {
+          float2 v[kR];
+#pragma unroll
+          for (int j = 0; j < kR; ++j)
+            v[j] = r0 + j < sd.shard_world ? __ldcg(all + (r0 + j) * H + h) : make_float2(-INFINITY, 0.f);
+          float Mn = M;
+#pragma unroll
+          for (int j = 0; j < kR; ++j) Mn = fmaxf(Mn, v[j].x);
+          if (Mn > -INFINITY) {
+            Z = M > -INFINITY ? Z * expf(M - Mn) : 0.f;
+#pragma unroll
+            for (int j = 0; j < kR; ++j)
+              if (v[j].x > -INFINITY) Z += v[j].y * expf(v[j].x - Mn);
+          }
+          M = Mn;
+        }
         ml[h] = mc > -INFINITY ? fast_exp(mc - M) / Z : 0.f;
       }
       __syncthreads();
