@@ -1530,7 +1530,7 @@ ts_status ts_shard_stats(ts_engine* e, const float* q, const float* k, const flo
     ss.T = ss.sel_on && hi > lo ? static_cast<int32_t>(hi - lo) : 0;
     DecodeParams p = shard_params(e, tsb::kModeCache | tsb::kModeScore | tsb::kModeSelect | tsb::kModeShardStats);
     p.seqs[0].shard_stats = stats_out;
-    if (ss.sel_on) ck(cudaMemsetAsync(stats_out, 0xff, c.num_heads * 2 * 4, e->stream), "memset stats");  // NaN: unset
+    // the kernel writes NaN (unset) over stats_out when it has no fresh statistics
     launch_decode(p, shard_plan_for(e), e->ws, e->stream);
   });
 }

@@ -1735,6 +1735,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
           sd.shard_stats[h * 2 + 1] = Z;
         }
       }
+    } else if (cs == 0) {
+      // no fresh statistics this step (a hit, or another method): all-ones
+      // bits (NaN) mark them unset for the other ranks
+      for (int i = tid; i < 2 * H; i += blockDim.x) reinterpret_cast<uint32_t*>(sd.shard_stats)[i] = 0xffffffffu;
     }
     return;
   }
