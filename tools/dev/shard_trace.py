@@ -37,3 +37,16 @@ shard.TRACE_POINTS = sa.Engine.TRACE_POINTS
 st = shard.stats(q, kt, kt, 0, N + 4)
 torch.cuda.synchronize()
 print("stats phase trace (us):", sa.Engine.read_trace(shard))
+cands = shard.select(st)
+torch.cuda.synchronize()
+print("select phase trace (us):", sa.Engine.read_trace(shard))
+part, ml = shard.attend(cands)
+torch.cuda.synchronize()
+print("attend phase trace (us):", sa.Engine.read_trace(shard))
+for name, fn in (("select", lambda: shard.select(st)), ("attend", lambda: shard.attend(cands))):
+    torch.cuda.synchronize()
+    ev[0].record()
+    fn()
+    ev[1].record()
+    torch.cuda.synchronize()
+    print(f"{name} launch: {ev[0].elapsed_time(ev[1]) * 1000:.1f} us")
