@@ -183,7 +183,7 @@ def decode_step(shard, exchange, q, k, v, base: int, n_global: int):
     return shard.combine_packed(exchange.all_gather(packed))
 
 
-def simulate_step(shards: Sequence, qkv_per_shard, bases: Sequence[int], n_global: int):
+def simulate_step(shards: Sequence, qkv_per_shard, bases: Sequence[int], n_global: int, return_packed=False):
     """All shards of one sequence in one process (single GPU): the exchanges
     are concatenations in rank order -- the same bytes NCCL would deliver
     (each shard's phase outputs are copied before the next shard reuses its
@@ -196,5 +196,5 @@ def simulate_step(shards: Sequence, qkv_per_shard, bases: Sequence[int], n_globa
     all_cands = torch.cat(cands)
     all_packed = torch.cat([s.attend_packed(all_cands).clone() for s in shards])
     outs = [s.combine_packed(all_packed) for s in shards]
-    simulate_step.last_packed = all_packed  # for tests: the gathered [world][H*d | H*2] blocks
-    return outs, all_cands
+    # return_packed: also the gathered [world][H*d | H*2] partial blocks
+    return (outs, all_cands, all_packed) if return_packed else (outs, all_cands)

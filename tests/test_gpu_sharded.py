@@ -68,10 +68,11 @@ def test_sharded_decode_matches_oracle(world):
         N = n + step
         o_ref, hit_ref, sel_ref = ref.decode(q, kt, vt)
         qd, kd, vd = (torch.from_numpy(x).cuda() for x in (q, kt, vt))
-        outs, all_cands = sharded.simulate_step(shards, [(qd, kd, vd)] * world, bases, N)
+        outs, all_cands, all_packed = sharded.simulate_step(shards, [(qd, kd, vd)] * world, bases, N,
+                                                            return_packed=True)
         torch.cuda.synchronize()
         # the two-array combine over the same blocks is the same merge
-        blocks = sharded.simulate_step.last_packed.view(world, -1)
+        blocks = all_packed.view(world, -1)
         two = shards[0].combine(blocks[:, : H * d].reshape(-1), blocks[:, H * d:].reshape(-1))
         assert torch.equal(two, outs[0]), "packed and two-array combines disagree"
         outs = [o.cpu().numpy() for o in outs]
