@@ -1601,6 +1601,8 @@ ts_status ts_shard_attend(ts_engine* e, const uint32_t* all_cands, float* out_pa
     const DeviceInfo& di = device_info();
     const Plan pl = make_plan(static_cast<int>(c.num_heads), static_cast<int>(c.num_kv_heads),
                               static_cast<int>(c.head_dim), 1, 0, di.num_sms * 64);
+    p.trace = e->trace_on ? e->trace.as<unsigned long long>() : nullptr;
+    if (p.trace) ck(cudaMemsetAsync(p.trace, 0, kTraceSlots * 8, st), "memset trace");
     launch_decode(p, pl, e->ws, st);
     if (appended) s.len += 1;
   });
