@@ -90,7 +90,9 @@ class NativeShard:
         # engine's own stream": pass cudaStreamLegacy (0x1) instead so both
         # sides order on the same stream
         st = torch.cuda.current_stream().cuda_stream or 1
-        check(lib.ts_engine_set_stream(self._h, C.c_void_p(st)))
+        self._stream = C.c_void_p(st)
+        check(lib.ts_engine_set_stream(self._h, self._stream))
+        self._out = torch.empty(1, num_heads * head_dim, dtype=torch.float32, device=dev)
 
     def __del__(self):
         if getattr(self, "_h", None) and lib is not None:
@@ -133,9 +135,11 @@ class NativeShard:
         return self._pm
 
     def combine_packed(self, all_packed):
-        out = self.torch.empty(1, self.H * self.d, dtype=self.torch.float32, device=all_packed.device)
+        """The step's [1 x H*d] output, on the engine's stream (like the
+        other phases). The buffer is reused by the next step's combine."""
+        out = self._out
         check(lib.ts_shard_combine_packed(self._p(all_packed), self.world, self.H, self.d, self._p(out),
-                                          C.c_void_p(self.torch.cuda.current_stream().cuda_stream)))
+                                          self._stream))
         return out
 
     def combine(self, all_part, all_ml):
@@ -162,6 +166,8 @@ class TorchDistExchange:
         import torch
 
         t = t.contiguous()
+        if self.world == 1:
+            return t  # a one-rank all-gather is the identity
         if self.nccl:
             key = (t.numel(), t.dtype, t.device)
             out = self._out.get(key)
