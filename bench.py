@@ -364,15 +364,16 @@ def run_decode_sharded(args, rank, world, local_rank):
     qs_e = rotating_stream(args.steps, seed + 7)
     ks_e, vs_e = step_kv(args.steps, seed + 7)
     e2e = []
+    pins = [torch.empty(x[0].size, dtype=torch.float32).pin_memory() for x in (qs_e, ks_e, vs_e)]
     for t in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize(dev)
         torch.distributed.barrier()
         t0 = time.perf_counter()
         with torch.cuda.stream(stream):
-            q = torch.from_numpy(qs_e[t]).pin_memory().to(dev, non_blocking=True).view(-1)
-            k = torch.from_numpy(ks_e[t]).pin_memory().to(dev, non_blocking=True).view(-1)
-            v = torch.from_numpy(vs_e[t]).pin_memory().to(dev, non_blocking=True).view(-1)
+            for pin, x in zip(pins, (qs_e[t], ks_e[t], vs_e[t])):
+                pin.copy_(torch.from_numpy(x).view(-1))  # host buffer -> pinned staging
+            q, k, v = (pin.to(dev, non_blocking=True) for pin in pins)
             sharded.decode_step(shard, ex, q, k, v, rr.base, n_global + total + t).cpu()
         e2e.append(time.perf_counter() - t0)
     mt = torch.tensor(step_us + [1e6 * statistics.mean(e2e)], device=dev, dtype=torch.float64)
