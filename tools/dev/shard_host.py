@@ -18,6 +18,17 @@ shard = sharded.NativeShard(0, 1, N + 4096, k=2048, n_local=512, n_init=128, chu
 K = torch.randn(N, Hkv * d, device="cuda").to(torch.bfloat16).view(torch.uint16)
 shard.append_bf16(K, K)
 ex = sharded.TorchDistExchange()
+if os.environ.get("FORCE_NCCL_GATHER"):  # time the NCCL all-gather even at world 1
+    class _Ex(sharded.TorchDistExchange):
+        def all_gather(self, t):
+            w, self.world = self.world, 2
+            try:
+                out = torch.empty(t.numel(), dtype=t.dtype, device=t.device)
+                self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
+                return out
+            finally:
+                self.world = w
+    ex = _Ex()
 q = torch.randn(H * d, device="cuda")
 kt = torch.randn(Hkv * d, device="cuda")
 names = ["stats", "gather stats", "select", "gather cands", "attend", "gather partials", "combine"]
