@@ -164,18 +164,83 @@ def reference_engine(kind: str):
     return Oracle(kind), kind
 
 
-def time_reference(steps: int, warmup: int, seed: int = 1):
-    """The reference's own decode_step (attention.cpp:172-200) on this host,
-    same config and stream shape. Single-threaded by design (README:192-193)."""
+def host_string() -> str:
+    """CPU model and core count of this host (hardware_string,
+    selattn_bench.cpp:133-145)."""
+    model = "unknown CPU"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return f"{model}, nproc {os.cpu_count()}"
+
+
+def reference_pool(seed: int = 1, steps: int = 0):
     o, kind = reference_engine("reference")
     g = np.random.default_rng(seed)
-    eng = o.engine(N_CTX + warmup + steps + 8, k=K_SEL, n_local=N_LOCAL, n_init=N_INIT, chunk_size=512,
+    eng = o.engine(N_CTX + steps + 64, k=K_SEL, n_local=N_LOCAL, n_init=N_INIT, chunk_size=512,
                    theta=THETA, num_heads=H, num_kv_heads=H_KV, head_dim=D, block_size=64)
     chunk = 16384
     for s0 in range(0, N_CTX, chunk):
         kk = (g.standard_normal((chunk, H_KV * D)) * 3.0).astype(np.float32)
         vv = g.standard_normal((chunk, H_KV * D)).astype(np.float32)
         eng.append(kk, vv)
+    return eng, kind
+
+
+def time_reference_split(n_miss: int = 5, n_hit: int = 5, warmup: int = 2, seed: int = 1):
+    """The reference's own decode_step (attention.cpp:172-200) on this host at
+    the bench's config, with the reference bench's methodology
+    (selattn_bench.cpp:147-159, 243-252): median of >= 5 timed calls after 2
+    warm-ups (monotonic clock), misses (forced with first_flag, the
+    cmd_cache_stats idiom at :439) and hits (the same query again) timed
+    separately. Single-threaded by design (README:192-193)."""
+    eng, kind = reference_pool(seed, warmup + n_miss + n_hit + 1)
+    qs = rotating_stream(warmup + n_miss + 1, seed)
+    ks, vs = step_kv(warmup + n_miss + n_hit + 1, seed)
+    miss, hit = [], []
+    t = 0
+    for i in range(warmup + n_miss):
+        eng.force_miss()
+        t0 = time.perf_counter()
+        _, h, _ = eng.decode(qs[i], ks[t], vs[t])
+        dt = time.perf_counter() - t0
+        assert not h
+        t += 1
+        if i >= warmup:
+            miss.append(dt)
+    q_last = qs[warmup + n_miss - 1]
+    for i in range(n_hit):
+        t0 = time.perf_counter()
+        _, h, _ = eng.decode(q_last, ks[t], vs[t])
+        dt = time.perf_counter() - t0
+        assert h
+        t += 1
+        hit.append(dt)
+    return 1e6 * statistics.median(miss), 1e6 * statistics.median(hit), kind
+
+
+def cpu_baseline_line(kinds, n_miss=5, n_hit=5, warmup=2):
+    """cpu_baseline object: the reference's median miss / hit step, weighted
+    by the hit rate of the GPU arm's own stream."""
+    miss_us, hit_us, kind = time_reference_split(n_miss, n_hit, warmup)
+    n_h = sum(kinds)
+    value = (miss_us * (len(kinds) - n_h) + hit_us * n_h) / len(kinds)
+    sample = (f"reference decode_step at {N_CTX // 1024}K context: median of {n_miss} forced misses and of {n_hit} "
+              f"hits after {warmup} warm-ups, weighted by this stream's {len(kinds) - n_h} misses / {n_h} hits; "
+              f"1 of {os.cpu_count()} host cores ({host_string()})")
+    return {"value": round(value, 1), "unit": UNIT, "cores": 1, "kind": kind, "sample": sample,
+            "miss_us": round(miss_us, 1), "hit_us": round(hit_us, 1), "host": host_string()}
+
+
+def time_reference(steps: int, warmup: int, seed: int = 1):
+    """--impl reference: the reference's decode_step over the bench's own
+    rotating stream (same config, metric and step count as our arm)."""
+    eng, kind = reference_pool(seed, warmup + steps)
     qs = rotating_stream(warmup + steps, seed)
     ks, vs = step_kv(warmup + steps, seed)
     times, hits = [], 0
@@ -188,7 +253,8 @@ def time_reference(steps: int, warmup: int, seed: int = 1):
             hits += int(hit)
     us = 1e6 * sum(times) / len(times)
     sample = (f"{len(times)} reference decode_step calls at {N_CTX // 1024}K context after {warmup} warm-up, "
-              f"rotating stream sim {SIMILARITY}, theta {THETA}: {len(times) - hits} misses / {hits} hits")
+              f"rotating stream sim {SIMILARITY}, theta {THETA}: {len(times) - hits} misses / {hits} hits; "
+              f"1 of {os.cpu_count()} host cores ({host_string()})")
     return us, kind, sample
 
 
@@ -207,11 +273,12 @@ def fill_bf16(append, n, kv_dim, dev, seed, chunk=16384, seq=None):
             append(kk, vv, seq)
 
 
-def timed_steps(stream, flush, run_step, steps, warmup, local_rank, world):
+def timed_steps(stream, flush, run_step, steps, warmup, local_rank, world, counter=None):
     """W untimed steps, then K steps each bracketed by CUDA events on `stream`,
     each preceded by an L2 flush (512 MB write) unless `flush` is empty
-    (inputs larger than L2); barrier + synchronize on both sides. Returns
-    per-step device us and the clock summary."""
+    (inputs larger than L2); barrier + synchronize on both sides. The timed
+    steps are queued ahead of the GPU (behind a device sleep), so a step's
+    time is its device time. Returns per-step device us and the clock summary."""
     import torch
 
     dev = torch.device("cuda", local_rank)
@@ -224,8 +291,15 @@ def timed_steps(stream, flush, run_step, steps, warmup, local_rank, world):
     if world > 1:
         torch.distributed.barrier()
     evs = []
+    c0 = counter() if counter else 0
     with ClockSampler(local_rank) as clk:
         torch.cuda.synchronize(dev)
+        # the K steps are queued behind a device-side sleep, so they run
+        # back to back on the GPU (as in a captured decode loop) and no step's
+        # events include the host's launch latency; the sleep itself is
+        # outside every step's event pair
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(int(2e6 + 2e5 * steps * (8 if world > 1 else 1)))  # ~1 ms + 0.1 ms/step (cycles)
         for t in range(steps):
             if flush.numel():
                 with torch.cuda.stream(stream):
@@ -237,9 +311,10 @@ def timed_steps(stream, flush, run_step, steps, warmup, local_rank, world):
             e1.record(stream)
             evs.append((e0, e1))
         torch.cuda.synchronize(dev)
+    launches = (counter() - c0) if counter else None  # our kernels launched in the timed region
     if world > 1:
         torch.distributed.barrier()
-    return [a.elapsed_time(b) * 1000.0 for a, b in evs], clk.summary()
+    return [a.elapsed_time(b) * 1000.0 for a, b in evs], clk.summary(), launches
 
 
 def split_by_kind(step_us, kinds):
@@ -288,10 +363,9 @@ def run_decode_single(args, local_rank):
         L, t = i % LAYERS, i // LAYERS
         engines[L].decode_async(qs[L][t], ks[L][t], vs[L][t], out)
 
-    launches0 = sa.launch_count()
     st0 = [eng.stats() for eng in engines]
-    step_us, clocks = timed_steps(stream, no_flush, step, args.steps, args.warmup, local_rank, 1)
-    launches = sa.launch_count() - launches0 - args.warmup  # timed region only (1 launch per step)
+    step_us, clocks, launches = timed_steps(stream, no_flush, step, args.steps, args.warmup, local_rank, 1,
+                                            sa.launch_count)
     st1 = [eng.stats() for eng in engines]
     kinds_l = [cache_decisions(q, THETA) for q in qs_h]
     all_kinds = [kinds_l[i % LAYERS][i // LAYERS] for i in range(total)]
@@ -320,7 +394,7 @@ def run_decode_single(args, local_rank):
         engines[L].decode_into(qs_e[L][t], kv_e[L][0][t], kv_e[L][1][t], out_h, hit_h)
         e2e.append(time.perf_counter() - t0)
     return {"step_us": statistics.mean(step_us), "miss_us": miss_us, "hit_us": hit_us, "hits": hits,
-            "lookups": lookups, "alg_bytes": alg, "launches": launches, "clocks": clocks,
+            "lookups": lookups, "kinds": kinds, "alg_bytes": alg, "launches": launches, "clocks": clocks,
             "e2e_us": 1e6 * statistics.mean(e2e), "h2d": (H * D + 2 * H_KV * D) * 4, "d2h": H * D * 4 + 48,
             "miss_bytes": algorithmic_bytes(n_mean, True), "hit_bytes": algorithmic_bytes(n_mean, False),
             "n_ctx": N_CTX, "per_gpu_bytes_div": 1}
@@ -336,7 +410,7 @@ def run_decode_sharded(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     total = args.warmup + args.steps
-    n_global = N_CTX * world
+    n_global = args.context or N_CTX * world
     ranges = sharded.shard_ranges(n_global, world, N_INIT, N_LOCAL)
     rr = ranges[rank]
     stream = torch.cuda.Stream(dev)
@@ -356,9 +430,8 @@ def run_decode_sharded(args, rank, world, local_rank):
         with torch.cuda.stream(stream):
             sharded.decode_step(shard, ex, qs[i].view(-1), ks[i].view(-1), vs[i].view(-1), rr.base, n_global + i)
 
-    launches0 = sa.launch_count()
-    step_us, clocks = timed_steps(stream, flush, step, args.steps, args.warmup, local_rank, world)
-    launches = sa.launch_count() - launches0 - 4 * args.warmup
+    step_us, clocks, launches = timed_steps(stream, flush, step, args.steps, args.warmup, local_rank, world,
+                                            sa.launch_count)
     kinds = cache_decisions(qs_h, THETA)[args.warmup:]
     # end-to-end: host q/k/v -> H2D, the sharded step, D2H of the output
     qs_e = rotating_stream(args.steps, seed + 7)
@@ -412,10 +485,8 @@ def run_batched(args, local_rank):
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.Stream(dev)
     eng.set_stream(stream.cuda_stream)
-    launches0 = sa.launch_count()
-    step_us, clocks = timed_steps(stream, flush, lambda i: eng.decode_async(qs[i], ks[i], vs[i], out), args.steps,
-                                  args.warmup, local_rank, 1)
-    launches = sa.launch_count() - launches0 - args.warmup
+    step_us, clocks, launches = timed_steps(stream, flush, lambda i: eng.decode_async(qs[i], ks[i], vs[i], out),
+                                            args.steps, args.warmup, local_rank, 1, sa.launch_count)
     kinds_b = [cache_decisions(qs_h[:, b], THETA)[args.warmup:] for b in range(B)]
     n_mean = n + args.warmup + args.steps // 2
     alg = sum(sum(algorithmic_bytes(n_mean, not kb[t], h, hkv, d) for kb in kinds_b)
@@ -448,10 +519,8 @@ def run_prefill(args, local_rank):
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.Stream(dev)
     eng.set_stream(stream.cuda_stream)
-    launches0 = sa.launch_count()
-    step_us, clocks = timed_steps(stream, flush, lambda i: eng.prefill(q[i], k[i], v[i]), args.steps, args.warmup,
-                                  local_rank, 1)
-    launches = sa.launch_count() - launches0
+    step_us, clocks, launches = timed_steps(stream, flush, lambda i: eng.prefill(q[i], k[i], v[i]), args.steps,
+                                            args.warmup, local_rank, 1, sa.launch_count)
     R = H_KV * D * 2
     T = N_CTX - N_INIT - N_LOCAL
     alg = T * (R + 4) + C * H * D * 4 + (N_INIT + K_SEL + N_LOCAL) * 2 * R + 2 * C * R + C * H * D * 4
@@ -495,8 +564,23 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--context", type=int, default=0,
+                    help="sharded workload: total context tokens (strong scaling, e.g. 1048576 for configs[3] "
+                         "at every N); default N x 128K (weak scaling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` without a launcher: re-execute under
+        # torch.distributed.run, one rank per GPU (rank 0 prints the line)
+        import socket
+
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
@@ -513,7 +597,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        steps = min(args.steps, 10)
+        steps = min(args.steps, 100)  # our arm's step count (bounded: ~1.8 s per reference miss)
         us, kind, sample = time_reference(steps, 2)
         config["context_tokens"] = N_CTX
         line = {"impl": "reference", "metric": METRIC, "value": round(us, 1), "unit": UNIT, "n_gpus": args.gpus,
@@ -528,7 +612,11 @@ def main():
         import torch
 
         torch.cuda.set_device(local_rank)
-        os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
+        # NCCL's communicator lines (transport, NVLS, ranks) go to stderr; stdout
+        # stays the one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,ENV")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29531")
         torch.distributed.init_process_group("nccl", rank=rank, world_size=world,
@@ -564,7 +652,8 @@ def main():
     line = {
         "metric": METRIC, "value": round(r["step_us"], 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(r["step_us"] / 1000, 5), "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "scaling": "strong" if (workload == "sharded" and args.context) else "weak", "vs_baseline": None,
+        "dtype": "bf16",
         "data": "synthetic (random bf16 KV, rotating query stream)", "config": config,
         "cache": {"lookups": r["lookups"], "hits": r["hits"]},
         "miss_step_us": round(r["miss_us"], 2) if r["miss_us"] else None,
@@ -572,12 +661,11 @@ def main():
         "roofline": roof,
         "e2e": ({"value": round(r["e2e_us"], 2), "unit": UNIT, "h2d_bytes_per_step": r["h2d"],
                  "d2h_bytes_per_step": r["d2h"]} if r["e2e_us"] else None),
-        "clocks": r["clocks"], "gpu_launches": r["launches"],
+        "clocks": r["clocks"], "gpu_launches": r["launches"], "gpus_active": world,
     }
     if rank == 0 and world == 1 and workload == "decode" and not args.no_cpu_baseline:
         try:
-            us, kind, sample = time_reference(4, 1)
-            line["cpu_baseline"] = {"value": round(us, 1), "unit": UNIT, "cores": 1, "kind": kind, "sample": sample}
+            line["cpu_baseline"] = cpu_baseline_line(r["kinds"])
         except Exception as e:  # the oracle build is test infrastructure; report, do not fail the bench
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                                     "sample": f"unavailable: {e}"}

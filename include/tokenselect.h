@@ -164,8 +164,12 @@ ts_status ts_engine_prefill(ts_engine* eng, size_t seq, const float* q, const fl
 ts_status ts_engine_decode(ts_engine* eng, const float* q, const float* k, const float* v,
                            float* out, int* cache_hit, uint32_t* sel_out, size_t* n_sel);
 /* Stream-ordered variant for device-resident inputs/outputs: no host sync,
- * no D2H. Query validity (non-zero) is checked on the device and reported
- * by the next ts_engine_stats call. */
+ * no D2H. Query validity (non-zero) is checked on the device: a zero query
+ * makes the step append nothing and leave the Selection Cache untouched
+ * (the reference throws before any mutation, selection_cache.cpp:18-27).
+ * The next ts_engine_sync / ts_engine_stats call (before another step) rolls
+ * the host's length back and returns TS_INVALID_ARGUMENT. ts_engine_decode
+ * (blocking) reports it from the same call. */
 ts_status ts_engine_decode_async(ts_engine* eng, const float* q, const float* k, const float* v,
                                  float* out);
 /* Forces the next lookup of sequence `seq` to miss (first_flag = true,

@@ -503,6 +503,10 @@ struct ts_engine {
   CacheState* h_cache = nullptr;
   uint32_t* h_sel = nullptr;
   Workspace ws;
+  // frames the last decode step appended, per sequence (-1: none); a step
+  // the device rejected (zero query) is rolled back with them
+  std::vector<int64_t> last_frames;
+  bool last_unchecked = false;  // decode_async: the step's error flag is read at the next sync / stats
   // device phase trace (%globaltimer stamps of CTA 0), when enabled
   DevBuf trace;
   bool trace_on = false;
@@ -1082,6 +1086,7 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
   const ts_engine_config& c = e->cfg;
   const size_t W = e->W(), KW = e->KW();
   std::vector<int> cap_fail(e->B, 0);
+  e->last_frames.assign(e->B, -1);
   cudaStream_t st = e->stream;
   for (size_t g0 = 0; g0 < e->B; g0 += tsb::kMaxSeqPerLaunch) {
     const double t0 = g_host_prof ? now_ns() : 0.0;
@@ -1125,6 +1130,7 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
         const uint32_t f = pool.free_list.back();
         pool.free_list.pop_back();
         s.frames.push_back(f);
+        e->last_frames[b] = f;
         sd.append_frame = static_cast<int32_t>(f);
         sd.append_slot = 0;
         sd.append_page = static_cast<int32_t>(N);
@@ -1150,6 +1156,34 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
       if (!cap_fail[g0 + i]) pool.state(e->seq_ids[g0 + i]).len += 1;
   }
   return cap_fail;
+}
+
+// Undoes the host side of the last step for sequence b (the device skipped
+// its append: zero query, reported through CacheState::error).
+void rollback_step(ts_engine* e, size_t b) {
+  if (b >= e->last_frames.size() || e->last_frames[b] < 0) return;
+  ts_pool& pool = *e->pool;
+  ts_pool::Seq& s = pool.state(e->seq_ids[b]);
+  s.frames.pop_back();
+  s.len -= 1;
+  pool.free_list.push_back(static_cast<uint32_t>(e->last_frames[b]));
+  e->last_frames[b] = -1;
+}
+
+// decode_async: reads the last step's per-sequence error flags (the stream is
+// synchronised by the caller), rolls back the rejected sequences and throws.
+void check_async_errors(ts_engine* e) {
+  if (!e->last_unchecked) return;
+  e->last_unchecked = false;
+  std::vector<CacheState> cs(e->B);
+  ck(cudaMemcpy(cs.data(), e->cache(0), e->B * sizeof(CacheState), cudaMemcpyDeviceToHost), "D2H");
+  bool bad = false;
+  for (size_t b = 0; b < e->B; ++b)
+    if (cs[b].error) {
+      rollback_step(e, b);
+      bad = true;
+    }
+  if (bad) fail(TS_INVALID_ARGUMENT, "lookup_or_select: zero query vector");
 }
 
 }  // namespace
@@ -1210,6 +1244,7 @@ ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const f
     }
     if (g_host_prof) tp[2] = now_ns();
     std::vector<int> cap_fail = engine_step(e, qd, kd, vd, od);
+    e->last_unchecked = false;  // checked below
     if (g_host_prof) tp[3] = now_ns();
     // every result rides one stream sync: output, cache states and (when
     // requested) the full selection slots
@@ -1231,7 +1266,11 @@ ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const f
     ts_pool& pool = *e->pool;
     for (size_t b = 0; b < B; ++b) {
       const CacheState& cs = e->h_cache[b];
-      if (cs.error) fail(TS_INVALID_ARGUMENT, "lookup_or_select: zero query vector");
+      if (cs.error) {
+        for (size_t b2 = 0; b2 < B; ++b2)
+          if (e->h_cache[b2].error) rollback_step(e, b2);
+        fail(TS_INVALID_ARGUMENT, "lookup_or_select: zero query vector");
+      }
       // the step ran a lookup iff selection was on for the sequence at step start
       const size_t N_after = pool.state(e->seq_ids[b]).len;
       const size_t N = N_after - (cap_fail[b] ? 0 : 1);
@@ -1255,6 +1294,7 @@ ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const f
 
 ts_status ts_engine_decode_async(ts_engine* e, const float* q, const float* k, const float* v, float* out) {
   return guarded([&] {
+    e->last_unchecked = true;
     std::vector<int> cap_fail = engine_step(e, q, k, v, out);
     for (size_t b = 0; b < e->B; ++b)
       if (cap_fail[b]) fail(TS_CAPACITY, "append_kv: pool exhausted (need 1 frames, 0 free)");
@@ -1304,16 +1344,13 @@ ts_status ts_engine_stats(const ts_engine* e, size_t seq, size_t* lookups, size_
     CacheState cs{};
     ck(cudaMemcpyAsync(&cs, e->cache(seq), sizeof(CacheState), cudaMemcpyDeviceToHost, e->stream), "D2H");
     ck(cudaStreamSynchronize(e->stream), "sync");
+    // the last (async) step rejected on the device: rolled back and reported
+    if (cs.error && e->last_unchecked) check_async_errors(const_cast<ts_engine*>(e));
     if (lookups) *lookups = cs.lookups;
     if (hits) *hits = cs.hits;
     if (len) *len = e->pool->state(e->seq_ids[seq]).len;
     if (last_hit) *last_hit = cs.last_hit;
     if (last_cos) *last_cos = cs.last_cos;
-    if (cs.error) {
-      const int zero = 0;
-      ck(cudaMemcpy(&e->cache(seq)->error, &zero, sizeof(int), cudaMemcpyHostToDevice), "H2D");
-      fail(TS_INVALID_ARGUMENT, "lookup_or_select: zero query vector");
-    }
   });
 }
 
@@ -1336,7 +1373,10 @@ ts_status ts_engine_cached_selection(const ts_engine* e, size_t seq, uint32_t* s
 }
 
 ts_status ts_engine_sync(ts_engine* e) {
-  return guarded([&] { ck(cudaStreamSynchronize(e->stream), "sync"); });
+  return guarded([&] {
+    ck(cudaStreamSynchronize(e->stream), "sync");
+    check_async_errors(e);
+  });
 }
 
 ts_status ts_engine_prefill(ts_engine* e, size_t seq, const float* q, const float* k, const float* v, size_t n,

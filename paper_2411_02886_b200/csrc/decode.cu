@@ -1420,15 +1420,6 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   const bool dec_early = sd.select && !(pmode & kModeShardSelect) && (pmode & kModeCache);
   if (dec_early) decision_issue(sd, width, dl);
   stamp(trc, 45);
-  if ((pmode & kModeAppend) && cs == 0 && sd.append_frame >= 0) {
-    const int row = p.H_kv * p.d;
-    const size_t off = (static_cast<size_t>(sd.append_frame) * p.page_size + sd.append_slot) * row;
-    for (int i = tid; i < row; i += blockDim.x) {
-      p.k_slab_w[off + i] = __bfloat16_as_ushort(__float2bfloat16_rn(sd.k_new[i]));
-      p.v_slab_w[off + i] = __bfloat16_as_ushort(__float2bfloat16_rn(sd.v_new[i]));
-    }
-    if (tid == 0 && sd.append_page >= 0) sd.page_table[sd.append_page] = sd.append_frame;
-  }
   const int T = sd.n_cand;
   const int j0 = min(T, cs * p.tpc);
   const int nloc = max(0, min(T, j0 + p.tpc) - j0);
@@ -1551,7 +1542,22 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     uint32_t* gh = p.ws_hist + static_cast<size_t>(seq_id) * 2 * kHistPass;
     for (int i = cs * blockDim.x + tid; i < 2 * kHistPass; i += p.ctas_per_seq * blockDim.x) gh[i] = 0u;
   }
-  if (cs == 0 && tid == 0 && own == 3) sd.cache->error = 1;
+  // zero query (lookup_or_select throws before any mutation,
+  // selection_cache.cpp:18-27): the flag is per step, and the step appends
+  // nothing and leaves the cache entry untouched
+  if (cs == 0 && tid == 0 && sd.select && (pmode & kModeCache)) sd.cache->error = own == 3 ? 1 : 0;
+  // append of the current token's row (kv_pool.cpp:55-85), after the decision.
+  // This step never reads row N: the candidates end at N - n_local and the
+  // current token is attended from k_new / v_new.
+  if ((pmode & kModeAppend) && cs == 0 && sd.append_frame >= 0 && own != 3) {
+    const int row = p.H_kv * p.d;
+    const size_t off = (static_cast<size_t>(sd.append_frame) * p.page_size + sd.append_slot) * row;
+    for (int i = tid; i < row; i += blockDim.x) {
+      p.k_slab_w[off + i] = __bfloat16_as_ushort(__float2bfloat16_rn(sd.k_new[i]));
+      p.v_slab_w[off + i] = __bfloat16_as_ushort(__float2bfloat16_rn(sd.v_new[i]));
+    }
+    if (tid == 0 && sd.append_page >= 0) sd.page_table[sd.append_page] = sd.append_frame;
+  }
   // LEAN miss: S goes to tensor memory (the whole 512 columns; one CTA per SM)
   const bool use_tmem = LEAN && own == 1;
   if (use_tmem && tid < 32) tmem_alloc512(&sm.scratch[kScratchTmem]);

