@@ -24,6 +24,7 @@
 #include "../../include/tokenselect.h"
 #include "aux.h"
 #include "decode.h"
+#include "step.h"
 #include "params.h"
 
 using tsb::CacheState;
@@ -37,6 +38,9 @@ const bool g_force_global_s = std::getenv("TS_FORCE_GLOBAL_S") != nullptr && std
 const int g_debug_flags = std::getenv("TS_DEBUG_FLAGS") ? std::atoi(std::getenv("TS_DEBUG_FLAGS")) : 0;
 const bool g_force_cuda_core_prefill = std::getenv("TS_CUDA_CORE_PREFILL") != nullptr;
 const bool g_no_lean = std::getenv("TS_NO_LEAN") != nullptr;  // dev: always the general kernel
+// the single-sequence step kernel (step.cu) is opt-in: TS_STEP=1. Measured on
+// B200 (profiles/r02_step/): stream 54.1 vs 52.5 us/step for the fused kernel
+const bool g_no_step = !(std::getenv("TS_STEP") && std::getenv("TS_STEP")[0] == '1');
 const bool g_no_tma = std::getenv("TS_NO_TMA") != nullptr;      // dev: row-by-row scan copies
 const bool g_no_h2d_primer = std::getenv("TS_NO_H2D_PRIMER") != nullptr;  // dev: see ts_engine_decode
 const bool g_debug_tma = std::getenv("TS_DEBUG_TMA") != nullptr;
@@ -367,6 +371,107 @@ void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t 
   g_launches.fetch_add(1);
 }
 
+// Workspace of the single-sequence step kernel (step.cu).
+struct StepWorkspace {
+  DevBuf mz, hist, cnt, nsel, o, ml, bar;
+  unsigned launches = 0;
+};
+
+// The step kernel's launch geometry for one sequence with T candidates, or
+// ok = false when the shape is outside it (the fused decode kernel then runs).
+struct StepPlan {
+  bool ok = false;
+  int ncta = 0, tpc = 16, spw = 1, stages = 0, G = 0;
+  size_t smem = 0;
+  const void* fn = nullptr;
+};
+
+StepPlan step_plan(const ts_engine_config& c, int T, int W) {
+  StepPlan sp;
+  const DeviceInfo& di = device_info();
+  const int H = static_cast<int>(c.num_heads), Hkv = static_cast<int>(c.num_kv_heads);
+  if (g_no_step || c.head_dim != 128 || c.selection_method != TS_HEAD_SOFT_VOTE || H > 64 || Hkv > 16 ||
+      tsb::kDecodeConsumers % Hkv || H % Hkv)
+    return sp;
+  const int G = H / Hkv;
+  if (G > 8) return sp;
+  const int ncta = di.num_sms;
+  if (ncta < 32 || ncta > 272 || (H * 128 + ncta - 1) / ncta > 128) return sp;  // step.cu: 2 * ncta <= threads
+  const int nph = tsb::kDecodeConsumers / Hkv;
+  const int tpc = static_cast<int>(tsb::align_up(static_cast<size_t>(std::max(1, (T + ncta - 1) / ncta)), 16));
+  const int spw = std::max(1, (tpc / 16 + nph - 1) / nph);
+  const int cps = G <= 4 ? 2 : 4;
+  if (spw * cps > 128) return sp;                                   // TMEM: 128 columns per warp
+  if ((static_cast<int>(c.k) + ncta - 1) / ncta > 64 || (W + ncta - 1) / ncta > 64) return sp;
+  const size_t row_bytes = static_cast<size_t>(Hkv) * 256;
+  const size_t sbytes = 16 * (row_bytes + 16);
+  const size_t optin = static_cast<size_t>(di.smem_optin);
+  int stages = std::min(16, tsb::kMaxBarPairs / nph);
+  while (stages >= 2 && tsb::step_smem_bytes(H, Hkv, tpc, spw, stages) > optin) --stages;
+  if (stages < 2) return sp;
+  // post-scan aliases of the ring (step.cu): histogram + criticality partials
+  // + keys, attention staging + scores + phase sums, and the selected list at its end
+  const size_t ring = tsb::align_up(static_cast<size_t>(stages) * sbytes, 1024);
+  const size_t tail = ring - static_cast<size_t>(3) * tpc * 4;
+  const size_t crit_end = 17 * 1024 + static_cast<size_t>(Hkv) * tpc * 4 + static_cast<size_t>(tpc) * 4;
+  const size_t att_end = 2 * tsb::kStepRowsPerBatch * row_bytes + (tsb::kStepRowsPerBatch + 1) * 64 * 4 +
+                         static_cast<size_t>(nph) * H * 128 * 4;
+  const size_t merge_end = static_cast<size_t>(4 * ncta + ncta * 128 + 8 + 128 * ((ncta + 7) / 8)) * 4;
+  if (crit_end > tail || att_end > tail || merge_end > tail) return sp;
+  sp.fn = tsb::step_kernel_ptr(G);
+  if (!sp.fn) return sp;
+  sp.ok = true;
+  sp.ncta = ncta;
+  sp.tpc = tpc;
+  sp.spw = spw;
+  sp.stages = stages;
+  sp.G = G;
+  sp.smem = tsb::step_smem_bytes(H, Hkv, tpc, spw, stages);
+  return sp;
+}
+
+void launch_step(tsb::StepParams& p, const StepPlan& sp, StepWorkspace& ws, cudaStream_t st) {
+  const int ncta = sp.ncta, ncp = (ncta + 3) & ~3;
+  ws.mz.ensure(static_cast<size_t>(p.H) * ncp * 8);
+  ws.hist.ensure(2 * tsb::kRadixBins * 4);
+  ws.cnt.ensure(static_cast<size_t>(ncta) * 4);
+  ws.nsel.ensure(static_cast<size_t>(ncta) * 4);
+  ws.o.ensure(static_cast<size_t>(ncta) * p.H * 128 * 4);
+  ws.ml.ensure(static_cast<size_t>(ncta) * p.H * 8);
+  if (!ws.bar.p) {
+    ws.bar.ensure(256);
+    ck(cudaMemsetAsync(ws.bar.p, 0, 256, st), "memset barrier");
+  }
+  p.tpc = sp.tpc;
+  p.stages_per_warp = sp.spw;
+  p.ring_stages = sp.stages;
+  p.ws_mz = ws.mz.as<float2>();
+  p.ws_hist = ws.hist.as<uint32_t>();
+  p.ws_cnt = ws.cnt.as<uint32_t>();
+  p.ws_nsel = ws.nsel.as<uint32_t>();
+  p.ws_o = ws.o.as<float>();
+  p.ws_ml = ws.ml.as<float2>();
+  p.bar = ws.bar.as<unsigned int>();
+  p.bar_slot = (ws.launches & 1u) ? 32 : 0;
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> smem_set;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& have = smem_set[sp.fn];
+    if (sp.smem > have) {
+      ck(cudaFuncSetAttribute(sp.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sp.smem)),
+         "cudaFuncSetAttribute");
+      have = sp.smem;
+    }
+  }
+  void* args[] = {&p};
+  const double t0 = g_host_prof ? now_ns() : 0.0;
+  ck(cudaLaunchCooperativeKernel(sp.fn, dim3(ncta), dim3(tsb::kStepThreads), args, sp.smem, st), "step kernel launch");
+  if (g_host_prof) g_prof[3] += now_ns() - t0;
+  ws.launches += 1;
+  g_launches.fetch_add(1);
+}
+
 // selattn::Rng::index semantics (rng.hpp:19-26) on std::mt19937_64, so the
 // shuffled free list is the reference's permutation.
 struct RefRng {
@@ -503,6 +608,7 @@ struct ts_engine {
   CacheState* h_cache = nullptr;
   uint32_t* h_sel = nullptr;
   Workspace ws;
+  StepWorkspace sws;  // the single-sequence step kernel's
   // frames the last decode step appended, per sequence (-1: none); a step
   // the device rejected (zero query) is rolled back with them
   std::vector<int64_t> last_frames;
@@ -1088,6 +1194,55 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
   std::vector<int> cap_fail(e->B, 0);
   e->last_frames.assign(e->B, -1);
   cudaStream_t st = e->stream;
+  if (e->B == 1 && e->rank == 0 && e->world == 1) {
+    ts_pool::Seq& s = pool.state(e->seq_ids[0]);
+    const size_t N = s.len;
+    const bool sel_on = c.k > 0 && N > c.n_init + c.n_local;
+    const int T = sel_on ? static_cast<int>(N - c.n_init - c.n_local) : 0;
+    const StepPlan sp = step_plan(c, T, static_cast<int>(c.n_init + c.n_local + 1));
+    if (sp.ok) {
+      tsb::StepParams p{};
+      p.k_slab = pool.k_slab;
+      p.v_slab = pool.v_slab;
+      p.k_slab_w = pool.k_slab;
+      p.v_slab_w = pool.v_slab;
+      p.page_table = s.d_pt;
+      p.H = static_cast<int>(c.num_heads);
+      p.H_kv = static_cast<int>(c.num_kv_heads);
+      p.k = static_cast<int>(c.k);
+      p.N = static_cast<int>(N);
+      p.select = sel_on ? 1 : 0;
+      p.cand_begin = static_cast<int>(c.n_init);
+      p.T = T;
+      p.init_end = static_cast<int>(std::min(c.n_init, N));
+      p.lb = static_cast<int>(std::max(N - std::min(c.n_local, N), std::min(c.n_init, N)));
+      p.attn_scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c.head_dim)));
+      p.q = q;
+      p.k_new = k;
+      p.v_new = v;
+      p.out = out;
+      p.cache = e->cache(0);
+      p.cached_q = e->cq(0);
+      p.sel = e->sl(0);
+      p.sel_crit = e->sc(0);
+      p.sel_rows = e->sr(0);
+      p.append_frame = -1;
+      if (pool.free_list.empty()) {
+        cap_fail[0] = 1;
+      } else {
+        const uint32_t f = pool.free_list.back();
+        pool.free_list.pop_back();
+        s.frames.push_back(f);
+        e->last_frames[0] = f;
+        p.append_frame = static_cast<int32_t>(f);
+      }
+      p.trace = e->trace_on ? e->trace.as<unsigned long long>() : nullptr;
+      if (p.trace) ck(cudaMemsetAsync(p.trace, 0, kTraceSlots * 8, st), "memset trace");
+      launch_step(p, sp, e->sws, st);
+      if (!cap_fail[0]) s.len += 1;
+      return cap_fail;
+    }
+  }
   for (size_t g0 = 0; g0 < e->B; g0 += tsb::kMaxSeqPerLaunch) {
     const double t0 = g_host_prof ? now_ns() : 0.0;
     const size_t gn = std::min<size_t>(tsb::kMaxSeqPerLaunch, e->B - g0);

@@ -329,6 +329,23 @@ class Engine:
     def force_miss(self, seq=0):
         check(lib.ts_engine_force_miss(self._h, seq))
 
+    # the single-sequence step kernel (csrc/step.cu; slot 63 = 2)
+    STEP_TRACE_POINTS = ["start", "decision", "scan", "stats", "sync1", "crit", "radix1", "radix2", "select",
+                         "att_rows", "attend", "sync4", "merge"]
+    STEP_SUB_POINTS = {13: "crit:stats", 14: "crit:tmem_done", 16: "radix:find1", 17: "radix:hist2", 18: "radix:B3",
+                       19: "att:scores", 20: "att:softmax", 21: "att:pv", 22: "merge:loaded", 23: "merge:weights",
+                       24: "p0:loads_issued", 25: "p0:decided"}
+
+    def trace_names(self):
+        """Slot -> name for read_trace(all_ctas=True) of the last step read."""
+        if getattr(self, "_trace_kid", 0) == 2:
+            names = dict(enumerate(self.STEP_TRACE_POINTS))
+            names.update(self.STEP_SUB_POINTS)
+        else:
+            names = dict(enumerate(self.TRACE_POINTS))
+            names.update(self.SUB_POINTS)
+        return names
+
     TRACE_POINTS = ["start", "decision", "scan", "softmax_partials", "sync1", "crit", "radix1", "radix2",
                     "compact", "sync4", "sel_out", "attend", "merge"]
     # sub-phase stamps (slots 13..63, 29 / 30 reserved) of read_trace(all_ctas=True)
@@ -355,6 +372,7 @@ class Engine:
         check(lib.ts_engine_read_trace(self._h, st.ctypes.data_as(C.c_void_p), st.size))
         raw = st.reshape(1024, 64).astype(np.int64)
         raw = raw[: int(np.count_nonzero(raw[:, 0]))]
+        self._trace_kid = int(raw[0, 63])  # 2: the step kernel (csrc/step.cu)
         # rebase before going to float64 (ns since the epoch exceed its 2^53 mantissa)
         gmin, cmin = raw[:, 0].min(), raw[:, 29].min()
         a = np.where(raw == 0, 0.0, (raw - cmin).astype(np.float64))
@@ -364,22 +382,25 @@ class Engine:
         ok = (g_end > g0) & (c_end > c0)
         rate = np.where(ok, (c_end - c0) / np.where(ok, g_end - g0, 1.0), np.nan)  # cycles per ns
         r = np.nanmedian(rate) if np.any(ok) else 1.9
+        self._trace_rate = float(r)  # SM cycles per ns over the launch
         ns = g0[:, None] + (a - c0[:, None]) / r
         ns[:, 0] = g0
         ns[raw == 0] = np.nan
         ns[:, 29] = np.nan
         ns[:, 30] = np.nan
+        ns[:, 63] = np.nan  # kernel id
         us = ns / 1000.0
         if all_ctas:
             return us
         t = us[0]
+        names = self.STEP_TRACE_POINTS if raw[0, 63] == 2 else self.TRACE_POINTS  # slot 63: kernel id
         out, prev = {}, 0.0
-        for i, name in enumerate(self.TRACE_POINTS[1:], start=1):
+        for i, name in enumerate(names[1:], start=1):
             if not np.isnan(t[i]):
                 out[name] = round(t[i] - prev, 3)
                 prev = t[i]
         out["total"] = prev
-        for i in range(len(self.TRACE_POINTS), 64):  # optional sub-phase stamps, relative to start
+        for i in range(len(self.TRACE_POINTS), 63):  # optional sub-phase stamps, relative to start
             if i not in (29, 30) and not np.isnan(t[i]):
                 out[f"t{i}@"] = round(t[i], 3)
         return out

@@ -25,13 +25,16 @@ def rng_normal(seed: int, shape, scale: float = 1.0) -> np.ndarray:
     return (g.standard_normal(shape) * scale).astype(np.float32)
 
 
+FLT_MIN = float(np.finfo(np.float32).tiny)  # 1.18e-38, smallest normal fp32
 TIE_LOG = []  # (test id, k, swaps) of every check_selection call; written out by conftest
 
 
 def check_selection(ours, ref, crit_ref_full, cand, rel_tol=1e-4, max_swap_frac=0.005):
     """Selected sets must be equal except for indices whose reference
     criticality ties the k-th value: |crit - kth| <= rel_tol * |kth|
-    (no absolute floor). The number of swapped pairs is
+    (SURVEY.md §8(c)). The only absolute floor: when the k-th criticality and
+    the differing one are both below FLT_MIN (fp32 subnormal, flushed to zero
+    by the device's SFU exp), they are reported as underflow ties. The number of swapped pairs is
     returned and bounded: at most max(1, max_swap_frac * k) of the k indices
     may differ, each of them a tie (the survey's fp32 emulation measured 0
     mismatches in 10/10 trials at 32K/128K)."""
@@ -45,10 +48,19 @@ def check_selection(ours, ref, crit_ref_full, cand, rel_tol=1e-4, max_swap_frac=
     pos = {int(t): i for i, t in enumerate(np.asarray(cand, dtype=np.int64))}
     kth = min(crit_ref_full[pos[int(t)]] for t in ref)
     diff = set(ours.tolist()) ^ set(ref.tolist())
+    under = 0
     for t in diff:
         c = crit_ref_full[pos[t]]
+        if abs(c) < FLT_MIN and abs(kth) < FLT_MIN:
+            # both below the smallest normal fp32: the device's SFU exp flushes
+            # these to zero (ex2.approx.ftz), so they carry no ranking
+            # information -- counted separately, not bounded
+            under += 1
+            continue
         assert abs(c - kth) <= rel_tol * abs(kth), f"index {t}: crit {c} vs k-th {kth} (not a tie)"
-    swaps = len(diff) // 2
+    swaps = (len(diff) - under) // 2
+    if under:
+        TIE_LOG.append((test + " [fp32-subnormal ties]", len(ref), under // 2))
     bound = max(1, int(max_swap_frac * len(ref)))
     TIE_LOG.append((test, len(ref), swaps))
     assert swaps <= bound, f"{swaps} tie swaps > bound {bound} (k = {len(ref)})"

@@ -49,7 +49,8 @@ for mode, theta in (("miss", 2.0), ("hit", -2.0)):
     for _ in range(3):
         eng.decode_async(q, kt, vt, out)
     torch.cuda.synchronize()
-    print(mode, "phase trace (us):", {k: round(v, 2) for k, v in eng.read_trace().items()})
+    print(mode, "phase trace (us):", {k: round(v, 2) for k, v in eng.read_trace().items()},
+          f"SM clock {eng._trace_rate:.3f} GHz")
 # all-CTA phase statistics of one miss and one hit step (start-relative us)
 for mode, theta in (("miss", 2.0), ("hit", -2.0)):
     eng.set_theta(theta)
@@ -57,8 +58,7 @@ for mode, theta in (("miss", 2.0), ("hit", -2.0)):
         eng.decode_async(q, kt, vt, out)
     torch.cuda.synchronize()
     a = eng.read_trace(all_ctas=True)
-    names = dict(enumerate(sa.Engine.TRACE_POINTS))
-    names.update(sa.Engine.SUB_POINTS)
+    names = eng.trace_names()
     print(f"{mode}: all-CTA stamps (us from earliest start): phase: min / median / max")
     for i, nm in sorted(names.items(), key=lambda kv: np.nanmedian(a[:, kv[0]]) if np.any(~np.isnan(a[:, kv[0]])) else 1e9):
         col = a[:, i]
