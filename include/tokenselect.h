@@ -198,6 +198,27 @@ ts_status ts_engine_sync(ts_engine* eng);
 ts_pool* ts_engine_pool(ts_engine* eng);
 uint32_t ts_engine_sequence(const ts_engine* eng, size_t seq);
 /* ------------------------------------------------------------------------
+ * Tensor utilities (the free functions of the reference's Python module,
+ * proj/python/bindings.cpp:60-116), computed on the device in fp64 like the
+ * reference. Arrays may be host or device pointers; every call blocks.
+ * ---------------------------------------------------------------------- */
+/* softmax_rows, tensor.cpp:31-52: m and out are [rows x cols] fp32. */
+ts_status ts_softmax_rows(const float* m, size_t rows, size_t cols, float* out);
+/* topk_indices, tensor.cpp:68-90: the min(k, n) largest scores (the smaller
+ * index wins a tie), indices ascending. n == 0 or k == 0: TS_INVALID_ARGUMENT. */
+ts_status ts_topk_indices(const double* scores, size_t n, size_t k, uint32_t* out, size_t* n_out);
+/* cosine, tensor.cpp:92-113 (fp64; +-1 exactly when dot^2 >= |u|^2 |v|^2;
+ * a zero-norm input is TS_INVALID_ARGUMENT). */
+ts_status ts_cosine(const double* u, const double* v, size_t n, double* out);
+/* chunk_mean, tensor.cpp:133-150: column mean of q_chunk [c x width] in fp64,
+ * rounded to fp32 (c == 1: identity). */
+ts_status ts_chunk_mean(const float* q_chunk, size_t c, size_t width, float* out);
+/* sdpa_full, attention.cpp:54-112: q [C x width] (width = H * d) over
+ * k_all / v_all [N x kv_width] (N >= C, the last C rows are the current
+ * tokens, causal among them), out [C x width]. */
+ts_status ts_sdpa_full(const float* q, size_t C, size_t width, const float* k_all, const float* v_all, size_t N,
+                       size_t kv_width, size_t num_heads, float* out);
+/* ------------------------------------------------------------------------
  * KV-sequence-sharded decode (BASELINE config 4). Each
  * shard (rank) owns a contiguous range [base, base + len) of one sequence in
  * its own engine: rank 0 holds the init window, the last rank the local

@@ -88,6 +88,11 @@ SIGNATURES = {
     "ts_shard_attend": (C.c_int, [_p, _p, _p, _p]),
     "ts_shard_combine": (C.c_int, [_p, _p, C.c_int, _sz, _sz, _p, _p]),
     "ts_shard_combine_packed": (C.c_int, [_p, C.c_int, _sz, _sz, _p, _p]),
+    "ts_softmax_rows": (C.c_int, [_p, _sz, _sz, _p]),
+    "ts_topk_indices": (C.c_int, [_p, _sz, _sz, _p, C.POINTER(_sz)]),
+    "ts_cosine": (C.c_int, [_p, _p, _sz, C.POINTER(C.c_double)]),
+    "ts_chunk_mean": (C.c_int, [_p, _sz, _sz, _p]),
+    "ts_sdpa_full": (C.c_int, [_p, _sz, _sz, _p, _p, _sz, _sz, _sz, _p]),
     "ts_engine_pool": (_p, [_p]),
     "ts_engine_sequence": (C.c_uint32, [_p, _sz]),
 }

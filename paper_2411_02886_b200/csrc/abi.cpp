@@ -25,6 +25,8 @@
 #include "aux.h"
 #include "decode.h"
 #include "step.h"
+#include "vote.h"
+#include "util.h"
 #include "params.h"
 
 using tsb::CacheState;
@@ -163,6 +165,17 @@ const T* dev_in(const T* p, size_t count, DevBuf& stage, cudaStream_t st) {
 // attention-merge arrival counters (both self-resetting across launches).
 struct Workspace {
   DevBuf s, keys, m, z, hist, cnt, nsel, sel_tok, sel_crit, sel_row, att, acnt, bar;
+  // select_head_vote (vote.cu): per-head thresholds, votes, and the scores it votes on
+  DevBuf v_thr, v_cut, v_votes, v_hist, v_s;
+  tsb::VoteWorkspace vote(int H, int T) {
+    return tsb::VoteWorkspace{static_cast<uint32_t*>(v_thr.ensure(static_cast<size_t>(H) * 4)),
+                              static_cast<int*>(v_cut.ensure(static_cast<size_t>(H) * 4)),
+                              static_cast<uint32_t*>(v_votes.ensure(static_cast<size_t>(T) * 4)),
+                              static_cast<uint32_t*>(v_hist.ensure(65 * 4))};
+  }
+  float* vote_scores(int n_seq, int H, int T) {
+    return static_cast<float*>(v_s.ensure(static_cast<size_t>(n_seq) * H * T * 4));
+  }
   size_t acnt_n = 0;
   unsigned launches = 0;
   void prepare(int n_ctas, int H, int H_kv, int d, int tpc, int s_in_smem, int n_seq, cudaStream_t st) {
@@ -653,9 +666,10 @@ void validate_cfg(const ts_engine_config& c) {
   if (c.selection_method < 0 || c.selection_method > 2) fail(TS_INVALID_ARGUMENT, "select_with: bad method");
 }
 
-void check_method_supported(int m) {
-  if (m == TS_HEAD_VOTE)
-    fail(TS_INVALID_ARGUMENT, "head_vote selection is not implemented on the device path yet");
+void check_method_supported(int m, bool sharded = false) {
+  if (m == TS_HEAD_VOTE && sharded)
+    fail(TS_INVALID_ARGUMENT, "head_vote selection is not supported by the sharded decode (per-head top-k across "
+                              "shards); use head_soft_vote or topk");
 }
 
 DecodeParams base_params(const ts_pool* pool, int H, int H_kv, int d, int k, int method, int mode) {
@@ -715,7 +729,23 @@ size_t run_select(const ts_pool* pool, const ts_pool::Seq* seq, int H, int H_kv,
   sd.cache = static_cast<CacheState*>(b_state.ensure(sizeof(CacheState)));
   ck(cudaMemsetAsync(sd.cache, 0, sizeof(CacheState), st), "memset");
   const Plan pl = make_plan(H, H_kv, d, 1, static_cast<int>(T), 1, false);
-  launch_decode(p, pl, ws, st);
+  if (method == TS_HEAD_VOTE && do_select) {
+    // select_head_vote (vote.cu) over S: given, or scored here into the workspace
+    const float* S = s_in;
+    if (!S) {
+      float* so = s_out_dev ? s_out_dev : ws.vote_scores(1, H, static_cast<int>(T));
+      p.mode = tsb::kModeScore | tsb::kModeSOut;
+      sd.s_out = so;
+      launch_decode(p, pl, ws, st);
+      S = so;
+    }
+    ck(tsb::launch_head_vote(S, H, static_cast<int>(T), static_cast<int>(k), cand_dev, 0, nullptr, sd.sel,
+                             sd.sel_crit, nullptr, &sd.cache->n_sel, ws.vote(H, static_cast<int>(T)), nullptr, st),
+       "head vote");
+    g_launches.fetch_add(3);
+  } else {
+    launch_decode(p, pl, ws, st);
+  }
   if (!do_select) {
     ck(cudaStreamSynchronize(st), "sync");
     return 0;
@@ -1305,6 +1335,33 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
     p.trace = e->trace_on ? e->trace.as<unsigned long long>() : nullptr;
     if (p.trace) ck(cudaMemsetAsync(p.trace, 0, kTraceSlots * 8, st), "memset trace");
     const double t3 = g_host_prof ? now_ns() : 0.0;
+    if (c.selection_method == TS_HEAD_VOTE) {
+      // select_head_vote (selector.cpp:101-111) needs every head's own top-k:
+      // (1) Selection Cache decision + S of the missing sequences into the
+      // workspace, (2) per sequence the vote kernels (no-ops on a hit),
+      // (3) attention over the cache entry's selection + the append
+      const int maxT = std::max(1, max_T);
+      float* S = e->ws.vote_scores(static_cast<int>(gn), static_cast<int>(c.num_heads), maxT);
+      DecodeParams p1 = p;
+      p1.mode = tsb::kModeCache | tsb::kModeScore | tsb::kModeSOut;
+      for (size_t i = 0; i < gn; ++i) {
+        p1.seqs[i].s_out = S + i * c.num_heads * maxT;
+        p1.seqs[i].append_frame = -1;
+        p1.seqs[i].append_page = -1;
+      }
+      launch_decode(p1, pl, e->ws, st);
+      for (size_t i = 0; i < gn; ++i) {
+        const SeqDesc& sd = p.seqs[i];
+        if (!sd.select) continue;
+        ck(tsb::launch_head_vote(S + i * c.num_heads * maxT, static_cast<int>(c.num_heads), sd.n_cand,
+                                 static_cast<int>(c.k), nullptr, sd.cand_begin, sd.page_table, sd.sel, sd.sel_crit,
+                                 sd.sel_rows, &sd.cache->n_sel, e->ws.vote(static_cast<int>(c.num_heads), sd.n_cand),
+                                 sd.cache, st),
+           "head vote");
+        g_launches.fetch_add(3);
+      }
+      p.mode = tsb::kModeAttend | tsb::kModeAppend | tsb::kModeUseCached;
+    }
     launch_decode(p, pl, e->ws, st);
     if (g_host_prof) g_prof[2] += now_ns() - t3;
     for (size_t i = 0; i < gn; ++i)
@@ -1593,7 +1650,19 @@ ts_status ts_engine_prefill(ts_engine* e, size_t seq, const float* q, const floa
         sd.sel = psel;
         sd.sel_crit = static_cast<float*>(e->p_crit.ensure(kk * 4));
         const Plan pl = make_plan(H, Hkv, d, 1, static_cast<int>(T), 1, false);
-        launch_decode(p, pl, e->ws, st);
+        if (c.selection_method == TS_HEAD_VOTE) {
+          float* S = e->ws.vote_scores(1, H, static_cast<int>(T));
+          p.mode = tsb::kModeScore | tsb::kModeSOut;
+          sd.s_out = S;
+          launch_decode(p, pl, e->ws, st);
+          ck(tsb::launch_head_vote(S, H, static_cast<int>(T), static_cast<int>(c.k), nullptr, static_cast<int>(c.n_init),
+                                   nullptr, psel, sd.sel_crit, nullptr, &pstate->n_sel,
+                                   e->ws.vote(H, static_cast<int>(T)), nullptr, st),
+             "head vote");
+          g_launches.fetch_add(3);
+        } else {
+          launch_decode(p, pl, e->ws, st);
+        }
       }
       // windows (make_windows) -> device merged list
       const int init_end = static_cast<int>(std::min(c.n_init, cached));
@@ -1643,12 +1712,108 @@ ts_status ts_engine_prefill(ts_engine* e, size_t seq, const float* q, const floa
 }
 
 
+// ------------------------------------------------------ tensor utilities
+// (the free functions of the reference's pybind module, bindings.cpp:60-116)
+ts_status ts_softmax_rows(const float* m, size_t rows, size_t cols, float* out) {
+  return guarded([&] {
+    if (rows == 0 || cols == 0) return;
+    GlobalCtx& g = gctx();
+    cudaStream_t st = g.stream;
+    const float* md = dev_in(m, rows * cols, g.a, st);
+    float* od = is_device_ptr(out) ? out : static_cast<float*>(g.b.ensure(rows * cols * 4));
+    ck(tsb::launch_softmax_rows(md, static_cast<int>(rows), static_cast<int>(cols), od, st), "softmax_rows");
+    g_launches.fetch_add(1);
+    if (od != out) copy_out(out, od, rows * cols * 4, st);
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+ts_status ts_topk_indices(const double* scores, size_t n, size_t k, uint32_t* out, size_t* n_out) {
+  return guarded([&] {
+    *n_out = 0;
+    if (n == 0) fail(TS_INVALID_ARGUMENT, "topk_indices: empty scores");
+    if (k == 0) fail(TS_INVALID_ARGUMENT, "topk_indices: k must be >= 1");
+    GlobalCtx& g = gctx();
+    cudaStream_t st = g.stream;
+    const double* sd = dev_in(scores, n, g.c, st);
+    const size_t take = std::min(k, n);
+    uint32_t* od = static_cast<uint32_t*>(g.d.ensure(take * 4 + 16));
+    int* nd = reinterpret_cast<int*>(od + take);
+    ck(tsb::launch_topk64(sd, static_cast<int>(n), static_cast<int>(k), od, nd, st), "topk_indices");
+    g_launches.fetch_add(1);
+    int nn = 0;
+    ck(cudaMemcpyAsync(&nn, nd, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+    copy_out(out, od, take * 4, st);
+    ck(cudaStreamSynchronize(st), "sync");
+    *n_out = static_cast<size_t>(nn);
+  });
+}
+
+ts_status ts_cosine(const double* u, const double* v, size_t n, double* out) {
+  return guarded([&] {
+    GlobalCtx& g = gctx();
+    cudaStream_t st = g.stream;
+    const double* ud = dev_in(u, n, g.c, st);
+    const double* vd = dev_in(v, n, g.e, st);
+    double* od = static_cast<double*>(g.f.ensure(16));
+    ck(tsb::launch_cosine(ud, vd, static_cast<int>(n), od, st), "cosine");
+    g_launches.fetch_add(1);
+    double r = 0.0;
+    ck(cudaMemcpyAsync(&r, od, 8, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+    if (std::isnan(r)) fail(TS_INVALID_ARGUMENT, "cosine: zero-norm input");
+    *out = r;
+  });
+}
+
+ts_status ts_chunk_mean(const float* q_chunk, size_t c, size_t width, float* out) {
+  return guarded([&] {
+    if (c == 0) fail(TS_INVALID_ARGUMENT, "chunk_mean: empty chunk");
+    GlobalCtx& g = gctx();
+    cudaStream_t st = g.stream;
+    const float* qd = dev_in(q_chunk, c * width, g.a, st);
+    float* od = is_device_ptr(out) ? out : static_cast<float*>(g.b.ensure(width * 4));
+    ck(tsb::launch_chunk_mean(qd, static_cast<int>(c), static_cast<int>(width), od, st), "chunk_mean");
+    g_launches.fetch_add(1);
+    if (od != out) copy_out(out, od, width * 4, st);
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+ts_status ts_sdpa_full(const float* q, size_t C, size_t width, const float* k_all, const float* v_all, size_t N,
+                       size_t kv_width, size_t num_heads, float* out) {
+  return guarded([&] {
+    if (num_heads == 0 || width == 0 || width % num_heads != 0)
+      fail(TS_INVALID_ARGUMENT, "sdpa_full: q must be [C x (H * d_h)]");
+    const size_t d = width / num_heads;
+    if (kv_width == 0 || kv_width % d != 0) fail(TS_INVALID_ARGUMENT, "sdpa_full: K/V must be [(N + C) x (H_kv * d_h)]");
+    const size_t H_kv = kv_width / d;
+    if (num_heads % H_kv != 0) fail(TS_INVALID_ARGUMENT, "sdpa_full: H must be a multiple of H_kv");
+    if (N < C) fail(TS_INVALID_ARGUMENT, "sdpa_full: fewer KV rows than query rows");
+    if (C == 0) return;
+    GlobalCtx& g = gctx();
+    cudaStream_t st = g.stream;
+    const float* qd = dev_in(q, C * width, g.a, st);
+    const float* kd = dev_in(k_all, N * kv_width, g.c, st);
+    const float* vd = dev_in(v_all, N * kv_width, g.e, st);
+    float* od = is_device_ptr(out) ? out : static_cast<float*>(g.b.ensure(C * width * 4));
+    double* ws = static_cast<double*>(g.f.ensure(C * num_heads * N * 8));
+    ck(tsb::launch_sdpa_full(qd, kd, vd, static_cast<int>(C), static_cast<int>(N), static_cast<int>(num_heads),
+                             static_cast<int>(H_kv), static_cast<int>(d), od, ws, st),
+       "sdpa_full");
+    g_launches.fetch_add(1);
+    if (od != out) copy_out(out, od, C * width * 4, st);
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
 // ------------------------------------------------------------ sharded decode
 ts_status ts_shard_engine_create(const ts_engine_config* cfg, size_t capacity_tokens, int rank, int world,
                                  ts_engine** out) {
   return guarded([&] {
     if (world < 1 || world > 64 || rank < 0 || rank >= world)
       fail(TS_INVALID_ARGUMENT, "shard: rank must be in [0, world), world in [1, 64]");
+    check_method_supported(cfg->selection_method, true);
     ts_status rc = ts_engine_create(cfg, capacity_tokens, 1, out);
     if (rc != TS_OK) fail(rc, g_err);
     (*out)->rank = rank;

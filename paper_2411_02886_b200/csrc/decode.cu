@@ -1448,7 +1448,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   }
   stamp(trc, 46);
   // hit prep: the cached selection (counted below init_end / local_begin after the decision)
-  const bool hit_prep = (LEAN || !sd.att_list) && sd.select && (pmode & kModeCache) && (pmode & kModeAttend);
+  const bool hit_prep = (LEAN || !sd.att_list) && sd.select && (pmode & (kModeCache | kModeUseCached)) &&
+                        (pmode & kModeAttend);
   const uint32_t ie = static_cast<uint32_t>(sd.init_end);
   const uint32_t lbs = static_cast<uint32_t>(max(sd.local_begin, sd.init_end));
   uint32_t selv[4];
@@ -1474,6 +1475,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   const bool shard_sel = (pmode & kModeShardSelect) != 0;
   if (sd.select && shard_sel) {
     own = __ldcg(&sd.cache->last_hit) == 1 ? 2 : 1;  // decided by the kModeShardStats launch
+  } else if (sd.select && (pmode & kModeUseCached)) {
+    // the selection was made (or kept) by earlier launches of this step; a
+    // query they rejected (zero) appends nothing
+    own = __ldcg(&sd.cache->error) ? 3 : 2;
   } else if (sd.select) {
     if (pmode & kModeCache) {
       trace_pt(p, 26);

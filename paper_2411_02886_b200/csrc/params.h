@@ -29,6 +29,7 @@ enum Mode : int {
   // KV-sequence-sharded decode (config 4), one launch per exchange phase:
   kModeShardStats = 128,   // stop after the scan: this shard's per-head (m, z) -> shard_stats
   kModeShardSelect = 256,  // resume from the spilled e^(S-m): global stats in, local top-k out
+  kModeUseCached = 512,    // attend over the cache entry's selection (decided by an earlier launch)
 };
 
 // One sequence (request) of a launch. Everything is a device pointer.

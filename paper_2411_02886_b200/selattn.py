@@ -19,7 +19,8 @@ _sz = C.c_size_t
 METHODS = {"topk": 0, "head_vote": 1, "head_soft_vote": 2}
 
 __all__ = ["PagedKvPool", "Engine", "score_paged", "select", "select_for_chunk", "sparse_attend",
-           "CapacityError", "METHODS", "version"]
+           "CapacityError", "METHODS", "version", "softmax_rows", "topk_indices", "cosine", "chunk_mean",
+           "sdpa_full"]
 
 
 def version() -> str:
@@ -225,6 +226,60 @@ def sparse_attend(q, k_cur, v_cur, pool: PagedKvPool, seq, forced_init=(), selec
 
 
 # ----------------------------------------------------------------- engine
+# ---------------------------------------------------- tensor utilities
+# (the free functions of the reference's module, bindings.cpp:60-116; on the device)
+def softmax_rows(m):
+    """softmax_rows (tensor.cpp:31-52) -> [rows x cols] fp32."""
+    a = _Arg(m, np.float32, 2)
+    o, op = _out(a.shape, a.cuda)
+    check(lib.ts_softmax_rows(a.ptr, a.shape[0], a.shape[1], op))
+    return o
+
+
+def topk_indices(scores, k):
+    """topk_indices (tensor.cpp:68-90): the min(k, n) largest, ties to the
+    smaller index, ascending."""
+    a = _Arg(np.ravel(np.asarray(scores, np.float64)), np.float64, 1)
+    n = a.shape[0]
+    out = np.zeros(max(1, min(int(k), n)), np.uint32)
+    m = _sz()
+    check(lib.ts_topk_indices(a.ptr, n, int(k), out.ctypes.data_as(C.c_void_p), C.byref(m)))
+    return [int(x) for x in out[: m.value]]
+
+
+def cosine(u, v):
+    """cosine (tensor.cpp:92-113), fp64."""
+    a = _Arg(np.ravel(np.asarray(u, np.float64)), np.float64, 1)
+    b = _Arg(np.ravel(np.asarray(v, np.float64)), np.float64, 1)
+    if a.shape[0] != b.shape[0]:
+        raise ValueError("cosine: length mismatch")
+    r = C.c_double()
+    check(lib.ts_cosine(a.ptr, b.ptr, a.shape[0], C.byref(r)))
+    return r.value
+
+
+def chunk_mean(q_chunk):
+    """chunk_mean (tensor.cpp:133-150) -> [H*d] fp32."""
+    a = _Arg(q_chunk, np.float32, 2)
+    o, op = _out((a.shape[1],), a.cuda)
+    check(lib.ts_chunk_mean(a.ptr, a.shape[0], a.shape[1], op))
+    return o
+
+
+def sdpa_full(q, k_all, v_all, num_heads):
+    """sdpa_full (attention.cpp:54-112): q [C x H*d] over k_all / v_all
+    [(N + C) x H_kv*d], causal within the last C rows."""
+    qa = _Arg(q, np.float32, 2)
+    ka = _Arg(k_all, np.float32, 2)
+    va = _Arg(v_all, np.float32, 2)
+    if ka.shape != va.shape:
+        raise ValueError("sdpa_full: K/V must be [(N + C) x (H_kv * d_h)]")
+    o, op = _out(qa.shape, qa.cuda)
+    check(lib.ts_sdpa_full(qa.ptr, qa.shape[0], qa.shape[1], ka.ptr, va.ptr, ka.shape[0], ka.shape[1],
+                           int(num_heads), op))
+    return o
+
+
 class Engine:
     """AttentionEngine (attention.hpp:94-115) on the device, optionally over
     ``n_seqs`` sequences decoded together (per-request page tables)."""
