@@ -530,6 +530,51 @@ def run_prefill(args, local_rank):
             "flops": 2 * H * sum(N_INIT + K_SEL + N_LOCAL + i + 1 for i in range(C)) * D * 2}
 
 
+def run_full(args, local_rank):
+    """The full-attention baseline (reference bench-attn's full path,
+    selattn_bench.cpp:214-226: sdpa_full over the whole cache + the current
+    token) on the same kernels: an engine with k = 0 and a local window
+    covering the whole context attends all N + 1 rows every step. Same
+    4-layer rotation as the decode workload; the ratio of the two is the
+    B200 speed-up of selective over full attention."""
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    from paper_2411_02886_b200 import selattn as sa
+
+    dev = torch.device("cuda", local_rank)
+    total = args.warmup + args.steps
+    per_layer = (total + LAYERS - 1) // LAYERS
+    engines = []
+    for L in range(LAYERS):
+        eng = sa.Engine(N_CTX + 2 * per_layer + 16, k=0, n_local=N_CTX + 2 * per_layer + 16, n_init=0,
+                        chunk_size=512, theta=THETA, num_heads=H, num_kv_heads=H_KV, head_dim=D, block_size=64)
+        fill_bf16(eng.append_bf16, N_CTX, H_KV * D, dev, 1234 + L)
+        engines.append(eng)
+    qs = [torch.from_numpy(rotating_stream(per_layer, 1234 + L)).to(dev) for L in range(LAYERS)]
+    kv = [step_kv(per_layer, 1234 + L) for L in range(LAYERS)]
+    ks = [torch.from_numpy(x[0]).to(dev) for x in kv]
+    vs = [torch.from_numpy(x[1]).to(dev) for x in kv]
+    out = torch.empty(1, H * D, device=dev)
+    no_flush = torch.empty(0, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream(dev)
+    for eng in engines:
+        eng.set_stream(stream.cuda_stream)
+
+    def step(i):
+        L, t = i % LAYERS, i // LAYERS
+        engines[L].decode_async(qs[L][t], ks[L][t], vs[L][t], out)
+
+    step_us, clocks, launches = timed_steps(stream, no_flush, step, args.steps, args.warmup, local_rank, 1,
+                                            sa.launch_count)
+    n_mean = N_CTX + per_layer
+    R = H_KV * D * 2
+    alg = n_mean * (2 * R + 4) + 2 * R + H * D * 4 * 2 + 2 * R  # all rows' K + V + page table, current, q, out, append
+    return {"step_us": statistics.mean(step_us), "miss_us": None, "hit_us": None, "hits": 0, "lookups": 0,
+            "kinds": [], "alg_bytes": alg, "launches": launches, "clocks": clocks, "e2e_us": None, "h2d": 0,
+            "d2h": 0, "miss_bytes": alg, "hit_bytes": alg, "n_ctx": N_CTX, "per_gpu_bytes_div": 1}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -553,6 +598,8 @@ WORKLOADS = {
                "all-gathers (configs[3]; 1M at N=8)",
     "batched": "Qwen2-7B layer decode, 16 requests x 64K, per-request page tables, one launch (configs[2])",
     "prefill": "Llama-3-8B chunked-prefill step: one 512-query chunk over a 128K context (configs[4])",
+    "full": "Llama-3-8B layer decode with FULL attention over the 128K paged bf16 KV (the reference bench-attn "
+            "full baseline, selattn_bench.cpp:214-226), same kernels, no selection",
 }
 
 
@@ -592,7 +639,8 @@ def main():
               "stream": f"rotating, consecutive cos {SIMILARITY}",
               "parallelism": f"KV-sequence shards x{world}" if workload == "sharded" else "single GPU",
               "l2": (f"no flush: {LAYERS} layer caches stepped round-robin, {LAYERS * 2 * N_CTX * H_KV * D * 2 >> 20} MB "
-                     f"of K/V > 126 MB L2" if workload == "decode" else "flushed (512 MB write) before every timed step")}
+                     f"of K/V > 126 MB L2" if workload in ("decode", "full")
+                     else "flushed (512 MB write) before every timed step")}
 
     if args.impl == "reference":
         if rank != 0:
@@ -627,6 +675,8 @@ def main():
         r = run_batched(args, local_rank)
     elif workload == "prefill":
         r = run_prefill(args, local_rank)
+    elif workload == "full":
+        r = run_full(args, local_rank)
     else:
         r = run_decode_single(args, local_rank)
     config["context_tokens"] = r["n_ctx"]

@@ -197,6 +197,15 @@ ts_status ts_engine_cached_selection(const ts_engine* eng, size_t seq, uint32_t*
 ts_status ts_engine_sync(ts_engine* eng);
 ts_pool* ts_engine_pool(ts_engine* eng);
 uint32_t ts_engine_sequence(const ts_engine* eng, size_t seq);
+/* Multi-layer engine (AttentionEngine generalised to a model's layers,
+ * attention.cpp:218-232): n_layers x n_seqs sequences in one
+ * pool, each (layer, sequence) with its own KV cache and Selection Cache
+ * entry. Every engine call acts on the current layer (initially 0);
+ * ts_engine_create is ts_engine_create_layers with n_layers = 1. */
+ts_status ts_engine_create_layers(const ts_engine_config* cfg, size_t capacity_tokens, size_t n_seqs,
+                                  size_t n_layers, ts_engine** out);
+ts_status ts_engine_set_layer(ts_engine* eng, size_t layer);
+size_t ts_engine_num_layers(const ts_engine* eng);
 /* ------------------------------------------------------------------------
  * Tensor utilities (the free functions of the reference's Python module,
  * proj/python/bindings.cpp:60-116), computed on the device in fp64 like the

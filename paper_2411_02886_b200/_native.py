@@ -67,6 +67,9 @@ SIGNATURES = {
                                       C.POINTER(_sz)]),
     "ts_sparse_attend": (C.c_int, [_p, C.c_uint32, _p, _p, _p, _sz, _sz, _p, _sz, _p, _sz, _p, _sz, _p]),
     "ts_engine_create": (C.c_int, [C.POINTER(EngineConfig), _sz, _sz, C.POINTER(_p)]),
+    "ts_engine_create_layers": (C.c_int, [C.POINTER(EngineConfig), _sz, _sz, _sz, C.POINTER(_p)]),
+    "ts_engine_set_layer": (C.c_int, [_p, _sz]),
+    "ts_engine_num_layers": (_sz, [_p]),
     "ts_engine_destroy": (None, [_p]),
     "ts_engine_set_stream": (C.c_int, [_p, _p]),
     "ts_engine_append": (C.c_int, [_p, _sz, _p, _p, _sz]),

@@ -606,8 +606,13 @@ struct ts_engine {
   ShardStep shard;
   DevBuf s_att, s_natt;     // sharded attend: attended local rows + count
   std::unique_ptr<ts_pool> pool;
-  std::vector<uint32_t> seq_ids;
-  size_t B = 1;
+  // multi-layer engine: n_layers x B sequences in one pool, each
+  // (layer, sequence) with its own Selection Cache entry; the calls act on
+  // the current layer (ts_engine_set_layer)
+  std::vector<uint32_t> seq_ids;  // [L][B]
+  size_t B = 1, L = 1, layer = 0;
+  size_t li(size_t b) const { return layer * B + b; }
+  uint32_t sid(size_t b) const { return seq_ids[li(b)]; }
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   // per-sequence Selection Cache entries (device)
@@ -642,16 +647,17 @@ struct ts_engine {
   }
   size_t W() const { return cfg.num_heads * cfg.head_dim; }
   size_t KW() const { return cfg.num_kv_heads * cfg.head_dim; }
-  // [B x H*d output | B cache states], 256-B aligned split
+  // [B x H*d output | L x B cache states], 256-B aligned split
   size_t out_bytes() const { return (B * W() * 4 + 255) / 256 * 256; }
-  size_t out_block_bytes() const { return out_bytes() + B * sizeof(CacheState); }
+  size_t out_block_bytes() const { return out_bytes() + L * B * sizeof(CacheState); }
   CacheState* cache(size_t b) const {
-    return reinterpret_cast<CacheState*>(d_out.as<char>() + out_bytes()) + b;
+    return reinterpret_cast<CacheState*>(d_out.as<char>() + out_bytes()) + li(b);
   }
-  float* cq(size_t b) const { return cached_q.as<float>() + b * W(); }
-  uint32_t* sl(size_t b) const { return sel.as<uint32_t>() + b * std::max<size_t>(cfg.k, 1); }
-  float* sc(size_t b) const { return sel_crit.as<float>() + b * std::max<size_t>(cfg.k, 1); }
-  int32_t* sr(size_t b) const { return sel_rows.as<int32_t>() + b * std::max<size_t>(cfg.k, 1); }
+  CacheState* hcache(size_t b) const { return h_cache + li(b); }
+  float* cq(size_t b) const { return cached_q.as<float>() + li(b) * W(); }
+  uint32_t* sl(size_t b) const { return sel.as<uint32_t>() + li(b) * std::max<size_t>(cfg.k, 1); }
+  float* sc(size_t b) const { return sel_crit.as<float>() + li(b) * std::max<size_t>(cfg.k, 1); }
+  int32_t* sr(size_t b) const { return sel_rows.as<int32_t>() + li(b) * std::max<size_t>(cfg.k, 1); }
 };
 
 namespace {
@@ -1116,22 +1122,30 @@ ts_status ts_sparse_attend(const ts_pool* cpool, uint32_t seq, const float* q, c
 }
 
 // ------------------------------------------------------------------ engine
-ts_status ts_engine_create(const ts_engine_config* cfg, size_t capacity_tokens, size_t n_seqs, ts_engine** out) {
+namespace {
+void check_async_errors(ts_engine* e);  // (defined with the decode path below)
+}  // namespace
+
+ts_status ts_engine_create_layers(const ts_engine_config* cfg, size_t capacity_tokens, size_t n_seqs, size_t n_layers,
+                                 ts_engine** out) {
   return guarded([&] {
     *out = nullptr;
     validate_cfg(*cfg);
     check_method_supported(cfg->selection_method);
     if (n_seqs == 0) fail(TS_INVALID_ARGUMENT, "AttentionEngine: n_seqs must be >= 1");
+    if (n_layers == 0) fail(TS_INVALID_ARGUMENT, "AttentionEngine: n_layers must be >= 1");
     device_info();
     auto e = std::make_unique<ts_engine>();
     e->cfg = *cfg;
     e->B = n_seqs;
+    e->L = n_layers;
+    const size_t NS = n_seqs * n_layers;  // (layer, sequence) pairs
     ts_pool* p = nullptr;
     // one shared pool, page_size 1 (attention.cpp:219), capacity per sequence
-    ts_status rc = ts_pool_create(capacity_tokens * n_seqs, 1, cfg->num_kv_heads, cfg->head_dim, &p);
+    ts_status rc = ts_pool_create(capacity_tokens * NS, 1, cfg->num_kv_heads, cfg->head_dim, &p);
     if (rc != TS_OK) fail(rc, g_err);
     e->pool.reset(p);
-    for (size_t b = 0; b < n_seqs; ++b) {
+    for (size_t b = 0; b < NS; ++b) {
       uint32_t id;
       rc = ts_pool_create_sequence(p, &id);
       if (rc != TS_OK) fail(rc, g_err);
@@ -1140,10 +1154,10 @@ ts_status ts_engine_create(const ts_engine_config* cfg, size_t capacity_tokens, 
     ck(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking), "stream");
     e->stream = e->own_stream;
     const size_t W = e->W(), KW = e->KW(), kk = std::max<size_t>(cfg->k, 1);
-    e->cached_q.ensure(n_seqs * W * 4);
-    e->sel.ensure(n_seqs * kk * 4);
-    e->sel_crit.ensure(n_seqs * kk * 4);
-    e->sel_rows.ensure(n_seqs * kk * 4);
+    e->cached_q.ensure(NS * W * 4);
+    e->sel.ensure(NS * kk * 4);
+    e->sel_crit.ensure(NS * kk * 4);
+    e->sel_rows.ensure(NS * kk * 4);
     e->d_q.ensure(n_seqs * (W + 2 * KW) * 4);  // q | k | v staging block
     e->d_k.ensure(n_seqs * KW * 4);
     e->d_v.ensure(n_seqs * KW * 4);
@@ -1153,7 +1167,7 @@ ts_status ts_engine_create(const ts_engine_config* cfg, size_t capacity_tokens, 
     ck(cudaMallocHost(&e->h_v, n_seqs * KW * 4), "pinned");
     ck(cudaMallocHost(&e->h_out, e->out_block_bytes()), "pinned");
     e->h_cache = reinterpret_cast<CacheState*>(reinterpret_cast<char*>(e->h_out) + e->out_bytes());
-    std::vector<CacheState> init(n_seqs);
+    std::vector<CacheState> init(NS);
     for (auto& c : init) {
       c = CacheState{};
       c.theta = cfg->theta;  // attention.cpp:222
@@ -1161,11 +1175,28 @@ ts_status ts_engine_create(const ts_engine_config* cfg, size_t capacity_tokens, 
       c.first_flag = 1;
       c.last_hit = -1;
     }
-    ck(cudaMemcpy(e->cache(0), init.data(), n_seqs * sizeof(CacheState), cudaMemcpyHostToDevice), "H2D");
-    ck(cudaMemset(e->cached_q.p, 0, n_seqs * W * 4), "memset");
+    ck(cudaMemcpy(e->cache(0), init.data(), NS * sizeof(CacheState), cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemset(e->cached_q.p, 0, NS * W * 4), "memset");
     *out = e.release();
   });
 }
+
+ts_status ts_engine_create(const ts_engine_config* cfg, size_t capacity_tokens, size_t n_seqs, ts_engine** out) {
+  return ts_engine_create_layers(cfg, capacity_tokens, n_seqs, 1, out);
+}
+
+ts_status ts_engine_set_layer(ts_engine* eng, size_t layer) {
+  return guarded([&] {
+    if (layer >= eng->L) fail(TS_INVALID_ARGUMENT, "engine: layer index out of range");
+    if (eng->last_unchecked) {  // a pending decode_async step belongs to the current layer
+      ck(cudaStreamSynchronize(eng->stream), "sync");
+      check_async_errors(eng);
+    }
+    eng->layer = layer;
+  });
+}
+
+size_t ts_engine_num_layers(const ts_engine* eng) { return eng->L; }
 
 void ts_engine_destroy(ts_engine* eng) {
   if (g_host_prof && g_prof_n)
@@ -1196,19 +1227,19 @@ ts_status ts_engine_set_stream(ts_engine* eng, void* stream) {
 }
 
 ts_pool* ts_engine_pool(ts_engine* eng) { return eng->pool.get(); }
-uint32_t ts_engine_sequence(const ts_engine* eng, size_t seq) { return eng->seq_ids.at(seq); }
+uint32_t ts_engine_sequence(const ts_engine* eng, size_t seq) { return eng->sid(seq); }
 
 ts_status ts_engine_append(ts_engine* eng, size_t seq, const float* k, const float* v, size_t t) {
   return guarded([&] {
     if (seq >= eng->B) fail(TS_INVALID_ARGUMENT, "engine: sequence index out of range");
-    eng->pool->append(eng->seq_ids[seq], k, v, t, false, nullptr, nullptr, eng->stream);
+    eng->pool->append(eng->sid(seq), k, v, t, false, nullptr, nullptr, eng->stream);
   });
 }
 
 ts_status ts_engine_append_bf16(ts_engine* eng, size_t seq, const uint16_t* k, const uint16_t* v, size_t t) {
   return guarded([&] {
     if (seq >= eng->B) fail(TS_INVALID_ARGUMENT, "engine: sequence index out of range");
-    eng->pool->append(eng->seq_ids[seq], k, v, t, true, nullptr, nullptr, eng->stream);
+    eng->pool->append(eng->sid(seq), k, v, t, true, nullptr, nullptr, eng->stream);
   });
 }
 
@@ -1225,7 +1256,7 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
   e->last_frames.assign(e->B, -1);
   cudaStream_t st = e->stream;
   if (e->B == 1 && e->rank == 0 && e->world == 1) {
-    ts_pool::Seq& s = pool.state(e->seq_ids[0]);
+    ts_pool::Seq& s = pool.state(e->sid(0));
     const size_t N = s.len;
     const bool sel_on = c.k > 0 && N > c.n_init + c.n_local;
     const int T = sel_on ? static_cast<int>(N - c.n_init - c.n_local) : 0;
@@ -1284,7 +1315,7 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
     int max_T = 0, max_rows = 0;
     for (size_t i = 0; i < gn; ++i) {
       const size_t b = g0 + i;
-      ts_pool::Seq& s = pool.state(e->seq_ids[b]);
+      ts_pool::Seq& s = pool.state(e->sid(b));
       const size_t N = s.len;
       SeqDesc& sd = p.seqs[i];
       sd.page_table = s.d_pt;
@@ -1365,7 +1396,7 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
     launch_decode(p, pl, e->ws, st);
     if (g_host_prof) g_prof[2] += now_ns() - t3;
     for (size_t i = 0; i < gn; ++i)
-      if (!cap_fail[g0 + i]) pool.state(e->seq_ids[g0 + i]).len += 1;
+      if (!cap_fail[g0 + i]) pool.state(e->sid(g0 + i)).len += 1;
   }
   return cap_fail;
 }
@@ -1375,7 +1406,7 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
 void rollback_step(ts_engine* e, size_t b) {
   if (b >= e->last_frames.size() || e->last_frames[b] < 0) return;
   ts_pool& pool = *e->pool;
-  ts_pool::Seq& s = pool.state(e->seq_ids[b]);
+  ts_pool::Seq& s = pool.state(e->sid(b));
   s.frames.pop_back();
   s.len -= 1;
   pool.free_list.push_back(static_cast<uint32_t>(e->last_frames[b]));
@@ -1414,7 +1445,7 @@ ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const f
     if (!q_dev) {
       ts_pool& pool = *e->pool;
       for (size_t b = 0; b < B; ++b) {
-        const size_t N = pool.state(e->seq_ids[b]).len;
+        const size_t N = pool.state(e->sid(b)).len;
         if (!(e->cfg.k > 0 && N > e->cfg.n_init + e->cfg.n_local)) continue;
         bool nz = false;
         for (size_t i = 0; i < W && !nz; ++i) nz = q[b * W + i] != 0.0f;
@@ -1466,7 +1497,7 @@ ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const f
     if (!out_dev)
       ck(cudaMemcpyAsync(e->h_out, od, e->out_block_bytes(), cudaMemcpyDeviceToHost, st), "D2H");
     else
-      ck(cudaMemcpyAsync(e->h_cache, e->cache(0), B * sizeof(CacheState), cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaMemcpyAsync(e->hcache(0), e->cache(0), B * sizeof(CacheState), cudaMemcpyDeviceToHost, st), "D2H");
     if (sel_out) {
       if (!e->h_sel) ck(cudaMallocHost(&e->h_sel, B * kk * 4), "pinned");
       ck(cudaMemcpyAsync(e->h_sel, e->sel.p, B * kk * 4, cudaMemcpyDeviceToHost, st), "D2H sel");
@@ -1477,14 +1508,14 @@ ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const f
     if (!out_dev) std::memcpy(out, e->h_out, B * W * 4);
     ts_pool& pool = *e->pool;
     for (size_t b = 0; b < B; ++b) {
-      const CacheState& cs = e->h_cache[b];
+      const CacheState& cs = *e->hcache(b);
       if (cs.error) {
         for (size_t b2 = 0; b2 < B; ++b2)
-          if (e->h_cache[b2].error) rollback_step(e, b2);
+          if (e->hcache(b2)->error) rollback_step(e, b2);
         fail(TS_INVALID_ARGUMENT, "lookup_or_select: zero query vector");
       }
       // the step ran a lookup iff selection was on for the sequence at step start
-      const size_t N_after = pool.state(e->seq_ids[b]).len;
+      const size_t N_after = pool.state(e->sid(b)).len;
       const size_t N = N_after - (cap_fail[b] ? 0 : 1);
       const bool sel_on = e->cfg.k > 0 && N > e->cfg.n_init + e->cfg.n_local;
       if (cache_hit) cache_hit[b] = sel_on ? cs.last_hit : 0;
@@ -1560,7 +1591,7 @@ ts_status ts_engine_stats(const ts_engine* e, size_t seq, size_t* lookups, size_
     if (cs.error && e->last_unchecked) check_async_errors(const_cast<ts_engine*>(e));
     if (lookups) *lookups = cs.lookups;
     if (hits) *hits = cs.hits;
-    if (len) *len = e->pool->state(e->seq_ids[seq]).len;
+    if (len) *len = e->pool->state(e->sid(seq)).len;
     if (last_hit) *last_hit = cs.last_hit;
     if (last_cos) *last_cos = cs.last_cos;
   });
@@ -1598,7 +1629,7 @@ ts_status ts_engine_prefill(ts_engine* e, size_t seq, const float* q, const floa
     if (n == 0) fail(TS_INVALID_ARGUMENT, "prefill: empty input");
     const ts_engine_config& c = e->cfg;
     ts_pool& pool = *e->pool;
-    const uint32_t sid = e->seq_ids[seq];
+    const uint32_t sid = e->sid(seq);
     const size_t W = e->W(), KW = e->KW();
     const int H = static_cast<int>(c.num_heads), Hkv = static_cast<int>(c.num_kv_heads), d = static_cast<int>(c.head_dim);
     cudaStream_t st = e->stream;
@@ -1831,7 +1862,7 @@ DecodeParams shard_params(ts_engine* e, int mode) {
   DecodeParams p = base_params(&pool, static_cast<int>(c.num_heads), static_cast<int>(c.num_kv_heads),
                                static_cast<int>(c.head_dim), static_cast<int>(c.k), c.selection_method, mode);
   p.n_seq = 1;
-  ts_pool::Seq& s = pool.state(e->seq_ids[0]);
+  ts_pool::Seq& s = pool.state(e->sid(0));
   SeqDesc& sd = p.seqs[0];
   sd.page_table = s.d_pt;
   sd.n_cached = static_cast<int32_t>(s.len);
@@ -1868,7 +1899,7 @@ ts_status ts_shard_stats(ts_engine* e, const float* q, const float* k, const flo
   return guarded([&] {
     const ts_engine_config& c = e->cfg;
     ShardStep& ss = e->shard;
-    const size_t n_r = e->pool->state(e->seq_ids[0]).len;
+    const size_t n_r = e->pool->state(e->sid(0)).len;
     const bool first = e->rank == 0, last = e->rank == e->world - 1;
     if (first && base != 0) fail(TS_INVALID_ARGUMENT, "shard: rank 0 must start at position 0");
     if (base + n_r > n_global) fail(TS_INVALID_ARGUMENT, "shard: rows beyond the global length");
@@ -1912,7 +1943,7 @@ ts_status ts_shard_attend(ts_engine* e, const uint32_t* all_cands, float* out_pa
     const ts_engine_config& c = e->cfg;
     ts_pool& pool = *e->pool;
     const ShardStep& ss = e->shard;
-    ts_pool::Seq& s = pool.state(e->seq_ids[0]);
+    ts_pool::Seq& s = pool.state(e->sid(0));
     const size_t n_r = s.len, N = ss.n_global;
     const bool first = e->rank == 0, last = e->rank == e->world - 1;
     const size_t ie = std::min(c.n_init, N);

@@ -286,7 +286,7 @@ class Engine:
 
     def __init__(self, capacity_tokens, k=2048, n_local=512, n_init=128, chunk_size=512, theta=0.9,
                  num_heads=8, num_kv_heads=8, head_dim=64, block_size=64, selection_method="head_soft_vote",
-                 n_seqs=1):
+                 n_seqs=1, n_layers=1):
         if selection_method not in METHODS:
             raise ValueError("unknown selection method: " + str(selection_method))
         cfg = EngineConfig(k, n_local, n_init, chunk_size, theta, num_heads, num_kv_heads, head_dim, block_size,
@@ -296,8 +296,9 @@ class Engine:
         self.model_dim = num_heads * head_dim
         self.kv_dim = num_kv_heads * head_dim
         h = C.c_void_p()
-        check(lib.ts_engine_create(C.byref(cfg), capacity_tokens, n_seqs, C.byref(h)))
+        check(lib.ts_engine_create_layers(C.byref(cfg), capacity_tokens, n_seqs, n_layers, C.byref(h)))
         self._h = h
+        self.n_layers = n_layers
         self.pool = PagedKvPool(0, 1, 1, 1, _handle=C.c_void_p(lib.ts_engine_pool(h)))
 
     def __del__(self):
@@ -307,6 +308,11 @@ class Engine:
 
     def sequence(self, i=0) -> int:
         return lib.ts_engine_sequence(self._h, i)
+
+    def set_layer(self, layer):
+        """Multi-layer engine: the layer the following calls act on (each
+        (layer, sequence) has its own KV cache and Selection Cache entry)."""
+        check(lib.ts_engine_set_layer(self._h, layer))
 
     def set_stream(self, stream_ptr):
         check(lib.ts_engine_set_stream(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))

@@ -291,3 +291,26 @@ def test_zero_query_device_tensor_rolls_back(sa):
     q = torch.from_numpy(rng_normal(6001, (1, H * d))).cuda()
     o, hit, sel = eng.decode(q, kt, vt)
     assert not hit and len(sel) == 64 and eng.stats()["len"] == n + 1 and eng.stats()["lookups"] == 1
+
+
+# --------------------------------------- full-attention baseline
+@pytest.mark.parametrize("n", [32768, 131072])
+def test_full_attention_decode_vs_oracle(sa, orc, n):
+    """The bench's `full` workload: k = 0 and a local window over the whole
+    context, so a decode step attends all N cached rows + the current token
+    (sdpa_full over the gathered cache, selattn_bench.cpp:214-226)."""
+    K, V = kv_rows(7000 + n, n + 2, L_HKV * D)
+    kw = dict(k=0, n_local=n + 64, n_init=0, chunk_size=512, theta=0.9, num_heads=L_H, num_kv_heads=L_HKV,
+              head_dim=D, block_size=64)
+    eng = sa.Engine(n + 64, **kw)
+    ref = orc.engine(n + 64, **kw)
+    append_chunked(eng.append, K[:n], V[:n])
+    append_chunked(ref.append, K[:n], V[:n])
+    for t in range(2):
+        q = rng_normal(7100 + t, (1, L_H * D))
+        kt, vt = K[n + t:n + t + 1], V[n + t:n + t + 1]
+        o1, h1, s1 = eng.decode(q, kt, vt)
+        o2, h2, s2 = ref.decode(q, kt, vt)
+        assert not h1 and not h2 and s1 == [] and len(s2) == 0
+        err = rel_fro(o1, o2)
+        assert err <= 1e-5 and np.abs(o1 - o2).max() <= 1e-4, (t, err)

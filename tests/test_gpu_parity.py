@@ -418,3 +418,55 @@ def test_prefill_single_chunk_fp32_kv_exact(sa, orc):
     want = orc.engine(n + 4, **kw).prefill(q, kk, vv)
     assert rel_fro(got, want) <= 1e-5, rel_fro(got, want)
     assert np.abs(got - want).max() <= 1e-4
+
+
+# ------------------------------------------------------ multi-layer engine
+def test_multi_layer_engine_vs_oracle(sa, orc):
+    """AttentionEngine over a model's layers (attention.cpp:218-232,
+    SPEC.md:174): 3 layers x 2 sequences in one engine, stepped layer by layer
+    like a decode loop; every (layer, sequence) matches its own oracle engine
+    (own KV cache, own Selection Cache entry)."""
+    L, B, H, H_kv, d, n, k = 3, 2, 8, 2, 128, 3000, 128
+    kw = dict(k=k, n_local=64, n_init=16, chunk_size=512, theta=0.9, num_heads=H, num_kv_heads=H_kv, head_dim=d,
+              block_size=64)
+    eng = sa.Engine(n + 16, n_seqs=B, n_layers=L, **kw)
+    assert eng.n_layers == L
+    refs, rows = {}, {}
+    for l in range(L):
+        eng.set_layer(l)
+        for b in range(B):
+            K = bf16_round(rng_normal(1000 + 10 * l + b, (n, H_kv * d), 3.0))
+            V = bf16_round(rng_normal(2000 + 10 * l + b, (n, H_kv * d)))
+            eng.append(K, V, b)
+            r = orc.engine(n + 16, **kw)
+            r.append(K, V)
+            refs[l, b], rows[l, b] = r, (K, V)
+    g = np.random.default_rng(5)
+    qbase = {key: g.standard_normal(H * d).astype(np.float32) for key in refs}
+    for step in range(3):  # a miss, then near-identical queries (hits)
+        for l in range(L):
+            eng.set_layer(l)
+            q = np.stack([qbase[l, b] + 1e-3 * step for b in range(B)]).astype(np.float32)
+            kt = bf16_round(rng_normal(300 + 10 * step + l, (B, H_kv * d), 3.0))
+            vt = bf16_round(rng_normal(400 + 10 * step + l, (B, H_kv * d)))
+            o1, h1, s1 = eng.decode(q, kt, vt)
+            for b in range(B):
+                o2, h2, s2 = refs[l, b].decode(q[b:b + 1], kt[b:b + 1], vt[b:b + 1])
+                assert h1[b] == h2 == (step > 0), (l, b, step)
+                K, V = rows[l, b]
+                if s1[b] != [int(x) for x in s2]:
+                    cand = np.arange(16, n - 64, dtype=np.uint32)
+                    S = orc.score_paged(qbase[l, b].reshape(H, d), K, H_kv, cand)
+                    check_selection(s1[b], s2, orc.criticality(S, k), cand)
+                    Ka = np.vstack([K] + [bf16_round(rng_normal(300 + 10 * t + l, (B, H_kv * d), 3.0))[b:b + 1]
+                                          for t in range(step)])
+                    Va = np.vstack([V] + [bf16_round(rng_normal(400 + 10 * t + l, (B, H_kv * d)))[b:b + 1]
+                                          for t in range(step)])
+                    att = orc.make_windows(n + step, 16, 64, np.asarray(s1[b], np.uint32))
+                    o2 = orc.sparse_attend(q[b:b + 1], kt[b:b + 1], vt[b:b + 1], Ka, Va, H, H_kv, att)
+                assert rel_fro(o1[b:b + 1], o2) <= 1e-5, (l, b, step)
+    for l in range(L):
+        eng.set_layer(l)
+        assert len(eng) == n + 3 and eng.stats()["lookups"] == 3 and eng.stats()["hits"] == 2
+    with pytest.raises(ValueError):
+        eng.set_layer(L)

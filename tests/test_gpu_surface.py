@@ -82,9 +82,12 @@ def test_topk_vs_oracle(sa, orc, n, k):
 def test_cosine_vs_oracle(sa, orc):
     g = np.random.default_rng(5)
     for n in (1, 7, 4096, 100000):
-        u, v = g.standard_normal(n), g.standard_normal(n)
+        # fp32 inputs: the oracle restates the fp32 instantiation (the Selection
+        # Cache's, tensor.cpp:92-113); ours reads them as exact doubles
+        u, v = g.standard_normal(n).astype(np.float32), g.standard_normal(n).astype(np.float32)
         assert abs(sa.cosine(u, v) - orc.cosine(u, v)) <= 1e-12
-        assert sa.cosine(u, -2.5 * u) == -1.0
+        w = (-2.5 * u).astype(np.float32)
+        assert abs(sa.cosine(u, w) - orc.cosine(u, w)) <= 1e-12
 
 
 @pytest.mark.parametrize("c,w", [(1, 64), (7, 4096), (512, 4096)])
