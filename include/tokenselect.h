@@ -194,6 +194,9 @@ ts_status ts_engine_stats(const ts_engine* eng, size_t seq, size_t* lookups, siz
 /* The current cached selection (SelectionCacheEntry::cached_result) of `seq`. */
 ts_status ts_engine_cached_selection(const ts_engine* eng, size_t seq, uint32_t* sel_out,
                                      double* crit_out, size_t* n_out);
+/* SelectionCacheEntry of `seq` (selection_cache.hpp:23-29) beyond the cached
+ * selection: the cached query [H*d] (nullable), first_flag and theta. */
+ts_status ts_engine_cache_entry(const ts_engine* eng, size_t seq, float* cached_q, int* first_flag, double* theta);
 ts_status ts_engine_sync(ts_engine* eng);
 ts_pool* ts_engine_pool(ts_engine* eng);
 uint32_t ts_engine_sequence(const ts_engine* eng, size_t seq);

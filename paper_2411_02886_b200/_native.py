@@ -85,6 +85,7 @@ SIGNATURES = {
                                   C.POINTER(C.c_double)]),
     "ts_engine_cached_selection": (C.c_int, [_p, _sz, _p, _p, C.POINTER(_sz)]),
     "ts_engine_sync": (C.c_int, [_p]),
+    "ts_engine_cache_entry": (C.c_int, [_p, _sz, _p, C.POINTER(C.c_int), C.POINTER(C.c_double)]),
     "ts_shard_engine_create": (C.c_int, [C.POINTER(EngineConfig), _sz, C.c_int, C.c_int, C.POINTER(_p)]),
     "ts_shard_stats": (C.c_int, [_p, _p, _p, _p, _sz, _sz, _p]),
     "ts_shard_select": (C.c_int, [_p, _p, _p]),

@@ -1615,6 +1615,18 @@ ts_status ts_engine_cached_selection(const ts_engine* e, size_t seq, uint32_t* s
   });
 }
 
+ts_status ts_engine_cache_entry(const ts_engine* e, size_t seq, float* cached_q, int* first_flag, double* theta) {
+  return guarded([&] {
+    if (seq >= e->B) fail(TS_INVALID_ARGUMENT, "engine: sequence index out of range");
+    CacheState cs{};
+    ck(cudaMemcpyAsync(&cs, e->cache(seq), sizeof(CacheState), cudaMemcpyDeviceToHost, e->stream), "D2H");
+    if (cached_q) ck(cudaMemcpyAsync(cached_q, e->cq(seq), e->W() * 4, cudaMemcpyDeviceToHost, e->stream), "D2H");
+    ck(cudaStreamSynchronize(e->stream), "sync");
+    if (first_flag) *first_flag = cs.first_flag;
+    if (theta) *theta = cs.theta;
+  });
+}
+
 ts_status ts_engine_sync(ts_engine* e) {
   return guarded([&] {
     ck(cudaStreamSynchronize(e->stream), "sync");
