@@ -326,7 +326,7 @@ def split_by_kind(step_us, kinds):
 LAYERS = 4  # decode workload: layer caches stepped round-robin (2.1 GB of K/V > 126 MB L2)
 
 
-def run_decode_single(args, local_rank):
+def run_decode_single(args, local_rank, n_ctx=N_CTX):
     """configs[1]: the fused single-launch decode step (N = 1).
 
     Like a model's decode loop, consecutive steps run different layers:
@@ -344,9 +344,9 @@ def run_decode_single(args, local_rank):
     per_layer = (total + LAYERS - 1) // LAYERS
     engines, streams = [], []
     for L in range(LAYERS):
-        eng = sa.Engine(N_CTX + 2 * per_layer + 16, k=K_SEL, n_local=N_LOCAL, n_init=N_INIT, chunk_size=512,
+        eng = sa.Engine(n_ctx + 2 * per_layer + 16, k=K_SEL, n_local=N_LOCAL, n_init=N_INIT, chunk_size=512,
                         theta=THETA, num_heads=H, num_kv_heads=H_KV, head_dim=D, block_size=64)
-        fill_bf16(eng.append_bf16, N_CTX, H_KV * D, dev, 1234 + L)
+        fill_bf16(eng.append_bf16, n_ctx, H_KV * D, dev, 1234 + L)
         engines.append(eng)
     qs_h = [rotating_stream(per_layer, 1234 + L) for L in range(LAYERS)]
     kv_h = [step_kv(per_layer, 1234 + L) for L in range(LAYERS)]
@@ -375,7 +375,7 @@ def run_decode_single(args, local_rank):
     assert dev_hits == sum(all_kinds), (dev_hits, sum(all_kinds))
     hits, lookups = sum(kinds), len(kinds)
     miss_us, hit_us = split_by_kind(step_us, kinds)
-    n_mean = N_CTX + per_layer
+    n_mean = n_ctx + per_layer
     alg = sum(algorithmic_bytes(n_mean, not h) for h in kinds) / len(kinds)
 
     # end-to-end: host buffers through the public C ABI (H2D + D2H inside the call)
@@ -397,7 +397,7 @@ def run_decode_single(args, local_rank):
             "lookups": lookups, "kinds": kinds, "alg_bytes": alg, "launches": launches, "clocks": clocks,
             "e2e_us": 1e6 * statistics.mean(e2e), "h2d": (H * D + 2 * H_KV * D) * 4, "d2h": H * D * 4 + 48,
             "miss_bytes": algorithmic_bytes(n_mean, True), "hit_bytes": algorithmic_bytes(n_mean, False),
-            "n_ctx": N_CTX, "per_gpu_bytes_div": 1}
+            "n_ctx": n_ctx, "per_gpu_bytes_div": 1}
 
 
 def run_decode_sharded(args, rank, world, local_rank):
@@ -424,11 +424,13 @@ def run_decode_sharded(args, rank, world, local_rank):
     ks_h, vs_h = step_kv(total, seed)
     qs, ks, vs = (torch.from_numpy(x).to(dev) for x in (qs_h, ks_h, vs_h))
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    ex = sharded.TorchDistExchange()
+    comm = sharded.LibraryComm(rank, world)  # the library's own NCCL communicator
+    out_d = torch.empty(1, H * D, dtype=torch.float32, device=dev)
 
     def step(i):
         with torch.cuda.stream(stream):
-            sharded.decode_step(shard, ex, qs[i].view(-1), ks[i].view(-1), vs[i].view(-1), rr.base, n_global + i)
+            sharded.decode_step_native(shard, comm, qs[i].view(-1), ks[i].view(-1), vs[i].view(-1), rr.base,
+                                       n_global + i, out_d)
 
     step_us, clocks, launches = timed_steps(stream, flush, step, args.steps, args.warmup, local_rank, world,
                                             sa.launch_count)
@@ -447,7 +449,7 @@ def run_decode_sharded(args, rank, world, local_rank):
             for pin, x in zip(pins, (qs_e[t], ks_e[t], vs_e[t])):
                 pin.copy_(torch.from_numpy(x).view(-1))  # host buffer -> pinned staging
             q, k, v = (pin.to(dev, non_blocking=True) for pin in pins)
-            sharded.decode_step(shard, ex, q, k, v, rr.base, n_global + total + t).cpu()
+            sharded.decode_step_native(shard, comm, q, k, v, rr.base, n_global + total + t, out_d).cpu()
         e2e.append(time.perf_counter() - t0)
     mt = torch.tensor(step_us + [1e6 * statistics.mean(e2e)], device=dev, dtype=torch.float64)
     torch.distributed.all_reduce(mt, op=torch.distributed.ReduceOp.MAX)  # max over ranks, per step
@@ -594,8 +596,9 @@ def traffic_per_launch():
 
 WORKLOADS = {
     "decode": "Llama-3-8B layer decode, 128K paged bf16 KV, k=2048, Selection Cache theta=0.9 (configs[1])",
-    "sharded": "Llama-3-8B layer decode, N x 128K-token context KV-sharded over N GPUs, NCCL stats/top-k/LSE "
-               "all-gathers (configs[3]; 1M at N=8)",
+    "sharded": "Llama-3-8B layer decode, KV-sequence-sharded over N GPUs (N x 128K tokens, weak scaling, 1M at "
+               "N=8; --context 1048576: 1M at every N), one library call per step: 4 shard launches + 3 "
+               "ncclAllGather of stats / top-k / LSE partials on the engine stream (configs[3])",
     "batched": "Qwen2-7B layer decode, 16 requests x 64K, per-request page tables, one launch (configs[2])",
     "prefill": "Llama-3-8B chunked-prefill step: one 512-query chunk over a 128K context (configs[4])",
     "full": "Llama-3-8B layer decode with FULL attention over the 128K paged bf16 KV (the reference bench-attn "
@@ -669,7 +672,10 @@ def main():
         os.environ.setdefault("MASTER_PORT", "29531")
         torch.distributed.init_process_group("nccl", rank=rank, world_size=world,
                                              device_id=torch.device("cuda", local_rank))
-    if workload == "sharded":
+    if workload == "sharded" and world == 1 and args.context:
+        # strong scaling's N = 1 point: the whole context on one GPU, fused kernel
+        r = run_decode_single(args, local_rank, args.context)
+    elif workload == "sharded":
         r = run_decode_sharded(args, rank, world, local_rank)
     elif workload == "batched":
         r = run_batched(args, local_rank)

@@ -265,6 +265,22 @@ ts_status ts_shard_combine_packed(const float* packed_all, int world, size_t num
 
 /* Kernel launches issued by this library since process start (evidence
  * counter for the benchmark's gpu_launches field). */
+/* In-library data plane of the sharded decode: an NCCL communicator the
+ * library drives itself (libnccl resolved at run time: the copy already in
+ * the process, else libnccl.so.2). Rank 0 makes the 128-byte unique id, the
+ * host broadcasts it (any bootstrap), every rank creates its communicator.
+ * world == 1 needs no id (id128 may be NULL). */
+typedef struct ts_comm ts_comm;
+ts_status ts_comm_unique_id(uint8_t* id128);
+ts_status ts_comm_create(const uint8_t* id128, int world, int rank, ts_comm** out);
+void ts_comm_destroy(ts_comm* comm);
+/* One whole sharded decode step on this rank: ts_shard_stats -> all-gather ->
+ * ts_shard_select -> all-gather -> ts_shard_attend -> all-gather ->
+ * ts_shard_combine_packed, launches and ncclAllGather calls all on the
+ * engine's stream, no host synchronisation (unless out is a host pointer).
+ * out [H*d] is identical on every rank. comm may be NULL at world 1. */
+ts_status ts_shard_decode_step(ts_engine* eng, ts_comm* comm, const float* q, const float* k, const float* v,
+                               size_t base, size_t n_global, float* out);
 uint64_t ts_launch_count(void);
 
 #if defined(__GNUC__)

@@ -97,6 +97,10 @@ SIGNATURES = {
     "ts_cosine": (C.c_int, [_p, _p, _sz, C.POINTER(C.c_double)]),
     "ts_chunk_mean": (C.c_int, [_p, _sz, _sz, _p]),
     "ts_sdpa_full": (C.c_int, [_p, _sz, _sz, _p, _p, _sz, _sz, _sz, _p]),
+    "ts_comm_unique_id": (C.c_int, [_p]),
+    "ts_comm_create": (C.c_int, [_p, C.c_int, C.c_int, C.POINTER(_p)]),
+    "ts_comm_destroy": (None, [_p]),
+    "ts_shard_decode_step": (C.c_int, [_p, _p, _p, _p, _p, _sz, _sz, _p]),
     "ts_engine_pool": (_p, [_p]),
     "ts_engine_sequence": (C.c_uint32, [_p, _sz]),
 }

@@ -27,6 +27,7 @@
 #include "step.h"
 #include "vote.h"
 #include "util.h"
+#include "comm.h"
 #include "params.h"
 
 using tsb::CacheState;
@@ -605,6 +606,7 @@ struct ts_engine {
   int rank = 0, world = 1;  // sharded decode: this shard's rank among `world`
   ShardStep shard;
   DevBuf s_att, s_natt;     // sharded attend: attended local rows + count
+  DevBuf s_blk, s_out;      // ts_shard_decode_step: exchanged blocks, staged output
   std::unique_ptr<ts_pool> pool;
   // multi-layer engine: n_layers x B sequences in one pool, each
   // (layer, sequence) with its own Selection Cache entry; the calls act on
@@ -1500,7 +1502,7 @@ ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const f
       ck(cudaMemcpyAsync(e->hcache(0), e->cache(0), B * sizeof(CacheState), cudaMemcpyDeviceToHost, st), "D2H");
     if (sel_out) {
       if (!e->h_sel) ck(cudaMallocHost(&e->h_sel, B * kk * 4), "pinned");
-      ck(cudaMemcpyAsync(e->h_sel, e->sel.p, B * kk * 4, cudaMemcpyDeviceToHost, st), "D2H sel");
+      ck(cudaMemcpyAsync(e->h_sel, e->sl(0), B * kk * 4, cudaMemcpyDeviceToHost, st), "D2H sel");  // this layer's slots
     }
     if (g_host_prof) tp[4] = now_ns();
     ck(cudaStreamSynchronize(st), "decode sync");
@@ -1996,6 +1998,7 @@ ts_status ts_shard_attend(ts_engine* e, const uint32_t* all_cands, float* out_pa
       const uint32_t f = pool.free_list.back();
       pool.free_list.pop_back();
       s.frames.push_back(f);
+      e->last_frames.assign(1, f);
       sd.append_frame = static_cast<int32_t>(f);
       sd.append_slot = 0;
       sd.append_page = static_cast<int32_t>(n_r);
@@ -2008,6 +2011,87 @@ ts_status ts_shard_attend(ts_engine* e, const uint32_t* all_cands, float* out_pa
     if (p.trace) ck(cudaMemsetAsync(p.trace, 0, kTraceSlots * 8, st), "memset trace");
     launch_decode(p, pl, e->ws, st);
     if (appended) s.len += 1;
+  });
+}
+
+// ---------------------------------------------- in-library data plane
+struct ts_comm {
+  tsb::Comm c;
+};
+
+ts_status ts_comm_unique_id(uint8_t* id128) {
+  return guarded([&] { tsb::nccl_unique_id(id128); });
+}
+
+ts_status ts_comm_create(const uint8_t* id128, int world, int rank, ts_comm** out) {
+  return guarded([&] {
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) fail(TS_INVALID_ARGUMENT, "comm: rank must be in [0, world)");
+    device_info();
+    auto c = std::make_unique<ts_comm>();
+    if (world > 1) tsb::nccl_comm_init(&c->c, id128, world, rank);
+    c->c.world = world;
+    c->c.rank = rank;
+    *out = c.release();
+  });
+}
+
+void ts_comm_destroy(ts_comm* c) {
+  if (!c) return;
+  tsb::nccl_comm_destroy(&c->c);
+  delete c;
+}
+
+// One sharded decode step: stats -> all-gather -> select ->
+// all-gather -> attend -> all-gather -> combine, every launch and every
+// ncclAllGather on the engine's stream, no host synchronisation (unless out
+// is a host pointer). A one-rank communicator (or comm == NULL at world 1)
+// passes each block straight to the next phase.
+ts_status ts_shard_decode_step(ts_engine* e, ts_comm* comm, const float* q, const float* k, const float* v,
+                               size_t base, size_t n_global, float* out) {
+  return guarded([&] {
+    const ts_engine_config& c = e->cfg;
+    const int world = e->world;
+    if ((comm ? comm->c.world : 1) != world || (comm ? comm->c.rank : 0) != e->rank)
+      fail(TS_INVALID_ARGUMENT, "shard: the communicator's rank / world differ from the shard engine's");
+    if (world > 1 && !comm) fail(TS_INVALID_ARGUMENT, "shard: world > 1 needs a communicator");
+    cudaStream_t st = e->stream;
+    const size_t W = e->W(), KW = e->KW(), H = c.num_heads, kk = std::max<size_t>(c.k, 1);
+    const float* qd = dev_in(q, W, e->d_q, st);
+    const float* kd = dev_in(k, KW, e->d_k, st);
+    const float* vd = dev_in(v, KW, e->d_v, st);
+    const size_t n_stats = H * 2, n_cands = 2 * kk + 1, n_pack = W + H * 2;
+    float* blk = static_cast<float*>(e->s_blk.ensure((n_stats + n_cands + n_pack) * (world + 1) * 4));
+    float* stats = blk;
+    uint32_t* cands = reinterpret_cast<uint32_t*>(stats + n_stats);
+    float* pack = reinterpret_cast<float*>(cands + n_cands);
+    float* all = pack + n_pack;
+    float* all_stats = all;
+    uint32_t* all_cands = reinterpret_cast<uint32_t*>(all_stats + world * n_stats);
+    float* all_pack = reinterpret_cast<float*>(all_cands + world * n_cands);
+    auto gather = [&](const void* send, void* recv, size_t words) -> const void* {
+      if (world == 1) return send;
+      tsb::nccl_all_gather(comm->c, send, recv, words * 4, st);
+      return recv;
+    };
+    ts_status rc = ts_shard_stats(e, qd, kd, vd, base, n_global, stats);
+    if (rc != TS_OK) fail(rc, g_err);
+    const float* gs = static_cast<const float*>(gather(stats, all_stats, n_stats));
+    rc = ts_shard_select(e, gs, cands);
+    if (rc != TS_OK) fail(rc, g_err);
+    const uint32_t* gc = static_cast<const uint32_t*>(gather(cands, all_cands, n_cands));
+    rc = ts_shard_attend(e, gc, pack, pack + W);
+    if (rc != TS_OK) fail(rc, g_err);
+    const float* gp = static_cast<const float*>(gather(pack, all_pack, n_pack));
+    float* od = is_device_ptr(out) ? out : static_cast<float*>(e->s_out.ensure(W * 4));
+    rc = ts_shard_combine_packed(gp, world, H, c.head_dim, od, st);
+    if (rc != TS_OK) fail(rc, g_err);
+    e->last_unchecked = true;  // a zero query is reported by the next sync / stats
+    if (od != out) {
+      ck(cudaMemcpyAsync(out, od, W * 4, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaStreamSynchronize(st), "sync");
+      check_async_errors(e);
+    }
   });
 }
 

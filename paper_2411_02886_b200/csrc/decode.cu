@@ -1474,7 +1474,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   double own_cos = NAN;
   const bool shard_sel = (pmode & kModeShardSelect) != 0;
   if (sd.select && shard_sel) {
-    own = __ldcg(&sd.cache->last_hit) == 1 ? 2 : 1;  // decided by the kModeShardStats launch
+    // decided by the kModeShardStats launch (a zero query there: nothing to select)
+    own = __ldcg(&sd.cache->error) ? 3 : __ldcg(&sd.cache->last_hit) == 1 ? 2 : 1;
   } else if (sd.select && (pmode & kModeUseCached)) {
     // the selection was made (or kept) by earlier launches of this step; a
     // query they rejected (zero) appends nothing
@@ -1554,7 +1555,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   // append of the current token's row (kv_pool.cpp:55-85), after the decision.
   // This step never reads row N: the candidates end at N - n_local and the
   // current token is attended from k_new / v_new.
-  if ((pmode & kModeAppend) && cs == 0 && sd.append_frame >= 0 && own != 3) {
+  // (an explicit-list attend launch of a sharded step whose stats launch
+  // rejected the query appends nothing either)
+  const bool rejected = !LEAN && sd.att_list && sd.cache && __ldcg(&sd.cache->error);
+  if ((pmode & kModeAppend) && cs == 0 && sd.append_frame >= 0 && own != 3 && !rejected) {
     const int row = p.H_kv * p.d;
     const size_t off = (static_cast<size_t>(sd.append_frame) * p.page_size + sd.append_slot) * row;
     for (int i = tid; i < row; i += blockDim.x) {

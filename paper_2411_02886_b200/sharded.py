@@ -17,9 +17,12 @@ ts_shard_*) with three all-gathers in between:
 The Selection Cache decision needs no exchange: q and the cached query are
 replicated, so every rank decides identically.
 
-Transport is pluggable:
-- ``TorchDistExchange``: torch.distributed all_gather, NCCL over
-  NVLink/NVSwitch on B200; gloo on CPU for the host-logic tests;
+Transport:
+- ``LibraryComm`` + ``decode_step_native``: the library's own NCCL
+  communicator; the whole step (launches + all-gathers) is one C call,
+  ts_shard_decode_step, on the engine's stream (the bench's path);
+- ``TorchDistExchange`` + ``decode_step``: the same protocol phase by phase
+  over torch.distributed (gloo on CPU for the host-logic tests);
 - ``simulate_step`` runs all shards of one sequence inside one process.
 
 All device work is the library's sm_100a kernels. This module only sequences
@@ -158,6 +161,47 @@ class NativeShard:
         check(lib.ts_shard_combine(self._p(all_part), self._p(all_ml), self.world, self.H, self.d, self._p(out),
                                    C.c_void_p(self.torch.cuda.current_stream().cuda_stream)))
         return out
+
+
+class LibraryComm:
+    """The library's own NCCL communicator (ts_comm_*): rank 0 makes the
+    unique id, torch.distributed broadcasts it (bootstrap only), and the
+    library then calls ncclAllGather itself on the engine's stream inside
+    ts_shard_decode_step. world == 1 needs no NCCL at all."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        self.rank, self.world = rank, world
+        idb = (C.c_uint8 * 128)()
+        if world > 1:
+            import torch.distributed as dist
+
+            if rank == 0:
+                check(lib.ts_comm_unique_id(C.cast(idb, C.c_void_p)))
+            obj = [bytes(idb)]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            C.memmove(idb, obj[0], 128)
+        h = C.c_void_p()
+        check(lib.ts_comm_create(C.cast(idb, C.c_void_p), world, rank, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and lib is not None:
+            lib.ts_comm_destroy(self._h)
+            self._h = None
+
+
+def decode_step_native(shard, comm: LibraryComm, q, k, v, base: int, n_global: int, out=None):
+    """One sharded decode step in ONE library call (ts_shard_decode_step):
+    the four shard launches and the three ncclAllGather exchanges are issued
+    by the library on the shard's stream. Returns the [1 x H*d] output."""
+    torch = shard.torch
+    shard._follow_stream()
+    if out is None:
+        out = torch.empty(1, shard.H * shard.d, dtype=torch.float32, device=q.device)
+    check(lib.ts_shard_decode_step(shard._h, comm._h, shard._p(q), shard._p(k), shard._p(v), base, n_global,
+                                   shard._p(out)))
+    shard._qkv = (q, k, v)
+    return out
 
 
 class TorchDistExchange:
