@@ -606,7 +606,21 @@ WORKLOADS = {
 }
 
 
+_OUT = None  # the process's real stdout: only the one JSON line goes there
+
+
+def emit(line: dict):
+    os.write(_OUT if _OUT is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    global _OUT
+    # everything else the process prints (NCCL's INFO lines and version banner,
+    # library diagnostics) goes to stderr: fd 1 is pointed at fd 2, the JSON
+    # line is written to a private duplicate of the original stdout
+    sys.stdout.flush()
+    _OUT = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
@@ -629,7 +643,7 @@ def main():
             port = s.getsockname()[1]
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
                "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
-        sys.stdout.flush()
+        os.dup2(_OUT, 1)  # the launcher's ranks write the line to the real stdout
         os.execv(sys.executable, cmd)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -656,7 +670,7 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic", "config": config,
                 "cpu_baseline": {"value": round(us, 1), "unit": UNIT, "cores": 1, "kind": kind, "sample": sample},
                 "e2e": {"value": round(us, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        emit(line)
         return
 
     if world > 1 or workload == "sharded":
@@ -726,7 +740,7 @@ def main():
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
     if rank == 0:
-        print(json.dumps(line))
+        emit(line)
     if world > 1 or workload == "sharded":
         import torch
 

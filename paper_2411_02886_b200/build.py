@@ -27,7 +27,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
           "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
-SOURCES = ["decode.cu", "step.cu", "vote.cu", "util.cu", "aux.cu", "prefill.cu", "comm.cpp", "abi.cpp"]
+SOURCES = ["decode.cu", "step.cu", "vote.cu", "util.cu", "aux.cu", "prefill.cu", "prefill_tc.cu", "comm.cpp", "abi.cpp"]
 HEADERS = ["common.cuh", "params.h", "decode.h", "aux.h", "step.h", "vote.h", "util.h", "comm.h"]
 
 

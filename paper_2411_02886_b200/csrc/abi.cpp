@@ -40,6 +40,7 @@ thread_local std::string g_err;
 const bool g_force_global_s = std::getenv("TS_FORCE_GLOBAL_S") != nullptr && std::getenv("TS_FORCE_GLOBAL_S")[0];
 const int g_debug_flags = std::getenv("TS_DEBUG_FLAGS") ? std::atoi(std::getenv("TS_DEBUG_FLAGS")) : 0;
 const bool g_force_cuda_core_prefill = std::getenv("TS_CUDA_CORE_PREFILL") != nullptr;
+const bool g_prefill_mma_sync = std::getenv("TS_PREFILL_MMA_SYNC") != nullptr;  // dev: the mma.sync prefill kernel
 const bool g_no_lean = std::getenv("TS_NO_LEAN") != nullptr;  // dev: always the general kernel
 // the single-sequence step kernel (step.cu) is opt-in: TS_STEP=1. Measured on
 // B200 (profiles/r02_step/): stream 54.1 vs 52.5 us/step for the fused kernel
@@ -778,6 +779,9 @@ cudaError_t launch_prefill(tsb::PrefillAttendParams& pa, DevBuf& split_ws, cudaS
   if (pa.d == 128 && pa.H / pa.H_kv <= 8 && !g_force_cuda_core_prefill) {
     // bf16 parts of the chunk's K/V, owned by the caller's pool / engine (stream-ordered reuse)
     pa.split_ws = static_cast<uint16_t*>(split_ws.ensure(static_cast<size_t>(2) * 3 * pa.C * pa.H_kv * pa.d * 2));
+    const int G = pa.H / pa.H_kv;
+    // tcgen05 (prefill_tc.cu) for G in {1, 2, 4, 8}; mma.sync (prefill.cu) for the other G
+    if ((G == 1 || G == 2 || G == 4 || G == 8) && !g_prefill_mma_sync) return tsb::launch_prefill_tc(pa, st);
     return tsb::launch_prefill_flash(pa, st);
   }
   return tsb::launch_prefill_attend(pa, st);
