@@ -52,20 +52,32 @@ __global__ void kv_gather_kernel(const uint16_t* k_slab, const uint16_t* v_slab,
 }
 
 // Sequential fp64 column sums in row order: bit-identical to chunk_mean.
-__global__ void chunk_mean_kernel(const float* q, int c, int width, float* out) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= width) return;
-  double acc = 0.0;  // row order, as tensor.cpp:133-150 (16 loads in flight ahead of the adds)
-  int i = 0;
-  for (; i + 16 <= c; i += 16) {
-    float v[16];
+// CTA = 64 columns x 4 row groups; rows go through shared memory in tiles of
+// 128 (each thread keeps 32 loads in flight), then one thread per column adds
+// the tile's rows in order -- the load latency is paid once per tile, not once
+// per 16 rows.
+constexpr int kCmCols = 64, kCmTile = 128;
+__global__ void __launch_bounds__(256) chunk_mean_kernel(const float* q, int c, int width, float* out) {
+  __shared__ float tile[kCmTile][kCmCols + 1];
+  const int col = threadIdx.x & (kCmCols - 1), grp = threadIdx.x / kCmCols;  // 4 row groups
+  const int j = blockIdx.x * kCmCols + col;
+  double acc = 0.0;  // row order, as tensor.cpp:133-150
+  for (int r0 = 0; r0 < c; r0 += kCmTile) {
+    const int nr = min(kCmTile, c - r0);
+    float v[kCmTile / 4];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) v[u] = __ldg(q + static_cast<size_t>(i + u) * width + j);
+    for (int u = 0; u < kCmTile / 4; ++u) {
+      const int r = grp * (kCmTile / 4) + u;
+      v[u] = (r < nr && j < width) ? __ldg(q + static_cast<size_t>(r0 + r) * width + j) : 0.f;
+    }
 #pragma unroll
-    for (int u = 0; u < 16; ++u) acc += static_cast<double>(v[u]);
+    for (int u = 0; u < kCmTile / 4; ++u) tile[grp * (kCmTile / 4) + u][col] = v[u];
+    __syncthreads();
+    if (grp == 0)
+      for (int r = 0; r < nr; ++r) acc += static_cast<double>(tile[r][col]);
+    __syncthreads();
   }
-  for (; i < c; ++i) acc += static_cast<double>(q[static_cast<size_t>(i) * width + j]);
-  out[j] = static_cast<float>(acc * (1.0 / static_cast<double>(c)));
+  if (grp == 0 && j < width) out[j] = static_cast<float>(acc * (1.0 / static_cast<double>(c)));
 }
 
 __global__ void max_index_kernel(const uint32_t* idx, int n, unsigned int* out) {
@@ -405,7 +417,7 @@ cudaError_t launch_kv_gather(const uint16_t* k_slab, const uint16_t* v_slab, con
 }
 
 cudaError_t launch_chunk_mean(const float* q, int c, int width, float* out, cudaStream_t st) {
-  chunk_mean_kernel<<<(width + 31) / 32, 32, 0, st>>>(q, c, width, out);  // spread over the SMs
+  chunk_mean_kernel<<<(width + kCmCols - 1) / kCmCols, 256, 0, st>>>(q, c, width, out);
   return cudaGetLastError();
 }
 

@@ -54,7 +54,8 @@ constexpr int kOffV = kOffK + 2 * kKVTile;       // 2 buffers of V
 constexpr int kOffP = kOffV + 2 * kKVTile;       // 3 P parts
 constexpr int kOffRows = kOffP + 3 * kPPart;     // slab rows of the cached keys
 constexpr int kOffBar = kOffRows + kRowsUpFront * 4;
-constexpr int kSmem = kOffBar + 64;
+constexpr int kOffRed = kOffBar + 64;               // [2][128] row-max / row-sum exchange
+constexpr int kSmem = kOffRed + 2 * kM * 4;
 
 __device__ __forceinline__ uint16_t bfb(float x) { return __bfloat16_as_ushort(__float2bfloat16_rn(x)); }
 __device__ __forceinline__ void sp3(float x, float& h, float& m, float& l) {
@@ -255,10 +256,15 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   };
 
   // per-row (thread = row for tid < 128) online softmax state
-  const int m = tid;  // TMEM lane = query row
+  // two threads per query row: warp w takes TMEM lane quarter w % 4 (rows
+  // 32 (w % 4) ..) and half w / 4 of every row's key columns (S) / d columns (O)
+  const int m = (warp & 3) * 32 + (tid & 31);  // TMEM lane = query row
+  const int half = warp >> 2;
+  const uint32_t lane_sel = static_cast<uint32_t>((warp & 3) * 32) << 16;
+  float* red = reinterpret_cast<float*>(smem + kOffRed);  // [2][kM]
   const int hm = m / rows_per_head;
   const int i_row = i0 + (m - hm * rows_per_head);
-  float m_ref = -INFINITY, l_run = 0.f;
+  float m_ref = -INFINITY, l_run = 0.f;  // (l_run: this thread's half of the row)
   const float sl2 = p.scale * kLog2e;
   bool o_started = false;
 
@@ -266,71 +272,75 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   // reference max, P = 2^(s - m_ref) split into three bf16 parts -> smem.
   // Needs the previous P.V complete (P buffer, O rescale).
   auto softmax_tile = [&](uint32_t s_addr, int k0, bool chunk) {
-    if (tid < kM) {
-      const int lim = chunk ? min(n_cur - 1, i_row) + 1 : n_cached;  // visible keys: [0, lim)
-      float s[kKT];
-      {
-        float v16[16];
+    constexpr int KH = kKT / 2;  // this thread's key columns
+    const int lim = chunk ? min(n_cur - 1, i_row) + 1 : n_cached;  // visible keys: [0, lim)
+    const int kb = k0 + half * KH;
+    float s[KH];
+    {
+      float v16[16];
 #pragma unroll
-        for (int q = 0; q < kKT / 16; ++q) {
-          tmem_ld16(s_addr + (static_cast<uint32_t>(warp * 32) << 16) + q * 16, v16);
+      for (int q = 0; q < KH / 16; ++q) {
+        tmem_ld16(s_addr + lane_sel + half * KH + q * 16, v16);
 #pragma unroll
-          for (int u = 0; u < 16; ++u) s[q * 16 + u] = v16[u];
-        }
+        for (int u = 0; u < 16; ++u) s[q * 16 + u] = v16[u];
       }
-      float mt = -INFINITY;
-#pragma unroll
-      for (int u = 0; u < kKT; ++u) {
-        const bool ok = i_row < p.C && k0 + u < lim;
-        s[u] = ok ? s[u] * sl2 : -INFINITY;  // log2-domain logits
-        mt = fmaxf(mt, s[u]);
-      }
-      // lazy reference max: move it (and rescale O, l) only when it grows by
-      // > 8; the TMEM accesses are warp-collective (.sync.aligned), so the
-      // warp rescales together (corr = 1 for its other rows)
-      const bool need = mt > m_ref + 8.f;
-      float corr = 1.f;
-      if (need) {
-        corr = m_ref == -INFINITY ? 0.f : ex2_approx(m_ref - mt);
-        l_run *= corr;
-        m_ref = mt;
-      }
-      if (o_started && __any_sync(0xffffffffu, need)) {
-        float v16[16];
-#pragma unroll 1
-        for (int q = 0; q < kD / 16; ++q) {
-          const uint32_t a = o_tmem + (static_cast<uint32_t>(warp * 32) << 16) + q * 16;
-          tmem_ld16(a, v16);
-#pragma unroll
-          for (int u = 0; u < 16; ++u) v16[u] *= corr;
-          tmem_st16(a, v16);
-        }
-        tmem_wait_st();
-      }
-      float ls = 0.f;
-#pragma unroll
-      for (int c = 0; c < kKT / 8; ++c) {
-        uint32_t hw[4], mw[4], lw[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float p0 = s[c * 8 + 2 * u] == -INFINITY ? 0.f : ex2_approx(s[c * 8 + 2 * u] - m_ref);
-          const float p1 = s[c * 8 + 2 * u + 1] == -INFINITY ? 0.f : ex2_approx(s[c * 8 + 2 * u + 1] - m_ref);
-          ls += p0 + p1;
-          float h0, m0, l0, h1, m1, l1;
-          sp3(p0, h0, m0, l0);
-          sp3(p1, h1, m1, l1);
-          hw[u] = bfb(h0) | (static_cast<uint32_t>(bfb(h1)) << 16);
-          mw[u] = bfb(m0) | (static_cast<uint32_t>(bfb(m1)) << 16);
-          lw[u] = bfb(l0) | (static_cast<uint32_t>(bfb(l1)) << 16);
-        }
-        const uint32_t off = static_cast<uint32_t>(m * 128 + ((c ^ (m & 7)) << 4));
-        *reinterpret_cast<uint4*>(smem + kOffP + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        *reinterpret_cast<uint4*>(smem + kOffP + kPPart + off) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
-        *reinterpret_cast<uint4*>(smem + kOffP + 2 * kPPart + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-      }
-      l_run += ls;
-      tmem_fence_before_sync();
     }
+    float mt = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < KH; ++u) {
+      const bool ok = i_row < p.C && kb + u < lim;
+      s[u] = ok ? s[u] * sl2 : -INFINITY;  // log2-domain logits
+      mt = fmaxf(mt, s[u]);
+    }
+    red[half * kM + m] = mt;
+    __syncthreads();
+    mt = fmaxf(mt, red[(half ^ 1) * kM + m]);  // the row's max (both threads agree)
+    // lazy reference max: move it (and rescale O, l) only when it grows by
+    // > 8; the TMEM accesses are warp-collective (.sync.aligned), so the
+    // warp rescales together (corr = 1 for its other rows)
+    const bool need = mt > m_ref + 8.f;
+    float corr = 1.f;
+    if (need) {
+      corr = m_ref == -INFINITY ? 0.f : ex2_approx(m_ref - mt);
+      l_run *= corr;
+      m_ref = mt;
+    }
+    if (o_started && __any_sync(0xffffffffu, need)) {
+      float v16[16];
+#pragma unroll 1
+      for (int q = 0; q < kD / 32; ++q) {  // this thread's 64 of the row's 128 O columns
+        const uint32_t a = o_tmem + lane_sel + half * (kD / 2) + q * 16;
+        tmem_ld16(a, v16);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v16[u] *= corr;
+        tmem_st16(a, v16);
+      }
+      tmem_wait_st();
+    }
+    float ls = 0.f;
+#pragma unroll
+    for (int c = 0; c < KH / 8; ++c) {
+      uint32_t hw[4], mw[4], lw[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float p0 = s[c * 8 + 2 * u] == -INFINITY ? 0.f : ex2_approx(s[c * 8 + 2 * u] - m_ref);
+        const float p1 = s[c * 8 + 2 * u + 1] == -INFINITY ? 0.f : ex2_approx(s[c * 8 + 2 * u + 1] - m_ref);
+        ls += p0 + p1;
+        float h0, m0, l0, h1, m1, l1;
+        sp3(p0, h0, m0, l0);
+        sp3(p1, h1, m1, l1);
+        hw[u] = bfb(h0) | (static_cast<uint32_t>(bfb(h1)) << 16);
+        mw[u] = bfb(m0) | (static_cast<uint32_t>(bfb(m1)) << 16);
+        lw[u] = bfb(l0) | (static_cast<uint32_t>(bfb(l1)) << 16);
+      }
+      const int cc = half * (KH / 8) + c;  // 16-byte chunk of the row's 128 B of P
+      const uint32_t off = static_cast<uint32_t>(m * 128 + ((cc ^ (m & 7)) << 4));
+      *reinterpret_cast<uint4*>(smem + kOffP + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      *reinterpret_cast<uint4*>(smem + kOffP + kPPart + off) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+      *reinterpret_cast<uint4*>(smem + kOffP + 2 * kPPart + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+    l_run += ls;
+    tmem_fence_before_sync();
     fence_async_smem();
     __syncthreads();
   };
@@ -414,15 +424,20 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
     }
     o_started = true;
   }
-  // ---- epilogue: O / l -> out row (i_row, head g + hm * H_kv)
-  if (tid < kM) {  // (warp-collective TMEM loads; rows past the chunk are not stored)
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    const bool live = i_row < p.C;
-    float* orow = p.out + static_cast<size_t>(live ? i_row : 0) * p.H * kD + static_cast<size_t>(g + hm * p.H_kv) * kD;
+  // ---- epilogue: O / l -> out row (i_row, head g + hm * H_kv), each thread
+  // its half of the d columns; l = the two halves' sums
+  red[half * kM + m] = l_run;
+  __syncthreads();
+  {
+    const float l = l_run + red[(half ^ 1) * kM + m];
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    const bool live = i_row < p.C;  // (warp-collective TMEM loads; rows past the chunk are not stored)
+    float* orow = p.out + static_cast<size_t>(live ? i_row : 0) * p.H * kD + static_cast<size_t>(g + hm * p.H_kv) * kD +
+                  half * (kD / 2);
     float v16[16];
 #pragma unroll 1
-    for (int q = 0; q < kD / 16; ++q) {
-      tmem_ld16(o_tmem + (static_cast<uint32_t>(warp * 32) << 16) + q * 16, v16);
+    for (int q = 0; q < kD / 32; ++q) {
+      tmem_ld16(o_tmem + lane_sel + half * (kD / 2) + q * 16, v16);
       if (live)
 #pragma unroll
         for (int u = 0; u < 16; u += 4)
