@@ -638,7 +638,7 @@ struct ts_engine {
   DevBuf trace;
   bool trace_on = false;
   // prefill scratch
-  DevBuf p_qmean, p_sel, p_crit, p_state, p_att, p_natt, p_bad, p_q, p_k, p_v, p_out, p_split;
+  DevBuf p_qmean, p_sel, p_crit, p_state, p_att, p_natt, p_bad, p_q, p_k, p_v, p_out, p_split, p_trace;
 
   ~ts_engine() {
     if (h_q) cudaFreeHost(h_q);
@@ -1741,8 +1741,30 @@ ts_status ts_engine_prefill(ts_engine* e, size_t seq, const float* q, const floa
       pa.d = d;
       pa.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
       pa.out = oc;
+      static const bool ptrace = std::getenv("TS_PREFILL_TRACE") != nullptr;  // dev: stamps of CTA (0, 0)
+      if (ptrace) {
+        pa.trace = static_cast<unsigned long long*>(e->p_trace.ensure(512 * 8));
+        ck(cudaMemsetAsync(pa.trace, 0, 512 * 8, st), "memset");
+      }
       ck(launch_prefill(pa, e->p_split, st), "prefill_attend");
       g_launches.fetch_add(1);
+      if (ptrace) {
+        unsigned long long h[512];
+        ck(cudaMemcpyAsync(h, pa.trace, sizeof h, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+        std::fprintf(stderr, "[prefill trace] q+tmem %.2f us, first tile wait %.2f us, cached tiles end %.2f us, chunk end %.2f, total %.2f\n",
+                     (h[5] - h[0]) / 1e3, (h[1] - h[0]) / 1e3, (h[2] - h[0]) / 1e3, (h[3] - h[0]) / 1e3, (h[4] - h[0]) / 1e3);
+        double w = 0, pu = 0, sm = 0, pv = 0;
+        int n = 0;
+        for (int t = 1; t < 100 && h[11 + 4 * t]; ++t, ++n) {
+          w += (h[8 + 4 * t] - h[11 + 4 * (t - 1)]) / 1e3;
+          pu += (h[9 + 4 * t] - h[8 + 4 * t]) / 1e3;
+          sm += (h[10 + 4 * t] - h[9 + 4 * t]) / 1e3;
+          pv += (h[11 + 4 * t] - h[10 + 4 * t]) / 1e3;
+        }
+        if (n) std::fprintf(stderr, "[prefill trace] per cached tile (%d): wait QK %.2f, publish+issue %.2f, softmax %.2f, PV %.2f us\n",
+                            n, w / n, pu / n, sm / n, pv / n);
+      }
       if (!o_dev) ck(cudaMemcpyAsync(out + begin * W, oc, len * W * 4, cudaMemcpyDeviceToHost, st), "D2H");
       if (trace_counts && chunk < max_chunks) {
         CacheState cs{};

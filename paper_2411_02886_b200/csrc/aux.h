@@ -21,6 +21,7 @@ struct PrefillAttendParams {
   float scale;
   float* out;              // [C][H*d]
   uint16_t* split_ws;      // tensor-core path: [2][3][C][H_kv*d] bf16 parts of the chunk K/V
+  unsigned long long* trace;  // dev: %globaltimer stamps of CTA (0, 0) of the tcgen05 kernel (nullptr: off)
 };
 
 cudaError_t launch_kv_append(uint16_t* k_slab, uint16_t* v_slab, const float* k, const float* v,

@@ -58,11 +58,20 @@ constexpr int kOffRed = kOffBar + 64;               // [2][128] row-max / row-su
 constexpr int kSmem = kOffRed + 2 * kM * 4;
 
 __device__ __forceinline__ uint16_t bfb(float x) { return __bfloat16_as_ushort(__float2bfloat16_rn(x)); }
+// x = h + m + l exactly: h = x truncated to bf16 (8 significant bits), the
+// residual r = x - h is exact in fp32 and has at most 16 significant bits,
+// m = r truncated, l = r - m has at most 8 -- every part is a bf16 value
+// (its fp32 bits end in 16 zeros). Bit masks and two FADDs: no conversion
+// instructions on the quarter-rate pipe.
 __device__ __forceinline__ void sp3(float x, float& h, float& m, float& l) {
-  h = __bfloat162float(__float2bfloat16_rn(x));
+  h = __uint_as_float(__float_as_uint(x) & 0xFFFF0000u);
   const float r = x - h;
-  m = __bfloat162float(__float2bfloat16_rn(r));
+  m = __uint_as_float(__float_as_uint(r) & 0xFFFF0000u);
   l = r - m;
+}
+// two bf16 values (fp32 with zero low halves) -> one packed word
+__device__ __forceinline__ uint32_t pk2(float lo, float hi) {
+  return __byte_perm(__float_as_uint(lo), __float_as_uint(hi), 0x7632);
 }
 
 // byte offset of 16-byte chunk c (0..15 along d) of row r in a K-major
@@ -159,6 +168,15 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);  // [0] QK done, [1] P.V done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 16);
   const bool rows_up_front = n_cached <= kRowsUpFront;
+  unsigned long long* trc = (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) ? p.trace : nullptr;
+  auto stamp = [&](int i) {
+    if (trc && i < 512) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      trc[i] = g;
+    }
+  };
+  stamp(0);
   auto lookup = [&](int key) -> int32_t {
     const uint32_t tok = p.att[key];
     return p.page_size == 1 ? p.page_table[tok]
@@ -171,6 +189,7 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, 256);
+  stamp(5);
   // ---- Q parts: row m = (head m / rows_per_head, chunk row i0 + m % rows_per_head)
   for (int idx = tid; idx < kM * (kD / 8); idx += kThr) {
     const int m = idx >> 4, c = idx & 15;
@@ -200,8 +219,24 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
     *reinterpret_cast<uint4*>(smem + kOffQ + kQPart + off) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
     *reinterpret_cast<uint4*>(smem + kOffQ + 2 * kQPart + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
   }
-  if (rows_up_front)
-    for (int key = tid; key < n_cached; key += kThr) rows_all[key] = lookup(key);
+  if (rows_up_front) {
+    // all of this thread's list loads in flight, then all its page-table loads
+    constexpr int kPer = kRowsUpFront / kThr;
+    uint32_t tok[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int key = tid + u * kThr;
+      tok[u] = key < n_cached ? __ldg(p.att + key) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int key = tid + u * kThr;
+      if (key < n_cached)
+        rows_all[key] = p.page_size == 1 ? __ldg(p.page_table + tok[u])
+                                         : __ldg(p.page_table + tok[u] / p.page_size) * p.page_size +
+                                               static_cast<int32_t>(tok[u] % p.page_size);
+    }
+  }
   tmem_fence_before_sync();
   __syncthreads();
   tmem_fence_after_sync();
@@ -271,7 +306,14 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   // ---- softmax of one tile's 64 scores per row (S at s_addr): mask, lazy
   // reference max, P = 2^(s - m_ref) split into three bf16 parts -> smem.
   // Needs the previous P.V complete (P buffer, O rescale).
-  auto softmax_tile = [&](uint32_t s_addr, int k0, bool chunk) {
+  uint32_t s_phase = 0, o_phase = 0;
+  auto wait_bar = [&](uint64_t* bb, uint32_t& ph) {
+    mbar_wait(bb, ph);
+    ph ^= 1u;
+    tmem_fence_after_sync();
+  };
+  bool pv_pending = false;  // a P.V whose completion nobody waited for yet
+  auto softmax_tile = [&](uint32_t s_addr, int k0, bool chunk, bool wait_v) {
     constexpr int KH = kKT / 2;  // this thread's key columns
     const int lim = chunk ? min(n_cur - 1, i_row) + 1 : n_cached;  // visible keys: [0, lim)
     const int kb = k0 + half * KH;
@@ -295,6 +337,10 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
     red[half * kM + m] = mt;
     __syncthreads();
     mt = fmaxf(mt, red[(half ^ 1) * kM + m]);  // the row's max (both threads agree)
+    if (pv_pending) {  // the previous P.V: O may be rescaled and P rewritten only after it
+      wait_bar(&bar[1], o_phase);
+      pv_pending = false;
+    }
     // lazy reference max: move it (and rescale O, l) only when it grows by
     // > 8; the TMEM accesses are warp-collective (.sync.aligned), so the
     // warp rescales together (corr = 1 for its other rows)
@@ -329,9 +375,9 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
         float h0, m0, l0, h1, m1, l1;
         sp3(p0, h0, m0, l0);
         sp3(p1, h1, m1, l1);
-        hw[u] = bfb(h0) | (static_cast<uint32_t>(bfb(h1)) << 16);
-        mw[u] = bfb(m0) | (static_cast<uint32_t>(bfb(m1)) << 16);
-        lw[u] = bfb(l0) | (static_cast<uint32_t>(bfb(l1)) << 16);
+        hw[u] = pk2(h0, h1);
+        mw[u] = pk2(m0, m1);
+        lw[u] = pk2(l0, l1);
       }
       const int cc = half * (KH / 8) + c;  // 16-byte chunk of the row's 128 B of P
       const uint32_t off = static_cast<uint32_t>(m * 128 + ((cc ^ (m & 7)) << 4));
@@ -340,6 +386,7 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
       *reinterpret_cast<uint4*>(smem + kOffP + 2 * kPPart + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
     l_run += ls;
+    if (wait_v) cp_async_wait<1>();  // this tile's V (the newest group, K(t + 2), may stay in flight)
     tmem_fence_before_sync();
     fence_async_smem();
     __syncthreads();
@@ -349,12 +396,6 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   // CUDA cores run softmax(t); K(t + 2) is gathered as soon as QK(t) freed
   // its buffer, V(t + 2) as soon as PV(t) did. Two S buffers in TMEM
   // (columns 0 / 64), two mbarriers (QK / PV completions) with their phases.
-  uint32_t s_phase = 0, o_phase = 0;
-  auto wait_bar = [&](uint64_t* bb, uint32_t& ph) {
-    mbar_wait(bb, ph);
-    ph ^= 1u;
-    tmem_fence_after_sync();
-  };
   if (nct > 0) {
     gather(0, 0, 0, true, true);
     if (nct > 1) gather(1, 1, 0, true, true);
@@ -367,31 +408,43 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
       umma_commit(&bar[0]);
     }
   }
+  stamp(1);
+  // cp.async groups per iteration, in order: K(t + 2) (after QK(t)), V(t + 1)
+  // (after PV(t - 1)) -- empty groups keep the count when a tile is absent
   for (int t = 0; t < nct; ++t) {
     const int b = t & 1;
     wait_bar(&bar[0], s_phase);  // QK(t) done: S[b] ready, K buffer b free
-    if (t + 1 < nct) {
-      // K(t + 1) / V(t + 1) landed (the only younger group: K(t + 2), not issued yet)
-      cp_async_wait<0>();
-      fence_async_smem();
-      __syncthreads();
-      if (tid == 0) {
-        tmem_fence_after_sync();
-        issue_qk(sbase + kOffQ, sbase + kOffK + (b ^ 1) * kKVTile, s_tmem + (b ^ 1) * kKT, 0, true);
-        umma_commit(&bar[0]);
-      }
+    stamp(8 + 4 * t);
+    cp_async_wait<1>();  // K(t + 1) landed (the newest group, V(t), may not have)
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0 && t + 1 < nct) {
+      tmem_fence_after_sync();
+      issue_qk(sbase + kOffQ, sbase + kOffK + (b ^ 1) * kKVTile, s_tmem + (b ^ 1) * kKT, 0, true);
+      umma_commit(&bar[0]);
     }
+    stamp(9 + 4 * t);
     if (t + 2 < nct) gather(t + 2, b, 0, true, false);  // K only: V buffer b still feeds PV(t)
-    softmax_tile(s_tmem + b * kKT, t * kKT, false);
+    else cp_async_commit();
+    softmax_tile(s_tmem + b * kKT, t * kKT, false, true);  // (waits PV(t - 1), then V(t))
+    stamp(10 + 4 * t);
     if (tid == 0) {
       tmem_fence_after_sync();
       issue_pv(sbase + kOffP, sbase + kOffV + b * kKVTile, o_tmem, 0, !o_started);
       umma_commit(&bar[1]);
     }
     o_started = true;
-    wait_bar(&bar[1], o_phase);  // PV(t) done: P and V buffer b free
-    if (t + 2 < nct) gather(t + 2, b, 0, false, true);
+    pv_pending = true;
+    stamp(11 + 4 * t);
+    // V(t + 1) into V buffer b ^ 1, freed by PV(t - 1) (V(1) came with the prologue)
+    if (t >= 1 && t + 1 < nct) gather(t + 1, b ^ 1, 0, false, true);
+    else cp_async_commit();
   }
+  if (pv_pending) {
+    wait_bar(&bar[1], o_phase);
+    pv_pending = false;
+  }
+  stamp(2);
   if (nct > 1) __syncthreads();
 
   // ---- the chunk's own rows: fp32 K/V in three exact bf16 parts, one part
@@ -408,7 +461,7 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
       wait_bar(&bar[0], s_phase);
       __syncthreads();
     }
-    softmax_tile(s_tmem, (t - nct) * kKT, true);
+    softmax_tile(s_tmem, (t - nct) * kKT, true, false);
     for (int pv = 0; pv < 3; ++pv) {
       if (pv > 0) {
         gather(t, 0, pv, false, true);
@@ -424,6 +477,7 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
     }
     o_started = true;
   }
+  stamp(3);
   // ---- epilogue: O / l -> out row (i_row, head g + hm * H_kv), each thread
   // its half of the d columns; l = the two halves' sums
   red[half * kM + m] = l_run;
@@ -445,6 +499,7 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
               make_float4(v16[u] * inv, v16[u + 1] * inv, v16[u + 2] * inv, v16[u + 3] * inv);
     }
   }
+  stamp(4);
   tmem_fence_before_sync();
   __syncthreads();
   if (warp == 0) {
@@ -457,9 +512,9 @@ __global__ void split3_tc_kernel(const float* __restrict__ x, int n, uint16_t* _
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     float h, m, l;
     sp3(x[i], h, m, l);
-    out[i] = bfb(h);
-    out[n + i] = bfb(m);
-    out[2 * static_cast<size_t>(n) + i] = bfb(l);
+    out[i] = static_cast<uint16_t>(__float_as_uint(h) >> 16);
+    out[n + i] = static_cast<uint16_t>(__float_as_uint(m) >> 16);
+    out[2 * static_cast<size_t>(n) + i] = static_cast<uint16_t>(__float_as_uint(l) >> 16);
   }
 }
 
