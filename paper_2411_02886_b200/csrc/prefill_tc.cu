@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
     mbar_init(&bar[1], 1);  // P.V completions
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc(tmem_slot, 256);
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
   stamp(5);
   // ---- Q parts: row m = (head m / rows_per_head, chunk row i0 + m % rows_per_head)
   for (int idx = tid; idx < kM * (kD / 8); idx += kThr) {
@@ -242,7 +242,8 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   tmem_fence_after_sync();
   const uint32_t tbase = *tmem_slot;
   const uint32_t s_tmem = tbase;        // columns [0, 64)
-  const uint32_t o_tmem = tbase + 128;  // columns [128, 256)
+  const uint32_t o_tmem = tbase + 128;   // columns [128, 256): one tile's P.V (fresh per tile)
+  const uint32_t orun_tmem = tbase + 256;  // columns [256, 384): the running O, fp32 round-to-nearest adds
 
   // gather of a tile's K and V rows (part `part` of the chunk's split copy
   // for chunk tiles) into buffer b, swizzled; padding rows zeroed
@@ -301,7 +302,7 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   const int i_row = i0 + (m - hm * rows_per_head);
   float m_ref = -INFINITY, l_run = 0.f;  // (l_run: this thread's half of the row)
   const float sl2 = p.scale * kLog2e;
-  bool o_started = false;
+
 
   // ---- softmax of one tile's 64 scores per row (S at s_addr): mask, lazy
   // reference max, P = 2^(s - m_ref) split into three bf16 parts -> smem.
@@ -312,7 +313,41 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
     ph ^= 1u;
     tmem_fence_after_sync();
   };
-  bool pv_pending = false;  // a P.V whose completion nobody waited for yet
+  bool pv_pending = false;     // a P.V whose completion nobody waited for yet
+  bool delta_pending = false;  // a completed tile P.V not yet added into O_run
+  bool o_folded = false;       // O_run holds data
+  // O_run (+)= delta, then * c: this thread's 64 of the row's 128 columns
+  auto fold = [&](float c) {
+    float a16[16], b16[16];
+#pragma unroll 1
+    for (int q = 0; q < kD / 32; ++q) {
+      const uint32_t col = lane_sel + half * (kD / 2) + q * 16;
+      tmem_ld16(o_tmem + col, a16);
+      if (o_folded) {
+        tmem_ld16(orun_tmem + col, b16);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) a16[u] = (b16[u] + a16[u]) * c;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) a16[u] *= c;
+      }
+      tmem_st16(orun_tmem + col, a16);
+    }
+    tmem_wait_st();
+    o_folded = true;
+  };
+  auto fold_scale = [&](float c) {
+    float a16[16];
+#pragma unroll 1
+    for (int q = 0; q < kD / 32; ++q) {
+      const uint32_t col = lane_sel + half * (kD / 2) + q * 16;
+      tmem_ld16(orun_tmem + col, a16);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) a16[u] *= c;
+      tmem_st16(orun_tmem + col, a16);
+    }
+    tmem_wait_st();
+  };
   auto softmax_tile = [&](uint32_t s_addr, int k0, bool chunk, bool wait_v) {
     constexpr int KH = kKT / 2;  // this thread's key columns
     const int lim = chunk ? min(n_cur - 1, i_row) + 1 : n_cached;  // visible keys: [0, lim)
@@ -351,17 +386,14 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
       l_run *= corr;
       m_ref = mt;
     }
-    if (o_started && __any_sync(0xffffffffu, need)) {
-      float v16[16];
-#pragma unroll 1
-      for (int q = 0; q < kD / 32; ++q) {  // this thread's 64 of the row's 128 O columns
-        const uint32_t a = o_tmem + lane_sel + half * (kD / 2) + q * 16;
-        tmem_ld16(a, v16);
-#pragma unroll
-        for (int u = 0; u < 16; ++u) v16[u] *= corr;
-        tmem_st16(a, v16);
-      }
-      tmem_wait_st();
+    // the previous tile's P.V enters the running O here, rescaled with it:
+    // O_run = (O_run + delta) * corr, on the CUDA cores (round-to-nearest;
+    // the tensor core only ever accumulates one tile)
+    if (delta_pending) {
+      fold(corr);
+      delta_pending = false;
+    } else if (o_folded && __any_sync(0xffffffffu, need)) {
+      fold_scale(corr);
     }
     float ls = 0.f;
 #pragma unroll
@@ -430,11 +462,11 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
     stamp(10 + 4 * t);
     if (tid == 0) {
       tmem_fence_after_sync();
-      issue_pv(sbase + kOffP, sbase + kOffV + b * kKVTile, o_tmem, 0, !o_started);
+      issue_pv(sbase + kOffP, sbase + kOffV + b * kKVTile, o_tmem, 0, true);
       umma_commit(&bar[1]);
     }
-    o_started = true;
     pv_pending = true;
+    delta_pending = true;
     stamp(11 + 4 * t);
     // V(t + 1) into V buffer b ^ 1, freed by PV(t - 1) (V(1) came with the prologue)
     if (t >= 1 && t + 1 < nct) gather(t + 1, b ^ 1, 0, false, true);
@@ -469,19 +501,20 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
       }
       if (tid == 0) {
         tmem_fence_after_sync();
-        issue_pv(sbase + kOffP, sbase + kOffV, o_tmem, pv, !o_started && pv == 0);
+        issue_pv(sbase + kOffP, sbase + kOffV, o_tmem, pv, pv == 0);
         umma_commit(&bar[1]);
       }
       wait_bar(&bar[1], o_phase);
       __syncthreads();
     }
-    o_started = true;
+    delta_pending = true;
   }
   stamp(3);
   // ---- epilogue: O / l -> out row (i_row, head g + hm * H_kv), each thread
   // its half of the d columns; l = the two halves' sums
   red[half * kM + m] = l_run;
   __syncthreads();
+  if (delta_pending) fold(1.f);  // (its P.V completed: waited after the loops)
   {
     const float l = l_run + red[(half ^ 1) * kM + m];
     const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -491,7 +524,7 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
     float v16[16];
 #pragma unroll 1
     for (int q = 0; q < kD / 32; ++q) {
-      tmem_ld16(o_tmem + lane_sel + half * (kD / 2) + q * 16, v16);
+      tmem_ld16(orun_tmem + lane_sel + half * (kD / 2) + q * 16, v16);
       if (live)
 #pragma unroll
         for (int u = 0; u < 16; u += 4)
@@ -504,7 +537,7 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   __syncthreads();
   if (warp == 0) {
     tmem_fence_after_sync();
-    tmem_dealloc(tbase, 256);
+    tmem_dealloc(tbase, 512);
   }
 }
 
