@@ -1392,11 +1392,6 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   const int tid = threadIdx.x;
   const bool do_select = (pmode & kModeSelect) != 0;
 
-  trace_pt(p, 0);
-  // the Selection Cache decision's operands first: they head the critical path
-  DecisionLoads dl{};
-  const bool dec_early = sd.select && !(pmode & kModeShardSelect) && (pmode & kModeCache);
-  if (dec_early) decision_issue(sd, width, dl);
   if (FAST && tid < kMaxBarPairs) {
     mbar_init(&sm.full[tid], 1);
     mbar_init(&sm.empty[tid], p.H_kv);  // the H_kv consumer warps of a phase
@@ -1416,9 +1411,14 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
     for (int i = tid; i < kMaxSeqPerLaunch * p.H_kv; i += blockDim.x) nxt[i] = 0u;
   }
 
+  trace_pt(p, 0);
   unsigned long long* const trc = p.trace ? p.trace + blockIdx.x * kTraceStride : nullptr;
   TSB_STOP_AT(15);  // launch + prologue only
   // ---- phase 0: append, scan frames, Selection Cache decision(s), hit prep
+  // the decision's loads first: they head the critical path
+  DecisionLoads dl{};
+  const bool dec_early = sd.select && !(pmode & kModeShardSelect) && (pmode & kModeCache);
+  if (dec_early) decision_issue(sd, width, dl);
   stamp(trc, 45);
   const int T = sd.n_cand;
   const int j0 = min(T, cs * p.tpc);
