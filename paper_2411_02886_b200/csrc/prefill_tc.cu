@@ -40,7 +40,9 @@ namespace {
 constexpr int kD = 128;
 constexpr int kM = 128;          // query rows per CTA (UMMA M)
 constexpr int kKT = 64;          // keys per tile (UMMA N of S, K of P.V)
-constexpr int kThr = 256;
+constexpr int kThr = 384;        // 8 softmax warps, 1 MMA warp, 3 producer warps
+constexpr int kSmThr = 256;      // softmax threads (two per query row)
+constexpr int kProdThr = 96;     // producer threads (warps 9-11)
 constexpr int kRowsUpFront = 4096;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -54,8 +56,8 @@ constexpr int kOffV = kOffK + 2 * kKVTile;       // 2 buffers of V
 constexpr int kOffP = kOffV + 2 * kKVTile;       // 3 P parts
 constexpr int kOffRows = kOffP + 3 * kPPart;     // slab rows of the cached keys
 constexpr int kOffBar = kOffRows + kRowsUpFront * 4;
-constexpr int kOffRed = kOffBar + 64;               // [2][128] row-max / row-sum exchange
-constexpr int kSmem = kOffRed + 2 * kM * 4;
+constexpr int kOffRed = kOffBar + 256;              // [2 tiles][2 halves][128] row-max / row-sum exchange
+constexpr int kSmem = kOffRed + 4 * kM * 4;
 
 __device__ __forceinline__ uint16_t bfb(float x) { return __bfloat16_as_ushort(__float2bfloat16_rn(x)); }
 // x = h + m + l exactly: h = x truncated to bf16 (8 significant bits), the
@@ -150,6 +152,20 @@ __device__ __forceinline__ void issue_pv(uint32_t p_base, uint32_t v_base, uint3
     }
 }
 
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// Warp roles in the cached-key loop (the chunk's own rows follow with every
+// thread on one serialised path):
+//   warps 0-7   softmax: two threads per query row (TMEM lane quarter w % 4,
+//               key / d column half w / 4)
+//   warp 8      MMA issue (lane 0): QK(t) as soon as K(t) landed and S[t % 2]
+//               was read, then P.V(t - 1) -- the tensor core runs QK(t) while
+//               the softmax warps work on tile t - 1
+//   warps 9-11  producers: cp.async gathers of K(t) / V(t) into the double
+//               buffers, each signalled by its own mbarrier
+// Every hand-off is an mbarrier per buffer, so no waiter can fall two phases
+// behind: s_full[b] (QK done), pv_done[b] (P.V done), kvk_full[b] / kvv_full[b]
+// (K / V landed), s_free[b] (S read), p_full (P written).
 __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams p, const uint16_t* kc3,
                                                              const uint16_t* vc3) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -157,7 +173,7 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   const int rows_per_head = kM / G;  // chunk rows per CTA
   const int g = blockIdx.y;
   const int i0 = blockIdx.x * rows_per_head;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int row_elems = p.H_kv * kD;
   const int n_cached = p.n_att_ptr ? *p.n_att_ptr : p.n_att;
   const int n_cur = min(p.C, i0 + rows_per_head);  // chunk rows any row here can see
@@ -165,15 +181,23 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   const int n_tiles = nct + (n_cur + kKT - 1) / kKT;
   const uint32_t sbase = smem_u32(smem);
   int32_t* rows_all = reinterpret_cast<int32_t*>(smem + kOffRows);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);  // [0] QK done, [1] P.V done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 16);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint64_t* s_full = bars + 0;    // [2]
+  uint64_t* pv_done = bars + 2;   // [2]
+  uint64_t* kvk_full = bars + 4;  // [2]
+  uint64_t* kvv_full = bars + 6;  // [2]
+  uint64_t* s_free = bars + 8;    // [2]
+  uint64_t* p_full = bars + 10;   // [1]
+  uint64_t* c_done = bars + 11;   // [1] the serialised chunk path's MMAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 128);
+  float* red = reinterpret_cast<float*>(smem + kOffRed);  // [2][2][kM]
   const bool rows_up_front = n_cached <= kRowsUpFront;
   unsigned long long* trc = (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) ? p.trace : nullptr;
   auto stamp = [&](int i) {
     if (trc && i < 512) {
-      unsigned long long g;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-      trc[i] = g;
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      trc[i] = gt;
     }
   };
   stamp(0);
@@ -184,8 +208,15 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   };
 
   if (tid == 0) {
-    mbar_init(&bar[0], 1);  // QK completions
-    mbar_init(&bar[1], 1);  // P.V completions
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&pv_done[i], 1);
+      mbar_init(&kvk_full[i], kProdThr);
+      mbar_init(&kvv_full[i], kProdThr);
+      mbar_init(&s_free[i], kSmThr);
+    }
+    mbar_init(p_full, kSmThr);
+    mbar_init(c_done, 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, 512);
@@ -210,9 +241,9 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
       float h0, m0, l0, h1, m1, l1;
       sp3(x[2 * u], h0, m0, l0);
       sp3(x[2 * u + 1], h1, m1, l1);
-      hw[u] = bfb(h0) | (static_cast<uint32_t>(bfb(h1)) << 16);
-      mw[u] = bfb(m0) | (static_cast<uint32_t>(bfb(m1)) << 16);
-      lw[u] = bfb(l0) | (static_cast<uint32_t>(bfb(l1)) << 16);
+      hw[u] = pk2(h0, h1);
+      mw[u] = pk2(m0, m1);
+      lw[u] = pk2(l0, l1);
     }
     const uint32_t off = sw_off(kM, m, c);
     *reinterpret_cast<uint4*>(smem + kOffQ + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
@@ -221,7 +252,7 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   }
   if (rows_up_front) {
     // all of this thread's list loads in flight, then all its page-table loads
-    constexpr int kPer = kRowsUpFront / kThr;
+    constexpr int kPer = (kRowsUpFront + kThr - 1) / kThr;
     uint32_t tok[kPer];
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
@@ -237,20 +268,22 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
                                                static_cast<int32_t>(tok[u] % p.page_size);
     }
   }
+  fence_async_smem();  // Q parts -> the tensor core
   tmem_fence_before_sync();
   __syncthreads();
   tmem_fence_after_sync();
   const uint32_t tbase = *tmem_slot;
-  const uint32_t s_tmem = tbase;        // columns [0, 64)
-  const uint32_t o_tmem = tbase + 128;   // columns [128, 256): one tile's P.V (fresh per tile)
+  const uint32_t s_tmem = tbase;           // columns [0, 128): S[2] of 64 columns
+  const uint32_t o_tmem = tbase + 128;     // columns [128, 256): one tile's P.V (fresh per tile)
   const uint32_t orun_tmem = tbase + 256;  // columns [256, 384): the running O, fp32 round-to-nearest adds
 
-  // gather of a tile's K and V rows (part `part` of the chunk's split copy
-  // for chunk tiles) into buffer b, swizzled; padding rows zeroed
-  auto gather = [&](int tile, int b, int part, bool k_on, bool v_on) {
+  // gather of a tile's K and/or V rows (part `part` of the chunk's split copy
+  // for chunk tiles) into buffer b, swizzled, by threads gt of gn; padding
+  // rows zeroed; one cp.async group
+  auto gather = [&](int tile, int b, int part, bool k_on, bool v_on, int gt, int gn) {
     uint8_t* kb = smem + kOffK + b * kKVTile;
     uint8_t* vb = smem + kOffV + b * kKVTile;
-    for (int idx = tid; idx < kKT * 16; idx += kThr) {
+    for (int idx = gt; idx < kKT * 16; idx += gn) {
       const int r = idx >> 4, c = idx & 15;
       const uint32_t off = sw_off(kKT, r, c);
       const uint16_t* ks = nullptr;
@@ -284,38 +317,19 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
     cp_async_commit();
   };
 
-  // operands written by this CTA's threads -> visible to the tensor core
-  auto publish = [&]() {
-    cp_async_wait<0>();
-    fence_async_smem();
-    __syncthreads();
-  };
-
-  // per-row (thread = row for tid < 128) online softmax state
-  // two threads per query row: warp w takes TMEM lane quarter w % 4 (rows
-  // 32 (w % 4) ..) and half w / 4 of every row's key columns (S) / d columns (O)
-  const int m = (warp & 3) * 32 + (tid & 31);  // TMEM lane = query row
-  const int half = warp >> 2;
+  // ---- softmax state: thread (row m, half) of warps 0-7
+  const bool is_sm = warp < 8;
+  const int m = (warp & 3) * 32 + lane;  // TMEM lane = query row
+  const int half = (warp >> 2) & 1;
   const uint32_t lane_sel = static_cast<uint32_t>((warp & 3) * 32) << 16;
-  float* red = reinterpret_cast<float*>(smem + kOffRed);  // [2][kM]
   const int hm = m / rows_per_head;
   const int i_row = i0 + (m - hm * rows_per_head);
   float m_ref = -INFINITY, l_run = 0.f;  // (l_run: this thread's half of the row)
   const float sl2 = p.scale * kLog2e;
-
-
-  // ---- softmax of one tile's 64 scores per row (S at s_addr): mask, lazy
-  // reference max, P = 2^(s - m_ref) split into three bf16 parts -> smem.
-  // Needs the previous P.V complete (P buffer, O rescale).
-  uint32_t s_phase = 0, o_phase = 0;
-  auto wait_bar = [&](uint64_t* bb, uint32_t& ph) {
-    mbar_wait(bb, ph);
-    ph ^= 1u;
-    tmem_fence_after_sync();
-  };
-  bool pv_pending = false;     // a P.V whose completion nobody waited for yet
   bool delta_pending = false;  // a completed tile P.V not yet added into O_run
   bool o_folded = false;       // O_run holds data
+  constexpr int KH = kKT / 2;  // this thread's key columns
+  float s[KH];
   // O_run (+)= delta, then * c: this thread's 64 of the row's 128 columns
   auto fold = [&](float c) {
     float a16[16], b16[16];
@@ -348,37 +362,32 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
     }
     tmem_wait_st();
   };
-  auto softmax_tile = [&](uint32_t s_addr, int k0, bool chunk, bool wait_v) {
-    constexpr int KH = kKT / 2;  // this thread's key columns
+  // (1) this thread's 32 scores of the tile -> s[], own max -> red[rb][half][m]
+  auto sm_load = [&](uint32_t s_addr, int k0, bool chunk, int rb) {
     const int lim = chunk ? min(n_cur - 1, i_row) + 1 : n_cached;  // visible keys: [0, lim)
-    const int kb = k0 + half * KH;
-    float s[KH];
-    {
-      float v16[16];
+    const int kb0 = k0 + half * KH;
+    float v16[16];
 #pragma unroll
-      for (int q = 0; q < KH / 16; ++q) {
-        tmem_ld16(s_addr + lane_sel + half * KH + q * 16, v16);
+    for (int q = 0; q < KH / 16; ++q) {
+      tmem_ld16(s_addr + lane_sel + half * KH + q * 16, v16);
 #pragma unroll
-        for (int u = 0; u < 16; ++u) s[q * 16 + u] = v16[u];
-      }
+      for (int u = 0; u < 16; ++u) s[q * 16 + u] = v16[u];
     }
     float mt = -INFINITY;
 #pragma unroll
     for (int u = 0; u < KH; ++u) {
-      const bool ok = i_row < p.C && kb + u < lim;
+      const bool ok = i_row < p.C && kb0 + u < lim;
       s[u] = ok ? s[u] * sl2 : -INFINITY;  // log2-domain logits
       mt = fmaxf(mt, s[u]);
     }
-    red[half * kM + m] = mt;
-    __syncthreads();
-    mt = fmaxf(mt, red[(half ^ 1) * kM + m]);  // the row's max (both threads agree)
-    if (pv_pending) {  // the previous P.V: O may be rescaled and P rewritten only after it
-      wait_bar(&bar[1], o_phase);
-      pv_pending = false;
-    }
-    // lazy reference max: move it (and rescale O, l) only when it grows by
-    // > 8; the TMEM accesses are warp-collective (.sync.aligned), so the
-    // warp rescales together (corr = 1 for its other rows)
+    red[(rb * 2 + half) * kM + m] = mt;
+  };
+  // (2) after the max exchange and after the previous P.V completed: lazy
+  // reference max (moved only when the max grows by > 8; the TMEM accesses
+  // are warp-collective, so a warp rescales together), the previous tile's
+  // P.V folded into O_run, P = 2^(s - m_ref) split into three bf16 parts -> smem
+  auto sm_finish = [&](int rb) {
+    const float mt = fmaxf(red[(rb * 2 + half) * kM + m], red[(rb * 2 + (half ^ 1)) * kM + m]);
     const bool need = mt > m_ref + 8.f;
     float corr = 1.f;
     if (need) {
@@ -386,9 +395,6 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
       l_run *= corr;
       m_ref = mt;
     }
-    // the previous tile's P.V enters the running O here, rescaled with it:
-    // O_run = (O_run + delta) * corr, on the CUDA cores (round-to-nearest;
-    // the tensor core only ever accumulates one tile)
     if (delta_pending) {
       fold(corr);
       delta_pending = false;
@@ -418,104 +424,132 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
       *reinterpret_cast<uint4*>(smem + kOffP + 2 * kPPart + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
     l_run += ls;
-    if (wait_v) cp_async_wait<1>();  // this tile's V (the newest group, K(t + 2), may stay in flight)
-    tmem_fence_before_sync();
-    fence_async_smem();
-    __syncthreads();
   };
 
-  // ---- cached tiles, pipelined: the tensor core runs QK(t + 1) while the
-  // CUDA cores run softmax(t); K(t + 2) is gathered as soon as QK(t) freed
-  // its buffer, V(t + 2) as soon as PV(t) did. Two S buffers in TMEM
-  // (columns 0 / 64), two mbarriers (QK / PV completions) with their phases.
+  stamp(1);
+  // ================================================ cached keys, specialised
   if (nct > 0) {
-    gather(0, 0, 0, true, true);
-    if (nct > 1) gather(1, 1, 0, true, true);
+    if (is_sm) {
+      for (int t = 0; t < nct; ++t) {
+        const int b = t & 1;
+        mbar_wait(&s_full[b], static_cast<uint32_t>(t >> 1) & 1u);  // QK(t) done
+        tmem_fence_after_sync();
+        sm_load(s_tmem + b * kKT, t * kKT, false, b);
+        tmem_fence_before_sync();
+        mbar_arrive(&s_free[b]);  // S[b] read: QK(t + 2) may overwrite it
+        named_sync(1, kSmThr);    // row maxima exchanged
+        if (t >= 1) {             // P.V(t - 1): its delta and the P buffer
+          mbar_wait(&pv_done[(t - 1) & 1], static_cast<uint32_t>((t - 1) >> 1) & 1u);
+          tmem_fence_after_sync();
+        }
+        sm_finish(b);
+        fence_async_smem();  // P -> the tensor core
+        tmem_fence_before_sync();
+        mbar_arrive(p_full);
+        delta_pending = true;  // P.V(t), once issued and completed
+        if (t == 0) stamp(8);
+      }
+      // the last P.V
+      mbar_wait(&pv_done[(nct - 1) & 1], static_cast<uint32_t>((nct - 1) >> 1) & 1u);
+      tmem_fence_after_sync();
+      stamp(2);
+    } else if (warp == 8) {
+      if (lane == 0) {
+        for (int t = 0; t <= nct; ++t) {
+          if (t < nct) {
+            const int b = t & 1;
+            mbar_wait(&kvk_full[b], static_cast<uint32_t>(t >> 1) & 1u);            // K(t) landed
+            if (t >= 2) mbar_wait(&s_free[b], static_cast<uint32_t>((t - 2) >> 1) & 1u);  // S[b] read
+            tmem_fence_after_sync();
+            issue_qk(sbase + kOffQ, sbase + kOffK + b * kKVTile, s_tmem + b * kKT, 0, true);
+            umma_commit(&s_full[b]);
+          }
+          if (t >= 1) {  // P.V(t - 1)
+            const int pb = (t - 1) & 1;
+            mbar_wait(p_full, static_cast<uint32_t>(t - 1) & 1u);                    // P(t - 1) written
+            mbar_wait(&kvv_full[pb], static_cast<uint32_t>((t - 1) >> 1) & 1u);       // V(t - 1) landed
+            tmem_fence_after_sync();
+            issue_pv(sbase + kOffP, sbase + kOffV + pb * kKVTile, o_tmem, 0, true);
+            umma_commit(&pv_done[pb]);
+          }
+        }
+      }
+      __syncwarp();
+    } else {
+      // producers: K(t) after QK(t - 2) freed buffer t % 2, V(t) after P.V(t - 2)
+      const int pt = tid - 9 * 32;
+      for (int t = 0; t < nct; ++t) {
+        const int b = t & 1;
+        if (t >= 2) mbar_wait(&s_full[b], static_cast<uint32_t>((t - 2) >> 1) & 1u);
+        gather(t, b, 0, true, false, pt, kProdThr);
+        if (t >= 2) mbar_wait(&pv_done[b], static_cast<uint32_t>((t - 2) >> 1) & 1u);
+        gather(t, b, 0, false, true, pt, kProdThr);
+        cp_async_wait<1>();  // K(t) landed
+        fence_async_smem();
+        mbar_arrive(&kvk_full[b]);
+        cp_async_wait<0>();  // V(t) landed
+        fence_async_smem();
+        mbar_arrive(&kvv_full[b]);
+      }
+    }
+  }
+  __syncthreads();
+  tmem_fence_after_sync();
+
+  // ================================================ the chunk's own rows
+  // fp32 K/V in three exact bf16 parts, one part at a time through buffer 0,
+  // causal; every thread on one serialised path (at most a few tiles)
+  uint32_t c_phase = 0;
+  auto c_mma_wait = [&]() {
+    mbar_wait(c_done, c_phase);
+    c_phase ^= 1u;
+    tmem_fence_after_sync();
+  };
+  auto publish = [&]() {
     cp_async_wait<0>();
     fence_async_smem();
     __syncthreads();
-    if (tid == 0) {
-      tmem_fence_after_sync();
-      issue_qk(sbase + kOffQ, sbase + kOffK, s_tmem, 0, true);
-      umma_commit(&bar[0]);
-    }
-  }
-  stamp(1);
-  // cp.async groups per iteration, in order: K(t + 2) (after QK(t)), V(t + 1)
-  // (after PV(t - 1)) -- empty groups keep the count when a tile is absent
-  for (int t = 0; t < nct; ++t) {
-    const int b = t & 1;
-    wait_bar(&bar[0], s_phase);  // QK(t) done: S[b] ready, K buffer b free
-    stamp(8 + 4 * t);
-    cp_async_wait<1>();  // K(t + 1) landed (the newest group, V(t), may not have)
-    fence_async_smem();
-    __syncthreads();
-    if (tid == 0 && t + 1 < nct) {
-      tmem_fence_after_sync();
-      issue_qk(sbase + kOffQ, sbase + kOffK + (b ^ 1) * kKVTile, s_tmem + (b ^ 1) * kKT, 0, true);
-      umma_commit(&bar[0]);
-    }
-    stamp(9 + 4 * t);
-    if (t + 2 < nct) gather(t + 2, b, 0, true, false);  // K only: V buffer b still feeds PV(t)
-    else cp_async_commit();
-    softmax_tile(s_tmem + b * kKT, t * kKT, false, true);  // (waits PV(t - 1), then V(t))
-    stamp(10 + 4 * t);
-    if (tid == 0) {
-      tmem_fence_after_sync();
-      issue_pv(sbase + kOffP, sbase + kOffV + b * kKVTile, o_tmem, 0, true);
-      umma_commit(&bar[1]);
-    }
-    pv_pending = true;
-    delta_pending = true;
-    stamp(11 + 4 * t);
-    // V(t + 1) into V buffer b ^ 1, freed by PV(t - 1) (V(1) came with the prologue)
-    if (t >= 1 && t + 1 < nct) gather(t + 1, b ^ 1, 0, false, true);
-    else cp_async_commit();
-  }
-  if (pv_pending) {
-    wait_bar(&bar[1], o_phase);
-    pv_pending = false;
-  }
-  stamp(2);
-  if (nct > 1) __syncthreads();
-
-  // ---- the chunk's own rows: fp32 K/V in three exact bf16 parts, one part
-  // at a time through buffer 0 (at most a few tiles), causal
+  };
   for (int t = nct; t < n_tiles; ++t) {
     for (int pk = 0; pk < 3; ++pk) {
-      gather(t, 0, pk, true, pk == 0);
+      gather(t, 0, pk, true, pk == 0, tid, kThr);
       publish();
       if (tid == 0) {
         tmem_fence_after_sync();
         issue_qk(sbase + kOffQ, sbase + kOffK, s_tmem, pk, pk == 0);
-        umma_commit(&bar[0]);
+        umma_commit(c_done);
       }
-      wait_bar(&bar[0], s_phase);
+      c_mma_wait();
       __syncthreads();
     }
-    softmax_tile(s_tmem, (t - nct) * kKT, true, false);
+    if (is_sm) sm_load(s_tmem, (t - nct) * kKT, true, 0);
+    __syncthreads();
+    if (is_sm) sm_finish(0);
+    if (is_sm) tmem_fence_before_sync();
+    fence_async_smem();
+    __syncthreads();
     for (int pv = 0; pv < 3; ++pv) {
       if (pv > 0) {
-        gather(t, 0, pv, false, true);
+        gather(t, 0, pv, false, true, tid, kThr);
         publish();
       }
       if (tid == 0) {
         tmem_fence_after_sync();
         issue_pv(sbase + kOffP, sbase + kOffV, o_tmem, pv, pv == 0);
-        umma_commit(&bar[1]);
+        umma_commit(c_done);
       }
-      wait_bar(&bar[1], o_phase);
+      c_mma_wait();
       __syncthreads();
     }
-    delta_pending = true;
+    if (is_sm) delta_pending = true;
   }
   stamp(3);
-  // ---- epilogue: O / l -> out row (i_row, head g + hm * H_kv), each thread
-  // its half of the d columns; l = the two halves' sums
-  red[half * kM + m] = l_run;
+  // ---- epilogue: O_run / l -> out row (i_row, head g + hm * H_kv), each
+  // softmax thread its half of the d columns; l = the two halves' sums
+  if (is_sm) red[half * kM + m] = l_run;
   __syncthreads();
-  if (delta_pending) fold(1.f);  // (its P.V completed: waited after the loops)
-  {
+  if (is_sm) {
+    if (delta_pending) fold(1.f);  // (its P.V completed)
     const float l = l_run + red[(half ^ 1) * kM + m];
     const float inv = l > 0.f ? 1.f / l : 0.f;
     const bool live = i_row < p.C;  // (warp-collective TMEM loads; rows past the chunk are not stored)
