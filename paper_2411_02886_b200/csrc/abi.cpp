@@ -778,7 +778,8 @@ size_t run_select(const ts_pool* pool, const ts_pool::Seq* seq, int H, int H_kv,
 cudaError_t launch_prefill(tsb::PrefillAttendParams& pa, DevBuf& split_ws, cudaStream_t st) {
   if (pa.d == 128 && pa.H / pa.H_kv <= 8 && !g_force_cuda_core_prefill) {
     // bf16 parts of the chunk's K/V, owned by the caller's pool / engine (stream-ordered reuse)
-    pa.split_ws = static_cast<uint16_t*>(split_ws.ensure(static_cast<size_t>(2) * 3 * pa.C * pa.H_kv * pa.d * 2));
+    pa.split_ws = static_cast<uint16_t*>(
+        split_ws.ensure(static_cast<size_t>(2) * (3 * pa.C + std::max(pa.n_att_max, 0)) * pa.H_kv * pa.d * 2));
     const int G = pa.H / pa.H_kv;
     // tcgen05 (prefill_tc.cu) for G in {1, 2, 4, 8}; mma.sync (prefill.cu) for the other G
     if ((G == 1 || G == 2 || G == 4 || G == 8) && !g_prefill_mma_sync) return tsb::launch_prefill_tc(pa, st);
@@ -1113,6 +1114,7 @@ ts_status ts_sparse_attend(const ts_pool* cpool, uint32_t seq, const float* q, c
       pa.att = ad;
       pa.n_att = static_cast<int>(merged.size());
       pa.n_att_ptr = nullptr;
+      pa.n_att_max = pa.n_att;
       pa.C = static_cast<int>(C);
       pa.H = static_cast<int>(num_heads);
       pa.H_kv = static_cast<int>(H_kv);
@@ -1735,35 +1737,29 @@ ts_status ts_engine_prefill(ts_engine* e, size_t seq, const float* q, const floa
       pa.page_size = static_cast<int>(pool.page_size);
       pa.att = att;
       pa.n_att_ptr = natt;
+      // init U selected U local, disjoint cached rows
+      pa.n_att_max = static_cast<int>(std::min<size_t>(cached, init_end + std::min<size_t>(kk, T) + (cached - local_begin)));
       pa.C = static_cast<int>(len);
       pa.H = H;
       pa.H_kv = Hkv;
       pa.d = d;
       pa.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
       pa.out = oc;
-      static const bool ptrace = std::getenv("TS_PREFILL_TRACE") != nullptr;  // dev: stamps of CTA (0, 0)
+      static const char* ptrace = std::getenv("TS_PREFILL_TRACE");  // dev: stamps -> this file (prefill_tc.cu)
       if (ptrace) {
-        pa.trace = static_cast<unsigned long long*>(e->p_trace.ensure(512 * 8));
-        ck(cudaMemsetAsync(pa.trace, 0, 512 * 8, st), "memset");
+        pa.trace = static_cast<unsigned long long*>(e->p_trace.ensure(4096 * 8));
+        ck(cudaMemsetAsync(pa.trace, 0, 4096 * 8, st), "memset");
       }
       ck(launch_prefill(pa, e->p_split, st), "prefill_attend");
       g_launches.fetch_add(1);
       if (ptrace) {
-        unsigned long long h[512];
-        ck(cudaMemcpyAsync(h, pa.trace, sizeof h, cudaMemcpyDeviceToHost, st), "D2H");
+        std::vector<unsigned long long> h(4096);
+        ck(cudaMemcpyAsync(h.data(), pa.trace, 4096 * 8, cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaStreamSynchronize(st), "sync");
-        std::fprintf(stderr, "[prefill trace] q+tmem %.2f us, first tile wait %.2f us, cached tiles end %.2f us, chunk end %.2f, total %.2f\n",
-                     (h[5] - h[0]) / 1e3, (h[1] - h[0]) / 1e3, (h[2] - h[0]) / 1e3, (h[3] - h[0]) / 1e3, (h[4] - h[0]) / 1e3);
-        double w = 0, pu = 0, sm = 0, pv = 0;
-        int n = 0;
-        for (int t = 1; t < 100 && h[11 + 4 * t]; ++t, ++n) {
-          w += (h[8 + 4 * t] - h[11 + 4 * (t - 1)]) / 1e3;
-          pu += (h[9 + 4 * t] - h[8 + 4 * t]) / 1e3;
-          sm += (h[10 + 4 * t] - h[9 + 4 * t]) / 1e3;
-          pv += (h[11 + 4 * t] - h[10 + 4 * t]) / 1e3;
+        if (FILE* f = std::fopen(ptrace, "wb")) {
+          std::fwrite(h.data(), 8, h.size(), f);
+          std::fclose(f);
         }
-        if (n) std::fprintf(stderr, "[prefill trace] per cached tile (%d): wait QK %.2f, publish+issue %.2f, softmax %.2f, PV %.2f us\n",
-                            n, w / n, pu / n, sm / n, pv / n);
       }
       if (!o_dev) ck(cudaMemcpyAsync(out + begin * W, oc, len * W * 4, cudaMemcpyDeviceToHost, st), "D2H");
       if (trace_counts && chunk < max_chunks) {

@@ -17,10 +17,12 @@ struct PrefillAttendParams {
   const uint32_t* att;     // attended cached rows (merged windows)
   int n_att;
   const int* n_att_ptr;    // device count (overrides n_att when set)
+  int n_att_max;           // bound on the attended count (the tensor-core paths' gathered copy)
   int C, H, H_kv, d;
   float scale;
   float* out;              // [C][H*d]
-  uint16_t* split_ws;      // tensor-core path: [2][3][C][H_kv*d] bf16 parts of the chunk K/V
+  uint16_t* split_ws;      // tensor-core paths: [2][3][C][H_kv*d] bf16 parts of the chunk K/V, then
+                           // (tcgen05) [2][n_att_max][H_kv*d] the attended cached K/V rows, gathered
   unsigned long long* trace;  // dev: %globaltimer stamps of CTA (0, 0) of the tcgen05 kernel (nullptr: off)
 };
 

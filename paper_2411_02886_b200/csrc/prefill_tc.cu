@@ -21,14 +21,20 @@
 //                 by more than 2^8), P split into three bf16 parts -> smem
 //   O += P V      tcgen05.mma M = 128, N = 128, K = 64 (4 steps),
 //                 A = P (smem, K-major SW128), B = V (smem, MN-major SW128),
-//                 D = O in TMEM (128 columns)
+//                 D = a fresh per-tile delta in TMEM (128 columns), added
+//                 into the running O (TMEM) on the CUDA cores with
+//                 round-to-nearest fp32 adds -- accumulating every tile in
+//                 the tensor core's own adder lost precision
 //
 // The tile's K/V rows arrive by 16-byte cp.async written straight into the
-// 128B-swizzled layouts the UMMA descriptors describe; the next cached tile's
-// gather is in flight while the current one is computed. Thread 0 issues
-// every MMA (tcgen05.commit -> mbarrier).
+// 128B-swizzled layouts the UMMA descriptors describe, two loads ahead of the
+// tensor core; one thread issues every MMA (tcgen05.commit -> mbarrier).
+#include <cuda.h>
+
 #include <cfloat>
 #include <cmath>
+#include <algorithm>
+#include <mutex>
 
 #include "aux.h"
 #include "common.cuh"
@@ -40,10 +46,8 @@ namespace {
 constexpr int kD = 128;
 constexpr int kM = 128;          // query rows per CTA (UMMA M)
 constexpr int kKT = 64;          // keys per tile (UMMA N of S, K of P.V)
-constexpr int kThr = 384;        // 8 softmax warps, 1 MMA warp, 3 producer warps
+constexpr int kThr = 352;        // 8 softmax warps, 1 MMA warp, a K and a V producer warp
 constexpr int kSmThr = 256;      // softmax threads (two per query row)
-constexpr int kProdThr = 96;     // producer threads (warps 9-11)
-constexpr int kRowsUpFront = 4096;
 constexpr float kLog2e = 1.4426950408889634f;
 
 // shared memory (bytes), every operand region 1024-B aligned
@@ -54,8 +58,7 @@ constexpr int kOffQ = 0;
 constexpr int kOffK = kOffQ + 3 * kQPart;        // 2 buffers of K
 constexpr int kOffV = kOffK + 2 * kKVTile;       // 2 buffers of V
 constexpr int kOffP = kOffV + 2 * kKVTile;       // 3 P parts
-constexpr int kOffRows = kOffP + 3 * kPPart;     // slab rows of the cached keys
-constexpr int kOffBar = kOffRows + kRowsUpFront * 4;
+constexpr int kOffBar = kOffP + 3 * kPPart;
 constexpr int kOffRed = kOffBar + 256;              // [2 tiles][2 halves][128] row-max / row-sum exchange
 constexpr int kSmem = kOffRed + 4 * kM * 4;
 
@@ -122,52 +125,75 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, int cols) {
 }
 
 // S (K part pk of the tile) += Q parts x K: the part pairs whose products
-// matter at fp32 resolution (q_lo x k_mid / k_lo fall below it)
-__device__ __forceinline__ void issue_qk(uint32_t q_base, uint32_t k_base, uint32_t s_tmem, int pk, bool first) {
-  const uint32_t id = idesc(kM, kKT, 0);
-  const int nq = pk == 0 ? 3 : 2;
-  bool acc = !first;
-  for (int pq = 0; pq < nq; ++pq)
+// matter at fp32 resolution (q_lo x k_mid / k_lo fall below it). dq / dk:
+// the descriptors of Q part 0 and of the K slot; a descriptor plus (byte
+// offset >> 4) is the descriptor of the offset address, so every MMA's
+// operands are one add of a constant away (the issue rate is the limit for
+// these small MMAs).
+__device__ __forceinline__ void issue_qk(uint64_t dq, uint64_t dk, uint32_t s_tmem, int pk, bool first) {
+  constexpr uint32_t id = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kKT >> 3) << 17) |
+                          (static_cast<uint32_t>(kM >> 4) << 24);
+#pragma unroll
+  for (int pq = 0; pq < 3; ++pq) {
+    if (pq == 2 && pk != 0) break;
 #pragma unroll
     for (int kk = 0; kk < kD / 16; ++kk) {
-      const uint32_t qa = q_base + pq * kQPart + (kk >> 2) * (kM * 128) + (kk & 3) * 32;
-      const uint32_t ka = k_base + (kk >> 2) * (kKT * 128) + (kk & 3) * 32;
-      umma(s_tmem, sdesc(qa, 16, 1024), sdesc(ka, 16, 1024), id, acc ? 1u : 0u);
-      acc = true;
+      const uint32_t qo = (pq * kQPart + (kk >> 2) * (kM * 128) + (kk & 3) * 32) >> 4;
+      const uint32_t ko = ((kk >> 2) * (kKT * 128) + (kk & 3) * 32) >> 4;
+      umma(s_tmem, dq + qo, dk + ko, id, (pq == 0 && kk == 0 && first) ? 0u : 1u);
     }
+  }
 }
 
 // O += P parts x V (V part pv): B = V as MN-major (d contiguous per key)
-__device__ __forceinline__ void issue_pv(uint32_t p_base, uint32_t v_base, uint32_t o_tmem, int pv, bool first) {
-  const uint32_t id = idesc(kM, kD, 1);
-  const int np = pv == 0 ? 3 : 2;
-  bool acc = !first;
-  for (int pp = 0; pp < np; ++pp)
+__device__ __forceinline__ void issue_pv(uint64_t dp, uint64_t dv, uint32_t o_tmem, int pv, bool first) {
+  constexpr uint32_t id = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (static_cast<uint32_t>(kD >> 3) << 17) |
+                          (static_cast<uint32_t>(kM >> 4) << 24);
+#pragma unroll
+  for (int pp = 0; pp < 3; ++pp) {
+    if (pp == 2 && pv != 0) break;
 #pragma unroll
     for (int kk = 0; kk < kKT / 16; ++kk) {
-      const uint32_t pa = p_base + pp * kPPart + kk * 32;
-      const uint32_t va = v_base + kk * 2048;  // 16 keys = two 8-key groups of 1024 B
-      umma(o_tmem, sdesc(pa, 16, 1024), sdesc(va, kKT * 128, 1024), id, acc ? 1u : 0u);
-      acc = true;
+      const uint32_t po = (pp * kPPart + kk * 32) >> 4;
+      const uint32_t vo = (kk * 2048) >> 4;  // 16 keys = two 8-key groups of 1024 B
+      umma(o_tmem, dp + po, dv + vo, id, (pp == 0 && kk == 0 && first) ? 0u : 1u);
     }
+  }
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(e));
+  return e != 0;
 }
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// Warp roles in the cached-key loop (the chunk's own rows follow with every
-// thread on one serialised path):
+// TMA: one 64 x 64 box at (col, row) -> 8 KB at dst
+__device__ __forceinline__ void tma_tile2d(void* dst, const CUtensorMap* tm, int col, int row, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(tm), "r"(col), "r"(row), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Warp roles (cached tiles and the chunk's own tiles alike):
 //   warps 0-7   softmax: two threads per query row (TMEM lane quarter w % 4,
 //               key / d column half w / 4)
 //   warp 8      MMA issue (lane 0): QK(t) as soon as K(t) landed and S[t % 2]
 //               was read, then P.V(t - 1) -- the tensor core runs QK(t) while
 //               the softmax warps work on tile t - 1
-//   warps 9-11  producers: cp.async gathers of K(t) / V(t) into the double
-//               buffers, each signalled by its own mbarrier
+//   warps 9-12  producers: cp.async gathers of the K loads (warps 9-10) and
+//               the V loads (11-12) into two slots each, one load per cached
+//               tile and three (the split parts) per chunk tile
 // Every hand-off is an mbarrier per buffer, so no waiter can fall two phases
-// behind: s_full[b] (QK done), pv_done[b] (P.V done), kvk_full[b] / kvv_full[b]
-// (K / V landed), s_free[b] (S read), p_full (P written).
-__global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams p, const uint16_t* kc3,
-                                                             const uint16_t* vc3) {
+// behind: s_full[b] (QK done), pv_done[b] (P.V done), kvk_full[s] / kvv_full[s]
+// (K / V load landed in slot s), k_free[s] / v_free[s] (the MMAs reading slot
+// s completed), s_free[b] (S read), p_full (P written).
+__global__ void __launch_bounds__(kThr, 1)
+    prefill_tc_kernel(PrefillAttendParams p, const __grid_constant__ CUtensorMap tm_kg, const __grid_constant__ CUtensorMap tm_vg,
+                      const __grid_constant__ CUtensorMap tm_kc, const __grid_constant__ CUtensorMap tm_vc) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int G = p.H / p.H_kv;
   const int rows_per_head = kM / G;  // chunk rows per CTA
@@ -180,7 +206,6 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   const int nct = (n_cached + kKT - 1) / kKT;
   const int n_tiles = nct + (n_cur + kKT - 1) / kKT;
   const uint32_t sbase = smem_u32(smem);
-  int32_t* rows_all = reinterpret_cast<int32_t*>(smem + kOffRows);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
   uint64_t* s_full = bars + 0;    // [2]
   uint64_t* pv_done = bars + 2;   // [2]
@@ -188,35 +213,43 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   uint64_t* kvv_full = bars + 6;  // [2]
   uint64_t* s_free = bars + 8;    // [2]
   uint64_t* p_full = bars + 10;   // [1]
-  uint64_t* c_done = bars + 11;   // [1] the serialised chunk path's MMAs
+  uint64_t* k_free = bars + 11;   // [2] the MMAs reading a K slot completed
+  uint64_t* v_free = bars + 13;   // [2] the MMAs reading a V slot completed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 128);
   float* red = reinterpret_cast<float*>(smem + kOffRed);  // [2][2][kM]
-  const bool rows_up_front = n_cached <= kRowsUpFront;
-  unsigned long long* trc = (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) ? p.trace : nullptr;
-  auto stamp = [&](int i) {
-    if (trc && i < 512) {
+  // dev trace (globaltimer stamps): CTA (0, 0) -> slots [0, 2048), the last
+  // row block -> [2048, 4096); [0, 16) phases, then per tile / load: 16 + t
+  // softmax done, 256 + t S ready, 512 + t QK issue, 768 + t P.V issue,
+  // 1024 + l K load landed, 1280 + l V load landed
+  unsigned long long* tcta = nullptr;
+  if (p.trace && blockIdx.y == 0) {
+    if (blockIdx.x == 0) tcta = p.trace;
+    else if (blockIdx.x == gridDim.x - 1) tcta = p.trace + 2048;
+  }
+  auto mark = [&](int i) {
+    if (tcta && i < 2048) {
       unsigned long long gt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-      trc[i] = gt;
+      tcta[i] = gt;
     }
   };
-  stamp(0);
-  auto lookup = [&](int key) -> int32_t {
-    const uint32_t tok = p.att[key];
-    return p.page_size == 1 ? p.page_table[tok]
-                            : p.page_table[tok / p.page_size] * p.page_size + static_cast<int32_t>(tok % p.page_size);
+  auto stamp = [&](int i) {
+    if (threadIdx.x == 0) mark(i);
   };
-
+  stamp(0);
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&pv_done[i], 1);
-      mbar_init(&kvk_full[i], kProdThr);
-      mbar_init(&kvv_full[i], kProdThr);
+      mbar_init(&kvk_full[i], 1);  // (+ the TMA transaction bytes)
+      mbar_init(&kvv_full[i], 1);
       mbar_init(&s_free[i], kSmThr);
     }
     mbar_init(p_full, kSmThr);
-    mbar_init(c_done, 1);
+    mbar_init(&k_free[0], 1);
+    mbar_init(&k_free[1], 1);
+    mbar_init(&v_free[0], 1);
+    mbar_init(&v_free[1], 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, 512);
@@ -250,24 +283,6 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
     *reinterpret_cast<uint4*>(smem + kOffQ + kQPart + off) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
     *reinterpret_cast<uint4*>(smem + kOffQ + 2 * kQPart + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
   }
-  if (rows_up_front) {
-    // all of this thread's list loads in flight, then all its page-table loads
-    constexpr int kPer = (kRowsUpFront + kThr - 1) / kThr;
-    uint32_t tok[kPer];
-#pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int key = tid + u * kThr;
-      tok[u] = key < n_cached ? __ldg(p.att + key) : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int key = tid + u * kThr;
-      if (key < n_cached)
-        rows_all[key] = p.page_size == 1 ? __ldg(p.page_table + tok[u])
-                                         : __ldg(p.page_table + tok[u] / p.page_size) * p.page_size +
-                                               static_cast<int32_t>(tok[u] % p.page_size);
-    }
-  }
   fence_async_smem();  // Q parts -> the tensor core
   tmem_fence_before_sync();
   __syncthreads();
@@ -277,44 +292,21 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   const uint32_t o_tmem = tbase + 128;     // columns [128, 256): one tile's P.V (fresh per tile)
   const uint32_t orun_tmem = tbase + 256;  // columns [256, 384): the running O, fp32 round-to-nearest adds
 
-  // gather of a tile's K and/or V rows (part `part` of the chunk's split copy
-  // for chunk tiles) into buffer b, swizzled, by threads gt of gn; padding
-  // rows zeroed; one cp.async group
-  auto gather = [&](int tile, int b, int part, bool k_on, bool v_on, int gt, int gn) {
-    uint8_t* kb = smem + kOffK + b * kKVTile;
-    uint8_t* vb = smem + kOffV + b * kKVTile;
-    for (int idx = gt; idx < kKT * 16; idx += gn) {
-      const int r = idx >> 4, c = idx & 15;
-      const uint32_t off = sw_off(kKT, r, c);
-      const uint16_t* ks = nullptr;
-      const uint16_t* vs = nullptr;
-      if (tile < nct) {
-        const int key = tile * kKT + r;
-        if (key < n_cached) {
-          const int32_t ri = rows_up_front ? rows_all[key] : lookup(key);
-          const size_t o = static_cast<size_t>(ri) * row_elems + static_cast<size_t>(g) * kD + c * 8;
-          ks = p.k_slab + o;
-          vs = p.v_slab + o;
-        }
-      } else {
-        const int j = (tile - nct) * kKT + r;
-        if (j < n_cur) {
-          const size_t o = static_cast<size_t>(part) * p.C * row_elems + static_cast<size_t>(j) * row_elems +
-                           static_cast<size_t>(g) * kD + c * 8;
-          ks = kc3 + o;
-          vs = vc3 + o;
-        }
-      }
-      if (k_on) {
-        if (ks) cp_async16(kb + off, ks);
-        else *reinterpret_cast<uint4*>(kb + off) = make_uint4(0u, 0u, 0u, 0u);
-      }
-      if (v_on) {
-        if (vs) cp_async16(vb + off, vs);
-        else *reinterpret_cast<uint4*>(vb + off) = make_uint4(0u, 0u, 0u, 0u);
-      }
+  // TMA load of part `part` of tile `tile`'s K or V rows into the 16-KB slot
+  // at `dst`: two 64 x 64 boxes (the d halves; 128B swizzle = the UMMA
+  // layout) of the gathered cached rows (tm_kg / tm_vg) or of the chunk's
+  // split copy (tm_kc / tm_vc), completing on `bar`. Rows past the attended
+  // count are zeros (prep_tc_kernel) or out of bounds (zero-filled); rows of
+  // the chunk past the causal limit are masked in the softmax.
+  auto tma_tile = [&](int tile, int part, bool is_k, uint8_t* dst, uint64_t* bar) {
+    if (lane == 0) mbar_arrive_expect_tx(bar, kKVTile);
+    __syncwarp();
+    if (lane < 2) {
+      const bool cached = tile < nct;
+      const CUtensorMap* tm = cached ? (is_k ? &tm_kg : &tm_vg) : (is_k ? &tm_kc : &tm_vc);
+      const int row = cached ? tile * kKT : part * p.C + (tile - nct) * kKT;
+      tma_tile2d(dst + lane * (kKT * 128), tm, g * kD + lane * 64, row, bar);
     }
-    cp_async_commit();
   };
 
   // ---- softmax state: thread (row m, half) of warps 0-7
@@ -327,6 +319,7 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   float m_ref = -INFINITY, l_run = 0.f;  // (l_run: this thread's half of the row)
   const float sl2 = p.scale * kLog2e;
   bool delta_pending = false;  // a completed tile P.V not yet added into O_run
+  int t_cur = 0;               // (dev trace)
   bool o_folded = false;       // O_run holds data
   constexpr int KH = kKT / 2;  // this thread's key columns
   float s[KH];
@@ -401,6 +394,7 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
     } else if (o_folded && __any_sync(0xffffffffu, need)) {
       fold_scale(corr);
     }
+    if (tid == 0 && t_cur < 64) mark(448 + t_cur);
     float ls = 0.f;
 #pragma unroll
     for (int c = 0; c < KH / 8; ++c) {
@@ -427,122 +421,111 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   };
 
   stamp(1);
-  // ================================================ cached keys, specialised
-  if (nct > 0) {
+  // ================================================ all tiles, specialised
+  // Tile t has nk(t) K loads and nk(t) V loads: one for a cached tile, the
+  // three exact bf16 parts for a tile of the chunk's own (fp32) rows. The
+  // loads stream through two K slots and two V slots in load order; a slot is
+  // refilled once the MMAs that read it completed (k_free / v_free).
+  auto nk = [&](int t) { return t < nct ? 1 : 3; };
+  auto first_load = [&](int t) { return t <= nct ? t : nct + 3 * (t - nct); };  // index of tile t's first load
+  if (n_tiles > 0) {
     if (is_sm) {
-      for (int t = 0; t < nct; ++t) {
+      for (int t = 0; t < n_tiles; ++t) {
         const int b = t & 1;
+        const bool chunk = t >= nct;
         mbar_wait(&s_full[b], static_cast<uint32_t>(t >> 1) & 1u);  // QK(t) done
         tmem_fence_after_sync();
-        sm_load(s_tmem + b * kKT, t * kKT, false, b);
+        if (tid == 0) mark(256 + t);
+        sm_load(s_tmem + b * kKT, chunk ? (t - nct) * kKT : t * kKT, chunk, b);
         tmem_fence_before_sync();
         mbar_arrive(&s_free[b]);  // S[b] read: QK(t + 2) may overwrite it
         named_sync(1, kSmThr);    // row maxima exchanged
+        if (tid == 0 && t < 64) mark(320 + t);
         if (t >= 1) {             // P.V(t - 1): its delta and the P buffer
           mbar_wait(&pv_done[(t - 1) & 1], static_cast<uint32_t>((t - 1) >> 1) & 1u);
           tmem_fence_after_sync();
         }
+        if (tid == 0 && t < 64) mark(384 + t);
+        t_cur = t;
         sm_finish(b);
         fence_async_smem();  // P -> the tensor core
         tmem_fence_before_sync();
         mbar_arrive(p_full);
         delta_pending = true;  // P.V(t), once issued and completed
-        if (t == 0) stamp(8);
+        if (t == nct - 1) stamp(2);
+        stamp(16 + t);
       }
       // the last P.V
-      mbar_wait(&pv_done[(nct - 1) & 1], static_cast<uint32_t>((nct - 1) >> 1) & 1u);
+      mbar_wait(&pv_done[(n_tiles - 1) & 1], static_cast<uint32_t>((n_tiles - 1) >> 1) & 1u);
       tmem_fence_after_sync();
-      stamp(2);
     } else if (warp == 8) {
-      if (lane == 0) {
-        for (int t = 0; t <= nct; ++t) {
-          if (t < nct) {
-            const int b = t & 1;
-            mbar_wait(&kvk_full[b], static_cast<uint32_t>(t >> 1) & 1u);            // K(t) landed
-            if (t >= 2) mbar_wait(&s_free[b], static_cast<uint32_t>((t - 2) >> 1) & 1u);  // S[b] read
+      // the whole warp runs the loop (warp-uniform operands stay in uniform
+      // registers); one elected lane issues the MMAs and commits
+      const uint64_t dq = sdesc(sbase + kOffQ, 16, 1024);
+      const uint64_t dp = sdesc(sbase + kOffP, 16, 1024);
+      const uint64_t dk0 = sdesc(sbase + kOffK, 16, 1024);
+      const uint64_t dv0 = sdesc(sbase + kOffV, kKT * 128, 1024);
+      for (int t = 0; t <= n_tiles; ++t) {
+        if (t < n_tiles) {  // QK(t): its K loads in order, accumulated into S[t % 2]
+          const int b = t & 1;
+          if (t >= 2) mbar_wait(&s_free[b], static_cast<uint32_t>((t - 2) >> 1) & 1u);  // S[b] read
+          if (lane == 0) mark(512 + t);
+          for (int pk = 0, li = first_load(t); pk < nk(t); ++pk, ++li) {
+            const int ks = li & 1;
+            mbar_wait(&kvk_full[ks], static_cast<uint32_t>(li >> 1) & 1u);  // this K load landed
             tmem_fence_after_sync();
-            issue_qk(sbase + kOffQ, sbase + kOffK + b * kKVTile, s_tmem + b * kKT, 0, true);
-            umma_commit(&s_full[b]);
+            if (lane == 0 && pk == 0 && t < 64) mark(576 + t);
+            if (elect_one()) {
+              issue_qk(dq, dk0 + ks * (kKVTile >> 4), s_tmem + b * kKT, pk, pk == 0);
+              umma_commit(&k_free[ks]);
+              if (pk == nk(t) - 1) umma_commit(&s_full[b]);
+            }
+            __syncwarp();
           }
-          if (t >= 1) {  // P.V(t - 1)
-            const int pb = (t - 1) & 1;
-            mbar_wait(p_full, static_cast<uint32_t>(t - 1) & 1u);                    // P(t - 1) written
-            mbar_wait(&kvv_full[pb], static_cast<uint32_t>((t - 1) >> 1) & 1u);       // V(t - 1) landed
+          if (lane == 0 && t < 64) mark(640 + t);
+        }
+        if (t >= 1) {  // P.V(t - 1): its V loads in order, into the fresh delta
+          const int u = t - 1;
+          mbar_wait(p_full, static_cast<uint32_t>(u) & 1u);  // P(t - 1) written
+          if (lane == 0) mark(768 + u);
+          for (int pv = 0, li = first_load(u); pv < nk(u); ++pv, ++li) {
+            const int vs = li & 1;
+            mbar_wait(&kvv_full[vs], static_cast<uint32_t>(li >> 1) & 1u);
             tmem_fence_after_sync();
-            issue_pv(sbase + kOffP, sbase + kOffV + pb * kKVTile, o_tmem, 0, true);
-            umma_commit(&pv_done[pb]);
+            if (lane == 0 && pv == 0 && u < 64) mark(832 + u);
+            if (elect_one()) {
+              issue_pv(dp, dv0 + vs * (kKVTile >> 4), o_tmem, pv, pv == 0);
+              umma_commit(&v_free[vs]);
+              if (pv == nk(u) - 1) umma_commit(&pv_done[u & 1]);
+            }
+            __syncwarp();
           }
+          if (lane == 0 && u < 64) mark(896 + u);
         }
       }
-      __syncwarp();
     } else {
-      // producers: K(t) after QK(t - 2) freed buffer t % 2, V(t) after P.V(t - 2)
-      const int pt = tid - 9 * 32;
-      for (int t = 0; t < nct; ++t) {
-        const int b = t & 1;
-        if (t >= 2) mbar_wait(&s_full[b], static_cast<uint32_t>((t - 2) >> 1) & 1u);
-        gather(t, b, 0, true, false, pt, kProdThr);
-        if (t >= 2) mbar_wait(&pv_done[b], static_cast<uint32_t>((t - 2) >> 1) & 1u);
-        gather(t, b, 0, false, true, pt, kProdThr);
-        cp_async_wait<1>();  // K(t) landed
-        fence_async_smem();
-        mbar_arrive(&kvk_full[b]);
-        cp_async_wait<0>();  // V(t) landed
-        fence_async_smem();
-        mbar_arrive(&kvv_full[b]);
+      // producers: warp 9 streams the K loads, warp 10 the V loads, each
+      // into its slot once the MMAs that read the slot's previous load
+      // completed. (The streams are independent: a tile's last K part is
+      // needed before the P.V that frees a V slot of the same tile.)
+      const bool is_k = warp == 9;
+      uint64_t* freed = is_k ? k_free : v_free;
+      uint64_t* full = is_k ? kvk_full : kvv_full;
+      uint8_t* slots = smem + (is_k ? kOffK : kOffV);
+      for (int t = 0; t < n_tiles; ++t) {
+        for (int part = 0, li = first_load(t); part < nk(t); ++part, ++li) {
+          const int sl = li & 1;
+          if (li >= 2) mbar_wait(&freed[sl], static_cast<uint32_t>((li - 2) >> 1) & 1u);
+          if (lane == 0) mark((is_k ? 1536 : 1792) + li);  // (slot free)
+          tma_tile(t, part, is_k, slots + sl * kKVTile, &full[sl]);
+          __syncwarp();
+          if (lane == 0) mark((is_k ? 1024 : 1280) + li);  // (issued)
+        }
       }
     }
   }
   __syncthreads();
   tmem_fence_after_sync();
-
-  // ================================================ the chunk's own rows
-  // fp32 K/V in three exact bf16 parts, one part at a time through buffer 0,
-  // causal; every thread on one serialised path (at most a few tiles)
-  uint32_t c_phase = 0;
-  auto c_mma_wait = [&]() {
-    mbar_wait(c_done, c_phase);
-    c_phase ^= 1u;
-    tmem_fence_after_sync();
-  };
-  auto publish = [&]() {
-    cp_async_wait<0>();
-    fence_async_smem();
-    __syncthreads();
-  };
-  for (int t = nct; t < n_tiles; ++t) {
-    for (int pk = 0; pk < 3; ++pk) {
-      gather(t, 0, pk, true, pk == 0, tid, kThr);
-      publish();
-      if (tid == 0) {
-        tmem_fence_after_sync();
-        issue_qk(sbase + kOffQ, sbase + kOffK, s_tmem, pk, pk == 0);
-        umma_commit(c_done);
-      }
-      c_mma_wait();
-      __syncthreads();
-    }
-    if (is_sm) sm_load(s_tmem, (t - nct) * kKT, true, 0);
-    __syncthreads();
-    if (is_sm) sm_finish(0);
-    if (is_sm) tmem_fence_before_sync();
-    fence_async_smem();
-    __syncthreads();
-    for (int pv = 0; pv < 3; ++pv) {
-      if (pv > 0) {
-        gather(t, 0, pv, false, true, tid, kThr);
-        publish();
-      }
-      if (tid == 0) {
-        tmem_fence_after_sync();
-        issue_pv(sbase + kOffP, sbase + kOffV, o_tmem, pv, pv == 0);
-        umma_commit(c_done);
-      }
-      c_mma_wait();
-      __syncthreads();
-    }
-    if (is_sm) delta_pending = true;
-  }
   stamp(3);
   // ---- epilogue: O_run / l -> out row (i_row, head g + hm * H_kv), each
   // softmax thread its half of the d columns; l = the two halves' sums
@@ -575,21 +558,92 @@ __global__ void __launch_bounds__(kThr, 1) prefill_tc_kernel(PrefillAttendParams
   }
 }
 
-__global__ void split3_tc_kernel(const float* __restrict__ x, int n, uint16_t* __restrict__ out) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+// Before the attention kernel, one launch: (1) the chunk's fp32 K and V split
+// exactly into three bf16 parts ([3][C][H_kv * d] each), (2) the attended
+// cached rows (init U selected U local, through the page table) gathered
+// into contiguous [n_att_max][H_kv * d] copies, a warp per row, zeros from
+// the attended count to the next 64-row tile boundary -- so every K/V tile
+// of the attention kernel is two plain TMA boxes (a row gather per tile,
+// TMA gather4 or cp.async, issues an order of magnitude slower).
+__global__ void prep_tc_kernel(PrefillAttendParams p, uint16_t* __restrict__ kc3, uint16_t* __restrict__ vc3,
+                               uint16_t* __restrict__ kg, uint16_t* __restrict__ vg) {
+  const int n = p.C * p.H_kv * kD;
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n; i += stride) {
+    const bool v = i >= n;
+    const int j = v ? i - n : i;
     float h, m, l;
-    sp3(x[i], h, m, l);
-    out[i] = static_cast<uint16_t>(__float_as_uint(h) >> 16);
-    out[n + i] = static_cast<uint16_t>(__float_as_uint(m) >> 16);
-    out[2 * static_cast<size_t>(n) + i] = static_cast<uint16_t>(__float_as_uint(l) >> 16);
+    sp3(v ? p.v_cur[j] : p.k_cur[j], h, m, l);
+    uint16_t* out = v ? vc3 : kc3;
+    out[j] = static_cast<uint16_t>(__float_as_uint(h) >> 16);
+    out[n + j] = static_cast<uint16_t>(__float_as_uint(m) >> 16);
+    out[2 * static_cast<size_t>(n) + j] = static_cast<uint16_t>(__float_as_uint(l) >> 16);
+  }
+  const int n_cached = p.n_att_ptr ? *p.n_att_ptr : p.n_att;
+  const int n_rows = min(p.n_att_max, (n_cached + kKT - 1) / kKT * kKT);
+  const int row_vec = p.H_kv * kD / 8;  // 16-byte vectors per row
+  const int lane = threadIdx.x & 31;
+  for (int key = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; key < n_rows; key += stride >> 5) {
+    uint4* kd = reinterpret_cast<uint4*>(kg + static_cast<size_t>(key) * row_vec * 8);
+    uint4* vd = reinterpret_cast<uint4*>(vg + static_cast<size_t>(key) * row_vec * 8);
+    if (key < n_cached) {
+      const uint32_t tok = p.att[key];
+      const int32_t ri = p.page_size == 1 ? p.page_table[tok]
+                                          : p.page_table[tok / p.page_size] * p.page_size + static_cast<int32_t>(tok % p.page_size);
+      const uint4* ks = reinterpret_cast<const uint4*>(p.k_slab + static_cast<size_t>(ri) * row_vec * 8);
+      const uint4* vs = reinterpret_cast<const uint4*>(p.v_slab + static_cast<size_t>(ri) * row_vec * 8);
+      for (int c = lane; c < row_vec; c += 32) {
+        kd[c] = __ldg(ks + c);
+        vd[c] = __ldg(vs + c);
+      }
+    } else {
+      for (int c = lane; c < row_vec; c += 32) kd[c] = vd[c] = make_uint4(0u, 0u, 0u, 0u);
+    }
   }
 }
 
 }  // namespace
 
+namespace {
+
+using TmapEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 2-D bf16 tensor map over [rows][width] (row pitch = width), box = 64 x 64,
+// 128B swizzle; false when the encoder is unavailable
+bool encode_2d(CUtensorMap* m, const void* base, size_t width, size_t rows) {
+  static TmapEncodeFn enc = []() {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<TmapEncodeFn>(nullptr);
+    return reinterpret_cast<TmapEncodeFn>(f);
+  }();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {width, rows};
+  const cuuint64_t strides[1] = {width * 2};
+  const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(kKT)};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// the maps of the last workspace layout seen, re-encoded when it changes
+struct MapCache {
+  std::mutex mu;
+  const void* ws = nullptr;
+  size_t rows = 0, width = 0, c = 0;
+  alignas(64) CUtensorMap tkg, tvg, tkc, tvc;
+};
+
+}  // namespace
+
 cudaError_t launch_prefill_tc(const PrefillAttendParams& p, cudaStream_t st) {
   const int G = p.H / p.H_kv;
-  if (p.d != kD || (G != 1 && G != 2 && G != 4 && G != 8) || p.page_size < 1 || !p.split_ws)
+  if (p.d != kD || (G != 1 && G != 2 && G != 4 && G != 8) || p.page_size < 1 || !p.split_ws || p.n_att_max < 0)
     return cudaErrorInvalidValue;
   static bool set = false;
   if (!set) {
@@ -597,14 +651,30 @@ cudaError_t launch_prefill_tc(const PrefillAttendParams& p, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     set = true;
   }
-  const int n = p.C * p.H_kv * kD;
+  const size_t width = static_cast<size_t>(p.H_kv) * kD;
+  const size_t n = static_cast<size_t>(p.C) * width;
   uint16_t* kc3 = p.split_ws;
-  uint16_t* vc3 = p.split_ws + 3 * static_cast<size_t>(n);
-  split3_tc_kernel<<<148, 512, 0, st>>>(p.k_cur, n, kc3);
-  split3_tc_kernel<<<148, 512, 0, st>>>(p.v_cur, n, vc3);
+  uint16_t* vc3 = kc3 + 3 * n;
+  uint16_t* kg = vc3 + 3 * n;
+  uint16_t* vg = kg + static_cast<size_t>(p.n_att_max) * width;
+  const size_t g_rows = std::max(p.n_att_max, 1);
+  static MapCache mc;
+  alignas(64) CUtensorMap tkg, tvg, tkc, tvc;
+  {
+    std::lock_guard<std::mutex> lk(mc.mu);
+    if (mc.ws != kc3 || mc.c != static_cast<size_t>(p.C) || mc.width != width || mc.rows != g_rows) {
+      mc.ws = nullptr;
+      if (!encode_2d(&mc.tkc, kc3, width, 3 * static_cast<size_t>(p.C)) || !encode_2d(&mc.tvc, vc3, width, 3 * static_cast<size_t>(p.C)) ||
+          !encode_2d(&mc.tkg, kg, width, g_rows) || !encode_2d(&mc.tvg, vg, width, g_rows))
+        return cudaErrorNotSupported;
+      mc.ws = kc3, mc.c = p.C, mc.width = width, mc.rows = g_rows;
+    }
+    tkg = mc.tkg, tvg = mc.tvg, tkc = mc.tkc, tvc = mc.tvc;
+  }
+  prep_tc_kernel<<<2 * 148, 512, 0, st>>>(p, kc3, vc3, kg, vg);
   const int rph = kM / G;
   dim3 grid((p.C + rph - 1) / rph, p.H_kv);
-  prefill_tc_kernel<<<grid, kThr, kSmem, st>>>(p, kc3, vc3);
+  prefill_tc_kernel<<<grid, kThr, kSmem, st>>>(p, tkg, tvg, tkc, tvc);
   return cudaGetLastError();
 }
 
