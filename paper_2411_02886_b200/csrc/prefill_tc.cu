@@ -51,14 +51,10 @@ constexpr int kSmThr = 256;      // softmax threads (two per query row)
 constexpr float kLog2e = 1.4426950408889634f;
 
 // shared memory (bytes), every operand region 1024-B aligned
-constexpr int kQPart = kM * kD * 2;    // 32 KB per Q part: [2 atoms][128 rows][128 B]
 constexpr int kKVTile = kKT * kD * 2;  // 16 KB: [2 atoms][64 rows][128 B]
-constexpr int kPPart = kM * kKT * 2;   // 16 KB per P part: [128 rows][128 B]
-constexpr int kOffQ = 0;
-constexpr int kOffK = kOffQ + 3 * kQPart;        // 2 buffers of K
+constexpr int kOffK = 0;                         // 2 buffers of K
 constexpr int kOffV = kOffK + 2 * kKVTile;       // 2 buffers of V
-constexpr int kOffP = kOffV + 2 * kKVTile;       // 3 P parts
-constexpr int kOffBar = kOffP + 3 * kPPart;
+constexpr int kOffBar = kOffV + 2 * kKVTile;
 constexpr int kOffRed = kOffBar + 256;              // [2 tiles][2 halves][128] row-max / row-sum exchange
 constexpr int kSmem = kOffRed + 4 * kM * 4;
 
@@ -108,6 +104,13 @@ __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, ui
       "l"(a), "l"(b), "r"(id), "r"(acc));
 }
 
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(id), "r"(acc));
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -125,12 +128,12 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, int cols) {
 }
 
 // S (K part pk of the tile) += Q parts x K: the part pairs whose products
-// matter at fp32 resolution (q_lo x k_mid / k_lo fall below it). dq / dk:
-// the descriptors of Q part 0 and of the K slot; a descriptor plus (byte
-// offset >> 4) is the descriptor of the offset address, so every MMA's
-// operands are one add of a constant away (the issue rate is the limit for
-// these small MMAs).
-__device__ __forceinline__ void issue_qk(uint64_t dq, uint64_t dk, uint32_t s_tmem, int pk, bool first) {
+// matter at fp32 resolution (q_lo x k_mid / k_lo fall below it). A = Q in
+// tensor memory (64 columns per part); dk: the descriptor of the K slot -- a
+// descriptor plus (byte offset >> 4) is the descriptor of the offset
+// address, so every MMA's operands are one add of a constant away (the
+// issue rate is the limit for these small MMAs).
+__device__ __forceinline__ void issue_qk(uint32_t q_tmem, uint64_t dk, uint32_t s_tmem, int pk, bool first) {
   constexpr uint32_t id = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kKT >> 3) << 17) |
                           (static_cast<uint32_t>(kM >> 4) << 24);
 #pragma unroll
@@ -138,15 +141,15 @@ __device__ __forceinline__ void issue_qk(uint64_t dq, uint64_t dk, uint32_t s_tm
     if (pq == 2 && pk != 0) break;
 #pragma unroll
     for (int kk = 0; kk < kD / 16; ++kk) {
-      const uint32_t qo = (pq * kQPart + (kk >> 2) * (kM * 128) + (kk & 3) * 32) >> 4;
       const uint32_t ko = ((kk >> 2) * (kKT * 128) + (kk & 3) * 32) >> 4;
-      umma(s_tmem, dq + qo, dk + ko, id, (pq == 0 && kk == 0 && first) ? 0u : 1u);
+      umma_ts(s_tmem, q_tmem + pq * (kD / 2) + kk * 8, dk + ko, id, (pq == 0 && kk == 0 && first) ? 0u : 1u);
     }
   }
 }
 
-// O += P parts x V (V part pv): B = V as MN-major (d contiguous per key)
-__device__ __forceinline__ void issue_pv(uint64_t dp, uint64_t dv, uint32_t o_tmem, int pv, bool first) {
+// delta (+)= P parts x V (V part pv): A = P in tensor memory (two bf16 per
+// 32-bit column, 32 columns per part), B = V as MN-major (d contiguous per key)
+__device__ __forceinline__ void issue_pv(uint32_t p_tmem, uint64_t dv, uint32_t o_tmem, int pv, bool first) {
   constexpr uint32_t id = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (static_cast<uint32_t>(kD >> 3) << 17) |
                           (static_cast<uint32_t>(kM >> 4) << 24);
 #pragma unroll
@@ -154,12 +157,28 @@ __device__ __forceinline__ void issue_pv(uint64_t dp, uint64_t dv, uint32_t o_tm
     if (pp == 2 && pv != 0) break;
 #pragma unroll
     for (int kk = 0; kk < kKT / 16; ++kk) {
-      const uint32_t po = (pp * kPPart + kk * 32) >> 4;
       const uint32_t vo = (kk * 2048) >> 4;  // 16 keys = two 8-key groups of 1024 B
-      umma(o_tmem, dp + po, dv + vo, id, (pp == 0 && kk == 0 && first) ? 0u : 1u);
+      umma_ts(o_tmem, p_tmem + pp * (kKT / 2) + kk * 8, dv + vo, id, (pp == 0 && kk == 0 && first) ? 0u : 1u);
     }
   }
 }
+
+// 32 consecutive TMEM columns of this thread's lane (no wait)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ bool elect_one() {
   uint32_t e;
@@ -211,7 +230,6 @@ __global__ void __launch_bounds__(kThr, 1)
   uint64_t* pv_done = bars + 2;   // [2]
   uint64_t* kvk_full = bars + 4;  // [2]
   uint64_t* kvv_full = bars + 6;  // [2]
-  uint64_t* s_free = bars + 8;    // [2]
   uint64_t* p_full = bars + 10;   // [1]
   uint64_t* k_free = bars + 11;   // [2] the MMAs reading a K slot completed
   uint64_t* v_free = bars + 13;   // [2] the MMAs reading a V slot completed
@@ -243,7 +261,6 @@ __global__ void __launch_bounds__(kThr, 1)
       mbar_init(&pv_done[i], 1);
       mbar_init(&kvk_full[i], 1);  // (+ the TMA transaction bytes)
       mbar_init(&kvv_full[i], 1);
-      mbar_init(&s_free[i], kSmThr);
     }
     mbar_init(p_full, kSmThr);
     mbar_init(&k_free[0], 1);
@@ -254,43 +271,16 @@ __global__ void __launch_bounds__(kThr, 1)
   }
   if (warp == 0) tmem_alloc(tmem_slot, 512);
   stamp(5);
-  // ---- Q parts: row m = (head m / rows_per_head, chunk row i0 + m % rows_per_head)
-  for (int idx = tid; idx < kM * (kD / 8); idx += kThr) {
-    const int m = idx >> 4, c = idx & 15;
-    const int hm = m / rows_per_head, i = i0 + (m - hm * rows_per_head);
-    float x[8];
-    if (i < p.C) {
-      const float4* src = reinterpret_cast<const float4*>(p.q + static_cast<size_t>(i) * p.H * kD +
-                                                          static_cast<size_t>(g + hm * p.H_kv) * kD + c * 8);
-      const float4 a = src[0], b = src[1];
-      x[0] = a.x, x[1] = a.y, x[2] = a.z, x[3] = a.w, x[4] = b.x, x[5] = b.y, x[6] = b.z, x[7] = b.w;
-    } else {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = 0.f;
-    }
-    uint32_t hw[4], mw[4], lw[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      float h0, m0, l0, h1, m1, l1;
-      sp3(x[2 * u], h0, m0, l0);
-      sp3(x[2 * u + 1], h1, m1, l1);
-      hw[u] = pk2(h0, h1);
-      mw[u] = pk2(m0, m1);
-      lw[u] = pk2(l0, l1);
-    }
-    const uint32_t off = sw_off(kM, m, c);
-    *reinterpret_cast<uint4*>(smem + kOffQ + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-    *reinterpret_cast<uint4*>(smem + kOffQ + kQPart + off) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
-    *reinterpret_cast<uint4*>(smem + kOffQ + 2 * kQPart + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-  }
-  fence_async_smem();  // Q parts -> the tensor core
   tmem_fence_before_sync();
   __syncthreads();
   tmem_fence_after_sync();
   const uint32_t tbase = *tmem_slot;
-  const uint32_t s_tmem = tbase;           // columns [0, 128): S[2] of 64 columns
-  const uint32_t o_tmem = tbase + 128;     // columns [128, 256): one tile's P.V (fresh per tile)
-  const uint32_t orun_tmem = tbase + 256;  // columns [256, 384): the running O, fp32 round-to-nearest adds
+  // tensor memory (512 columns x 128 lanes = query rows):
+  const uint32_t sp_tmem = tbase;       // [0, 192): S/P[2], 96 columns each -- S (fp32, 64 columns),
+                                        //   then P over it (3 bf16 parts x 32 columns)
+  const uint32_t q_tmem = tbase + 192;  // [192, 384): Q, 3 bf16 parts x 64 columns
+  const uint32_t o_tmem = tbase + 384;  // [384, 512): one tile's P.V (fresh per tile)
+  constexpr int kSP = 3 * kKT / 2;      // columns per S/P buffer
 
   // TMA load of part `part` of tile `tile`'s K or V rows into the 16-KB slot
   // at `dst`: two 64 x 64 boxes (the d halves; 128B swizzle = the UMMA
@@ -318,107 +308,109 @@ __global__ void __launch_bounds__(kThr, 1)
   const int i_row = i0 + (m - hm * rows_per_head);
   float m_ref = -INFINITY, l_run = 0.f;  // (l_run: this thread's half of the row)
   const float sl2 = p.scale * kLog2e;
-  bool delta_pending = false;  // a completed tile P.V not yet added into O_run
   int t_cur = 0;               // (dev trace)
-  bool o_folded = false;       // O_run holds data
   constexpr int KH = kKT / 2;  // this thread's key columns
   float s[KH];
-  // O_run (+)= delta, then * c: this thread's 64 of the row's 128 columns
+  // the running O: this thread's 64 of the row's 128 columns, in registers
+  // (fp32 round-to-nearest adds of every tile's P.V delta)
+  float orun[kD / 2];
+#pragma unroll
+  for (int u = 0; u < kD / 2; ++u) orun[u] = 0.f;
+  // O_run = (O_run + delta) * c
   auto fold = [&](float c) {
-    float a16[16], b16[16];
-#pragma unroll 1
-    for (int q = 0; q < kD / 32; ++q) {
-      const uint32_t col = lane_sel + half * (kD / 2) + q * 16;
-      tmem_ld16(o_tmem + col, a16);
-      if (o_folded) {
-        tmem_ld16(orun_tmem + col, b16);
+    float a[32];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) a16[u] = (b16[u] + a16[u]) * c;
-      } else {
+    for (int q = 0; q < kD / 64; ++q) {
+      tmem_ld32(o_tmem + lane_sel + half * (kD / 2) + q * 32, a);
+      tmem_wait_ld();
 #pragma unroll
-        for (int u = 0; u < 16; ++u) a16[u] *= c;
-      }
-      tmem_st16(orun_tmem + col, a16);
+      for (int u = 0; u < 32; ++u) orun[q * 32 + u] = (orun[q * 32 + u] + a[u]) * c;
     }
-    tmem_wait_st();
-    o_folded = true;
-  };
-  auto fold_scale = [&](float c) {
-    float a16[16];
-#pragma unroll 1
-    for (int q = 0; q < kD / 32; ++q) {
-      const uint32_t col = lane_sel + half * (kD / 2) + q * 16;
-      tmem_ld16(orun_tmem + col, a16);
-#pragma unroll
-      for (int u = 0; u < 16; ++u) a16[u] *= c;
-      tmem_st16(orun_tmem + col, a16);
-    }
-    tmem_wait_st();
   };
   // (1) this thread's 32 scores of the tile -> s[], own max -> red[rb][half][m]
   auto sm_load = [&](uint32_t s_addr, int k0, bool chunk, int rb) {
     const int lim = chunk ? min(n_cur - 1, i_row) + 1 : n_cached;  // visible keys: [0, lim)
     const int kb0 = k0 + half * KH;
-    float v16[16];
-#pragma unroll
-    for (int q = 0; q < KH / 16; ++q) {
-      tmem_ld16(s_addr + lane_sel + half * KH + q * 16, v16);
-#pragma unroll
-      for (int u = 0; u < 16; ++u) s[q * 16 + u] = v16[u];
-    }
-    float mt = -INFINITY;
+    static_assert(KH == 32, "one x32 load per thread");
+    tmem_ld32(s_addr + lane_sel + half * KH, s);
+    tmem_wait_ld();
+    float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    const int nv = i_row < p.C ? lim - kb0 : 0;  // visible keys among this thread's 32
 #pragma unroll
     for (int u = 0; u < KH; ++u) {
-      const bool ok = i_row < p.C && kb0 + u < lim;
-      s[u] = ok ? s[u] * sl2 : -INFINITY;  // log2-domain logits
-      mt = fmaxf(mt, s[u]);
+      s[u] = u < nv ? s[u] * sl2 : -INFINITY;  // log2-domain logits
+      mx[u & 3] = fmaxf(mx[u & 3], s[u]);
     }
-    red[(rb * 2 + half) * kM + m] = mt;
+    red[(rb * 2 + half) * kM + m] = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
   };
-  // (2) after the max exchange and after the previous P.V completed: lazy
-  // reference max (moved only when the max grows by > 8; the TMEM accesses
-  // are warp-collective, so a warp rescales together), the previous tile's
-  // P.V folded into O_run, P = 2^(s - m_ref) split into three bf16 parts -> smem
-  auto sm_finish = [&](int rb) {
+  // (2) after the max exchange: lazy reference max (moved only when the max
+  // grows by > 8), P = 2^(s - m_ref) split into three bf16 parts -> P[rb] in
+  // tensor memory; returns the factor that moves O and l to the new reference
+  auto sm_p = [&](int rb) -> float {
     const float mt = fmaxf(red[(rb * 2 + half) * kM + m], red[(rb * 2 + (half ^ 1)) * kM + m]);
-    const bool need = mt > m_ref + 8.f;
     float corr = 1.f;
-    if (need) {
+    if (mt > m_ref + 8.f) {
       corr = m_ref == -INFINITY ? 0.f : ex2_approx(m_ref - mt);
       l_run *= corr;
       m_ref = mt;
     }
-    if (delta_pending) {
-      fold(corr);
-      delta_pending = false;
-    } else if (o_folded && __any_sync(0xffffffffu, need)) {
-      fold_scale(corr);
-    }
-    if (tid == 0 && t_cur < 64) mark(448 + t_cur);
-    float ls = 0.f;
+    float ls[4] = {0.f, 0.f, 0.f, 0.f};
+    float hw[KH / 2], mw[KH / 2], lw[KH / 2];  // packed pairs (bit patterns)
+    const float mu = m_ref == -INFINITY ? 0.f : m_ref;  // (a row with no visible key yet: every p = 2^-inf = 0)
 #pragma unroll
-    for (int c = 0; c < KH / 8; ++c) {
-      uint32_t hw[4], mw[4], lw[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float p0 = s[c * 8 + 2 * u] == -INFINITY ? 0.f : ex2_approx(s[c * 8 + 2 * u] - m_ref);
-        const float p1 = s[c * 8 + 2 * u + 1] == -INFINITY ? 0.f : ex2_approx(s[c * 8 + 2 * u + 1] - m_ref);
-        ls += p0 + p1;
-        float h0, m0, l0, h1, m1, l1;
-        sp3(p0, h0, m0, l0);
-        sp3(p1, h1, m1, l1);
-        hw[u] = pk2(h0, h1);
-        mw[u] = pk2(m0, m1);
-        lw[u] = pk2(l0, l1);
-      }
-      const int cc = half * (KH / 8) + c;  // 16-byte chunk of the row's 128 B of P
-      const uint32_t off = static_cast<uint32_t>(m * 128 + ((cc ^ (m & 7)) << 4));
-      *reinterpret_cast<uint4*>(smem + kOffP + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-      *reinterpret_cast<uint4*>(smem + kOffP + kPPart + off) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
-      *reinterpret_cast<uint4*>(smem + kOffP + 2 * kPPart + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    for (int c = 0; c < KH / 2; ++c) {
+      const float p0 = ex2_approx(s[2 * c] - mu);
+      const float p1 = ex2_approx(s[2 * c + 1] - mu);
+      ls[c & 3] += p0 + p1;
+      float h0, m0, l0, h1, m1, l1;
+      sp3(p0, h0, m0, l0);
+      sp3(p1, h1, m1, l1);
+      hw[c] = __uint_as_float(pk2(h0, h1));
+      mw[c] = __uint_as_float(pk2(m0, m1));
+      lw[c] = __uint_as_float(pk2(l0, l1));
     }
-    l_run += ls;
+    l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+    const uint32_t pa = sp_tmem + rb * kSP + lane_sel + half * (KH / 2);
+    tmem_st16(pa, hw);
+    tmem_st16(pa + kKT / 2, mw);
+    tmem_st16(pa + kKT, lw);
+    return corr;
   };
+
+  // ---- Q -> tensor memory: thread (row m, half) splits its 64 d columns of
+  // the row's query (head g + hm * H_kv, chunk row i_row) into three exact
+  // bf16 parts, two per 32-bit column
+  if (is_sm) {
+    const float4* src = reinterpret_cast<const float4*>(p.q + static_cast<size_t>(i_row < p.C ? i_row : 0) * p.H * kD +
+                                                        static_cast<size_t>(g + hm * p.H_kv) * kD + half * (kD / 2));
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {  // 32 d columns -> 16 TMEM columns per part
+      float hw[16], mw[16], lw[16];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        float4 x = i_row < p.C ? src[c * 8 + u] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float h0, m0, l0, h1, m1, l1;
+        sp3(x.x, h0, m0, l0);
+        sp3(x.y, h1, m1, l1);
+        hw[2 * u] = __uint_as_float(pk2(h0, h1));
+        mw[2 * u] = __uint_as_float(pk2(m0, m1));
+        lw[2 * u] = __uint_as_float(pk2(l0, l1));
+        sp3(x.z, h0, m0, l0);
+        sp3(x.w, h1, m1, l1);
+        hw[2 * u + 1] = __uint_as_float(pk2(h0, h1));
+        mw[2 * u + 1] = __uint_as_float(pk2(m0, m1));
+        lw[2 * u + 1] = __uint_as_float(pk2(l0, l1));
+      }
+      const uint32_t qa = q_tmem + lane_sel + half * (kD / 4) + c * 16;
+      tmem_st16(qa, hw);
+      tmem_st16(qa + kD / 2, mw);
+      tmem_st16(qa + kD, lw);
+    }
+    tmem_wait_st();
+  }
+  tmem_fence_before_sync();
+  __syncthreads();
+  tmem_fence_after_sync();
 
   stamp(1);
   // ================================================ all tiles, specialised
@@ -436,39 +428,37 @@ __global__ void __launch_bounds__(kThr, 1)
         mbar_wait(&s_full[b], static_cast<uint32_t>(t >> 1) & 1u);  // QK(t) done
         tmem_fence_after_sync();
         if (tid == 0) mark(256 + t);
-        sm_load(s_tmem + b * kKT, chunk ? (t - nct) * kKT : t * kKT, chunk, b);
-        tmem_fence_before_sync();
-        mbar_arrive(&s_free[b]);  // S[b] read: QK(t + 2) may overwrite it
-        named_sync(1, kSmThr);    // row maxima exchanged
+        sm_load(sp_tmem + b * kSP, chunk ? (t - nct) * kKT : t * kKT, chunk, b);
+        named_sync(1, kSmThr);  // row maxima exchanged; every thread's S[b] loads done (P goes over them)
         if (tid == 0 && t < 64) mark(320 + t);
-        if (t >= 1) {             // P.V(t - 1): its delta and the P buffer
+        t_cur = t;
+        const float corr = sm_p(b);
+        if (tid == 0 && t < 64) mark(384 + t);
+        if (t >= 1) {  // P.V(t - 1) completed: its delta into O_run
           mbar_wait(&pv_done[(t - 1) & 1], static_cast<uint32_t>((t - 1) >> 1) & 1u);
           tmem_fence_after_sync();
+          if (tid == 0 && t < 64) mark(448 + t);
+          fold(corr);
         }
-        if (tid == 0 && t < 64) mark(384 + t);
-        t_cur = t;
-        sm_finish(b);
-        fence_async_smem();  // P -> the tensor core
+        tmem_wait_st();  // P stored
         tmem_fence_before_sync();
         mbar_arrive(p_full);
-        delta_pending = true;  // P.V(t), once issued and completed
         if (t == nct - 1) stamp(2);
         stamp(16 + t);
       }
       // the last P.V
       mbar_wait(&pv_done[(n_tiles - 1) & 1], static_cast<uint32_t>((n_tiles - 1) >> 1) & 1u);
       tmem_fence_after_sync();
+      fold(1.f);
     } else if (warp == 8) {
       // the whole warp runs the loop (warp-uniform operands stay in uniform
       // registers); one elected lane issues the MMAs and commits
-      const uint64_t dq = sdesc(sbase + kOffQ, 16, 1024);
-      const uint64_t dp = sdesc(sbase + kOffP, 16, 1024);
       const uint64_t dk0 = sdesc(sbase + kOffK, 16, 1024);
       const uint64_t dv0 = sdesc(sbase + kOffV, kKT * 128, 1024);
       for (int t = 0; t <= n_tiles; ++t) {
         if (t < n_tiles) {  // QK(t): its K loads in order, accumulated into S[t % 2]
           const int b = t & 1;
-          if (t >= 2) mbar_wait(&s_free[b], static_cast<uint32_t>((t - 2) >> 1) & 1u);  // S[b] read
+          // (S[b] = P(t - 2): its P.V was issued before this QK; the tensor core runs them in order)
           if (lane == 0) mark(512 + t);
           for (int pk = 0, li = first_load(t); pk < nk(t); ++pk, ++li) {
             const int ks = li & 1;
@@ -476,7 +466,7 @@ __global__ void __launch_bounds__(kThr, 1)
             tmem_fence_after_sync();
             if (lane == 0 && pk == 0 && t < 64) mark(576 + t);
             if (elect_one()) {
-              issue_qk(dq, dk0 + ks * (kKVTile >> 4), s_tmem + b * kKT, pk, pk == 0);
+              issue_qk(q_tmem, dk0 + ks * (kKVTile >> 4), sp_tmem + b * kSP, pk, pk == 0);
               umma_commit(&k_free[ks]);
               if (pk == nk(t) - 1) umma_commit(&s_full[b]);
             }
@@ -494,7 +484,7 @@ __global__ void __launch_bounds__(kThr, 1)
             tmem_fence_after_sync();
             if (lane == 0 && pv == 0 && u < 64) mark(832 + u);
             if (elect_one()) {
-              issue_pv(dp, dv0 + vs * (kKVTile >> 4), o_tmem, pv, pv == 0);
+              issue_pv(sp_tmem + (u & 1) * kSP, dv0 + vs * (kKVTile >> 4), o_tmem, pv, pv == 0);
               umma_commit(&v_free[vs]);
               if (pv == nk(u) - 1) umma_commit(&pv_done[u & 1]);
             }
@@ -532,22 +522,15 @@ __global__ void __launch_bounds__(kThr, 1)
   if (is_sm) red[half * kM + m] = l_run;
   __syncthreads();
   if (is_sm) {
-    if (delta_pending) fold(1.f);  // (its P.V completed)
     const float l = l_run + red[(half ^ 1) * kM + m];
     const float inv = l > 0.f ? 1.f / l : 0.f;
     const bool live = i_row < p.C;  // (warp-collective TMEM loads; rows past the chunk are not stored)
     float* orow = p.out + static_cast<size_t>(live ? i_row : 0) * p.H * kD + static_cast<size_t>(g + hm * p.H_kv) * kD +
                   half * (kD / 2);
-    float v16[16];
-#pragma unroll 1
-    for (int q = 0; q < kD / 32; ++q) {
-      tmem_ld16(orun_tmem + lane_sel + half * (kD / 2) + q * 16, v16);
-      if (live)
+    if (live)
 #pragma unroll
-        for (int u = 0; u < 16; u += 4)
-          *reinterpret_cast<float4*>(orow + q * 16 + u) =
-              make_float4(v16[u] * inv, v16[u + 1] * inv, v16[u + 2] * inv, v16[u + 3] * inv);
-    }
+      for (int u = 0; u < kD / 2; u += 4)
+        *reinterpret_cast<float4*>(orow + u) = make_float4(orun[u] * inv, orun[u + 1] * inv, orun[u + 2] * inv, orun[u + 3] * inv);
   }
   stamp(4);
   tmem_fence_before_sync();
