@@ -9,26 +9,28 @@
 // through the page table) and then the chunk's own rows, causal (:83).
 //
 //   S = Q K^T     tcgen05.mma kind::f16, M = 128, N = 64, K = 128 (8 steps),
-//                 A = Q (smem, K-major SW128), B = K (smem, K-major SW128),
+//                 A = Q (tensor memory), B = K (smem, K-major SW128),
 //                 D = S in TMEM (64 columns). Q (fp32) is split exactly into
 //                 three bf16 parts; cached K is bf16 (exact); the chunk's own
 //                 K (fp32 in the reference) is split into three parts as well
 //                 (loaded one part at a time), so every product is exact and
 //                 only the fp32 summation order differs from the reference.
-//   softmax       thread = query row = TMEM lane: tcgen05.ld of its 64 scores,
-//                 mask, online softmax in the exp2 domain with a lazily moved
-//                 reference max (O and l are rescaled only when the max grows
-//                 by more than 2^8), P split into three bf16 parts -> smem
+//   softmax       thread = query row = TMEM lane (two threads per row, one per
+//                 key half): tcgen05.ld of its 32 scores, mask, online
+//                 softmax in the exp2 domain with a lazily moved reference
+//                 max (O and l are rescaled only when the max grows by more
+//                 than 2^8), P split into three bf16 parts -> TMEM, over S
 //   O += P V      tcgen05.mma M = 128, N = 128, K = 64 (4 steps),
-//                 A = P (smem, K-major SW128), B = V (smem, MN-major SW128),
+//                 A = P (tensor memory), B = V (smem, MN-major SW128),
 //                 D = a fresh per-tile delta in TMEM (128 columns), added
-//                 into the running O (TMEM) on the CUDA cores with
+//                 into the running O (registers) on the CUDA cores with
 //                 round-to-nearest fp32 adds -- accumulating every tile in
 //                 the tensor core's own adder lost precision
 //
-// The tile's K/V rows arrive by 16-byte cp.async written straight into the
-// 128B-swizzled layouts the UMMA descriptors describe, two loads ahead of the
-// tensor core; one thread issues every MMA (tcgen05.commit -> mbarrier).
+// K/V tiles arrive by TMA (two 64 x 64 boxes per 16 KB tile, 128B swizzle =
+// the UMMA layout) from prep_tc_kernel's contiguous copies, two loads ahead of
+// the tensor core; one elected lane of the MMA warp issues every MMA
+// (tcgen05.commit -> mbarrier).
 #include <cuda.h>
 
 #include <cfloat>
@@ -199,17 +201,17 @@ __device__ __forceinline__ void tma_tile2d(void* dst, const CUtensorMap* tm, int
 
 // Warp roles (cached tiles and the chunk's own tiles alike):
 //   warps 0-7   softmax: two threads per query row (TMEM lane quarter w % 4,
-//               key / d column half w / 4)
-//   warp 8      MMA issue (lane 0): QK(t) as soon as K(t) landed and S[t % 2]
-//               was read, then P.V(t - 1) -- the tensor core runs QK(t) while
-//               the softmax warps work on tile t - 1
-//   warps 9-12  producers: cp.async gathers of the K loads (warps 9-10) and
-//               the V loads (11-12) into two slots each, one load per cached
-//               tile and three (the split parts) per chunk tile
+//               key / d column half w / 4); P(t) goes over S(t) in TMEM
+//   warp 8      MMA issue (one elected lane): QK(t) as soon as its K loads
+//               landed, then P.V(t - 1) once P(t - 1) is written -- the tensor
+//               core runs QK(t) while the softmax warps work on tile t - 1,
+//               and runs P.V(t - 2) before the QK(t) that overwrites its P
+//   warp 9/10   TMA producers of the K / V loads into two slots each: one load
+//               per cached tile, three (the split parts) per chunk tile
 // Every hand-off is an mbarrier per buffer, so no waiter can fall two phases
 // behind: s_full[b] (QK done), pv_done[b] (P.V done), kvk_full[s] / kvv_full[s]
 // (K / V load landed in slot s), k_free[s] / v_free[s] (the MMAs reading slot
-// s completed), s_free[b] (S read), p_full (P written).
+// s completed), p_full (P written and the previous delta folded).
 __global__ void __launch_bounds__(kThr, 1)
     prefill_tc_kernel(PrefillAttendParams p, const __grid_constant__ CUtensorMap tm_kg, const __grid_constant__ CUtensorMap tm_vg,
                       const __grid_constant__ CUtensorMap tm_kc, const __grid_constant__ CUtensorMap tm_vc) {
