@@ -773,16 +773,15 @@ size_t run_select(const ts_pool* pool, const ts_pool::Seq* seq, int H, int H_kv,
   return n;
 }
 
-// C-row sparse attention: the tensor-core kernel where it applies (d = 128,
+// C-row sparse attention: the tcgen05 kernel where it applies (d = 128,
 // G <= 8), the CUDA-core kernel otherwise.
 cudaError_t launch_prefill(tsb::PrefillAttendParams& pa, DevBuf& split_ws, cudaStream_t st) {
   if (pa.d == 128 && pa.H / pa.H_kv <= 8 && !g_force_cuda_core_prefill) {
     // bf16 parts of the chunk's K/V, owned by the caller's pool / engine (stream-ordered reuse)
     pa.split_ws = static_cast<uint16_t*>(
         split_ws.ensure(static_cast<size_t>(2) * (3 * pa.C + std::max(pa.n_att_max, 0)) * pa.H_kv * pa.d * 2));
-    const int G = pa.H / pa.H_kv;
-    // tcgen05 (prefill_tc.cu) for G in {1, 2, 4, 8}; mma.sync (prefill.cu) for the other G
-    if ((G == 1 || G == 2 || G == 4 || G == 8) && !g_prefill_mma_sync) return tsb::launch_prefill_tc(pa, st);
+    // tcgen05 (prefill_tc.cu); the mma.sync kernel (prefill.cu) on request (TS_PREFILL_MMA_SYNC=1)
+    if (!g_prefill_mma_sync) return tsb::launch_prefill_tc(pa, st);
     return tsb::launch_prefill_flash(pa, st);
   }
   return tsb::launch_prefill_attend(pa, st);

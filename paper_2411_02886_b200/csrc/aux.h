@@ -40,7 +40,7 @@ cudaError_t launch_windows(const uint32_t* sel, const int* n_sel_ptr, int n_sel_
 cudaError_t launch_prefill_attend(const PrefillAttendParams& p, cudaStream_t st);
 // tensor-core path (prefill.cu): d = 128, G <= 8; cudaErrorInvalidValue otherwise
 cudaError_t launch_prefill_flash(const PrefillAttendParams& p, cudaStream_t st);
-// tcgen05 path (prefill_tc.cu): d = 128, G in {1, 2, 4, 8}; cudaErrorInvalidValue otherwise
+// tcgen05 path (prefill_tc.cu): d = 128, G <= 16; cudaErrorInvalidValue otherwise
 cudaError_t launch_prefill_tc(const PrefillAttendParams& p, cudaStream_t st);
 cudaError_t launch_shard_merge(const uint32_t* all, int world, int k, uint32_t ie, uint32_t lbs, uint32_t base,
                                uint32_t n_r, uint32_t init_hi, uint32_t loc_lo, uint32_t* att, int* n_att,

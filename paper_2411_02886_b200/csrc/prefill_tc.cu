@@ -1,10 +1,11 @@
 // Chunked-prefill sparse attention on the 5th-generation tensor cores
 // (tcgen05.mma, accumulators in tensor memory): the C-row case of
 // sparse_attend (attention.cpp:114-123 -> sdpa_full :54-112) for head_dim
-// 128 and G = H / H_kv in {1, 2, 4, 8}.
+// 128 and G = H / H_kv <= 16.
 //
 // One CTA = 128 query rows = the G query heads of KV head g (h mod H_kv,
-// :78) x 128 / G chunk rows; grid = (C / (128 / G), H_kv). Keys come in
+// :78) x floor(128 / G) chunk rows (the rest padding when G does not divide
+// 128, e.g. Qwen2's 7); grid = (C / floor(128 / G), H_kv). Keys come in
 // tiles of 64: the merged cached rows (init U selected U local, gathered
 // through the page table) and then the chunk's own rows, causal (:83).
 //
@@ -306,8 +307,9 @@ __global__ void __launch_bounds__(kThr, 1)
   const int m = (warp & 3) * 32 + lane;  // TMEM lane = query row
   const int half = (warp >> 2) & 1;
   const uint32_t lane_sel = static_cast<uint32_t>((warp & 3) * 32) << 16;
-  const int hm = m / rows_per_head;
+  const int hm = m / rows_per_head;  // (G * rows_per_head <= 128: rows past it are padding)
   const int i_row = i0 + (m - hm * rows_per_head);
+  const bool row_ok = hm < G && i_row < p.C;
   float m_ref = -INFINITY, l_run = 0.f;  // (l_run: this thread's half of the row)
   const float sl2 = p.scale * kLog2e;
   int t_cur = 0;               // (dev trace)
@@ -337,7 +339,7 @@ __global__ void __launch_bounds__(kThr, 1)
     tmem_ld32(s_addr + lane_sel + half * KH, s);
     tmem_wait_ld();
     float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-    const int nv = i_row < p.C ? lim - kb0 : 0;  // visible keys among this thread's 32
+    const int nv = row_ok ? lim - kb0 : 0;  // visible keys among this thread's 32
 #pragma unroll
     for (int u = 0; u < KH; ++u) {
       s[u] = u < nv ? s[u] * sl2 : -INFINITY;  // log2-domain logits
@@ -383,14 +385,14 @@ __global__ void __launch_bounds__(kThr, 1)
   // the row's query (head g + hm * H_kv, chunk row i_row) into three exact
   // bf16 parts, two per 32-bit column
   if (is_sm) {
-    const float4* src = reinterpret_cast<const float4*>(p.q + static_cast<size_t>(i_row < p.C ? i_row : 0) * p.H * kD +
-                                                        static_cast<size_t>(g + hm * p.H_kv) * kD + half * (kD / 2));
+    const float4* src = reinterpret_cast<const float4*>(p.q + static_cast<size_t>(row_ok ? i_row : 0) * p.H * kD +
+                                                        static_cast<size_t>(g + (row_ok ? hm : 0) * p.H_kv) * kD + half * (kD / 2));
 #pragma unroll
     for (int c = 0; c < 2; ++c) {  // 32 d columns -> 16 TMEM columns per part
       float hw[16], mw[16], lw[16];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        float4 x = i_row < p.C ? src[c * 8 + u] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 x = row_ok ? src[c * 8 + u] : make_float4(0.f, 0.f, 0.f, 0.f);
         float h0, m0, l0, h1, m1, l1;
         sp3(x.x, h0, m0, l0);
         sp3(x.y, h1, m1, l1);
@@ -526,8 +528,8 @@ __global__ void __launch_bounds__(kThr, 1)
   if (is_sm) {
     const float l = l_run + red[(half ^ 1) * kM + m];
     const float inv = l > 0.f ? 1.f / l : 0.f;
-    const bool live = i_row < p.C;  // (warp-collective TMEM loads; rows past the chunk are not stored)
-    float* orow = p.out + static_cast<size_t>(live ? i_row : 0) * p.H * kD + static_cast<size_t>(g + hm * p.H_kv) * kD +
+    const bool live = row_ok;  // (rows past the chunk and padding rows are not stored)
+    float* orow = p.out + static_cast<size_t>(live ? i_row : 0) * p.H * kD + static_cast<size_t>(g + (live ? hm : 0) * p.H_kv) * kD +
                   half * (kD / 2);
     if (live)
 #pragma unroll
@@ -628,7 +630,7 @@ struct MapCache {
 
 cudaError_t launch_prefill_tc(const PrefillAttendParams& p, cudaStream_t st) {
   const int G = p.H / p.H_kv;
-  if (p.d != kD || (G != 1 && G != 2 && G != 4 && G != 8) || p.page_size < 1 || !p.split_ws || p.n_att_max < 0)
+  if (p.d != kD || p.H % p.H_kv != 0 || G < 1 || G > 16 || p.page_size < 1 || !p.split_ws || p.n_att_max < 0)
     return cudaErrorInvalidValue;
   static bool set = false;
   if (!set) {
