@@ -627,6 +627,13 @@ struct ts_engine {
   float* h_v = nullptr;
   float* h_out = nullptr;
   CacheState* h_cache = nullptr;
+  // h_out's device alias (mapped pinned memory): the synchronous host-buffer
+  // decode writes its output and cache states there directly, no D2H copy
+  // (nullptr: not mappable, or TS_NO_ZERO_COPY)
+  char* h_out_dev = nullptr;
+  // set for one engine_step: the launch mirrors the cache states into h_out_dev
+  bool mirror_cache = false;
+  bool mirror_done = false;  // the last engine_step's launches wrote the mirror
   uint32_t* h_sel = nullptr;
   Workspace ws;
   StepWorkspace sws;  // the single-sequence step kernel's
@@ -1174,6 +1181,11 @@ ts_status ts_engine_create_layers(const ts_engine_config* cfg, size_t capacity_t
     ck(cudaMallocHost(&e->h_v, n_seqs * KW * 4), "pinned");
     ck(cudaMallocHost(&e->h_out, e->out_block_bytes()), "pinned");
     e->h_cache = reinterpret_cast<CacheState*>(reinterpret_cast<char*>(e->h_out) + e->out_bytes());
+    if (!std::getenv("TS_NO_ZERO_COPY")) {
+      void* dp = nullptr;
+      if (cudaHostGetDevicePointer(&dp, e->h_out, 0) == cudaSuccess) e->h_out_dev = static_cast<char*>(dp);
+      else cudaGetLastError();
+    }
     std::vector<CacheState> init(NS);
     for (auto& c : init) {
       c = CacheState{};
@@ -1261,6 +1273,7 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
   const size_t W = e->W(), KW = e->KW();
   std::vector<int> cap_fail(e->B, 0);
   e->last_frames.assign(e->B, -1);
+  e->mirror_done = false;
   cudaStream_t st = e->stream;
   if (e->B == 1 && e->rank == 0 && e->world == 1) {
     ts_pool::Seq& s = pool.state(e->sid(0));
@@ -1311,6 +1324,7 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
       return cap_fail;
     }
   }
+  e->mirror_done = e->mirror_cache;
   for (size_t g0 = 0; g0 < e->B; g0 += tsb::kMaxSeqPerLaunch) {
     const double t0 = g_host_prof ? now_ns() : 0.0;
     const size_t gn = std::min<size_t>(tsb::kMaxSeqPerLaunch, e->B - g0);
@@ -1344,6 +1358,8 @@ std::vector<int> engine_step(ts_engine* e, const float* q, const float* k, const
       sd.sel = e->sl(b);
       sd.sel_crit = e->sc(b);
       sd.sel_rows = e->sr(b);
+      sd.cache_mirror = e->mirror_cache
+                            ? reinterpret_cast<CacheState*>(e->h_out_dev + e->out_bytes()) + e->li(b) : nullptr;
       // frame for logical position N (page_size 1): LIFO pop, after-the-step failure
       if (pool.free_list.empty()) {
         cap_fail[b] = 1;
@@ -1466,7 +1482,10 @@ ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const f
       return dbuf.as<float>();
     };
     const float *qd, *kd, *vd;
-    float* od = out_dev ? out : e->d_out.as<float>();
+    // a host output: written straight into mapped pinned memory, with the
+    // cache states mirrored next to it (no D2H copy on the critical path)
+    const bool zc = !out_dev && e->h_out_dev != nullptr;
+    float* od = out_dev ? out : zc ? reinterpret_cast<float*>(e->h_out_dev) : e->d_out.as<float>();
     if (!q_dev && !k_dev && !v_dev) {
       // host inputs: one pinned staging block, one H2D copy
       std::memcpy(e->h_q, q, B * W * 4);
@@ -1493,7 +1512,15 @@ ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const f
       vd = stage(v, v_dev, e->h_v, e->d_v, B * KW);
     }
     if (g_host_prof) tp[2] = now_ns();
-    std::vector<int> cap_fail = engine_step(e, qd, kd, vd, od);
+    e->mirror_cache = zc;
+    std::vector<int> cap_fail;
+    try {
+      cap_fail = engine_step(e, qd, kd, vd, od);
+    } catch (...) {
+      e->mirror_cache = false;
+      throw;
+    }
+    e->mirror_cache = false;
     e->last_unchecked = false;  // checked below
     if (g_host_prof) tp[3] = now_ns();
     // every result rides one stream sync: output, cache states and (when
@@ -1501,7 +1528,12 @@ ts_status ts_engine_decode(ts_engine* e, const float* q, const float* k, const f
     const size_t kk = std::max<size_t>(e->cfg.k, 1);
     // d_out and the cache states are one device block (and h_out / h_cache
     // one pinned block): a host output rides the same D2H copy
-    if (!out_dev)
+    if (zc) {
+      // (the output is host-visible; so are the cache states unless the
+      // launch was the opt-in step kernel, which does not mirror them)
+      if (!e->mirror_done)
+        ck(cudaMemcpyAsync(e->hcache(0), e->cache(0), B * sizeof(CacheState), cudaMemcpyDeviceToHost, st), "D2H");
+    } else if (!out_dev)
       ck(cudaMemcpyAsync(e->h_out, od, e->out_block_bytes(), cudaMemcpyDeviceToHost, st), "D2H");
     else
       ck(cudaMemcpyAsync(e->hcache(0), e->cache(0), B * sizeof(CacheState), cudaMemcpyDeviceToHost, st), "D2H");

@@ -2204,6 +2204,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       trace_pt(p, 31);
     }
   }
+  // the cache entry for the host (every field this launch changes was written
+  // by this thread: error, the lookup bookkeeping, n_sel)
+  if (sd.cache_mirror && cs == 0 && tid == 0) *sd.cache_mirror = *sd.cache;
   trace_pt(p, 12);
 }
 

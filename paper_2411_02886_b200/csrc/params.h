@@ -69,6 +69,10 @@ struct SeqDesc {
   const int32_t* n_att_dev;    // device count of att_list (overrides n_att)
   float* ml_out;               // out [H][2]: (M, L) of the normalised output
   int32_t no_cur;              // 1: the current token belongs to another shard
+  // synchronous host-buffer API: host-visible (mapped pinned) copy of the
+  // cache entry, written by the sequence's CTA 0 at the end of the launch
+  // (nullptr: none); `out` may then point into mapped pinned memory too
+  CacheState* cache_mirror;
 };
 
 constexpr int kMaxSeqPerLaunch = 16;
