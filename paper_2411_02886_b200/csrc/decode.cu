@@ -1647,12 +1647,14 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       const int nit = (nloc + 15) >> 4, nr = nit > ph ? (nit - ph + nph - 1) / nph : 0;
       const uint32_t tw = tmem_warp_base(tbase, warp);
       float z0 = 0.f, z1 = 0.f;
+      // eight stages per TMEM round trip (the loads' latency, not the math,
+      // is this loop's cost)
 #pragma unroll 1
-      for (int r0 = 0; r0 < nr; r0 += 4) {
-        float v[16];
-        tmem_ld16(tw + static_cast<uint32_t>(r0 * 4), v);
+      for (int r0 = 0; r0 < nr; r0 += 8) {
+        float v[32];
+        tmem_ld32(tw + static_cast<uint32_t>(r0 * 4), v);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 8; ++q) {
           const int rbase = (ph + (r0 + q) * nph) * 16 + (lane >> 2);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -1664,7 +1666,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
             else z0 += w;
           }
         }
-        tmem_st16(tw + static_cast<uint32_t>(r0 * 4), v);
+        tmem_st32(tw + static_cast<uint32_t>(r0 * 4), v);
       }
       tmem_wait_st();
 #pragma unroll
@@ -1857,27 +1859,43 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
         const int nit = (nloc + 15) >> 4, nr = nit > ph ? (nit - ph + nph - 1) / nph : 0;
         const uint32_t tw = tmem_warp_base(tbase, warp);
         float* cp = cpart + kvh * p.tpc;
+        // eight stages per TMEM round trip; the 16 (stage, row half) sums of
+        // a row quad meet by a transposing reduction over lanes ^1 and ^2
+        // (12 shuffles), after which lane b + 2c of the quad holds the sums
+        // of x[8b + 4c .. 8b + 4c + 3]
+        const int b1 = lane & 1, c1 = (lane >> 1) & 1;
 #pragma unroll 1
-        for (int r0 = 0; r0 < nr; r0 += 4) {
-          float v[16];
-          tmem_ld16(tw + static_cast<uint32_t>(r0 * 4), v);
+        for (int r0 = 0; r0 < nr; r0 += 8) {
+          float v[32];
+          tmem_ld32(tw + static_cast<uint32_t>(r0 * 4), v);
+          float x[16];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float lo = fmaf(v[q * 4 + 1], f1, v[q * 4 + 0] * f0);  // row lane/4
-            float hi = fmaf(v[q * 4 + 3], f1, v[q * 4 + 2] * f0);  // row lane/4 + 8
-            lo += __shfl_xor_sync(0xffffffffu, lo, 1);
-            hi += __shfl_xor_sync(0xffffffffu, hi, 1);
-            lo += __shfl_xor_sync(0xffffffffu, lo, 2);
-            hi += __shfl_xor_sync(0xffffffffu, hi, 2);
-            const int row = (ph + (r0 + q) * nph) * 16 + (lane >> 2);
-            if ((lane & 3) == 0 && r0 + q < nr) {
-              if (row < nloc) cp[row] = lo;
-              if (row + 8 < nloc) cp[row + 8] = hi;
-            }
+          for (int q = 0; q < 8; ++q) {
+            x[2 * q] = fmaf(v[q * 4 + 1], f1, v[q * 4 + 0] * f0);      // row lane/4
+            x[2 * q + 1] = fmaf(v[q * 4 + 3], f1, v[q * 4 + 2] * f0);  // row lane/4 + 8
+          }
+          float y[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float send = b1 ? x[i] : x[i + 8];
+            y[i] = (b1 ? x[i + 8] : x[i]) + __shfl_xor_sync(0xffffffffu, send, 1);
+          }
+          float z[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float send = c1 ? y[i] : y[i + 4];
+            z[i] = (c1 ? y[i + 4] : y[i]) + __shfl_xor_sync(0xffffffffu, send, 2);
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int idx = 8 * b1 + 4 * c1 + i, q = idx >> 1;
+            const int row = (ph + (r0 + q) * nph) * 16 + (lane >> 2) + (idx & 1) * 8;
+            if (r0 + q < nr && row < nloc) cp[row] = z[i];
           }
         }
       }
       tmem_release();  // (its barrier also publishes cpart)
+      stamp(trc, 48);
       for (int base = 0; base < nloc; base += blockDim.x) {
         const int jl = base + tid;
         float c = 0.f;
@@ -1887,6 +1905,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
         if (jl < nloc) keys[jl] = key;
         if (radix_own) hist_add(sm.hist, key, jl < nloc, 20);
       }
+      stamp(trc, 49);
     } else {
       const int n2 = (nloc + 1) >> 1;
       const bool soft = method == 2;

@@ -166,23 +166,6 @@ __device__ __forceinline__ void issue_pv(uint32_t p_tmem, uint64_t dv, uint32_t 
   }
 }
 
-// 32 consecutive TMEM columns of this thread's lane (no wait)
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr)
-      : "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
 __device__ __forceinline__ bool elect_one() {
   uint32_t e;
   asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(e));
@@ -326,7 +309,6 @@ __global__ void __launch_bounds__(kThr, 1)
 #pragma unroll
     for (int q = 0; q < kD / 64; ++q) {
       tmem_ld32(o_tmem + lane_sel + half * (kD / 2) + q * 32, a);
-      tmem_wait_ld();
 #pragma unroll
       for (int u = 0; u < 32; ++u) orun[q * 32 + u] = (orun[q * 32 + u] + a[u]) * c;
     }
@@ -337,7 +319,6 @@ __global__ void __launch_bounds__(kThr, 1)
     const int kb0 = k0 + half * KH;
     static_assert(KH == 32, "one x32 load per thread");
     tmem_ld32(s_addr + lane_sel + half * KH, s);
-    tmem_wait_ld();
     float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
     const int nv = row_ok ? lim - kb0 : 0;  // visible keys among this thread's 32
 #pragma unroll

@@ -416,7 +416,7 @@ class Engine:
                   33: "find1:loaded", 36: "find2:loaded", 38: "hist2:zeroed", 39: "hist2:counted",
                   40: "compact:iter", 41: "sel_out:prefix", 42: "merge:loaded", 43: "merge:weights",
                   26: "dec:issued", 44: "dev:att_rep",
-                  45: "p0:dec_loads", 46: "p0:frames", 47: "p0:hit_prep"}
+                  45: "p0:dec_loads", 46: "p0:frames", 47: "p0:hit_prep", 48: "crit:tmem_done", 49: "crit:keys"}
 
     def set_trace(self, enable=True):
         check(lib.ts_engine_set_trace(self._h, 1 if enable else 0))
