@@ -521,13 +521,34 @@ def run_prefill(args, local_rank):
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.Stream(dev)
     eng.set_stream(stream.cuda_stream)
-    step_us, clocks, launches = timed_steps(stream, flush, lambda i: eng.prefill(q[i], k[i], v[i]), args.steps,
-                                            args.warmup, local_rank, 1, sa.launch_count)
+    out = torch.empty(C, H * D, device=dev)
+    # device time: the stream-ordered entry (the synchronous one would put the
+    # host's launch and sync latency between the steps' events)
+    step_us, clocks, launches = timed_steps(stream, flush, lambda i: eng.prefill_async(q[i], k[i], v[i], out),
+                                            args.steps, args.warmup, local_rank, 1, sa.launch_count)
+    eng.sync()
+    # end to end: the synchronous prefill with host buffers (H2D of the chunk's
+    # q/k/v and D2H of its output inside the call)
+    n_e = max(3, min(args.steps, 10))
+    e_eng = sa.Engine(N_CTX + C * (n_e + 1) + 16, k=K_SEL, n_local=N_LOCAL, n_init=N_INIT, chunk_size=C, theta=THETA,
+                      num_heads=H, num_kv_heads=H_KV, head_dim=D, block_size=64)
+    del eng
+    fill_bf16(e_eng.append_bf16, N_CTX, H_KV * D, dev, 1234)
+    qh = [q[i % total].cpu().numpy() for i in range(n_e + 1)]
+    kh = [k[i % total].cpu().numpy() for i in range(n_e + 1)]
+    vh = [v[i % total].cpu().numpy() for i in range(n_e + 1)]
+    e_eng.prefill(qh[0], kh[0], vh[0])  # warm-up
+    e2e = []
+    for i in range(1, n_e + 1):
+        t0 = time.perf_counter()
+        e_eng.prefill(qh[i], kh[i], vh[i])
+        e2e.append(time.perf_counter() - t0)
     R = H_KV * D * 2
     T = N_CTX - N_INIT - N_LOCAL
     alg = T * (R + 4) + C * H * D * 4 + (N_INIT + K_SEL + N_LOCAL) * 2 * R + 2 * C * R + C * H * D * 4
     return {"step_us": statistics.mean(step_us), "miss_us": None, "hit_us": None, "hits": 0, "lookups": 0,
-            "alg_bytes": alg, "launches": launches, "clocks": clocks, "e2e_us": None, "h2d": 0, "d2h": 0,
+            "alg_bytes": alg, "launches": launches, "clocks": clocks, "e2e_us": 1e6 * statistics.median(e2e),
+            "h2d": C * (H * D + 2 * H_KV * D) * 4, "d2h": C * H * D * 4,
             "miss_bytes": alg, "hit_bytes": alg, "n_ctx": N_CTX, "per_gpu_bytes_div": 1,
             "flops": 2 * H * sum(N_INIT + K_SEL + N_LOCAL + i + 1 for i in range(C)) * D * 2}
 

@@ -156,6 +156,11 @@ ts_status ts_engine_append_bf16(ts_engine* eng, size_t seq, const uint16_t* k,
 ts_status ts_engine_prefill(ts_engine* eng, size_t seq, const float* q, const float* k,
                             const float* v, size_t n, float* out, uint32_t* trace_sel,
                             size_t* trace_counts, size_t max_chunks);
+/* Stream-ordered prefill (no host sync, no trace): q/k/v/out must be device
+ * buffers; errors of the queued work surface at the next ts_engine_sync.
+ * Same computation as ts_engine_prefill (attention.cpp:135-170). */
+ts_status ts_engine_prefill_async(ts_engine* eng, size_t seq, const float* q, const float* k,
+                                  const float* v, size_t n, float* out);
 /* AttentionEngine::decode / decode_step, attention.cpp:172-200, for all
  * n_seqs sequences at once: q [B x H*d], k/v [B x H_kv*d], out [B x H*d].
  * cache_hit [B] (optional), selected: if sel_out != NULL, B x k slots and

@@ -75,6 +75,7 @@ SIGNATURES = {
     "ts_engine_append": (C.c_int, [_p, _sz, _p, _p, _sz]),
     "ts_engine_append_bf16": (C.c_int, [_p, _sz, _p, _p, _sz]),
     "ts_engine_prefill": (C.c_int, [_p, _sz, _p, _p, _p, _sz, _p, _p, _p, _sz]),
+    "ts_engine_prefill_async": (C.c_int, [_p, _sz, _p, _p, _p, _sz, _p]),
     "ts_engine_decode": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _p]),
     "ts_engine_decode_async": (C.c_int, [_p, _p, _p, _p, _p]),
     "ts_engine_force_miss": (C.c_int, [_p, _sz]),

@@ -139,6 +139,8 @@ struct DevBuf {
   // and every reallocation (cudaFree) synchronises the device
   void* ensure(size_t bytes) {
     if (bytes <= n) return p;
+    static const bool dbg = std::getenv("TS_DEBUG_ALLOC") != nullptr;
+    if (dbg) std::fprintf(stderr, "[tokenselect] DevBuf %p: %zu -> %zu bytes\n", static_cast<void*>(this), n, bytes);
     if (p) cudaFree(p);
     p = nullptr;
     const size_t want = std::max<size_t>({bytes, n + n / 2, 256});
@@ -1196,6 +1198,22 @@ ts_status ts_engine_create_layers(const ts_engine_config* cfg, size_t capacity_t
     }
     ck(cudaMemcpy(e->cache(0), init.data(), NS * sizeof(CacheState), cudaMemcpyHostToDevice), "H2D");
     ck(cudaMemset(e->cached_q.p, 0, NS * W * 4), "memset");
+    // the decode workspace at the capacity's candidate count: the per-step
+    // plan tracks the growing context, and a reallocation mid-stream would
+    // synchronise the device (the GPU idles while the host frees and mallocs)
+    if (cfg->k > 0 && capacity_tokens > cfg->n_init + cfg->n_local && !std::getenv("TS_NO_RESERVE")) {
+      const int gn = static_cast<int>(std::min<size_t>(tsb::kMaxSeqPerLaunch, n_seqs));
+      const int max_T = static_cast<int>(capacity_tokens - cfg->n_init - cfg->n_local);
+      const int max_rows = static_cast<int>(cfg->n_init + std::min(cfg->k, capacity_tokens) + cfg->n_local + 1);
+      try {
+        const Plan pl = make_plan(static_cast<int>(cfg->num_heads), static_cast<int>(cfg->num_kv_heads),
+                                  static_cast<int>(cfg->head_dim), gn, max_T, max_rows);
+        e->ws.prepare(gn * pl.ctas_per_seq, static_cast<int>(cfg->num_heads), static_cast<int>(cfg->num_kv_heads),
+                      static_cast<int>(cfg->head_dim), pl.tpc, pl.s_in_smem, gn, e->stream);
+      } catch (const std::exception&) {
+        cudaGetLastError();  // (a shape the decode kernel rejects fails at its first step, as before)
+      }
+    }
     *out = e.release();
   });
 }
@@ -1673,9 +1691,11 @@ ts_status ts_engine_sync(ts_engine* e) {
   });
 }
 
-ts_status ts_engine_prefill(ts_engine* e, size_t seq, const float* q, const float* k, const float* v, size_t n,
-                            float* out, uint32_t* trace_sel, size_t* trace_counts, size_t max_chunks) {
-  return guarded([&] {
+namespace {
+
+void prefill_impl(ts_engine* e, size_t seq, const float* q, const float* k, const float* v, size_t n, float* out,
+                  uint32_t* trace_sel, size_t* trace_counts, size_t max_chunks, bool sync) {
+  {
     if (seq >= e->B) fail(TS_INVALID_ARGUMENT, "engine: sequence index out of range");
     if (n == 0) fail(TS_INVALID_ARGUMENT, "prefill: empty input");
     const ts_engine_config& c = e->cfg;
@@ -1749,7 +1769,8 @@ ts_status ts_engine_prefill(ts_engine* e, size_t seq, const float* q, const floa
       // windows (make_windows) -> device merged list
       const int init_end = static_cast<int>(std::min(c.n_init, cached));
       const int local_begin = static_cast<int>(cached - std::min(c.n_local, cached));
-      uint32_t* att = static_cast<uint32_t*>(e->p_att.ensure((cached + kk + 1) * 4));
+      // merged windows: init U selected U local (<= n_init + k + n_local rows)
+      uint32_t* att = static_cast<uint32_t*>(e->p_att.ensure((c.n_init + kk + c.n_local + 1) * 4));
       int* natt = static_cast<int*>(e->p_natt.ensure(16));
       unsigned int* bad = static_cast<unsigned int*>(e->p_bad.ensure(16));
       ck(cudaMemsetAsync(bad, 0, 4, st), "memset");
@@ -1805,7 +1826,23 @@ ts_status ts_engine_prefill(ts_engine* e, size_t seq, const float* q, const floa
       // append the chunk after attending (attention.cpp:167)
       pool.append(sid, kc, vc, len, false, nullptr, nullptr, st, false);
     }
-    ck(cudaStreamSynchronize(st), "sync");
+    if (sync) ck(cudaStreamSynchronize(st), "sync");
+  }
+}
+
+}  // namespace
+
+ts_status ts_engine_prefill(ts_engine* e, size_t seq, const float* q, const float* k, const float* v, size_t n,
+                            float* out, uint32_t* trace_sel, size_t* trace_counts, size_t max_chunks) {
+  return guarded([&] { prefill_impl(e, seq, q, k, v, n, out, trace_sel, trace_counts, max_chunks, true); });
+}
+
+ts_status ts_engine_prefill_async(ts_engine* e, size_t seq, const float* q, const float* k, const float* v, size_t n,
+                                  float* out) {
+  return guarded([&] {
+    if (!is_device_ptr(q) || !is_device_ptr(k) || !is_device_ptr(v) || !is_device_ptr(out))
+      fail(TS_INVALID_ARGUMENT, "prefill_async: q, k, v and out must be device buffers");
+    prefill_impl(e, seq, q, k, v, n, out, nullptr, nullptr, 0, false);
   });
 }
 

@@ -349,6 +349,13 @@ class Engine:
         offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
         return o, [[int(x) for x in flat[offs[i]:offs[i + 1]]] for i in range(chunks)]
 
+    def prefill_async(self, q, k, v, out, seq=0):
+        """Stream-ordered prefill on device tensors (no host sync): q [n x H*d],
+        k/v [n x H_kv*d], out [n x H*d], all float32 CUDA tensors."""
+        n = q.shape[0]
+        check(lib.ts_engine_prefill_async(self._h, seq, C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()),
+                                          C.c_void_p(v.data_ptr()), n, C.c_void_p(out.data_ptr())))
+
     def decode(self, q, k, v):
         """decode_step (attention.cpp:172-200) -> (output, cache_hit, selected).
 

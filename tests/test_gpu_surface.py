@@ -151,3 +151,30 @@ def test_engine_decode_cache_smoke(sa):
     out1, hit1, sel1 = engine.decode(q, kt, vt)
     out2, hit2, sel2 = engine.decode(q, kt, vt)
     assert not hit1 and hit2 and sel1 == sel2 and out1.shape == (1, 8) and engine.cache_hits == 1
+
+
+def test_prefill_async_matches_prefill(sa):
+    """ts_engine_prefill_async (stream-ordered, device buffers) computes what
+    the synchronous ts_engine_prefill does: same outputs, same pool state."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    H, H_kv, d, n0, n = 8, 2, 128, 3000, 700
+    kw = dict(k=256, n_local=64, n_init=16, chunk_size=256, num_heads=H, num_kv_heads=H_kv, head_dim=d, block_size=64)
+    k0 = bf16_round(rng.standard_normal((n0, H_kv * d), dtype=np.float32))
+    v0 = bf16_round(rng.standard_normal((n0, H_kv * d), dtype=np.float32))
+    q = rng.standard_normal((n, H * d), dtype=np.float32)
+    k = rng.standard_normal((n, H_kv * d), dtype=np.float32)
+    v = rng.standard_normal((n, H_kv * d), dtype=np.float32)
+    a = sa.Engine(n0 + n + 8, **kw)
+    b = sa.Engine(n0 + n + 8, **kw)
+    for e in (a, b):
+        e.append(k0, v0)
+    want = a.prefill(q, k, v)
+    out = torch.empty(n, H * d, device="cuda")
+    b.prefill_async(torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), out)
+    b.sync()
+    assert np.array_equal(out.cpu().numpy(), want)
+    assert len(a) == len(b) == n0 + n
+    with pytest.raises(ValueError):
+        b.prefill_async(torch.from_numpy(q), torch.from_numpy(k), torch.from_numpy(v), out)
