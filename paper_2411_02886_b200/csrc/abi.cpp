@@ -782,9 +782,15 @@ size_t run_select(const ts_pool* pool, const ts_pool::Seq* seq, int H, int H_kv,
   return n;
 }
 
+// the tcgen05 prefill kernel applies (d = 128, G <= 8, not overridden)
+bool prefill_uses_tc(int H, int H_kv, int d) {
+  return d == 128 && H / H_kv <= 8 && !g_force_cuda_core_prefill && !g_prefill_mma_sync;
+}
+
 // C-row sparse attention: the tcgen05 kernel where it applies (d = 128,
 // G <= 8), the CUDA-core kernel otherwise.
 cudaError_t launch_prefill(tsb::PrefillAttendParams& pa, DevBuf& split_ws, cudaStream_t st) {
+  if (!pa.att && !prefill_uses_tc(pa.H, pa.H_kv, pa.d)) return cudaErrorInvalidValue;  // (implicit windows: tcgen05 only)
   if (pa.d == 128 && pa.H / pa.H_kv <= 8 && !g_force_cuda_core_prefill) {
     // bf16 parts of the chunk's K/V, owned by the caller's pool / engine (stream-ordered reuse)
     pa.split_ws = static_cast<uint16_t*>(
@@ -1772,12 +1778,18 @@ void prefill_impl(ts_engine* e, size_t seq, const float* q, const float* k, cons
       // merged windows: init U selected U local (<= n_init + k + n_local rows)
       uint32_t* att = static_cast<uint32_t*>(e->p_att.ensure((c.n_init + kk + c.n_local + 1) * 4));
       int* natt = static_cast<int*>(e->p_natt.ensure(16));
-      unsigned int* bad = static_cast<unsigned int*>(e->p_bad.ensure(16));
-      ck(cudaMemsetAsync(bad, 0, 4, st), "memset");
-      ck(tsb::launch_windows(psel, T > 0 ? &pstate->n_sel : nullptr, 0, static_cast<int>(cached), init_end,
-                             local_begin, att, natt, bad, st),
-         "windows");
-      g_launches.fetch_add(1);
+      // the tcgen05 attention forms the windows inside its prep launch; the
+      // other kernels read the merged list windows_kernel writes
+      const bool implicit = prefill_uses_tc(static_cast<int>(c.num_heads), static_cast<int>(c.num_kv_heads),
+                                            static_cast<int>(c.head_dim));
+      if (!implicit) {
+        unsigned int* bad = static_cast<unsigned int*>(e->p_bad.ensure(16));
+        ck(cudaMemsetAsync(bad, 0, 4, st), "memset");
+        ck(tsb::launch_windows(psel, T > 0 ? &pstate->n_sel : nullptr, 0, static_cast<int>(cached), init_end,
+                               local_begin, att, natt, bad, st),
+           "windows");
+        g_launches.fetch_add(1);
+      }
       float* oc = o_dev ? out + begin * W : static_cast<float*>(e->p_out.ensure(len * W * 4));
       tsb::PrefillAttendParams pa{};
       pa.q = qc;
@@ -1787,8 +1799,16 @@ void prefill_impl(ts_engine* e, size_t seq, const float* q, const float* k, cons
       pa.v_slab = pool.v_slab;
       pa.page_table = s.d_pt;
       pa.page_size = static_cast<int>(pool.page_size);
-      pa.att = att;
+      pa.att = implicit ? nullptr : att;
       pa.n_att_ptr = natt;
+      if (implicit) {
+        pa.win_sel = T > 0 ? psel : nullptr;
+        pa.win_n_sel = T > 0 ? &pstate->n_sel : nullptr;
+        pa.win_init_end = init_end;
+        pa.win_local_begin = local_begin;
+        pa.win_cached = static_cast<int>(cached);
+        pa.win_n_att = natt;
+      }
       // init U selected U local, disjoint cached rows
       pa.n_att_max = static_cast<int>(std::min<size_t>(cached, init_end + std::min<size_t>(kk, T) + (cached - local_begin)));
       pa.C = static_cast<int>(len);

@@ -18,6 +18,15 @@ struct PrefillAttendParams {
   int n_att;
   const int* n_att_ptr;    // device count (overrides n_att when set)
   int n_att_max;           // bound on the attended count (the tensor-core paths' gathered copy)
+  // tcgen05 path, implicit windows (att == nullptr): the attended rows are
+  // [0, win_init_end) ++ the selection inside [win_init_end, win_local_begin)
+  // ++ [max(win_local_begin, win_init_end), win_cached) -- make_windows +
+  // merged() (attention.cpp:21-52) formed inside prep_tc_kernel, which also
+  // writes the count to win_n_att (then n_att_ptr)
+  const uint32_t* win_sel;   // ascending selection (nullptr: none)
+  const int* win_n_sel;      // its device count
+  int win_init_end, win_local_begin, win_cached;
+  int* win_n_att;
   int C, H, H_kv, d;
   float scale;
   float* out;              // [C][H*d]

@@ -547,7 +547,42 @@ __global__ void prep_tc_kernel(PrefillAttendParams p, uint16_t* __restrict__ kc3
     out[n + j] = static_cast<uint16_t>(__float_as_uint(m) >> 16);
     out[2 * static_cast<size_t>(n) + j] = static_cast<uint16_t>(__float_as_uint(l) >> 16);
   }
-  const int n_cached = p.n_att_ptr ? *p.n_att_ptr : p.n_att;
+  // the attended list: explicit (p.att), or the implicit windows around the
+  // selection -- its split points by counting (one pass over the selection
+  // per CTA, one L2 round trip; a binary search is a chain of them)
+  int n_cached, ie = 0, lb = 0, lo1 = 0, n1 = 0;
+  if (!p.att) {
+    const int n_sel = p.win_sel && p.win_n_sel ? *p.win_n_sel : 0;
+    ie = p.win_init_end;
+    lb = max(p.win_local_begin, ie);
+    int c_ie = 0, c_lb = 0;
+    for (int i = threadIdx.x; i < n_sel; i += blockDim.x) {
+      const uint32_t t = __ldcg(p.win_sel + i);
+      c_ie += t < static_cast<uint32_t>(ie);
+      c_lb += t < static_cast<uint32_t>(p.win_local_begin);
+    }
+    __shared__ int red[2][32];
+    for (int o = 16; o > 0; o >>= 1) {
+      c_ie += __shfl_xor_sync(0xffffffffu, c_ie, o);
+      c_lb += __shfl_xor_sync(0xffffffffu, c_lb, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      red[0][threadIdx.x >> 5] = c_ie;
+      red[1][threadIdx.x >> 5] = c_lb;
+    }
+    __syncthreads();
+    int a = 0, b = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    lo1 = a;
+    n1 = p.win_local_begin > ie ? max(0, b - a) : 0;
+    n_cached = ie + n1 + max(0, p.win_cached - lb);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *p.win_n_att = n_cached;
+  } else {
+    n_cached = p.n_att_ptr ? *p.n_att_ptr : p.n_att;
+  }
   const int n_rows = min(p.n_att_max, (n_cached + kKT - 1) / kKT * kKT);
   const int row_vec = p.H_kv * kD / 8;  // 16-byte vectors per row
   const int lane = threadIdx.x & 31;
@@ -555,7 +590,10 @@ __global__ void prep_tc_kernel(PrefillAttendParams p, uint16_t* __restrict__ kc3
     uint4* kd = reinterpret_cast<uint4*>(kg + static_cast<size_t>(key) * row_vec * 8);
     uint4* vd = reinterpret_cast<uint4*>(vg + static_cast<size_t>(key) * row_vec * 8);
     if (key < n_cached) {
-      const uint32_t tok = p.att[key];
+      const uint32_t tok = p.att ? p.att[key]
+                                 : key < ie ? static_cast<uint32_t>(key)
+                                 : key < ie + n1 ? __ldcg(p.win_sel + lo1 + key - ie)
+                                                 : static_cast<uint32_t>(lb + key - ie - n1);
       const int32_t ri = p.page_size == 1 ? p.page_table[tok]
                                           : p.page_table[tok / p.page_size] * p.page_size + static_cast<int32_t>(tok % p.page_size);
       const uint4* ks = reinterpret_cast<const uint4*>(p.k_slab + static_cast<size_t>(ri) * row_vec * 8);
