@@ -51,33 +51,55 @@ __global__ void kv_gather_kernel(const uint16_t* k_slab, const uint16_t* v_slab,
   }
 }
 
-// Sequential fp64 column sums in row order: bit-identical to chunk_mean.
-// CTA = 64 columns x 4 row groups; rows go through shared memory in tiles of
-// 128 (each thread keeps 32 loads in flight), then one thread per column adds
-// the tile's rows in order -- the load latency is paid once per tile, not once
-// per 16 rows.
-constexpr int kCmCols = 64, kCmTile = 128;
-__global__ void __launch_bounds__(256) chunk_mean_kernel(const float* q, int c, int width, float* out) {
-  __shared__ float tile[kCmTile][kCmCols + 1];
-  const int col = threadIdx.x & (kCmCols - 1), grp = threadIdx.x / kCmCols;  // 4 row groups
+// Sequential fp64 column sums in row order: bit-identical to chunk_mean
+// (tensor.cpp:133-150). CTA = 32 columns; rows pass through shared memory in
+// tiles of 128, double-buffered: every thread issues its 16 loads of tile
+// t + 1 before warp 0 adds tile t's rows in order (one dependent fp64 add per
+// row and column -- the chain the reference's order imposes), so the loads'
+// latency hides behind the chain instead of adding to it.
+constexpr int kCmCols = 32, kCmTile = 128, kCmThr = 256;
+__global__ void __launch_bounds__(kCmThr) chunk_mean_kernel(const float* q, int c, int width, float* out) {
+  __shared__ float tile[2][kCmTile][kCmCols];
+  constexpr int kPer = kCmTile * kCmCols / kCmThr;  // loads per thread per tile (16)
+  const int col = threadIdx.x & (kCmCols - 1), rb = threadIdx.x / kCmCols;
   const int j = blockIdx.x * kCmCols + col;
-  double acc = 0.0;  // row order, as tensor.cpp:133-150
-  for (int r0 = 0; r0 < c; r0 += kCmTile) {
-    const int nr = min(kCmTile, c - r0);
-    float v[kCmTile / 4];
+  const int ntile = (c + kCmTile - 1) / kCmTile;
+  float v[kPer];
+  auto load = [&](int t) {
+    const int r0 = t * kCmTile, nr = min(kCmTile, c - r0);
 #pragma unroll
-    for (int u = 0; u < kCmTile / 4; ++u) {
-      const int r = grp * (kCmTile / 4) + u;
+    for (int u = 0; u < kPer; ++u) {
+      const int r = rb + u * (kCmThr / kCmCols);
       v[u] = (r < nr && j < width) ? __ldg(q + static_cast<size_t>(r0 + r) * width + j) : 0.f;
     }
+  };
+  auto store = [&](int b) {
 #pragma unroll
-    for (int u = 0; u < kCmTile / 4; ++u) tile[grp * (kCmTile / 4) + u][col] = v[u];
-    __syncthreads();
-    if (grp == 0)
-      for (int r = 0; r < nr; ++r) acc += static_cast<double>(tile[r][col]);
+    for (int u = 0; u < kPer; ++u) tile[b][rb + u * (kCmThr / kCmCols)][col] = v[u];
+  };
+  double acc = 0.0;
+  load(0);
+  store(0);
+  __syncthreads();
+  for (int t = 0; t < ntile; ++t) {
+    if (t + 1 < ntile) load(t + 1);  // in flight during the adds below
+    if (threadIdx.x < kCmCols) {
+      const int nr = min(kCmTile, c - t * kCmTile);
+      const float* tc = &tile[t & 1][0][col];
+      int r = 0;
+      for (; r + 8 <= nr; r += 8) {  // (the loads and conversions of 8 rows ahead of the add chain)
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = static_cast<double>(tc[(r + u) * kCmCols]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += x[u];
+      }
+      for (; r < nr; ++r) acc += static_cast<double>(tc[r * kCmCols]);
+    }
+    if (t + 1 < ntile) store((t + 1) & 1);
     __syncthreads();
   }
-  if (grp == 0 && j < width) out[j] = static_cast<float>(acc * (1.0 / static_cast<double>(c)));
+  if (threadIdx.x < kCmCols && j < width) out[j] = static_cast<float>(acc * (1.0 / static_cast<double>(c)));
 }
 
 __global__ void max_index_kernel(const uint32_t* idx, int n, unsigned int* out) {
@@ -417,7 +439,7 @@ cudaError_t launch_kv_gather(const uint16_t* k_slab, const uint16_t* v_slab, con
 }
 
 cudaError_t launch_chunk_mean(const float* q, int c, int width, float* out, cudaStream_t st) {
-  chunk_mean_kernel<<<(width + kCmCols - 1) / kCmCols, 256, 0, st>>>(q, c, width, out);
+  chunk_mean_kernel<<<(width + kCmCols - 1) / kCmCols, kCmThr, 0, st>>>(q, c, width, out);
   return cudaGetLastError();
 }
 
