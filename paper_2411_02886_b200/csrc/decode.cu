@@ -305,6 +305,7 @@ __device__ int cache_decision(const SeqDesc& sd, int width, const DecisionLoads&
 
 // --------------------------------------------------------------- the scan
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
 constexpr int kScratchTmem = 250;  // sm.scratch word holding the TMEM base address
 constexpr int kScratchStageMode = 200;  // sm.scratch words [200, 216): the scan ring's per-slot layout
 constexpr size_t kCritPartOffset = 64 * 1024;  // TMEM mode: per-kv-head criticality partials in the ring
@@ -360,9 +361,15 @@ __device__ __forceinline__ uint32_t tmem_warp_base(uint32_t tbase, int warp) {
   return tbase + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>(((warp - 1) >> 2) * kTmemColsPerWarp);
 }
 
+// zw (S spilled to global memory, soft vote): each consumer lane also keeps
+// the softmax partial (m, z) of its two heads online -- log2-domain reference
+// moved lazily (by > 8), z = sum 2^(S log2e - m) -- and the warps leave them
+// in zw[phase][H] (the idle radix histogram), so phase 2 does not stream the
+// spilled S through HBM twice (a read and an e^(S - m) write back).
 template <int D, int G, bool TM>
 __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& sm, int j0,
-                          int nloc, float* Sbuf, int sstride, float* s_out_row0, int pre, uint32_t tbase) {
+                          int nloc, float* Sbuf, int sstride, float* s_out_row0, int pre, uint32_t tbase,
+                          float2* zw = nullptr) {
   constexpr int KC = D / 16;  // k-chunks of 16 along d
   const int Hkv = p.H_kv;
   const int row_bytes = Hkv * D * 2;
@@ -471,6 +478,17 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
   // running max of this lane's two heads (the consumers stay lean: they
   // gate the ring's refill, so the scan's speed is theirs)
   float runmax0 = -INFINITY, runmax1 = -INFINITY;
+  float zm0 = -INFINITY, zm1 = -INFINITY, zz0 = 0.f, zz1 = 0.f;  // online (m, z), log2 domain (zw)
+  auto zadd = [](float& zm, float& zz, float a, float b) {  // a, b: logits (-inf: none)
+    const float x = a * kLog2e, y = b * kLog2e, mx = fmaxf(x, y);
+    if (mx > -INFINITY) {
+      if (mx > zm + 8.f) {
+        zz = zm > -INFINITY ? zz * ex2_approx(zm - mx) : 0.f;
+        zm = mx;
+      }
+      zz += ex2_approx(x - zm) + ex2_approx(y - zm);
+    }
+  };
   // ldmatrix row address: matrix lane/8 -> rows +8 for odd, cols +8 for >= 16
   const uint32_t lrow = static_cast<uint32_t>((lane & 7) + ((lane >> 3) & 1) * 8);
   const uint32_t lcol = static_cast<uint32_t>((lane >> 4) * 16 + kvh * D * 2);
@@ -522,6 +540,30 @@ __device__ void scan_fast(const DecodeParams& p, const SeqDesc& sd, const Smem& 
     runmax0 = fmaxf(runmax0, fmaxf(v[0], v[2]));
     runmax1 = fmaxf(runmax1, fmaxf(v[1], v[3]));
     if constexpr (TM) tmem_st4(tmem_warp_base(tbase, warp) + static_cast<uint32_t>(r * 4), c[0], c[1], c[2], c[3]);
+    else if (zw) {
+      zadd(zm0, zz0, v[0], v[2]);
+      zadd(zm1, zz1, v[1], v[3]);
+    }
+  }
+  if (!TM && zw) {
+    // this warp's (m, z) per head: the eight lanes of a head pair, merged
+    auto zmerge = [](float& zm, float& zz, int o) {
+      const float om = __shfl_xor_sync(0xffffffffu, zm, o), oz = __shfl_xor_sync(0xffffffffu, zz, o);
+      const float mx = fmaxf(zm, om);
+      if (mx > -INFINITY) {
+        zz = (zm > -INFINITY ? zz * ex2_approx(zm - mx) : 0.f) + (om > -INFINITY ? oz * ex2_approx(om - mx) : 0.f);
+        zm = mx;
+      }
+    };
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      zmerge(zm0, zz0, o);
+      zmerge(zm1, zz1, o);
+    }
+    if (lane < 4) {
+      if (g0 < G) zw[phase * p.H + g0 * Hkv + kvh] = make_float2(zm0, zz0);
+      if (g0 + 1 < G) zw[phase * p.H + (g0 + 1) * Hkv + kvh] = make_float2(zm1, zz1);
+    }
   }
   if constexpr (TM) tmem_wait_st();
   runmax0 = fmaxf(runmax0, __shfl_xor_sync(0xffffffffu, runmax0, 4));
@@ -1338,15 +1380,16 @@ __device__ __noinline__ void softmax_partials(float* Sbuf, int sstride, int nloc
     float4* sr = reinterpret_cast<float4*>(Sbuf + static_cast<size_t>(h) * sstride);
     float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
     if (m > -INFINITY) {
-      // S <- e^(S - m) in place (the soft vote then needs FMAs only); four
-      // float4 per lane in flight (S may be spilled to global memory)
-      for (int q0 = lane; q0 < n4; q0 += 4 * 32) {
-        float4 v[4];
+      // S <- e^(S - m) in place (the soft vote then needs FMAs only); eight
+      // float4 per lane in flight (S may be spilled to global memory: each
+      // round of loads is an L2 / HBM round trip)
+      for (int q0 = lane; q0 < n4; q0 += 8 * 32) {
+        float4 v[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < 8; ++u)
           if (q0 + u * 32 < n4) v[u] = sr[q0 + u * 32];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < 8; ++u)
           if (q0 + u * 32 < n4) {
             v[u].x = ex2_approx(fmaf(v[u].x, kLog2e, -ml));
             v[u].y = ex2_approx(fmaf(v[u].y, kLog2e, -ml));
@@ -1603,6 +1646,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   uint32_t* keys = s_in_smem != kSGlobal ? sm.keys : p.ws_keys + static_cast<size_t>(cta) * p.tpc;
   const int sstride = p.tpc;
   const bool scanning = (own == 1) && ((pmode & (kModeScore | kModeSIn)) != 0);
+  // S spilled to global memory with the soft vote: the scan forms the
+  // softmax partials online and the criticality pass reads S once (raw)
+  const bool online_z = FAST && !LEAN && s_in_smem == kSGlobal && method == 2 && do_select &&
+                        !(pmode & (kModeShardStats | kModeShardSelect | kModeSIn));
   if (scanning) {
     if (pmode & kModeSIn) {
       for (int idx = tid; idx < H * nloc; idx += blockDim.x) {
@@ -1613,7 +1660,14 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       }
     } else {
       float* so = (pmode & kModeSOut) ? sd.s_out + j0 : nullptr;
-      if constexpr (FAST) scan_fast<D, G, LEAN>(p, sd, sm, j0, nloc, Sbuf, sstride, so, pre, tbase);
+      if (online_z) {  // partials of phases that get no stage stay empty
+        float2* zw = reinterpret_cast<float2*>(sm.hist);
+        for (int i = tid; i < (kDecodeConsumers / p.H_kv) * H; i += blockDim.x) zw[i] = make_float2(-INFINITY, 0.f);
+        __syncthreads();
+      }
+      if constexpr (FAST)
+        scan_fast<D, G, LEAN>(p, sd, sm, j0, nloc, Sbuf, sstride, so, pre, tbase,
+                              online_z ? reinterpret_cast<float2*>(sm.hist) : nullptr);
       else scan_generic(p, sd, sm, j0, nloc, Sbuf, sstride, so);
     }
   }
@@ -1691,7 +1745,27 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   } else if (do_select && own == 1 && method == 2 && !shard_sel) {
     const size_t sh = stats_stride(p.ctas_per_seq);
     const size_t so = static_cast<size_t>(seq_id) * H * sh + cs;
-    softmax_partials(Sbuf, sstride, nloc, H, sm.headmax, p.ws_m + so, p.ws_z + so, sh);
+    if (online_z) {
+      // the consumer warps' (m, z) per head, merged in phase order
+      __syncthreads();
+      const float2* zw = reinterpret_cast<const float2*>(sm.hist);
+      const int nph = kDecodeConsumers / p.H_kv;
+      for (int h = tid; h < H; h += blockDim.x) {
+        float zm = -INFINITY, zz = 0.f;
+        for (int q = 0; q < nph; ++q) {
+          const float2 w = zw[q * H + h];
+          const float mx = fmaxf(zm, w.x);
+          if (mx > -INFINITY) {
+            zz = (zm > -INFINITY ? zz * ex2_approx(zm - mx) : 0.f) + (w.x > -INFINITY ? w.y * ex2_approx(w.x - mx) : 0.f);
+            zm = mx;
+          }
+        }
+        p.ws_m[so + h * sh] = zm * kLn2;  // natural-log domain, like the other paths
+        p.ws_z[so + h * sh] = zz;
+      }
+    } else {
+      softmax_partials(Sbuf, sstride, nloc, H, sm.headmax, p.ws_m + so, p.ws_z + so, sh);
+    }
   }
   TSB_STOP_AT(3);
   trace_pt(p, 3);
@@ -1827,8 +1901,15 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);
         if (hv && sub == 0) {
-          const float mc = ord_float(sm.headmax[h]);
-          ml[h] = mc > -INFINITY ? fast_exp(mc - M) / Z : 0.f;  // f_h: local e^(S - m_c) -> softmax
+          if (online_z) {
+            // raw S: softmax_h(S) = 2^(S log2e - M_h log2e) / Z_h (the shift
+            // kept in the head-max slot, which nothing reads past this point)
+            ml[h] = Z > 0.f ? 1.f / Z : 0.f;
+            reinterpret_cast<float*>(sm.headmax)[h] = M > -INFINITY ? M * kLog2e : 0.f;
+          } else {
+            const float mc = ord_float(sm.headmax[h]);
+            ml[h] = mc > -INFINITY ? fast_exp(mc - M) / Z : 0.f;  // f_h: local e^(S - m_c) -> softmax
+          }
         }
       }
       __syncthreads();
@@ -1906,6 +1987,47 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
         if (radix_own) hist_add(sm.hist, key, jl < nloc, 20);
       }
       stamp(trc, 49);
+    } else if (online_z) {
+      // raw S (spilled): crit_j = sum_h 2^(S_hj log2e - M_h log2e) / Z_h, even
+      // heads then odd into separate sums, each in head order
+      const float* shift = reinterpret_cast<const float*>(sm.headmax);
+      const int n2 = (nloc + 1) >> 1;
+      const int hp = H & ~1;
+      for (int base = 0; base < n2; base += blockDim.x) {
+        const int q = base + tid;
+        float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+        if (q < n2) {
+          const float* s2 = Sbuf + 2 * q;
+          int h = 0;
+          for (; h < hp; h += 16) {
+            float2 a[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+              if (h + u < hp) a[u] = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h + u) * sstride);
+#pragma unroll
+            for (int u = 0; u < 16; u += 2)
+              if (h + u < hp) {
+                const float sa = shift[h + u], sb = shift[h + u + 1], fa = ml[h + u], fb = ml[h + u + 1];
+                c0 = fmaf(ex2_approx(fmaf(a[u].x, kLog2e, -sa)), fa, c0);
+                c1 = fmaf(ex2_approx(fmaf(a[u].y, kLog2e, -sa)), fa, c1);
+                c2 = fmaf(ex2_approx(fmaf(a[u + 1].x, kLog2e, -sb)), fb, c2);
+                c3 = fmaf(ex2_approx(fmaf(a[u + 1].y, kLog2e, -sb)), fb, c3);
+              }
+          }
+          h = hp;
+          if (h < H) {
+            const float2 a = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h) * sstride);
+            c0 = fmaf(ex2_approx(fmaf(a.x, kLog2e, -shift[h])), ml[h], c0);
+            c1 = fmaf(ex2_approx(fmaf(a.y, kLog2e, -shift[h])), ml[h], c1);
+          }
+        }
+        const uint32_t k0 = float_key(c0 + c2), k1 = float_key(c1 + c3);
+        if (q < n2) *reinterpret_cast<uint2*>(keys + 2 * q) = make_uint2(k0, k1);
+        if (radix_own) {
+          hist_add(sm.hist, k0, q < n2 && 2 * q < nloc, 20);
+          hist_add(sm.hist, k1, q < n2 && 2 * q + 1 < nloc, 20);
+        }
+      }
     } else {
       const int n2 = (nloc + 1) >> 1;
       const bool soft = method == 2;
@@ -1915,28 +2037,26 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
         if (q < n2) {
           const float* s2 = Sbuf + 2 * q;
           int h = 0;
-          for (; h + 7 < H; h += 8) {  // eight loads in flight (S may be spilled to global memory)
-            float2 a[8];
+          // sixteen heads' loads in flight (S may be spilled to global
+          // memory: each round is an L2 / HBM round trip); even heads into
+          // c0 / c1, odd heads into c2 / c3, each in head order
+          const int hp = H & ~1;  // the heads taken in pairs
+          for (; h < hp; h += 16) {
+            float2 a[16];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) a[u] = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h + u) * sstride);
+            for (int u = 0; u < 16; ++u)
+              if (h + u < hp) a[u] = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h + u) * sstride);
 #pragma unroll
-            for (int u = 0; u < 8; u += 2) {
-              const float fa = soft ? ml[h + u] : 1.f, fb = soft ? ml[h + u + 1] : 1.f;
-              c0 = fmaf(a[u].x, fa, c0);
-              c1 = fmaf(a[u].y, fa, c1);
-              c2 = fmaf(a[u + 1].x, fb, c2);
-              c3 = fmaf(a[u + 1].y, fb, c3);
-            }
+            for (int u = 0; u < 16; u += 2)
+              if (h + u < hp) {
+                const float fa = soft ? ml[h + u] : 1.f, fb = soft ? ml[h + u + 1] : 1.f;
+                c0 = fmaf(a[u].x, fa, c0);
+                c1 = fmaf(a[u].y, fa, c1);
+                c2 = fmaf(a[u + 1].x, fb, c2);
+                c3 = fmaf(a[u + 1].y, fb, c3);
+              }
           }
-          for (; h + 1 < H; h += 2) {
-            const float2 a = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h) * sstride);
-            const float2 b = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h + 1) * sstride);
-            const float fa = soft ? ml[h] : 1.f, fb = soft ? ml[h + 1] : 1.f;
-            c0 = fmaf(a.x, fa, c0);
-            c1 = fmaf(a.y, fa, c1);
-            c2 = fmaf(b.x, fb, c2);
-            c3 = fmaf(b.y, fb, c3);
-          }
+          h = hp;
           if (h < H) {
             const float2 a = *reinterpret_cast<const float2*>(s2 + static_cast<size_t>(h) * sstride);
             const float fa = soft ? ml[h] : 1.f;
