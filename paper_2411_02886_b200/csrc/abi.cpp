@@ -790,7 +790,7 @@ bool prefill_uses_tc(int H, int H_kv, int d) {
 // C-row sparse attention: the tcgen05 kernel where it applies (d = 128,
 // G <= 8), the CUDA-core kernel otherwise.
 cudaError_t launch_prefill(tsb::PrefillAttendParams& pa, DevBuf& split_ws, cudaStream_t st) {
-  if (!pa.att && !prefill_uses_tc(pa.H, pa.H_kv, pa.d)) return cudaErrorInvalidValue;  // (implicit windows: tcgen05 only)
+  if (pa.win_n_att && !prefill_uses_tc(pa.H, pa.H_kv, pa.d)) return cudaErrorInvalidValue;  // (implicit windows: tcgen05 only)
   if (pa.d == 128 && pa.H / pa.H_kv <= 8 && !g_force_cuda_core_prefill) {
     // bf16 parts of the chunk's K/V, owned by the caller's pool / engine (stream-ordered reuse)
     pa.split_ws = static_cast<uint16_t*>(

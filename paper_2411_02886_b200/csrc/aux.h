@@ -18,7 +18,7 @@ struct PrefillAttendParams {
   int n_att;
   const int* n_att_ptr;    // device count (overrides n_att when set)
   int n_att_max;           // bound on the attended count (the tensor-core paths' gathered copy)
-  // tcgen05 path, implicit windows (att == nullptr): the attended rows are
+  // tcgen05 path, implicit windows (win_n_att set): the attended rows are
   // [0, win_init_end) ++ the selection inside [win_init_end, win_local_begin)
   // ++ [max(win_local_begin, win_init_end), win_cached) -- make_windows +
   // merged() (attention.cpp:21-52) formed inside prep_tc_kernel, which also

@@ -551,7 +551,7 @@ __global__ void prep_tc_kernel(PrefillAttendParams p, uint16_t* __restrict__ kc3
   // selection -- its split points by counting (one pass over the selection
   // per CTA, one L2 round trip; a binary search is a chain of them)
   int n_cached, ie = 0, lb = 0, lo1 = 0, n1 = 0;
-  if (!p.att) {
+  if (p.win_n_att) {
     const int n_sel = p.win_sel && p.win_n_sel ? *p.win_n_sel : 0;
     ie = p.win_init_end;
     lb = max(p.win_local_begin, ie);
@@ -590,7 +590,7 @@ __global__ void prep_tc_kernel(PrefillAttendParams p, uint16_t* __restrict__ kc3
     uint4* kd = reinterpret_cast<uint4*>(kg + static_cast<size_t>(key) * row_vec * 8);
     uint4* vd = reinterpret_cast<uint4*>(vg + static_cast<size_t>(key) * row_vec * 8);
     if (key < n_cached) {
-      const uint32_t tok = p.att ? p.att[key]
+      const uint32_t tok = !p.win_n_att ? p.att[key]
                                  : key < ie ? static_cast<uint32_t>(key)
                                  : key < ie + n1 ? __ldcg(p.win_sel + lo1 + key - ie)
                                                  : static_cast<uint32_t>(lb + key - ie - n1);
