@@ -793,8 +793,9 @@ cudaError_t launch_prefill(tsb::PrefillAttendParams& pa, DevBuf& split_ws, cudaS
   if (pa.win_n_att && !prefill_uses_tc(pa.H, pa.H_kv, pa.d)) return cudaErrorInvalidValue;  // (implicit windows: tcgen05 only)
   if (pa.d == 128 && pa.H / pa.H_kv <= 8 && !g_force_cuda_core_prefill) {
     // bf16 parts of the chunk's K/V, owned by the caller's pool / engine (stream-ordered reuse)
-    pa.split_ws = static_cast<uint16_t*>(
-        split_ws.ensure(static_cast<size_t>(2) * (3 * pa.C + std::max(pa.n_att_max, 0)) * pa.H_kv * pa.d * 2));
+    const size_t base = static_cast<size_t>(2) * (3 * pa.C + std::max(pa.n_att_max, 0)) * pa.H_kv * pa.d * 2;
+    const size_t extra = prefill_uses_tc(pa.H, pa.H_kv, pa.d) ? tsb::prefill_tc_extra_ws_bytes(pa, st) + 256 : 0;
+    pa.split_ws = static_cast<uint16_t*>(split_ws.ensure(base + extra));
     // tcgen05 (prefill_tc.cu); the mma.sync kernel (prefill.cu) on request (TS_PREFILL_MMA_SYNC=1)
     if (!g_prefill_mma_sync) return tsb::launch_prefill_tc(pa, st);
     return tsb::launch_prefill_flash(pa, st);

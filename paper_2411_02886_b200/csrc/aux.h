@@ -51,6 +51,9 @@ cudaError_t launch_prefill_attend(const PrefillAttendParams& p, cudaStream_t st)
 cudaError_t launch_prefill_flash(const PrefillAttendParams& p, cudaStream_t st);
 // tcgen05 path (prefill_tc.cu): d = 128, G <= 16; cudaErrorInvalidValue otherwise
 cudaError_t launch_prefill_tc(const PrefillAttendParams& p, cudaStream_t st);
+// extra bytes launch_prefill_tc needs in split_ws past the gathered rows (the
+// balanced plan's partial slots and piece counters), + 256 for alignment
+size_t prefill_tc_extra_ws_bytes(const PrefillAttendParams& p, cudaStream_t st);
 cudaError_t launch_shard_merge(const uint32_t* all, int world, int k, uint32_t ie, uint32_t lbs, uint32_t base,
                                uint32_t n_r, uint32_t init_hi, uint32_t loc_lo, uint32_t* att, int* n_att,
                                cudaStream_t st);

@@ -37,7 +37,10 @@
 #include <cfloat>
 #include <cmath>
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "aux.h"
 #include "common.cuh"
@@ -59,7 +62,9 @@ constexpr int kOffK = 0;                         // 2 buffers of K
 constexpr int kOffV = kOffK + 2 * kKVTile;       // 2 buffers of V
 constexpr int kOffBar = kOffV + 2 * kKVTile;
 constexpr int kOffRed = kOffBar + 256;              // [2 tiles][2 halves][128] row-max / row-sum exchange
-constexpr int kSmem = kOffRed + 4 * kM * 4;
+constexpr int kOutStride = kD + 4;                  // staged output row (floats; 16-B aligned, conflict-light)
+constexpr int kOffOut = kOffRed + 4 * kM * 4;       // [128 rows][kOutStride] output staging
+constexpr int kSmem = kOffOut + kM * kOutStride * 4;
 
 __device__ __forceinline__ uint16_t bfb(float x) { return __bfloat16_as_ushort(__float2bfloat16_rn(x)); }
 // x = h + m + l exactly: h = x truncated to bf16 (8 significant bits), the
@@ -183,64 +188,87 @@ __device__ __forceinline__ void tma_tile2d(void* dst, const CUtensorMap* tm, int
       : "memory");
 }
 
-// Warp roles (cached tiles and the chunk's own tiles alike):
+// Work items. A unit is (row block x, KV head g): 128 query rows against its
+// tiles -- the cached tiles [0, nct) (the same attended rows for every unit)
+// then the chunk's own tiles, causal, so later row blocks have more of them.
+// Units differ in cost by up to 40 %, so the host cuts the concatenated tile
+// sequence of all units into one contiguous, equal-cost range per CTA; a
+// range may end inside a unit (a piece). A unit cut into pieces leaves each
+// piece's unnormalised O, log2 reference max and row sum in a partial slot,
+// and the last of its pieces to finish merges them (log-sum-exp, piece order).
+constexpr int kMaxPieces = 4;
+struct TcPiece {
+  int16_t x, g, t0, t1;  // unit and its tile range [t0, t1)
+  int16_t slot;          // partial slot (-1: the whole unit, written directly)
+  int16_t unit;
+};
+struct TcWork {
+  int32_t n;
+  TcPiece pc[kMaxPieces];
+};
+struct TcSplit {
+  const TcWork* work;        // [grid]
+  const int16_t* unit_slot0; // [units] first partial slot of a split unit
+  const int16_t* unit_np;    // [units] its pieces
+  float* part_o;             // [slots][128 rows][128]
+  float* part_ml;            // [slots][128 rows][2]: log2 reference max, row sum
+  unsigned* cnt;             // [units] pieces finished (zeroed by prep_tc_kernel)
+  int nct;                   // cached tiles per unit (planned from n_att_max)
+};
+
+// Warp roles (cached tiles and the chunk's own tiles alike, over the CTA's
+// pieces in order):
 //   warps 0-7   softmax: two threads per query row (TMEM lane quarter w % 4,
-//               key / d column half w / 4); P(t) goes over S(t) in TMEM
+//               key / d column half w / 4); P(t) goes over S(t) in TMEM; at
+//               a piece start they stage its Q in TMEM (q_ready), at its end
+//               they write the output rows or the partial (and merge)
 //   warp 8      MMA issue (one elected lane): QK(t) as soon as its K loads
 //               landed, then P.V(t - 1) once P(t - 1) is written -- the tensor
 //               core runs QK(t) while the softmax warps work on tile t - 1,
-//               and runs P.V(t - 2) before the QK(t) that overwrites its P
+//               and runs P.V(t - 2) before the QK(t) that overwrites its P; at
+//               a piece start P.V(t - 1) goes first, then it waits for the Q
 //   warp 9/10   TMA producers of the K / V loads into two slots each: one load
 //               per cached tile, three (the split parts) per chunk tile
 // Every hand-off is an mbarrier per buffer, so no waiter can fall two phases
 // behind: s_full[b] (QK done), pv_done[b] (P.V done), kvk_full[s] / kvv_full[s]
 // (K / V load landed in slot s), k_free[s] / v_free[s] (the MMAs reading slot
-// s completed), p_full (P written and the previous delta folded).
+// s completed), p_full (P written and the previous delta folded), q_ready
+// (a piece's Q staged). Tile-indexed barriers count the CTA's tiles across
+// its pieces.
 __global__ void __launch_bounds__(kThr, 1)
-    prefill_tc_kernel(PrefillAttendParams p, const __grid_constant__ CUtensorMap tm_kg, const __grid_constant__ CUtensorMap tm_vg,
-                      const __grid_constant__ CUtensorMap tm_kc, const __grid_constant__ CUtensorMap tm_vc) {
+    prefill_tc_kernel(PrefillAttendParams p, TcSplit sp, const __grid_constant__ CUtensorMap tm_kg,
+                      const __grid_constant__ CUtensorMap tm_vg, const __grid_constant__ CUtensorMap tm_kc,
+                      const __grid_constant__ CUtensorMap tm_vc) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int G = p.H / p.H_kv;
-  const int rows_per_head = kM / G;  // chunk rows per CTA
-  const int g = blockIdx.y;
-  const int i0 = blockIdx.x * rows_per_head;
+  const int rows_per_head = kM / G;  // chunk rows per unit
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int row_elems = p.H_kv * kD;
-  const int n_cached = p.n_att_ptr ? *p.n_att_ptr : p.n_att;
-  const int n_cur = min(p.C, i0 + rows_per_head);  // chunk rows any row here can see
-  const int nct = (n_cached + kKT - 1) / kKT;
-  const int n_tiles = nct + (n_cur + kKT - 1) / kKT;
+  const int n_cached = p.n_att_ptr ? *p.n_att_ptr : p.n_att;  // (<= nct * 64)
+  const int nct = sp.nct;
+  const TcWork wk = sp.work[blockIdx.x];
   const uint32_t sbase = smem_u32(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
   uint64_t* s_full = bars + 0;    // [2]
   uint64_t* pv_done = bars + 2;   // [2]
   uint64_t* kvk_full = bars + 4;  // [2]
   uint64_t* kvv_full = bars + 6;  // [2]
+  uint64_t* q_ready = bars + 8;   // [1]
   uint64_t* p_full = bars + 10;   // [1]
   uint64_t* k_free = bars + 11;   // [2] the MMAs reading a K slot completed
   uint64_t* v_free = bars + 13;   // [2] the MMAs reading a V slot completed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 128);
+  int* last_flag = reinterpret_cast<int*>(smem + kOffBar + 136);
   float* red = reinterpret_cast<float*>(smem + kOffRed);  // [2][2][kM]
-  // dev trace (globaltimer stamps): CTA (0, 0) -> slots [0, 2048), the last
-  // row block -> [2048, 4096); [0, 16) phases, then per tile / load: 16 + t
-  // softmax done, 256 + t S ready, 512 + t QK issue, 768 + t P.V issue,
-  // 1024 + l K load landed, 1280 + l V load landed
-  unsigned long long* tcta = nullptr;
-  if (p.trace && blockIdx.y == 0) {
-    if (blockIdx.x == 0) tcta = p.trace;
-    else if (blockIdx.x == gridDim.x - 1) tcta = p.trace + 2048;
-  }
-  auto mark = [&](int i) {
-    if (tcta && i < 2048) {
+  // dev trace (TS_PREFILL_TRACE): %globaltimer at the CTA's start, each
+  // piece's end and the CTA's end -> trace[cta * 8 + slot]
+  auto mark = [&](int slot) {
+    if (p.trace && blockIdx.x < 512) {
       unsigned long long gt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-      tcta[i] = gt;
+      p.trace[blockIdx.x * 8 + slot] = gt;
     }
   };
-  auto stamp = [&](int i) {
-    if (threadIdx.x == 0) mark(i);
-  };
-  stamp(0);
+  if (tid == 0) mark(0);
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
@@ -248,6 +276,7 @@ __global__ void __launch_bounds__(kThr, 1)
       mbar_init(&kvk_full[i], 1);  // (+ the TMA transaction bytes)
       mbar_init(&kvv_full[i], 1);
     }
+    mbar_init(q_ready, kSmThr);
     mbar_init(p_full, kSmThr);
     mbar_init(&k_free[0], 1);
     mbar_init(&k_free[1], 1);
@@ -256,7 +285,6 @@ __global__ void __launch_bounds__(kThr, 1)
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, 512);
-  stamp(5);
   tmem_fence_before_sync();
   __syncthreads();
   tmem_fence_after_sync();
@@ -267,14 +295,16 @@ __global__ void __launch_bounds__(kThr, 1)
   const uint32_t q_tmem = tbase + 192;  // [192, 384): Q, 3 bf16 parts x 64 columns
   const uint32_t o_tmem = tbase + 384;  // [384, 512): one tile's P.V (fresh per tile)
   constexpr int kSP = 3 * kKT / 2;      // columns per S/P buffer
+  auto nk = [&](int t) { return t < nct ? 1 : 3; };  // loads per tile
 
-  // TMA load of part `part` of tile `tile`'s K or V rows into the 16-KB slot
-  // at `dst`: two 64 x 64 boxes (the d halves; 128B swizzle = the UMMA
-  // layout) of the gathered cached rows (tm_kg / tm_vg) or of the chunk's
-  // split copy (tm_kc / tm_vc), completing on `bar`. Rows past the attended
-  // count are zeros (prep_tc_kernel) or out of bounds (zero-filled); rows of
-  // the chunk past the causal limit are masked in the softmax.
-  auto tma_tile = [&](int tile, int part, bool is_k, uint8_t* dst, uint64_t* bar) {
+  // TMA load of part `part` of unit-tile `tile` (KV head g)'s K or V rows
+  // into the 16-KB slot at `dst`: two 64 x 64 boxes (the d halves; 128B
+  // swizzle = the UMMA layout) of the gathered cached rows (tm_kg / tm_vg)
+  // or of the chunk's split copy (tm_kc / tm_vc), completing on `bar`. Rows
+  // past the attended count are zeros (prep_tc_kernel) or out of bounds
+  // (zero-filled); rows of the chunk past the causal limit are masked in the
+  // softmax.
+  auto tma_tile = [&](int g, int tile, int part, bool is_k, uint8_t* dst, uint64_t* bar) {
     if (lane == 0) mbar_arrive_expect_tx(bar, kKVTile);
     __syncwarp();
     if (lane < 2) {
@@ -285,258 +315,323 @@ __global__ void __launch_bounds__(kThr, 1)
     }
   };
 
-  // ---- softmax state: thread (row m, half) of warps 0-7
-  const bool is_sm = warp < 8;
-  const int m = (warp & 3) * 32 + lane;  // TMEM lane = query row
-  const int half = (warp >> 2) & 1;
-  const uint32_t lane_sel = static_cast<uint32_t>((warp & 3) * 32) << 16;
-  const int hm = m / rows_per_head;  // (G * rows_per_head <= 128: rows past it are padding)
-  const int i_row = i0 + (m - hm * rows_per_head);
-  const bool row_ok = hm < G && i_row < p.C;
-  float m_ref = -INFINITY, l_run = 0.f;  // (l_run: this thread's half of the row)
-  const float sl2 = p.scale * kLog2e;
-  int t_cur = 0;               // (dev trace)
-  constexpr int KH = kKT / 2;  // this thread's key columns
-  float s[KH];
-  // the running O: this thread's 64 of the row's 128 columns, in registers
-  // (fp32 round-to-nearest adds of every tile's P.V delta)
-  float orun[kD / 2];
+  if (warp < 8) {
+    // ================================================ softmax warps
+    const int m = (warp & 3) * 32 + lane;  // TMEM lane = query row
+    const int half = (warp >> 2) & 1;
+    const uint32_t lane_sel = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const int hm = m / rows_per_head;  // (G * rows_per_head <= 128: rows past it are padding)
+    const float sl2 = p.scale * kLog2e;
+    constexpr int KH = kKT / 2;  // this thread's key columns
+    float s[KH];
+    float orun[kD / 2];  // the running O: this thread's 64 of the row's 128 columns
+    float m_ref, l_run;  // (l_run: this thread's half of the row)
+    int i_row = 0, n_cur = 0;
+    bool row_ok = false;
+    // O_run = (O_run + delta) * c
+    auto fold = [&](float c) {
+      float a[32];
 #pragma unroll
-  for (int u = 0; u < kD / 2; ++u) orun[u] = 0.f;
-  // O_run = (O_run + delta) * c
-  auto fold = [&](float c) {
-    float a[32];
+      for (int q = 0; q < kD / 64; ++q) {
+        tmem_ld32(o_tmem + lane_sel + half * (kD / 2) + q * 32, a);
 #pragma unroll
-    for (int q = 0; q < kD / 64; ++q) {
-      tmem_ld32(o_tmem + lane_sel + half * (kD / 2) + q * 32, a);
-#pragma unroll
-      for (int u = 0; u < 32; ++u) orun[q * 32 + u] = (orun[q * 32 + u] + a[u]) * c;
-    }
-  };
-  // (1) this thread's 32 scores of the tile -> s[], own max -> red[rb][half][m]
-  auto sm_load = [&](uint32_t s_addr, int k0, bool chunk, int rb) {
-    const int lim = chunk ? min(n_cur - 1, i_row) + 1 : n_cached;  // visible keys: [0, lim)
-    const int kb0 = k0 + half * KH;
-    static_assert(KH == 32, "one x32 load per thread");
-    tmem_ld32(s_addr + lane_sel + half * KH, s);
-    float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-    const int nv = row_ok ? lim - kb0 : 0;  // visible keys among this thread's 32
-#pragma unroll
-    for (int u = 0; u < KH; ++u) {
-      s[u] = u < nv ? s[u] * sl2 : -INFINITY;  // log2-domain logits
-      mx[u & 3] = fmaxf(mx[u & 3], s[u]);
-    }
-    red[(rb * 2 + half) * kM + m] = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-  };
-  // (2) after the max exchange: lazy reference max (moved only when the max
-  // grows by > 8), P = 2^(s - m_ref) split into three bf16 parts -> P[rb] in
-  // tensor memory; returns the factor that moves O and l to the new reference
-  auto sm_p = [&](int rb) -> float {
-    const float mt = fmaxf(red[(rb * 2 + half) * kM + m], red[(rb * 2 + (half ^ 1)) * kM + m]);
-    float corr = 1.f;
-    if (mt > m_ref + 8.f) {
-      corr = m_ref == -INFINITY ? 0.f : ex2_approx(m_ref - mt);
-      l_run *= corr;
-      m_ref = mt;
-    }
-    float ls[4] = {0.f, 0.f, 0.f, 0.f};
-    float hw[KH / 2], mw[KH / 2], lw[KH / 2];  // packed pairs (bit patterns)
-    const float mu = m_ref == -INFINITY ? 0.f : m_ref;  // (a row with no visible key yet: every p = 2^-inf = 0)
-#pragma unroll
-    for (int c = 0; c < KH / 2; ++c) {
-      const float p0 = ex2_approx(s[2 * c] - mu);
-      const float p1 = ex2_approx(s[2 * c + 1] - mu);
-      ls[c & 3] += p0 + p1;
-      float h0, m0, l0, h1, m1, l1;
-      sp3(p0, h0, m0, l0);
-      sp3(p1, h1, m1, l1);
-      hw[c] = __uint_as_float(pk2(h0, h1));
-      mw[c] = __uint_as_float(pk2(m0, m1));
-      lw[c] = __uint_as_float(pk2(l0, l1));
-    }
-    l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-    const uint32_t pa = sp_tmem + rb * kSP + lane_sel + half * (KH / 2);
-    tmem_st16(pa, hw);
-    tmem_st16(pa + kKT / 2, mw);
-    tmem_st16(pa + kKT, lw);
-    return corr;
-  };
-
-  // ---- Q -> tensor memory: thread (row m, half) splits its 64 d columns of
-  // the row's query (head g + hm * H_kv, chunk row i_row) into three exact
-  // bf16 parts, two per 32-bit column
-  if (is_sm) {
-    const float4* src = reinterpret_cast<const float4*>(p.q + static_cast<size_t>(row_ok ? i_row : 0) * p.H * kD +
-                                                        static_cast<size_t>(g + (row_ok ? hm : 0) * p.H_kv) * kD + half * (kD / 2));
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {  // 32 d columns -> 16 TMEM columns per part
-      float hw[16], mw[16], lw[16];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        float4 x = row_ok ? src[c * 8 + u] : make_float4(0.f, 0.f, 0.f, 0.f);
-        float h0, m0, l0, h1, m1, l1;
-        sp3(x.x, h0, m0, l0);
-        sp3(x.y, h1, m1, l1);
-        hw[2 * u] = __uint_as_float(pk2(h0, h1));
-        mw[2 * u] = __uint_as_float(pk2(m0, m1));
-        lw[2 * u] = __uint_as_float(pk2(l0, l1));
-        sp3(x.z, h0, m0, l0);
-        sp3(x.w, h1, m1, l1);
-        hw[2 * u + 1] = __uint_as_float(pk2(h0, h1));
-        mw[2 * u + 1] = __uint_as_float(pk2(m0, m1));
-        lw[2 * u + 1] = __uint_as_float(pk2(l0, l1));
+        for (int u = 0; u < 32; ++u) orun[q * 32 + u] = (orun[q * 32 + u] + a[u]) * c;
       }
-      const uint32_t qa = q_tmem + lane_sel + half * (kD / 4) + c * 16;
-      tmem_st16(qa, hw);
-      tmem_st16(qa + kD / 2, mw);
-      tmem_st16(qa + kD, lw);
-    }
-    tmem_wait_st();
-  }
-  tmem_fence_before_sync();
-  __syncthreads();
-  tmem_fence_after_sync();
-
-  stamp(1);
-  // ================================================ all tiles, specialised
-  // Tile t has nk(t) K loads and nk(t) V loads: one for a cached tile, the
-  // three exact bf16 parts for a tile of the chunk's own (fp32) rows. The
-  // loads stream through two K slots and two V slots in load order; a slot is
-  // refilled once the MMAs that read it completed (k_free / v_free).
-  auto nk = [&](int t) { return t < nct ? 1 : 3; };
-  auto first_load = [&](int t) { return t <= nct ? t : nct + 3 * (t - nct); };  // index of tile t's first load
-  if (n_tiles > 0) {
-    if (is_sm) {
-      for (int t = 0; t < n_tiles; ++t) {
-        const int b = t & 1;
+    };
+    // the normalised rows -> out, through shared memory so that a warp stores
+    // whole 512-B rows (a thread's own 256 B of a row, 16 KB apart from its
+    // neighbours', would scatter every store instruction over 32 lines)
+    float* ostage = reinterpret_cast<float*>(smem + kOffOut);
+    auto write_rows = [&](float inv, int g, int i0) {
+#pragma unroll
+      for (int u = 0; u < kD / 2; u += 4)
+        *reinterpret_cast<float4*>(ostage + m * kOutStride + half * (kD / 2) + u) =
+            make_float4(orun[u] * inv, orun[u + 1] * inv, orun[u + 2] * inv, orun[u + 3] * inv);
+      named_sync(1, kSmThr);
+      for (int r = warp; r < kM; r += kSmThr / 32) {  // warp per row, lane per 16 B
+        const int hr = r / rows_per_head, ir = i0 + (r - hr * rows_per_head);
+        if (hr < G && ir < p.C)
+          *reinterpret_cast<float4*>(p.out + static_cast<size_t>(ir) * p.H * kD + static_cast<size_t>(g + hr * p.H_kv) * kD + lane * 4) =
+              *reinterpret_cast<const float4*>(ostage + r * kOutStride + lane * 4);
+      }
+    };
+    // (1) this thread's 32 scores of the tile -> s[], own max -> red[rb][half][m]
+    auto sm_load = [&](uint32_t s_addr, int k0, bool chunk, int rb) {
+      const int lim = chunk ? min(n_cur - 1, i_row) + 1 : n_cached;  // visible keys: [0, lim)
+      const int kb0 = k0 + half * KH;
+      tmem_ld32(s_addr + lane_sel + half * KH, s);
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      const int nv = row_ok ? lim - kb0 : 0;  // visible keys among this thread's 32
+#pragma unroll
+      for (int u = 0; u < KH; ++u) {
+        s[u] = u < nv ? s[u] * sl2 : -INFINITY;  // log2-domain logits
+        mx[u & 3] = fmaxf(mx[u & 3], s[u]);
+      }
+      red[(rb * 2 + half) * kM + m] = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+    };
+    // (2) after the max exchange: lazy reference max (moved only when the max
+    // grows by > 8), P = 2^(s - m_ref) split into three bf16 parts -> P[rb] in
+    // tensor memory; returns the factor that moves O and l to the new reference
+    auto sm_p = [&](int rb) -> float {
+      const float mt = fmaxf(red[(rb * 2 + half) * kM + m], red[(rb * 2 + (half ^ 1)) * kM + m]);
+      float corr = 1.f;
+      if (mt > m_ref + 8.f) {
+        corr = m_ref == -INFINITY ? 0.f : ex2_approx(m_ref - mt);
+        l_run *= corr;
+        m_ref = mt;
+      }
+      float ls[4] = {0.f, 0.f, 0.f, 0.f};
+      float hw[KH / 2], mw[KH / 2], lw[KH / 2];  // packed pairs (bit patterns)
+      const float mu = m_ref == -INFINITY ? 0.f : m_ref;  // (a row with no visible key yet: every p = 2^-inf = 0)
+#pragma unroll
+      for (int c = 0; c < KH / 2; ++c) {
+        const float p0 = ex2_approx(s[2 * c] - mu);
+        const float p1 = ex2_approx(s[2 * c + 1] - mu);
+        ls[c & 3] += p0 + p1;
+        float h0, m0, l0, h1, m1, l1;
+        sp3(p0, h0, m0, l0);
+        sp3(p1, h1, m1, l1);
+        hw[c] = __uint_as_float(pk2(h0, h1));
+        mw[c] = __uint_as_float(pk2(m0, m1));
+        lw[c] = __uint_as_float(pk2(l0, l1));
+      }
+      l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      const uint32_t pa = sp_tmem + rb * kSP + lane_sel + half * (KH / 2);
+      tmem_st16(pa, hw);
+      tmem_st16(pa + kKT / 2, mw);
+      tmem_st16(pa + kKT, lw);
+      return corr;
+    };
+    // ---- a unit's Q -> tensor memory: thread (row m, half) splits its 64 d
+    // columns of the row's query (head g + hm * H_kv, chunk row ir) into
+    // three exact bf16 parts, two per 32-bit column; then q_ready. (Called
+    // for the next piece as soon as the current piece's last QK completed,
+    // so the next piece's first QK overlaps this piece's drain.)
+    auto stage_q = [&](const TcPiece& pc) {
+      const int ir = pc.x * rows_per_head + (m - hm * rows_per_head);
+      const bool ok = hm < G && ir < p.C;
+      const float4* src = reinterpret_cast<const float4*>(p.q + static_cast<size_t>(ok ? ir : 0) * p.H * kD +
+                                                          static_cast<size_t>(pc.g + (ok ? hm : 0) * p.H_kv) * kD +
+                                                          half * (kD / 2));
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {  // 32 d columns -> 16 TMEM columns per part
+        float hw[16], mw[16], lw[16];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          float4 xv = ok ? src[c * 8 + u] : make_float4(0.f, 0.f, 0.f, 0.f);
+          float h0, m0, l0, h1, m1, l1;
+          sp3(xv.x, h0, m0, l0);
+          sp3(xv.y, h1, m1, l1);
+          hw[2 * u] = __uint_as_float(pk2(h0, h1));
+          mw[2 * u] = __uint_as_float(pk2(m0, m1));
+          lw[2 * u] = __uint_as_float(pk2(l0, l1));
+          sp3(xv.z, h0, m0, l0);
+          sp3(xv.w, h1, m1, l1);
+          hw[2 * u + 1] = __uint_as_float(pk2(h0, h1));
+          mw[2 * u + 1] = __uint_as_float(pk2(m0, m1));
+          lw[2 * u + 1] = __uint_as_float(pk2(l0, l1));
+        }
+        const uint32_t qa = q_tmem + lane_sel + half * (kD / 4) + c * 16;
+        tmem_st16(qa, hw);
+        tmem_st16(qa + kD / 2, mw);
+        tmem_st16(qa + kD, lw);
+      }
+      tmem_wait_st();
+      tmem_fence_before_sync();
+      mbar_arrive(q_ready);
+    };
+    int i = 0;  // the CTA's tile counter
+    if (wk.n > 0) stage_q(wk.pc[0]);
+    for (int pi = 0; pi < wk.n; ++pi) {
+      const TcPiece pc = wk.pc[pi];
+      const int g = pc.g, i0 = pc.x * rows_per_head;
+      n_cur = min(p.C, i0 + rows_per_head);  // chunk rows any row here can see
+      i_row = i0 + (m - hm * rows_per_head);
+      row_ok = hm < G && i_row < p.C;
+      m_ref = -INFINITY;
+      l_run = 0.f;
+#pragma unroll
+      for (int u = 0; u < kD / 2; ++u) orun[u] = 0.f;
+      for (int t = pc.t0; t < pc.t1; ++t, ++i) {
+        const int b = i & 1;
         const bool chunk = t >= nct;
-        mbar_wait(&s_full[b], static_cast<uint32_t>(t >> 1) & 1u);  // QK(t) done
+        mbar_wait(&s_full[b], static_cast<uint32_t>(i >> 1) & 1u);  // QK(i) done
         tmem_fence_after_sync();
-        if (tid == 0) mark(256 + t);
         sm_load(sp_tmem + b * kSP, chunk ? (t - nct) * kKT : t * kKT, chunk, b);
         named_sync(1, kSmThr);  // row maxima exchanged; every thread's S[b] loads done (P goes over them)
-        if (tid == 0 && t < 64) mark(320 + t);
-        t_cur = t;
         const float corr = sm_p(b);
-        if (tid == 0 && t < 64) mark(384 + t);
-        if (t >= 1) {  // P.V(t - 1) completed: its delta into O_run
-          mbar_wait(&pv_done[(t - 1) & 1], static_cast<uint32_t>((t - 1) >> 1) & 1u);
+        if (t > pc.t0) {  // P.V(i - 1) completed: its delta into O_run
+          mbar_wait(&pv_done[(i - 1) & 1], static_cast<uint32_t>((i - 1) >> 1) & 1u);
           tmem_fence_after_sync();
-          if (tid == 0 && t < 64) mark(448 + t);
           fold(corr);
         }
         tmem_wait_st();  // P stored
         tmem_fence_before_sync();
         mbar_arrive(p_full);
-        if (t == nct - 1) stamp(2);
-        stamp(16 + t);
+        if (t == pc.t1 - 1 && pi + 1 < wk.n) stage_q(wk.pc[pi + 1]);  // (every QK of this piece completed)
       }
-      // the last P.V
-      mbar_wait(&pv_done[(n_tiles - 1) & 1], static_cast<uint32_t>((n_tiles - 1) >> 1) & 1u);
+      // the piece's last P.V
+      if (tid == 0 && pi == 0) mark(4);
+      mbar_wait(&pv_done[(i - 1) & 1], static_cast<uint32_t>((i - 1) >> 1) & 1u);
       tmem_fence_after_sync();
+      if (tid == 0 && pi == 0) mark(3);
       fold(1.f);
-    } else if (warp == 8) {
-      // the whole warp runs the loop (warp-uniform operands stay in uniform
-      // registers); one elected lane issues the MMAs and commits
-      const uint64_t dk0 = sdesc(sbase + kOffK, 16, 1024);
-      const uint64_t dv0 = sdesc(sbase + kOffV, kKT * 128, 1024);
-      for (int t = 0; t <= n_tiles; ++t) {
-        if (t < n_tiles) {  // QK(t): its K loads in order, accumulated into S[t % 2]
-          const int b = t & 1;
-          // (S[b] = P(t - 2): its P.V was issued before this QK; the tensor core runs them in order)
-          if (lane == 0) mark(512 + t);
-          for (int pk = 0, li = first_load(t); pk < nk(t); ++pk, ++li) {
-            const int ks = li & 1;
-            mbar_wait(&kvk_full[ks], static_cast<uint32_t>(li >> 1) & 1u);  // this K load landed
-            tmem_fence_after_sync();
-            if (lane == 0 && pk == 0 && t < 64) mark(576 + t);
-            if (elect_one()) {
-              issue_qk(q_tmem, dk0 + ks * (kKVTile >> 4), sp_tmem + b * kSP, pk, pk == 0);
-              umma_commit(&k_free[ks]);
-              if (pk == nk(t) - 1) umma_commit(&s_full[b]);
-            }
-            __syncwarp();
-          }
-          if (lane == 0 && t < 64) mark(640 + t);
+      // ---- the piece's rows: l = the two halves' sums
+      named_sync(1, kSmThr);  // (every thread past its last red[] read)
+      red[half * kM + m] = l_run;
+      named_sync(1, kSmThr);
+      if (tid == 0 && pi == 0) mark(6);
+      const float l = l_run + red[(half ^ 1) * kM + m];
+      if (pc.slot < 0) {
+        write_rows(l > 0.f ? 1.f / l : 0.f, g, pc.x * rows_per_head);
+      } else {
+        // partial: unnormalised O (log2 reference m_ref), the row sum
+        // layout [slot][half][16 float4][128 rows]: a warp's lanes (rows)
+        // store 512 contiguous bytes per float4
+        float4* po = reinterpret_cast<float4*>(sp.part_o) + (static_cast<size_t>(pc.slot) * 2 + half) * (kD / 8) * kM + m;
+#pragma unroll
+        for (int u = 0; u < kD / 8; ++u) po[u * kM] = make_float4(orun[4 * u], orun[4 * u + 1], orun[4 * u + 2], orun[4 * u + 3]);
+        if (half == 0)
+          *reinterpret_cast<float2*>(sp.part_ml + (static_cast<size_t>(pc.slot) * kM + m) * 2) = make_float2(m_ref, l);
+        named_sync(1, kSmThr);
+        // release: the barrier orders every thread's partial stores before
+        // thread 0's gpu-scope fence (cumulative), then the arrival
+        if (tid == 0) {
+          __threadfence();
+          *last_flag = atomicAdd(sp.cnt + pc.unit, 1u) + 1u == static_cast<unsigned>(sp.unit_np[pc.unit]);
         }
-        if (t >= 1) {  // P.V(t - 1): its V loads in order, into the fresh delta
-          const int u = t - 1;
-          mbar_wait(p_full, static_cast<uint32_t>(u) & 1u);  // P(t - 1) written
-          if (lane == 0) mark(768 + u);
-          for (int pv = 0, li = first_load(u); pv < nk(u); ++pv, ++li) {
-            const int vs = li & 1;
-            mbar_wait(&kvv_full[vs], static_cast<uint32_t>(li >> 1) & 1u);
-            tmem_fence_after_sync();
-            if (lane == 0 && pv == 0 && u < 64) mark(832 + u);
-            if (elect_one()) {
-              issue_pv(sp_tmem + (u & 1) * kSP, dv0 + vs * (kKVTile >> 4), o_tmem, pv, pv == 0);
-              umma_commit(&v_free[vs]);
-              if (pv == nk(u) - 1) umma_commit(&pv_done[u & 1]);
+        named_sync(1, kSmThr);
+        if (tid == 0 && pi == 0) mark(5);
+        if (*last_flag) {
+          // the unit's last piece: log-sum-exp merge of its pieces in order
+          // (acquire: thread 0's fenced atomic saw every other arrival)
+          __threadfence();
+          const int s0 = sp.unit_slot0[pc.unit], np = sp.unit_np[pc.unit];
+          float M = -INFINITY;
+          for (int k = 0; k < np; ++k) M = fmaxf(M, __ldcg(sp.part_ml + (static_cast<size_t>(s0 + k) * kM + m) * 2));
+          float L = 0.f;
+#pragma unroll
+          for (int u = 0; u < kD / 2; ++u) orun[u] = 0.f;
+          for (int k = 0; k < np; ++k) {
+            const float2 ml = __ldcg(reinterpret_cast<const float2*>(sp.part_ml + (static_cast<size_t>(s0 + k) * kM + m) * 2));
+            const float w = ml.x == -INFINITY ? 0.f : ex2_approx(ml.x - M);
+            L = fmaf(w, ml.y, L);
+            const float4* pk = reinterpret_cast<const float4*>(sp.part_o) + (static_cast<size_t>(s0 + k) * 2 + half) * (kD / 8) * kM + m;
+#pragma unroll
+            for (int u = 0; u < kD / 8; ++u) {
+              const float4 o = __ldcg(pk + u * kM);
+              orun[4 * u] = fmaf(w, o.x, orun[4 * u]);
+              orun[4 * u + 1] = fmaf(w, o.y, orun[4 * u + 1]);
+              orun[4 * u + 2] = fmaf(w, o.z, orun[4 * u + 2]);
+              orun[4 * u + 3] = fmaf(w, o.w, orun[4 * u + 3]);
             }
-            __syncwarp();
           }
-          if (lane == 0 && u < 64) mark(896 + u);
+          write_rows(L > 0.f ? 1.f / L : 0.f, g, pc.x * rows_per_head);
         }
       }
-    } else {
-      // producers: warp 9 streams the K loads, warp 10 the V loads, each
-      // into its slot once the MMAs that read the slot's previous load
-      // completed. (The streams are independent: a tile's last K part is
-      // needed before the P.V that frees a V slot of the same tile.)
-      const bool is_k = warp == 9;
-      uint64_t* freed = is_k ? k_free : v_free;
-      uint64_t* full = is_k ? kvk_full : kvv_full;
-      uint8_t* slots = smem + (is_k ? kOffK : kOffV);
-      for (int t = 0; t < n_tiles; ++t) {
-        for (int part = 0, li = first_load(t); part < nk(t); ++part, ++li) {
-          const int sl = li & 1;
-          if (li >= 2) mbar_wait(&freed[sl], static_cast<uint32_t>((li - 2) >> 1) & 1u);
-          if (lane == 0) mark((is_k ? 1536 : 1792) + li);  // (slot free)
-          tma_tile(t, part, is_k, slots + sl * kKVTile, &full[sl]);
-          __syncwarp();
-          if (lane == 0) mark((is_k ? 1024 : 1280) + li);  // (issued)
+      named_sync(1, kSmThr);  // (red[] and last_flag reused by the next piece)
+      if (tid == 0 && pi < 3) mark(1 + pi);
+    }
+  } else if (warp == 8) {
+    // ================================================ MMA issue
+    // the whole warp runs the loop (warp-uniform operands stay in uniform
+    // registers); one elected lane issues the MMAs and commits
+    const uint64_t dk0 = sdesc(sbase + kOffK, 16, 1024);
+    const uint64_t dv0 = sdesc(sbase + kOffV, kKT * 128, 1024);
+    int i = 0, lk = 0, lv = 0;  // tile counter; next K / V load to consume
+    int prev_i = -1, prev_nk = 0;
+    auto do_pv = [&](int u, int nku) {  // P.V(u): its V loads in order, into the fresh delta
+      mbar_wait(p_full, static_cast<uint32_t>(u) & 1u);  // P(u) written (and delta(u - 1) folded)
+      for (int pv = 0; pv < nku; ++pv, ++lv) {
+        const int vs = lv & 1;
+        mbar_wait(&kvv_full[vs], static_cast<uint32_t>(lv >> 1) & 1u);
+        tmem_fence_after_sync();
+        if (elect_one()) {
+          issue_pv(sp_tmem + (u & 1) * kSP, dv0 + vs * (kKVTile >> 4), o_tmem, pv, pv == 0);
+          umma_commit(&v_free[vs]);
+          if (pv == nku - 1) umma_commit(&pv_done[u & 1]);
         }
+        __syncwarp();
+      }
+    };
+    for (int pi = 0; pi < wk.n; ++pi) {
+      const TcPiece pc = wk.pc[pi];
+      for (int t = pc.t0; t < pc.t1; ++t, ++i) {
+        if (t == pc.t0) {
+          // a new piece: the previous piece's last P.V first (its softmax
+          // finishes with it and then stages this piece's Q)
+          if (prev_i >= 0) {
+            do_pv(prev_i, prev_nk);
+            prev_i = -1;
+          }
+          mbar_wait(q_ready, static_cast<uint32_t>(pi) & 1u);
+          tmem_fence_after_sync();
+        }
+        // QK(i): its K loads in order, accumulated into S[i % 2] (S[b] =
+        // P(i - 2): its P.V was issued before this QK; the tensor core runs
+        // them in order)
+        const int b = i & 1, nkt = nk(t);
+        for (int pk = 0; pk < nkt; ++pk, ++lk) {
+          const int ks = lk & 1;
+          mbar_wait(&kvk_full[ks], static_cast<uint32_t>(lk >> 1) & 1u);  // this K load landed
+          tmem_fence_after_sync();
+          if (elect_one()) {
+            issue_qk(q_tmem, dk0 + ks * (kKVTile >> 4), sp_tmem + b * kSP, pk, pk == 0);
+            umma_commit(&k_free[ks]);
+            if (pk == nkt - 1) umma_commit(&s_full[b]);
+          }
+          __syncwarp();
+        }
+        if (prev_i >= 0) do_pv(prev_i, prev_nk);
+        prev_i = i;
+        prev_nk = nkt;
       }
     }
+    if (prev_i >= 0) do_pv(prev_i, prev_nk);
+  } else {
+    // ================================================ TMA producers
+    // warp 9 streams the K loads, warp 10 the V loads, each into its slot
+    // once the MMAs that read the slot's previous load completed. (The
+    // streams are independent: a tile's last K part is needed before the
+    // P.V that frees a V slot of the same tile.)
+    const bool is_k = warp == 9;
+    uint64_t* freed = is_k ? k_free : v_free;
+    uint64_t* full = is_k ? kvk_full : kvv_full;
+    uint8_t* slots = smem + (is_k ? kOffK : kOffV);
+    int li = 0;
+    for (int pi = 0; pi < wk.n; ++pi) {
+      const TcPiece pc = wk.pc[pi];
+      for (int t = pc.t0; t < pc.t1; ++t)
+        for (int part = 0; part < nk(t); ++part, ++li) {
+          const int sl = li & 1;
+          if (li >= 2) mbar_wait(&freed[sl], static_cast<uint32_t>((li - 2) >> 1) & 1u);
+          tma_tile(pc.g, t, part, is_k, slots + sl * kKVTile, &full[sl]);
+        }
+    }
   }
-  __syncthreads();
-  tmem_fence_after_sync();
-  stamp(3);
-  // ---- epilogue: O_run / l -> out row (i_row, head g + hm * H_kv), each
-  // softmax thread its half of the d columns; l = the two halves' sums
-  if (is_sm) red[half * kM + m] = l_run;
-  __syncthreads();
-  if (is_sm) {
-    const float l = l_run + red[(half ^ 1) * kM + m];
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    const bool live = row_ok;  // (rows past the chunk and padding rows are not stored)
-    float* orow = p.out + static_cast<size_t>(live ? i_row : 0) * p.H * kD + static_cast<size_t>(g + (live ? hm : 0) * p.H_kv) * kD +
-                  half * (kD / 2);
-    if (live)
-#pragma unroll
-      for (int u = 0; u < kD / 2; u += 4)
-        *reinterpret_cast<float4*>(orow + u) = make_float4(orun[u] * inv, orun[u + 1] * inv, orun[u + 2] * inv, orun[u + 3] * inv);
-  }
-  stamp(4);
   tmem_fence_before_sync();
   __syncthreads();
   if (warp == 0) {
     tmem_fence_after_sync();
     tmem_dealloc(tbase, 512);
   }
+  if (tid == 0) mark(7);
 }
 
 // Before the attention kernel, one launch: (1) the chunk's fp32 K and V split
 // exactly into three bf16 parts ([3][C][H_kv * d] each), (2) the attended
 // cached rows (init U selected U local, through the page table) gathered
 // into contiguous [n_att_max][H_kv * d] copies, a warp per row, zeros from
-// the attended count to the next 64-row tile boundary -- so every K/V tile
+// the attended count to n_att_max -- so every K/V tile
 // of the attention kernel is two plain TMA boxes (a row gather per tile,
 // TMA gather4 or cp.async, issues an order of magnitude slower).
 __global__ void prep_tc_kernel(PrefillAttendParams p, uint16_t* __restrict__ kc3, uint16_t* __restrict__ vc3,
-                               uint16_t* __restrict__ kg, uint16_t* __restrict__ vg) {
+                               uint16_t* __restrict__ kg, uint16_t* __restrict__ vg, unsigned* __restrict__ cnt,
+                               int n_units) {
   const int n = p.C * p.H_kv * kD;
   const int stride = gridDim.x * blockDim.x;
+  if (blockIdx.x == 0)
+    for (int u = threadIdx.x; u < n_units; u += blockDim.x) cnt[u] = 0u;  // the split units' piece counters
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n; i += stride) {
     const bool v = i >= n;
     const int j = v ? i - n : i;
@@ -583,7 +678,9 @@ __global__ void prep_tc_kernel(PrefillAttendParams p, uint16_t* __restrict__ kc3
   } else {
     n_cached = p.n_att_ptr ? *p.n_att_ptr : p.n_att;
   }
-  const int n_rows = min(p.n_att_max, (n_cached + kKT - 1) / kKT * kKT);
+  // rows past the attended count, up to the planned bound, are zeros (the
+  // attention kernel's tile grid follows the bound)
+  const int n_rows = p.n_att_max;
   const int row_vec = p.H_kv * kD / 8;  // 16-byte vectors per row
   const int lane = threadIdx.x & 31;
   for (int key = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; key < n_rows; key += stride >> 5) {
@@ -647,6 +744,150 @@ struct MapCache {
 
 }  // namespace
 
+namespace {
+
+// The work plan of one launch shape (host; cached with its device copy).
+struct TcPlan {
+  int grid = 0, nct = 0, n_units = 0, n_slots = 0;
+  std::vector<TcWork> work;
+  std::vector<int16_t> slot0, np;
+  void* dev = nullptr;  // [work | slot0 | np]
+};
+
+// Equal-cost contiguous ranges of the units' concatenated tiles (KV-head
+// major, so neighbouring pieces share K/V columns), one per SM. A chunk tile
+// costs ~2.2 cached tiles (three K and three V parts; measured 3.6 vs 1.6 us).
+// Falls back to one unit per CTA (no split) when a CTA would need more than
+// kMaxPieces pieces or TS_PREFILL_NO_SPLIT is set.
+TcPlan make_tc_plan(int C, int H, int H_kv, int n_att_max, int n_sms) {
+  const int G = H / H_kv, rph = kM / G;
+  const int nx = (C + rph - 1) / rph;
+  TcPlan pl;
+  pl.nct = (n_att_max + kKT - 1) / kKT;
+  pl.n_units = nx * H_kv;
+  auto tiles = [&](int x) { return pl.nct + (min(C, (x + 1) * rph) + kKT - 1) / kKT; };
+  auto cost = [&](int t) { return t < pl.nct ? 10L : 22L; };
+  long W = 0;
+  for (int x = 0; x < nx; ++x)
+    for (int t = 0; t < tiles(x); ++t) W += H_kv * cost(t);
+  auto unsplit = [&]() {
+    pl.grid = pl.n_units;
+    pl.n_slots = 0;
+    pl.work.assign(pl.grid, TcWork{});
+    pl.slot0.assign(pl.n_units, -1);
+    pl.np.assign(pl.n_units, 1);
+    for (int g = 0; g < H_kv; ++g)
+      for (int x = 0; x < nx; ++x) {
+        const int u = g * nx + x;
+        TcWork& w = pl.work[u];
+        w.n = 1;
+        w.pc[0] = TcPiece{static_cast<int16_t>(x), static_cast<int16_t>(g), 0, static_cast<int16_t>(tiles(x)), -1,
+                          static_cast<int16_t>(u)};
+      }
+  };
+  static const bool no_split = std::getenv("TS_PREFILL_NO_SPLIT") != nullptr;
+  if (no_split || pl.n_units >= n_sms || pl.nct + nx > 30000) {
+    unsplit();
+    return pl;
+  }
+  pl.grid = n_sms;
+  pl.work.assign(pl.grid, TcWork{});
+  std::vector<int> pieces(pl.n_units, 0);
+  int c = 0;
+  long acc = 0;
+  // no sliver pieces: a piece costs a pipeline drain and refill (and a merge
+  // when its unit is split), so a unit that would start with less than kSliver
+  // of a CTA's budget left starts on the next CTA, and a unit within kSliver
+  // of its end is finished where it is
+  constexpr long kSliver = 60;  // (6 cached tiles)
+  for (int g = 0; g < H_kv; ++g)
+    for (int x = 0; x < nx; ++x) {
+      const int u = g * nx + x;
+      long rem = 0;
+      for (int t = 0; t < tiles(x); ++t) rem += cost(t);
+      if (c < pl.grid - 1 && pl.work[c].n > 0 && W * (c + 1) / pl.grid - acc < kSliver) ++c;
+      for (int t = 0; t < tiles(x); ++t) {
+        if (acc >= W * (c + 1) / pl.grid && c < pl.grid - 1 && rem > kSliver) ++c;
+        rem -= cost(t);
+        TcWork& w = pl.work[c];
+        if (w.n == 0 || w.pc[w.n - 1].unit != u) {
+          if (w.n == kMaxPieces) {
+            unsplit();
+            return pl;
+          }
+          w.pc[w.n++] = TcPiece{static_cast<int16_t>(x), static_cast<int16_t>(g), static_cast<int16_t>(t),
+                                static_cast<int16_t>(t + 1), -1, static_cast<int16_t>(u)};
+          ++pieces[u];
+        } else {
+          w.pc[w.n - 1].t1 = static_cast<int16_t>(t + 1);
+        }
+        acc += cost(t);
+      }
+    }
+  pl.slot0.assign(pl.n_units, -1);
+  pl.np.assign(pl.n_units, 1);
+  std::vector<int> next(pl.n_units, 0);
+  for (int u = 0; u < pl.n_units; ++u)
+    if (pieces[u] > 1) {
+      pl.slot0[u] = static_cast<int16_t>(pl.n_slots);
+      pl.np[u] = static_cast<int16_t>(pieces[u]);
+      pl.n_slots += pieces[u];
+    }
+  for (TcWork& w : pl.work)  // CTA order = each unit's piece order
+    for (int k = 0; k < w.n; ++k) {
+      TcPiece& pc = w.pc[k];
+      if (pieces[pc.unit] > 1) pc.slot = static_cast<int16_t>(pl.slot0[pc.unit] + next[pc.unit]++);
+    }
+  return pl;
+}
+
+struct PlanCache {
+  std::mutex mu;
+  int key[5] = {-1, -1, -1, -1, -1};
+  TcPlan plan;
+};
+
+// the cached plan of this shape (re-planned and re-uploaded when it changes)
+const TcPlan& tc_plan(const PrefillAttendParams& p, cudaStream_t st, cudaError_t* err) {
+  static PlanCache pc;
+  static int n_sms = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  std::lock_guard<std::mutex> lk(pc.mu);
+  const int key[5] = {p.C, p.H, p.H_kv, p.n_att_max, n_sms};
+  *err = cudaSuccess;
+  if (std::equal(key, key + 5, pc.key)) return pc.plan;
+  if (pc.plan.dev) {
+    cudaFree(pc.plan.dev);  // (synchronises the device: no launch still reads it)
+    pc.plan.dev = nullptr;
+  }
+  pc.plan = make_tc_plan(p.C, p.H, p.H_kv, p.n_att_max, n_sms);
+  const size_t wb = pc.plan.work.size() * sizeof(TcWork), ub = pc.plan.n_units * sizeof(int16_t);
+  std::vector<uint8_t> h(wb + 2 * ub);
+  std::memcpy(h.data(), pc.plan.work.data(), wb);
+  std::memcpy(h.data() + wb, pc.plan.slot0.data(), ub);
+  std::memcpy(h.data() + wb + ub, pc.plan.np.data(), ub);
+  if ((*err = cudaMalloc(&pc.plan.dev, h.size())) != cudaSuccess) return pc.plan;
+  if ((*err = cudaMemcpy(pc.plan.dev, h.data(), h.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return pc.plan;
+  std::copy(key, key + 5, pc.key);
+  (void)st;
+  return pc.plan;
+}
+
+size_t tc_split_bytes(const TcPlan& pl) {
+  return (static_cast<size_t>(pl.n_slots) * kM * (kD + 2) * 4 + static_cast<size_t>(pl.n_units) * 4 + 255) / 256 * 256;
+}
+
+}  // namespace
+
+size_t prefill_tc_extra_ws_bytes(const PrefillAttendParams& p, cudaStream_t st) {
+  cudaError_t e;
+  const TcPlan& pl = tc_plan(p, st, &e);
+  return e == cudaSuccess ? tc_split_bytes(pl) : 0;
+}
+
 cudaError_t launch_prefill_tc(const PrefillAttendParams& p, cudaStream_t st) {
   const int G = p.H / p.H_kv;
   if (p.d != kD || p.H % p.H_kv != 0 || G < 1 || G > 16 || p.page_size < 1 || !p.split_ws || p.n_att_max < 0)
@@ -663,6 +904,20 @@ cudaError_t launch_prefill_tc(const PrefillAttendParams& p, cudaStream_t st) {
   uint16_t* vc3 = kc3 + 3 * n;
   uint16_t* kg = vc3 + 3 * n;
   uint16_t* vg = kg + static_cast<size_t>(p.n_att_max) * width;
+  cudaError_t perr;
+  const TcPlan& pl = tc_plan(p, st, &perr);
+  if (perr != cudaSuccess) return perr;
+  // the split units' partials and piece counters, after the gathered rows
+  uint8_t* xs = reinterpret_cast<uint8_t*>(vg + static_cast<size_t>(p.n_att_max) * width);
+  xs = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(xs) + 255) & ~static_cast<uintptr_t>(255));
+  TcSplit sp{};
+  sp.work = static_cast<const TcWork*>(pl.dev);
+  sp.unit_slot0 = reinterpret_cast<const int16_t*>(static_cast<const uint8_t*>(pl.dev) + pl.work.size() * sizeof(TcWork));
+  sp.unit_np = sp.unit_slot0 + pl.n_units;
+  sp.part_o = reinterpret_cast<float*>(xs);
+  sp.part_ml = sp.part_o + static_cast<size_t>(pl.n_slots) * kM * kD;
+  sp.cnt = reinterpret_cast<unsigned*>(sp.part_ml + static_cast<size_t>(pl.n_slots) * kM * 2);
+  sp.nct = pl.nct;
   const size_t g_rows = std::max(p.n_att_max, 1);
   static MapCache mc;
   alignas(64) CUtensorMap tkg, tvg, tkc, tvc;
@@ -677,10 +932,8 @@ cudaError_t launch_prefill_tc(const PrefillAttendParams& p, cudaStream_t st) {
     }
     tkg = mc.tkg, tvg = mc.tvg, tkc = mc.tkc, tvc = mc.tvc;
   }
-  prep_tc_kernel<<<2 * 148, 512, 0, st>>>(p, kc3, vc3, kg, vg);
-  const int rph = kM / G;
-  dim3 grid((p.C + rph - 1) / rph, p.H_kv);
-  prefill_tc_kernel<<<grid, kThr, kSmem, st>>>(p, tkg, tvg, tkc, tvc);
+  prep_tc_kernel<<<2 * 148, 512, 0, st>>>(p, kc3, vc3, kg, vg, sp.cnt, pl.n_units);
+  prefill_tc_kernel<<<pl.grid, kThr, kSmem, st>>>(p, sp, tkg, tvg, tkc, tvc);
   return cudaGetLastError();
 }
 
