@@ -250,6 +250,7 @@ struct Plan {
   size_t smem;
   const void* fn;
   const void* fn_lean;  // the single-sequence decode-step specialisation (nullptr: none)
+  const void* fn_lean_sel;  // its select-only twin (select_for_chunk)
   // the LEAN kernel's layout: S in tensor memory, the rest of smem to the ring
   bool lean_ok;
   int lean_ring_bytes, lean_att_bytes;
@@ -274,9 +275,10 @@ Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows, bool 
   const DeviceInfo& di = device_info();
   Plan pl{};
   const tsb::ScanGeom g = tsb::scan_geom(H, H_kv, d);
-  pl.fn = tsb::decode_kernel_ptr(d, H / H_kv, g.fast != 0, false);
-  pl.fn_lean = pl.fn ? tsb::decode_kernel_ptr(d, H / H_kv, g.fast != 0, true) : nullptr;
-  if (!pl.fn) pl.fn = tsb::decode_kernel_ptr(0, 0, false, false);
+  pl.fn = tsb::decode_kernel_ptr(d, H / H_kv, g.fast != 0, 0);
+  pl.fn_lean = pl.fn ? tsb::decode_kernel_ptr(d, H / H_kv, g.fast != 0, 1) : nullptr;
+  pl.fn_lean_sel = pl.fn ? tsb::decode_kernel_ptr(d, H / H_kv, g.fast != 0, 2) : nullptr;
+  if (!pl.fn) pl.fn = tsb::decode_kernel_ptr(0, 0, false, 0);
   const int base = std::max(max_T, att_rows);
   int c = (base + 63) / 64;
   c = std::max(1, std::min(c, std::max(1, di.num_sms / n_seq)));
@@ -287,6 +289,7 @@ Plan make_plan(int H, int H_kv, int d, int n_seq, int max_T, int att_rows, bool 
   // dynamic shared memory left next to the kernel's static allocation
   size_t stat = static_smem(pl.fn);
   if (pl.fn_lean) stat = std::max(stat, static_smem(pl.fn_lean));
+  if (pl.fn_lean_sel) stat = std::max(stat, static_smem(pl.fn_lean_sel));
   const size_t optin = static_cast<size_t>(di.smem_optin) - stat;
   tsb::SmemLayout L = tsb::smem_layout(H, row_bytes, pl.tpc, 1);
   if (L.total <= optin && !g_force_global_s && !force_spill) {
@@ -324,11 +327,14 @@ void launch_decode(DecodeParams& p, const Plan& pl, Workspace& ws, cudaStream_t 
   // the engine's plain single-sequence step runs the specialisation with the
   // other modes compiled out and S in tensor memory (decode.cu, LEAN)
   const tsb::SeqDesc& s0 = p.seqs[0];
-  const bool lean = pl.lean_ok && !g_no_lean && !g_force_global_s && p.n_seq == 1 && p.method == 2 &&
-                    p.mode == (tsb::kModeSelect | tsb::kModeScore | tsb::kModeCache | tsb::kModeAttend | tsb::kModeAppend) &&
-                    !s0.att_list && !s0.no_cur && s0.shard_base == 0 && !s0.cand && s0.sel_rows && !s0.ml_out &&
-                    (p.page_size & (p.page_size - 1)) == 0;
-  const void* fn = lean ? pl.fn_lean : pl.fn;
+  const bool lean_shape = pl.lean_ok && !g_no_lean && !g_force_global_s && p.n_seq == 1 && p.method == 2 &&
+                          !s0.att_list && !s0.no_cur && s0.shard_base == 0 && !s0.cand && s0.sel_rows && !s0.ml_out &&
+                          !s0.s_out && (p.page_size & (p.page_size - 1)) == 0;
+  const bool lean_step = lean_shape && p.mode == (tsb::kModeSelect | tsb::kModeScore | tsb::kModeCache | tsb::kModeAttend |
+                                                  tsb::kModeAppend);
+  const bool lean_sel = lean_shape && pl.fn_lean_sel && p.mode == (tsb::kModeSelect | tsb::kModeScore);
+  const bool lean = lean_step || lean_sel;
+  const void* fn = lean_step ? pl.fn_lean : lean_sel ? pl.fn_lean_sel : pl.fn;
   const size_t smem = lean ? pl.lean_smem : pl.smem;
   const double tq0 = g_host_prof ? now_ns() : 0.0;
   ws.prepare(n_ctas, p.H, p.H_kv, p.d, pl.tpc, lean ? 1 : pl.s_in_smem, p.n_seq, st);
@@ -647,7 +653,7 @@ struct ts_engine {
   DevBuf trace;
   bool trace_on = false;
   // prefill scratch
-  DevBuf p_qmean, p_sel, p_crit, p_state, p_att, p_natt, p_bad, p_q, p_k, p_v, p_out, p_split, p_trace;
+  DevBuf p_qmean, p_sel, p_crit, p_selrows, p_state, p_att, p_natt, p_bad, p_q, p_k, p_v, p_out, p_split, p_trace;
 
   ~ts_engine() {
     if (h_q) cudaFreeHost(h_q);
@@ -1758,6 +1764,7 @@ void prefill_impl(ts_engine* e, size_t seq, const float* q, const float* k, cons
         sd.cache = pstate;
         sd.sel = psel;
         sd.sel_crit = static_cast<float*>(e->p_crit.ensure(kk * 4));
+        sd.sel_rows = static_cast<int32_t*>(e->p_selrows.ensure(kk * 4));  // (the LEAN select-only kernel publishes them)
         const Plan pl = make_plan(H, Hkv, d, 1, static_cast<int>(T), 1, false);
         if (c.selection_method == TS_HEAD_VOTE) {
           float* S = e->ws.vote_scores(1, H, static_cast<int>(T));

@@ -310,6 +310,7 @@ constexpr int kScratchTmem = 250;  // sm.scratch word holding the TMEM base addr
 constexpr int kScratchStageMode = 200;  // sm.scratch words [200, 216): the scan ring's per-slot layout
 constexpr size_t kCritPartOffset = 64 * 1024;  // TMEM mode: per-kv-head criticality partials in the ring
 constexpr int kLeanMode = kModeSelect | kModeScore | kModeCache | kModeAttend | kModeAppend;
+constexpr int kLeanSelMode = kModeSelect | kModeScore;  // select_for_chunk's launch (prefill)
 // Fast path (sm_100a tensor cores, mma.sync bf16 -> fp32). The K rows of a
 // stage (16 tokens, padded stride so ldmatrix is bank-conflict free) are the
 // M x K operand; the query, exactly split into three bf16 parts
@@ -1416,13 +1417,14 @@ __device__ __noinline__ void softmax_partials(float* Sbuf, int sstride, int nloc
 // constants, so the instantiation carries no code for the other modes: the
 // one-shot phases run from a cold instruction cache, and their code size and
 // branch count are their latency.
-template <int D, int G, bool FAST, bool LEAN>
+template <int D, int G, bool FAST, int LM>
 __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeParams p) {
+  constexpr bool LEAN = LM != 0;  // LM: the specialisation's fixed mode (kLeanMode / kLeanSelMode), 0: p.mode
   extern __shared__ __align__(1024) uint8_t smem_raw[];  // TMA 128B-swizzle atoms (checked: else row copies)
   const Smem sm = carve(smem_raw, p);
   const int cta = blockIdx.x;
   const int nblocks = gridDim.x;
-  const int pmode = LEAN ? kLeanMode : p.mode;
+  const int pmode = LEAN ? LM : p.mode;
   const int n_seq = LEAN ? 1 : p.n_seq;
   const int s_in_smem = LEAN ? kSTmem : p.s_in_smem;
   const int method = LEAN ? 2 : p.method;
@@ -2351,10 +2353,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
 
 }  // namespace
 
-const void* decode_kernel_ptr(int D, int G, bool fast, bool lean) {
-#define TSB_K(d, g) \
-  return lean ? reinterpret_cast<const void*>(&decode_kernel<d, g, true, true>) \
-              : reinterpret_cast<const void*>(&decode_kernel<d, g, true, false>)
+const void* decode_kernel_ptr(int D, int G, bool fast, int variant) {
+#define TSB_K(d, g)                                                                                 \
+  return variant == 1   ? reinterpret_cast<const void*>(&decode_kernel<d, g, true, kLeanMode>)     \
+         : variant == 2 ? reinterpret_cast<const void*>(&decode_kernel<d, g, true, kLeanSelMode>)  \
+                        : reinterpret_cast<const void*>(&decode_kernel<d, g, true, 0>)
   if (fast) {
     if (D == 128) {
       switch (G) {
@@ -2376,8 +2379,8 @@ const void* decode_kernel_ptr(int D, int G, bool fast, bool lean) {
     return nullptr;
   }
 #undef TSB_K
-  if (lean) return nullptr;  // the LEAN specialisation exists for the tensor-core path only
-  return reinterpret_cast<const void*>(&decode_kernel<0, 0, false, false>);
+  if (variant) return nullptr;  // the LEAN specialisations exist for the tensor-core path only
+  return reinterpret_cast<const void*>(&decode_kernel<0, 0, false, 0>);
 }
 
 }  // namespace tsb

@@ -132,6 +132,8 @@ TSB_HD inline AttSplit att_split(int H_kv, int ctas_per_seq) {
   return a;
 }
 
-const void* decode_kernel_ptr(int D, int G, bool fast, bool lean);
+// variant 0: the general kernel; 1: LEAN, the engine's single-sequence decode
+// step; 2: LEAN select-only (select_for_chunk)
+const void* decode_kernel_ptr(int D, int G, bool fast, int variant);
 
 }  // namespace tsb
