@@ -2,7 +2,7 @@
 # Round-2 evidence run: full -m gpu suite, smoke, every bench workload, the
 # reference arm, the ncu launch list of the default bench command, ncu --set
 # full of the decode kernel (miss + hit) and of the prefill kernel, phase traces.
-O=gpurun_out/final2
+O=${O:-gpurun_out/final3}
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log; tail -2 $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log; tail -1 $O/smoke.log
