@@ -178,6 +178,15 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// named barrier that also ORs a predicate over its participants
+__device__ __forceinline__ bool bar_red_or(int id, int n, bool v) {
+  uint32_t r;
+  asm volatile("{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %3, 0;\n\tbarrier.cta.red.or.pred q, %1, %2, p;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+               : "=r"(r)
+               : "r"(id), "r"(n), "r"(v ? 1u : 0u)
+               : "memory");
+  return r != 0;
+}
 
 // TMA: one 64 x 64 box at (col, row) -> 8 KB at dst
 __device__ __forceinline__ void tma_tile2d(void* dst, const CUtensorMap* tm, int col, int row, uint64_t* bar) {
@@ -214,6 +223,7 @@ struct TcSplit {
   float* part_ml;            // [slots][128 rows][2]: log2 reference max, row sum
   unsigned* cnt;             // [units] pieces finished (zeroed by prep_tc_kernel)
   int nct;                   // cached tiles per unit (planned from n_att_max)
+  int fold;                  // fold the P.V delta into O every `fold` tiles (1 or 2; see the softmax loop)
 };
 
 // Warp roles (cached tiles and the chunk's own tiles alike, over the CTA's
@@ -258,6 +268,7 @@ __global__ void __launch_bounds__(kThr, 1)
   uint64_t* v_free = bars + 13;   // [2] the MMAs reading a V slot completed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 128);
   int* last_flag = reinterpret_cast<int*>(smem + kOffBar + 136);
+  volatile int* fresh_flag = reinterpret_cast<volatile int*>(smem + kOffBar + 144);  // [2] P.V(t) starts a fresh delta
   float* red = reinterpret_cast<float*>(smem + kOffRed);  // [2][2][kM]
   // dev trace (TS_PREFILL_TRACE): %globaltimer at the CTA's start, each
   // piece's end and the CTA's end -> trace[cta * 8 + slot]
@@ -356,7 +367,7 @@ __global__ void __launch_bounds__(kThr, 1)
       }
     };
     // (1) this thread's 32 scores of the tile -> s[], own max -> red[rb][half][m]
-    auto sm_load = [&](uint32_t s_addr, int k0, bool chunk, int rb) {
+    auto sm_load = [&](uint32_t s_addr, int k0, bool chunk, int rb) -> bool {
       const int lim = chunk ? min(n_cur - 1, i_row) + 1 : n_cached;  // visible keys: [0, lim)
       const int kb0 = k0 + half * KH;
       tmem_ld32(s_addr + lane_sel + half * KH, s);
@@ -367,7 +378,9 @@ __global__ void __launch_bounds__(kThr, 1)
         s[u] = u < nv ? s[u] * sl2 : -INFINITY;  // log2-domain logits
         mx[u & 3] = fmaxf(mx[u & 3], s[u]);
       }
-      red[(rb * 2 + half) * kM + m] = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      const float mh = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      red[(rb * 2 + half) * kM + m] = mh;
+      return mh > m_ref + 8.f;  // (the row moves its reference iff either half says so)
     };
     // (2) after the max exchange: lazy reference max (moved only when the max
     // grows by > 8), P = 2^(s - m_ref) split into three bf16 parts -> P[rb] in
@@ -440,7 +453,8 @@ __global__ void __launch_bounds__(kThr, 1)
       tmem_fence_before_sync();
       mbar_arrive(q_ready);
     };
-    int i = 0;  // the CTA's tile counter
+    int i = 0;    // the CTA's tile counter
+    int unf = 0;  // tiles whose P.V the delta holds unfolded
     if (wk.n > 0) stage_q(wk.pc[0]);
     for (int pi = 0; pi < wk.n; ++pi) {
       const TcPiece pc = wk.pc[pi];
@@ -457,14 +471,29 @@ __global__ void __launch_bounds__(kThr, 1)
         const bool chunk = t >= nct;
         mbar_wait(&s_full[b], static_cast<uint32_t>(i >> 1) & 1u);  // QK(i) done
         tmem_fence_after_sync();
-        sm_load(sp_tmem + b * kSP, chunk ? (t - nct) * kKT : t * kKT, chunk, b);
-        named_sync(1, kSmThr);  // row maxima exchanged; every thread's S[b] loads done (P goes over them)
+        const bool need = sm_load(sp_tmem + b * kSP, chunk ? (t - nct) * kKT : t * kKT, chunk, b);
+        // row maxima exchanged (every thread's S[b] loads done: P goes over
+        // them), and whether any row of the CTA moves its reference max
+        const bool any_need = bar_red_or(1, kSmThr, need);
         const float corr = sm_p(b);
-        if (t > pc.t0) {  // P.V(i - 1) completed: its delta into O_run
-          mbar_wait(&pv_done[(i - 1) & 1], static_cast<uint32_t>((i - 1) >> 1) & 1u);
-          tmem_fence_after_sync();
-          fold(corr);
+        // the delta holds the P.V of the `unf` tiles since the last fold; it
+        // is folded every kFold tiles, and before any reference move (its
+        // tiles and P(t) would otherwise mix two references)
+        bool fresh = true;
+        if (t > pc.t0) {
+          if (unf >= sp.fold || any_need) {  // P.V(i - 1) completed: the delta into O_run
+            mbar_wait(&pv_done[(i - 1) & 1], static_cast<uint32_t>((i - 1) >> 1) & 1u);
+            tmem_fence_after_sync();
+            fold(corr);
+            unf = 1;
+          } else {
+            fresh = false;  // P.V(t) accumulates onto the delta
+            ++unf;
+          }
+        } else {
+          unf = 1;
         }
+        if (tid == 0) fresh_flag[b] = fresh ? 1 : 0;
         tmem_wait_st();  // P stored
         tmem_fence_before_sync();
         mbar_arrive(p_full);
@@ -541,13 +570,14 @@ __global__ void __launch_bounds__(kThr, 1)
     int i = 0, lk = 0, lv = 0;  // tile counter; next K / V load to consume
     int prev_i = -1, prev_nk = 0;
     auto do_pv = [&](int u, int nku) {  // P.V(u): its V loads in order, into the fresh delta
-      mbar_wait(p_full, static_cast<uint32_t>(u) & 1u);  // P(u) written (and delta(u - 1) folded)
+      mbar_wait(p_full, static_cast<uint32_t>(u) & 1u);  // P(u) written (and the delta folded, or kept)
+      const bool fresh = fresh_flag[u & 1] != 0;
       for (int pv = 0; pv < nku; ++pv, ++lv) {
         const int vs = lv & 1;
         mbar_wait(&kvv_full[vs], static_cast<uint32_t>(lv >> 1) & 1u);
         tmem_fence_after_sync();
         if (elect_one()) {
-          issue_pv(sp_tmem + (u & 1) * kSP, dv0 + vs * (kKVTile >> 4), o_tmem, pv, pv == 0);
+          issue_pv(sp_tmem + (u & 1) * kSP, dv0 + vs * (kKVTile >> 4), o_tmem, pv, fresh && pv == 0);
           umma_commit(&v_free[vs]);
           if (pv == nku - 1) umma_commit(&pv_done[u & 1]);
         }
@@ -918,6 +948,10 @@ cudaError_t launch_prefill_tc(const PrefillAttendParams& p, cudaStream_t st) {
   sp.part_ml = sp.part_o + static_cast<size_t>(pl.n_slots) * kM * kD;
   sp.cnt = reinterpret_cast<unsigned*>(sp.part_ml + static_cast<size_t>(pl.n_slots) * kM * 2);
   sp.nct = pl.nct;
+  static const int fold_every = std::getenv("TS_PREFILL_FOLD1") ? 1
+                               : std::getenv("TS_PREFILL_FOLD") ? std::max(1, std::atoi(std::getenv("TS_PREFILL_FOLD")))
+                                                                : 2;
+  sp.fold = fold_every;
   const size_t g_rows = std::max(p.n_att_max, 1);
   static MapCache mc;
   alignas(64) CUtensorMap tkg, tvg, tkc, tvc;
