@@ -37,6 +37,7 @@
 #include <cfloat>
 #include <cmath>
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -957,12 +958,14 @@ cudaError_t launch_prefill_tc(const PrefillAttendParams& p, cudaStream_t st) {
   alignas(64) CUtensorMap tkg, tvg, tkc, tvc;
   {
     std::lock_guard<std::mutex> lk(mc.mu);
-    if (mc.ws != kc3 || mc.c != static_cast<size_t>(p.C) || mc.width != width || mc.rows != g_rows) {
+    // (keyed on n_att_max itself: it also places vg, and a reallocated
+    // workspace can come back at the same address)
+    if (mc.ws != kc3 || mc.c != static_cast<size_t>(p.C) || mc.width != width || mc.rows != static_cast<size_t>(p.n_att_max)) {
       mc.ws = nullptr;
       if (!encode_2d(&mc.tkc, kc3, width, 3 * static_cast<size_t>(p.C)) || !encode_2d(&mc.tvc, vc3, width, 3 * static_cast<size_t>(p.C)) ||
           !encode_2d(&mc.tkg, kg, width, g_rows) || !encode_2d(&mc.tvg, vg, width, g_rows))
         return cudaErrorNotSupported;
-      mc.ws = kc3, mc.c = p.C, mc.width = width, mc.rows = g_rows;
+      mc.ws = kc3, mc.c = p.C, mc.width = width, mc.rows = static_cast<size_t>(p.n_att_max);
     }
     tkg = mc.tkg, tvg = mc.tvg, tkc = mc.tkc, tvc = mc.tvc;
   }
