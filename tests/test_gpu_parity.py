@@ -156,6 +156,27 @@ def test_sparse_attend_select_all_equals_full(sa, orc, C, d):
     assert np.abs(got - want).max() <= 1e-4
 
 
+@pytest.mark.parametrize("C,n,page,H,H_kv", [(100, 300, 4, 4, 2), (700, 1000, 4, 32, 8), (37, 513, 2, 28, 4)])
+def test_sparse_attend_paged_tc_equals_full(sa, orc, C, n, page, H, H_kv):
+    """The tcgen05 C-row attention over a paged pool with shuffled frames
+    (prep_tc_kernel gathers through the page table) and several work pieces:
+    select-all equals full attention (attention.cpp:114-123 -> :54-112)."""
+    d = 128
+    k = bf16_round(rng_normal(41, (n, H_kv * d)))
+    v = bf16_round(rng_normal(42, (n, H_kv * d)))
+    q = rng_normal(43, (C, H * d))
+    kc = rng_normal(44, (C, H_kv * d))
+    vc = rng_normal(45, (C, H_kv * d))
+    pool = sa.PagedKvPool(n + 4 * page, page, H_kv, d)
+    pool.shuffle_free_frames(7)
+    seq = pool.create_sequence()
+    pool.append_kv(seq, k, v)
+    got = sa.sparse_attend(q, kc, vc, pool, seq, selected=list(range(n)), num_heads=H)
+    want = orc.sdpa_full(q, np.vstack([k, kc]), np.vstack([v, vc]), H)
+    assert rel_fro(got, want) <= 1e-5, rel_fro(got, want)
+    assert np.abs(got - want).max() <= 1e-4
+
+
 def test_sparse_attend_empty_windows(sa):
     pool = sa.PagedKvPool(8, 1, 1, 4)
     seq = pool.create_sequence()
