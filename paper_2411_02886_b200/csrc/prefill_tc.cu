@@ -37,9 +37,11 @@
 #include <cfloat>
 #include <cmath>
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -872,13 +874,16 @@ TcPlan make_tc_plan(int C, int H, int H_kv, int n_att_max, int n_sms) {
   return pl;
 }
 
+// Plans by shape, kept for the process's lifetime: a plan depends on the
+// cached tiles (ceil(n_att_max / 64)), not on n_att_max itself, so a growing
+// context makes a few dozen at most; entries never move or free, so a
+// concurrent launch from another thread never sees its plan released.
 struct PlanCache {
   std::mutex mu;
-  int key[5] = {-1, -1, -1, -1, -1};
-  TcPlan plan;
+  std::map<std::array<int, 5>, TcPlan> plans;
 };
 
-// the cached plan of this shape (re-planned and re-uploaded when it changes)
+// the cached plan of this shape (made and uploaded on first use)
 const TcPlan& tc_plan(const PrefillAttendParams& p, cudaStream_t st, cudaError_t* err) {
   static PlanCache pc;
   static int n_sms = [] {
@@ -886,25 +891,27 @@ const TcPlan& tc_plan(const PrefillAttendParams& p, cudaStream_t st, cudaError_t
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n;
   }();
-  std::lock_guard<std::mutex> lk(pc.mu);
-  const int key[5] = {p.C, p.H, p.H_kv, p.n_att_max, n_sms};
-  *err = cudaSuccess;
-  if (std::equal(key, key + 5, pc.key)) return pc.plan;
-  if (pc.plan.dev) {
-    cudaFree(pc.plan.dev);  // (synchronises the device: no launch still reads it)
-    pc.plan.dev = nullptr;
-  }
-  pc.plan = make_tc_plan(p.C, p.H, p.H_kv, p.n_att_max, n_sms);
-  const size_t wb = pc.plan.work.size() * sizeof(TcWork), ub = pc.plan.n_units * sizeof(int16_t);
-  std::vector<uint8_t> h(wb + 2 * ub);
-  std::memcpy(h.data(), pc.plan.work.data(), wb);
-  std::memcpy(h.data() + wb, pc.plan.slot0.data(), ub);
-  std::memcpy(h.data() + wb + ub, pc.plan.np.data(), ub);
-  if ((*err = cudaMalloc(&pc.plan.dev, h.size())) != cudaSuccess) return pc.plan;
-  if ((*err = cudaMemcpy(pc.plan.dev, h.data(), h.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return pc.plan;
-  std::copy(key, key + 5, pc.key);
   (void)st;
-  return pc.plan;
+  std::lock_guard<std::mutex> lk(pc.mu);
+  const std::array<int, 5> key = {p.C, p.H, p.H_kv, (p.n_att_max + kKT - 1) / kKT, n_sms};
+  *err = cudaSuccess;
+  auto it = pc.plans.find(key);
+  if (it != pc.plans.end() && it->second.dev) return it->second;
+  TcPlan& pl = pc.plans[key];
+  pl = make_tc_plan(p.C, p.H, p.H_kv, p.n_att_max, n_sms);
+  const size_t wb = pl.work.size() * sizeof(TcWork), ub = pl.n_units * sizeof(int16_t);
+  std::vector<uint8_t> h(wb + 2 * ub);
+  std::memcpy(h.data(), pl.work.data(), wb);
+  std::memcpy(h.data() + wb, pl.slot0.data(), ub);
+  std::memcpy(h.data() + wb + ub, pl.np.data(), ub);
+  void* d = nullptr;
+  if ((*err = cudaMalloc(&d, h.size())) != cudaSuccess) return pl;
+  if ((*err = cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice)) != cudaSuccess) {
+    cudaFree(d);
+    return pl;
+  }
+  pl.dev = d;
+  return pl;
 }
 
 size_t tc_split_bytes(const TcPlan& pl) {
