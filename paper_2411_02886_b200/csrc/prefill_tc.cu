@@ -181,6 +181,10 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// programmatic dependent launch: the attention kernel starts (TMEM, barriers,
+// its Q) while prep_tc_kernel finishes, and waits here for prep's results
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 // named barrier that also ORs a predicate over its participants
 __device__ __forceinline__ bool bar_red_or(int id, int n, bool v) {
   uint32_t r;
@@ -256,7 +260,7 @@ __global__ void __launch_bounds__(kThr, 1)
   const int G = p.H / p.H_kv;
   const int rows_per_head = kM / G;  // chunk rows per unit
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int n_cached = p.n_att_ptr ? *p.n_att_ptr : p.n_att;  // (<= nct * 64)
+  int n_cached = 0;  // (<= nct * 64; read after the programmatic-launch wait)
   const int nct = sp.nct;
   const TcWork wk = sp.work[blockIdx.x];
   const uint32_t sbase = smem_u32(smem);
@@ -458,7 +462,9 @@ __global__ void __launch_bounds__(kThr, 1)
     };
     int i = 0;    // the CTA's tile counter
     int unf = 0;  // tiles whose P.V the delta holds unfolded
-    if (wk.n > 0) stage_q(wk.pc[0]);
+    if (wk.n > 0) stage_q(wk.pc[0]);  // (the query is an input: before prep_tc_kernel's results)
+    grid_dep_wait();
+    n_cached = p.n_att_ptr ? *p.n_att_ptr : p.n_att;
     for (int pi = 0; pi < wk.n; ++pi) {
       const TcPiece pc = wk.pc[pi];
       const int g = pc.g, i0 = pc.x * rows_per_head;
@@ -565,6 +571,7 @@ __global__ void __launch_bounds__(kThr, 1)
       if (tid == 0 && pi < 3) mark(1 + pi);
     }
   } else if (warp == 8) {
+    grid_dep_wait();
     // ================================================ MMA issue
     // the whole warp runs the loop (warp-uniform operands stay in uniform
     // registers); one elected lane issues the MMAs and commits
@@ -627,6 +634,7 @@ __global__ void __launch_bounds__(kThr, 1)
     // once the MMAs that read the slot's previous load completed. (The
     // streams are independent: a tile's last K part is needed before the
     // P.V that frees a V slot of the same tile.)
+    grid_dep_wait();  // (the tiles come from prep_tc_kernel's copies)
     const bool is_k = warp == 9;
     uint64_t* freed = is_k ? k_free : v_free;
     uint64_t* full = is_k ? kvk_full : kvv_full;
@@ -663,6 +671,7 @@ __global__ void prep_tc_kernel(PrefillAttendParams p, uint16_t* __restrict__ kc3
                                int n_units) {
   const int n = p.C * p.H_kv * kD;
   const int stride = gridDim.x * blockDim.x;
+  grid_dep_launch();  // (the attention kernel waits for this grid's completion before reading its results)
   if (blockIdx.x == 0)
     for (int u = threadIdx.x; u < n_units; u += blockDim.x) cnt[u] = 0u;  // the split units' piece counters
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n; i += stride) {
@@ -977,7 +986,19 @@ cudaError_t launch_prefill_tc(const PrefillAttendParams& p, cudaStream_t st) {
     tkg = mc.tkg, tvg = mc.tvg, tkc = mc.tkc, tvc = mc.tvc;
   }
   prep_tc_kernel<<<2 * 148, 512, 0, st>>>(p, kc3, vc3, kg, vg, sp.cnt, pl.n_units);
-  prefill_tc_kernel<<<pl.grid, kThr, kSmem, st>>>(p, sp, tkg, tvg, tkc, tvc);
+  static const bool no_pdl = std::getenv("TS_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pl.grid);
+  cfg.blockDim = dim3(kThr);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t le = cudaLaunchKernelEx(&cfg, prefill_tc_kernel, p, sp, tkg, tvg, tkc, tvc);
+  if (le != cudaSuccess) return le;
   return cudaGetLastError();
 }
 
