@@ -654,8 +654,15 @@ struct ts_engine {
   bool trace_on = false;
   // prefill scratch
   DevBuf p_qmean, p_sel, p_crit, p_selrows, p_state, p_att, p_natt, p_bad, p_q, p_k, p_v, p_out, p_split, p_trace;
+  // host-buffer prefill: the chunk's K/V copies run on their own stream,
+  // behind the query's, while the selection (which needs only the query) runs
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_q = nullptr, ev_kv = nullptr;
 
   ~ts_engine() {
+    if (ev_q) cudaEventDestroy(ev_q);
+    if (ev_kv) cudaEventDestroy(ev_kv);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (h_q) cudaFreeHost(h_q);
     if (h_k) cudaFreeHost(h_k);
     if (h_v) cudaFreeHost(h_v);
@@ -1729,14 +1736,30 @@ void prefill_impl(ts_engine* e, size_t seq, const float* q, const float* k, cons
         qc = static_cast<float*>(e->p_q.ensure(len * W * 4));
         ck(cudaMemcpyAsync(const_cast<float*>(qc), q + begin * W, len * W * 4, cudaMemcpyHostToDevice, st), "H2D");
       }
+      // host K/V: copied on the engine's copy stream once the query's copy
+      // (and everything before it on the stream, e.g. the previous chunk's
+      // reads of these buffers) is done, overlapping the selection launches
+      const bool kv_side = !k_dev || !v_dev;
+      if (kv_side) {
+        if (!e->copy_stream) {
+          ck(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking), "stream");
+          ck(cudaEventCreateWithFlags(&e->ev_q, cudaEventDisableTiming), "event");
+          ck(cudaEventCreateWithFlags(&e->ev_kv, cudaEventDisableTiming), "event");
+        }
+        ck(cudaEventRecord(e->ev_q, st), "event");
+        ck(cudaStreamWaitEvent(e->copy_stream, e->ev_q, 0), "event");
+      }
       if (!k_dev) {
         kc = static_cast<float*>(e->p_k.ensure(len * KW * 4));
-        ck(cudaMemcpyAsync(const_cast<float*>(kc), k + begin * KW, len * KW * 4, cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(const_cast<float*>(kc), k + begin * KW, len * KW * 4, cudaMemcpyHostToDevice,
+                           e->copy_stream), "H2D");
       }
       if (!v_dev) {
         vc = static_cast<float*>(e->p_v.ensure(len * KW * 4));
-        ck(cudaMemcpyAsync(const_cast<float*>(vc), v + begin * KW, len * KW * 4, cudaMemcpyHostToDevice, st), "H2D");
+        ck(cudaMemcpyAsync(const_cast<float*>(vc), v + begin * KW, len * KW * 4, cudaMemcpyHostToDevice,
+                           e->copy_stream), "H2D");
       }
+      if (kv_side) ck(cudaEventRecord(e->ev_kv, e->copy_stream), "event");
       ts_pool::Seq& s = pool.state(sid);
       const size_t cached = s.len;
       uint32_t* psel = static_cast<uint32_t*>(e->p_sel.ensure(kk * 4));
@@ -1780,6 +1803,7 @@ void prefill_impl(ts_engine* e, size_t seq, const float* q, const float* k, cons
           launch_decode(p, pl, e->ws, st);
         }
       }
+      if (kv_side) ck(cudaStreamWaitEvent(st, e->ev_kv, 0), "event");  // (the attention reads the chunk's K/V)
       // windows (make_windows) -> device merged list
       const int init_end = static_cast<int>(std::min(c.n_init, cached));
       const int local_begin = static_cast<int>(cached - std::min(c.n_local, cached));

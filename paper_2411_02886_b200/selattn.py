@@ -328,7 +328,11 @@ class Engine:
         va = _Arg(v_bits, np.uint16, 2)
         check(lib.ts_engine_append_bf16(self._h, seq, ka.ptr, va.ptr, ka.shape[0]))
 
-    def prefill(self, q, k, v, seq=0, trace=False):
+    def prefill(self, q, k, v, seq=0, trace=False, out=None):
+        """prefill (attention.cpp:135-170) -> output [n x H*d] (and the chunk
+        traces with trace=True). `out`: an optional preallocated float32
+        [n x H*d] array (host, e.g. a view of pinned memory, or a CUDA tensor)
+        the output is written into and returned."""
         qa = _Arg(q, np.float32, 2)
         ka = _Arg(k, np.float32, 2)
         va = _Arg(v, np.float32, 2)
@@ -337,7 +341,13 @@ class Engine:
             raise ValueError("prefill: empty input")
         if qa.shape[1] != self.model_dim or ka.shape[1] != self.kv_dim or ka.shape != va.shape or ka.shape[0] != n:
             raise ValueError("prefill: inconsistent input shapes")
-        o, op = _out(qa.shape, qa.cuda)
+        if out is None:
+            o, op = _out(qa.shape, qa.cuda)
+        else:
+            oa = _Arg(out, np.float32, 2)
+            if oa.shape != qa.shape or (isinstance(out, np.ndarray) and oa.obj is not out):
+                raise ValueError("prefill: out must be a contiguous float32 array shaped like q")
+            o, op = out, oa.ptr
         if not trace:
             check(lib.ts_engine_prefill(self._h, seq, qa.ptr, ka.ptr, va.ptr, n, op, None, None, 0))
             return o

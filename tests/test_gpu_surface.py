@@ -178,3 +178,34 @@ def test_prefill_async_matches_prefill(sa):
     assert len(a) == len(b) == n0 + n
     with pytest.raises(ValueError):
         b.prefill_async(torch.from_numpy(q), torch.from_numpy(k), torch.from_numpy(v), out)
+
+
+def test_prefill_pinned_host_buffers(sa):
+    """Host-buffer prefill over several chunks (the chunk K/V copies run on
+    the engine's copy stream, overlapping the selection): pinned and pageable
+    inputs, a caller-provided pinned output, all equal to the device-buffer
+    path; a wrongly shaped `out` is rejected."""
+    import torch
+
+    rng = np.random.default_rng(12)
+    H, H_kv, d, n0, n = 8, 2, 128, 3000, 700
+    kw = dict(k=256, n_local=64, n_init=16, chunk_size=256, num_heads=H, num_kv_heads=H_kv, head_dim=d, block_size=64)
+    k0 = bf16_round(rng.standard_normal((n0, H_kv * d), dtype=np.float32))
+    v0 = bf16_round(rng.standard_normal((n0, H_kv * d), dtype=np.float32))
+    q = rng.standard_normal((n, H * d), dtype=np.float32)
+    k = rng.standard_normal((n, H_kv * d), dtype=np.float32)
+    v = rng.standard_normal((n, H_kv * d), dtype=np.float32)
+    engines = [sa.Engine(n0 + n + 8, **kw) for _ in range(3)]
+    for e in engines:
+        e.append(k0, v0)
+    dev_out = torch.empty(n, H * d, device="cuda")
+    engines[0].prefill_async(torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), dev_out)
+    engines[0].sync()
+    want = dev_out.cpu().numpy()
+    pin = lambda x: torch.from_numpy(x).pin_memory().numpy()  # noqa: E731
+    out = torch.empty(n, H * d).pin_memory().numpy()
+    got = engines[1].prefill(pin(q), pin(k), pin(v), out=out)
+    assert got is out and np.array_equal(out, want)
+    assert np.array_equal(engines[2].prefill(q, k, v), want)
+    with pytest.raises(ValueError):
+        engines[2].prefill(q, k, v, out=np.empty((n, H * d + 1), np.float32))
