@@ -1705,24 +1705,72 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       float z0 = 0.f, z1 = 0.f;
       // eight stages per TMEM round trip (the loads' latency, not the math,
       // is this loop's cost)
+      if constexpr (G == 4) {
+        // four query heads per KV head: the lanes of heads 4..7 (lane & 2)
+        // hold no scores, so each takes the upper four stages of its partner
+        // lane (lane ^ 2) -- half the exponentials per lane -- and hands the
+        // results back for the store (the SFU issue, not the loads, bounds
+        // this loop)
+        const bool helper = (lane & 2) != 0;
+        const float pl0 = __shfl_xor_sync(0xffffffffu, ml0, 2), pl1 = __shfl_xor_sync(0xffffffffu, ml1, 2);
+        const float m0 = helper ? pl0 : ml0, m1 = helper ? pl1 : ml1;
 #pragma unroll 1
-      for (int r0 = 0; r0 < nr; r0 += 8) {
-        float v[32];
-        tmem_ld32(tw + static_cast<uint32_t>(r0 * 4), v);
+        for (int r0 = 0; r0 < nr; r0 += 8) {
+          float v[32];
+          tmem_ld32(tw + static_cast<uint32_t>(r0 * 4), v);
+          float u[16];  // owner: its stages 0..3; helper: the owner's stages 4..7
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int rbase = (ph + (r0 + q) * nph) * 16 + (lane >> 2);
+          for (int i = 0; i < 16; ++i) {
+            const float up = __shfl_xor_sync(0xffffffffu, v[16 + i], 2);
+            u[i] = helper ? up : v[i];
+          }
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int g = g0 + (e & 1), row = rbase + (e >> 1) * 8;
-            const bool ok = r0 + q < nr && g < G && row < nloc;
-            const float w = ok ? ex2_approx(fmaf(v[q * 4 + e], kLog2e, -((e & 1) ? ml1 : ml0))) : 0.f;
-            v[q * 4 + e] = w;
+          for (int i = 0; i < 16; ++i) {
+            const int q = (helper ? 4 : 0) + (i >> 2), e = i & 3;
+            const int row = (ph + (r0 + q) * nph) * 16 + (lane >> 2) + (e >> 1) * 8;
+            const bool ok = r0 + q < nr && row < nloc;
+            const float w = ok ? ex2_approx(fmaf(u[i], kLog2e, -((e & 1) ? m1 : m0))) : 0.f;
+            u[i] = w;
             if (e & 1) z1 += w;
             else z0 += w;
           }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float back = __shfl_xor_sync(0xffffffffu, u[i], 2);
+            v[i] = helper ? 0.f : u[i];
+            v[16 + i] = helper ? 0.f : back;
+          }
+          tmem_st32(tw + static_cast<uint32_t>(r0 * 4), v);
         }
-        tmem_st32(tw + static_cast<uint32_t>(r0 * 4), v);
+        // the helpers' sums belong to their owners' heads
+        const float hz0 = __shfl_xor_sync(0xffffffffu, z0, 2), hz1 = __shfl_xor_sync(0xffffffffu, z1, 2);
+        if (!helper) {
+          z0 += hz0;
+          z1 += hz1;
+        } else {
+          z0 = 0.f;
+          z1 = 0.f;
+        }
+      } else {
+#pragma unroll 1
+        for (int r0 = 0; r0 < nr; r0 += 8) {
+          float v[32];
+          tmem_ld32(tw + static_cast<uint32_t>(r0 * 4), v);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int rbase = (ph + (r0 + q) * nph) * 16 + (lane >> 2);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int g = g0 + (e & 1), row = rbase + (e >> 1) * 8;
+              const bool ok = r0 + q < nr && g < G && row < nloc;
+              const float w = ok ? ex2_approx(fmaf(v[q * 4 + e], kLog2e, -((e & 1) ? ml1 : ml0))) : 0.f;
+              v[q * 4 + e] = w;
+              if (e & 1) z1 += w;
+              else z0 += w;
+            }
+          }
+          tmem_st32(tw + static_cast<uint32_t>(r0 * 4), v);
+        }
       }
       tmem_wait_st();
 #pragma unroll

@@ -65,3 +65,11 @@ for mode, theta in (("miss", 2.0), ("hit", -2.0)):
         col = col[~np.isnan(col)]
         if col.size:
             print(f"  {i:2d} {nm:18s} {col.min():8.2f} {np.median(col):8.2f} {col.max():8.2f}  (n={col.size})")
+    # QT_DIFF="a,b,c": per-CTA differences of consecutive listed slots (median / max over CTAs, us)
+    if os.environ.get("QT_DIFF"):
+        sl = [int(x) for x in os.environ["QT_DIFF"].split(",")]
+        for x, y in zip(sl, sl[1:]):
+            dd = a[:, y] - a[:, x]
+            dd = dd[~np.isnan(dd)]
+            if dd.size:
+                print(f"  {mode} {names.get(x, x)} -> {names.get(y, y)}: median {np.median(dd):.2f} max {dd.max():.2f} us")
