@@ -43,6 +43,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "aux.h"
@@ -80,6 +81,12 @@ __device__ __forceinline__ void sp3(float x, float& h, float& m, float& l) {
   const float r = x - h;
   m = __uint_as_float(__float_as_uint(r) & 0xFFFF0000u);
   l = r - m;
+}
+// two floats -> round-to-nearest bf16 pair (a in the low half)
+__device__ __forceinline__ uint32_t bf2_rn(float a, float b) {
+  uint32_t w;
+  asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(w) : "f"(a), "f"(b));
+  return w;
 }
 // two bf16 values (fp32 with zero low halves) -> one packed word
 __device__ __forceinline__ uint32_t pk2(float lo, float hi) {
@@ -160,12 +167,12 @@ __device__ __forceinline__ void issue_qk(uint32_t q_tmem, uint64_t dk, uint32_t 
 
 // delta (+)= P parts x V (V part pv): A = P in tensor memory (two bf16 per
 // 32-bit column, 32 columns per part), B = V as MN-major (d contiguous per key)
-__device__ __forceinline__ void issue_pv(uint32_t p_tmem, uint64_t dv, uint32_t o_tmem, int pv, bool first) {
+__device__ __forceinline__ void issue_pv(uint32_t p_tmem, uint64_t dv, uint32_t o_tmem, int pv, bool first, bool p3) {
   constexpr uint32_t id = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (static_cast<uint32_t>(kD >> 3) << 17) |
                           (static_cast<uint32_t>(kM >> 4) << 24);
 #pragma unroll
   for (int pp = 0; pp < 3; ++pp) {
-    if (pp == 2 && pv != 0) break;
+    if (pp == 2 && (pv != 0 || !p3)) break;
 #pragma unroll
     for (int kk = 0; kk < kKT / 16; ++kk) {
       const uint32_t vo = (kk * 2048) >> 4;  // 16 keys = two 8-key groups of 1024 B
@@ -231,6 +238,7 @@ struct TcSplit {
   unsigned* cnt;             // [units] pieces finished (zeroed by prep_tc_kernel)
   int nct;                   // cached tiles per unit (planned from n_att_max)
   int fold;                  // fold the P.V delta into O every `fold` tiles (1 or 2; see the softmax loop)
+  int p3;                    // P in three truncated bf16 parts (1) or two rounded ones (0; see sm_p)
 };
 
 // Warp roles (cached tiles and the chunk's own tiles alike, over the CTA's
@@ -392,7 +400,12 @@ __global__ void __launch_bounds__(kThr, 1)
     // (2) after the max exchange: lazy reference max (moved only when the max
     // grows by > 8), P = 2^(s - m_ref) split into three bf16 parts -> P[rb] in
     // tensor memory; returns the factor that moves O and l to the new reference
-    auto sm_p = [&](int rb) -> float {
+    // P3: three truncated parts (exact to 24 bits); else two round-to-nearest
+    // parts, hi = rn(p), mid = rn(p - hi): |error| <= 2^-17 p, unbiased,
+    // which keeps the output within the 1e-5 relative-Frobenius bar with a
+    // third of the P.V products and of the P stores saved
+    auto sm_p = [&](int rb, auto p3tag) -> float {
+      constexpr bool P3 = decltype(p3tag)::value;
       const float mt = fmaxf(red[(rb * 2 + half) * kM + m], red[(rb * 2 + (half ^ 1)) * kM + m]);
       float corr = 1.f;
       if (mt > m_ref + 8.f) {
@@ -408,18 +421,24 @@ __global__ void __launch_bounds__(kThr, 1)
         const float p0 = ex2_approx(s[2 * c] - mu);
         const float p1 = ex2_approx(s[2 * c + 1] - mu);
         ls[c & 3] += p0 + p1;
-        float h0, m0, l0, h1, m1, l1;
-        sp3(p0, h0, m0, l0);
-        sp3(p1, h1, m1, l1);
-        hw[c] = __uint_as_float(pk2(h0, h1));
-        mw[c] = __uint_as_float(pk2(m0, m1));
-        lw[c] = __uint_as_float(pk2(l0, l1));
+        if constexpr (P3) {
+          float h0, m0, l0, h1, m1, l1;
+          sp3(p0, h0, m0, l0);
+          sp3(p1, h1, m1, l1);
+          hw[c] = __uint_as_float(pk2(h0, h1));
+          mw[c] = __uint_as_float(pk2(m0, m1));
+          lw[c] = __uint_as_float(pk2(l0, l1));
+        } else {
+          const uint32_t h = bf2_rn(p0, p1);
+          hw[c] = __uint_as_float(h);
+          mw[c] = __uint_as_float(bf2_rn(p0 - __uint_as_float(h << 16), p1 - __uint_as_float(h & 0xFFFF0000u)));
+        }
       }
       l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
       const uint32_t pa = sp_tmem + rb * kSP + lane_sel + half * (KH / 2);
       tmem_st16(pa, hw);
       tmem_st16(pa + kKT / 2, mw);
-      tmem_st16(pa + kKT, lw);
+      if constexpr (P3) tmem_st16(pa + kKT, lw);
       return corr;
     };
     // ---- a unit's Q -> tensor memory: thread (row m, half) splits its 64 d
@@ -484,7 +503,7 @@ __global__ void __launch_bounds__(kThr, 1)
         // row maxima exchanged (every thread's S[b] loads done: P goes over
         // them), and whether any row of the CTA moves its reference max
         const bool any_need = bar_red_or(1, kSmThr, need);
-        const float corr = sm_p(b);
+        const float corr = sp.p3 ? sm_p(b, std::true_type{}) : sm_p(b, std::false_type{});
         // the delta holds the P.V of the `unf` tiles since the last fold; it
         // is folded every kFold tiles, and before any reference move (its
         // tiles and P(t) would otherwise mix two references)
@@ -587,7 +606,7 @@ __global__ void __launch_bounds__(kThr, 1)
         mbar_wait(&kvv_full[vs], static_cast<uint32_t>(lv >> 1) & 1u);
         tmem_fence_after_sync();
         if (elect_one()) {
-          issue_pv(sp_tmem + (u & 1) * kSP, dv0 + vs * (kKVTile >> 4), o_tmem, pv, fresh && pv == 0);
+          issue_pv(sp_tmem + (u & 1) * kSP, dv0 + vs * (kKVTile >> 4), o_tmem, pv, fresh && pv == 0, sp.p3 != 0);
           umma_commit(&v_free[vs]);
           if (pv == nku - 1) umma_commit(&pv_done[u & 1]);
         }
@@ -969,6 +988,8 @@ cudaError_t launch_prefill_tc(const PrefillAttendParams& p, cudaStream_t st) {
                                : std::getenv("TS_PREFILL_FOLD") ? std::max(1, std::atoi(std::getenv("TS_PREFILL_FOLD")))
                                                                 : 2;
   sp.fold = fold_every;
+  static const bool p3 = std::getenv("TS_PREFILL_P3") != nullptr;  // (A/B: the exact three-part P)
+  sp.p3 = p3 ? 1 : 0;
   const size_t g_rows = std::max(p.n_att_max, 1);
   static MapCache mc;
   alignas(64) CUtensorMap tkg, tvg, tkc, tvc;
