@@ -357,11 +357,17 @@ __global__ void __launch_bounds__(kThr, 1)
     // O_run = (O_run + delta) * c
     auto fold = [&](float c) {
       float a[32];
+      const bool moved = __any_sync(0xffffffffu, c != 1.f);  // (rare: a reference move in the warp's rows)
 #pragma unroll
       for (int q = 0; q < kD / 64; ++q) {
         tmem_ld32(o_tmem + lane_sel + half * (kD / 2) + q * 32, a);
+        if (moved) {
 #pragma unroll
-        for (int u = 0; u < 32; ++u) orun[q * 32 + u] = (orun[q * 32 + u] + a[u]) * c;
+          for (int u = 0; u < 32; ++u) orun[q * 32 + u] = (orun[q * 32 + u] + a[u]) * c;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 32; ++u) orun[q * 32 + u] += a[u];
+        }
       }
     };
     // the normalised rows -> out, through shared memory so that a warp stores
@@ -388,12 +394,15 @@ __global__ void __launch_bounds__(kThr, 1)
       tmem_ld32(s_addr + lane_sel + half * KH, s);
       float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
       const int nv = row_ok ? lim - kb0 : 0;  // visible keys among this thread's 32
+      // raw scores (the log2-domain scale sl2 > 0 is applied in sm_p's FMA);
+      // keys past the visible limit -> -inf (only a boundary tile has them)
+      if (__any_sync(0xffffffffu, nv < KH)) {
 #pragma unroll
-      for (int u = 0; u < KH; ++u) {
-        s[u] = u < nv ? s[u] * sl2 : -INFINITY;  // log2-domain logits
-        mx[u & 3] = fmaxf(mx[u & 3], s[u]);
+        for (int u = 0; u < KH; ++u) s[u] = u < nv ? s[u] : -INFINITY;
       }
-      const float mh = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+#pragma unroll
+      for (int u = 0; u < KH; ++u) mx[u & 3] = fmaxf(mx[u & 3], s[u]);
+      const float mh = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * sl2;  // log2-domain max
       red[(rb * 2 + half) * kM + m] = mh;
       return mh > m_ref + 8.f;  // (the row moves its reference iff either half says so)
     };
@@ -418,8 +427,8 @@ __global__ void __launch_bounds__(kThr, 1)
       const float mu = m_ref == -INFINITY ? 0.f : m_ref;  // (a row with no visible key yet: every p = 2^-inf = 0)
 #pragma unroll
       for (int c = 0; c < KH / 2; ++c) {
-        const float p0 = ex2_approx(s[2 * c] - mu);
-        const float p1 = ex2_approx(s[2 * c + 1] - mu);
+        const float p0 = ex2_approx(fmaf(s[2 * c], sl2, -mu));
+        const float p1 = ex2_approx(fmaf(s[2 * c + 1], sl2, -mu));
         ls[c & 3] += p0 + p1;
         if constexpr (P3) {
           float h0, m0, l0, h1, m1, l1;
