@@ -699,33 +699,43 @@ __global__ void prep_tc_kernel(PrefillAttendParams p, uint16_t* __restrict__ kc3
                                int n_units) {
   const int n = p.C * p.H_kv * kD;
   const int stride = gridDim.x * blockDim.x;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   grid_dep_launch();  // (the attention kernel waits for this grid's completion before reading its results)
   if (blockIdx.x == 0)
     for (int u = threadIdx.x; u < n_units; u += blockDim.x) cnt[u] = 0u;  // the split units' piece counters
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n; i += stride) {
-    const bool v = i >= n;
-    const int j = v ? i - n : i;
-    float h, m, l;
-    sp3(v ? p.v_cur[j] : p.k_cur[j], h, m, l);
-    uint16_t* out = v ? vc3 : kc3;
-    out[j] = static_cast<uint16_t>(__float_as_uint(h) >> 16);
-    out[n + j] = static_cast<uint16_t>(__float_as_uint(m) >> 16);
-    out[2 * static_cast<size_t>(n) + j] = static_cast<uint16_t>(__float_as_uint(l) >> 16);
-  }
-  // the attended list: explicit (p.att), or the implicit windows around the
-  // selection -- its split points by counting (one pass over the selection
-  // per CTA, one L2 round trip; a binary search is a chain of them)
-  int n_cached, ie = 0, lb = 0, lo1 = 0, n1 = 0;
+  // (1) the attended list: explicit (p.att), or the implicit windows around
+  // the selection -- its split points by counting (one pass over the
+  // selection per CTA: one L2 round trip, overlapping (2); a binary search is
+  // a chain of them)
+  int ie = 0, lb = 0, c_ie = 0, c_lb = 0;
   if (p.win_n_att) {
     const int n_sel = p.win_sel && p.win_n_sel ? *p.win_n_sel : 0;
     ie = p.win_init_end;
     lb = max(p.win_local_begin, ie);
-    int c_ie = 0, c_lb = 0;
     for (int i = threadIdx.x; i < n_sel; i += blockDim.x) {
       const uint32_t t = __ldcg(p.win_sel + i);
       c_ie += t < static_cast<uint32_t>(ie);
       c_lb += t < static_cast<uint32_t>(p.win_local_begin);
     }
+  }
+  // (2) the chunk's K / V -> three exact bf16 parts, four elements per thread
+  const int n4 = n >> 2;  // (n: a multiple of kD)
+  for (int i = gtid; i < 2 * n4; i += stride) {
+    const bool v = i >= n4;
+    const int j = v ? i - n4 : i;
+    const float4 x = __ldg(reinterpret_cast<const float4*>(v ? p.v_cur : p.k_cur) + j);
+    float h[4], m[4], l[4];
+    sp3(x.x, h[0], m[0], l[0]);
+    sp3(x.y, h[1], m[1], l[1]);
+    sp3(x.z, h[2], m[2], l[2]);
+    sp3(x.w, h[3], m[3], l[3]);
+    uint2* out = reinterpret_cast<uint2*>(v ? vc3 : kc3);
+    out[j] = make_uint2(pk2(h[0], h[1]), pk2(h[2], h[3]));
+    out[n4 + j] = make_uint2(pk2(m[0], m[1]), pk2(m[2], m[3]));
+    out[2 * n4 + j] = make_uint2(pk2(l[0], l[1]), pk2(l[2], l[3]));
+  }
+  int n_cached, lo1 = 0, n1 = 0;
+  if (p.win_n_att) {
     __shared__ int red[2][32];
     for (int o = 16; o > 0; o >>= 1) {
       c_ie += __shfl_xor_sync(0xffffffffu, c_ie, o);
@@ -748,12 +758,15 @@ __global__ void prep_tc_kernel(PrefillAttendParams p, uint16_t* __restrict__ kc3
   } else {
     n_cached = p.n_att_ptr ? *p.n_att_ptr : p.n_att;
   }
-  // rows past the attended count, up to the planned bound, are zeros (the
-  // attention kernel's tile grid follows the bound)
+  // (3) the attended rows, gathered: a warp per row, all of a lane's loads
+  // in flight before its stores. Rows past the attended count, up to the
+  // planned bound, are zeros (the attention kernel's tile grid follows the
+  // bound)
+  constexpr int kPerLane = 4;  // 16-byte vectors per lane and pass (a whole row for H_kv <= 8)
   const int n_rows = p.n_att_max;
   const int row_vec = p.H_kv * kD / 8;  // 16-byte vectors per row
   const int lane = threadIdx.x & 31;
-  for (int key = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; key < n_rows; key += stride >> 5) {
+  for (int key = gtid >> 5; key < n_rows; key += stride >> 5) {
     uint4* kd = reinterpret_cast<uint4*>(kg + static_cast<size_t>(key) * row_vec * 8);
     uint4* vd = reinterpret_cast<uint4*>(vg + static_cast<size_t>(key) * row_vec * 8);
     if (key < n_cached) {
@@ -765,9 +778,24 @@ __global__ void prep_tc_kernel(PrefillAttendParams p, uint16_t* __restrict__ kc3
                                           : p.page_table[tok / p.page_size] * p.page_size + static_cast<int32_t>(tok % p.page_size);
       const uint4* ks = reinterpret_cast<const uint4*>(p.k_slab + static_cast<size_t>(ri) * row_vec * 8);
       const uint4* vs = reinterpret_cast<const uint4*>(p.v_slab + static_cast<size_t>(ri) * row_vec * 8);
-      for (int c = lane; c < row_vec; c += 32) {
-        kd[c] = __ldg(ks + c);
-        vd[c] = __ldg(vs + c);
+      for (int c0 = 0; c0 < row_vec; c0 += 32 * kPerLane) {
+        uint4 kb[kPerLane], vb[kPerLane];
+#pragma unroll
+        for (int u = 0; u < kPerLane; ++u) {
+          const int c = c0 + lane + 32 * u;
+          if (c < row_vec) {
+            kb[u] = __ldg(ks + c);
+            vb[u] = __ldg(vs + c);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kPerLane; ++u) {
+          const int c = c0 + lane + 32 * u;
+          if (c < row_vec) {
+            kd[c] = kb[u];
+            vd[c] = vb[u];
+          }
+        }
       }
     } else {
       for (int c = lane; c < row_vec; c += 32) kd[c] = vd[c] = make_uint4(0u, 0u, 0u, 0u);
