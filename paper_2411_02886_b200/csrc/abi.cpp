@@ -571,14 +571,17 @@ struct ts_pool {
 
   // sync = false: the caller's later work on `st` is stream-ordered after
   // the append (the engine's prefill); the public pool API stays synchronous.
+  // reserved: the caller ran reserve(t) already (the engine's prefill, so
+  // that the append launch follows the attention directly: pdl, a
+  // programmatic launch after it)
   void append(uint32_t id, const void* k, const void* v, size_t t, bool bf16, size_t* first,
-              size_t* last, cudaStream_t st, bool sync = true) {
+              size_t* last, cudaStream_t st, bool sync = true, bool reserved = false, bool pdl = false) {
     Seq& s = state(id);
     const size_t f = s.len;
     if (first) *first = f;
     if (last) *last = f + t;
     if (t == 0) return;
-    reserve(s, t, st);  // rows come from the page table on the device (no host round trip)
+    if (!reserved) reserve(s, t, st);  // rows come from the page table on the device (no host round trip)
     const size_t n = t * row;
     if (bf16) {
       const uint16_t* kd = dev_in(static_cast<const uint16_t*>(k), n, st_b, st);
@@ -592,7 +595,7 @@ struct ts_pool {
       const float* vd = dev_in(static_cast<const float*>(v), n, st_c, st);
       ck(tsb::launch_kv_append(k_slab, v_slab, kd, vd, nullptr, nullptr, nullptr, static_cast<int>(t),
                                static_cast<int>(row), st, s.d_pt, static_cast<int64_t>(s.len),
-                               static_cast<int>(page_size)),
+                               static_cast<int>(page_size), pdl),
          "kv_append");
     }
     g_launches.fetch_add(1);
@@ -1762,6 +1765,9 @@ void prefill_impl(ts_engine* e, size_t seq, const float* q, const float* k, cons
       if (kv_side) ck(cudaEventRecord(e->ev_kv, e->copy_stream), "event");
       ts_pool::Seq& s = pool.state(sid);
       const size_t cached = s.len;
+      // the chunk's page-table entries now (capacity checked before any work
+      // of the chunk), so that its append can follow the attention directly
+      pool.reserve(s, len, st);
       uint32_t* psel = static_cast<uint32_t*>(e->p_sel.ensure(kk * 4));
       CacheState* pstate = static_cast<CacheState*>(e->p_state.ensure(sizeof(CacheState)));
       ck(cudaMemsetAsync(pstate, 0, sizeof(CacheState), st), "memset");
@@ -1876,7 +1882,8 @@ void prefill_impl(ts_engine* e, size_t seq, const float* q, const float* k, cons
         trace_off += ns;
       }
       // append the chunk after attending (attention.cpp:167)
-      pool.append(sid, kc, vc, len, false, nullptr, nullptr, st, false);
+      static const bool no_pdl = std::getenv("TS_NO_PDL") != nullptr;
+      pool.append(sid, kc, vc, len, false, nullptr, nullptr, st, false, true, !no_pdl && implicit);
     }
     if (sync) ck(cudaStreamSynchronize(st), "sync");
   }

@@ -37,6 +37,10 @@ __global__ void kv_append_kernel(uint16_t* k_slab, uint16_t* v_slab, const float
       v_slab[off] = vb[i];
     }
   }
+  // launched programmatically after the prefill attention (which reads none
+  // of these rows): done only once that grid is, so later work on the stream
+  // sees both complete (a no-op for an ordinary launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 __global__ void kv_gather_kernel(const uint16_t* k_slab, const uint16_t* v_slab, const int64_t* src_rows,
@@ -421,12 +425,24 @@ __global__ void shard_combine_kernel(const float* o_all, const float* ml_all, in
 
 cudaError_t launch_kv_append(uint16_t* k_slab, uint16_t* v_slab, const float* k, const float* v,
                              const uint16_t* kb, const uint16_t* vb, const int64_t* dst_rows, int t,
-                             int row, cudaStream_t st, const int32_t* pt, int64_t pos0, int page_size) {
+                             int row, cudaStream_t st, const int32_t* pt, int64_t pos0, int page_size, bool pdl) {
   if (t <= 0) return cudaSuccess;
   const int64_t total = static_cast<int64_t>(t) * row;
   const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-  kv_append_kernel<<<blocks, 256, 0, st>>>(k_slab, v_slab, k, v, kb, vb, dst_rows, pt, pos0, page_size, t, row);
-  return cudaGetLastError();
+  if (!pdl) {
+    kv_append_kernel<<<blocks, 256, 0, st>>>(k_slab, v_slab, k, v, kb, vb, dst_rows, pt, pos0, page_size, t, row);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kv_append_kernel, k_slab, v_slab, k, v, kb, vb, dst_rows, pt, pos0, page_size, t, row);
 }
 
 cudaError_t launch_kv_gather(const uint16_t* k_slab, const uint16_t* v_slab, const int64_t* src_rows,

@@ -38,7 +38,7 @@ struct PrefillAttendParams {
 cudaError_t launch_kv_append(uint16_t* k_slab, uint16_t* v_slab, const float* k, const float* v,
                              const uint16_t* kb, const uint16_t* vb, const int64_t* dst_rows, int t,
                              int row, cudaStream_t st,
-                             const int32_t* pt = nullptr, int64_t pos0 = 0, int page_size = 1);
+                             const int32_t* pt = nullptr, int64_t pos0 = 0, int page_size = 1, bool pdl = false);
 cudaError_t launch_kv_gather(const uint16_t* k_slab, const uint16_t* v_slab, const int64_t* src_rows,
                              int n, int row, float* k_out, float* v_out, cudaStream_t st);
 cudaError_t launch_chunk_mean(const float* q, int c, int width, float* out, cudaStream_t st);

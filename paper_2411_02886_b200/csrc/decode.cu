@@ -1436,6 +1436,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   const int width = H * p.d;
   const int tid = threadIdx.x;
   const bool do_select = (pmode & kModeSelect) != 0;
+  // a launch queued programmatically behind this one (the prefill's prep
+  // kernel after the selection launch) may be scheduled now; it waits for
+  // this grid's completion before reading anything it writes
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (FAST && tid < kMaxBarPairs) {
     mbar_init(&sm.full[tid], 1);

@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(kThr, 1)
                       const __grid_constant__ CUtensorMap tm_vg, const __grid_constant__ CUtensorMap tm_kc,
                       const __grid_constant__ CUtensorMap tm_vc) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  grid_dep_launch();  // (the chunk's append, launched after this grid, reads none of its inputs)
   const int G = p.H / p.H_kv;
   const int rows_per_head = kM / G;  // chunk rows per unit
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -703,22 +704,9 @@ __global__ void prep_tc_kernel(PrefillAttendParams p, uint16_t* __restrict__ kc3
   grid_dep_launch();  // (the attention kernel waits for this grid's completion before reading its results)
   if (blockIdx.x == 0)
     for (int u = threadIdx.x; u < n_units; u += blockDim.x) cnt[u] = 0u;  // the split units' piece counters
-  // (1) the attended list: explicit (p.att), or the implicit windows around
-  // the selection -- its split points by counting (one pass over the
-  // selection per CTA: one L2 round trip, overlapping (2); a binary search is
-  // a chain of them)
-  int ie = 0, lb = 0, c_ie = 0, c_lb = 0;
-  if (p.win_n_att) {
-    const int n_sel = p.win_sel && p.win_n_sel ? *p.win_n_sel : 0;
-    ie = p.win_init_end;
-    lb = max(p.win_local_begin, ie);
-    for (int i = threadIdx.x; i < n_sel; i += blockDim.x) {
-      const uint32_t t = __ldcg(p.win_sel + i);
-      c_ie += t < static_cast<uint32_t>(ie);
-      c_lb += t < static_cast<uint32_t>(p.win_local_begin);
-    }
-  }
-  // (2) the chunk's K / V -> three exact bf16 parts, four elements per thread
+  // (1) the chunk's K / V -> three exact bf16 parts, four elements per
+  // thread (an input: this runs while the selection launch before it ends,
+  // this kernel being launched programmatically after it)
   const int n4 = n >> 2;  // (n: a multiple of kD)
   for (int i = gtid; i < 2 * n4; i += stride) {
     const bool v = i >= n4;
@@ -733,6 +721,21 @@ __global__ void prep_tc_kernel(PrefillAttendParams p, uint16_t* __restrict__ kc3
     out[j] = make_uint2(pk2(h[0], h[1]), pk2(h[2], h[3]));
     out[n4 + j] = make_uint2(pk2(m[0], m[1]), pk2(m[2], m[3]));
     out[2 * n4 + j] = make_uint2(pk2(l[0], l[1]), pk2(l[2], l[3]));
+  }
+  grid_dep_wait();  // the selection (and its count) complete
+  // (2) the attended list: explicit (p.att), or the implicit windows around
+  // the selection -- its split points by counting (one pass over the
+  // selection per CTA: one L2 round trip; a binary search is a chain of them)
+  int ie = 0, lb = 0, c_ie = 0, c_lb = 0;
+  if (p.win_n_att) {
+    const int n_sel = p.win_sel && p.win_n_sel ? *p.win_n_sel : 0;
+    ie = p.win_init_end;
+    lb = max(p.win_local_begin, ie);
+    for (int i = threadIdx.x; i < n_sel; i += blockDim.x) {
+      const uint32_t t = __ldcg(p.win_sel + i);
+      c_ie += t < static_cast<uint32_t>(ie);
+      c_lb += t < static_cast<uint32_t>(p.win_local_begin);
+    }
   }
   int n_cached, lo1 = 0, n1 = 0;
   if (p.win_n_att) {
@@ -1043,8 +1046,22 @@ cudaError_t launch_prefill_tc(const PrefillAttendParams& p, cudaStream_t st) {
     }
     tkg = mc.tkg, tvg = mc.tvg, tkc = mc.tkc, tvc = mc.tvc;
   }
-  prep_tc_kernel<<<2 * 148, 512, 0, st>>>(p, kc3, vc3, kg, vg, sp.cnt, pl.n_units);
   static const bool no_pdl = std::getenv("TS_NO_PDL") != nullptr;
+  {
+    // programmatic launch after the selection launch (its chunk split
+    // overlaps the selection's end; it waits before reading the selection)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * 148);
+    cfg.blockDim = dim3(512);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t pe = cudaLaunchKernelEx(&cfg, prep_tc_kernel, p, kc3, vc3, kg, vg, sp.cnt, pl.n_units);
+    if (pe != cudaSuccess) return pe;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(pl.grid);
   cfg.blockDim = dim3(kThr);
