@@ -56,40 +56,49 @@ __global__ void kv_gather_kernel(const uint16_t* k_slab, const uint16_t* v_slab,
 }
 
 // Sequential fp64 column sums in row order: bit-identical to chunk_mean
-// (tensor.cpp:133-150). CTA = 32 columns; rows pass through shared memory in
-// tiles of 128, double-buffered: every thread issues its 16 loads of tile
-// t + 1 before warp 0 adds tile t's rows in order (one dependent fp64 add per
-// row and column -- the chain the reference's order imposes), so the loads'
-// latency hides behind the chain instead of adding to it.
-constexpr int kCmCols = 32, kCmTile = 128, kCmThr = 256;
+// (tensor.cpp:133-150). CTA = 16 columns (256 CTAs for a 4096-wide query);
+// rows pass through shared memory in tiles of 256 by cp.async, two tiles in
+// flight from the start (a 512-row chunk is loaded with one round trip), and
+// a half warp adds each landed tile's rows in order (one dependent fp64 add
+// per row and column -- the chain the reference's order imposes) while the
+// next tile lands.
+constexpr int kCmCols = 16, kCmTile = 256, kCmThr = 128;
 __global__ void __launch_bounds__(kCmThr) chunk_mean_kernel(const float* q, int c, int width, float* out) {
-  __shared__ float tile[2][kCmTile][kCmCols];
-  constexpr int kPer = kCmTile * kCmCols / kCmThr;  // loads per thread per tile (16)
-  const int col = threadIdx.x & (kCmCols - 1), rb = threadIdx.x / kCmCols;
-  const int j = blockIdx.x * kCmCols + col;
+  __shared__ __align__(16) float tile[2][kCmTile][kCmCols];
+  constexpr int kVec = kCmCols / 4;                       // 16-byte pieces per row
+  constexpr int kPer = kCmTile * kVec / kCmThr;           // pieces per thread per tile (8)
+  const int tid = threadIdx.x;
+  const int j0 = blockIdx.x * kCmCols;
   const int ntile = (c + kCmTile - 1) / kCmTile;
-  float v[kPer];
-  auto load = [&](int t) {
+  const bool vec = (width & 3) == 0;  // rows 16-byte aligned
+  auto issue = [&](int t) {
     const int r0 = t * kCmTile, nr = min(kCmTile, c - r0);
+    float* buf = &tile[t & 1][0][0];
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
-      const int r = rb + u * (kCmThr / kCmCols);
-      v[u] = (r < nr && j < width) ? __ldg(q + static_cast<size_t>(r0 + r) * width + j) : 0.f;
-    }
-  };
-  auto store = [&](int b) {
+      const int i = tid + u * kCmThr, r = i / kVec, cv = (i % kVec) * 4;
+      if (r >= nr) continue;
+      const float* src = q + static_cast<size_t>(r0 + r) * width + j0 + cv;
+      float* dst = buf + r * kCmCols + cv;
+      if (vec && j0 + cv + 4 <= width) {
+        cp_async16(dst, src);
+      } else {
 #pragma unroll
-    for (int u = 0; u < kPer; ++u) tile[b][rb + u * (kCmThr / kCmCols)][col] = v[u];
+        for (int e = 0; e < 4; ++e) dst[e] = j0 + cv + e < width ? __ldg(src + e) : 0.f;
+      }
+    }
+    cp_async_commit();
   };
+  issue(0);
+  if (ntile > 1) issue(1);
+  else cp_async_commit();  // (an empty group: the wait below counts two)
   double acc = 0.0;
-  load(0);
-  store(0);
-  __syncthreads();
   for (int t = 0; t < ntile; ++t) {
-    if (t + 1 < ntile) load(t + 1);  // in flight during the adds below
-    if (threadIdx.x < kCmCols) {
+    cp_async_wait<1>();  // tile t landed (tile t + 1 may still be in flight)
+    __syncthreads();
+    if (tid < kCmCols) {
       const int nr = min(kCmTile, c - t * kCmTile);
-      const float* tc = &tile[t & 1][0][col];
+      const float* tc = &tile[t & 1][0][tid];
       int r = 0;
       for (; r + 8 <= nr; r += 8) {  // (the loads and conversions of 8 rows ahead of the add chain)
         double x[8];
@@ -100,10 +109,12 @@ __global__ void __launch_bounds__(kCmThr) chunk_mean_kernel(const float* q, int 
       }
       for (; r < nr; ++r) acc += static_cast<double>(tc[r * kCmCols]);
     }
-    if (t + 1 < ntile) store((t + 1) & 1);
-    __syncthreads();
+    __syncthreads();  // (buffer t & 1 free)
+    if (t + 2 < ntile) issue(t + 2);
+    else cp_async_commit();
   }
-  if (threadIdx.x < kCmCols && j < width) out[j] = static_cast<float>(acc * (1.0 / static_cast<double>(c)));
+  const int j = j0 + tid;
+  if (tid < kCmCols && j < width) out[j] = static_cast<float>(acc * (1.0 / static_cast<double>(c)));
 }
 
 __global__ void max_index_kernel(const uint32_t* idx, int n, unsigned int* out) {

@@ -90,7 +90,7 @@ def test_cosine_vs_oracle(sa, orc):
         assert abs(sa.cosine(u, w) - orc.cosine(u, w)) <= 1e-12
 
 
-@pytest.mark.parametrize("c,w", [(1, 64), (7, 4096), (512, 4096)])
+@pytest.mark.parametrize("c,w", [(1, 64), (7, 4096), (512, 4096), (700, 4096), (300, 37), (257, 100)])
 def test_chunk_mean_vs_oracle(sa, orc, c, w):
     q = np.random.default_rng(c).standard_normal((c, w)).astype(np.float32)
     assert np.array_equal(sa.chunk_mean(q), orc.chunk_mean(q))
