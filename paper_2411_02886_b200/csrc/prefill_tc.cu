@@ -491,6 +491,16 @@ __global__ void __launch_bounds__(kThr, 1)
     };
     int i = 0;    // the CTA's tile counter
     int unf = 0;  // tiles whose P.V the delta holds unfolded
+    // a tile whose P.V completion was not waited for (the delta kept
+    // accumulating): observed before the next wait on the other buffer's
+    // barrier, so that with fold 2 every completion of pv_done is waited
+    // for in order (never more than one phase ahead)
+    int unwaited = -1;
+    auto wait_pv = [&](int u) {
+      if (unwaited >= 0 && unwaited == u - 1) mbar_wait(&pv_done[unwaited & 1], static_cast<uint32_t>(unwaited >> 1) & 1u);
+      unwaited = -1;
+      mbar_wait(&pv_done[u & 1], static_cast<uint32_t>(u >> 1) & 1u);
+    };
     if (wk.n > 0) stage_q(wk.pc[0]);  // (the query is an input: before prep_tc_kernel's results)
     grid_dep_wait();
     n_cached = p.n_att_ptr ? *p.n_att_ptr : p.n_att;
@@ -520,13 +530,14 @@ __global__ void __launch_bounds__(kThr, 1)
         bool fresh = true;
         if (t > pc.t0) {
           if (unf >= sp.fold || any_need) {  // P.V(i - 1) completed: the delta into O_run
-            mbar_wait(&pv_done[(i - 1) & 1], static_cast<uint32_t>((i - 1) >> 1) & 1u);
+            wait_pv(i - 1);
             tmem_fence_after_sync();
             fold(corr);
             unf = 1;
           } else {
             fresh = false;  // P.V(t) accumulates onto the delta
             ++unf;
+            unwaited = i - 1;
           }
         } else {
           unf = 1;
@@ -539,7 +550,7 @@ __global__ void __launch_bounds__(kThr, 1)
       }
       // the piece's last P.V
       if (tid == 0 && pi == 0) mark(4);
-      mbar_wait(&pv_done[(i - 1) & 1], static_cast<uint32_t>((i - 1) >> 1) & 1u);
+      wait_pv(i - 1);
       tmem_fence_after_sync();
       if (tid == 0 && pi == 0) mark(3);
       fold(1.f);
