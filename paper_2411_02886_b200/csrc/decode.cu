@@ -1934,24 +1934,43 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
       mbar_wait(sm.aux, aux_phase);
       aux_phase ^= 1u;
       trace_pt(p, 13);
-      // M_h = max_c m_c, Z_h = sum_c z_c e^(m_c - M_h): 16 threads per head
+      // M_h = max_c m_c, Z_h = sum_c z_c e^(m_c - M_h): 16 threads per head,
+      // a thread's partials (c = sub, sub + 16, ...) loaded together
       const int sub = tid & 15;
+      constexpr int kPerS = kMaxPrefix / 16;
       for (int h0 = 0; h0 < H; h0 += blockDim.x >> 4) {  // warp-uniform trip count
         const int h = h0 + (tid >> 4);
         const bool hv = h < H;
-        float M = -INFINITY;
-        if (hv)
-          #pragma unroll 1
-          for (int c = sub; c < nc; c += 16) M = fmaxf(M, pm[h * ncp + c]);
+        float M = -INFINITY, Z = 0.f;
+        if constexpr (LEAN) {  // (a whole-GPU launch: ~10 partials per thread)
+          float mv[kPerS], zv[kPerS];
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-        float Z = 0.f;
-        if (hv)
-          #pragma unroll 1
-          for (int c = sub; c < nc; c += 16) {
-            const float mc = pm[h * ncp + c];
-            if (mc > -INFINITY) Z += pz[h * ncp + c] * fast_exp(mc - M);
+          for (int j = 0; j < kPerS; ++j) {
+            const int c = sub + 16 * j;
+            const bool ok = hv && c < nc;
+            mv[j] = ok ? pm[h * ncp + c] : -INFINITY;
+            zv[j] = ok ? pz[h * ncp + c] : 0.f;
           }
+#pragma unroll
+          for (int j = 0; j < kPerS; ++j) M = fmaxf(M, mv[j]);
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+#pragma unroll
+          for (int j = 0; j < kPerS; ++j)
+            if (mv[j] > -INFINITY) Z += zv[j] * fast_exp(mv[j] - M);
+        } else {  // (batched launches: a few CTAs per sequence)
+          if (hv)
+            #pragma unroll 1
+            for (int c = sub; c < nc; c += 16) M = fmaxf(M, pm[h * ncp + c]);
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+          if (hv)
+            #pragma unroll 1
+            for (int c = sub; c < nc; c += 16) {
+              const float mc = pm[h * ncp + c];
+              if (mc > -INFINITY) Z += pz[h * ncp + c] * fast_exp(mc - M);
+            }
+        }
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);
         if (hv && sub == 0) {
