@@ -878,7 +878,8 @@ TcPlan make_tc_plan(int C, int H, int H_kv, int n_att_max, int n_sms) {
   pl.nct = (n_att_max + kKT - 1) / kKT;
   pl.n_units = nx * H_kv;
   auto tiles = [&](int x) { return pl.nct + (min(C, (x + 1) * rph) + kKT - 1) / kKT; };
-  auto cost = [&](int t) { return t < pl.nct ? 10L : 22L; };
+  static const long chunk_cost = std::getenv("TS_PREFILL_CCOST") ? std::atol(std::getenv("TS_PREFILL_CCOST")) : 22L;
+  auto cost = [&](int t) { return t < pl.nct ? 10L : chunk_cost; };
   long W = 0;
   for (int x = 0; x < nx; ++x)
     for (int t = 0; t < tiles(x); ++t) W += H_kv * cost(t);
