@@ -1468,6 +1468,29 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_kernel(const DecodeP
   DecisionLoads dl{};
   const bool dec_early = sd.select && !(pmode & kModeShardSelect) && (pmode & kModeCache);
   if (dec_early) decision_issue(sd, width, dl);
+  // a possible hit's row indices (the cached selection's slab rows, 4 B each)
+  // and the windows' page-table entries into L2 now, so the attention's
+  // index pass after the decision reads them from L2 (tiny: one bulk
+  // prefetch per CTA, 256 B, on the first CTAs)
+  if (LEAN && tid == 0 && sd.select && (pmode & kModeAttend)) {
+    const uint64_t pol = policy_evict_last();
+    // [first, first + n) of a 4-byte array, 16-byte aligned whole pieces only
+    auto pf = [&](const void* base, int first, int n) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(base) + static_cast<uintptr_t>(first) * 4;
+      const uint32_t bytes = static_cast<uint32_t>(n * 4) & ~15u;
+      if ((a & 15) == 0 && bytes) bulk_prefetch_l2(reinterpret_cast<const void*>(a), bytes, pol);
+    };
+    const int nsl = (p.k + 63) / 64;  // 256-B blocks of sel_rows
+    const int n_pages = (sd.n_cached + p.page_size - 1) / p.page_size;
+    if (cs < nsl) {
+      pf(sd.sel_rows, cs * 64, min(64, p.k - cs * 64));
+    } else if (cs == nsl) {
+      pf(sd.page_table, 0, min(64, n_pages));  // the init window's pages
+    } else if (cs == nsl + 1) {
+      const int pg = (max(0, sd.local_begin) / p.page_size) & ~3;  // the local window's pages
+      pf(sd.page_table, pg, min(64, n_pages - pg));
+    }
+  }
   stamp(trc, 45);
   const int T = sd.n_cand;
   const int j0 = min(T, cs * p.tpc);
